@@ -1,0 +1,317 @@
+"""Generate the golden fixtures that pin the oracle to the reference.
+
+Runs the UNMODIFIED reference package (``/root/reference/pkg/src``, imported
+read-only) on seeded synthetic inputs and writes its outputs to small .npz
+files next to this script.  It only runs in the build container (the GPU box
+has no /root/reference); the fixtures are committed so that the oracle tests
+(tests/test_oracle_golden.py) and the GPU parity tests can use them anywhere.
+
+Inputs are rounded to float32 (descriptors to bf16-representable values)
+before the reference sees their exact float64 upcasts, so the CUDA path —
+which stores pointmaps / descriptors in those narrower types — sees
+bit-identical inputs.
+
+    python tests/golden/make_golden.py
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = os.environ.get("EC3R_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.join(os.path.dirname(REF), "tests"))
+
+from submap_slam import backend as rbackend  # noqa: E402
+from submap_slam.database import KeyframeDatabase  # noqa: E402
+from submap_slam.errors import SubmapSlamError  # noqa: E402
+from submap_slam.liegroups import Sim3Transform  # noqa: E402
+from submap_slam.loops import FlushBatch, LoopConfig, SimilarityMatrix, update_similarity  # noqa: E402
+from submap_slam.mapping import Mapping  # noqa: E402
+from submap_slam.registration import align_point_sets  # noqa: E402
+from submap_slam.scenesim import TrajectorySpec, WorldConfig, generate_trajectory, generate_world  # noqa: E402
+from submap_slam.tracking import match_descriptors  # noqa: E402
+
+from helpers import random_sim3  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def bf16(x):
+    """Round float64 -> bf16 (nearest-even) -> exact float64 value."""
+    a = np.asarray(x, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# 1. Umeyama known answers (pkg/tests/test_registration.py:34-154 seeds) plus
+#    random problems; outputs of registration.align_point_sets.
+
+def gen_registration():
+    cases = []
+    rng = np.random.default_rng(20)                      # test_registration.py:35
+    gt = Sim3Transform(1.7, random_sim3(rng).rotation, rng.normal(size=3))
+    p = rng.normal(size=(10, 3))
+    cases.append((p, gt.apply(p), None, True))
+    rng = np.random.default_rng(21)                      # :45
+    p = rng.normal(size=(8, 3))
+    cases.append((p, p.copy(), None, True))
+    rng = np.random.default_rng(22)                      # :53
+    gt = random_sim3(rng)
+    p = rng.normal(size=(50, 3))
+    q = gt.apply(p) + rng.normal(size=(50, 3)) * 0.01
+    cases.append((p, q, np.ones(50), True))
+    cases.append((np.concatenate([p, [[100.0, -100.0, 100.0]]]),
+                  np.concatenate([q, [[-100.0, 100.0, -100.0]]]),
+                  np.concatenate([np.ones(50), [0.0]]), True))
+    p = np.array([[0.0, 0, 0], [1, 0, 0], [2, 0, 0]])    # :75 collinear
+    cases.append((p, p + 1.0, None, True))
+    d = np.array([0.3, -1.1, 2.7])                        # collinear, general direction
+    p = np.outer(np.linspace(-2, 3, 7), d) + np.array([5.0, 1.0, -2.0])
+    cases.append((p, p * 1.3 + 0.2, None, True))
+    cases.append((np.zeros((2, 3)), np.zeros((2, 3)), None, True))   # :81 too few
+    cases.append((np.ones((5, 3)), np.ones((5, 3)), np.zeros(5), True))  # all zero
+    rng = np.random.default_rng(23)                      # :89 minimizer problems
+    for _ in range(20):
+        gt = random_sim3(rng)
+        n = int(rng.integers(4, 30))
+        p = rng.normal(size=(n, 3))
+        w = rng.uniform(0.1, 2.0, size=n)
+        q = gt.apply(p) + rng.normal(size=(n, 3)) * 0.05
+        cases.append((p, q, w, True))
+    rng = np.random.default_rng(26)                      # :134 near planar
+    for _ in range(10):
+        n = int(rng.integers(4, 20))
+        p = rng.normal(size=(n, 3))
+        p[:, 2] *= 1e-8
+        q = rng.normal(size=(n, 3))
+        q[:, 2] *= 1e-8
+        cases.append((p, q, None, True))
+    rng = np.random.default_rng(1234)                    # large, offset, with_scale False
+    for n, off in ((5000, 0.0), (20000, 100.0), (3000, -40.0)):
+        gt = random_sim3(rng)
+        p = rng.normal(size=(n, 3)) * 2.0 + off
+        q = gt.apply(p) + rng.normal(size=(n, 3)) * 0.01
+        w = rng.uniform(0.0, 1.0, size=n)
+        w[rng.uniform(size=n) < 0.1] = 0.0
+        cases.append((p, q, w, True))
+    p = rng.normal(size=(40, 3))
+    cases.append((p, random_sim3(rng).apply(p), None, False))
+
+    out = {}
+    for i, (p, q, w, ws) in enumerate(cases):
+        out[f"c{i}_p"] = p
+        out[f"c{i}_q"] = q
+        out[f"c{i}_w"] = w if w is not None else np.zeros(0)
+        out[f"c{i}_hasw"] = np.array(w is not None)
+        out[f"c{i}_withscale"] = np.array(ws)
+        try:
+            tr, rms = align_point_sets(p, q, w, with_scale=ws)
+            out[f"c{i}_status"] = np.array("ok")
+            out[f"c{i}_s"] = np.array(tr.scale)
+            out[f"c{i}_quat"] = np.array(tr.rotation.q)
+            out[f"c{i}_t"] = np.array(tr.translation)
+            out[f"c{i}_rms"] = np.array(rms)
+        except SubmapSlamError as e:
+            out[f"c{i}_status"] = np.array(type(e).__name__)
+        except ValueError:
+            out[f"c{i}_status"] = np.array("ValueError")
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(OUT, "registration.npz"), **out)
+    print("registration:", len(cases), "cases")
+
+
+# ---------------------------------------------------------------------------
+# 2/3. inverse_project, submap registration and fused cloud through the
+#      reference Mapping (pkg/tests/test_mapping.py fixture, noisy decode).
+
+class F32Backend(rbackend.SyntheticBackend):
+    """Reference SyntheticBackend whose decode output is rounded to float32
+    (the storage type of the CUDA path); captures every decode."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.captured = []
+
+    def decode(self, embeddings):
+        out = super().decode(embeddings)
+        out = rbackend.ReconstructionOutput(
+            out.frame_ids, f32(out.depths), f32(out.confidences), out.poses,
+            out.intrinsics, out.call_index)
+        self.captured.append(out)
+        return out
+
+
+def _dense(out):
+    return dict(
+        depth=out.depths.astype(np.float32),
+        conf=out.confidences.astype(np.float32),
+        frame_ids=np.array(out.frame_ids, np.int64),
+        pose_q=np.array([p.rotation.q for p in out.poses]),
+        pose_t=np.array([p.translation for p in out.poses]),
+        K=np.array([out.intrinsics.fx, out.intrinsics.fy, out.intrinsics.cx, out.intrinsics.cy]),
+    )
+
+
+def gen_mapping():
+    world = generate_world(WorldConfig(room_size=(8.0, 8.0, 4.0), landmark_count=300), 0)
+    spec = TrajectorySpec(kind="circle", frame_count=16, radius=2.0, step_bound=1.0)
+    traj = generate_trajectory(spec, world)
+    cfg = rbackend.SyntheticBackendConfig(depth_resolution=(80, 60), focal=70.0)
+    be = F32Backend(world, traj, cfg, seed=100)
+    mp = Mapping(be)
+    batches = [FlushBatch(new_ids=(0, 1, 2, 3, 4), old_ids=()),
+               FlushBatch(new_ids=(5, 6, 7, 8), old_ids=(4,)),
+               FlushBatch(new_ids=(9, 10, 11, 12), old_ids=(8,))]
+    out = {}
+    for j, b in enumerate(batches):
+        sm = mp.build_submap(b)
+        dec = be.captured[-1]
+        d = _dense(dec)
+        for k, v in d.items():
+            out[f"sm{j}_{k}"] = v
+        if j == 0:
+            cloud = sm.cloud
+            out["ip_points"] = cloud.points
+            out["ip_conf"] = cloud.confidences
+            out["ip_fids"] = cloud.frame_ids
+            out["ip_pixels"] = cloud.pixels
+        else:
+            other = mp.submaps[j - 1]
+            p, q, w = mp._shared_correspondences(sm, other)
+            floor = 0.1 * float(w.max())
+            out[f"e{j}_p"] = p
+            out[f"e{j}_q"] = q
+            out[f"e{j}_w"] = w
+            out[f"e{j}_keep"] = w >= floor
+            edges = mp._registration_edges(sm)
+            (sid, tr, info, count, rms), = edges
+            out[f"e{j}_partner"] = np.array(sid)
+            out[f"e{j}_s"] = np.array(tr.scale)
+            out[f"e{j}_quat"] = np.array(tr.rotation.q)
+            out[f"e{j}_t"] = np.array(tr.translation)
+            out[f"e{j}_rms"] = np.array(rms)
+            out[f"e{j}_count"] = np.array(count)
+        mp.register_submap(sm)
+        g = sm.global_pose
+        out[f"sm{j}_gs"] = np.array(g.scale)
+        out[f"sm{j}_gq"] = np.array(g.rotation.q)
+        out[f"sm{j}_gt"] = np.array(g.translation)
+    pts, conf = mp.fused_cloud()
+    out["fused_points"] = pts
+    out["fused_conf"] = conf
+    out["n_submaps"] = np.array(len(batches))
+    np.savez_compressed(os.path.join(OUT, "mapping.npz"), **out)
+    print("mapping:", len(pts), "fused points")
+
+
+# ---------------------------------------------------------------------------
+# 4. Descriptor matching (tracking.py:143-170) on bf16-representable inputs.
+
+def _desc_pair(rng, n, m, d, sigma, spurious=0.2):
+    a = rng.normal(size=(n, d))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    perm = rng.permutation(n)[:m] if m <= n else rng.integers(0, n, m)
+    b = a[perm] + rng.normal(size=(m, d)) * sigma
+    b /= np.linalg.norm(b, axis=1, keepdims=True)
+    spur = rng.uniform(size=m) < spurious
+    fresh = rng.normal(size=(int(spur.sum()), d))
+    b[spur] = fresh / np.linalg.norm(fresh, axis=1, keepdims=True)
+    return bf16(a), bf16(b)
+
+
+def gen_match():
+    rng = np.random.default_rng(4242)
+    cases = []
+    cases.append(_desc_pair(rng, 200, 180, 256, 0.10))      # stress noise
+    cases.append(_desc_pair(rng, 150, 220, 256, 0.05))      # default noise, N != M
+    cases.append(_desc_pair(rng, 97, 61, 64, 0.10))         # synthetic D = 64
+    cases.append(_desc_pair(rng, 33, 1, 256, 0.05))         # M == 1: no ratio test
+    cases.append((np.eye(60, 80), np.eye(60, 80)))          # test_loops.py:176-177 ties
+    cases.append((np.eye(100, 128), np.eye(100, 128)))      # test_loops.py:155
+    a, b = _desc_pair(rng, 40, 40, 32, 0.0, spurious=0.0)   # duplicate rows in B
+    b[5] = b[7]
+    cases.append((a, b))
+    cases.append((np.zeros((0, 16)), bf16(rng.normal(size=(5, 16)))))  # empty
+    out = {}
+    for i, (a, b) in enumerate(cases):
+        m = match_descriptors(a, b, 0.8)
+        out[f"c{i}_a"] = a.astype(np.float32)
+        out[f"c{i}_b"] = b.astype(np.float32)
+        out[f"c{i}_matches"] = np.array(m, dtype=np.int64).reshape(-1, 2)
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(OUT, "match.npz"), **out)
+    print("match:", len(cases), "cases")
+
+
+# ---------------------------------------------------------------------------
+# 5. Global retrieval (loops.py:184-243) incl. the admitted-once state.
+
+def _retrieval_case(db, stride, cfg, calls=2):
+    matrix = SimilarityMatrix()
+    res = [update_similarity(matrix, db, stride, cfg) for _ in range(calls)]
+    kf = [k for k in db.ids_in_order() if db.get(k).pooled is not None]
+    pooled = np.array([db.get(k).pooled for k in kf])
+    items = sorted(matrix.items())
+    return kf, pooled, res, items
+
+
+def gen_retrieval():
+    out = {}
+    cases = []
+    dim = 32                                                 # test_loops.py:218-232
+    vecs = [np.eye(dim)[i % dim] for i in range(23)]
+    vecs[20] = vecs[0]
+    db = KeyframeDatabase()
+    for k, v in enumerate(vecs):
+        db.store_embedding(k, np.asarray(v, float)[None, :])
+    cases.append((db, 5, LoopConfig(buffer_capacity=5)))
+    world = generate_world(WorldConfig(room_size=(10.0, 10.0, 4.0), landmark_count=300), 5)
+    spec = TrajectorySpec(kind="square-loop", frame_count=41, radius=3.0, step_bound=0.7)
+    be = rbackend.SyntheticBackend(world, generate_trajectory(spec, world), seed=6)
+    db = KeyframeDatabase()                                  # test_loops.py:247-264
+    for fid in range(41):
+        db.store_embedding(fid, be.encode(fid).tokens)
+    cases.append((db, 5, LoopConfig(buffer_capacity=2)))
+    spec = TrajectorySpec(kind="square-loop", frame_count=201, radius=3.0, step_bound=0.7)
+    traj = generate_trajectory(spec, world)
+    traj = traj + traj[1:100]                                # 1.5 laps: many revisits
+    be = rbackend.SyntheticBackend(world, traj, seed=7)
+    db = KeyframeDatabase()
+    for fid in range(len(traj)):
+        if fid % 13 == 5:
+            db.ensure(fid)                                   # record without a pooled vector
+            continue
+        db.store_embedding(fid, be.encode(fid).tokens)
+    cases.append((db, 5, LoopConfig(buffer_capacity=5)))
+    for i, (db, stride, cfg) in enumerate(cases):
+        kf, pooled, res, items = _retrieval_case(db, stride, cfg)
+        out[f"c{i}_kf"] = np.array(kf, np.int64)
+        out[f"c{i}_pooled"] = pooled
+        out[f"c{i}_stride"] = np.array(stride)
+        out[f"c{i}_excl"] = np.array(cfg.exclusion_zone())
+        out[f"c{i}_tau"] = np.array([cfg.tau_global, cfg.tau_local])
+        for c, r in enumerate(res):
+            out[f"c{i}_call{c}_pairs"] = np.array([p for p, _ in r], np.int64).reshape(-1, 2)
+            out[f"c{i}_call{c}_scores"] = np.array([s for _, s in r], float)
+        out[f"c{i}_matrix_keys"] = np.array([k for k, _ in items], np.int64).reshape(-1, 2)
+        out[f"c{i}_matrix_vals"] = np.array([v for _, v in items], float)
+        print(f"retrieval case {i}: K={len(kf)} admitted={[len(r) for r in res]} matrix={len(items)}")
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(OUT, "retrieval.npz"), **out)
+
+
+if __name__ == "__main__":
+    gen_registration()
+    gen_mapping()
+    gen_match()
+    gen_retrieval()

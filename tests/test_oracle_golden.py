@@ -1,0 +1,116 @@
+"""Pin the CPU oracle to the reference's own outputs (tests/golden/*.npz were
+produced by tests/golden/make_golden.py running the unmodified reference)."""
+
+import numpy as np
+import pytest
+
+from oracle import fuse as ofuse
+from oracle import ref_numpy as ref
+from tests.conftest import mapping_submaps
+
+STATUS = {"ok": ref.STATUS_OK, "TooFewCorrespondences": ref.STATUS_TOO_FEW,
+          "ValueError": ref.STATUS_SHAPE, "AllZeroConfidence": ref.STATUS_ALL_ZERO,
+          "DegenerateConfiguration": ref.STATUS_DEGENERATE}
+
+
+def test_registration_cases(golden):
+    g = golden("registration")
+    for i in range(int(g["n_cases"])):
+        w = g[f"c{i}_w"] if bool(g[f"c{i}_hasw"]) else None
+        s, q, t, rms, st = ref.align_point_sets(g[f"c{i}_p"], g[f"c{i}_q"], w,
+                                                bool(g[f"c{i}_withscale"]))
+        assert st == STATUS[str(g[f"c{i}_status"])], i
+        if st != ref.STATUS_OK:
+            continue
+        assert abs(s - float(g[f"c{i}_s"])) <= 1e-12 * abs(s), i
+        np.testing.assert_allclose(ref.canonical_quat(q), ref.canonical_quat(g[f"c{i}_quat"]),
+                                   atol=1e-12)
+        np.testing.assert_allclose(t, g[f"c{i}_t"], atol=1e-10)
+        assert abs(rms - float(g[f"c{i}_rms"])) <= 1e-12
+
+
+def test_inverse_project_bit_exact(golden):
+    g = golden("mapping")
+    sms, _ = mapping_submaps(g)
+    sm = sms[0]
+    pts, conf, fids, pix = ref.inverse_project(sm["depth"], sm["conf"], sm["frame_ids"],
+                                               sm["pose_q"], sm["pose_t"], sm["K"])
+    np.testing.assert_array_equal(pts, g["ip_points"])
+    np.testing.assert_array_equal(conf, g["ip_conf"])
+    np.testing.assert_array_equal(fids, g["ip_fids"])
+    np.testing.assert_array_equal(pix, g["ip_pixels"])
+
+
+@pytest.mark.parametrize("j", [1, 2])
+def test_shared_correspondences_and_edges(golden, j):
+    g = golden("mapping")
+    sms, _ = mapping_submaps(g)
+    p, q, w = ref.shared_correspondences(sms[j], sms[j - 1])
+    np.testing.assert_array_equal(p, g[f"e{j}_p"])
+    np.testing.assert_array_equal(q, g[f"e{j}_q"])
+    np.testing.assert_array_equal(w, g[f"e{j}_w"])
+    e = ref.registration_edge(sms[j], sms[j - 1])
+    np.testing.assert_array_equal(e["keep"], g[f"e{j}_keep"])
+    assert e["status"] == ref.STATUS_OK
+    assert e["count"] == int(g[f"e{j}_count"])
+    assert abs(e["s"] - float(g[f"e{j}_s"])) < 1e-12
+    np.testing.assert_allclose(ref.canonical_quat(e["q"]), ref.canonical_quat(g[f"e{j}_quat"]),
+                               atol=1e-12)
+    np.testing.assert_allclose(e["t"], g[f"e{j}_t"], atol=1e-12)
+    assert abs(e["rms"] - float(g[f"e{j}_rms"])) < 1e-12
+
+
+def test_chained_global_poses(golden):
+    """register_submap (mapping.py:200-204): global = partner.global o T."""
+    g = golden("mapping")
+    sms, globs = mapping_submaps(g)
+    cur = (1.0, np.array([1.0, 0, 0, 0]), np.zeros(3))
+    for j in range(1, len(sms)):
+        e = ref.registration_edge(sms[j], sms[j - 1])
+        cur = ref.sim3_compose(globs[j - 1], (e["s"], e["q"], e["t"]))
+        s, q, t = globs[j]
+        assert abs(cur[0] - s) < 1e-12
+        np.testing.assert_allclose(ref.canonical_quat(cur[1]), ref.canonical_quat(q), atol=1e-12)
+        np.testing.assert_allclose(cur[2], t, atol=1e-12)
+
+
+def test_fused_cloud_bit_exact_and_keys(golden):
+    g = golden("mapping")
+    sms, globs = mapping_submaps(g)
+    pts, conf = ref.fused_cloud(sms, globs)
+    np.testing.assert_array_equal(pts, g["fused_points"])
+    np.testing.assert_array_equal(conf, g["fused_conf"])
+    f = ofuse.fuse_points(pts, conf, 0.02)
+    assert f["count"].sum() == f["n_in"] == int((conf > 0).sum())
+    assert np.all(np.diff(f["keys"]) > 0)
+    cells = ref.unpack(f["keys"])
+    np.testing.assert_array_equal(ref.pack(cells), f["keys"])
+    lo = cells * 0.02
+    assert np.all(f["centroid"] >= lo - 1e-9) and np.all(f["centroid"] <= lo + 0.02 + 1e-9)
+
+
+def test_match_cases(golden):
+    g = golden("match")
+    for i in range(int(g["n_cases"])):
+        a = g[f"c{i}_a"].astype(np.float64)
+        b = g[f"c{i}_b"].astype(np.float64)
+        exp = g[f"c{i}_matches"]
+        got = np.array(ref.match_descriptors(a, b, 0.8), np.int64).reshape(-1, 2)
+        np.testing.assert_array_equal(got, exp)
+        np.testing.assert_array_equal(ref.match_descriptors_vec(a, b, 0.8), exp)
+
+
+def test_retrieval_cases(golden):
+    g = golden("retrieval")
+    for i in range(int(g["n_cases"])):
+        st = ref.SimilarityState()
+        tg, tl = g[f"c{i}_tau"]
+        for c in range(2):
+            res = ref.update_similarity(st, g[f"c{i}_kf"], g[f"c{i}_pooled"],
+                                        int(g[f"c{i}_stride"]), int(g[f"c{i}_excl"]), tg, tl)
+            pairs = np.array([p for p, _ in res], np.int64).reshape(-1, 2)
+            np.testing.assert_array_equal(pairs, g[f"c{i}_call{c}_pairs"])
+            np.testing.assert_allclose([s for _, s in res], g[f"c{i}_call{c}_scores"],
+                                       rtol=0, atol=1e-15)
+        keys = np.array(sorted(st.scores), np.int64).reshape(-1, 2)
+        np.testing.assert_array_equal(keys, g[f"c{i}_matrix_keys"])
