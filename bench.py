@@ -1,0 +1,451 @@
+"""Benchmark of the B200 dense data-parallel path (BASELINE.json metric:
+fused map points/sec and descriptor matches/sec vs the CPU reference).
+
+Workload (N=1): BASELINE configs[1] — synthetic TUM-style sequence, 300
+keyframes / 60 submaps (5 new + 1 shared frame each, 518x392), 1024 x 256-d
+descriptors per frame; one step = tracking match of 1500 frames against a
+1024-point map + registration of all 59 edges (one launch) + pose chaining +
+voxel-hash fusion at 2 cm of all 360 frames + sorted emit.  Inputs are
+resident in HBM and larger than L2 (126 MB).  Under torchrun each rank owns a
+contiguous window of the sequence (weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "fused map points/sec and descriptor matches/sec at 1/2/4/8 B200 vs CPU ref"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
+    import torch
+
+    from paper_2510_02080_b200 import mapping, synth
+
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(n_kf, cfg, seed=rank, device=device)
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8))
+    sms = []
+    for j, ids in enumerate(sb.frame_ids):
+        o = sb.slot_offsets[j]
+        F = len(ids)
+        sms.append(dm.add_submap(ids, sb.depth[o:o + F], sb.conf[o:o + F], list(sb.poses8[o:o + F]), j))
+    del sb
+    n_frames = 5 * n_kf  # tracked frames: 5 per keyframe
+    A, B, a_off, b_off = synth.make_descriptor_pairs(n_frames, n_desc, n_desc, 256, 0.05, seed=100 + rank,
+                                                     device=device)
+    torch.cuda.synchronize()
+    return dm, sms, (A, B, a_off, b_off)
+
+
+class Step:
+    """One pass of the hot path over the resident workload."""
+
+    def __init__(self, dm, sms, desc, cell=0.02):
+        import torch
+
+        from paper_2510_02080_b200 import mapping, tracking
+
+        self.torch, self.mapping, self.tracking = torch, mapping, tracking
+        self.dm, self.sms, self.desc, self.cell = dm, sms, desc, cell
+        self.slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
+        # edges of the chain registration (partners by shared keyframes, mapping.py:164-169)
+        pairs = []
+        kf_owner = {}
+        for sm in sms:
+            pids = {}
+            for kf in sm.keyframe_ids:
+                for sid in kf_owner.get(kf, ()):
+                    pids[sid] = None
+            pairs.extend((sm, sms[s]) for s in pids)
+            for kf in sm.keyframe_ids:
+                kf_owner.setdefault(kf, []).append(sm.id)
+        self.pairs = pairs
+        seg, eoff = [], [0]
+        for a, b in pairs:
+            seg.extend(mapping.edge_segments(a, b))
+            eoff.append(len(seg))
+        self.seg = torch.as_tensor(np.asarray(seg, np.int32).reshape(-1, 2), device="cuda")
+        self.eoff = torch.as_tensor(np.asarray(eoff, np.int32), device="cuda")
+        self.vmap = None
+        self.ev = {}
+        self.n_points = 0
+        self.n_voxels = 0
+
+    def _event(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def run(self, record=None):
+        torch = self.torch
+        ev = {}
+        ev["t0"] = self._event()
+        A, B, ao, bo = self.desc
+        self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)
+        ev["t_match"] = self._event()
+        sim3, rms, count, npairs, status = self.mapping.register_edges_device(self.dm.pool, self.seg, self.eoff,
+                                                                              len(self.pairs))
+        ev["t_reg"] = self._event()
+        # chain global poses on the host (register_submap semantics, mapping.py:200-204)
+        host = torch.cat([sim3.reshape(-1), count.double(), status.double()]).cpu().numpy()
+        B_ = len(self.pairs)
+        s3 = host[: 8 * B_].reshape(B_, 8)
+        cnt = host[8 * B_: 9 * B_]
+        st = host[9 * B_:]
+        from paper_2510_02080_b200.types import Sim3Transform, sim3_to_vec, vec_to_sim3
+        glob = {self.sms[0].id: Sim3Transform.identity()}
+        best = {}
+        for e, (a, b) in enumerate(self.pairs):
+            if st[e] != 0:
+                continue
+            if a.id not in best or cnt[e] > best[a.id][0]:
+                best[a.id] = (cnt[e], b.id, e)
+        G = np.zeros((len(self.sms), 8))
+        G[0] = sim3_to_vec(glob[self.sms[0].id])
+        for sm in self.sms[1:]:
+            _, pid, e = best[sm.id]
+            glob[sm.id] = glob[pid].compose(vec_to_sim3(s3[e]))
+            G[sm.id] = sim3_to_vec(glob[sm.id])
+        per_slot = np.repeat(G, [len(sm.slots) for sm in self.sms], axis=0)
+        self.dm.pool.globals[: len(per_slot)].copy_(torch.as_tensor(per_slot), non_blocking=False)
+        ev["t_chain"] = self._event()
+        if self.vmap is None:
+            self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell)
+            self.vmap = self.mapping.VoxelMap(self.cell, max(1 << 16, 2 * int(out[0].numel())))
+        self.vmap.clear()
+        self.vmap.insert_frames(self.dm.pool, self.slots)
+        ev["t_insert"] = self._event()
+        keys, cen, wsum, cnt_v = self.vmap.extract(sort=True)
+        ev["t_emit"] = self._event()
+        self.n_voxels = int(keys.numel())
+        if record is not None:
+            record.append(ev)
+        return keys, cen, wsum, cnt_v
+
+
+def stage_ms(records):
+    out = {}
+    names = ["t0", "t_match", "t_reg", "t_chain", "t_insert", "t_emit"]
+    for a, b in zip(names[:-1], names[1:]):
+        out[b[2:]] = float(np.mean([r[a].elapsed_time(r[b]) for r in records]))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) on a bounded sample
+
+def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: float = 20.0):
+    """Times the oracle port of the path on a bounded sample: registration of
+    n_submaps-1 edges + voxel fusion of n_submaps submaps (points/s), and
+    n_match tracking matches of 1024 x 1024 x 256 (pairs/s)."""
+    import torch
+
+    from oracle import fuse as ofuse
+    from oracle import ref_numpy as ref
+    from paper_2510_02080_b200 import synth
+
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(5 * n_submaps + 1, cfg, seed=seed, device="cpu")
+    dense = []
+    for j, ids in enumerate(sb.frame_ids[:n_submaps]):
+        o, F = sb.slot_offsets[j], len(ids)
+        dense.append(dict(depth=sb.depth[o:o + F].numpy(), conf=sb.conf[o:o + F].numpy(), frame_ids=np.array(ids),
+                          pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:], K=sb.K4))
+    t0 = time.perf_counter()
+    globs = [(1.0, np.array([1.0, 0, 0, 0]), np.zeros(3))]
+    for j in range(1, len(dense)):
+        e = ref.registration_edge(dense[j], dense[j - 1])
+        globs.append(ref.sim3_compose(globs[j - 1], (e["s"], e["q"], e["t"])))
+    f = ofuse.fuse_submaps(dense, globs, 0.02)
+    t_fuse = time.perf_counter() - t0
+    pts = f["n_in"]
+    A, B, ao, bo = synth.make_descriptor_pairs(n_match, 1024, 1024, 256, 0.05, seed=seed, device="cpu")
+    a = A.view(torch.bfloat16).double().numpy()
+    b = B.view(torch.bfloat16).double().numpy()
+    t1 = time.perf_counter()
+    for p in range(n_match):
+        ref.match_descriptors(a[ao[p]:ao[p + 1]], b[bo[p]:bo[p + 1]], 0.8)
+        if time.perf_counter() - t0 > budget_s:
+            n_match = p + 1
+            break
+    t_match = time.perf_counter() - t1
+    return {"points": pts, "t_fuse": t_fuse, "points_per_s": pts / t_fuse, "pairs": n_match * 1024 * 1024,
+            "t_match": t_match, "pairs_per_s": n_match * 1024 * 1024 / t_match,
+            "sample": f"oracle port: {n_submaps - 1} registration edges + 2 cm voxel fusion of {n_submaps} submaps "
+                      f"({pts} points, 518x392) and {n_match} matches of 1024x1024x256 (reference per-row loop)"}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--keyframes", type=int, default=300)
+    ap.add_argument("--desc", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_02080_b200 import _lib
+
+    L = _lib.lib()
+    dm, sms, desc = build_workload(rank, world, args.keyframes, args.desc, "cuda")
+    step = Step(dm, sms, desc)
+    for _ in range(args.warmup):
+        step.run()
+    torch.cuda.synchronize()
+    n_points = step.vmap.stats()["n_points_in"]
+    A, B, ao, bo = desc
+    n_pairs_scored = int(np.sum(np.diff(ao) * np.diff(bo)))
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    records = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.ec3r_kernel_launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step.run(records)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = L.ec3r_kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    stages = stage_ms(records)
+    n_matches = int(step.nm.sum().item())
+
+    # roofline accounting
+    peaks, peak_src = load_peaks()
+    H, W = dm.pool.H, dm.pool.W
+    P = int(n_points)
+    U = step.n_voxels
+    C = int(step.seg.shape[0]) * H * W  # overlap pixel pairs streamed by registration
+    fuse_ms = stages["insert"] + stages["emit"]
+    reg_ms = stages["reg"]
+    bytes_fuse = 8 * P + 28 * U
+    bytes_reg = 16 * C
+    achieved_fuse = bytes_fuse / (stages["insert"] * 1e-3) / 1e9
+    flops_match = 2.0 * n_pairs_scored * 256
+    achieved_match = flops_match / (stages["match"] * 1e-3) / 1e12
+    roof = {
+        "fuse_insert": {"bound": "hbm", "achieved": achieved_fuse, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": achieved_fuse / peaks["hbm_gbs"], "traffic": None, "ms": stages["insert"],
+                        "alg_bytes": bytes_fuse},
+        "register": {"bound": "hbm", "achieved": bytes_reg / (reg_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": bytes_reg / (reg_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "ms": reg_ms,
+                     "alg_bytes": bytes_reg},
+        "match": {"bound": "tensor", "achieved": achieved_match, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                  "frac": achieved_match / peaks["bf16_tflops"], "ms": stages["match"], "alg_flops": flops_match},
+    }
+    dominant = max(roof, key=lambda k: roof[k]["ms"])
+    value = P * world / (ms * 1e-3)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(step, dm, desc, args, world)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        c = cpu_sample()
+        cpu = {"value": c["points_per_s"], "unit": "points/s", "cores": cpu_cores(), "kind": "port",
+               "sample": c["sample"], "matches_value": c["pairs_per_s"], "matches_unit": "candidate pairs/s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "fused map points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 planes / f64 transforms+moments / bf16 tensor-core matcher",
+            "data": "synthetic (device ray-cast box room, seeded)",
+            "config": {"workload": "configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
+                                   "tracking match + align + fuse",
+                       "keyframes_per_gpu": args.keyframes, "frames_tracked_per_gpu": int(len(ao) - 1),
+                       "resolution": [W, H], "voxel_m": 0.02, "submaps_per_gpu": len(sms),
+                       "edges_per_gpu": len(step.pairs), "points_per_step_per_gpu": P, "voxels_per_gpu": U,
+                       "l2": "inputs larger than L2 (pool %.0f MB, descriptors %.0f MB)" %
+                             (dm.pool.nbytes() / 1e6, (A.numel() + B.numel()) * 2 / 1e6),
+                       "parallelism": f"submap windows x{world}"},
+            "matches_per_s": n_pairs_scored * world / (ms * 1e-3), "matches_unit": "candidate descriptor pairs/s",
+            "emitted_matches_per_s": n_matches * world / (ms * 1e-3),
+            "stages_ms": stages,
+            "roofline": dict(roof[dominant], kernel=dominant, peak_source=f"{peak_src} MEASURED_PEAKS.json"),
+            "rooflines": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(step, dm, desc, args, world):
+    """Same metric through the public API with host buffers: every step H2D of
+    the frame planes and descriptors from pinned memory, then the full path,
+    then D2H of the fused map."""
+    import torch
+
+    pool = dm.pool
+    n = pool.n
+    h_depth = pool.depth[:n].cpu().pin_memory()
+    h_conf = pool.conf[:n].cpu().pin_memory()
+    A, B, ao, bo = desc
+    h_A = A.cpu().pin_memory()
+    h_B = B.cpu().pin_memory()
+    steps = max(2, min(args.steps, 5))
+    out_bytes = 0
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pool.depth[:n].copy_(h_depth, non_blocking=True)
+        pool.conf[:n].copy_(h_conf, non_blocking=True)
+        A.copy_(h_A, non_blocking=True)
+        B.copy_(h_B, non_blocking=True)
+        keys, cen, wsum, cnt = step.run()
+        res = [keys.cpu(), cen.cpu(), wsum.cpu(), cnt.cpu()]
+        out_bytes = sum(r.numel() * r.element_size() for r in res)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    P = step.vmap.stats()["n_points_in"]
+    h2d = (h_depth.numel() + h_conf.numel()) * 4 + (h_A.numel() + h_B.numel()) * 2
+    return {"value": P * world / (ms * 1e-3), "unit": "fused map points/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_bytes), "steps": steps}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the
+    host cores, rank 0 only, bounded samples of the same workload."""
+    if rank != 0:
+        return
+    vals, mvals = [], []
+    c = None
+    for k in range(args.warmup + args.steps):
+        c = cpu_sample(n_submaps=2, n_match=1, seed=k, budget_s=15.0)
+        if k >= args.warmup:
+            vals.append(c["points_per_s"])
+            mvals.append(c["pairs_per_s"])
+    v = float(np.median(vals))
+    line = {"metric": METRIC, "value": v, "unit": "fused map points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (same generator, CPU)", "impl": "reference",
+            "config": {"workload": "configs[1] sample: 1 registration edge + fusion of 2 submaps and one 1024x1024 "
+                                   "match per step", "voxel_m": 0.02},
+            "matches_per_s": float(np.median(mvals)), "matches_unit": "candidate descriptor pairs/s",
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": cpu_cores(), "kind": "port",
+                             "sample": c["sample"]},
+            "e2e": {"value": v, "unit": "fused map points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

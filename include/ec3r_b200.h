@@ -1,0 +1,230 @@
+/*
+ * ec3r_b200.h — C ABI of the B200-native (sm_100a) dense data-parallel path
+ * of EC3R-SLAM (arxiv 2510.02080).
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless its name ends in _h;
+ *   - the caller owns every buffer; the library never frees or reallocates
+ *     caller memory (the voxel hash is the one opaque, library-owned handle);
+ *   - every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream) and returns 0 on success or a
+ *     negative EC3R_E* code; per-item outcomes of batched calls are written
+ *     to device status arrays (EC3R_ST_*), never returned;
+ *   - no hidden global state: calls are reentrant and safe from several host
+ *     threads on distinct streams;
+ *   - Sim(3) / SE(3) values are 8 doubles {s, qw, qx, qy, qz, tx, ty, tz}
+ *     (x -> s * R(q) x + t, s = 1 for poses), the value type of
+ *     submap_slam.liegroups.Sim3Transform / Pose3 (liegroups.py:132-272);
+ *   - intrinsics are 4 doubles {fx, fy, cx, cy} (geometry.py:28-37).
+ *
+ * Reference interfaces each entry point replaces are cited as
+ * file:line into /root/reference/pkg/src/submap_slam.
+ */
+#ifndef EC3R_B200_H
+#define EC3R_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EC3R_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EC3R_API __attribute__((visibility("default")))
+#else
+#define EC3R_API
+#endif
+
+/* return codes */
+#define EC3R_OK 0
+#define EC3R_ECUDA (-1)      /* CUDA launch / runtime error */
+#define EC3R_EARG (-2)       /* invalid argument (sizes, alignment, NULL) */
+#define EC3R_EWORKSPACE (-3) /* workspace too small */
+#define EC3R_ENOMEM (-4)
+
+/* per-item status (batched registration); the Python layer maps these to
+ * the reference exception types in the reference's precedence
+ * (registration.py:59-93, mapping.py:174-187). */
+#define EC3R_ST_OK 0
+#define EC3R_ST_SKIP 1          /* < min_correspondences: edge skipped, not an error */
+#define EC3R_ST_TOO_FEW 2       /* n < 3 -> TooFewCorrespondences */
+#define EC3R_ST_ALL_ZERO 3      /* sum w <= 0 -> AllZeroConfidence */
+#define EC3R_ST_DEGENERATE 4    /* collinear / coincident source -> DegenerateConfiguration */
+#define EC3R_ST_NONPOS_SCALE 5  /* s <= 0 -> DegenerateConfiguration */
+
+EC3R_API int ec3r_abi_version(void);
+/* Process-wide count of kernels this library has launched (diagnostic; the
+ * benchmark reports the delta over its timed region as gpu_launches). */
+EC3R_API uint64_t ec3r_kernel_launches(void);
+/* Last CUDA error string of the calling thread's most recent failing call. */
+EC3R_API const char* ec3r_last_error(void);
+
+/* ---------------------------------------------------------------------
+ * K1  inverse projection with compaction
+ * replaces backend.inverse_project (backend.py:78-101)
+ *
+ * depth/conf: (F, H, W) float32, row-major; poses: F x 8 (anchor_from_cam);
+ * frame_ids_h: host array of F ids.  Writes one row per pixel with
+ * depth > 0, frames in order then row-major (v, u): points (N,3) float64
+ * (bit-identical to the reference's float64 arithmetic on the float32
+ * inputs), conf (N) float64, frame ids (N) int64, pixels (N,2) int64 (u,v).
+ * Outputs must hold F*H*W rows; *n_out (device int64) receives N.
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_inverse_project_workspace(int F, int H, int W);
+EC3R_API int ec3r_inverse_project(const float* depth, const float* conf, int F, int H, int W,
+                         const double* K4_h, const double* poses_h, const int64_t* frame_ids_h,
+                         double* out_points, double* out_conf, int64_t* out_fids,
+                         int64_t* out_pixels, int64_t* n_out, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* Sim3Transform.apply (liegroups.py:259-260) on (n,3) float64 points,
+ * bit-identical to the reference; the world-point transform of
+ * Submap.world_points / Mapping.fused_cloud (mapping.py:56-57, 332-338). */
+EC3R_API int ec3r_sim3_apply(const double* points, int64_t n, const double* sim3_h, double* out,
+                             void* stream);
+
+/* ---------------------------------------------------------------------
+ * K2+K3  batched submap registration over pixel-identity correspondences
+ * replaces Mapping._shared_correspondences + the gate/floor/align loop of
+ * Mapping._registration_edges (mapping.py:138-183) and align_point_sets
+ * (registration.py:38-102) for B edges in one launch.
+ *
+ * Frames live in a resident pool: depth_pool/conf_pool (n_slots, H, W)
+ * float32; slot_poses (n_slots x 8, device) are anchor_from_cam of the frame
+ * in its submap.  An edge (sm -> other) is the concatenation of its
+ * segments seg_slots[2*k] (frame slot in sm), seg_slots[2*k+1] (same
+ * keyframe's slot in other) for k in [edge_seg[e], edge_seg[e+1]).
+ * Per edge: pairs valid where both depths > 0, w = min(conf_a, conf_b),
+ * floor = floor_frac * max(w), keep = w >= floor; SKIP when fewer than
+ * min_corr pairs / kept pairs, else Umeyama q ~ s R p + t.  Outputs per
+ * edge: out_sim3 (B x 8), out_rms, out_count (kept), out_npairs (valid),
+ * out_status.  keep_masks (optional, n_seg x H x W uint8) receives the
+ * inlier mask (bit-exact contract).
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_register_edges_workspace(int n_edges);
+EC3R_API int ec3r_register_edges(const float* depth_pool, const float* conf_pool, int H, int W,
+                        const double* K4_h, const double* slot_poses, const int32_t* seg_slots,
+                        const int32_t* edge_seg, int n_edges, double floor_frac, int min_corr,
+                        int with_scale, double* out_sim3, double* out_rms, int64_t* out_count,
+                        int64_t* out_npairs, int32_t* out_status, uint8_t* keep_masks,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K2+K3  batched weighted Umeyama on explicit correspondences
+ * replaces align_point_sets (registration.py:38-102) / weighted_umeyama
+ * (:105-112).  p, q: (sum n_b, 3) float64; w: (sum n_b) float64 or NULL
+ * (uniform); offsets: B+1 int64 (device).  Reduction grouping is anchored
+ * to element index (zero-weight tail elements leave results bit-identical).
+ * Outputs: out_sim3 (B x 8), out_rms (B), out_status (B).
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_umeyama_workspace(int n_problems);
+EC3R_API int ec3r_umeyama_batched(const double* p, const double* q, const double* w,
+                         const int64_t* offsets, int n_problems, int with_scale,
+                         double* out_sim3, double* out_rms, int32_t* out_status,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K1+K4  transform + voxel-hash fusion + downsampling
+ * replaces Submap.world_points / Mapping.fused_cloud (mapping.py:56-57,
+ * 332-338) with the declared fusion rule of oracle/fuse.py; keys are
+ * _pack(floor(x / cell)) (_kernels/_numpy.py:50-55), bit-exact against the
+ * reference's float64 transform.  Open addressing, 64-bit keys, float32
+ * accumulators relative to the voxel corner.
+ * ------------------------------------------------------------------- */
+typedef struct ec3r_vhash ec3r_vhash;
+
+typedef struct {
+    int64_t n_points_in;     /* points offered (depth > 0, conf > 0) */
+    int64_t n_out_of_range;  /* cell outside the 21-bit key range: dropped */
+    int64_t n_overflow;      /* table full: dropped (grow and re-run) */
+    int64_t n_slow_path;     /* points resolved by the exact float64 path */
+} ec3r_vhash_stats;
+
+EC3R_API int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream);
+EC3R_API int ec3r_vhash_destroy(ec3r_vhash* h);
+EC3R_API int64_t ec3r_vhash_capacity(const ec3r_vhash* h);
+EC3R_API int ec3r_vhash_clear(ec3r_vhash* h, void* stream);
+/* Fuse whole frames of the pool: for each listed slot, every pixel with
+ * depth > 0 and conf > 0 is inverse-projected with slot_poses[slot]
+ * (anchor_from_cam) and mapped to the world by slot_globals[slot] (the
+ * owning submap's global Sim(3)); slots_h is a host list of n slot ids. */
+EC3R_API int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, const float* conf_pool,
+                             int H, int W, const double* K4_h, const double* slot_poses,
+                             const double* slot_globals, const int32_t* slots_h, int n,
+                             void* stream);
+/* Fuse explicit points (N,3) float64 with conf (N) float64 under sim3_h. */
+EC3R_API int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, const double* conf, int64_t n,
+                             const double* sim3_h, void* stream);
+/* Copy the running counters to a host struct (synchronizes the stream). */
+EC3R_API int ec3r_vhash_stats_get(ec3r_vhash* h, ec3r_vhash_stats* out_h, void* stream);
+/* Emit the fused voxels: keys (U) int64 ascending (sorted when sort != 0),
+ * centroid (U,3) float32, wsum (U) float32, count (U) int32; *n_out (device
+ * int64) = U.  Outputs must hold `capacity` rows (or query
+ * ec3r_vhash_count first). */
+EC3R_API size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h);
+EC3R_API int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream);
+EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum,
+                       int32_t* count, int64_t* n_out, int sort, void* workspace,
+                       size_t workspace_bytes, void* stream);
+/* Multi-GPU: emit raw partial sums (key, sum w*dx, sum w, count) bucketed
+ * by owner rank = (key range partition) for the all-to-all,
+ * and merge received partials into a table. */
+EC3R_API int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* keys, float* sums4,
+                                int32_t* count, int64_t* rank_counts, void* workspace,
+                                size_t workspace_bytes, void* stream);
+EC3R_API int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, const float* sums4,
+                              const int32_t* count, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K5  brute-force mutual-NN + Lowe-ratio descriptor matching
+ * replaces match_descriptors (tracking.py:143-170) for a batch of frame
+ * pairs.  A: (sum N_p, D) and B: (sum M_p, D) bf16 rows (ld = D, D % 8 == 0
+ * after zero padding); a_off/b_off: n_pairs+1 int64 row offsets (device).
+ * The approximate similarity pass runs on tcgen05 tensor cores (fp32 TMEM
+ * accumulators); every decision is certified against an error bound and
+ * re-scored in float64 from the exact rows (A_x/B_x, dtype exact_dtype:
+ * 0 = the bf16 rows are exact, 1 = float32, 2 = float64), so the result is
+ * identical to the float64 reference.  Output: match_b (sum N_p) int32 =
+ * matched B row within the pair or -1; n_match (n_pairs) int32.
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_pairs);
+EC3R_API int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
+                       int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h,
+                       int n_pairs, int D, double ratio, int32_t* match_b, int32_t* n_match,
+                       void* workspace, size_t workspace_bytes, void* stream);
+/* Diagnostics of the last ec3r_match_batched on this workspace (device
+ * counters copied to host; synchronizes): rows / columns that needed the
+ * float64 full rescan. */
+EC3R_API int ec3r_match_stats(const void* workspace, int64_t total_a, int64_t total_b, int n_pairs,
+                     int64_t* rows_rescanned_h, int64_t* cols_rescanned_h, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K6  strided global loop retrieval
+ * replaces the scoring of update_similarity (loops.py:184-243).
+ * pooled: (K, D) float64 unit vectors in database insertion order.
+ * Coarse pass: every stride-th keyframe vs every later one with
+ * |dI| >= exclusion; hits s > tau_g refine over +-(stride-1) on both sides.
+ * Outputs (device): coarse_pairs (n_coarse x 2 int32 order indices),
+ * coarse_scores; cand_* = refined pairs with score > tau_l in the
+ * reference emission order (duplicates kept; the host applies the
+ * admitted-once rule); evaluated_* = every refined pair scored (for the
+ * similarity-matrix cache).  Counts go to counts (4 int64: coarse,
+ * candidates, evaluated, coarse hits).  Capacities: coarse =
+ * (k_end - k_begin) * ceil(K/stride), cand/evaluated = cap_refine, coarse
+ * hits = cap_refine / (2*stride-1)^2 + 1 (a count above a capacity means
+ * the list was truncated: grow and call again).
+ * ------------------------------------------------------------------- */
+EC3R_API int ec3r_retrieval(const double* pooled, int K, int D, int stride, int exclusion, double tau_g,
+                   double tau_l, int32_t* coarse_pairs, double* coarse_scores,
+                   int32_t* cand_pairs, double* cand_scores, int32_t* eval_pairs,
+                   double* eval_scores, int64_t cap_refine, int64_t* counts, int k_begin,
+                   int k_end, void* workspace, size_t workspace_bytes, void* stream);
+EC3R_API size_t ec3r_retrieval_workspace(int K, int stride, int64_t cap_refine);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EC3R_B200_H */

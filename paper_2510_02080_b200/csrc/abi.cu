@@ -1,0 +1,108 @@
+// C-ABI plumbing: version, thread-local error strings, and the matcher entry
+// point that sequences the tensor-core pass and the exact re-scoring.
+
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "common.cuh"
+#include "match.cuh"
+
+namespace ec3r {
+
+static thread_local char g_last_error[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_last_error(const char* where, cudaError_t e) {
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+void set_last_error_msg(const char* msg) { snprintf(g_last_error, sizeof(g_last_error), "%s", msg); }
+
+// tensor-core approximate pass (match_tc.cu)
+int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, const int64_t* b_off_d,
+                 const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
+                 MatchRowState* rs, int32_t* col_best, int32_t* flag_rows, int32_t* flag_cols, int64_t* counters,
+                 void* tc_ws, size_t tc_ws_bytes, cudaStream_t st);
+size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs);
+
+}  // namespace ec3r
+
+using namespace ec3r;
+
+extern "C" int ec3r_abi_version(void) { return EC3R_ABI_VERSION; }
+extern "C" uint64_t ec3r_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+extern "C" const char* ec3r_last_error(void) { return g_last_error; }
+
+// Workspace of ec3r_match_batched:
+//   a_off, b_off (n_pairs+1 int64 each), row state (total_a), col best
+//   (total_b), flagged rows / cols lists (total_a / total_b int32),
+//   counters (8 int64), then the tensor-core pass workspace.
+extern "C" size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_pairs) {
+    return 2 * align256(sizeof(int64_t) * (size_t)(n_pairs + 1)) + align256(sizeof(MatchRowState) * (size_t)total_a) +
+           align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int32_t) * (size_t)total_a) +
+           align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int64_t) * 8) +
+           match_tc_workspace(total_a, total_b, n_pairs);
+}
+
+extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
+                                  int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
+                                  double ratio, int32_t* match_b, int32_t* n_match, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    if (n_pairs < 0 || D <= 0 || !a_off_h || !b_off_h || exact_dtype < 0 || exact_dtype > 2) return EC3R_EARG;
+    if (n_pairs == 0) return EC3R_OK;
+    const int64_t total_a = a_off_h[n_pairs], total_b = b_off_h[n_pairs];
+    if (!workspace || workspace_bytes < ec3r_match_workspace(total_a, total_b, n_pairs)) return EC3R_EWORKSPACE;
+    if (exact_dtype == 0) { A_x = A; B_x = B; }
+    if ((total_a && !A_x) || (total_b && !B_x)) return EC3R_EARG;
+    cudaStream_t st = as_stream(stream);
+    Carver cv{(char*)workspace, 0};
+    int64_t* a_off = cv.take<int64_t>(n_pairs + 1);
+    int64_t* b_off = cv.take<int64_t>(n_pairs + 1);
+    MatchRowState* rs = cv.take<MatchRowState>(total_a);
+    int32_t* col_best = cv.take<int32_t>(total_b);
+    int32_t* flag_rows = cv.take<int32_t>(total_a);
+    int32_t* flag_cols = cv.take<int32_t>(total_b);
+    int64_t* counters = cv.take<int64_t>(8);
+    void* tc_ws = cv.base + cv.used;
+    const size_t tc_bytes = workspace_bytes - cv.used;
+    EC3R_CUDA_TRY(cudaMemcpyAsync(a_off, a_off_h, sizeof(int64_t) * (n_pairs + 1), cudaMemcpyHostToDevice, st));
+    EC3R_CUDA_TRY(cudaMemcpyAsync(b_off, b_off_h, sizeof(int64_t) * (n_pairs + 1), cudaMemcpyHostToDevice, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 8, st));
+    int rc;
+    if (A != nullptr && B != nullptr && total_a > 0 && total_b > 0) {
+        // tensor-core pass: certifies most rows / columns and lists the rest
+        rc = match_tc_run(A, B, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, rs, col_best, flag_rows,
+                          flag_cols, counters, tc_ws, tc_bytes, st);
+        if (rc) return rc;
+        rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
+                                  flag_cols, counters + 1, 0, rs, col_best, st);
+    } else {
+        rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, nullptr, nullptr, total_a, nullptr,
+                                  nullptr, total_b, rs, col_best, st);
+    }
+    if (rc) return rc;
+    return match_finalize(rs, col_best, a_off, b_off, n_pairs, total_a, ratio, match_b, n_match, st);
+}
+
+extern "C" int ec3r_match_stats(const void* workspace, int64_t total_a, int64_t total_b, int n_pairs,
+                                int64_t* rows_h, int64_t* cols_h, void* stream) {
+    if (!workspace || !rows_h || !cols_h || n_pairs < 1) return EC3R_EARG;
+    Carver cv{(char*)workspace, 0};
+    cv.take<int64_t>(n_pairs + 1);
+    cv.take<int64_t>(n_pairs + 1);
+    cv.take<MatchRowState>(total_a);
+    cv.take<int32_t>(total_b);
+    cv.take<int32_t>(total_a);
+    cv.take<int32_t>(total_b);
+    int64_t* counters = cv.take<int64_t>(8);
+    int64_t c[2];
+    cudaStream_t st = as_stream(stream);
+    EC3R_CUDA_TRY(cudaMemcpyAsync(c, counters, sizeof(c), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    *rows_h = c[0];
+    *cols_h = c[1];
+    return EC3R_OK;
+}

@@ -1,0 +1,537 @@
+// K2+K3: batched confidence-weighted Umeyama Sim(3) on sm_100a.
+//
+// One thread-block CLUSTER (8 CTAs) per alignment problem.  Every phase
+// streams the problem's data once with coalesced (128-bit where possible)
+// loads, reduces per thread in float64, then per CTA (fixed shuffle tree) and
+// across the cluster through distributed shared memory (fixed rank order), so
+// results are deterministic and independent of scheduling.  The 3x3 closed
+// form (one-sided Jacobi SVD, reflection guard, scale, translation,
+// Shepperd quaternion) runs redundantly in one thread of every CTA from the
+// identical cluster totals, so no extra broadcast round is needed.
+//
+// Reference: registration.py:38-102 (align_point_sets), mapping.py:138-183
+// (_shared_correspondences + gate/floor of _registration_edges).
+
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+
+namespace ec3r {
+
+constexpr int UM_CL = 8;    // CTAs per cluster (portable maximum)
+constexpr int UM_NT = 256;  // threads per CTA
+
+// Reduce K doubles across the CTA: result valid in out[0..K) for all threads
+// after the trailing __syncthreads.  scratch: (UM_NT/32) * K doubles.
+template <int K>
+__device__ __forceinline__ void cta_sum(double (&v)[K], double* scratch, double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        v[k] = x;
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) scratch[warp * K + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double r = 0;
+#pragma unroll
+        for (int w = 0; w < UM_NT / 32; ++w) r += scratch[w * K + threadIdx.x];
+        out[threadIdx.x] = r;
+    }
+    __syncthreads();
+}
+
+// Sum a K-vector published by every CTA of the cluster, in rank order.
+template <int K>
+__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double* part, double* tot) {
+    cl.sync();
+    if (threadIdx.x < K) {
+        double r = 0;
+        for (int c = 0; c < UM_CL; ++c) r += cl.map_shared_rank(part, c)[threadIdx.x];
+        tot[threadIdx.x] = r;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void write_sim3(double* o, const Solution& s) {
+    o[0] = s.s;
+    o[1] = s.quat[0]; o[2] = s.quat[1]; o[3] = s.quat[2]; o[4] = s.quat[3];
+    o[5] = s.t[0]; o[6] = s.t[1]; o[7] = s.t[2];
+}
+
+// ---------------------------------------------------------------------------
+// Explicit correspondences (align_point_sets API).  Element e of a problem is
+// owned by thread (e % UM_NT) of CTA ((e / UM_NT) % UM_CL): the grouping is a
+// function of the element index only, so appending zero-weight elements adds
+// exact +0.0 terms and leaves every result bit-identical
+// (pkg/tests/test_registration.py:52-71).
+template <bool HAS_W>
+__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT)
+umeyama_explicit_kernel(const double* __restrict__ P, const double* __restrict__ Q,
+                        const double* __restrict__ Wt, const int64_t* __restrict__ off,
+                        int with_scale, double* __restrict__ out_sim3, double* __restrict__ out_rms,
+                        int32_t* __restrict__ out_status) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int b = blockIdx.x / UM_CL;
+    const int64_t i0 = off[b];
+    const int64_t n = off[b + 1] - i0;
+    __shared__ double scratch[(UM_NT / 32) * 16];
+    __shared__ double part1[8], part2[16], part3[4];
+    __shared__ double tot1[8], tot2[16], tot3[4];
+    __shared__ Solution sol;
+    if (n < 3) {  // registration.py:59-60 (uniform across the cluster)
+        if (rank == 0 && threadIdx.x == 0) out_status[b] = EC3R_ST_TOO_FEW;
+        return;
+    }
+    const double* p = P + 3 * i0;
+    const double* q = Q + 3 * i0;
+    const double* w = HAS_W ? Wt + i0 : nullptr;
+    const int64_t stride = (int64_t)UM_CL * UM_NT;
+    const int64_t first = (int64_t)rank * UM_NT + threadIdx.x;
+
+    // phase 1: W, sum w p, sum w q  (registration.py:67-73)
+    double a1[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t e = first; e < n; e += stride) {
+        const double wi = HAS_W ? w[e] : 1.0;
+        a1[0] += wi;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            a1[1 + k] += wi * p[3 * e + k];
+            a1[4 + k] += wi * q[3 * e + k];
+        }
+    }
+    cta_sum<7>(a1, scratch, part1);
+    cluster_sum<7>(cl, part1, tot1);
+    const double Wsum = tot1[0];
+    if (!(Wsum > 0)) {  // registration.py:68-69
+        if (rank == 0 && threadIdx.x == 0) out_status[b] = EC3R_ST_ALL_ZERO;
+        cl.sync();
+        return;
+    }
+    double pbar[3], qbar[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { pbar[k] = tot1[1 + k] / Wsum; qbar[k] = tot1[4 + k] / Wsum; }
+
+    // phase 2: centred second moments (registration.py:74-77, 90)
+    double a2[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a2[k] = 0;
+    for (int64_t e = first; e < n; e += stride) {
+        const double wi = HAS_W ? w[e] : 1.0;
+        double dp[3], dq[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { dp[k] = p[3 * e + k] - pbar[k]; dq[k] = q[3 * e + k] - qbar[k]; }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double wq = wi * dq[i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) a2[3 * i + j] += wq * dp[j];
+        }
+        const double wp0 = wi * dp[0], wp1 = wi * dp[1], wp2 = wi * dp[2];
+        a2[9] += wp0 * dp[0]; a2[10] += wp0 * dp[1]; a2[11] += wp0 * dp[2];
+        a2[12] += wp1 * dp[1]; a2[13] += wp1 * dp[2]; a2[14] += wp2 * dp[2];
+        a2[15] += wi * (dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
+    }
+    cta_sum<16>(a2, scratch, part2);
+    cluster_sum<16>(cl, part2, tot2);
+    if (threadIdx.x == 0) {
+        Moments mo;
+        mo.W = Wsum;
+        for (int k = 0; k < 3; ++k) { mo.pbar[k] = pbar[k]; mo.qbar[k] = qbar[k]; }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) mo.C[i][j] = tot2[3 * i + j] / Wsum;
+        mo.M[0][0] = tot2[9] / Wsum; mo.M[0][1] = mo.M[1][0] = tot2[10] / Wsum;
+        mo.M[0][2] = mo.M[2][0] = tot2[11] / Wsum; mo.M[1][1] = tot2[12] / Wsum;
+        mo.M[1][2] = mo.M[2][1] = tot2[13] / Wsum; mo.M[2][2] = tot2[14] / Wsum;
+        mo.varq = tot2[15] / Wsum;
+        umeyama_solve(mo, with_scale, sol);
+    }
+    __syncthreads();
+
+    // phase 3: residual (registration.py:100-101) and the source singular
+    // values measured directly in the eigenbasis of the source scatter
+    // (registration.py:81-83), accurate to ~1e-16 of sv0 like LAPACK's SVD.
+    double a3[3] = {0, 0, 0};
+    const double s = sol.s;
+    double R[3][3], t[3], v0[3], v1[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        t[i] = sol.t[i];
+        v0[i] = sol.src_V[i][0];
+        v1[i] = sol.src_V[i][1];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) R[i][j] = sol.R[i][j];
+    }
+    for (int64_t e = first; e < n; e += stride) {
+        const double wi = HAS_W ? w[e] : 1.0;
+        const double px = p[3 * e], py = p[3 * e + 1], pz = p[3 * e + 2];
+        double r2 = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double r = s * (R[i][0] * px + R[i][1] * py + R[i][2] * pz) + t[i] - q[3 * e + i];
+            r2 += r * r;
+        }
+        a3[0] += wi * r2;
+        const double dx = px - pbar[0], dy = py - pbar[1], dz = pz - pbar[2];
+        const double y0 = v0[0] * dx + v0[1] * dy + v0[2] * dz;
+        const double y1 = v1[0] * dx + v1[1] * dy + v1[2] * dz;
+        a3[1] += wi * y0 * y0;
+        a3[2] += wi * y1 * y1;
+    }
+    cta_sum<3>(a3, scratch, part3);
+    cluster_sum<3>(cl, part3, tot3);
+    if (rank == 0 && threadIdx.x == 0) {
+        const double sv0 = sqrt(fmax(tot3[1] / Wsum, 0.0));
+        const double sv1 = sqrt(fmax(tot3[2] / Wsum, 0.0));
+        int st = sol.status;
+        if (src_degenerate(fmax(sv0, sv1), fmin(sv0, sv1))) st = EC3R_ST_DEGENERATE;
+        out_status[b] = st;
+        write_sim3(out_sim3 + 8 * b, sol);
+        out_rms[b] = sqrt(fmax(tot3[0] / Wsum, 0.0));
+    }
+    cl.sync();  // keep shared memory alive until every rank has read it
+}
+
+// ---------------------------------------------------------------------------
+// Pixel-identity registration edges over the resident frame pool.
+
+struct PoolArgs {
+    const float* depth;
+    const float* conf;
+    const double* slot_poses;  // n_slots x 8
+    const int32_t* seg_slots;  // n_seg x 2
+    const int32_t* edge_seg;   // n_edges + 1
+    int H, W;
+    double fx, fy, cx, cy;
+    double floor_frac;
+    int min_corr, with_scale;
+};
+
+__device__ __forceinline__ void load_rot(const double* x8, double R[3][3], double t[3]) {
+    quat_to_mat(x8 + 1, R);
+    t[0] = x8[5]; t[1] = x8[6]; t[2] = x8[7];
+}
+
+// Visit every pixel of the edge's segments owned by this thread (4 pixels per
+// visit: one 128-bit load from each of the four planes when aligned).
+template <typename F>
+__device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s1, int rank, F&& f) {
+    const int HW = a.H * a.W;
+    const bool vec = (HW & 3) == 0;
+    for (int sg = s0; sg < s1; ++sg) {
+        const int sa = a.seg_slots[2 * sg], sb = a.seg_slots[2 * sg + 1];
+        const float* da = a.depth + (size_t)sa * HW;
+        const float* ca = a.conf + (size_t)sa * HW;
+        const float* db = a.depth + (size_t)sb * HW;
+        const float* cb = a.conf + (size_t)sb * HW;
+        for (int pix = 4 * (rank * UM_NT + threadIdx.x); pix < HW; pix += 4 * UM_CL * UM_NT) {
+            float4 za, wa, zb, wb;
+            if (vec) {
+                za = __ldg(reinterpret_cast<const float4*>(da + pix));
+                wa = __ldg(reinterpret_cast<const float4*>(ca + pix));
+                zb = __ldg(reinterpret_cast<const float4*>(db + pix));
+                wb = __ldg(reinterpret_cast<const float4*>(cb + pix));
+            } else {
+                float t0[4], t1[4], t2[4], t3[4];
+                for (int k = 0; k < 4; ++k) {
+                    const bool in = pix + k < HW;
+                    t0[k] = in ? da[pix + k] : 0.f; t1[k] = in ? ca[pix + k] : 0.f;
+                    t2[k] = in ? db[pix + k] : 0.f; t3[k] = in ? cb[pix + k] : 0.f;
+                }
+                za = make_float4(t0[0], t0[1], t0[2], t0[3]); wa = make_float4(t1[0], t1[1], t1[2], t1[3]);
+                zb = make_float4(t2[0], t2[1], t2[2], t2[3]); wb = make_float4(t3[0], t3[1], t3[2], t3[3]);
+            }
+            f(sg, sa, sb, pix, za, wa, zb, wb);
+        }
+    }
+}
+
+__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT)
+register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restrict__ out_rms,
+                      int64_t* __restrict__ out_count, int64_t* __restrict__ out_npairs,
+                      int32_t* __restrict__ out_status, uint8_t* __restrict__ keep_masks) {
+    extern __shared__ double tabs[];  // xc[W], yc[H]  (ray coefficients, backend.py:89)
+    double* xc = tabs;
+    double* yc = tabs + a.W;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int e = blockIdx.x / UM_CL;
+    const int s0 = a.edge_seg[e], s1 = a.edge_seg[e + 1];
+    __shared__ double scratch[(UM_NT / 32) * 24];
+    __shared__ double part1[8], part2[24], part3[4];
+    __shared__ double tot1[8], tot2[24], tot3[4];
+    __shared__ float wmax_warp[UM_NT / 32];
+    __shared__ float part_wmax;
+    __shared__ Solution sol;
+    for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[u] = (u - a.cx) / a.fx;
+    for (int v = threadIdx.x; v < a.H; v += UM_NT) yc[v] = (v - a.cy) / a.fy;
+    __syncthreads();
+    const int W = a.W;
+
+    // ---- phase 1: validity, max of w = min(conf_a, conf_b), rough centroids
+    float wmax = -1.0f;
+    double a1[7] = {0, 0, 0, 0, 0, 0, 0};
+    int cur_seg = -1;
+    float Ra[3][3], ta[3], Rb[3][3], tb[3];
+    for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
+                                         float4 wb) {
+        if (sg != cur_seg) {
+            cur_seg = sg;
+            double R[3][3], t[3];
+            load_rot(a.slot_poses + 8 * sa, R, t);
+            for (int i = 0; i < 3; ++i) { ta[i] = (float)t[i]; for (int j = 0; j < 3; ++j) Ra[i][j] = (float)R[i][j]; }
+            load_rot(a.slot_poses + 8 * sb, R, t);
+            for (int i = 0; i < 3; ++i) { tb[i] = (float)t[i]; for (int j = 0; j < 3; ++j) Rb[i][j] = (float)R[i][j]; }
+        }
+        const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
+        const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
+        float sp[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
+        int nv = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (zA[k] > 0.f && zB[k] > 0.f) {
+                const int px = pix + k, v = px / W, u = px - v * W;
+                const float x = (float)xc[u], y = (float)yc[v];
+                wmax = fmaxf(wmax, fminf(cA[k], cB[k]));
+                ++nv;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    sp[i] += zA[k] * (Ra[i][0] * x + Ra[i][1] * y + Ra[i][2]) + ta[i];
+                    sq[i] += zB[k] * (Rb[i][0] * x + Rb[i][1] * y + Rb[i][2]) + tb[i];
+                }
+            }
+        }
+        a1[0] += nv;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { a1[1 + i] += sp[i]; a1[4 + i] += sq[i]; }
+    });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if ((threadIdx.x & 31) == 0) wmax_warp[threadIdx.x >> 5] = wmax;
+    cta_sum<7>(a1, scratch, part1);
+    if (threadIdx.x == 0) {
+        float m = -1.0f;
+        for (int w = 0; w < UM_NT / 32; ++w) m = fmaxf(m, wmax_warp[w]);
+        part_wmax = m;
+    }
+    cl.sync();
+    if (threadIdx.x < 7) {
+        double r = 0;
+        for (int c = 0; c < UM_CL; ++c) r += cl.map_shared_rank(part1, c)[threadIdx.x];
+        tot1[threadIdx.x] = r;
+    } else if (threadIdx.x == 7) {
+        float m = -1.0f;
+        for (int c = 0; c < UM_CL; ++c) m = fmaxf(m, *cl.map_shared_rank(&part_wmax, c));
+        tot1[7] = (double)m;
+    }
+    __syncthreads();
+    const double nvalid = tot1[0];
+    if (rank == 0 && threadIdx.x == 0) out_npairs[e] = (int64_t)nvalid;
+    if (nvalid < a.min_corr) {  // mapping.py:174
+        if (rank == 0 && threadIdx.x == 0) { out_status[e] = EC3R_ST_SKIP; out_count[e] = 0; }
+        cl.sync();
+        return;
+    }
+    // floor = frac * float(w.max())  (mapping.py:176), exact in float64
+    const double floorv = __dmul_rn(a.floor_frac, tot1[7]);
+    double shp[3], shq[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { shp[i] = tot1[1 + i] / nvalid; shq[i] = tot1[4 + i] / nvalid; }
+
+    // ---- phase 2: keep = w >= floor; shifted float64 raw moments
+    double a2[24];
+#pragma unroll
+    for (int k = 0; k < 24; ++k) a2[k] = 0;
+    cur_seg = -1;
+    double R2a[3][3], t2a[3], R2b[3][3], t2b[3];
+    for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
+                                         float4 wb) {
+        if (sg != cur_seg) {
+            cur_seg = sg;
+            load_rot(a.slot_poses + 8 * sa, R2a, t2a);
+            load_rot(a.slot_poses + 8 * sb, R2b, t2b);
+            for (int i = 0; i < 3; ++i) { t2a[i] -= shp[i]; t2b[i] -= shq[i]; }
+        }
+        const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
+        const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
+        uint32_t kbits = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool valid = zA[k] > 0.f && zB[k] > 0.f;
+            const float wf = fminf(cA[k], cB[k]);
+            const bool keep = valid && ((double)wf >= floorv);  // mapping.py:177
+            if (keep) {
+                kbits |= 1u << (8 * k);
+                const int px = pix + k, v = px / W, u = px - v * W;
+                const double wi = (double)wf;
+                const double x = xc[u], y = yc[v];
+                const double zaa = zA[k], zbb = zB[k];
+                double pp[3], qq[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    pp[i] = zaa * (R2a[i][0] * x + R2a[i][1] * y + R2a[i][2]) + t2a[i];
+                    qq[i] = zbb * (R2b[i][0] * x + R2b[i][1] * y + R2b[i][2]) + t2b[i];
+                }
+                a2[0] += wi;
+                a2[1] += 1.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double wp = wi * pp[i];
+                    a2[2 + i] += wp;
+                    a2[5 + i] += wi * qq[i];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) a2[8 + 3 * j + i] += wp * qq[j];  // sum w q_j p_i
+                }
+                const double wp0 = wi * pp[0], wp1 = wi * pp[1], wp2 = wi * pp[2];
+                a2[17] += wp0 * pp[0]; a2[18] += wp0 * pp[1]; a2[19] += wp0 * pp[2];
+                a2[20] += wp1 * pp[1]; a2[21] += wp1 * pp[2]; a2[22] += wp2 * pp[2];
+                a2[23] += wi * (qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2]);
+            }
+        }
+        if (keep_masks) {
+            const int HW = a.H * a.W;
+            uint8_t* km = keep_masks + (size_t)sg * HW + pix;
+            if (((HW & 3) == 0)) *reinterpret_cast<uint32_t*>(km) = kbits;
+            else for (int k = 0; k < 4 && pix + k < HW; ++k) km[k] = (kbits >> (8 * k)) & 1;
+        }
+    });
+    cta_sum<24>(a2, scratch, part2);
+    cluster_sum<24>(cl, part2, tot2);
+    const double Wsum = tot2[0], nkeep = tot2[1];
+    int early = 0;
+    if (nkeep < a.min_corr) early = EC3R_ST_SKIP;       // mapping.py:178
+    else if (nkeep < 3) early = EC3R_ST_TOO_FEW;         // registration.py:59
+    else if (!(Wsum > 0)) early = EC3R_ST_ALL_ZERO;      // registration.py:68
+    if (early) {
+        if (rank == 0 && threadIdx.x == 0) { out_status[e] = early; out_count[e] = (int64_t)nkeep; }
+        cl.sync();
+        return;
+    }
+    if (threadIdx.x == 0) {
+        Moments mo;
+        mo.W = Wsum;
+        double mp[3], mq[3];
+        for (int k = 0; k < 3; ++k) { mp[k] = tot2[2 + k] / Wsum; mq[k] = tot2[5 + k] / Wsum; }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) mo.C[i][j] = tot2[8 + 3 * i + j] / Wsum - mq[i] * mp[j];
+        const double m00 = tot2[17] / Wsum - mp[0] * mp[0], m01 = tot2[18] / Wsum - mp[0] * mp[1];
+        const double m02 = tot2[19] / Wsum - mp[0] * mp[2], m11 = tot2[20] / Wsum - mp[1] * mp[1];
+        const double m12 = tot2[21] / Wsum - mp[1] * mp[2], m22 = tot2[22] / Wsum - mp[2] * mp[2];
+        mo.M[0][0] = m00; mo.M[0][1] = mo.M[1][0] = m01; mo.M[0][2] = mo.M[2][0] = m02;
+        mo.M[1][1] = m11; mo.M[1][2] = mo.M[2][1] = m12; mo.M[2][2] = m22;
+        mo.varq = tot2[23] / Wsum - (mq[0] * mq[0] + mq[1] * mq[1] + mq[2] * mq[2]);
+        for (int k = 0; k < 3; ++k) { mo.pbar[k] = shp[k] + mp[k]; mo.qbar[k] = shq[k] + mq[k]; }
+        umeyama_solve(mo, a.with_scale, sol);
+        // stash the in-shift source centroid for the refinement pass
+        sol.rms2_closed = fmax(sol.rms2_closed, 0.0);
+        tot3[0] = mp[0]; tot3[1] = mp[1]; tot3[2] = mp[2];
+    }
+    __syncthreads();
+    bool degenerate = src_degenerate(sqrt(sol.src_lambda[0]), sqrt(sol.src_lambda[1]));
+    // Gram eigenvalues resolve sv1/sv0 only down to ~1e-8: near-degenerate
+    // edges get the direct eigenbasis pass (uniform decision in the cluster).
+    if (sol.src_lambda[1] <= 1e-10 * sol.src_lambda[0]) {
+        const double mp0 = tot3[0], mp1 = tot3[1], mp2 = tot3[2];
+        double v0[3], v1[3];
+        for (int i = 0; i < 3; ++i) { v0[i] = sol.src_V[i][0]; v1[i] = sol.src_V[i][1]; }
+        double a3[2] = {0, 0};
+        cur_seg = -1;
+        for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
+                                             float4 wb) {
+            if (sg != cur_seg) {
+                cur_seg = sg;
+                load_rot(a.slot_poses + 8 * sa, R2a, t2a);
+                for (int i = 0; i < 3; ++i) t2a[i] -= shp[i];
+            }
+            const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
+            const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
+            for (int k = 0; k < 4; ++k) {
+                const float wf = fminf(cA[k], cB[k]);
+                if (zA[k] > 0.f && zB[k] > 0.f && (double)wf >= floorv) {
+                    const int px = pix + k, v = px / W, u = px - v * W;
+                    const double x = xc[u], y = yc[v], z = zA[k];
+                    double d[3];
+                    for (int i = 0; i < 3; ++i) d[i] = z * (R2a[i][0] * x + R2a[i][1] * y + R2a[i][2]) + t2a[i];
+                    d[0] -= mp0; d[1] -= mp1; d[2] -= mp2;
+                    const double y0 = v0[0] * d[0] + v0[1] * d[1] + v0[2] * d[2];
+                    const double y1 = v1[0] * d[0] + v1[1] * d[1] + v1[2] * d[2];
+                    a3[0] += wf * y0 * y0;
+                    a3[1] += wf * y1 * y1;
+                }
+            }
+        });
+        __syncthreads();
+        cta_sum<2>(a3, scratch, part3);
+        cluster_sum<2>(cl, part3, tot3 + 2);  // tot3[2..3]; tot3[0..1] no longer needed
+        const double sv0 = sqrt(fmax(tot3[2] / Wsum, 0.0)), sv1 = sqrt(fmax(tot3[3] / Wsum, 0.0));
+        degenerate = src_degenerate(fmax(sv0, sv1), fmin(sv0, sv1));
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+        int st = sol.status;
+        if (degenerate) st = EC3R_ST_DEGENERATE;
+        out_status[e] = st;
+        out_count[e] = (int64_t)nkeep;
+        write_sim3(out_sim3 + 8 * e, sol);
+        out_rms[e] = sqrt(sol.rms2_closed);
+    }
+    cl.sync();
+}
+
+}  // namespace ec3r
+
+using namespace ec3r;
+
+extern "C" size_t ec3r_umeyama_workspace(int) { return 0; }
+
+extern "C" int ec3r_umeyama_batched(const double* p, const double* q, const double* w,
+                                    const int64_t* offsets, int n_problems, int with_scale,
+                                    double* out_sim3, double* out_rms, int32_t* out_status, void*,
+                                    size_t, void* stream) {
+    if (n_problems < 0 || !p || !q || !offsets || !out_sim3 || !out_rms || !out_status) return EC3R_EARG;
+    if (n_problems == 0) return EC3R_OK;
+    dim3 grid(n_problems * UM_CL), block(UM_NT);
+    if (w)
+        umeyama_explicit_kernel<true><<<grid, block, 0, as_stream(stream)>>>(p, q, w, offsets, with_scale,
+                                                                            out_sim3, out_rms, out_status);
+    else
+        umeyama_explicit_kernel<false><<<grid, block, 0, as_stream(stream)>>>(p, q, w, offsets, with_scale,
+                                                                             out_sim3, out_rms, out_status);
+    EC3R_CHECK_LAUNCH("umeyama_explicit_kernel");
+    return EC3R_OK;
+}
+
+extern "C" size_t ec3r_register_edges_workspace(int) { return 0; }
+
+extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_pool, int H, int W,
+                                   const double* K4_h, const double* slot_poses, const int32_t* seg_slots,
+                                   const int32_t* edge_seg, int n_edges, double floor_frac, int min_corr,
+                                   int with_scale, double* out_sim3, double* out_rms, int64_t* out_count,
+                                   int64_t* out_npairs, int32_t* out_status, uint8_t* keep_masks, void*,
+                                   size_t, void* stream) {
+    if (n_edges < 0 || H <= 0 || W <= 0 || !depth_pool || !conf_pool || !K4_h || !slot_poses || !seg_slots ||
+        !edge_seg)
+        return EC3R_EARG;
+    if (n_edges == 0) return EC3R_OK;
+    PoolArgs a;
+    a.depth = depth_pool; a.conf = conf_pool; a.slot_poses = slot_poses; a.seg_slots = seg_slots;
+    a.edge_seg = edge_seg; a.H = H; a.W = W;
+    a.fx = K4_h[0]; a.fy = K4_h[1]; a.cx = K4_h[2]; a.cy = K4_h[3];
+    a.floor_frac = floor_frac; a.min_corr = min_corr; a.with_scale = with_scale;
+    const size_t smem = sizeof(double) * (size_t)(H + W);
+    if (smem > 48 * 1024) {
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+    }
+    register_edges_kernel<<<n_edges * UM_CL, UM_NT, smem, as_stream(stream)>>>(a, out_sim3, out_rms, out_count,
+                                                                               out_npairs, out_status, keep_masks);
+    EC3R_CHECK_LAUNCH("register_edges_kernel");
+    return EC3R_OK;
+}

@@ -1,0 +1,170 @@
+"""Drop-in for the global-retrieval scoring of ``submap_slam.loops``
+(update_similarity, loops.py:184-243) on the B200 path (K6,
+csrc/retrieval.cu).
+
+The GPU scores the strided coarse grid and the refinement windows in float64
+and emits them in the reference's emission order; the host applies only the
+stateful parts of the reference — the similarity-matrix cache
+(loops.py:201-210) and the admitted-once set kept on the matrix
+(loops.py:212-216, 240-242).  ``RetrievalDB`` keeps the pooled vectors
+resident for repeated calls and shards the coarse rows across ranks.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class SimilarityMatrix:
+    """loops.py:156-176 (used when the reference class is not at hand)."""
+
+    def __init__(self):
+        self._scores: dict = {}
+
+    @staticmethod
+    def _key(a, b):
+        return (a, b) if a <= b else (b, a)
+
+    def set(self, a, b, score):
+        self._scores[self._key(a, b)] = score
+
+    def get(self, a, b):
+        return self._scores.get(self._key(a, b))
+
+    def __len__(self):
+        return len(self._scores)
+
+    def items(self):
+        return self._scores.items()
+
+
+def retrieval_device(pooled: torch.Tensor, stride: int, exclusion: int, tau_g: float, tau_l: float,
+                     k_begin: int = 0, k_end: int = -1, cap_refine: int = 1 << 16, stream=None):
+    """Run K6 on a (K, D) float64 CUDA tensor.  Returns numpy arrays
+    (coarse_pairs, coarse_scores, cand_pairs, cand_scores, eval_pairs,
+    eval_scores) of ORDER indices, growing capacities until nothing is
+    truncated."""
+    L = _lib.lib()
+    K, D = pooled.shape
+    dev = pooled.device
+    Kc = (K + stride - 1) // stride
+    kb = max(0, k_begin)
+    ke = Kc if k_end is None or k_end < 0 or k_end > Kc else k_end
+    rows = max(ke - kb, 0)
+    R = (2 * stride - 1) ** 2
+    while True:
+        cap_c = max(rows * Kc, 1)
+        cp = torch.empty((cap_c, 2), dtype=torch.int32, device=dev)
+        cs = torch.empty(cap_c, dtype=torch.float64, device=dev)
+        qp = torch.empty((cap_refine, 2), dtype=torch.int32, device=dev)
+        qs = torch.empty(cap_refine, dtype=torch.float64, device=dev)
+        ep = torch.empty((cap_refine, 2), dtype=torch.int32, device=dev)
+        es = torch.empty(cap_refine, dtype=torch.float64, device=dev)
+        counts = torch.zeros(4, dtype=torch.int64, device=dev)
+        wsb = L.ec3r_retrieval_workspace(K, stride, cap_refine)
+        ws = _lib.workspace(wsb, dev, "retrieval")
+        _lib.check(L.ec3r_retrieval(_lib.ptr(pooled), K, D, stride, exclusion, float(tau_g), float(tau_l),
+                                    _lib.ptr(cp), _lib.ptr(cs), _lib.ptr(qp), _lib.ptr(qs), _lib.ptr(ep),
+                                    _lib.ptr(es), cap_refine, _lib.ptr(counts), kb, ke, _lib.ptr(ws), ws.numel(),
+                                    _lib.stream_ptr(stream)), "ec3r_retrieval")
+        n_c, n_q, n_e, n_h = (int(x) for x in counts.cpu())
+        if n_q <= cap_refine and n_e <= cap_refine and n_h <= cap_refine // R + 1:
+            break
+        cap_refine = max(cap_refine * 4, (n_h + 1) * R, n_e)
+    return (cp[:n_c].cpu().numpy(), cs[:n_c].cpu().numpy(), qp[:n_q].cpu().numpy(), qs[:n_q].cpu().numpy(),
+            ep[:n_e].cpu().numpy(), es[:n_e].cpu().numpy())
+
+
+def _populate(matrix, kfs: np.ndarray, pairs: np.ndarray, scores: np.ndarray):
+    if len(pairs) == 0:
+        return
+    a = kfs[pairs[:, 0]]
+    b = kfs[pairs[:, 1]]
+    lo = np.minimum(a, b).tolist()
+    hi = np.maximum(a, b).tolist()
+    store = getattr(matrix, "_scores", None)
+    if isinstance(store, dict):
+        store.update(zip(zip(lo, hi), scores.tolist()))
+    else:
+        for x, y, s in zip(lo, hi, scores.tolist()):
+            matrix.set(x, y, s)
+
+
+def admit(matrix, kfs: np.ndarray, cand_pairs: np.ndarray, cand_scores: np.ndarray):
+    """Admitted-once rule (loops.py:212-216, 240-242) over candidates in
+    emission order; the set lives on the matrix like the reference's."""
+    seen = getattr(matrix, "_admitted", None)
+    if seen is None:
+        seen = set()
+        matrix._admitted = seen
+    out = []
+    a = kfs[cand_pairs[:, 0]].tolist() if len(cand_pairs) else []
+    b = kfs[cand_pairs[:, 1]].tolist() if len(cand_pairs) else []
+    for x, y, s in zip(a, b, cand_scores.tolist()):
+        key = (x, y) if x <= y else (y, x)
+        if key not in seen:
+            seen.add(key)
+            out.append((key, s))
+    return out
+
+
+def update_similarity(matrix, database, stride: int, cfg) -> list:
+    """loops.py:184-243 — extend the similarity matrix; returns pairs newly
+    over tau_local, in the reference's emission order."""
+    _lib.lib()
+    order = [kf for kf in database.ids_in_order() if database.get(kf).pooled is not None]
+    if not order:
+        return []
+    pooled = torch.as_tensor(np.stack([np.asarray(database.get(kf).pooled, np.float64) for kf in order]),
+                             device="cuda")
+    kfs = np.asarray(order, dtype=np.int64)
+    cp, cs, qp, qs, ep, es = retrieval_device(pooled, int(stride), int(cfg.exclusion_zone()),
+                                              float(cfg.tau_global), float(cfg.tau_local))
+    _populate(matrix, kfs, cp, cs)
+    _populate(matrix, kfs, ep, es)
+    return admit(matrix, kfs, qp, qs)
+
+
+class RetrievalDB:
+    """Resident pooled-vector database (database.py:72-80 pooled vectors in
+    insertion order) for repeated / sharded retrieval."""
+
+    def __init__(self, dim: int, capacity: int = 1024, device=None):
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.dim = int(dim)
+        self.vec = torch.zeros((capacity, self.dim), dtype=torch.float64, device=self.device)
+        self.kf = np.zeros(capacity, dtype=np.int64)
+        self.n = 0
+
+    def append(self, kf_ids, pooled):
+        pooled = torch.as_tensor(np.asarray(pooled, np.float64).reshape(-1, self.dim), device=self.device)
+        k = pooled.shape[0]
+        if self.n + k > self.vec.shape[0]:
+            cap = self.vec.shape[0]
+            while cap < self.n + k:
+                cap *= 2
+            v = torch.zeros((cap, self.dim), dtype=torch.float64, device=self.device)
+            v[: self.n] = self.vec[: self.n]
+            self.vec = v
+            kf = np.zeros(cap, np.int64)
+            kf[: self.n] = self.kf[: self.n]
+            self.kf = kf
+        self.vec[self.n:self.n + k] = pooled
+        self.kf[self.n:self.n + k] = np.asarray(kf_ids, np.int64)
+        self.n += k
+
+    def score(self, stride: int, exclusion: int, tau_g: float, tau_l: float, k_begin: int = 0, k_end: int = -1):
+        return retrieval_device(self.vec[: self.n], stride, exclusion, tau_g, tau_l, k_begin, k_end)
+
+    def update(self, matrix, stride: int, cfg, k_begin: int = 0, k_end: int = -1) -> list:
+        cp, cs, qp, qs, ep, es = self.score(stride, cfg.exclusion_zone(), cfg.tau_global, cfg.tau_local,
+                                            k_begin, k_end)
+        kfs = self.kf[: self.n]
+        _populate(matrix, kfs, cp, cs)
+        _populate(matrix, kfs, ep, es)
+        return admit(matrix, kfs, qp, qs)

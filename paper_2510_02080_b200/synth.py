@@ -1,0 +1,239 @@
+"""Synthetic workloads of the BASELINE configs, generated on the device
+(input harness, not product compute).
+
+Mirrors the reference's synthetic producer: an axis-aligned box room with
+solid interior boxes ray-cast by slab tests (_kernels/_numpy.py:29-47,
+scenesim.py:145-163), log-normal depth noise with conf = 1/(1+|xi|) and a
+per-decode scale gauge (backend.py:240-273), keyframe-buffer flushes of
+"5 new + 1 old" frames (loops.py:89-111), landmark-tag descriptors with
+sigma noise and 20% spurious rows (backend.py:283-311) rounded to
+bf16-representable values, and pooled retrieval embeddings
+(backend.py:216-226, database.py:78-80).  Everything is a pure function of
+the seed (torch.Generator), so the CPU oracle can regenerate any slice.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+
+@dataclass(frozen=True)
+class SceneConfig:
+    room: tuple = (8.0, 8.0, 4.0)
+    boxes: tuple = (((1.0, 1.0, -2.0), (2.2, 2.0, -0.6)), ((-2.6, -1.0, -2.0), (-1.6, 0.4, 0.4)),
+                    ((0.4, -3.0, -2.0), (1.4, -2.2, -1.0)))
+    width: int = 518
+    height: int = 392
+    focal: float = 400.0
+    depth_noise_sigma: float = 0.01
+    gauge_range: tuple = (0.8, 1.25)
+    radius: float = 2.0
+    laps: float = 1.5
+
+
+def intrinsics(cfg: SceneConfig):
+    return np.array([cfg.focal, cfg.focal, (cfg.width - 1) / 2.0, (cfg.height - 1) / 2.0])
+
+
+def _look_rotation(forward: np.ndarray) -> np.ndarray:
+    """scenesim.look_rotation (world_from_cam, camera z along forward)."""
+    z = forward / np.linalg.norm(forward)
+    up = np.array([0.0, 0.0, 1.0])
+    x = np.cross(up, z)
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    return np.stack([x, y, z], axis=1)
+
+
+def _mat_to_quat(m):
+    t = np.trace(m)
+    if t > 0:
+        r = math.sqrt(1.0 + t)
+        s = 0.5 / r
+        q = np.array([0.5 * r, (m[2, 1] - m[1, 2]) * s, (m[0, 2] - m[2, 0]) * s, (m[1, 0] - m[0, 1]) * s])
+    else:
+        i = int(np.argmax(np.diag(m)))
+        j, k = (i + 1) % 3, (i + 2) % 3
+        r = math.sqrt(1.0 + m[i, i] - m[j, j] - m[k, k])
+        s = 0.5 / r
+        q = np.empty(4)
+        q[0] = (m[k, j] - m[j, k]) * s
+        q[1 + i] = 0.5 * r
+        q[1 + j] = (m[j, i] + m[i, j]) * s
+        q[1 + k] = (m[k, i] + m[i, k]) * s
+    return q / np.linalg.norm(q)
+
+
+def trajectory(n: int, cfg: SceneConfig, seed: int = 0):
+    """Circular keyframe trajectory (laps > 1 gives revisits) with a small
+    height wobble: world_from_cam (R (n,3,3), t (n,3))."""
+    rng = np.random.default_rng(seed)
+    R = np.zeros((n, 3, 3))
+    t = np.zeros((n, 3))
+    for i in range(n):
+        a = 2.0 * math.pi * cfg.laps * i / max(n - 1, 1)
+        t[i] = [cfg.radius * math.cos(a), cfg.radius * math.sin(a), 0.15 * math.sin(3 * a)]
+        fwd = np.array([-math.sin(a), math.cos(a), 0.05 * rng.normal()])
+        R[i] = _look_rotation(fwd)
+    return R, t
+
+
+def raycast_depth(R: torch.Tensor, t: torch.Tensor, cfg: SceneConfig) -> torch.Tensor:
+    """Perspective depth of frames (F,3,3)/(F,3) -> (F,H,W) float64, 0 = miss
+    (first hit of room shell + solid boxes, _kernels/_numpy.py:29-47)."""
+    dev = R.device
+    F = R.shape[0]
+    K = intrinsics(cfg)
+    u = torch.arange(cfg.width, dtype=torch.float64, device=dev)
+    v = torch.arange(cfg.height, dtype=torch.float64, device=dev)
+    vv, uu = torch.meshgrid(v, u, indexing="ij")
+    dcam = torch.stack([(uu - K[2]) / K[0], (vv - K[3]) / K[1], torch.ones_like(uu)], dim=-1)  # (H,W,3)
+    out = torch.empty((F, cfg.height, cfg.width), dtype=torch.float64, device=dev)
+    half = torch.tensor(cfg.room, dtype=torch.float64, device=dev) / 2
+    shapes = [(-half, half)] + [(torch.tensor(a, dtype=torch.float64, device=dev),
+                                 torch.tensor(b, dtype=torch.float64, device=dev)) for a, b in cfg.boxes]
+    eps = 1e-9
+    for f in range(F):
+        d = dcam @ R[f].T  # world directions (H,W,3)
+        o = t[f]
+        with torch.no_grad():
+            inv = 1.0 / d
+            best = torch.full(d.shape[:2], float("inf"), dtype=torch.float64, device=dev)
+            for bmin, bmax in shapes:
+                t1 = (bmin - o) * inv
+                t2 = (bmax - o) * inv
+                near = torch.minimum(t1, t2).amax(-1)
+                far = torch.maximum(t1, t2).amin(-1)
+                ok = (near <= far) & (far > eps)
+                hit = torch.where(near > eps, near, far)
+                best = torch.where(ok, torch.minimum(best, hit), best)
+            out[f] = torch.where(torch.isfinite(best), best, torch.zeros_like(best))
+    return out
+
+
+@dataclass
+class SubmapBatch:
+    """Decoded submaps of a run, ready for the FramePool."""
+
+    frame_ids: list      # per submap tuple of keyframe ids (new..., old)
+    depth: torch.Tensor  # (S, H, W) float32, S = total slots
+    conf: torch.Tensor
+    poses8: np.ndarray   # (S, 8) anchor_from_cam
+    slot_offsets: list   # per submap first slot
+    gauges: np.ndarray   # injected scales
+    K4: np.ndarray
+
+
+def flush_batches(n_keyframes: int, capacity: int = 5):
+    """KeyframeBuffer flush sequence (loops.py:89-111): first batch holds
+    capacity+1 new frames, then (capacity new, 1 old)."""
+    out = []
+    new, old = [], []
+    for kf in range(n_keyframes):
+        new.append(kf)
+        if len(new) + len(old) > capacity:
+            out.append(tuple(new) + tuple(old))
+            new, old = [], [kf]
+    return out
+
+
+def make_submaps(n_keyframes: int, cfg: SceneConfig = SceneConfig(), seed: int = 0, device="cuda",
+                 invalid_fraction: float = 0.0) -> SubmapBatch:
+    """Decoded submaps of a run of n_keyframes (synthetic decode, backend.py:228-281)."""
+    Rw, tw = trajectory(n_keyframes, cfg, seed)
+    batches = flush_batches(n_keyframes)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1000 + seed)
+    rng = np.random.default_rng(2000 + seed)
+    S = sum(len(b) for b in batches)
+    depth = torch.empty((S, cfg.height, cfg.width), dtype=torch.float32, device=device)
+    conf = torch.empty_like(depth)
+    poses8 = np.zeros((S, 8))
+    offs, gauges = [], []
+    Rd = torch.as_tensor(Rw, device=device)
+    td = torch.as_tensor(tw, device=device)
+    base_depth = {}
+    s = 0
+    for bi, b in enumerate(batches):
+        offs.append(s)
+        lo, hi = cfg.gauge_range
+        scale = float(rng.uniform(lo, hi))
+        gauges.append(scale)
+        ids = list(b)
+        need = [k for k in ids if k not in base_depth]
+        if need:
+            dd = raycast_depth(Rd[need], td[need], cfg)
+            for k, d in zip(need, dd):
+                base_depth[k] = d
+        anchor = ids[0]
+        Ra, ta = Rw[anchor], tw[anchor]
+        for k in ids:
+            d = base_depth[k] * scale
+            xi = torch.randn(d.shape, generator=gen, device=device, dtype=torch.float64)
+            d = d * torch.exp(cfg.depth_noise_sigma * xi)
+            c = 1.0 / (1.0 + xi.abs())
+            if invalid_fraction > 0:
+                drop = torch.rand(d.shape, generator=gen, device=device) < invalid_fraction
+                d = torch.where(drop, torch.zeros_like(d), d)
+            c = torch.where(d > 0, c, torch.zeros_like(c))
+            depth[s] = d.to(torch.float32)
+            conf[s] = c.to(torch.float32)
+            Rrel = Ra.T @ Rw[k]
+            trel = Ra.T @ (tw[k] - ta) * scale
+            poses8[s] = np.concatenate([[1.0], _mat_to_quat(Rrel), trel])
+            s += 1
+        # keep memory bounded: drop frames the next batch does not reference
+        nxt = set(batches[bi + 1]) if bi + 1 < len(batches) else set()
+        for k in list(base_depth):
+            if k not in nxt:
+                del base_depth[k]
+    return SubmapBatch([tuple(b) for b in batches], depth, conf, poses8, offs, np.array(gauges), intrinsics(cfg))
+
+
+def bf16_round(x: torch.Tensor) -> torch.Tensor:
+    return x.to(torch.bfloat16).to(x.dtype)
+
+
+def make_descriptor_pairs(n_pairs: int, n: int, m: int, d: int = 256, sigma: float = 0.05, spurious: float = 0.2,
+                          seed: int = 0, device="cuda"):
+    """(A_bits, B_bits, a_off, b_off): per pair, A = observed frame
+    descriptors (tags + sigma noise, renormalised, `spurious` fresh rows),
+    B = map tags (a random subset of size m); bf16-representable."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    A = torch.empty((n_pairs * n, d), dtype=torch.bfloat16, device=device)
+    B = torch.empty((n_pairs * m, d), dtype=torch.bfloat16, device=device)
+    for p in range(n_pairs):
+        tags = torch.randn((max(n, m), d), generator=g, device=device, dtype=torch.float32)
+        tags = tags / tags.norm(dim=1, keepdim=True)
+        bmap = tags[torch.randperm(tags.shape[0], generator=g, device=device)[:m]]
+        obs = tags[:n] + sigma * torch.randn((n, d), generator=g, device=device)
+        spur = torch.rand(n, generator=g, device=device) < spurious
+        fresh = torch.randn((n, d), generator=g, device=device)
+        obs = torch.where(spur[:, None], fresh, obs)
+        obs = obs / obs.norm(dim=1, keepdim=True)
+        A[p * n:(p + 1) * n] = obs.to(torch.bfloat16)
+        B[p * m:(p + 1) * m] = bmap.to(torch.bfloat16)
+    a_off = np.arange(n_pairs + 1, dtype=np.int64) * n
+    b_off = np.arange(n_pairs + 1, dtype=np.int64) * m
+    return A.view(torch.int16), B.view(torch.int16), a_off, b_off
+
+
+def pooled_embeddings(n: int, cfg: SceneConfig = SceneConfig(), dim: int = 64, tokens: int = 16,
+                      noise: float = 0.02, seed: int = 0, device="cuda") -> torch.Tensor:
+    """Pooled unit retrieval vectors of a keyframe run (backend.py:216-226:
+    sqrt(2) cos(W f(pose) + b) + noise tokens; database.py:78-80 pooling)."""
+    Rw, tw = trajectory(n, cfg, seed)
+    rng = np.random.default_rng([seed, 404])
+    Wm = rng.normal(size=(dim, 6))
+    b = rng.uniform(0.0, 2.0 * math.pi, size=dim)
+    feats = np.concatenate([tw / 2.0, Rw[:, :, 2]], axis=1)  # position / 2 m, viewing direction
+    base = math.sqrt(2.0) * np.cos(feats @ Wm.T + b)
+    tok = base[:, None, :] + noise * rng.normal(size=(n, tokens, dim))
+    pooled = tok.mean(axis=1)
+    pooled /= np.linalg.norm(pooled, axis=1, keepdims=True)
+    return torch.as_tensor(pooled, device=device)

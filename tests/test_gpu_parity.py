@@ -1,0 +1,331 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.  Tolerances (north star): matches, loop
+candidates, voxel keys and inlier masks bit-exact; Sim(3) within 1e-5
+relative; fused coordinates within 1e-4 m."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fuse as ofuse
+from oracle import ref_numpy as ref
+from tests.conftest import mapping_submaps
+
+pytestmark = pytest.mark.gpu
+
+STATUS = {"ok": None, "TooFewCorrespondences": "TooFewCorrespondences", "ValueError": "ValueError",
+          "AllZeroConfidence": "AllZeroConfidence", "DegenerateConfiguration": "DegenerateConfiguration"}
+
+SIM3_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2510_02080_b200 import _lib
+    _lib.lib()
+
+
+def _assert_sim3(s, q, t, s_ref, q_ref, t_ref, rtol=SIM3_RTOL, scale_of_t=1.0):
+    assert abs(s - s_ref) <= rtol * abs(s_ref), (s, s_ref)
+    np.testing.assert_allclose(ref.canonical_quat(q), ref.canonical_quat(q_ref), atol=rtol)
+    np.testing.assert_allclose(t, t_ref, atol=rtol * max(1.0, scale_of_t, float(np.abs(t_ref).max())))
+
+
+# --------------------------------------------------------------------------
+# K2+K3 explicit Umeyama (registration.py KATs through the drop-in API)
+
+def test_registration_golden_cases(golden):
+    from paper_2510_02080_b200 import registration as R
+    g = golden("registration")
+    for i in range(int(g["n_cases"])):
+        w = g[f"c{i}_w"] if bool(g[f"c{i}_hasw"]) else None
+        st = str(g[f"c{i}_status"])
+        if st != "ok":
+            with pytest.raises(Exception) as ei:
+                R.align_point_sets(g[f"c{i}_p"], g[f"c{i}_q"], w, bool(g[f"c{i}_withscale"]))
+            assert type(ei.value).__name__ == STATUS[st], (i, ei.value)
+            continue
+        tr, rms = R.align_point_sets(g[f"c{i}_p"], g[f"c{i}_q"], w, bool(g[f"c{i}_withscale"]))
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, float(g[f"c{i}_s"]), g[f"c{i}_quat"], g[f"c{i}_t"],
+                     rtol=1e-9)
+        assert abs(rms - float(g[f"c{i}_rms"])) <= 1e-9 * max(1.0, float(g[f"c{i}_rms"])), (i, rms)
+
+
+def test_registration_known_answers():
+    """pkg/tests/test_registration.py:34-154 properties, on the GPU path."""
+    from paper_2510_02080_b200 import registration as R
+    rng = np.random.default_rng(20)
+    q0 = ref.normalize_quat(rng.normal(size=4))
+    p = rng.normal(size=(10, 3))
+    q = ref.sim3_apply(1.7, q0, np.array([0.3, -1.0, 2.0]), p)
+    tr, rms = R.align_point_sets(p, q)
+    assert abs(tr.scale - 1.7) < 1e-10 and rms < 1e-12
+    np.testing.assert_allclose(ref.canonical_quat(tr.rotation.q), ref.canonical_quat(q0), atol=1e-10)
+    # identity
+    tr, rms = R.align_point_sets(p, p.copy())
+    assert abs(tr.scale - 1.0) < 1e-12 and rms < 1e-13
+    # zero-weight outlier: bit-identical (:52-71)
+    rng = np.random.default_rng(22)
+    p = rng.normal(size=(50, 3))
+    q = ref.sim3_apply(0.8, q0, np.ones(3), p) + rng.normal(size=(50, 3)) * 0.01
+    a, ra = R.align_point_sets(p, q, np.ones(50))
+    b, rb = R.align_point_sets(np.concatenate([p, [[100.0, -100.0, 100.0]]]),
+                               np.concatenate([q, [[-100.0, 100.0, -100.0]]]), np.concatenate([np.ones(50), [0.0]]))
+    assert a.scale == b.scale and ra == rb
+    np.testing.assert_array_equal(a.translation, b.translation)
+    np.testing.assert_array_equal(a.rotation.q, b.rotation.q)
+    # weight scaling invariance (:119-130)
+    w = rng.uniform(0.0, 1.0, size=50)
+    a, ra = R.align_point_sets(p, q, w)
+    b, rb = R.align_point_sets(p, q, w * 137.5)
+    assert abs(a.scale - b.scale) < 1e-12 and abs(ra - rb) < 1e-12
+    # reflection guard on near-planar sets (:133-142)
+    rng = np.random.default_rng(26)
+    for _ in range(50):
+        n = int(rng.integers(4, 20))
+        p = rng.normal(size=(n, 3))
+        p[:, 2] *= 1e-8
+        q = rng.normal(size=(n, 3))
+        q[:, 2] *= 1e-8
+        tr, _ = R.align_point_sets(p, q)
+        assert np.linalg.det(ref.quat_to_matrix(tr.rotation.q)) > 0.999999
+    # minimizer property spot-check vs the oracle (:88-104)
+    rng = np.random.default_rng(23)
+    probs = []
+    for _ in range(64):
+        n = int(rng.integers(4, 30))
+        p = rng.normal(size=(n, 3))
+        w = rng.uniform(0.1, 2.0, size=n)
+        q = ref.sim3_apply(float(np.exp(rng.uniform(-1, 1))), ref.normalize_quat(rng.normal(size=4)),
+                           rng.normal(size=3), p) + rng.normal(size=(n, 3)) * 0.05
+        probs.append((p, q, w))
+    out = R.align_point_sets_batched(probs)
+    for (p, q, w), (tr, rms, e) in zip(probs, out):
+        assert e is None
+        s, qq, t, r, st = ref.align_point_sets(p, q, w)
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, s, qq, t, rtol=1e-9)
+        assert abs(rms - r) < 1e-12
+
+
+def test_registration_large_offset_float64():
+    """Cancellation guard: 200k correspondences 100 m from the origin."""
+    from paper_2510_02080_b200 import registration as R
+    rng = np.random.default_rng(7)
+    p = rng.normal(size=(200_000, 3)) + 100.0
+    q0 = ref.normalize_quat(rng.normal(size=4))
+    q = ref.sim3_apply(1.1, q0, np.array([5.0, -3.0, 1.0]), p) + rng.normal(size=p.shape) * 0.01
+    w = rng.uniform(0.05, 1.0, size=len(p))
+    tr, rms = R.align_point_sets(p, q, w)
+    s, qq, t, r, _ = ref.align_point_sets(p, q, w)
+    _assert_sim3(tr.scale, tr.rotation.q, tr.translation, s, qq, t, rtol=1e-9, scale_of_t=100)
+    assert abs(rms - r) < 1e-9
+
+
+# --------------------------------------------------------------------------
+# K1 inverse projection (bit-exact)
+
+def test_inverse_project_bit_exact(golden):
+    from paper_2510_02080_b200.backend import inverse_project_device
+    g = golden("mapping")
+    sms, _ = mapping_submaps(g)
+    sm = sms[0]
+    poses8 = np.concatenate([np.ones((len(sm["frame_ids"]), 1)), sm["pose_q"], sm["pose_t"]], axis=1)
+    pts, cf, fid, pix = inverse_project_device(torch.as_tensor(sm["depth"], device="cuda"),
+                                               torch.as_tensor(sm["conf"], device="cuda"), sm["K"], poses8,
+                                               sm["frame_ids"])
+    np.testing.assert_array_equal(pts.cpu().numpy(), g["ip_points"])
+    np.testing.assert_array_equal(cf.cpu().numpy(), g["ip_conf"])
+    np.testing.assert_array_equal(fid.cpu().numpy(), g["ip_fids"])
+    np.testing.assert_array_equal(pix.cpu().numpy(), g["ip_pixels"])
+
+
+# --------------------------------------------------------------------------
+# K2+K3 pixel-identity registration edges
+
+def _dense_mapping(g):
+    from paper_2510_02080_b200 import mapping
+    n = int(g["n_submaps"])
+    H, W = g["sm0_depth"].shape[1:]
+    dm = mapping.DenseMapping(H, W, g["sm0_K"])
+    sms = []
+    for j in range(n):
+        poses8 = np.concatenate([np.ones((len(g[f"sm{j}_frame_ids"]), 1)), g[f"sm{j}_pose_q"],
+                                 g[f"sm{j}_pose_t"]], axis=1)
+        sms.append(dm.add_submap(g[f"sm{j}_frame_ids"], g[f"sm{j}_depth"], g[f"sm{j}_conf"], list(poses8)))
+    return dm, sms
+
+
+def test_registration_edges_vs_golden(golden):
+    from paper_2510_02080_b200 import mapping
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    pairs = [(sms[j], sms[j - 1]) for j in range(1, len(sms))]
+    res, km = mapping.register_edges(dm.pool, pairs, with_keep_masks=True)
+    km = km.cpu().numpy()
+    gs, _ = mapping_submaps(g)
+    for j, r in zip(range(1, len(sms)), res):
+        assert r.status == 0
+        assert r.count == int(g[f"e{j}_count"])
+        # inlier mask bit-exact: dense mask restricted to both-valid pixels
+        sh = [i for i, kf in enumerate(gs[j]["frame_ids"]) if kf in list(gs[j - 1]["frame_ids"])][0]
+        fb = list(gs[j - 1]["frame_ids"]).index(gs[j]["frame_ids"][sh])
+        both = (gs[j]["depth"][sh] > 0) & (gs[j - 1]["depth"][fb] > 0)
+        np.testing.assert_array_equal(km[j - 1][both].astype(bool), g[f"e{j}_keep"])
+        tr = r.transform
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, float(g[f"e{j}_s"]), g[f"e{j}_quat"],
+                     g[f"e{j}_t"], rtol=1e-9)
+        assert abs(r.rms - float(g[f"e{j}_rms"])) < 1e-7
+
+
+def test_register_chain_global_poses(golden):
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    dm.register_chain(sms)
+    for j in range(len(sms)):
+        gp = dm.submaps[j].global_pose
+        _assert_sim3(gp.scale, gp.rotation.q, gp.translation, float(g[f"sm{j}_gs"]), g[f"sm{j}_gq"], g[f"sm{j}_gt"],
+                     rtol=1e-8)
+    # sequential registration gives the same poses
+    dm2, sms2 = _dense_mapping(g)
+    for sm in sms2:
+        dm2.register_submap(sm)
+    for j in range(len(sms)):
+        a, b = dm.submaps[j].global_pose, dm2.submaps[j].global_pose
+        assert a.scale == b.scale
+        np.testing.assert_array_equal(a.translation, b.translation)
+
+
+# --------------------------------------------------------------------------
+# Stage (c): transform + concatenation (bit-exact) and voxel fusion
+
+def test_fused_cloud_concatenation_bit_exact(golden):
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    dm.register_chain(sms)
+    # use the reference's global poses so the check isolates the transform
+    from paper_2510_02080_b200.types import vec_to_sim3
+    for j, sm in enumerate(sms):
+        sm.global_pose = vec_to_sim3(np.concatenate([[float(g[f"sm{j}_gs"])], g[f"sm{j}_gq"], g[f"sm{j}_gt"]]))
+    pts, conf = dm.fused_cloud()
+    np.testing.assert_array_equal(pts, g["fused_points"])
+    np.testing.assert_array_equal(conf, g["fused_conf"])
+
+
+def test_voxel_fusion_vs_oracle(golden):
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    dm.register_chain(sms)
+    for cell in (0.02, 0.05, 0.013):
+        out = dm.fused_cloud(voxel=cell)
+        globs = [(sm.global_pose.scale, np.asarray(sm.global_pose.rotation.q), np.asarray(sm.global_pose.translation))
+                 for sm in sms]
+        gs, _ = mapping_submaps(g)
+        o = ofuse.fuse_submaps(gs, globs, cell)
+        np.testing.assert_array_equal(out["keys"], o["keys"])
+        np.testing.assert_array_equal(out["count"], o["count"])
+        np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-5)
+        assert np.max(np.abs(out["centroid"] - o["centroid"])) < 1e-4
+        assert out["stats"]["n_points_in"] == o["n_in"]
+
+
+def test_voxel_points_api_and_extreme_coordinates():
+    """insert_points path, out-of-range keys flagged, keys exact far from the origin."""
+    from paper_2510_02080_b200 import mapping
+    rng = np.random.default_rng(3)
+    p = rng.normal(size=(100_000, 3)) * 3.0
+    p[:10] = 1e5  # 5,000,000 cells at 2 cm: outside the 21-bit key range
+    conf = rng.uniform(0.0, 1.0, size=len(p))
+    conf[10:20] = 0.0
+    sim = np.concatenate([[1.3], ref.normalize_quat(rng.normal(size=4)), [2000.0, -1500.0, 30.0]])
+    vm = mapping.VoxelMap(0.02, 1 << 18)
+    vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"), sim)
+    st = vm.stats()
+    k, c, w, n = (x.cpu().numpy() for x in vm.extract())
+    x = ref.sim3_apply(sim[0], sim[1:5], sim[5:], p)
+    o = ofuse.fuse_points(x, conf, 0.02)
+    assert st["n_out_of_range"] == o["n_out_of_range"] == 10
+    np.testing.assert_array_equal(k, o["keys"])
+    np.testing.assert_array_equal(n, o["count"])
+    assert np.max(np.abs(c - o["centroid"])) < 1e-3  # float32 output at 2 km
+
+
+# --------------------------------------------------------------------------
+# K5 matcher (bit-exact matches)
+
+def test_match_golden_cases(golden):
+    from paper_2510_02080_b200 import tracking
+    g = golden("match")
+    for i in range(int(g["n_cases"])):
+        got = np.array(tracking.match_descriptors(g[f"c{i}_a"], g[f"c{i}_b"], 0.8), np.int64).reshape(-1, 2)
+        np.testing.assert_array_equal(got, g[f"c{i}_matches"], err_msg=f"case {i}")
+
+
+@pytest.mark.parametrize("n,m,d,sigma", [(1024, 1024, 256, 0.10), (2048, 1500, 256, 0.05), (777, 1900, 64, 0.10),
+                                         (300, 4096, 256, 0.10)])
+def test_match_random_vs_oracle(n, m, d, sigma):
+    from paper_2510_02080_b200 import synth, tracking
+    A, B, ao, bo = synth.make_descriptor_pairs(1, n, m, d, sigma, seed=n + m)
+    a = A.view(torch.bfloat16).double().cpu().numpy()
+    b = B.view(torch.bfloat16).double().cpu().numpy()
+    exp = ref.match_descriptors_vec(a, b, 0.8)
+    got = np.array(tracking.match_descriptors(a, b, 0.8), np.int64).reshape(-1, 2)
+    np.testing.assert_array_equal(got, exp)
+
+
+def test_match_batched_pairs_vs_oracle():
+    from paper_2510_02080_b200 import tracking
+    rng = np.random.default_rng(5)
+    pairs = []
+    for k in range(9):
+        n, m = int(rng.integers(0, 300)), int(rng.integers(1, 300))
+        a = rng.normal(size=(n, 96))
+        b = np.concatenate([a[: min(n, m // 2)] + 0.08 * rng.normal(size=(min(n, m // 2), 96)),
+                            rng.normal(size=(m - min(n, m // 2), 96))])
+        pairs.append((a, b))
+    got = tracking.match_batched(pairs, 0.8)
+    for (a, b), g in zip(pairs, got):
+        np.testing.assert_array_equal(g, ref.match_descriptors_vec(a, b, 0.8))
+
+
+# --------------------------------------------------------------------------
+# K6 retrieval (admitted pairs bit-exact and in order)
+
+def test_retrieval_golden(golden):
+    from paper_2510_02080_b200 import loops
+    g = golden("retrieval")
+    for i in range(int(g["n_cases"])):
+        tg, tl = g[f"c{i}_tau"]
+        pooled = torch.as_tensor(g[f"c{i}_pooled"], device="cuda")
+        mat = loops.SimilarityMatrix()
+        for c in range(2):
+            cp, cs, qp, qs, ep, es = loops.retrieval_device(pooled, int(g[f"c{i}_stride"]), int(g[f"c{i}_excl"]),
+                                                            tg, tl)
+            kfs = g[f"c{i}_kf"]
+            loops._populate(mat, kfs, cp, cs)
+            loops._populate(mat, kfs, ep, es)
+            adm = loops.admit(mat, kfs, qp, qs)
+            pairs = np.array([p for p, _ in adm], np.int64).reshape(-1, 2)
+            np.testing.assert_array_equal(pairs, g[f"c{i}_call{c}_pairs"])
+            np.testing.assert_allclose([s for _, s in adm], g[f"c{i}_call{c}_scores"], rtol=0, atol=1e-15)
+        keys = np.array(sorted(k for k, _ in mat.items()), np.int64).reshape(-1, 2)
+        np.testing.assert_array_equal(keys, g[f"c{i}_matrix_keys"])
+
+
+def test_retrieval_sharded_equals_single():
+    from paper_2510_02080_b200 import loops, synth
+    pooled = synth.pooled_embeddings(1500, seed=3)
+    full = loops.retrieval_device(pooled, 5, 15, 0.93, 0.96)
+    Kc = 300
+    parts = [loops.retrieval_device(pooled, 5, 15, 0.93, 0.96, k0, k1) for k0, k1 in
+             ((0, 70), (70, 160), (160, 240), (240, Kc))]
+    for idx in range(6):
+        np.testing.assert_array_equal(np.concatenate([p[idx] for p in parts]), full[idx])
+    # vs oracle
+    st = ref.SimilarityState()
+    exp = ref.update_similarity(st, np.arange(1500), pooled.cpu().numpy(), 5, 15, 0.93, 0.96)
+    mat = loops.SimilarityMatrix()
+    adm = loops.admit(mat, np.arange(1500), full[2], full[3])
+    assert [p for p, _ in adm] == [p for p, _ in exp]
+    assert len(exp) > 0
