@@ -121,24 +121,9 @@ class Step:
         self.torch, self.mapping, self.tracking = torch, mapping, tracking
         self.dm, self.sms, self.desc, self.cell = dm, sms, desc, cell
         self.slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
-        # edges of the chain registration (partners by shared keyframes, mapping.py:164-169)
-        pairs = []
-        kf_owner = {}
-        for sm in sms:
-            pids = {}
-            for kf in sm.keyframe_ids:
-                for sid in kf_owner.get(kf, ()):
-                    pids[sid] = None
-            pairs.extend((sm, sms[s]) for s in pids)
-            for kf in sm.keyframe_ids:
-                kf_owner.setdefault(kf, []).append(sm.id)
-        self.pairs = pairs
-        seg, eoff = [], [0]
-        for a, b in pairs:
-            seg.extend(mapping.edge_segments(a, b))
-            eoff.append(len(seg))
-        self.seg = torch.as_tensor(np.asarray(seg, np.int32).reshape(-1, 2), device="cuda")
-        self.eoff = torch.as_tensor(np.asarray(eoff, np.int32), device="cuda")
+        self.plan = mapping.ChainPlan(sms)
+        self.pairs = self.plan.pairs
+        self.seg = self.plan.seg
         self.vmap = None
         self.ev = {}
         self.n_points = 0
@@ -156,31 +141,10 @@ class Step:
         A, B, ao, bo = self.desc
         self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)
         ev["t_match"] = self._event()
-        sim3, rms, count, npairs, status = self.mapping.register_edges_device(self.dm.pool, self.seg, self.eoff,
-                                                                              len(self.pairs))
-        ev["t_reg"] = self._event()
-        # chain global poses on the host (register_submap semantics, mapping.py:200-204)
-        host = torch.cat([sim3.reshape(-1), count.double(), status.double()]).cpu().numpy()
-        B_ = len(self.pairs)
-        s3 = host[: 8 * B_].reshape(B_, 8)
-        cnt = host[8 * B_: 9 * B_]
-        st = host[9 * B_:]
-        from paper_2510_02080_b200.types import Sim3Transform, sim3_to_vec, vec_to_sim3
-        glob = {self.sms[0].id: Sim3Transform.identity()}
-        best = {}
-        for e, (a, b) in enumerate(self.pairs):
-            if st[e] != 0:
-                continue
-            if a.id not in best or cnt[e] > best[a.id][0]:
-                best[a.id] = (cnt[e], b.id, e)
-        G = np.zeros((len(self.sms), 8))
-        G[0] = sim3_to_vec(glob[self.sms[0].id])
-        for sm in self.sms[1:]:
-            _, pid, e = best[sm.id]
-            glob[sm.id] = glob[pid].compose(vec_to_sim3(s3[e]))
-            G[sm.id] = sim3_to_vec(glob[sm.id])
-        per_slot = np.repeat(G, [len(sm.slots) for sm in self.sms], axis=0)
-        self.dm.pool.globals[: len(per_slot)].copy_(torch.as_tensor(per_slot), non_blocking=False)
+        # registration of all edges (one launch) + device pose chain (one launch)
+        out = self.plan.run(self.dm.pool)
+        ev["t_reg"] = self._event()  # both launches: stage "reg" = registration + chain
+        self.edge_status, self.sub_status = out[4], out[6]
         ev["t_chain"] = self._event()
         if self.vmap is None:
             self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell)

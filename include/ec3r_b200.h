@@ -112,6 +112,21 @@ EC3R_API int ec3r_register_edges(const float* depth_pool, const float* conf_pool
                         int64_t* out_npairs, int32_t* out_status, uint8_t* keep_masks,
                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* Pose chaining of register_submap (mapping.py:200-204) on the device:
+ * submaps 0..n_sub-1 in registration order; submap j's edges are
+ * [sub_edge_off[j], sub_edge_off[j+1]) with edge_partner[e] < j the partner
+ * submap index.  The OK edge with the largest count (first on ties) sets
+ * sub_globals[j] = sub_globals[partner] o edge_sim3[e]; submaps with an
+ * empty edge range keep the caller's sub_globals entry (gauge / already
+ * registered); sub_status[j] = EC3R_ST_SKIP when no edge survived
+ * (NoSharedKeyframes).  slot_globals[s] for s in
+ * [sub_slot_off[j], sub_slot_off[j+1]) receives sub_globals[j]. */
+EC3R_API int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_count,
+                              const int32_t* edge_status, const int32_t* edge_partner,
+                              const int32_t* sub_edge_off, int n_sub, const int32_t* sub_slot_off,
+                              double* sub_globals, double* slot_globals, int32_t* sub_status,
+                              void* stream);
+
 /* ---------------------------------------------------------------------
  * K2+K3  batched weighted Umeyama on explicit correspondences
  * replaces align_point_sets (registration.py:38-102) / weighted_umeyama

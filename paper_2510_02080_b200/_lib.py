@@ -31,6 +31,7 @@ _PROTOS = {
     "ec3r_register_edges_workspace": (_SZ, [_I]),
     "ec3r_register_edges": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _D, _I, _I, _P, _P, _P, _P, _P, _P,
                                  _P, _SZ, _P]),
+    "ec3r_chain_poses": (_I, [_P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P]),
     "ec3r_umeyama_workspace": (_SZ, [_I]),
     "ec3r_umeyama_batched": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _SZ, _P]),
     "ec3r_vhash_create": (_I, [C.POINTER(_P), _I64, _D, _P]),

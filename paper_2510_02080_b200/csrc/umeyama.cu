@@ -485,9 +485,67 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     cl.sync();
 }
 
+// ---------------------------------------------------------------------------
+// Pose chaining of register_submap (mapping.py:200-204): the strongest edge
+// (max count, first on ties — Python max()) sets
+// global_j = global_partner o T (sim3_compose, liegroups.py:275-281).  One
+// thread; the chain is sequential and tiny, but keeping it on the device
+// removes the host round trip between registration and fusion.
+__device__ void sim3_compose_dev(const double* a, const double* b, double* o) {
+    const double aw = a[1], ax = a[2], ay = a[3], az = a[4];
+    const double bw = b[1], bx = b[2], by = b[3], bz = b[4];
+    double q[4] = {aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                   aw * by - ax * bz + ay * bw + az * bx, aw * bz + ax * by - ay * bx + az * bw};
+    const double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double r[3];
+    const double tb[3] = {b[5], b[6], b[7]};
+    quat_rotate_exact(a + 1, tb, r);
+    o[0] = a[0] * b[0];
+    for (int k = 0; k < 4; ++k) o[1 + k] = q[k] / n;
+    for (int k = 0; k < 3; ++k) o[5 + k] = a[0] * r[k] + a[5 + k];
+}
+
+__global__ void chain_poses_kernel(const double* __restrict__ esim, const int64_t* __restrict__ ecount,
+                                   const int32_t* __restrict__ estatus, const int32_t* __restrict__ epartner,
+                                   const int32_t* __restrict__ sub_edge_off, int n_sub,
+                                   const int32_t* __restrict__ sub_slot_off, double* __restrict__ sub_globals,
+                                   double* __restrict__ slot_globals, int32_t* __restrict__ sub_status) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        for (int j = 0; j < n_sub; ++j) {
+            const int e0 = sub_edge_off[j], e1 = sub_edge_off[j + 1];
+            int best = -1;
+            for (int e = e0; e < e1; ++e)
+                if (estatus[e] == EC3R_ST_OK && (best < 0 || ecount[e] > ecount[best])) best = e;
+            int st = EC3R_ST_OK;
+            if (e1 > e0) {
+                if (best < 0) st = EC3R_ST_SKIP;  // NoSharedKeyframes
+                else sim3_compose_dev(sub_globals + 8 * epartner[best], esim + 8 * best, sub_globals + 8 * j);
+            }
+            if (sub_status) sub_status[j] = st;
+        }
+    }
+    __syncthreads();
+    for (int j = blockIdx.x; j < n_sub; j += gridDim.x)
+        for (int s = sub_slot_off[j] + threadIdx.x; s < sub_slot_off[j + 1]; s += blockDim.x)
+            for (int k = 0; k < 8; ++k) slot_globals[8 * s + k] = sub_globals[8 * j + k];
+}
+
 }  // namespace ec3r
 
 using namespace ec3r;
+
+extern "C" int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_count, const int32_t* edge_status,
+                                const int32_t* edge_partner, const int32_t* sub_edge_off, int n_sub,
+                                const int32_t* sub_slot_off, double* sub_globals, double* slot_globals,
+                                int32_t* sub_status, void* stream) {
+    if (n_sub < 0 || !sub_edge_off || !sub_globals) return EC3R_EARG;
+    if (n_sub == 0) return EC3R_OK;
+    chain_poses_kernel<<<1, 256, 0, as_stream(stream)>>>(edge_sim3, edge_count, edge_status, edge_partner,
+                                                         sub_edge_off, n_sub, sub_slot_off, sub_globals,
+                                                         slot_globals, sub_status);
+    EC3R_CHECK_LAUNCH("chain_poses_kernel");
+    return EC3R_OK;
+}
 
 extern "C" size_t ec3r_umeyama_workspace(int) { return 0; }
 

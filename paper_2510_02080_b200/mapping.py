@@ -128,6 +128,65 @@ def register_edges(pool: FramePool, pairs: Sequence, config: MappingConfig = Map
     return out
 
 
+class ChainPlan:
+    """Device-resident plan for registering a run of submaps in order: the
+    edges of every submap to its earlier partners (partners = submaps sharing
+    a keyframe, mapping.py:164-169), their pixel segments, and the offsets
+    the device pose chain (ec3r_chain_poses) walks."""
+
+    def __init__(self, sms: Sequence[DenseSubmap], device="cuda"):
+        self.sms = list(sms)
+        index = {sm.id: i for i, sm in enumerate(self.sms)}
+        owners: dict = {}
+        pairs, partner, sub_edge_off = [], [], [0]
+        for sm in self.sms:
+            pids = {}
+            for kf in sm.keyframe_ids:
+                for sid in owners.get(kf, ()):
+                    pids[sid] = None
+            for sid in pids:
+                pairs.append((sm, self.sms[index[sid]]))
+                partner.append(index[sid])
+            sub_edge_off.append(len(pairs))
+            for kf in sm.keyframe_ids:
+                owners.setdefault(kf, []).append(sm.id)
+        self.pairs = pairs
+        seg, eoff = [], [0]
+        for a, b in pairs:
+            seg.extend(edge_segments(a, b))
+            eoff.append(len(seg))
+        t = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=device)  # noqa: E731
+        self.seg = t(np.asarray(seg, np.int32).reshape(-1, 2))
+        self.eoff = t(eoff)
+        self.partner = t(partner if partner else [0])
+        self.sub_edge_off = t(sub_edge_off)
+        self.sub_slot_off = t(np.concatenate([[0], np.cumsum([len(sm.slots) for sm in self.sms])]))
+        self.slot0 = int(self.sms[0].slots[0]) if self.sms else 0
+        self.n_edges = len(pairs)
+
+    def run(self, pool: FramePool, config: MappingConfig = MappingConfig(), sub_globals: Optional[torch.Tensor] = None,
+            stream=None):
+        """Registration of every edge (one launch) + device pose chain (one
+        launch) writing the pool's slot globals.  No host synchronisation.
+        Returns (edge sim3, rms, count, npairs, status, sub_globals, sub_status)."""
+        sim3, rms, count, npairs, status = register_edges_device(pool, self.seg, self.eoff, self.n_edges,
+                                                                 config.confidence_floor_frac,
+                                                                 config.min_correspondences, True, None, stream)
+        S = len(self.sms)
+        if sub_globals is None:
+            sub_globals = torch.zeros((S, 8), dtype=torch.float64, device=pool.device)
+            sub_globals[:, 0] = 1.0
+            sub_globals[:, 1] = 1.0
+        sub_status = torch.empty(S, dtype=torch.int32, device=pool.device)
+        slot_globals = pool.globals[self.slot0:]
+        _lib.check(_lib.lib().ec3r_chain_poses(_lib.ptr(sim3), _lib.ptr(count), _lib.ptr(status),
+                                               _lib.ptr(self.partner), _lib.ptr(self.sub_edge_off), S,
+                                               _lib.ptr(self.sub_slot_off), _lib.ptr(sub_globals),
+                                               _lib.ptr(slot_globals), _lib.ptr(sub_status),
+                                               _lib.stream_ptr(stream)), "ec3r_chain_poses")
+        return sim3, rms, count, npairs, status, sub_globals, sub_status
+
+
 class VoxelMap:
     """Owner of one ec3r_vhash handle (K4)."""
 

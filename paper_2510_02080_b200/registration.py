@@ -106,12 +106,13 @@ def align_point_sets_batched(problems, with_scale: bool = True):
         qs.append(q.reshape(-1, 3))
         ws.append(np.ones(len(p)) if w is None else np.asarray(w, dtype=float).reshape(-1))
         offs.append(offs[-1] + len(p))
-    P = _dev(np.concatenate(ps) if ps else np.zeros((0, 3)))
-    Q = _dev(np.concatenate(qs) if qs else np.zeros((0, 3)))
-    Wt = _dev(np.concatenate(ws)) if any_w else None
-    O = torch.as_tensor(np.asarray(offs, np.int64), device="cuda")
-    sim3, rms, status = align_batched_device(P, Q, Wt, O, with_scale)
-    sim3, rms, status = sim3.cpu().numpy(), rms.cpu().numpy(), status.cpu().numpy()
+    if len(bad) < len(problems):
+        P = _dev(np.concatenate(ps))
+        Q = _dev(np.concatenate(qs))
+        Wt = _dev(np.concatenate(ws)) if any_w else None
+        O = torch.as_tensor(np.asarray(offs, np.int64), device="cuda")
+        sim3, rms, status = align_batched_device(P, Q, Wt, O, with_scale)
+        sim3, rms, status = sim3.cpu().numpy(), rms.cpu().numpy(), status.cpu().numpy()
     out = []
     for i in range(len(problems)):
         if i in bad:

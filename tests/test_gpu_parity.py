@@ -197,6 +197,26 @@ def test_register_chain_global_poses(golden):
         np.testing.assert_array_equal(a.translation, b.translation)
 
 
+def test_device_chain_matches_host_registration(golden):
+    from paper_2510_02080_b200 import mapping
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    plan = mapping.ChainPlan(sms)
+    out = plan.run(dm.pool)
+    sub_g = out[5].cpu().numpy()
+    assert (out[6].cpu().numpy() == 0).all()
+    dm2, sms2 = _dense_mapping(g)
+    dm2.register_chain(sms2)
+    for j, sm in enumerate(sms2):
+        gp = sm.global_pose
+        assert abs(sub_g[j, 0] - gp.scale) < 1e-12
+        np.testing.assert_allclose(ref.canonical_quat(sub_g[j, 1:5]), ref.canonical_quat(gp.rotation.q), atol=1e-12)
+        np.testing.assert_allclose(sub_g[j, 5:], gp.translation, atol=1e-12)
+    slot_g = dm.pool.globals[: dm.pool.n].cpu().numpy()
+    for j, sm in enumerate(sms):
+        np.testing.assert_array_equal(slot_g[sm.slots], np.repeat(sub_g[j:j + 1], len(sm.slots), axis=0))
+
+
 # --------------------------------------------------------------------------
 # Stage (c): transform + concatenation (bit-exact) and voxel fusion
 
