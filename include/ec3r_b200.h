@@ -202,14 +202,16 @@ EC3R_API int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, const
  * accumulators); every decision is certified against an error bound and
  * re-scored in float64 from the exact rows (A_x/B_x, dtype exact_dtype:
  * 0 = the bf16 rows are exact, 1 = float32, 2 = float64), so the result is
- * identical to the float64 reference.  Output: match_b (sum N_p) int32 =
+ * identical to the float64 reference.  norm_bound = max|a| * max|b| over the
+ * rows (<= 0: computed on the device) scales the error bound.
+ * Output: match_b (sum N_p) int32 =
  * matched B row within the pair or -1; n_match (n_pairs) int32.
  * ------------------------------------------------------------------- */
 EC3R_API size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_pairs);
 EC3R_API int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
                        int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h,
-                       int n_pairs, int D, double ratio, int32_t* match_b, int32_t* n_match,
-                       void* workspace, size_t workspace_bytes, void* stream);
+                       int n_pairs, int D, double ratio, double norm_bound, int32_t* match_b,
+                       int32_t* n_match, void* workspace, size_t workspace_bytes, void* stream);
 /* Diagnostics of the last ec3r_match_batched on this workspace (device
  * counters copied to host; synchronizes): rows / columns that needed the
  * float64 full rescan. */

@@ -22,10 +22,10 @@ void set_last_error(const char* where, cudaError_t e) {
 void set_last_error_msg(const char* msg) { snprintf(g_last_error, sizeof(g_last_error), "%s", msg); }
 
 // tensor-core approximate pass (match_tc.cu)
-int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, const int64_t* b_off_d,
-                 const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
-                 MatchRowState* rs, int32_t* col_best, int32_t* flag_rows, int32_t* flag_cols, int64_t* counters,
-                 void* tc_ws, size_t tc_ws_bytes, cudaStream_t st);
+int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x, const int64_t* a_off_d,
+                 const int64_t* b_off_d, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
+                 int exact_dtype, double norm_bound, MatchRowState* rs, int32_t* col_best, int32_t* flag_rows,
+                 int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes, cudaStream_t st);
 size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs);
 
 }  // namespace ec3r
@@ -49,7 +49,7 @@ extern "C" size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_p
 
 extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
                                   int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
-                                  double ratio, int32_t* match_b, int32_t* n_match, void* workspace,
+                                  double ratio, double norm_bound, int32_t* match_b, int32_t* n_match, void* workspace,
                                   size_t workspace_bytes, void* stream) {
     if (n_pairs < 0 || D <= 0 || !a_off_h || !b_off_h || exact_dtype < 0 || exact_dtype > 2) return EC3R_EARG;
     if (n_pairs == 0) return EC3R_OK;
@@ -74,8 +74,8 @@ extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const vo
     int rc;
     if (A != nullptr && B != nullptr && total_a > 0 && total_b > 0) {
         // tensor-core pass: certifies most rows / columns and lists the rest
-        rc = match_tc_run(A, B, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, rs, col_best, flag_rows,
-                          flag_cols, counters, tc_ws, tc_bytes, st);
+        rc = match_tc_run(A, B, A_x, B_x, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound, rs,
+                          col_best, flag_rows, flag_cols, counters, tc_ws, tc_bytes, st);
         if (rc) return rc;
         rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
                                   flag_cols, counters + 1, 0, rs, col_best, st);

@@ -36,7 +36,7 @@ def to_bf16_bits(x: torch.Tensor) -> torch.Tensor:
 
 
 def match_batched_device(A_bits: torch.Tensor, B_bits: torch.Tensor, A_x, B_x, exact_dtype: int,
-                         a_off: np.ndarray, b_off: np.ndarray, ratio: float, stream=None):
+                         a_off: np.ndarray, b_off: np.ndarray, ratio: float, norm_bound: float = 0.0, stream=None):
     """One launch sequence of ec3r_match_batched.
 
     A_bits/B_bits: (rows, D) int16 bf16 bits (D % 16 == 0); A_x/B_x: exact
@@ -56,9 +56,25 @@ def match_batched_device(A_bits: torch.Tensor, B_bits: torch.Tensor, A_x, B_x, e
     ws = _lib.workspace(ws_bytes, dev, "match")
     _lib.check(L.ec3r_match_batched(_lib.ptr(A_bits), _lib.ptr(B_bits), _lib.ptr(A_x), _lib.ptr(B_x),
                                     int(exact_dtype), a_off.ctypes.data, b_off.ctypes.data, P, D, float(ratio),
-                                    _lib.ptr(match_b), _lib.ptr(n_match), _lib.ptr(ws), ws.numel(),
+                                    float(norm_bound), _lib.ptr(match_b), _lib.ptr(n_match), _lib.ptr(ws), ws.numel(),
                                     _lib.stream_ptr(stream)), "ec3r_match_batched")
+    _last.update(ws=ws, ta=ta, tb=tb, P=P)
     return match_b[:ta], n_match[:P]
+
+
+_last: dict = {}
+
+
+def last_match_stats(stream=None) -> dict:
+    """Rows / columns of the last match_batched_device call that needed the
+    float64 full re-scan (the tensor-core pass certified the rest)."""
+    import ctypes as C
+
+    L = _lib.lib()
+    r, c = C.c_int64(), C.c_int64()
+    _lib.check(L.ec3r_match_stats(_lib.ptr(_last["ws"]), _last["ta"], _last["tb"], _last["P"], C.byref(r),
+                                  C.byref(c), _lib.stream_ptr(stream)), "ec3r_match_stats")
+    return {"rows_rescanned": r.value, "cols_rescanned": c.value, "rows": _last["ta"], "cols": _last["tb"]}
 
 
 def prepare_rows(descs: Sequence, D: int):
