@@ -13,6 +13,60 @@ struct MatchRowState {
     int32_t pad;
 };
 
+// 16-byte row chunks widened to float64 (rows are 16-byte aligned: D is
+// padded to a multiple of 16 elements by the host layer).
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<uint16_t> {
+    static constexpr int N = 8;
+    __device__ __forceinline__ static void load(const uint16_t* p, double (&o)[8]) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = (double)__uint_as_float(w[i] << 16);
+            o[2 * i + 1] = (double)__uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+};
+template <>
+struct Vec16<float> {
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void load(const float* p, double (&o)[4]) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+template <>
+struct Vec16<double> {
+    static constexpr int N = 2;
+    __device__ __forceinline__ static void load(const double* p, double (&o)[2]) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        o[0] = v.x; o[1] = v.y;
+    }
+};
+
+// Warp-cooperative float64 dot of two D-element rows (every lane returns
+// the total).  Products of bf16 values are exact in float64 and the sums of
+// <= 2^k such terms stay exact for descriptor-range exponents, so the result
+// equals the reference's dgemm entry.
+template <typename T>
+__device__ __forceinline__ double warp_dot16(const T* a, const T* b, int D, int lane) {
+    constexpr int N = Vec16<T>::N;
+    double s = 0.0;
+    for (int k = lane * N; k < D; k += 32 * N) {
+        double x[N], y[N];
+        Vec16<T>::load(a + k, x);
+        Vec16<T>::load(b + k, y);
+#pragma unroll
+        for (int i = 0; i < N; ++i) s = fma(x[i], y[i], s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 int match_exact_dispatch(const void* A, const void* B, int dtype, int D, const int64_t* a_off, const int64_t* b_off,
                          int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
                          const int32_t* cols, const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs,

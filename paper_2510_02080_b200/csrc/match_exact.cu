@@ -20,17 +20,6 @@
 
 namespace ec3r {
 
-template <typename T>
-__device__ __forceinline__ double ldx(const T* p, int64_t i);
-template <>
-__device__ __forceinline__ double ldx<uint16_t>(const uint16_t* p, int64_t i) {
-    return (double)__uint_as_float(((uint32_t)p[i]) << 16);
-}
-template <>
-__device__ __forceinline__ double ldx<float>(const float* p, int64_t i) { return (double)p[i]; }
-template <>
-__device__ __forceinline__ double ldx<double>(const double* p, int64_t i) { return p[i]; }
-
 __device__ __forceinline__ int find_pair(const int64_t* __restrict__ off, int n_pairs, int64_t r) {
     int lo = 0, hi = n_pairs;  // off[lo] <= r < off[hi]
     while (hi - lo > 1) {
@@ -47,49 +36,65 @@ __device__ __forceinline__ double d2_of(double sim) {
 // (d, idx) lexicographic "better": smaller d, then smaller index
 __device__ __forceinline__ bool better(double d, int i, double db, int ib) { return d < db || (d == db && i < ib); }
 
+// Four warp-cooperative float64 dots of one row x against rows y0..y0+3 of
+// Y (16-byte chunks per lane, four independent loads in flight); every lane
+// returns all four totals.  Rows past y_end contribute 0 (ignored).
+template <typename T>
+__device__ __forceinline__ void warp_dot4(const T* x, const T* Y, int64_t y0, int64_t y_end, int D, int lane,
+                                          double (&s)[4]) {
+    constexpr int N = Vec16<T>::N;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = 0.0;
+    for (int k = lane * N; k < D; k += 32 * N) {
+        double a[N];
+        Vec16<T>::load(x + k, a);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (y0 + u < y_end) {
+                double b[N];
+                Vec16<T>::load(Y + (y0 + u) * D + k, b);
+#pragma unroll
+                for (int i = 0; i < N; ++i) s[u] = fma(a[i], b[i], s[u]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+}
+
 // Exact row scan: for rows listed in `rows` (global A-row ids; or all rows
 // when rows == nullptr), best column (first index on ties), d_first and the
-// second order statistic of the row's d2 values.  One warp per row.
+// second order statistic of the row's d2 values.  One warp per row; the
+// warp walks the pair's B rows in order, so the running (best, second) is
+// warp-uniform and needs no final merge.
 template <typename T>
 __global__ void __launch_bounds__(256) mx_rows_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
                                                       const int64_t* __restrict__ a_off,
                                                       const int64_t* __restrict__ b_off, int n_pairs,
                                                       const int32_t* __restrict__ rows, const int64_t* __restrict__ n_rows_ptr,
                                                       int64_t n_rows_all, MatchRowState* __restrict__ rs) {
-    extern __shared__ double arow_all[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* arow = arow_all + (size_t)warp * D;
     const int64_t n_rows = rows ? *n_rows_ptr : n_rows_all;
     for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < n_rows;
          t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
         const int64_t r = rows ? (int64_t)rows[t] : t;
         const int p = find_pair(a_off, n_pairs, r);
         const int64_t b0 = b_off[p], b1 = b_off[p + 1];
-        __syncwarp();
-        for (int k = lane; k < D; k += 32) arow[k] = ldx<T>(A, r * D + k);
-        __syncwarp();
         double d1 = INFINITY, d2nd = INFINITY;
         int i1 = INT_MAX;
-        for (int64_t j = b0 + lane; j < b1; j += 32) {
-            double s = 0.0;
-            const T* brow = B + j * D;
-            for (int k = 0; k < D; ++k) s = fma(arow[k], ldx<T>(brow, k), s);
-            const double d = d2_of(s);
-            const int jj = (int)(j - b0);
-            if (better(d, jj, d1, i1)) { d2nd = d1; d1 = d; i1 = jj; }
-            else if (d < d2nd) d2nd = d;
-        }
+        for (int64_t j = b0; j < b1; j += 4) {
+            double s[4];
+            warp_dot4<T>(A + r * D, B, j, b1, D, lane, s);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double od1 = __shfl_xor_sync(0xffffffffu, d1, o);
-            const double od2 = __shfl_xor_sync(0xffffffffu, d2nd, o);
-            const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
-            // merge two (best, second) summaries
-            double nd1, nd2;
-            int ni1;
-            if (better(od1, oi1, d1, i1)) { nd1 = od1; ni1 = oi1; nd2 = fmin(d1, od2); }
-            else { nd1 = d1; ni1 = i1; nd2 = fmin(od1, d2nd); }
-            d1 = nd1; i1 = ni1; d2nd = nd2;
+            for (int u = 0; u < 4; ++u) {
+                if (j + u >= b1) break;
+                const double d = d2_of(s[u]);
+                const int jj = (int)(j + u - b0);
+                if (better(d, jj, d1, i1)) { d2nd = d1; d1 = d; i1 = jj; }
+                else if (d < d2nd) d2nd = d;
+            }
         }
         if (lane == 0) {
             rs[r].best = (b1 > b0) ? i1 : -1;
@@ -106,33 +111,25 @@ __global__ void __launch_bounds__(256) mx_cols_kernel(const T* __restrict__ A, c
                                                       const int64_t* __restrict__ b_off, int n_pairs,
                                                       const int32_t* __restrict__ cols, const int64_t* __restrict__ n_cols_ptr,
                                                       int64_t n_cols_all, int32_t* __restrict__ col_best) {
-    extern __shared__ double brow_all[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* brow = brow_all + (size_t)warp * D;
     const int64_t n_cols = cols ? *n_cols_ptr : n_cols_all;
     for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < n_cols;
          t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
         const int64_t c = cols ? (int64_t)cols[t] : t;
         const int p = find_pair(b_off, n_pairs, c);
         const int64_t a0 = a_off[p], a1 = a_off[p + 1];
-        __syncwarp();
-        for (int k = lane; k < D; k += 32) brow[k] = ldx<T>(B, c * D + k);
-        __syncwarp();
         double d1 = INFINITY;
         int i1 = INT_MAX;
-        for (int64_t i = a0 + lane; i < a1; i += 32) {
-            double s = 0.0;
-            const T* arow = A + i * D;
-            for (int k = 0; k < D; ++k) s = fma(ldx<T>(arow, k), brow[k], s);
-            const double d = d2_of(s);
-            const int ii = (int)(i - a0);
-            if (better(d, ii, d1, i1)) { d1 = d; i1 = ii; }
-        }
+        for (int64_t i = a0; i < a1; i += 4) {
+            double s[4];
+            warp_dot4<T>(B + c * D, A, i, a1, D, lane, s);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, d1, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, i1, o);
-            if (better(od, oi, d1, i1)) { d1 = od; i1 = oi; }
+            for (int u = 0; u < 4; ++u) {
+                if (i + u >= a1) break;
+                const double d = d2_of(s[u]);
+                const int ii = (int)(i + u - a0);
+                if (better(d, ii, d1, i1)) { d1 = d; i1 = ii; }
+            }
         }
         if (lane == 0) col_best[c] = (a1 > a0) ? i1 : -1;
     }
@@ -163,11 +160,8 @@ int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int6
                  const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all, const int32_t* cols,
                  const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs, int32_t* col_best,
                  cudaStream_t st) {
-    const size_t smem = sizeof(double) * (size_t)D * 8;
-    if (smem > 48 * 1024) {
-        EC3R_CUDA_TRY(cudaFuncSetAttribute(mx_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        EC3R_CUDA_TRY(cudaFuncSetAttribute(mx_cols_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    if (D % Vec16<T>::N != 0) return EC3R_EARG;  // rows must be 16-byte chunked
+    const size_t smem = 0;
     const unsigned grid = kNumSMs * 8;
     if (rows != nullptr || n_rows_all > 0) {
         mx_rows_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, n_pairs, rows, n_rows_ptr, n_rows_all, rs);

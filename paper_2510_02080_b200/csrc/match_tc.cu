@@ -34,13 +34,18 @@ constexpr int TC_NA = 2;         // A blocks resident per unit
 constexpr int TC_BN = 128;       // columns per B tile (UMMA N)
 constexpr int TC_BK = 64;        // bf16 per 128-byte swizzle row
 constexpr int TC_STAGES = 4;     // B ring depth
-constexpr int TC_THREADS = 192;  // 6 warps
+constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: one per A block
+constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
+constexpr int TC_THREADS = 64 + TC_EPI_THREADS;  // producer + MMA + epilogue warps
 constexpr int TC_BOX_BYTES = TC_BM * TC_BK * 2;  // 16 KB (A box and B box alike)
 constexpr int TC_TMEM_COLS = 512;
 
-struct RowCand {
-    float v[3];
-    int32_t c[3];
+// Per A-row approximate top-4 (value, column): the first three are re-scored
+// in float64, the fourth bounds every other column.
+constexpr int TC_TOPK = 4;
+struct __align__(16) RowCand {
+    float v[TC_TOPK];
+    int32_t c[TC_TOPK];
 };
 
 struct TcParams {
@@ -135,15 +140,15 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-__device__ __forceinline__ void top3_insert(float v, int c, float& t1, int& c1, float& t2, int& c2, float& t3,
-                                            int& c3) {
-    if (v > t3) {
-        if (v > t2) {
-            t3 = t2; c3 = c2;
-            if (v > t1) { t2 = t1; c2 = c1; t1 = v; c1 = c; }
-            else { t2 = v; c2 = c; }
-        } else {
-            t3 = v; c3 = c;
+// Insert into a descending top-4 (caller has checked v > t[3]); strict >
+// keeps the earlier column on equal values.
+__device__ __forceinline__ void top4_insert(float v, int c, float (&t)[TC_TOPK], int (&ci)[TC_TOPK]) {
+    t[3] = v; ci[3] = c;
+#pragma unroll
+    for (int k = 3; k > 0; --k) {
+        if (t[k] > t[k - 1]) {
+            const float tv = t[k]; t[k] = t[k - 1]; t[k - 1] = tv;
+            const int tc = ci[k]; ci[k] = ci[k - 1]; ci[k - 1] = tc;
         }
     }
 }
@@ -174,7 +179,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         mbar_init(a_full, 1);
         mbar_init(a_empty, 1);
         for (int s = 0; s < TC_STAGES; ++s) { mbar_init(b_full + s, 1); mbar_init(b_empty + s, 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(t_full + s, 1); mbar_init(t_empty + s, 128); }
+        for (int s = 0; s < 2; ++s) { mbar_init(t_full + s, 1); mbar_init(t_empty + s, TC_EPI_THREADS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -263,9 +268,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
-        const int q = warp & 3;                // TMEM lane quarter this warp may access
-        const int et = threadIdx.x - 64;       // 0..127
+        // ===================== epilogue (warps 2..9) =====================
+        // warp -> (A block b, TMEM lane quarter q): each thread owns one row.
+        const int q = warp & 3;
+        const int b = (warp - 2) >> 2;
+        const int et = threadIdx.x - 64;       // 0..255
         const uint32_t lane_code = 31u - (uint32_t)lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -275,48 +282,53 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (M + TC_BN - 1) / TC_BN;
-            float t1[TC_NA], t2[TC_NA], t3[TC_NA];
-            int c1[TC_NA], c2[TC_NA], c3[TC_NA];
-            bool rvalid[TC_NA];
+            float tk[TC_TOPK];
+            int ck[TC_TOPK];
 #pragma unroll
-            for (int b = 0; b < TC_NA; ++b) {
-                t1[b] = t2[b] = t3[b] = -INFINITY;
-                c1[b] = c2[b] = c3[b] = -1;
-                rvalid[b] = (int64_t)un.y + b * TC_BM + q * 32 + lane < a1;
-            }
+            for (int k = 0; k < TC_TOPK; ++k) { tk[k] = -INFINITY; ck[k] = -1; }
+            const int64_t my_row = (int64_t)un.y + b * TC_BM + q * 32 + lane;
+            const bool rvalid = my_row < a1;
             for (int t = 0; t < n_tiles; ++t) {
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
                 const int col0 = t * TC_BN;
-#pragma unroll
-                for (int b = 0; b < TC_NA; ++b) {
 #pragma unroll 1
-                    for (int ch = 0; ch < TC_BN / 32; ++ch) {
-                        uint32_t r[32];
-                        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + b * TC_BN + ch * 32),
-                                  r);
-                        const int cbase = col0 + ch * 32;
-                        uint32_t cm = 0, cm2 = 0;
+                for (int ch = 0; ch < TC_BN / 32; ++ch) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + b * TC_BN + ch * 32),
+                              r);
+                    const int cbase = col0 + ch * 32;
+                    const int nvalid = rvalid ? min(32, M - cbase) : 0;  // valid columns of this thread
+                    // row side: running top-3 (rarely taken after the first tiles)
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float v = __uint_as_float(r[j]);
-                            const bool ok = rvalid[b] && (cbase + j < M);
-                            if (ok) top3_insert(v, cbase + j, t1[b], c1[b], t2[b], c2[b], t3[b], c3[b]);
-                            const uint32_t key = ok ? ((__float_as_uint(v + p.bias) & 0xFFFFFFE0u) | lane_code) : 0u;
-                            const uint32_t m = __reduce_max_sync(0xffffffffu, key);
-                            const uint32_t m2 = __reduce_max_sync(0xffffffffu, key == m ? 0u : key);
-                            if (lane == j) { cm = m; cm2 = m2; }
-                        }
-                        colbuf[(b * 4 + q) * TC_BN + ch * 32 + lane] = make_uint2(cm, cm2);
+                    for (int j = 0; j < 32; ++j) {
+                        const float v = __uint_as_float(r[j]);
+                        if (j < nvalid && v > tk[TC_TOPK - 1]) top4_insert(v, cbase + j, tk, ck);
                     }
+                    // column side: 32 independent warp reductions (keys embed the lane)
+                    uint32_t key[32], m[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        key[j] = (j < nvalid) ? ((__float_as_uint(__uint_as_float(r[j]) + p.bias) & 0xFFFFFFE0u) | lane_code)
+                                              : 0u;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) m[j] = __reduce_max_sync(0xffffffffu, key[j]);
+                    uint32_t cm = 0, cm2 = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, key[j] == m[j] ? 0u : key[j]);
+                        cm = (lane == j) ? m[j] : cm;
+                        cm2 = (lane == j) ? m2 : cm2;
+                    }
+                    colbuf[(b * 4 + q) * TC_BN + ch * 32 + lane] = make_uint2(cm, cm2);
                 }
                 // accumulator drained: hand the TMEM buffer back to the MMA warp
                 tc_fence_before();
                 mbar_arrive(t_empty + acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                named_sync(1, 128);
+                named_sync(1, TC_EPI_THREADS);
                 // merge the 8 partials of column et and fold into the global state
-                if (col0 + et < M) {
+                if (et < TC_BN && col0 + et < M) {
                     unsigned long long best = 0;
                     uint32_t second = 0;
 #pragma unroll
@@ -344,16 +356,13 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                         if (sec) atomicMax(p.col_second + gc, sec);
                     }
                 }
-                named_sync(1, 128);
+                named_sync(1, TC_EPI_THREADS);
             }
+            if (rvalid) {
+                RowCand rc;
 #pragma unroll
-            for (int b = 0; b < TC_NA; ++b) {
-                if (rvalid[b]) {
-                    RowCand rc;
-                    rc.v[0] = t1[b]; rc.v[1] = t2[b]; rc.v[2] = t3[b];
-                    rc.c[0] = c1[b]; rc.c[1] = c2[b]; rc.c[2] = c3[b];
-                    p.cand[(int64_t)un.y + b * TC_BM + q * 32 + lane] = rc;
-                }
+                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk[k]; rc.c[k] = ck[k]; }
+                p.cand[my_row] = rc;
             }
         }
     }
@@ -369,26 +378,6 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 // ---------------------------------------------------------------------------
 // certification
 
-template <typename T>
-__device__ __forceinline__ double ldv(const T* p, int64_t i);
-template <>
-__device__ __forceinline__ double ldv<uint16_t>(const uint16_t* p, int64_t i) {
-    return (double)__uint_as_float(((uint32_t)p[i]) << 16);
-}
-template <>
-__device__ __forceinline__ double ldv<float>(const float* p, int64_t i) { return (double)p[i]; }
-template <>
-__device__ __forceinline__ double ldv<double>(const double* p, int64_t i) { return p[i]; }
-
-template <typename T>
-__device__ __forceinline__ double warp_dot(const T* a, const T* b, int D, int lane) {
-    double s = 0.0;
-    for (int k = lane; k < D; k += 32) s = fma(ldv<T>(a, k), ldv<T>(b, k), s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    return s;
-}
-
 __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pairs, int64_t r) {
     int lo = 0, hi = n_pairs;
     while (hi - lo > 1) {
@@ -400,8 +389,9 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
 
 __device__ __forceinline__ double d2x(double s) { return fmax(__dsub_rn(2.0, __dmul_rn(2.0, s)), 0.0); }
 
-// Row side: candidates c1, c2 re-scored in float64; certified when every
-// other column is provably below both (sim and clamped d2), else listed.
+// Row side: candidates c1..c3 re-scored in float64; certified when every
+// non-candidate column (sim <= v[3] + eps) is provably worse than the
+// second best candidate in clamped d2, else listed for the re-scan.
 template <typename T>
 __global__ void mt_certify_rows(const T* __restrict__ A, const T* __restrict__ B, int D,
                                 const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
@@ -418,30 +408,31 @@ __global__ void mt_certify_rows(const T* __restrict__ A, const T* __restrict__ B
         return;
     }
     const RowCand c = cand[r];
-    bool ok = c.c[0] >= 0 && M >= 1;
-    double e1 = 0, e2 = 0;
-    if (ok) e1 = warp_dot<T>(A + r * D, B + (b0 + c.c[0]) * D, D, lane);
-    if (ok && M >= 2) {
-        ok = c.c[1] >= 0;
-        if (ok) e2 = warp_dot<T>(A + r * D, B + (b0 + c.c[1]) * D, D, lane);
+    const int nc = (int)(M < 3 ? M : 3);  // candidates to re-score
+    bool ok = true;
+    double d[3];
+    int ci[3];
+    for (int k = 0; k < nc; ++k) {
+        ci[k] = c.c[k];
+        ok = ok && ci[k] >= 0;
+        d[k] = ok ? d2x(warp_dot16<T>(A + r * D, B + (b0 + ci[k]) * D, D, lane)) : INFINITY;
     }
-    if (ok) {
-        if (M >= 3) {
-            const double others = (double)c.v[2] + eps;  // bound on every non-candidate column
-            const double lo = (M >= 2) ? fmin(e1, e2) : e1;
-            ok = others < lo && others < 1.0;
+    // order the candidates by (d2, column): insertion sort of <= 3
+    for (int i = 1; i < nc; ++i)
+        for (int k = i; k > 0 && (d[k] < d[k - 1] || (d[k] == d[k - 1] && ci[k] < ci[k - 1])); --k) {
+            const double td = d[k]; d[k] = d[k - 1]; d[k - 1] = td;
+            const int tc = ci[k]; ci[k] = ci[k - 1]; ci[k - 1] = tc;
         }
+    if (ok && M > 3) {
+        // every other column has sim <= v[3] + eps, i.e. d2 >= 2 - 2(v[3] + eps)
+        const double others = (double)c.v[3] + eps;
+        ok = others < 1.0 && __dsub_rn(2.0, __dmul_rn(2.0, others)) > d[1];
     }
     if (lane == 0) {
         if (ok) {
-            double d1 = d2x(e1), dd2 = INFINITY;
-            int best = c.c[0];
-            if (M >= 2) {
-                const double d_b = d2x(e2);
-                if (d_b < d1 || (d_b == d1 && c.c[1] < best)) { dd2 = d1; d1 = d_b; best = c.c[1]; }
-                else dd2 = d_b;
-            }
-            rs[r].best = best; rs[r].d1 = d1; rs[r].d2 = dd2;
+            rs[r].best = ci[0];
+            rs[r].d1 = d[0];
+            rs[r].d2 = (M >= 2) ? d[1] : INFINITY;
         } else {
             const unsigned long long i = atomicAdd((unsigned long long*)&counters[0], 1ull);
             flag_rows[i] = (int32_t)r;
@@ -474,7 +465,7 @@ __global__ void mt_certify_cols(const T* __restrict__ A, const T* __restrict__ B
     if (ok) {
         r1 = (int64_t)(0xFFFFFFFFull - (k & 0xFFFFFFFFull));
         ok = r1 >= 0 && r1 < N;
-        if (ok) e1 = warp_dot<T>(A + (a0 + r1) * D, B + c * D, D, lane);
+        if (ok) e1 = warp_dot16<T>(A + (a0 + r1) * D, B + c * D, D, lane);
     }
     if (ok && N >= 2) {
         const unsigned int s2 = col_second[c];
@@ -497,9 +488,11 @@ __global__ void mt_norm_kernel(const uint16_t* __restrict__ X, int64_t rows, int
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= rows) return;
     float s = 0.f;
-    for (int k = lane; k < D; k += 32) {
-        const float v = __uint_as_float(((uint32_t)X[r * D + k]) << 16);
-        s = fmaf(v, v, s);
+    for (int k = lane * 8; k < D; k += 256) {
+        double x[8];
+        Vec16<uint16_t>::load(X + r * D + k, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s = fmaf((float)x[i], (float)x[i], s);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
