@@ -170,6 +170,17 @@ EC3R_API int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, co
                              int H, int W, const double* K4_h, const double* slot_poses,
                              const double* slot_globals, const int32_t* slots_h, int n,
                              void* stream);
+/* Same fusion with CTA-level aggregation: slot group g is
+ * slots[group_off[g] .. group_off[g+1]) (device arrays); every CTA takes one
+ * band of image rows across all frames of a group (frames of one submap, or
+ * of neighbouring submaps, see the same surface), accumulates its voxels in
+ * shared memory and flushes each distinct voxel to the table once.
+ * max_frames_per_group bounds the fixed-point accumulator range. */
+EC3R_API int ec3r_vhash_insert_frame_groups(ec3r_vhash* h, const float* depth_pool,
+                                            const float* conf_pool, int H, int W, const double* K4_h,
+                                            const double* slot_poses, const double* slot_globals,
+                                            const int32_t* slots, const int32_t* group_off, int n_groups,
+                                            int max_frames_per_group, void* stream);
 /* Fuse explicit points (N,3) float64 with conf (N) float64 under sim3_h. */
 EC3R_API int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, const double* conf, int64_t n,
                              const double* sim3_h, void* stream);

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(FI_NT) vh_insert_frames_kernel(FuseArgs a) {
     const float* cp = a.conf + (size_t)slot * HW + (size_t)v0 * W;
     const int npix = nrows * W;
     const bool vec = ((((size_t)slot * HW + (size_t)v0 * W) & 3) == 0) && ((npix & 3) == 0);
-    unsigned long long n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
+    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;  // per-thread counts
 
     for (int base = 4 * threadIdx.x; base < npix; base += 4 * FI_NT) {
         float zs[4], cs[4];
@@ -254,10 +254,220 @@ __global__ void __launch_bounds__(FI_NT) vh_insert_frames_kernel(FuseArgs a) {
         n_slow += __shfl_xor_sync(0xffffffffu, n_slow, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&cta_cnt[0], n_in);
-        atomicAdd(&cta_cnt[1], n_oor);
-        atomicAdd(&cta_cnt[2], n_ovf);
-        atomicAdd(&cta_cnt[3], n_slow);
+        atomicAdd(&cta_cnt[0], (unsigned long long)n_in);
+        atomicAdd(&cta_cnt[1], (unsigned long long)n_oor);
+        atomicAdd(&cta_cnt[2], (unsigned long long)n_ovf);
+        atomicAdd(&cta_cnt[3], (unsigned long long)n_slow);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && cta_cnt[threadIdx.x]) atomicAdd(&a.counters[threadIdx.x], cta_cnt[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// Grouped insertion with CTA-level aggregation.
+//
+// Measured on this part (tools/atomics_probe.cu): random global atomics into a
+// DRAM-resident table run at ~22-33 G op/s, shared-memory integer atomics at
+// ~2 T op/s.  Frames of a submap (and of neighbouring submaps) see the same
+// surface, so a CTA takes one band of AG_ROWS image rows across every frame of
+// a slot group, accumulates the voxels in a shared-memory open-addressing
+// table with fixed-point integer atomics, and flushes each distinct voxel to
+// the global hash once.  Keys use the same exact fast/slow path as above.
+
+constexpr int AG_NT = 512;
+constexpr int AG_ROWS = 4;
+constexpr int AG_SLOTS = 3840;  // 8 B key + 5 x 4 B accumulators: 105 KB, two CTAs per SM
+constexpr int AG_PROBES = 32;
+
+struct GroupArgs {
+    FuseArgs f;
+    const int32_t* group_off;  // n_groups + 1 offsets into f.slots
+    float qscale;              // fixed-point scale of the shared accumulators
+};
+
+__device__ __forceinline__ bool sm_insert(unsigned long long* skeys, unsigned int* sacc, unsigned long long key,
+                                          unsigned int qx, unsigned int qy, unsigned int qz, unsigned int qw) {
+    unsigned int h = (unsigned int)(((mix64(key) >> 32) * (unsigned long long)AG_SLOTS) >> 32);
+#pragma unroll 1
+    for (int probe = 0; probe < AG_PROBES; ++probe) {
+        unsigned long long k = skeys[h];
+        if (k == kEmpty) {
+            const unsigned long long prev = atomicCAS(&skeys[h], kEmpty, key);
+            k = (prev == kEmpty) ? key : prev;
+        }
+        if (k == key) {
+            atomicAdd(&sacc[0 * AG_SLOTS + h], qx);
+            atomicAdd(&sacc[1 * AG_SLOTS + h], qy);
+            atomicAdd(&sacc[2 * AG_SLOTS + h], qz);
+            atomicAdd(&sacc[3 * AG_SLOTS + h], qw);
+            atomicAdd(&sacc[4 * AG_SLOTS + h], 1u);
+            return true;
+        }
+        h = (h + 1 == AG_SLOTS) ? 0u : h + 1;
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(AG_NT, 2) vh_insert_groups_kernel(GroupArgs ga) {
+    const FuseArgs& a = ga.f;
+    extern __shared__ __align__(16) unsigned char gsm[];
+    unsigned long long* skeys = reinterpret_cast<unsigned long long*>(gsm);
+    unsigned int* sacc = reinterpret_cast<unsigned int*>(skeys + AG_SLOTS);  // [5][AG_SLOTS]
+    float* xcf = reinterpret_cast<float*>(sacc + 5 * AG_SLOTS);               // [W]
+    __shared__ float ycf[AG_ROWS];
+    __shared__ float Mf[12];
+    __shared__ double Pd[8], Gd[8];
+    __shared__ unsigned long long cta_cnt[4];
+
+    const int W = a.W;
+    const int v0 = blockIdx.x * AG_ROWS;
+    const int nrows = min(AG_ROWS, a.H - v0);
+    const int g0 = ga.group_off[blockIdx.y], g1 = ga.group_off[blockIdx.y + 1];
+    for (int i = threadIdx.x; i < AG_SLOTS; i += AG_NT) skeys[i] = kEmpty;
+    for (int i = threadIdx.x; i < 5 * AG_SLOTS; i += AG_NT) sacc[i] = 0u;
+    for (int u = threadIdx.x; u < W; u += AG_NT) xcf[u] = (float)((u - a.cx) / a.fx);
+    if (threadIdx.x < nrows) ycf[threadIdx.x] = (float)((v0 + threadIdx.x - a.cy) / a.fy);
+    if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
+    const float inv = a.inv_cell_f, cellf = a.cell_f, qs = ga.qscale;
+    const float qcell = qs / cellf;
+    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;  // per-thread counts
+    const size_t HW = (size_t)a.H * W;
+    const int npix = nrows * W;
+
+    for (int gi = g0; gi < g1; ++gi) {
+        const int slot = a.slots[gi];
+        __syncthreads();  // previous frame's Mf / Pd / Gd consumers are done
+        if (threadIdx.x < 8) {
+            Pd[threadIdx.x] = a.slot_poses[8 * slot + threadIdx.x];
+            Gd[threadIdx.x] = a.slot_globals[8 * slot + threadIdx.x];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double RG[3][3], RP[3][3];
+            quat_to_mat(Gd + 1, RG);
+            quat_to_mat(Pd + 1, RP);
+            for (int i = 0; i < 3; ++i) {
+                for (int j = 0; j < 3; ++j)
+                    Mf[3 * i + j] =
+                        (float)(Gd[0] * (RG[i][0] * RP[0][j] + RG[i][1] * RP[1][j] + RG[i][2] * RP[2][j]));
+                Mf[9 + i] = (float)(Gd[0] * (RG[i][0] * Pd[5] + RG[i][1] * Pd[6] + RG[i][2] * Pd[7]) + Gd[5 + i]);
+            }
+        }
+        __syncthreads();
+        // composite rotation*scale row-major m{i}{j} = M[i][j]; translation Mf[9..11]
+        const float m00 = Mf[0], m01 = Mf[1], m02 = Mf[2], m10 = Mf[3], m11 = Mf[4], m12 = Mf[5];
+        const float m20 = Mf[6], m21 = Mf[7], m22 = Mf[8], tx = Mf[9], ty = Mf[10], tz = Mf[11];
+        const float tabs = fabsf(tx) + fabsf(ty) + fabsf(tz);
+        const float* dp = a.depth + (size_t)slot * HW + (size_t)v0 * W;
+        const float* cp = a.conf + (size_t)slot * HW + (size_t)v0 * W;
+        const bool vec = ((((size_t)slot * HW + (size_t)v0 * W) & 3) == 0) && ((npix & 3) == 0);
+        for (int base = 4 * threadIdx.x; base < npix; base += 4 * AG_NT) {
+            float zs[4], cs[4];
+            if (vec) {
+                const float4 z4 = __ldcs(reinterpret_cast<const float4*>(dp + base));
+                const float4 c4 = __ldcs(reinterpret_cast<const float4*>(cp + base));
+                zs[0] = z4.x; zs[1] = z4.y; zs[2] = z4.z; zs[3] = z4.w;
+                cs[0] = c4.x; cs[1] = c4.y; cs[2] = c4.z; cs[3] = c4.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool in = base + k < npix;
+                    zs[k] = in ? dp[base + k] : 0.f;
+                    cs[k] = in ? cp[base + k] : 0.f;
+                }
+            }
+            int r = base / W;
+            int u = base - r * W;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float z = zs[k], c = cs[k];
+                if (z > 0.f && c > 0.f) {
+                    ++n_in;
+                    const float xu = xcf[u], yv = ycf[r];
+                    const float ax = m00 * xu, ay = m10 * xu, az = m20 * xu;
+                    const float bx = m01 * yv, by = m11 * yv, bz = m21 * yv;
+                    const float dx = ax + bx + m02, dy = ay + by + m12, dz = az + bz + m22;
+                    const float x = fmaf(z, dx, tx), y = fmaf(z, dy, ty), zz = fmaf(z, dz, tz);
+                    const float sa = fabsf(ax) + fabsf(ay) + fabsf(az) + fabsf(bx) + fabsf(by) + fabsf(bz) +
+                                     fabsf(m02) + fabsf(m12) + fabsf(m22);
+                    const float axs = fabsf(x) + fabsf(y) + fabsf(zz);
+                    // first-order float32 error bound of x,y,z (x8 safety), see vh_insert_frames_kernel
+                    const float err = 4.76837158203125e-07f * (2.0f * z * sa + tabs + 2.0f * axs) + 1e-9f;
+                    const float margin = err * inv + 2.4e-7f;
+                    const float qx = x * inv, qy = y * inv, qz = zz * inv;
+                    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+                    const bool near = (qx - fx < margin) || (fx + 1.0f - qx < margin) || (qy - fy < margin) ||
+                                      (fy + 1.0f - qy < margin) || (qz - fz < margin) || (fz + 1.0f - qz < margin) ||
+                                      fabsf(qx) > 1.0e6f || fabsf(qy) > 1.0e6f || fabsf(qz) > 1.0e6f;
+                    long long cxl, cyl, czl;
+                    if (!near) {
+                        cxl = (long long)fx; cyl = (long long)fy; czl = (long long)fz;
+                    } else {
+                        long long cc[3];
+                        exact_cells(Pd, Gd, ray_coef(u, a.cx, a.fx), ray_coef(v0 + r, a.cy, a.fy), z, a.cell, cc);
+                        cxl = cc[0]; cyl = cc[1]; czl = cc[2];
+                        ++n_slow;
+                    }
+                    if (cell_in_range(cxl) && cell_in_range(cyl) && cell_in_range(czl)) {
+                        const unsigned long long key = pack_cells(cxl, cyl, czl);
+                        const float ox = x - (float)cxl * cellf, oy = y - (float)cyl * cellf,
+                                    oz = zz - (float)czl * cellf;
+                        const unsigned int ux = __float2uint_rn(fminf(fmaxf(c * ox * qcell, 0.f), qs));
+                        const unsigned int uy = __float2uint_rn(fminf(fmaxf(c * oy * qcell, 0.f), qs));
+                        const unsigned int uz = __float2uint_rn(fminf(fmaxf(c * oz * qcell, 0.f), qs));
+                        const unsigned int uw = __float2uint_rn(c * qs);
+                        if (!sm_insert(skeys, sacc, key, ux, uy, uz, uw)) {
+                            // shared table saturated: this point goes straight to the global hash
+                            if (!vh_insert(a.table, a.mask, key, c * ox, c * oy, c * oz, c)) ++n_ovf;
+                        }
+                    } else {
+                        ++n_oor;
+                    }
+                }
+                if (++u == W) { u = 0; ++r; }
+            }
+        }
+    }
+    __syncthreads();
+    // flush: one global insert per distinct voxel of this CTA
+    const float back = cellf / qs, wback = 1.0f / qs;
+    for (int i = threadIdx.x; i < AG_SLOTS; i += AG_NT) {
+        const unsigned long long key = skeys[i];
+        if (key == kEmpty) continue;
+        const float sx = (float)sacc[i] * back, sy = (float)sacc[AG_SLOTS + i] * back;
+        const float sz = (float)sacc[2 * AG_SLOTS + i] * back, sw = (float)sacc[3 * AG_SLOTS + i] * wback;
+        const unsigned int cnt = sacc[4 * AG_SLOTS + i];
+        unsigned long long idx = mix64(key) & a.mask;
+        bool done = false;
+        for (unsigned long long probe = 0; probe <= a.mask; ++probe) {
+            Slot* s = a.table + idx;
+            unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(&s->key);
+            if (k == kEmpty) {
+                const unsigned long long prev = atomicCAS(&s->key, kEmpty, key);
+                k = (prev == kEmpty) ? key : prev;
+            }
+            if (k == key) {
+                red_add_v4(&s->sx, sx, sy, sz, sw);
+                atomicAdd(&s->cnt, cnt);
+                done = true;
+                break;
+            }
+            idx = (idx + 1) & a.mask;
+        }
+        if (!done) n_ovf += cnt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
+        n_oor += __shfl_xor_sync(0xffffffffu, n_oor, o);
+        n_ovf += __shfl_xor_sync(0xffffffffu, n_ovf, o);
+        n_slow += __shfl_xor_sync(0xffffffffu, n_slow, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&cta_cnt[0], (unsigned long long)n_in);
+        atomicAdd(&cta_cnt[1], (unsigned long long)n_oor);
+        atomicAdd(&cta_cnt[2], (unsigned long long)n_ovf);
+        atomicAdd(&cta_cnt[3], (unsigned long long)n_slow);
     }
     __syncthreads();
     if (threadIdx.x < 4 && cta_cnt[threadIdx.x]) atomicAdd(&a.counters[threadIdx.x], cta_cnt[threadIdx.x]);
@@ -456,6 +666,35 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     dim3 grid((H + FI_ROWS - 1) / FI_ROWS, n);
     vh_insert_frames_kernel<<<grid, FI_NT, smem, as_stream(stream)>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
+    return EC3R_OK;
+}
+
+extern "C" int ec3r_vhash_insert_frame_groups(ec3r_vhash* h, const float* depth_pool, const float* conf_pool, int H,
+                                              int W, const double* K4_h, const double* slot_poses,
+                                              const double* slot_globals, const int32_t* slots,
+                                              const int32_t* group_off, int n_groups, int max_frames_per_group,
+                                              void* stream) {
+    if (!h || H <= 0 || W <= 0 || !K4_h || n_groups < 0 || max_frames_per_group < 1) return EC3R_EARG;
+    if (n_groups == 0) return EC3R_OK;
+    GroupArgs ga;
+    FuseArgs& a = ga.f;
+    a.depth = depth_pool; a.conf = conf_pool; a.slot_poses = slot_poses; a.slot_globals = slot_globals;
+    a.slots = slots; a.H = H; a.W = W;
+    a.fx = K4_h[0]; a.fy = K4_h[1]; a.cx = K4_h[2]; a.cy = K4_h[3];
+    a.cell = h->cell; a.inv_cell_f = (float)(1.0 / h->cell); a.cell_f = (float)h->cell;
+    a.table = h->slots; a.mask = h->mask; a.counters = h->counters;
+    ga.group_off = group_off;
+    // fixed-point scale: every point adds <= qscale per accumulator and a CTA
+    // sees <= max_frames * AG_ROWS * W points, so sums stay below 2^32
+    const double max_pts = (double)max_frames_per_group * AG_ROWS * W;
+    double qs = 65536.0;
+    while (qs > 1.0 && qs * max_pts >= 4294967295.0) qs *= 0.5;
+    ga.qscale = (float)qs;
+    const size_t smem = (size_t)AG_SLOTS * (8 + 5 * 4) + (size_t)W * 4;
+    EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((H + AG_ROWS - 1) / AG_ROWS, n_groups);
+    vh_insert_groups_kernel<<<grid, AG_NT, smem, as_stream(stream)>>>(ga);
+    EC3R_CHECK_LAUNCH("vh_insert_groups_kernel");
     return EC3R_OK;
 }
 

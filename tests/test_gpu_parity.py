@@ -245,9 +245,60 @@ def test_voxel_fusion_vs_oracle(golden):
         o = ofuse.fuse_submaps(gs, globs, cell)
         np.testing.assert_array_equal(out["keys"], o["keys"])
         np.testing.assert_array_equal(out["count"], o["count"])
-        np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-5)
+        np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-4)
         assert np.max(np.abs(out["centroid"] - o["centroid"])) < 1e-4
         assert out["stats"]["n_points_in"] == o["n_in"]
+
+
+def test_grouped_and_per_frame_fusion_agree(golden):
+    """CTA-aggregated insertion (fixed-point shared accumulators) vs the
+    per-frame kernel: identical keys and counts, centroids within 1e-5 m."""
+    from paper_2510_02080_b200 import mapping
+    g = golden("mapping")
+    dm, sms = _dense_mapping(g)
+    dm.register_chain(sms)
+    for per_group in (1, 2, 3):
+        groups = mapping.SlotGroups(sms, per_group)
+        a = mapping.VoxelMap(0.02, 1 << 16)
+        a.insert_groups(dm.pool, groups)
+        b = mapping.VoxelMap(0.02, 1 << 16)
+        b.insert_frames(dm.pool, groups.slots)
+        ka, ca, wa, na = (x.cpu().numpy() for x in a.extract())
+        kb, cb, wb, nb = (x.cpu().numpy() for x in b.extract())
+        np.testing.assert_array_equal(ka, kb)
+        np.testing.assert_array_equal(na, nb)
+        assert np.max(np.abs(ca - cb)) < 1e-5
+        np.testing.assert_allclose(wa, wb, rtol=1e-4)
+        assert a.stats()["n_points_in"] == b.stats()["n_points_in"]
+
+
+def test_voxel_fusion_full_resolution_submaps():
+    """Two 518x392 synthetic submaps (cfg-1 scale): keys / counts bit-exact vs
+    the oracle's float64 transform, centroids within 1e-4 m."""
+    from paper_2510_02080_b200 import mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(11, cfg, seed=5, device="cuda")
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms = [dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    dm.register_chain(sms)
+    out = dm.fused_cloud(voxel=0.02)
+    dense = []
+    for sm, ids, o in zip(sms, sb.frame_ids, sb.slot_offsets):
+        F = len(ids)
+        dense.append(dict(depth=sb.depth[o:o + F].cpu().numpy(), conf=sb.conf[o:o + F].cpu().numpy(),
+                          frame_ids=np.array(ids), pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:],
+                          K=sb.K4))
+    globs = [(sm.global_pose.scale, np.asarray(sm.global_pose.rotation.q), np.asarray(sm.global_pose.translation))
+             for sm in sms]
+    o = ofuse.fuse_submaps(dense, globs, 0.02)
+    np.testing.assert_array_equal(out["keys"], o["keys"])
+    np.testing.assert_array_equal(out["count"], o["count"])
+    assert np.max(np.abs(out["centroid"] - o["centroid"])) < 1e-4
+    np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-4)
+    st = out["stats"]
+    assert st["n_points_in"] == o["n_in"] and st["n_overflow"] == 0
+    assert st["n_slow_path"] < 0.02 * st["n_points_in"]
 
 
 def test_voxel_points_api_and_extreme_coordinates():
