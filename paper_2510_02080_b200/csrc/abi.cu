@@ -24,8 +24,9 @@ void set_last_error_msg(const char* msg) { snprintf(g_last_error, sizeof(g_last_
 // tensor-core approximate pass (match_tc.cu)
 int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x, const int64_t* a_off_d,
                  const int64_t* b_off_d, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
-                 int exact_dtype, double norm_bound, MatchRowState* rs, int32_t* col_best, int32_t* flag_rows,
-                 int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes, cudaStream_t st);
+                 int exact_dtype, double norm_bound, double ratio, MatchRowState* rs, int32_t* col_best,
+                 int32_t* flag_rows, int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes,
+                 cudaStream_t st);
 size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs);
 
 }  // namespace ec3r
@@ -74,8 +75,8 @@ extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const vo
     int rc;
     if (A != nullptr && B != nullptr && total_a > 0 && total_b > 0) {
         // tensor-core pass: certifies most rows / columns and lists the rest
-        rc = match_tc_run(A, B, A_x, B_x, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound, rs,
-                          col_best, flag_rows, flag_cols, counters, tc_ws, tc_bytes, st);
+        rc = match_tc_run(A, B, A_x, B_x, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound, ratio,
+                          rs, col_best, flag_rows, flag_cols, counters, tc_ws, tc_bytes, st);
         if (rc) return rc;
         rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
                                   flag_cols, counters + 1, 0, rs, col_best, st);

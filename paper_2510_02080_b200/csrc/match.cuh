@@ -10,7 +10,7 @@ struct MatchRowState {
     double d1;   // d2 value of the best column
     double d2;   // second order statistic of the row's d2 values
     int32_t best;  // best column within the pair (first index on ties), -1 if none
-    int32_t pad;
+    int32_t ratio_ok;  // -1: decide from (d1, d2); 0 / 1: ratio test already certified reject / pass
 };
 
 // 16-byte row chunks widened to float64 (rows are 16-byte aligned: D is

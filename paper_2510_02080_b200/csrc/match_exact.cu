@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(256) mx_rows_kernel(const T* __restrict__ A, c
             rs[r].best = (b1 > b0) ? i1 : -1;
             rs[r].d1 = d1;
             rs[r].d2 = d2nd;
+            rs[r].ratio_ok = -1;
         }
     }
 }
@@ -148,7 +149,8 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
     const MatchRowState s = rs[r];
     if (m > 0 && s.best >= 0 && col_best[b0 + s.best] == (int)(r - a0)) {
         bool ok = true;
-        if (m > 1 && s.d1 > ratio2 * s.d2) ok = false;
+        if (s.ratio_ok >= 0) ok = s.ratio_ok != 0;  // certified from the tensor-core values
+        else if (m > 1 && s.d1 > ratio2 * s.d2) ok = false;
         if (ok) out = s.best;
     }
     match_b[r] = out;

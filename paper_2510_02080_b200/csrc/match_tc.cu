@@ -389,24 +389,93 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
 
 __device__ __forceinline__ double d2x(double s) { return fmax(__dsub_rn(2.0, __dmul_rn(2.0, s)), 0.0); }
 
-// Row side: candidates c1..c3 re-scored in float64; certified when every
-// non-candidate column (sim <= v[3] + eps) is provably worse than the
-// second best candidate in clamped d2, else listed for the re-scan.
+// Stage 1 (one thread per row): decide from the approximate values alone.
+// Every true similarity is within eps of its tensor-core value, so the
+// approximate order statistics bound the true ones: the argmax is certain
+// when a1 - a2 > 2 eps (and the runner-up cannot clamp to d2 = 0), and the
+// ratio test d1 > r^2 d2 (tracking.py:167) is certain when its interval
+// bounds do not straddle.  Everything else goes to the float64 stages.
+__device__ __forceinline__ double d2c(double s) { return fmax(2.0 - 2.0 * s, 0.0); }
+
+__global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
+                               int64_t total_a, const RowCand* __restrict__ cand, double eps, double ratio2,
+                               MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
+                               int64_t* __restrict__ counters) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= total_a) return;
+    const int p = pair_of(a_off, n_pairs, r);
+    const int64_t M = b_off[p + 1] - b_off[p];
+    MatchRowState s;
+    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = -1;
+    bool decided = false;
+    if (M == 0) {
+        decided = true;
+    } else {
+        const RowCand c = cand[r];
+        const double a1 = c.v[0];
+        if (M == 1) {
+            decided = c.c[0] >= 0;
+            s.best = c.c[0];
+            s.ratio_ok = 1;  // ratio test skipped for a single column (tracking.py:165)
+        } else {
+            const double a2 = c.v[1];
+            if (c.c[0] >= 0 && c.c[1] >= 0 && a1 - a2 > 2.0 * eps && a2 + eps < 1.0) {
+                const double d1_lo = d2c(a1 + eps), d1_hi = d2c(a1 - eps);
+                const double s_lo = d2c(a2 + eps), s_hi = d2c(a2 - eps);
+                if (d1_lo > ratio2 * s_hi) { decided = true; s.ratio_ok = 0; }
+                else if (d1_hi < ratio2 * s_lo) { decided = true; s.ratio_ok = 1; }
+                s.best = c.c[0];
+            }
+        }
+    }
+    if (decided) rs[r] = s;
+    else pending[atomicAdd((unsigned long long*)&counters[2], 1ull)] = (int32_t)r;
+}
+
+// Column side, stage 1: argmax certain when the best (quantised) key beats
+// the second by more than the bound and the runner-up cannot clamp.
+__global__ void mt_decide_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
+                               int64_t total_b, const unsigned long long* __restrict__ col_key,
+                               const unsigned int* __restrict__ col_second, double bias, double eps,
+                               int32_t* __restrict__ col_best, int32_t* __restrict__ pending,
+                               int64_t* __restrict__ counters) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= total_b) return;
+    const int p = pair_of(b_off, n_pairs, c);
+    const int64_t N = a_off[p + 1] - a_off[p];
+    if (N == 0) { col_best[c] = -1; return; }
+    const unsigned long long k = col_key[c];
+    const int64_t r1 = (int64_t)(0xFFFFFFFFull - (k & 0xFFFFFFFFull));
+    bool ok = k != 0 && r1 >= 0 && r1 < N;
+    if (ok && N >= 2) {
+        const unsigned int s2 = col_second[c];
+        if (s2 != 0) {
+            const double a1 = (double)__uint_as_float((unsigned int)(k >> 32)) - bias;
+            const double a2 = (double)__uint_as_float(s2) - bias;
+            ok = (a1 - eps > a2 + eps) && (a2 + eps < 1.0);
+        }
+    }
+    if (ok) col_best[c] = (int32_t)r1;
+    else pending[atomicAdd((unsigned long long*)&counters[3], 1ull)] = (int32_t)c;
+}
+
+// Stage 2 (one warp per pending row): candidates c1..c3 re-scored in float64;
+// certified when every non-candidate column (sim <= v[3] + eps) is provably
+// worse than the second best candidate in clamped d2, else listed for the
+// full re-scan.
 template <typename T>
 __global__ void mt_certify_rows(const T* __restrict__ A, const T* __restrict__ B, int D,
                                 const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                                int64_t total_a, const RowCand* __restrict__ cand, double eps,
+                                const int32_t* __restrict__ pending, const RowCand* __restrict__ cand, double eps,
                                 MatchRowState* __restrict__ rs, int32_t* __restrict__ flag_rows,
                                 int64_t* __restrict__ counters) {
     const int lane = threadIdx.x & 31;
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (r >= total_a) return;
+    const int64_t n_pend = counters[2];
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_pend;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = pending[t];
     const int p = pair_of(a_off, n_pairs, r);
     const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
-    if (M == 0) {
-        if (lane == 0) { rs[r].best = -1; rs[r].d1 = INFINITY; rs[r].d2 = INFINITY; }
-        return;
-    }
     const RowCand c = cand[r];
     const int nc = (int)(M < 3 ? M : 3);  // candidates to re-score
     bool ok = true;
@@ -433,31 +502,32 @@ __global__ void mt_certify_rows(const T* __restrict__ A, const T* __restrict__ B
             rs[r].best = ci[0];
             rs[r].d1 = d[0];
             rs[r].d2 = (M >= 2) ? d[1] : INFINITY;
+            rs[r].ratio_ok = -1;
         } else {
             const unsigned long long i = atomicAdd((unsigned long long*)&counters[0], 1ull);
             flag_rows[i] = (int32_t)r;
         }
     }
+    }
 }
 
-// Column side: the best row is re-scored; certified when the column's
-// second value (plus the bound) is below it and below 1 (d2 clamp).
+// Column side, stage 2 (one warp per pending column): the best row is
+// re-scored; certified when the column's second value (plus the bound) is
+// below it and below 1 (d2 clamp), else listed for the full re-scan.
 template <typename T>
 __global__ void mt_certify_cols(const T* __restrict__ A, const T* __restrict__ B, int D,
                                 const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                                int64_t total_b, const unsigned long long* __restrict__ col_key,
+                                const int32_t* __restrict__ pending, const unsigned long long* __restrict__ col_key,
                                 const unsigned int* __restrict__ col_second, double bias, double eps,
                                 int32_t* __restrict__ col_best, int32_t* __restrict__ flag_cols,
                                 int64_t* __restrict__ counters) {
     const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (c >= total_b) return;
+    const int64_t n_pend = counters[3];
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_pend;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t c = pending[t];
     const int p = pair_of(b_off, n_pairs, c);
     const int64_t a0 = a_off[p], N = a_off[p + 1] - a0;
-    if (N == 0) {
-        if (lane == 0) col_best[c] = -1;
-        return;
-    }
     const unsigned long long k = col_key[c];
     bool ok = k != 0;
     int64_t r1 = 0;
@@ -480,6 +550,7 @@ __global__ void mt_certify_cols(const T* __restrict__ A, const T* __restrict__ B
             const unsigned long long i = atomicAdd((unsigned long long*)&counters[1], 1ull);
             flag_cols[i] = (int32_t)c;
         }
+    }
     }
 }
 
@@ -543,19 +614,31 @@ static size_t tc_smem_bytes(int kblocks) {
 size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs) {
     const int64_t max_units = total_a / TC_BM + n_pairs + 1;
     return align256(sizeof(RowCand) * (size_t)total_a) + align256(8 * (size_t)total_b) +
-           align256(4 * (size_t)total_b) + align256(sizeof(int2) * (size_t)max_units) + align256(64);
+           align256(4 * (size_t)total_b) + align256(sizeof(int2) * (size_t)max_units) + align256(64) +
+           align256(4 * (size_t)total_a) + align256(4 * (size_t)total_b);
 }
 
+// Stage 1 on every row / column, then stage-2 float64 certification of the
+// pending ones.  The pending counts live on the device; stage 2 runs on a
+// fixed persistent grid that strides over the lists, so no host
+// synchronisation is needed.
 template <typename T>
 static int certify(const void* Ax, const void* Bx, int D, const int64_t* a_off, const int64_t* b_off, int n_pairs,
                    int64_t ta, int64_t tb, const RowCand* cand, const unsigned long long* ck, const unsigned int* cs,
-                   double bias, double eps_row, double eps_col, MatchRowState* rs, int32_t* col_best,
-                   int32_t* flag_rows, int32_t* flag_cols, int64_t* counters, cudaStream_t st) {
-    mt_certify_rows<T><<<(unsigned)((ta * 32 + 255) / 256), 256, 0, st>>>(
-        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, ta, cand, eps_row, rs, flag_rows, counters);
+                   double bias, double eps_row, double eps_col, double ratio2, MatchRowState* rs, int32_t* col_best,
+                   int32_t* pend_rows, int32_t* pend_cols, int32_t* flag_rows, int32_t* flag_cols,
+                   int64_t* counters, cudaStream_t st) {
+    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, ta, cand, eps_row, ratio2, rs,
+                                                                 pend_rows, counters);
+    EC3R_CHECK_LAUNCH("mt_decide_rows");
+    mt_decide_cols<<<(unsigned)((tb + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, tb, ck, cs, bias, eps_col,
+                                                                 col_best, pend_cols, counters);
+    EC3R_CHECK_LAUNCH("mt_decide_cols");
+    mt_certify_rows<T><<<kNumSMs * 4, 256, 0, st>>>(
+        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, pend_rows, cand, eps_row, rs, flag_rows, counters);
     EC3R_CHECK_LAUNCH("mt_certify_rows");
-    mt_certify_cols<T><<<(unsigned)((tb * 32 + 255) / 256), 256, 0, st>>>(
-        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, tb, ck, cs, bias, eps_col, col_best, flag_cols,
+    mt_certify_cols<T><<<kNumSMs * 4, 256, 0, st>>>(
+        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, pend_cols, ck, cs, bias, eps_col, col_best, flag_cols,
         counters);
     EC3R_CHECK_LAUNCH("mt_certify_cols");
     return EC3R_OK;
@@ -563,8 +646,9 @@ static int certify(const void* Ax, const void* Bx, int D, const int64_t* a_off, 
 
 int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x, const int64_t* a_off_d,
                  const int64_t* b_off_d, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
-                 int exact_dtype, double norm_bound, MatchRowState* rs, int32_t* col_best, int32_t* flag_rows,
-                 int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes, cudaStream_t st) {
+                 int exact_dtype, double norm_bound, double ratio, MatchRowState* rs, int32_t* col_best,
+                 int32_t* flag_rows, int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes,
+                 cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
     const bool tc_ok = (D % TC_BK == 0) && D <= 256 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0 && ta > 0 &&
                        tb > 0 && get_encode() != nullptr;
@@ -585,6 +669,8 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
     const int64_t max_units = ta / TC_BM + n_pairs + 1;
     int2* units = cv.take<int2>(max_units);
     unsigned int* nb = cv.take<unsigned int>(16);
+    int32_t* pend_rows = cv.take<int32_t>(ta);
+    int32_t* pend_cols = cv.take<int32_t>(tb);
     if (cv.used > tc_ws_bytes) return EC3R_EWORKSPACE;
     std::vector<int2> hu;
     hu.reserve(max_units);
@@ -635,17 +721,20 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
         mt_tc_kernel<<<grid, TC_THREADS, smem, st>>>(tmA, tmB, prm);
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
     }
-    EC3R_CUDA_TRY(cudaMemsetAsync(counters, 0, 16, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(counters, 0, 32, st));
+    const double ratio2 = ratio * ratio;  // tracking.py:158
     switch (exact_dtype) {
         case 0:
             return certify<uint16_t>(A, B, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row, eps_col,
-                                     rs, col_best, flag_rows, flag_cols, counters, st);
+                                     ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols, counters, st);
         case 1:
             return certify<float>(A_x, B_x, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row,
-                                  eps_col, rs, col_best, flag_rows, flag_cols, counters, st);
+                                  eps_col, ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols, counters,
+                                  st);
         default:
             return certify<double>(A_x, B_x, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row,
-                                   eps_col, rs, col_best, flag_rows, flag_cols, counters, st);
+                                   eps_col, ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols,
+                                   counters, st);
     }
 }
 
