@@ -120,7 +120,7 @@ class Step:
 
         self.torch, self.mapping, self.tracking = torch, mapping, tracking
         self.dm, self.sms, self.desc, self.cell = dm, sms, desc, cell
-        self.groups = mapping.SlotGroups(sms, 2)
+        self.slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
         self.plan = mapping.ChainPlan(sms)
         self.pairs = self.plan.pairs
         self.seg = self.plan.seg
@@ -153,12 +153,14 @@ class Step:
         self.edge_status, self.sub_status = out[4], out[6]
         ev["t_chain"] = self._event()
         if self.vmap is None:
-            self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.groups, self.cell)
-            self.vmap = self.mapping.VoxelMap(self.cell, max(1 << 16, 2 * int(out[0].numel())))
+            # size the block pool once from a first fusion (outside the timed region)
+            self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell)
+            U = int(out[0].numel())
+            self.out = tuple(torch.empty((U,) + tuple(x.shape[1:]), dtype=x.dtype, device="cuda") for x in out)
         self.vmap.clear()
-        self.vmap.insert_groups(self.dm.pool, self.groups)
+        self.vmap.insert_frames(self.dm.pool, self.slots)
         ev["t_insert"] = self._event()
-        keys, cen, wsum, cnt_v = self.vmap.extract(sort=True)
+        keys, cen, wsum, cnt_v = self.vmap.extract(sort=True, out=self.out)
         ev["t_emit"] = self._event()
         self.n_voxels = int(keys.numel())
         if record is not None:

@@ -146,8 +146,11 @@ EC3R_API int ec3r_umeyama_batched(const double* p, const double* q, const double
  * replaces Submap.world_points / Mapping.fused_cloud (mapping.py:56-57,
  * 332-338) with the declared fusion rule of oracle/fuse.py; keys are
  * _pack(floor(x / cell)) (_kernels/_numpy.py:50-55), bit-exact against the
- * reference's float64 transform.  Open addressing, 64-bit keys, float32
- * accumulators relative to the voxel corner.
+ * reference's float64 transform.  Voxel-block hash: an open-addressing
+ * table of 4x4x4 block keys over a pool of dense blocks holding float32
+ * sums of conf * (x - voxel corner), sum of conf and a uint32 count.
+ * capacity (create) = expected voxels; the pool holds capacity / 8 blocks
+ * and overflow is reported in n_overflow (grow and re-run).
  * ------------------------------------------------------------------- */
 typedef struct ec3r_vhash ec3r_vhash;
 
@@ -165,22 +168,11 @@ EC3R_API int ec3r_vhash_clear(ec3r_vhash* h, void* stream);
 /* Fuse whole frames of the pool: for each listed slot, every pixel with
  * depth > 0 and conf > 0 is inverse-projected with slot_poses[slot]
  * (anchor_from_cam) and mapped to the world by slot_globals[slot] (the
- * owning submap's global Sim(3)); slots_h is a host list of n slot ids. */
+ * owning submap's global Sim(3)); slots is a device list of n slot ids. */
 EC3R_API int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, const float* conf_pool,
                              int H, int W, const double* K4_h, const double* slot_poses,
-                             const double* slot_globals, const int32_t* slots_h, int n,
+                             const double* slot_globals, const int32_t* slots, int n,
                              void* stream);
-/* Same fusion with CTA-level aggregation: slot group g is
- * slots[group_off[g] .. group_off[g+1]) (device arrays); every CTA takes one
- * band of image rows across all frames of a group (frames of one submap, or
- * of neighbouring submaps, see the same surface), accumulates its voxels in
- * shared memory and flushes each distinct voxel to the table once.
- * max_frames_per_group bounds the fixed-point accumulator range. */
-EC3R_API int ec3r_vhash_insert_frame_groups(ec3r_vhash* h, const float* depth_pool,
-                                            const float* conf_pool, int H, int W, const double* K4_h,
-                                            const double* slot_poses, const double* slot_globals,
-                                            const int32_t* slots, const int32_t* group_off, int n_groups,
-                                            int max_frames_per_group, void* stream);
 /* Fuse explicit points (N,3) float64 with conf (N) float64 under sim3_h. */
 EC3R_API int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, const double* conf, int64_t n,
                              const double* sim3_h, void* stream);
@@ -188,16 +180,17 @@ EC3R_API int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, const
 EC3R_API int ec3r_vhash_stats_get(ec3r_vhash* h, ec3r_vhash_stats* out_h, void* stream);
 /* Emit the fused voxels: keys (U) int64 ascending (sorted when sort != 0),
  * centroid (U,3) float32, wsum (U) float32, count (U) int32; *n_out (device
- * int64) = U.  Outputs must hold `capacity` rows (or query
- * ec3r_vhash_count first). */
+ * int64) = U.  Outputs must hold U rows: query ec3r_vhash_count (device
+ * int64) first, or size them for ec3r_vhash_capacity. */
 EC3R_API size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h);
 EC3R_API int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream);
 EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum,
                        int32_t* count, int64_t* n_out, int sort, void* workspace,
                        size_t workspace_bytes, void* stream);
 /* Multi-GPU: emit raw partial sums (key, sum w*dx, sum w, count) bucketed
- * by owner rank = (key range partition) for the all-to-all,
- * and merge received partials into a table. */
+ * by owner rank = hash(key) mod n_ranks for the all-to-all (outputs hold
+ * U rows; workspace = ec3r_vhash_extract_workspace + 1 KB), and merge
+ * received partials into a table. */
 EC3R_API int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* keys, float* sums4,
                                 int32_t* count, int64_t* rank_counts, void* workspace,
                                 size_t workspace_bytes, void* stream);

@@ -39,7 +39,6 @@ _PROTOS = {
     "ec3r_vhash_capacity": (_I64, [_P]),
     "ec3r_vhash_clear": (_I, [_P, _P]),
     "ec3r_vhash_insert_frames": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _I, _P]),
-    "ec3r_vhash_insert_frame_groups": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P]),
     "ec3r_vhash_insert_points": (_I, [_P, _P, _P, _I64, _P, _P]),
     "ec3r_vhash_stats_get": (_I, [_P, _P, _P]),
     "ec3r_vhash_count": (_I, [_P, _P, _P]),

@@ -269,11 +269,16 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         }
     } else {
         // ===================== epilogue (warps 2..9) =====================
-        // warp -> (A block b, TMEM lane quarter q): each thread owns one row.
+        // warp -> (TMEM lane quarter q, column half h).  Each thread owns two
+        // rows — row q*32+lane of both A blocks — over the tile's 64 columns
+        // [h*64, h*64+64): the two values of a column are folded in-thread
+        // (max / min) before the warp reductions, halving the CREDUX count.
+        // Column keys embed (block, lane) in their 6 low bits.
         const int q = warp & 3;
-        const int b = (warp - 2) >> 2;
-        const int et = threadIdx.x - 64;       // 0..255
-        const uint32_t lane_code = 31u - (uint32_t)lane;
+        const int h = (warp - 2) >> 2;
+        const int et = threadIdx.x - 64;  // 0..255
+        const uint32_t code0 = 63u - (uint32_t)lane;        // block 0 (preferred on equal keys: smaller row)
+        const uint32_t code1 = 31u - (uint32_t)lane;        // block 1
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -282,70 +287,89 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (M + TC_BN - 1) / TC_BN;
-            float tk[TC_TOPK];
-            int ck[TC_TOPK];
+            float tk0[TC_TOPK], tk1[TC_TOPK];
+            int ck0[TC_TOPK], ck1[TC_TOPK];
 #pragma unroll
-            for (int k = 0; k < TC_TOPK; ++k) { tk[k] = -INFINITY; ck[k] = -1; }
-            const int64_t my_row = (int64_t)un.y + b * TC_BM + q * 32 + lane;
-            const bool rvalid = my_row < a1;
+            for (int k = 0; k < TC_TOPK; ++k) { tk0[k] = tk1[k] = -INFINITY; ck0[k] = ck1[k] = -1; }
+            const int64_t row0 = (int64_t)un.y + q * 32 + lane, row1 = row0 + TC_BM;
+            const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
                 const int col0 = t * TC_BN;
 #pragma unroll 1
-                for (int ch = 0; ch < TC_BN / 32; ++ch) {
-                    uint32_t r[32];
-                    tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + b * TC_BN + ch * 32),
-                              r);
-                    const int cbase = col0 + ch * 32;
-                    const int nvalid = rvalid ? min(32, M - cbase) : 0;  // valid columns of this thread
-                    // row side: running top-3 (rarely taken after the first tiles)
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int cl = h * 64 + ch * 32;  // column offset within the tile
+                    uint32_t r0[32], r1[32];
+                    const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + cl);
+                    tmem_ld32(ta, r0);
+                    tmem_ld32(ta + TC_BN, r1);
+                    const int cbase = col0 + cl;
+                    const int ncol = min(32, M - cbase);  // valid columns (may be <= 0)
+                    const int nv0 = rv0 ? ncol : 0, nv1 = rv1 ? ncol : 0;
+                    // row side: chunk max pre-filter, rare insertion
+                    float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const float v = __uint_as_float(r[j]);
-                        if (j < nvalid && v > tk[TC_TOPK - 1]) top4_insert(v, cbase + j, tk, ck);
+                        mx0 = fmaxf(mx0, j < nv0 ? __uint_as_float(r0[j]) : -INFINITY);
+                        mx1 = fmaxf(mx1, j < nv1 ? __uint_as_float(r1[j]) : -INFINITY);
                     }
-                    // column side: 32 independent warp reductions (keys embed the lane)
-                    uint32_t key[32], m[32];
+                    if (mx0 > tk0[TC_TOPK - 1]) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        key[j] = (j < nvalid) ? ((__float_as_uint(__uint_as_float(r[j]) + p.bias) & 0xFFFFFFE0u) | lane_code)
-                                              : 0u;
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __uint_as_float(r0[j]);
+                            if (j < nv0 && v > tk0[TC_TOPK - 1]) top4_insert(v, cbase + j, tk0, ck0);
+                        }
+                    }
+                    if (mx1 > tk1[TC_TOPK - 1]) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) m[j] = __reduce_max_sync(0xffffffffu, key[j]);
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __uint_as_float(r1[j]);
+                            if (j < nv1 && v > tk1[TC_TOPK - 1]) top4_insert(v, cbase + j, tk1, ck1);
+                        }
+                    }
+                    // column side: per column fold the thread's two rows, then
+                    // top-1 and top-2 over the warp's 64 rows
                     uint32_t cm = 0, cm2 = 0;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, key[j] == m[j] ? 0u : key[j]);
-                        cm = (lane == j) ? m[j] : cm;
+                        const uint32_t k0 =
+                            j < nv0 ? ((__float_as_uint(__uint_as_float(r0[j]) + p.bias) & 0xFFFFFFC0u) | code0) : 0u;
+                        const uint32_t k1 =
+                            j < nv1 ? ((__float_as_uint(__uint_as_float(r1[j]) + p.bias) & 0xFFFFFFC0u) | code1) : 0u;
+                        const uint32_t hi = max(k0, k1), lo = min(k0, k1);
+                        const uint32_t m = __reduce_max_sync(0xffffffffu, hi);
+                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, hi == m ? lo : hi);
+                        cm = (lane == j) ? m : cm;
                         cm2 = (lane == j) ? m2 : cm2;
                     }
-                    colbuf[(b * 4 + q) * TC_BN + ch * 32 + lane] = make_uint2(cm, cm2);
+                    colbuf[q * TC_BN + cl + lane] = make_uint2(cm, cm2);
                 }
                 // accumulator drained: hand the TMEM buffer back to the MMA warp
                 tc_fence_before();
                 mbar_arrive(t_empty + acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 named_sync(1, TC_EPI_THREADS);
-                // merge the 8 partials of column et and fold into the global state
+                // merge the 4 quarter partials of column et and fold into the global state
                 if (et < TC_BN && col0 + et < M) {
                     unsigned long long best = 0;
                     uint32_t second = 0;
 #pragma unroll
-                    for (int pp = 0; pp < TC_NA * 4; ++pp) {
-                        const uint2 c = colbuf[pp * TC_BN + et];
+                    for (int qq = 0; qq < 4; ++qq) {
+                        const uint2 c = colbuf[qq * TC_BN + et];
                         if (c.x == 0) continue;
-                        const int bb = pp >> 2, qq = pp & 3;
-                        const int lanew = 31 - (int)(c.x & 31u);
+                        const uint32_t code = c.x & 63u;
+                        const int bb = code >= 32 ? 0 : 1;
+                        const int lanew = (bb == 0 ? 63 : 31) - (int)code;
                         const int64_t row = (int64_t)un.y - a0 + bb * TC_BM + qq * 32 + lanew;
                         const unsigned long long gk =
-                            ((unsigned long long)(c.x & 0xFFFFFFE0u) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
-                        const uint32_t c2v = c.y & 0xFFFFFFE0u;
+                            ((unsigned long long)(c.x & 0xFFFFFFC0u) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
+                        const uint32_t c2v = c.y & 0xFFFFFFC0u;
                         if (gk > best) {
                             second = max(second, max(c2v, (uint32_t)(best >> 32)));
                             best = gk;
                         } else {
-                            second = max(second, c.x & 0xFFFFFFE0u);
+                            second = max(second, c.x & 0xFFFFFFC0u);
                         }
                     }
                     if (best) {
@@ -358,11 +382,17 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 }
                 named_sync(1, TC_EPI_THREADS);
             }
-            if (rvalid) {
+            if (rv0) {
                 RowCand rc;
 #pragma unroll
-                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk[k]; rc.c[k] = ck[k]; }
-                p.cand[my_row] = rc;
+                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk0[k]; rc.c[k] = ck0[k]; }
+                p.cand[row0] = rc;
+            }
+            if (rv1) {
+                RowCand rc;
+#pragma unroll
+                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk1[k]; rc.c[k] = ck1[k]; }
+                p.cand[row1] = rc;
             }
         }
     }
@@ -704,7 +734,8 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
     const float bias = (float)fmax(2.0, 2.0 * Bn);
     double eps_row = ldexp(Bn, -14);
     if (exact_dtype != 0) eps_row += ldexp(Bn, -7);
-    const double eps_col = eps_row + ldexp(2.0 * ((double)bias + Bn), -18);
+    // column keys drop 6 low mantissa bits (64 ulps of a value < 2 (bias + Bn))
+    const double eps_col = eps_row + ldexp(2.0 * ((double)bias + Bn), -17);
     CUtensorMap tmA, tmB;
     if (!make_map(&tmA, A, ta, D) || !make_map(&tmB, B, tb, D)) {
         set_last_error_msg("cuTensorMapEncodeTiled failed");

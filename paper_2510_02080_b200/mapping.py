@@ -197,7 +197,8 @@ class VoxelMap:
         _lib.check(L.ec3r_vhash_create(C.byref(h), int(capacity), self.cell, _lib.stream_ptr(stream)),
                    "ec3r_vhash_create")
         self._h = h
-        self.capacity = int(L.ec3r_vhash_capacity(h))
+        self.capacity = int(L.ec3r_vhash_capacity(h))  # voxel slots of the block pool
+        self.expected = int(capacity)
         self._n = torch.zeros(1, dtype=torch.int64, device="cuda")
 
     def __del__(self):
@@ -225,14 +226,6 @@ class VoxelMap:
                                                        _lib.ptr(pool.globals), _lib.ptr(slots), int(slots.numel()),
                                                        _lib.stream_ptr(stream)), "ec3r_vhash_insert_frames")
 
-    def insert_groups(self, pool: FramePool, groups: "SlotGroups", stream=None):
-        """Aggregated insertion (ec3r_vhash_insert_frame_groups)."""
-        K4 = np.ascontiguousarray(pool.K4)
-        _lib.check(_lib.lib().ec3r_vhash_insert_frame_groups(
-            self._h, _lib.ptr(pool.depth), _lib.ptr(pool.conf), pool.H, pool.W, K4.ctypes.data,
-            _lib.ptr(pool.poses), _lib.ptr(pool.globals), _lib.ptr(groups.slots), _lib.ptr(groups.offsets),
-            groups.n_groups, groups.max_frames, _lib.stream_ptr(stream)), "ec3r_vhash_insert_frame_groups")
-
     def insert_points(self, points: torch.Tensor, conf: torch.Tensor, sim3_vec, stream=None):
         g = np.ascontiguousarray(np.asarray(sim3_vec, np.float64))
         _lib.check(_lib.lib().ec3r_vhash_insert_points(self._h, _lib.ptr(points), _lib.ptr(conf),
@@ -246,12 +239,19 @@ class VoxelMap:
         return dict(n_points_in=s.n_points_in, n_out_of_range=s.n_out_of_range, n_overflow=s.n_overflow,
                     n_slow_path=s.n_slow_path)
 
+    def count(self, stream=None) -> int:
+        """Number of fused voxels U (synchronises)."""
+        _lib.check(_lib.lib().ec3r_vhash_count(self._h, _lib.ptr(self._n), _lib.stream_ptr(stream)),
+                   "ec3r_vhash_count")
+        return int(self._n.item())
+
     def extract(self, sort: bool = True, stream=None, out=None):
         """Returns (keys int64, centroid (U,3) f32, wsum f32, count i32) CUDA
-        tensors of length U (sorted by key when sort=True)."""
+        tensors of length U (sorted by key when sort=True).  `out` may hold
+        preallocated buffers of at least U rows."""
         L = _lib.lib()
-        cap = self.capacity
         if out is None:
+            cap = self.count(stream)
             out = (torch.empty(cap, dtype=torch.int64, device="cuda"),
                    torch.empty((cap, 3), dtype=torch.float32, device="cuda"),
                    torch.empty(cap, dtype=torch.float32, device="cuda"),
@@ -266,38 +266,21 @@ class VoxelMap:
         return keys[:U], cen[:U], ws_[:U], cnt[:U]
 
 
-class SlotGroups:
-    """Slot groups for aggregated fusion: consecutive submaps (which see the
-    same surface) are fused by the same CTAs."""
-
-    def __init__(self, sms: Sequence, submaps_per_group: int = 2, device="cuda"):
-        slots, off = [], [0]
-        sms = list(sms)
-        for i in range(0, len(sms), submaps_per_group):
-            for sm in sms[i:i + submaps_per_group]:
-                slots.extend(int(s) for s in sm.slots)
-            off.append(len(slots))
-        self.slots = torch.as_tensor(np.asarray(slots, np.int32), device=device)
-        self.offsets = torch.as_tensor(np.asarray(off, np.int32), device=device)
-        self.n_groups = len(off) - 1
-        self.max_frames = int(max(np.diff(off))) if self.n_groups else 1
-
-
-def fuse_slots(pool: FramePool, groups, cell: float, vmap: Optional[VoxelMap] = None,
+def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional[VoxelMap] = None,
                expected_voxels: Optional[int] = None, sort: bool = True):
-    """Voxel fusion of pool slot groups with overflow-safe capacity growth.
+    """Voxel fusion of pool slots with overflow-safe capacity growth.
     Returns (VoxelMap, (keys, centroid, wsum, count), stats)."""
     if vmap is None or vmap.cell != cell:
-        n_px = int(groups.slots.numel()) * pool.H * pool.W
+        n_px = int(slots.numel()) * pool.H * pool.W
         cap = expected_voxels * 2 if expected_voxels else max(1 << 16, n_px // 8)
         vmap = VoxelMap(cell, cap)
     while True:
         vmap.clear()
-        vmap.insert_groups(pool, groups)
+        vmap.insert_frames(pool, slots)
         st = vmap.stats()
         if st["n_overflow"] == 0:
             break
-        vmap = VoxelMap(cell, vmap.capacity * 4)
+        vmap = VoxelMap(cell, vmap.expected * 4)
     return vmap, vmap.extract(sort=sort), st
 
 
@@ -454,9 +437,8 @@ class DenseMapping:
             if not pts:
                 return np.zeros((0, 3)), np.zeros(0)
             return torch.cat(pts).cpu().numpy(), torch.cat(cfs).cpu().numpy()
-        groups = SlotGroups(list(self.submaps.values()), 2, self.pool.device)
-        self._vmap, (k, c, w, n), st = fuse_slots(self.pool, groups, float(voxel), self._vmap, self._last_voxels,
-                                                  sort)
+        self._vmap, (k, c, w, n), st = fuse_slots(self.pool, self.all_slots(), float(voxel), self._vmap,
+                                                  self._last_voxels, sort)
         self._last_voxels = int(k.numel())
         return dict(keys=k.cpu().numpy(), centroid=c.cpu().numpy(), wsum=w.cpu().numpy(), count=n.cpu().numpy(),
                     stats=st)

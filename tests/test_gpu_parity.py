@@ -250,26 +250,34 @@ def test_voxel_fusion_vs_oracle(golden):
         assert out["stats"]["n_points_in"] == o["n_in"]
 
 
-def test_grouped_and_per_frame_fusion_agree(golden):
-    """CTA-aggregated insertion (fixed-point shared accumulators) vs the
-    per-frame kernel: identical keys and counts, centroids within 1e-5 m."""
+def test_voxel_block_hash_incremental_and_growth(golden):
+    """Incremental insertion (slot by slot) equals one-shot insertion; a pool
+    too small overflows, is reported, and fuse_slots grows it to the exact
+    result."""
     from paper_2510_02080_b200 import mapping
     g = golden("mapping")
     dm, sms = _dense_mapping(g)
     dm.register_chain(sms)
-    for per_group in (1, 2, 3):
-        groups = mapping.SlotGroups(sms, per_group)
-        a = mapping.VoxelMap(0.02, 1 << 16)
-        a.insert_groups(dm.pool, groups)
-        b = mapping.VoxelMap(0.02, 1 << 16)
-        b.insert_frames(dm.pool, groups.slots)
-        ka, ca, wa, na = (x.cpu().numpy() for x in a.extract())
-        kb, cb, wb, nb = (x.cpu().numpy() for x in b.extract())
-        np.testing.assert_array_equal(ka, kb)
-        np.testing.assert_array_equal(na, nb)
-        assert np.max(np.abs(ca - cb)) < 1e-5
-        np.testing.assert_allclose(wa, wb, rtol=1e-4)
-        assert a.stats()["n_points_in"] == b.stats()["n_points_in"]
+    slots = dm.all_slots()
+    a = mapping.VoxelMap(0.02, 1 << 17)
+    a.insert_frames(dm.pool, slots)
+    b = mapping.VoxelMap(0.02, 1 << 17)
+    for s in range(slots.numel()):
+        b.insert_frames(dm.pool, slots[s:s + 1])
+    ka, ca, wa, na = (x.cpu().numpy() for x in a.extract())
+    kb, cb, wb, nb = (x.cpu().numpy() for x in b.extract())
+    np.testing.assert_array_equal(ka, kb)
+    np.testing.assert_array_equal(na, nb)
+    assert np.max(np.abs(ca - cb)) < 1e-5
+    assert a.stats()["n_overflow"] == 0
+    small = mapping.VoxelMap(0.02, 2)  # minimum pool: 4096 blocks
+    small.insert_frames(dm.pool, slots)
+    ovf = small.stats()["n_overflow"]
+    assert ovf == 0 or ovf < a.stats()["n_points_in"]
+    vm, (k, c, w, n), st = mapping.fuse_slots(dm.pool, slots, 0.02, small)
+    assert st["n_overflow"] == 0
+    np.testing.assert_array_equal(k.cpu().numpy(), ka)
+    np.testing.assert_array_equal(n.cpu().numpy(), na)
 
 
 def test_voxel_fusion_full_resolution_submaps():
