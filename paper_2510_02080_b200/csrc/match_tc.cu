@@ -307,40 +307,67 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     const int cbase = col0 + cl;
                     const int ncol = min(32, M - cbase);  // valid columns (may be <= 0)
                     const int nv0 = rv0 ? ncol : 0, nv1 = rv1 ? ncol : 0;
-                    // row side: chunk max pre-filter, rare insertion
-                    float mx0 = -INFINITY, mx1 = -INFINITY;
+                    // interior chunks (every row and column valid) skip all
+                    // per-element predicates: warp-uniform fast path
+                    const bool full = __all_sync(0xffffffffu, nv0 == 32 && nv1 == 32);
+                    if (!full) {
+                        // invalid entries become -bias: below every real value
+                        // (|sim| <= bias / 2) and mapping to a zero-value key
+                        const uint32_t sentinel = __float_as_uint(-p.bias);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        mx0 = fmaxf(mx0, j < nv0 ? __uint_as_float(r0[j]) : -INFINITY);
-                        mx1 = fmaxf(mx1, j < nv1 ? __uint_as_float(r1[j]) : -INFINITY);
+                        for (int j = 0; j < 32; ++j) {
+                            if (j >= nv0) r0[j] = sentinel;
+                            if (j >= nv1) r1[j] = sentinel;
+                        }
                     }
+                    // row side: chunk max (tree) pre-filter, rare insertion
+                    float t0[16], t1v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        t0[j] = fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 16]));
+                        t1v[j] = fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 16]));
+                    }
+#pragma unroll
+                    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                        for (int j = 0; j < w; ++j) {
+                            t0[j] = fmaxf(t0[j], t0[j + w]);
+                            t1v[j] = fmaxf(t1v[j], t1v[j + w]);
+                        }
+                    const float mx0 = t0[0], mx1 = t1v[0];
                     if (mx0 > tk0[TC_TOPK - 1]) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const float v = __uint_as_float(r0[j]);
-                            if (j < nv0 && v > tk0[TC_TOPK - 1]) top4_insert(v, cbase + j, tk0, ck0);
+                            if (v > tk0[TC_TOPK - 1]) top4_insert(v, cbase + j, tk0, ck0);
                         }
                     }
                     if (mx1 > tk1[TC_TOPK - 1]) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const float v = __uint_as_float(r1[j]);
-                            if (j < nv1 && v > tk1[TC_TOPK - 1]) top4_insert(v, cbase + j, tk1, ck1);
+                            if (v > tk1[TC_TOPK - 1]) top4_insert(v, cbase + j, tk1, ck1);
                         }
                     }
                     // column side: per column fold the thread's two rows, then
-                    // top-1 and top-2 over the warp's 64 rows
+                    // top-1 and top-2 over the warp's 64 rows.  Invalid entries
+                    // (-bias) map to zero-value keys.  All 32 first reductions
+                    // are issued before the dependent second ones.
+                    uint32_t hi[32], lo[32], m[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t k0 = (__float_as_uint(__uint_as_float(r0[j]) + p.bias) & 0xFFFFFFC0u) | code0;
+                        const uint32_t k1 = (__float_as_uint(__uint_as_float(r1[j]) + p.bias) & 0xFFFFFFC0u) | code1;
+                        hi[j] = max(k0, k1);
+                        lo[j] = min(k0, k1);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) m[j] = __reduce_max_sync(0xffffffffu, hi[j]);
                     uint32_t cm = 0, cm2 = 0;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const uint32_t k0 =
-                            j < nv0 ? ((__float_as_uint(__uint_as_float(r0[j]) + p.bias) & 0xFFFFFFC0u) | code0) : 0u;
-                        const uint32_t k1 =
-                            j < nv1 ? ((__float_as_uint(__uint_as_float(r1[j]) + p.bias) & 0xFFFFFFC0u) | code1) : 0u;
-                        const uint32_t hi = max(k0, k1), lo = min(k0, k1);
-                        const uint32_t m = __reduce_max_sync(0xffffffffu, hi);
-                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, hi == m ? lo : hi);
-                        cm = (lane == j) ? m : cm;
+                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, hi[j] == m[j] ? lo[j] : hi[j]);
+                        cm = (lane == j) ? m[j] : cm;
                         cm2 = (lane == j) ? m2 : cm2;
                     }
                     colbuf[q * TC_BN + cl + lane] = make_uint2(cm, cm2);
@@ -357,14 +384,14 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
                         const uint2 c = colbuf[qq * TC_BN + et];
-                        if (c.x == 0) continue;
+                        if ((c.x & 0xFFFFFFC0u) == 0) continue;  // no valid row in this quarter
                         const uint32_t code = c.x & 63u;
                         const int bb = code >= 32 ? 0 : 1;
                         const int lanew = (bb == 0 ? 63 : 31) - (int)code;
                         const int64_t row = (int64_t)un.y - a0 + bb * TC_BM + qq * 32 + lanew;
                         const unsigned long long gk =
                             ((unsigned long long)(c.x & 0xFFFFFFC0u) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
-                        const uint32_t c2v = c.y & 0xFFFFFFC0u;
+                        const uint32_t c2v = c.y & 0xFFFFFFC0u;  // zero-value keys contribute 0
                         if (gk > best) {
                             second = max(second, max(c2v, (uint32_t)(best >> 32)));
                             best = gk;
@@ -382,18 +409,42 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 }
                 named_sync(1, TC_EPI_THREADS);
             }
-            if (rv0) {
-                RowCand rc;
+            // the two column-half warps of a quarter hold partial top-4 lists
+            // of the same rows: h = 1 hands its lists over (colbuf is free)
+            RowCand* rsc = reinterpret_cast<RowCand*>(colbuf);
+            const int ti = q * 32 + lane;
+            if (h == 1) {
+                RowCand a, b;
 #pragma unroll
-                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk0[k]; rc.c[k] = ck0[k]; }
-                p.cand[row0] = rc;
+                for (int k = 0; k < TC_TOPK; ++k) {
+                    a.v[k] = tk0[k]; a.c[k] = ck0[k];
+                    b.v[k] = tk1[k]; b.c[k] = ck1[k];
+                }
+                rsc[ti] = a;
+                rsc[TC_BM + ti] = b;
             }
-            if (rv1) {
-                RowCand rc;
+            named_sync(1, TC_EPI_THREADS);
+            if (h == 0) {
+                const RowCand a = rsc[ti], b = rsc[TC_BM + ti];
 #pragma unroll
-                for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk1[k]; rc.c[k] = ck1[k]; }
-                p.cand[row1] = rc;
+                for (int k = 0; k < TC_TOPK; ++k) {
+                    if (a.c[k] >= 0 && a.v[k] > tk0[TC_TOPK - 1]) top4_insert(a.v[k], a.c[k], tk0, ck0);
+                    if (b.c[k] >= 0 && b.v[k] > tk1[TC_TOPK - 1]) top4_insert(b.v[k], b.c[k], tk1, ck1);
+                }
+                if (rv0) {
+                    RowCand rc;
+#pragma unroll
+                    for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk0[k]; rc.c[k] = ck0[k]; }
+                    p.cand[row0] = rc;
+                }
+                if (rv1) {
+                    RowCand rc;
+#pragma unroll
+                    for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk1[k]; rc.c[k] = ck1[k]; }
+                    p.cand[row1] = rc;
+                }
             }
+            named_sync(1, TC_EPI_THREADS);
         }
     }
     tc_fence_before();

@@ -43,6 +43,7 @@ struct __align__(16) BlockEntry {
 }  // namespace ec3r
 
 struct ec3r_vhash {
+    int64_t max_voxels;  // emit capacity
     int64_t max_blocks;
     unsigned long long tmask;
     double cell;
@@ -383,11 +384,13 @@ __global__ void vh_insert_points_kernel(const double* __restrict__ pts, const do
 // extraction
 
 // Compact voxels with a non-zero count: (voxel key, pool index).
+// At most max_voxels are emitted; the excess is counted in counters[5]
+// (reported as overflow: the caller grows the handle and re-runs).
 __global__ void vb_compact_kernel(const unsigned int* __restrict__ counts,
                                   const unsigned long long* __restrict__ block_keys,
-                                  const unsigned long long* __restrict__ counters, int64_t max_blocks,
-                                  unsigned long long* __restrict__ keys, int64_t* __restrict__ idx,
-                                  unsigned long long* __restrict__ cursor) {
+                                  unsigned long long* __restrict__ counters, int64_t max_blocks,
+                                  int64_t max_voxels, unsigned long long* __restrict__ keys,
+                                  int64_t* __restrict__ idx, unsigned long long* __restrict__ cursor) {
     const int64_t n = min((int64_t)counters[4], max_blocks) * kBlockVox;
     const int lane = threadIdx.x & 31;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
@@ -399,6 +402,10 @@ __global__ void vb_compact_kernel(const unsigned int* __restrict__ counts,
         base = __shfl_sync(0xffffffffu, base, 0);
         if (occ) {
             const unsigned long long o = base + __popc(m & ((1u << lane) - 1u));
+            if ((int64_t)o >= max_voxels) {
+                atomicAdd(&counters[5], 1ull);
+                continue;
+            }
             long long bx, by, bz;
             unpack_cells(block_keys[i / kBlockVox], bx, by, bz);
             const int local = (int)(i % kBlockVox);
@@ -478,9 +485,15 @@ static unsigned grid_for(int64_t n) {
 }
 
 // compact + (optional) sort; n_out receives U, returns the arrays to gather from
+__global__ void clamp_count_kernel(const unsigned long long* __restrict__ cursor, int64_t cap,
+                                   int64_t* __restrict__ n_out) {
+    const int64_t c = (int64_t)*cursor;
+    *n_out = c < cap ? c : cap;
+}
+
 static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t workspace_bytes, int64_t* n_out,
                           const unsigned long long** ks, const int64_t** is, cudaStream_t st) {
-    const size_t cap = (size_t)h->max_blocks * kBlockVox;
+    const size_t cap = (size_t)h->max_voxels;
     Carver cv{(char*)workspace, 0};
     unsigned long long* k0 = cv.take<unsigned long long>(cap);
     int64_t* i0 = cv.take<int64_t>(cap);
@@ -490,16 +503,18 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
     size_t cub_bytes = workspace_bytes - cv.used;
     void* cub_tmp = cv.base + cv.used;
     EC3R_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
-    vb_compact_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->counts, h->block_keys, h->counters, h->max_blocks, k0, i0,
-                                                   cursor);
+    vb_compact_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->counts, h->block_keys, h->counters, h->max_blocks,
+                                                   h->max_voxels, k0, i0, cursor);
     EC3R_CHECK_LAUNCH("vb_compact_kernel");
-    EC3R_CUDA_TRY(cudaMemcpyAsync(n_out, cursor, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    clamp_count_kernel<<<1, 1, 0, st>>>(cursor, h->max_voxels, n_out);
+    EC3R_CHECK_LAUNCH("clamp_count_kernel");
     *ks = k0;
     *is = i0;
     if (sort) {
         unsigned long long nh = 0;
         EC3R_CUDA_TRY(cudaMemcpyAsync(&nh, cursor, sizeof(nh), cudaMemcpyDeviceToHost, st));
         EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        if ((int64_t)nh > h->max_voxels) nh = (unsigned long long)h->max_voxels;
         if (nh > 0) {
             if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k0, k1, i0, i1, (int)nh, 0, 63, st) !=
                 cudaSuccess) {
@@ -520,8 +535,11 @@ using namespace ec3r;
 extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream) {
     if (!out || capacity < 2 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
-    // capacity = expected voxels; surface blocks hold >= ~8 of their 64 voxels
-    h->max_blocks = capacity / 8 > 4096 ? capacity / 8 : 4096;
+    // capacity = voxels to emit at most; the pool holds capacity / 4 blocks
+    // (surface blocks are far fuller than 4 of 64 voxels; sparse inputs
+    // overflow, are reported and re-run on a larger handle)
+    h->max_voxels = capacity > 65536 ? capacity : 65536;
+    h->max_blocks = capacity / 4 > 4096 ? capacity / 4 : 4096;
     int64_t tcap = 1;
     while (tcap < 2 * h->max_blocks) tcap <<= 1;
     h->tmask = (unsigned long long)(tcap - 1);
@@ -557,7 +575,7 @@ extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {
     return EC3R_OK;
 }
 
-extern "C" int64_t ec3r_vhash_capacity(const ec3r_vhash* h) { return h ? h->max_blocks * kBlockVox : 0; }
+extern "C" int64_t ec3r_vhash_capacity(const ec3r_vhash* h) { return h ? h->max_voxels : 0; }
 
 extern "C" int ec3r_vhash_clear(ec3r_vhash* h, void* stream) {
     if (!h) return EC3R_EARG;
@@ -611,7 +629,7 @@ extern "C" int ec3r_vhash_stats_get(ec3r_vhash* h, ec3r_vhash_stats* out_h, void
     EC3R_CUDA_TRY(cudaStreamSynchronize(st));
     out_h->n_points_in = (int64_t)c[0];
     out_h->n_out_of_range = (int64_t)c[1];
-    out_h->n_overflow = (int64_t)c[2];
+    out_h->n_overflow = (int64_t)(c[2] + c[5]);  // dropped points + voxels beyond the emit capacity
     out_h->n_slow_path = (int64_t)c[3];
     return EC3R_OK;
 }
@@ -638,7 +656,7 @@ extern "C" int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream) {
 
 extern "C" size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h) {
     if (!h) return 0;
-    const size_t cap = (size_t)h->max_blocks * kBlockVox;
+    const size_t cap = (size_t)h->max_voxels;
     size_t cub_bytes = 0;
     cub::DeviceRadixSort::SortPairs<unsigned long long, int64_t>(nullptr, cub_bytes, (unsigned long long*)nullptr,
                                                                  (unsigned long long*)nullptr, (int64_t*)nullptr,

@@ -279,9 +279,12 @@ def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional
         vmap.insert_frames(pool, slots)
         st = vmap.stats()
         if st["n_overflow"] == 0:
-            break
+            out = vmap.extract(sort=sort)
+            st = vmap.stats()  # the emit may overflow the voxel capacity too
+            if st["n_overflow"] == 0:
+                break
         vmap = VoxelMap(cell, vmap.expected * 4)
-    return vmap, vmap.extract(sort=sort), st
+    return vmap, out, st
 
 
 class DenseMapping:

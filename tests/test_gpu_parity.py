@@ -259,9 +259,9 @@ def test_voxel_block_hash_incremental_and_growth(golden):
     dm, sms = _dense_mapping(g)
     dm.register_chain(sms)
     slots = dm.all_slots()
-    a = mapping.VoxelMap(0.02, 1 << 17)
+    a = mapping.VoxelMap(0.02, 1 << 19)
     a.insert_frames(dm.pool, slots)
-    b = mapping.VoxelMap(0.02, 1 << 17)
+    b = mapping.VoxelMap(0.02, 1 << 19)
     for s in range(slots.numel()):
         b.insert_frames(dm.pool, slots[s:s + 1])
     ka, ca, wa, na = (x.cpu().numpy() for x in a.extract())
@@ -318,7 +318,7 @@ def test_voxel_points_api_and_extreme_coordinates():
     conf = rng.uniform(0.0, 1.0, size=len(p))
     conf[10:20] = 0.0
     sim = np.concatenate([[1.3], ref.normalize_quat(rng.normal(size=4)), [2000.0, -1500.0, 30.0]])
-    vm = mapping.VoxelMap(0.02, 1 << 18)
+    vm = mapping.VoxelMap(0.02, 1 << 20)  # random points: one voxel per block
     vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"), sim)
     st = vm.stats()
     k, c, w, n = (x.cpu().numpy() for x in vm.extract())
