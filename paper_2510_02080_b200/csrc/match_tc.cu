@@ -86,6 +86,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Same wait for the single-thread producer / MMA roles with a suspend-time
+// hint, so their waits sleep instead of competing for issue slots with the
+// epilogue warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -139,19 +153,6 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
                             ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
-
-// Insert into a descending top-4 (caller has checked v > t[3]); strict >
-// keeps the earlier column on equal values.
-__device__ __forceinline__ void top4_insert(float v, int c, float (&t)[TC_TOPK], int (&ci)[TC_TOPK]) {
-    t[3] = v; ci[3] = c;
-#pragma unroll
-    for (int k = 3; k > 0; --k) {
-        if (t[k] > t[k - 1]) {
-            const float tv = t[k]; t[k] = t[k - 1]; t[k - 1] = tv;
-            const int tc = ci[k]; ci[k] = ci[k - 1]; ci[k - 1] = tc;
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 
@@ -207,7 +208,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 const int2 un = p.units[u];
                 const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
                 const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
-                mbar_wait(a_empty, a_phase ^ 1);
+                mbar_wait_sleep(a_empty, a_phase ^ 1);
                 mbar_expect_tx(a_full, (uint32_t)(TC_NA * KB * TC_BOX_BYTES));
                 for (int b = 0; b < TC_NA; ++b)
                     for (int kb = 0; kb < KB; ++kb)
@@ -216,7 +217,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 a_phase ^= 1;
                 for (int t = 0; t < n_tiles; ++t) {
                     for (int kb = 0; kb < KB; ++kb) {
-                        mbar_wait(b_empty + stage, phase ^ 1);
+                        mbar_wait_sleep(b_empty + stage, phase ^ 1);
                         mbar_expect_tx(b_full + stage, TC_BOX_BYTES);
                         tma_load_2d(sB + (size_t)stage * TC_BOX_BYTES, &tmB, b_full + stage, kb * TC_BK,
                                     (int)(b0 + t * TC_BN));
@@ -237,15 +238,15 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 const int2 un = p.units[u];
                 const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
                 const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
-                mbar_wait(a_full, a_phase);
+                mbar_wait_sleep(a_full, a_phase);
                 a_phase ^= 1;
                 tc_fence_after();
                 for (int t = 0; t < n_tiles; ++t) {
-                    mbar_wait(t_empty + acc, acc_phase ^ 1);
+                    mbar_wait_sleep(t_empty + acc, acc_phase ^ 1);
                     tc_fence_after();
                     const uint32_t d_base = tmem_base + (uint32_t)(acc * TC_NA * TC_BN);
                     for (int kb = 0; kb < KB; ++kb) {
-                        mbar_wait(b_full + stage, phase);
+                        mbar_wait_sleep(b_full + stage, phase);
                         tc_fence_after();
                         const uint32_t bB = sB_addr + (uint32_t)(stage * TC_BOX_BYTES);
 #pragma unroll
@@ -287,10 +288,10 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (M + TC_BN - 1) / TC_BN;
-            float tk0[TC_TOPK], tk1[TC_TOPK];
-            int ck0[TC_TOPK], ck1[TC_TOPK];
-#pragma unroll
-            for (int k = 0; k < TC_TOPK; ++k) { tk0[k] = tk1[k] = -INFINITY; ck0[k] = ck1[k] = -1; }
+            // row state: best value / column and the second value (order
+            // statistic, duplicates count) — all the decision stage needs
+            float b0v = -INFINITY, s0v = -INFINITY, b1v = -INFINITY, s1v = -INFINITY;
+            int b0c = -1, b1c = -1;
             const int64_t row0 = (int64_t)un.y + q * 32 + lane, row1 = row0 + TC_BM;
             const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
@@ -320,34 +321,17 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                             if (j >= nv1) r1[j] = sentinel;
                         }
                     }
-                    // row side: chunk max (tree) pre-filter, rare insertion
-                    float t0[16], t1v[16];
+                    // row side, branch-free: second = max(second, min(v, best));
+                    // strict > keeps the first column on equal values
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        t0[j] = fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 16]));
-                        t1v[j] = fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 16]));
-                    }
-#pragma unroll
-                    for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-                        for (int j = 0; j < w; ++j) {
-                            t0[j] = fmaxf(t0[j], t0[j + w]);
-                            t1v[j] = fmaxf(t1v[j], t1v[j + w]);
-                        }
-                    const float mx0 = t0[0], mx1 = t1v[0];
-                    if (mx0 > tk0[TC_TOPK - 1]) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float v = __uint_as_float(r0[j]);
-                            if (v > tk0[TC_TOPK - 1]) top4_insert(v, cbase + j, tk0, ck0);
-                        }
-                    }
-                    if (mx1 > tk1[TC_TOPK - 1]) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float v = __uint_as_float(r1[j]);
-                            if (v > tk1[TC_TOPK - 1]) top4_insert(v, cbase + j, tk1, ck1);
-                        }
+                    for (int j = 0; j < 32; ++j) {
+                        const float v0 = __uint_as_float(r0[j]), v1 = __uint_as_float(r1[j]);
+                        s0v = fmaxf(s0v, fminf(v0, b0v));
+                        b0c = v0 > b0v ? cbase + j : b0c;
+                        b0v = fmaxf(b0v, v0);
+                        s1v = fmaxf(s1v, fminf(v1, b1v));
+                        b1c = v1 > b1v ? cbase + j : b1c;
+                        b1v = fmaxf(b1v, v1);
                     }
                     // column side: per column fold the thread's two rows, then
                     // top-1 and top-2 over the warp's 64 rows.  Invalid entries
@@ -409,38 +393,37 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 }
                 named_sync(1, TC_EPI_THREADS);
             }
-            // the two column-half warps of a quarter hold partial top-4 lists
-            // of the same rows: h = 1 hands its lists over (colbuf is free)
-            RowCand* rsc = reinterpret_cast<RowCand*>(colbuf);
+            // the two column-half warps of a quarter hold partial states of
+            // the same rows: h = 1 hands its (best, column, second) over
+            float4* rsc = reinterpret_cast<float4*>(colbuf);
             const int ti = q * 32 + lane;
             if (h == 1) {
-                RowCand a, b;
-#pragma unroll
-                for (int k = 0; k < TC_TOPK; ++k) {
-                    a.v[k] = tk0[k]; a.c[k] = ck0[k];
-                    b.v[k] = tk1[k]; b.c[k] = ck1[k];
-                }
-                rsc[ti] = a;
-                rsc[TC_BM + ti] = b;
+                rsc[ti] = make_float4(b0v, __int_as_float(b0c), s0v, 0.f);
+                rsc[TC_BM + ti] = make_float4(b1v, __int_as_float(b1c), s1v, 0.f);
             }
             named_sync(1, TC_EPI_THREADS);
             if (h == 0) {
-                const RowCand a = rsc[ti], b = rsc[TC_BM + ti];
-#pragma unroll
-                for (int k = 0; k < TC_TOPK; ++k) {
-                    if (a.c[k] >= 0 && a.v[k] > tk0[TC_TOPK - 1]) top4_insert(a.v[k], a.c[k], tk0, ck0);
-                    if (b.c[k] >= 0 && b.v[k] > tk1[TC_TOPK - 1]) top4_insert(b.v[k], b.c[k], tk1, ck1);
-                }
+                const float4 o0 = rsc[ti], o1 = rsc[TC_BM + ti];
+                // merge two (best, column, second) summaries; h = 0 holds the
+                // smaller columns of every tile only per tile, so ties go to
+                // the smaller column explicitly
+                auto merge = [](float& bv, int& bc, float& sv, float ov, int oc, float os) {
+                    const bool take = ov > bv || (ov == bv && oc >= 0 && (bc < 0 || oc < bc));
+                    sv = fmaxf(fminf(bv, ov), fmaxf(sv, os));
+                    if (take) { bv = ov; bc = oc; }
+                };
+                merge(b0v, b0c, s0v, o0.x, __float_as_int(o0.y), o0.z);
+                merge(b1v, b1c, s1v, o1.x, __float_as_int(o1.y), o1.z);
                 if (rv0) {
                     RowCand rc;
-#pragma unroll
-                    for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk0[k]; rc.c[k] = ck0[k]; }
+                    rc.v[0] = b0v; rc.v[1] = s0v; rc.v[2] = rc.v[3] = -INFINITY;
+                    rc.c[0] = b0c; rc.c[1] = rc.c[2] = rc.c[3] = -1;
                     p.cand[row0] = rc;
                 }
                 if (rv1) {
                     RowCand rc;
-#pragma unroll
-                    for (int k = 0; k < TC_TOPK; ++k) { rc.v[k] = tk1[k]; rc.c[k] = ck1[k]; }
+                    rc.v[0] = b1v; rc.v[1] = s1v; rc.v[2] = rc.v[3] = -INFINITY;
+                    rc.c[0] = b1c; rc.c[1] = rc.c[2] = rc.c[3] = -1;
                     p.cand[row1] = rc;
                 }
             }
@@ -500,7 +483,7 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
             s.ratio_ok = 1;  // ratio test skipped for a single column (tracking.py:165)
         } else {
             const double a2 = c.v[1];
-            if (c.c[0] >= 0 && c.c[1] >= 0 && a1 - a2 > 2.0 * eps && a2 + eps < 1.0) {
+            if (c.c[0] >= 0 && a1 - a2 > 2.0 * eps && a2 + eps < 1.0) {
                 const double d1_lo = d2c(a1 + eps), d1_hi = d2c(a1 - eps);
                 const double s_lo = d2c(a2 + eps), s_hi = d2c(a2 - eps);
                 if (d1_lo > ratio2 * s_hi) { decided = true; s.ratio_ok = 0; }
@@ -509,8 +492,9 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
             }
         }
     }
+    // undecided rows (~0.1-1%) go straight to the float64 full-row re-scan
     if (decided) rs[r] = s;
-    else pending[atomicAdd((unsigned long long*)&counters[2], 1ull)] = (int32_t)r;
+    else pending[atomicAdd((unsigned long long*)&counters[0], 1ull)] = (int32_t)r;
 }
 
 // Column side, stage 1: argmax certain when the best (quantised) key beats
@@ -538,58 +522,6 @@ __global__ void mt_decide_cols(const int64_t* __restrict__ a_off, const int64_t*
     }
     if (ok) col_best[c] = (int32_t)r1;
     else pending[atomicAdd((unsigned long long*)&counters[3], 1ull)] = (int32_t)c;
-}
-
-// Stage 2 (one warp per pending row): candidates c1..c3 re-scored in float64;
-// certified when every non-candidate column (sim <= v[3] + eps) is provably
-// worse than the second best candidate in clamped d2, else listed for the
-// full re-scan.
-template <typename T>
-__global__ void mt_certify_rows(const T* __restrict__ A, const T* __restrict__ B, int D,
-                                const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                                const int32_t* __restrict__ pending, const RowCand* __restrict__ cand, double eps,
-                                MatchRowState* __restrict__ rs, int32_t* __restrict__ flag_rows,
-                                int64_t* __restrict__ counters) {
-    const int lane = threadIdx.x & 31;
-    const int64_t n_pend = counters[2];
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_pend;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t r = pending[t];
-    const int p = pair_of(a_off, n_pairs, r);
-    const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
-    const RowCand c = cand[r];
-    const int nc = (int)(M < 3 ? M : 3);  // candidates to re-score
-    bool ok = true;
-    double d[3];
-    int ci[3];
-    for (int k = 0; k < nc; ++k) {
-        ci[k] = c.c[k];
-        ok = ok && ci[k] >= 0;
-        d[k] = ok ? d2x(warp_dot16<T>(A + r * D, B + (b0 + ci[k]) * D, D, lane)) : INFINITY;
-    }
-    // order the candidates by (d2, column): insertion sort of <= 3
-    for (int i = 1; i < nc; ++i)
-        for (int k = i; k > 0 && (d[k] < d[k - 1] || (d[k] == d[k - 1] && ci[k] < ci[k - 1])); --k) {
-            const double td = d[k]; d[k] = d[k - 1]; d[k - 1] = td;
-            const int tc = ci[k]; ci[k] = ci[k - 1]; ci[k - 1] = tc;
-        }
-    if (ok && M > 3) {
-        // every other column has sim <= v[3] + eps, i.e. d2 >= 2 - 2(v[3] + eps)
-        const double others = (double)c.v[3] + eps;
-        ok = others < 1.0 && __dsub_rn(2.0, __dmul_rn(2.0, others)) > d[1];
-    }
-    if (lane == 0) {
-        if (ok) {
-            rs[r].best = ci[0];
-            rs[r].d1 = d[0];
-            rs[r].d2 = (M >= 2) ? d[1] : INFINITY;
-            rs[r].ratio_ok = -1;
-        } else {
-            const unsigned long long i = atomicAdd((unsigned long long*)&counters[0], 1ull);
-            flag_rows[i] = (int32_t)r;
-        }
-    }
-    }
 }
 
 // Column side, stage 2 (one warp per pending column): the best row is
@@ -709,15 +641,13 @@ static int certify(const void* Ax, const void* Bx, int D, const int64_t* a_off, 
                    double bias, double eps_row, double eps_col, double ratio2, MatchRowState* rs, int32_t* col_best,
                    int32_t* pend_rows, int32_t* pend_cols, int32_t* flag_rows, int32_t* flag_cols,
                    int64_t* counters, cudaStream_t st) {
+    (void)pend_rows;
     mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, ta, cand, eps_row, ratio2, rs,
-                                                                 pend_rows, counters);
+                                                                 flag_rows, counters);
     EC3R_CHECK_LAUNCH("mt_decide_rows");
     mt_decide_cols<<<(unsigned)((tb + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, tb, ck, cs, bias, eps_col,
                                                                  col_best, pend_cols, counters);
     EC3R_CHECK_LAUNCH("mt_decide_cols");
-    mt_certify_rows<T><<<kNumSMs * 4, 256, 0, st>>>(
-        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, pend_rows, cand, eps_row, rs, flag_rows, counters);
-    EC3R_CHECK_LAUNCH("mt_certify_rows");
     mt_certify_cols<T><<<kNumSMs * 4, 256, 0, st>>>(
         (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, pend_cols, ck, cs, bias, eps_col, col_best, flag_cols,
         counters);
