@@ -66,25 +66,30 @@ __device__ __forceinline__ void warp_dot4(const T* x, const T* Y, int64_t y0, in
 
 // Exact row scan: for rows listed in `rows` (global A-row ids; or all rows
 // when rows == nullptr), best column (first index on ties), d_first and the
-// second order statistic of the row's d2 values.  One warp per row; the
-// warp walks the pair's B rows in order, so the running (best, second) is
-// warp-uniform and needs no final merge.
+// second order statistic of the row's d2 values.  One CTA per row: its 8
+// warps split the pair's B rows in 4-row strides (every warp-local running
+// summary is warp-uniform), then warp 0 merges the 8 summaries.
+constexpr int MX_NT = 256;
+constexpr int MX_WARPS = MX_NT / 32;
+
 template <typename T>
-__global__ void __launch_bounds__(256) mx_rows_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
-                                                      const int64_t* __restrict__ a_off,
-                                                      const int64_t* __restrict__ b_off, int n_pairs,
-                                                      const int32_t* __restrict__ rows, const int64_t* __restrict__ n_rows_ptr,
-                                                      int64_t n_rows_all, MatchRowState* __restrict__ rs) {
+__global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
+                                                        const int64_t* __restrict__ a_off,
+                                                        const int64_t* __restrict__ b_off, int n_pairs,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int64_t* __restrict__ n_rows_ptr, int64_t n_rows_all,
+                                                        MatchRowState* __restrict__ rs) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ double sd1[MX_WARPS], sd2[MX_WARPS];
+    __shared__ int si1[MX_WARPS];
     const int64_t n_rows = rows ? *n_rows_ptr : n_rows_all;
-    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < n_rows;
-         t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    for (int64_t t = blockIdx.x; t < n_rows; t += gridDim.x) {
         const int64_t r = rows ? (int64_t)rows[t] : t;
         const int p = find_pair(a_off, n_pairs, r);
         const int64_t b0 = b_off[p], b1 = b_off[p + 1];
         double d1 = INFINITY, d2nd = INFINITY;
         int i1 = INT_MAX;
-        for (int64_t j = b0; j < b1; j += 4) {
+        for (int64_t j = b0 + 4 * warp; j < b1; j += 4 * MX_WARPS) {
             double s[4];
             warp_dot4<T>(A + r * D, B, j, b1, D, lane, s);
 #pragma unroll
@@ -96,32 +101,44 @@ __global__ void __launch_bounds__(256) mx_rows_kernel(const T* __restrict__ A, c
                 else if (d < d2nd) d2nd = d;
             }
         }
-        if (lane == 0) {
-            rs[r].best = (b1 > b0) ? i1 : -1;
-            rs[r].d1 = d1;
-            rs[r].d2 = d2nd;
+        if (lane == 0) { sd1[warp] = d1; sd2[warp] = d2nd; si1[warp] = i1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m1 = sd1[0], m2 = sd2[0];
+            int mi = si1[0];
+            for (int w = 1; w < MX_WARPS; ++w) {  // merge (best, second) summaries
+                if (better(sd1[w], si1[w], m1, mi)) { m2 = fmin(m1, sd2[w]); m1 = sd1[w]; mi = si1[w]; }
+                else m2 = fmin(m2, sd1[w]);
+            }
+            rs[r].best = (b1 > b0) ? mi : -1;
+            rs[r].d1 = m1;
+            rs[r].d2 = m2;
             rs[r].ratio_ok = -1;
         }
+        __syncthreads();
     }
 }
 
-// Exact column scan: argmin over the pair's A rows of d2 (first index).
+// Exact column scan: argmin over the pair's A rows of d2 (first index); one
+// CTA per column.
 template <typename T>
-__global__ void __launch_bounds__(256) mx_cols_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
-                                                      const int64_t* __restrict__ a_off,
-                                                      const int64_t* __restrict__ b_off, int n_pairs,
-                                                      const int32_t* __restrict__ cols, const int64_t* __restrict__ n_cols_ptr,
-                                                      int64_t n_cols_all, int32_t* __restrict__ col_best) {
+__global__ void __launch_bounds__(MX_NT) mx_cols_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
+                                                        const int64_t* __restrict__ a_off,
+                                                        const int64_t* __restrict__ b_off, int n_pairs,
+                                                        const int32_t* __restrict__ cols,
+                                                        const int64_t* __restrict__ n_cols_ptr, int64_t n_cols_all,
+                                                        int32_t* __restrict__ col_best) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ double sd1[MX_WARPS];
+    __shared__ int si1[MX_WARPS];
     const int64_t n_cols = cols ? *n_cols_ptr : n_cols_all;
-    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < n_cols;
-         t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    for (int64_t t = blockIdx.x; t < n_cols; t += gridDim.x) {
         const int64_t c = cols ? (int64_t)cols[t] : t;
         const int p = find_pair(b_off, n_pairs, c);
         const int64_t a0 = a_off[p], a1 = a_off[p + 1];
         double d1 = INFINITY;
         int i1 = INT_MAX;
-        for (int64_t i = a0; i < a1; i += 4) {
+        for (int64_t i = a0 + 4 * warp; i < a1; i += 4 * MX_WARPS) {
             double s[4];
             warp_dot4<T>(B + c * D, A, i, a1, D, lane, s);
 #pragma unroll
@@ -132,7 +149,16 @@ __global__ void __launch_bounds__(256) mx_cols_kernel(const T* __restrict__ A, c
                 if (better(d, ii, d1, i1)) { d1 = d; i1 = ii; }
             }
         }
-        if (lane == 0) col_best[c] = (a1 > a0) ? i1 : -1;
+        if (lane == 0) { sd1[warp] = d1; si1[warp] = i1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double m1 = sd1[0];
+            int mi = si1[0];
+            for (int w = 1; w < MX_WARPS; ++w)
+                if (better(sd1[w], si1[w], m1, mi)) { m1 = sd1[w]; mi = si1[w]; }
+            col_best[c] = (a1 > a0) ? mi : -1;
+        }
+        __syncthreads();
     }
 }
 
@@ -154,7 +180,10 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
         if (ok) out = s.best;
     }
     match_b[r] = out;
-    if (out >= 0) atomicAdd(&n_match[p], 1);
+    // one atomic per (warp, pair) instead of one per match
+    const unsigned same = __match_any_sync(__activemask(), p);
+    const unsigned hits = __ballot_sync(__activemask(), out >= 0) & same;
+    if (hits && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&n_match[p], __popc(hits));
 }
 
 template <typename T>

@@ -132,15 +132,27 @@ __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk
 // Warp-cooperative insert: every lane of the warp calls it (valid = has a
 // point).  Lanes sharing a block key elect one leader for the table lookup.
 // Returns 1 when this lane's point was dropped (pool / table overflow).
+// (cbk, cidx): the lane's last (block key, block index); consecutive points
+// of a lane usually fall in the same 8 cm block and skip the table.
 __device__ __forceinline__ unsigned vb_insert_warp(const VB& v, bool valid, long long cx, long long cy, long long cz,
-                                                   float wx, float wy, float wz, float w, unsigned cnt) {
+                                                   float wx, float wy, float wz, float w, unsigned cnt,
+                                                   unsigned long long& cbk, int& cidx) {
     const int lane = threadIdx.x & 31;
     const unsigned long long bk = valid ? pack_cells(cx >> 2, cy >> 2, cz >> 2) : kEmpty;
-    const unsigned peers = __match_any_sync(0xffffffffu, bk);
-    const int leader = __ffs(peers) - 1;
-    int idx = -2;
-    if (valid && lane == leader) idx = vb_find_or_insert(v, bk);
-    idx = __shfl_sync(0xffffffffu, idx, leader);
+    const bool need = valid && bk != cbk;
+    int idx = cidx;
+    if (__any_sync(0xffffffffu, need)) {
+        const unsigned peers = __match_any_sync(0xffffffffu, need ? bk : kEmpty);
+        const int leader = __ffs(peers) - 1;
+        int got = -2;
+        if (need && lane == leader) got = vb_find_or_insert(v, bk);
+        got = __shfl_sync(0xffffffffu, got, leader);
+        if (need) {
+            idx = got;
+            cbk = bk;
+            cidx = got;
+        }
+    }
     if (!valid) return 0u;
     if (idx < 0) return 1u;
     const int local = (int)(cx & 3) | ((int)(cy & 3) << 2) | ((int)(cz & 3) << 4);
@@ -262,6 +274,8 @@ __global__ void __launch_bounds__(FI_NT, 4) vh_insert_frames_kernel(FuseArgs a) 
     const bool vec = ((((size_t)slot * HW + (size_t)v0 * W) & 3) == 0) && ((npix & 3) == 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;  // per-thread counts
+    unsigned long long cbk = kEmpty;  // last block of this lane
+    int cidx = -2;
 
     // warp-uniform loop: the warp covers 128 consecutive pixels per iteration
     for (int wbase = warp * 128; wbase < npix; wbase += (FI_NT / 32) * 128) {
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(FI_NT, 4) vh_insert_frames_kernel(FuseArgs a) 
                     valid = false;
                 }
             }
-            n_ovf += vb_insert_warp(a.vb, valid, cxl, cyl, czl, ox, oy, oz, c, 1u);
+            n_ovf += vb_insert_warp(a.vb, valid, cxl, cyl, czl, ox, oy, oz, c, 1u, cbk, cidx);
             if (++u == W) { u = 0; ++r; }
         }
     }
@@ -373,7 +387,9 @@ __global__ void vh_insert_points_kernel(const double* __restrict__ pts, const do
                 }
             }
         }
-        const unsigned ovf = vb_insert_warp(vb, valid, cc[0], cc[1], cc[2], ox, oy, oz, w, 1u);
+        unsigned long long cbk = kEmpty;
+        int cidx = -2;
+        const unsigned ovf = vb_insert_warp(vb, valid, cc[0], cc[1], cc[2], ox, oy, oz, w, 1u, cbk, cidx);
         if (c_in) atomicAdd(&vb.counters[0], 1ull);
         if (c_oor) atomicAdd(&vb.counters[1], 1ull);
         if (ovf) atomicAdd(&vb.counters[2], 1ull);
@@ -386,13 +402,17 @@ __global__ void vh_insert_points_kernel(const double* __restrict__ pts, const do
 // Compact voxels with a non-zero count: (voxel key, pool index).
 // At most max_voxels are emitted; the excess is counted in counters[5]
 // (reported as overflow: the caller grows the handle and re-runs).
+// Also accumulates the cell bounding box bbox[6] = {min x,y,z, max x,y,z}
+// (pre-set to +/-inf) used to shrink the sort key.
 __global__ void vb_compact_kernel(const unsigned int* __restrict__ counts,
                                   const unsigned long long* __restrict__ block_keys,
                                   unsigned long long* __restrict__ counters, int64_t max_blocks,
                                   int64_t max_voxels, unsigned long long* __restrict__ keys,
-                                  int64_t* __restrict__ idx, unsigned long long* __restrict__ cursor) {
+                                  int64_t* __restrict__ idx, unsigned long long* __restrict__ cursor,
+                                  int* __restrict__ bbox) {
     const int64_t n = min((int64_t)counters[4], max_blocks) * kBlockVox;
     const int lane = threadIdx.x & 31;
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
         const bool occ = i < n && counts[i] != 0u;
@@ -409,9 +429,58 @@ __global__ void vb_compact_kernel(const unsigned int* __restrict__ counts,
             long long bx, by, bz;
             unpack_cells(block_keys[i / kBlockVox], bx, by, bz);
             const int local = (int)(i % kBlockVox);
-            keys[o] = pack_cells(bx * 4 + (local & 3), by * 4 + ((local >> 2) & 3), bz * 4 + (local >> 4));
+            const long long c[3] = {bx * 4 + (local & 3), by * 4 + ((local >> 2) & 3), bz * 4 + (local >> 4)};
+            keys[o] = pack_cells(c[0], c[1], c[2]);
             idx[o] = i;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { mn[k] = min(mn[k], (int)c[k]); mx[k] = max(mx[k], (int)c[k]); }
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = min(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = max(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+        if (lane == 0 && mn[k] <= mx[k]) { atomicMin(&bbox[k], mn[k]); atomicMax(&bbox[3 + k], mx[k]); }
+    }
+}
+
+// Sort-key compaction: (cx, cy, cz) relative to the bounding box packed
+// into 32 bits preserve the lexicographic order of _pack keys.
+__global__ void vb_pack32_kernel(const unsigned long long* __restrict__ keys, const int64_t* __restrict__ idx,
+                                 const int64_t* __restrict__ n_ptr, const int* __restrict__ bbox, int by_bits,
+                                 int bz_bits, uint32_t* __restrict__ k32, uint32_t* __restrict__ i32) {
+    const int64_t n = *n_ptr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        long long cx, cy, cz;
+        unpack_cells(keys[i], cx, cy, cz);
+        k32[i] = ((uint32_t)(cx - bbox[0]) << (by_bits + bz_bits)) | ((uint32_t)(cy - bbox[1]) << bz_bits) |
+                 (uint32_t)(cz - bbox[2]);
+        i32[i] = (uint32_t)idx[i];
+    }
+}
+
+__global__ void vb_gather32_kernel(const float4* __restrict__ sums, const unsigned int* __restrict__ counts,
+                                   const unsigned long long* __restrict__ block_keys, const uint32_t* __restrict__ i32,
+                                   const int64_t* __restrict__ n_ptr, double cell, int64_t* __restrict__ okeys,
+                                   float* __restrict__ cen, float* __restrict__ wsum, int32_t* __restrict__ cnt) {
+    const int64_t n = *n_ptr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = i32[i];
+        const float4 s = sums[v];
+        long long bx, by, bz;
+        unpack_cells(block_keys[v / kBlockVox], bx, by, bz);
+        const int local = (int)(v % kBlockVox);
+        const long long cx = bx * 4 + (local & 3), cy = by * 4 + ((local >> 2) & 3), cz = bz * 4 + (local >> 4);
+        okeys[i] = (int64_t)pack_cells(cx, cy, cz);
+        const double w = s.w;
+        cen[3 * i + 0] = (float)((double)cx * cell + (double)s.x / w);
+        cen[3 * i + 1] = (float)((double)cy * cell + (double)s.y / w);
+        cen[3 * i + 2] = (float)((double)cz * cell + (double)s.z / w);
+        wsum[i] = s.w;
+        cnt[i] = (int32_t)counts[v];
     }
 }
 
@@ -474,7 +543,10 @@ __global__ void vb_merge_kernel(const int64_t* __restrict__ keys, const float* _
             s = reinterpret_cast<const float4*>(sums4)[i];
             c = (unsigned)cnt[i];
         }
-        if (vb_insert_warp(vb, valid, cx, cy, cz, s.x, s.y, s.z, s.w, c)) atomicAdd(&vb.counters[2], 1ull);
+        unsigned long long cbk = kEmpty;
+        int cidx = -2;
+        if (vb_insert_warp(vb, valid, cx, cy, cz, s.x, s.y, s.z, s.w, c, cbk, cidx))
+            atomicAdd(&vb.counters[2], 1ull);
     }
 }
 
@@ -491,31 +563,71 @@ __global__ void clamp_count_kernel(const unsigned long long* __restrict__ cursor
     *n_out = c < cap ? c : cap;
 }
 
+__global__ void bbox_init_kernel(int* bbox) {
+    if (threadIdx.x < 3) { bbox[threadIdx.x] = INT_MAX; bbox[3 + threadIdx.x] = INT_MIN; }
+}
+
+static int bits_for(int range) {  // bits to hold values 0..range
+    int b = 0;
+    while (b < 31 && (1u << b) <= (unsigned)range) ++b;
+    return b;
+}
+
+// Compact + (optional) sort.  *n_out (device) receives U.  Without sort, or
+// with the 64-bit key sort, (*ks, *is) are the arrays to gather from and
+// *i32 = nullptr; with the 32-bit key sort (bounding box fits 32 bits: the
+// usual case, 4 radix passes instead of 8) *i32 holds the sorted pool
+// indices.
 static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t workspace_bytes, int64_t* n_out,
-                          const unsigned long long** ks, const int64_t** is, cudaStream_t st) {
+                          const unsigned long long** ks, const int64_t** is, const uint32_t** i32,
+                          cudaStream_t st) {
     const size_t cap = (size_t)h->max_voxels;
     Carver cv{(char*)workspace, 0};
     unsigned long long* k0 = cv.take<unsigned long long>(cap);
     int64_t* i0 = cv.take<int64_t>(cap);
     unsigned long long* k1 = cv.take<unsigned long long>(cap);
     int64_t* i1 = cv.take<int64_t>(cap);
-    unsigned long long* cursor = cv.take<unsigned long long>(8);
+    unsigned long long* cursor = cv.take<unsigned long long>(8);  // [0] cursor, [1..3] bbox (6 ints)
+    int* bbox = reinterpret_cast<int*>(cursor + 1);
     size_t cub_bytes = workspace_bytes - cv.used;
     void* cub_tmp = cv.base + cv.used;
     EC3R_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+    bbox_init_kernel<<<1, 32, 0, st>>>(bbox);
+    EC3R_CHECK_LAUNCH("bbox_init_kernel");
     vb_compact_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->counts, h->block_keys, h->counters, h->max_blocks,
-                                                   h->max_voxels, k0, i0, cursor);
+                                                   h->max_voxels, k0, i0, cursor, bbox);
     EC3R_CHECK_LAUNCH("vb_compact_kernel");
     clamp_count_kernel<<<1, 1, 0, st>>>(cursor, h->max_voxels, n_out);
     EC3R_CHECK_LAUNCH("clamp_count_kernel");
     *ks = k0;
     *is = i0;
+    *i32 = nullptr;
     if (sort) {
-        unsigned long long nh = 0;
-        EC3R_CUDA_TRY(cudaMemcpyAsync(&nh, cursor, sizeof(nh), cudaMemcpyDeviceToHost, st));
+        unsigned long long hst[4] = {0, 0, 0, 0};
+        EC3R_CUDA_TRY(cudaMemcpyAsync(hst, cursor, sizeof(hst), cudaMemcpyDeviceToHost, st));
         EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        unsigned long long nh = hst[0];
+        int bb[6];
+        memcpy(bb, hst + 1, sizeof(bb));
         if ((int64_t)nh > h->max_voxels) nh = (unsigned long long)h->max_voxels;
         if (nh > 0) {
+            const int bx = bits_for(bb[3] - bb[0]), by = bits_for(bb[4] - bb[1]), bz = bits_for(bb[5] - bb[2]);
+            const int total = bx + by + bz;
+            if (total <= 32 && cap <= 0xFFFFFFFFull) {
+                uint32_t* k32 = reinterpret_cast<uint32_t*>(k1);
+                uint32_t* v32 = reinterpret_cast<uint32_t*>(i1);
+                uint32_t* k32s = k32 + cap;
+                uint32_t* v32s = v32 + cap;
+                vb_pack32_kernel<<<kNumSMs * 8, 256, 0, st>>>(k0, i0, n_out, bbox, by, bz, k32, v32);
+                EC3R_CHECK_LAUNCH("vb_pack32_kernel");
+                if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k32, k32s, v32, v32s, (int)nh, 0,
+                                                    total > 0 ? total : 1, st) != cudaSuccess) {
+                    set_last_error("cub::DeviceRadixSort::SortPairs(u32)", cudaGetLastError());
+                    return EC3R_ECUDA;
+                }
+                *i32 = v32s;
+                return EC3R_OK;
+            }
             if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k0, k1, i0, i1, (int)nh, 0, 63, st) !=
                 cudaSuccess) {
                 set_last_error("cub::DeviceRadixSort::SortPairs", cudaGetLastError());
@@ -661,6 +773,10 @@ extern "C" size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h) {
     cub::DeviceRadixSort::SortPairs<unsigned long long, int64_t>(nullptr, cub_bytes, (unsigned long long*)nullptr,
                                                                  (unsigned long long*)nullptr, (int64_t*)nullptr,
                                                                  (int64_t*)nullptr, (int)cap, 0, 63);
+    size_t cub32 = 0;
+    cub::DeviceRadixSort::SortPairs<uint32_t, uint32_t>(nullptr, cub32, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                                        (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cap, 0, 32);
+    if (cub32 > cub_bytes) cub_bytes = cub32;
     return 4 * align256(sizeof(int64_t) * cap) + align256(64) + align256(cub_bytes);
 }
 
@@ -671,8 +787,15 @@ extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid,
     cudaStream_t st = as_stream(stream);
     const unsigned long long* ks;
     const int64_t* is;
-    const int rc = compact_sorted(h, sort, workspace, workspace_bytes, n_out, &ks, &is, st);
+    const uint32_t* i32;
+    const int rc = compact_sorted(h, sort, workspace, workspace_bytes, n_out, &ks, &is, &i32, st);
     if (rc) return rc;
+    if (i32) {
+        vb_gather32_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->sums, h->counts, h->block_keys, i32, n_out, h->cell, keys,
+                                                        centroid, wsum, count);
+        EC3R_CHECK_LAUNCH("vb_gather32_kernel");
+        return EC3R_OK;
+    }
     vb_gather_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->sums, h->counts, ks, is, n_out, h->cell, keys, centroid, wsum,
                                                   count);
     EC3R_CHECK_LAUNCH("vb_gather_kernel");
@@ -693,7 +816,8 @@ extern "C" int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* 
     void* cws = cv.base + cv.used;
     const unsigned long long* ks;
     const int64_t* is;
-    const int rc = compact_sorted(h, 0, cws, workspace_bytes - cv.used, n_dev, &ks, &is, st);
+    const uint32_t* i32;
+    const int rc = compact_sorted(h, 0, cws, workspace_bytes - cv.used, n_dev, &ks, &is, &i32, st);
     if (rc) return rc;
     EC3R_CUDA_TRY(cudaMemsetAsync(rank_counts, 0, sizeof(int64_t) * n_ranks, st));
     EC3R_CUDA_TRY(cudaMemsetAsync(cursors, 0, sizeof(unsigned long long) * n_ranks, st));
