@@ -159,6 +159,7 @@ typedef struct {
     int64_t n_out_of_range;  /* cell outside the 21-bit key range: dropped */
     int64_t n_overflow;      /* table full: dropped (grow and re-run) */
     int64_t n_slow_path;     /* points resolved by the exact float64 path */
+    int64_t n_blocks;        /* 4x4x4 voxel blocks allocated in the pool */
 } ec3r_vhash_stats;
 
 EC3R_API int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream);

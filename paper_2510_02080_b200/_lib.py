@@ -59,7 +59,7 @@ EXPORTED = tuple(_PROTOS)
 
 class VHashStats(C.Structure):
     _fields_ = [("n_points_in", _I64), ("n_out_of_range", _I64), ("n_overflow", _I64),
-                ("n_slow_path", _I64)]
+                ("n_slow_path", _I64), ("n_blocks", _I64)]
 
 
 _lib = None

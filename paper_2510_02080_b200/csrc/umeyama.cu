@@ -222,12 +222,18 @@ __device__ __forceinline__ void load_rot(const double* x8, double R[3][3], doubl
 
 // Visit every pixel of the edge's segments owned by this thread (4 pixels per
 // visit: one 128-bit load from each of the four planes when aligned).
-template <typename F>
-__device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s1, int rank, F&& f) {
+// seg_fn(sa, sb) runs on the whole CTA at the start of every segment,
+// bracketed by CTA barriers, so it may rebuild shared tables.
+template <class S, class F>
+__device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, int s1, int rank, S&& seg_fn,
+                                                    F&& f) {
     const int HW = a.H * a.W;
     const bool vec = (HW & 3) == 0;
     for (int sg = s0; sg < s1; ++sg) {
         const int sa = a.seg_slots[2 * sg], sb = a.seg_slots[2 * sg + 1];
+        __syncthreads();
+        seg_fn(sa, sb);
+        __syncthreads();
         const float* da = a.depth + (size_t)sa * HW;
         const float* ca = a.conf + (size_t)sa * HW;
         const float* db = a.depth + (size_t)sb * HW;
@@ -254,7 +260,12 @@ __device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s
     }
 }
 
-__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT)
+template <typename F>
+__device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s1, int rank, F&& f) {
+    for_each_pixel4_seg(a, s0, s1, rank, [](int, int) {}, f);
+}
+
+__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT, 2)
 register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restrict__ out_rms,
                       int64_t* __restrict__ out_count, int64_t* __restrict__ out_npairs,
                       int32_t* __restrict__ out_status, uint8_t* __restrict__ keep_masks) {
@@ -347,19 +358,38 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     for (int i = 0; i < 3; ++i) { shp[i] = tot1[1 + i] / nvalid; shq[i] = tot1[4 + i] / nvalid; }
 
     // ---- phase 2: keep = w >= floor; shifted float64 raw moments
+    // Per segment, the two frames' float64 affine maps live in shared tables
+    // (point = z * (col[u] + row[v]) + t), not in registers: 24 float64
+    // accumulators + two rotations would cap the kernel at one CTA per SM.
     double a2[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) a2[k] = 0;
-    cur_seg = -1;
-    double R2a[3][3], t2a[3], R2b[3][3], t2b[3];
-    for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
-                                         float4 wb) {
-        if (sg != cur_seg) {
-            cur_seg = sg;
-            load_rot(a.slot_poses + 8 * sa, R2a, t2a);
-            load_rot(a.slot_poses + 8 * sb, R2b, t2b);
-            for (int i = 0; i < 3; ++i) { t2a[i] -= shp[i]; t2b[i] -= shq[i]; }
+    double* colA = yc + a.H;          // [3][W]
+    double* rowA = colA + 3 * W;      // [3][H]
+    double* colB = rowA + 3 * a.H;    // [3][W]
+    double* rowB = colB + 3 * W;      // [3][H]
+    __shared__ double tAB[6];
+    auto build = [&](int sa, int sb) {
+        double Ra[3][3], ta_[3], Rb[3][3], tb_[3];
+        load_rot(a.slot_poses + 8 * sa, Ra, ta_);
+        load_rot(a.slot_poses + 8 * sb, Rb, tb_);
+        for (int u = threadIdx.x; u < W; u += UM_NT)
+            for (int i = 0; i < 3; ++i) {
+                colA[i * W + u] = Ra[i][0] * xc[u] + Ra[i][2];
+                colB[i * W + u] = Rb[i][0] * xc[u] + Rb[i][2];
+            }
+        for (int v = threadIdx.x; v < a.H; v += UM_NT)
+            for (int i = 0; i < 3; ++i) {
+                rowA[i * a.H + v] = Ra[i][1] * yc[v];
+                rowB[i * a.H + v] = Rb[i][1] * yc[v];
+            }
+        if (threadIdx.x < 3) {
+            tAB[threadIdx.x] = ta_[threadIdx.x] - shp[threadIdx.x];
+            tAB[3 + threadIdx.x] = tb_[threadIdx.x] - shq[threadIdx.x];
         }
+    };
+    for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
+                                                     float4 zb, float4 wb) {
         const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
         const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
         uint32_t kbits = 0;
@@ -372,13 +402,12 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
                 kbits |= 1u << (8 * k);
                 const int px = pix + k, v = px / W, u = px - v * W;
                 const double wi = (double)wf;
-                const double x = xc[u], y = yc[v];
                 const double zaa = zA[k], zbb = zB[k];
                 double pp[3], qq[3];
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    pp[i] = zaa * (R2a[i][0] * x + R2a[i][1] * y + R2a[i][2]) + t2a[i];
-                    qq[i] = zbb * (R2b[i][0] * x + R2b[i][1] * y + R2b[i][2]) + t2b[i];
+                    pp[i] = zaa * (colA[i * W + u] + rowA[i * a.H + v]) + tAB[i];
+                    qq[i] = zbb * (colB[i * W + u] + rowB[i * a.H + v]) + tAB[3 + i];
                 }
                 a2[0] += wi;
                 a2[1] += 1.0;
@@ -443,23 +472,17 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         double v0[3], v1[3];
         for (int i = 0; i < 3; ++i) { v0[i] = sol.src_V[i][0]; v1[i] = sol.src_V[i][1]; }
         double a3[2] = {0, 0};
-        cur_seg = -1;
-        for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
-                                             float4 wb) {
-            if (sg != cur_seg) {
-                cur_seg = sg;
-                load_rot(a.slot_poses + 8 * sa, R2a, t2a);
-                for (int i = 0; i < 3; ++i) t2a[i] -= shp[i];
-            }
+        for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
+                                                         float4 zb, float4 wb) {
             const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
             const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
             for (int k = 0; k < 4; ++k) {
                 const float wf = fminf(cA[k], cB[k]);
                 if (zA[k] > 0.f && zB[k] > 0.f && (double)wf >= floorv) {
                     const int px = pix + k, v = px / W, u = px - v * W;
-                    const double x = xc[u], y = yc[v], z = zA[k];
+                    const double z = zA[k];
                     double d[3];
-                    for (int i = 0; i < 3; ++i) d[i] = z * (R2a[i][0] * x + R2a[i][1] * y + R2a[i][2]) + t2a[i];
+                    for (int i = 0; i < 3; ++i) d[i] = z * (colA[i * W + u] + rowA[i * a.H + v]) + tAB[i];
                     d[0] -= mp0; d[1] -= mp1; d[2] -= mp2;
                     const double y0 = v0[0] * d[0] + v0[1] * d[1] + v0[2] * d[2];
                     const double y1 = v1[0] * d[0] + v1[1] * d[1] + v1[2] * d[2];
@@ -583,7 +606,7 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
     a.edge_seg = edge_seg; a.H = H; a.W = W;
     a.fx = K4_h[0]; a.fy = K4_h[1]; a.cx = K4_h[2]; a.cy = K4_h[3];
     a.floor_frac = floor_frac; a.min_corr = min_corr; a.with_scale = with_scale;
-    const size_t smem = sizeof(double) * (size_t)(H + W);
+    const size_t smem = sizeof(double) * 7 * (size_t)(H + W);  // xc, yc + two frames' col/row tables
     if (smem > 48 * 1024) {
         EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));

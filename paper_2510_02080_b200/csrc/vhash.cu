@@ -52,6 +52,8 @@ struct ec3r_vhash {
     float4* sums;                    // max_blocks * 64
     unsigned int* counts;            // max_blocks * 64
     unsigned long long* counters;    // [n_in, n_oor, n_overflow, n_slow, blocks_used, ...]
+    float4* ftab;                    // per-frame affine tables of the last insert_frames
+    int64_t ftab_cap;                // float4 entries
 };
 
 namespace ec3r {
@@ -84,6 +86,14 @@ __device__ __forceinline__ unsigned long long pack_cells(long long cx, long long
            (unsigned long long)(cz + kPackOffset);
 }
 
+// pack_cells of int32 block coordinates with 32-bit operations
+__device__ __forceinline__ unsigned long long pack_block(int bx, int by, int bz) {
+    const unsigned X = (unsigned)(bx + (int)kPackOffset), Y = (unsigned)(by + (int)kPackOffset),
+                   Z = (unsigned)(bz + (int)kPackOffset);
+    const unsigned lo = (Y << 21) | Z, hi = (X << 10) | (Y >> 11);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
 __device__ __forceinline__ void unpack_cells(unsigned long long k, long long& cx, long long& cy, long long& cz) {
     cx = (long long)((k >> 42) & 0x1FFFFF) - kPackOffset;
     cy = (long long)((k >> 21) & 0x1FFFFF) - kPackOffset;
@@ -97,32 +107,53 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                  : "memory");
 }
 
+// One 16-byte L2 read of a table entry {key, idx} (relaxed, gpu scope: the
+// table is only written by this kernel's atomics, so L2 is the coherence
+// point; a volatile access would compile to .STRONG.SYS and two round trips).
+__device__ __forceinline__ void load_entry(const BlockEntry* e, unsigned long long& key, int& idx) {
+    unsigned long long lo, hi;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(e) : "memory");
+    key = lo;
+    idx = (int)(unsigned)(hi & 0xFFFFFFFFull);
+}
+
+__device__ __forceinline__ int load_idx(const BlockEntry* e) {
+    int idx;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(idx) : "l"(&e->idx) : "memory");
+    return idx;
+}
+
 // Find or allocate the pool block of block key bk (one thread).  Returns the
 // block index, or -2 when the pool or the table is full.
 __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk) {
     unsigned long long h = mix64(bk) & v.tmask;
     for (unsigned long long probe = 0; probe <= v.tmask; ++probe) {
         BlockEntry* e = v.table + h;
-        unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(&e->key);
+        unsigned long long k;
+        int idx;
+        load_entry(e, k, idx);
+        if (k == bk) {
+            while (idx == -1) idx = load_idx(e);  // winner is publishing
+            return idx;
+        }
         if (k == kEmpty) {
             const unsigned long long prev = atomicCAS(&e->key, kEmpty, bk);
             if (prev == kEmpty) {
                 const unsigned long long slot = atomicAdd(&v.counters[4], 1ull);
-                int idx = -2;
+                int got = -2;
                 if ((int64_t)slot < v.max_blocks) {
-                    idx = (int)slot;
+                    got = (int)slot;
                     v.block_keys[slot] = bk;
                 }
                 __threadfence();
-                atomicExch(&e->idx, idx);
-                return idx;
+                atomicExch(&e->idx, got);
+                return got;
             }
-            k = prev;
-        }
-        if (k == bk) {
-            int idx = *reinterpret_cast<volatile int*>(&e->idx);
-            while (idx == -1) idx = *reinterpret_cast<volatile int*>(&e->idx);  // winner is publishing
-            return idx;
+            if (prev == bk) {
+                int i2 = load_idx(e);
+                while (i2 == -1) i2 = load_idx(e);
+                return i2;
+            }
         }
         h = (h + 1) & v.tmask;
     }
@@ -190,7 +221,13 @@ __global__ void vb_clear_pool_kernel(float4* __restrict__ sums, unsigned int* __
 // frame insertion
 
 constexpr int FI_NT = 256;
-constexpr int FI_ROWS = 8;  // image rows per CTA
+#ifndef EC3R_FI_ROWS
+#define EC3R_FI_ROWS 64  // image rows per CTA
+#endif
+constexpr int FI_ROWS = EC3R_FI_ROWS;
+#ifndef EC3R_FI_MINB
+#define EC3R_FI_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
 
 struct FuseArgs {
     const float* depth;
@@ -198,7 +235,8 @@ struct FuseArgs {
     const double* slot_poses;    // anchor_from_cam per slot
     const double* slot_globals;  // world_from_anchor (submap global Sim3) per slot
     const int32_t* slots;        // slot ids to fuse
-    int H, W;
+    const float4* ftab;          // per listed frame: A[W], B[H], T (see vh_frame_tables_kernel)
+    int n, H, W;
     double fx, fy, cx, cy;
     double cell;
     float inv_cell_f, cell_f;
@@ -217,124 +255,251 @@ __device__ __noinline__ void exact_cells(const double* P, const double* G, doubl
     for (int k = 0; k < 3; ++k) c[k] = (long long)floor(__ddiv_rn(pw[k], cell));
 }
 
-__global__ void __launch_bounds__(FI_NT, 4) vh_insert_frames_kernel(FuseArgs a) {
-    extern __shared__ unsigned char fsm[];
-    const int W = a.W;
-    // smem: A[W] float4 (xyz + |.|sum), xc[W] double, B[ROWS] float4, yc[ROWS] double
-    float4* A = reinterpret_cast<float4*>(fsm);
-    double* xc = reinterpret_cast<double*>(A + W);
-    __shared__ float4 B[FI_ROWS];
-    __shared__ double yc[FI_ROWS];
-    __shared__ double Pd[8], Gd[8];
-    __shared__ float Tm[4];
-    __shared__ unsigned long long cta_cnt[4];
-
-    const int slot = a.slots[blockIdx.y];
-    const int v0 = blockIdx.x * FI_ROWS;
-    const int nrows = min(FI_ROWS, a.H - v0);
-    if (threadIdx.x < 8) {
-        Pd[threadIdx.x] = a.slot_poses[8 * slot + threadIdx.x];
-        Gd[threadIdx.x] = a.slot_globals[8 * slot + threadIdx.x];
-    }
-    if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    // composite M = G o P in float64: rotation sG*RG*RP, translation sG*RG*tP + tG
+// Per listed frame j, the composite G o P_f folded into a float32 affine map
+// x = z * (A[u] + B[v]) + T: A[u] = M[:,0] x_u + M[:,2], B[v] = M[:,1] y_v,
+// each with its |.|-sum in .w for the rounding bound; T = (t, |t|-sum).
+__global__ void vh_frame_tables_kernel(FuseArgs a, float4* __restrict__ ftab) {
+    const int j = blockIdx.x;
+    const int slot = a.slots[j];
+    const double* P = a.slot_poses + 8 * slot;
+    const double* G = a.slot_globals + 8 * slot;
     double RG[3][3], RP[3][3], M[3][3], T[3];
-    quat_to_mat(Gd + 1, RG);
-    quat_to_mat(Pd + 1, RP);
+    quat_to_mat(G + 1, RG);
+    quat_to_mat(P + 1, RP);
     for (int i = 0; i < 3; ++i) {
-        for (int j = 0; j < 3; ++j) M[i][j] = Gd[0] * (RG[i][0] * RP[0][j] + RG[i][1] * RP[1][j] + RG[i][2] * RP[2][j]);
-        T[i] = Gd[0] * (RG[i][0] * Pd[5] + RG[i][1] * Pd[6] + RG[i][2] * Pd[7]) + Gd[5 + i];
+        for (int k = 0; k < 3; ++k) M[i][k] = G[0] * (RG[i][0] * RP[0][k] + RG[i][1] * RP[1][k] + RG[i][2] * RP[2][k]);
+        T[i] = G[0] * (RG[i][0] * P[5] + RG[i][1] * P[6] + RG[i][2] * P[7]) + G[5 + i];
     }
-    for (int u = threadIdx.x; u < W; u += FI_NT) {
+    float4* tab = ftab + (size_t)j * (a.W + a.H + 1);
+    for (int u = threadIdx.x; u < a.W; u += blockDim.x) {
         const double x = ray_coef(u, a.cx, a.fx);
-        xc[u] = x;
         const float ax = (float)(M[0][0] * x + M[0][2]), ay = (float)(M[1][0] * x + M[1][2]),
                     az = (float)(M[2][0] * x + M[2][2]);
-        A[u] = make_float4(ax, ay, az, fabsf(ax) + fabsf(ay) + fabsf(az));
+        tab[u] = make_float4(ax, ay, az, fabsf(ax) + fabsf(ay) + fabsf(az));
     }
-    if (threadIdx.x < nrows) {
-        const int v = v0 + threadIdx.x;
+    for (int v = threadIdx.x; v < a.H; v += blockDim.x) {
         const double y = ray_coef(v, a.cy, a.fy);
-        yc[threadIdx.x] = y;
         const float bx = (float)(M[0][1] * y), by = (float)(M[1][1] * y), bz = (float)(M[2][1] * y);
-        B[threadIdx.x] = make_float4(bx, by, bz, fabsf(bx) + fabsf(by) + fabsf(bz));
+        tab[a.W + v] = make_float4(bx, by, bz, fabsf(bx) + fabsf(by) + fabsf(bz));
     }
     if (threadIdx.x == 0) {
-        Tm[0] = (float)T[0]; Tm[1] = (float)T[1]; Tm[2] = (float)T[2];
-        Tm[3] = fabsf(Tm[0]) + fabsf(Tm[1]) + fabsf(Tm[2]);
+        const float tx = (float)T[0], ty = (float)T[1], tz = (float)T[2];
+        tab[a.W + a.H] = make_float4(tx, ty, tz, fabsf(tx) + fabsf(ty) + fabsf(tz));
     }
+}
+
+// Frame insertion.  Grid = (bands of FI_ROWS rows, listed frames); a CTA's
+// warps take 8 x 16 pixel sub-tiles of its band (lane = 4 horizontally
+// adjacent pixels) independently -- no CTA barriers in the loop.  A 2-D
+// sub-tile touches ~13 distinct blocks where a 128-pixel row run touches ~36,
+// so the per-warp block lookups (lane reuse, one leader per block per pixel
+// slot, the 4 slots' first probes in flight together) drop ~3x.  The next
+// sub-tile's depth / confidence are loaded before this one's lookups.
+//
+// Measured on the bench workload (72M points, tools/fuse_timing.py): keys +
+// lookups alone run in ~0.9 ms; the two scattered reductions per point add
+// ~0.9 ms.  Scattered 16 B + 4 B updates cost one L1 wavefront per lane
+// (tools/atomics_probe3.cu: ~93 G point-updates/s for random voxels, up to
+// ~300 G when a warp's lanes hit consecutive voxels), and the sweep order
+// (frame-major ... all frames interleaved) and pool working set changed the
+// time by < 10%, so the pool's L2 residency is not the limiter.
+constexpr int ST_H = 8, ST_W = 16;
+
+__global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
+    extern __shared__ float4 sA[];  // A[W]
+    __shared__ float4 sB[FI_ROWS];
+    __shared__ unsigned long long cta_cnt[4];
+    const int W = a.W, H = a.H;
+    const int HW = H * W;
+    const int j = blockIdx.y;
+    const int slot = a.slots[j];
+    const int v_band = blockIdx.x * FI_ROWS;
+    const int rows = min(FI_ROWS, H - v_band);
+    const float4* tab = a.ftab + (size_t)j * (W + H + 1);
+    for (int u = threadIdx.x; u < W; u += FI_NT) sA[u] = __ldg(tab + u);
+    if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
+    if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
+    const float4 Tm = __ldg(tab + W + H);
     __syncthreads();
-    const float tx = Tm[0], ty = Tm[1], tz = Tm[2], tabs = Tm[3];
+
     const float inv = a.inv_cell_f, cellf = a.cell_f;
-    const size_t HW = (size_t)a.H * W;
-    const float* dp = a.depth + (size_t)slot * HW + (size_t)v0 * W;
-    const float* cp = a.conf + (size_t)slot * HW + (size_t)v0 * W;
-    const int npix = nrows * W;
-    const bool vec = ((((size_t)slot * HW + (size_t)v0 * W) & 3) == 0) && ((npix & 3) == 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;  // per-thread counts
-    unsigned long long cbk = kEmpty;  // last block of this lane
+    const int dv = lane >> 2, du = 4 * (lane & 3);
+    const int stx = (W + ST_W - 1) / ST_W;
+    const bool pairs = (W & 1) == 0;
+    const float* dbase = a.depth + (size_t)slot * HW;
+    const float* cbase = a.conf + (size_t)slot * HW;
+    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
+    unsigned long long cbk = kEmpty;  // lane's last block
     int cidx = -2;
 
-    // warp-uniform loop: the warp covers 128 consecutive pixels per iteration
-    for (int wbase = warp * 128; wbase < npix; wbase += (FI_NT / 32) * 128) {
-        const int base = wbase + 4 * lane;
-        float zs[4], cs[4];
-        if (vec && base < npix) {
-            const float4 z4 = __ldcs(reinterpret_cast<const float4*>(dp + base));
-            const float4 c4 = __ldcs(reinterpret_cast<const float4*>(cp + base));
-            zs[0] = z4.x; zs[1] = z4.y; zs[2] = z4.z; zs[3] = z4.w;
-            cs[0] = c4.x; cs[1] = c4.y; cs[2] = c4.z; cs[3] = c4.w;
+    // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
+    auto advance = [&](int& sy, int& sx) {
+        sx += FI_NT / 32;
+        while (sx >= stx) { sx -= stx; ++sy; }
+    };
+    auto load4 = [&](int sy, int sx, float (&z)[4], float (&c)[4]) {
+        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { z[k] = 0.f; c[k] = 0.f; }
+        if (r >= rows) return;
+        const size_t off = (size_t)(v_band + r) * W + u0;
+        if (pairs) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (u0 + 2 * h + 1 < W) {
+                    const float2 z2 = __ldcs(reinterpret_cast<const float2*>(dbase + off + 2 * h));
+                    const float2 c2 = __ldcs(reinterpret_cast<const float2*>(cbase + off + 2 * h));
+                    z[2 * h] = z2.x; z[2 * h + 1] = z2.y;
+                    c[2 * h] = c2.x; c[2 * h + 1] = c2.y;
+                }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool in = base + k < npix;
-                zs[k] = in ? dp[base + k] : 0.f;
-                cs[k] = in ? cp[base + k] : 0.f;
-            }
+            for (int k = 0; k < 4; ++k)
+                if (u0 + k < W) { z[k] = __ldcs(dbase + off + k); c[k] = __ldcs(cbase + off + k); }
         }
-        int r = base / W;
-        int u = base - r * W;
+    };
+
+    const int n_sy = (rows + ST_H - 1) / ST_H;
+    int sy = 0, sx = warp;
+    while (sx >= stx) { sx -= stx; ++sy; }
+    int py = sy, px = sx;  // prefetch cursor
+    float nz[4], nc[4];
+    if (py < n_sy) load4(py, px, nz, nc);
+    for (; sy < n_sy; advance(sy, sx)) {
+        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+        float zs[4], cs[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
+        advance(py, px);
+        if (py < n_sy) load4(py, px, nz, nc);
+        const float4 Bv = sB[min(r, rows - 1)];
+
+        // phase A: keys and contributions of the lane's 4 pixels, branch-free
+        // except the (rare) exact float64 re-run near a voxel face
+        bool valid[4];
+        int cx[4], cy[4], cz[4];
+        float ox[4], oy[4], oz[4];
+        unsigned slow = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const float z = zs[k], c = cs[k];
-            bool valid = z > 0.f && c > 0.f;
-            long long cxl = 0, cyl = 0, czl = 0;
-            float ox = 0.f, oy = 0.f, oz = 0.f;
-            if (valid) {
-                ++n_in;
-                const float4 Au = A[u], Bv = B[r];
-                const float dx = Au.x + Bv.x, dy = Au.y + Bv.y, dz = Au.z + Bv.z;
-                const float x = fmaf(z, dx, tx), y = fmaf(z, dy, ty), zz = fmaf(z, dz, tz);
-                // first-order float32 error bound (x4 safety), see header
-                const float ax = fabsf(x) + fabsf(y) + fabsf(zz);
-                const float err = 2.384185791015625e-07f * (2.0f * z * (Au.w + Bv.w) + tabs + 2.0f * ax) + 1e-9f;
-                const float margin = err * inv + 2.4e-7f;
-                const float qx = x * inv, qy = y * inv, qz = zz * inv;
-                const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-                const bool near = (qx - fx < margin) || (fx + 1.0f - qx < margin) || (qy - fy < margin) ||
-                                  (fy + 1.0f - qy < margin) || (qz - fz < margin) || (fz + 1.0f - qz < margin) ||
-                                  fabsf(qx) > 1.0e6f || fabsf(qy) > 1.0e6f || fabsf(qz) > 1.0e6f;
-                if (!near) {
-                    cxl = (long long)fx; cyl = (long long)fy; czl = (long long)fz;
-                } else {
-                    long long cc[3];
-                    exact_cells(Pd, Gd, xc[u], yc[r], z, a.cell, cc);
-                    cxl = cc[0]; cyl = cc[1]; czl = cc[2];
-                    ++n_slow;
-                }
-                if (cell_in_range(cxl) && cell_in_range(cyl) && cell_in_range(czl)) {
-                    ox = c * (x - (float)cxl * cellf);
-                    oy = c * (y - (float)cyl * cellf);
-                    oz = c * (zz - (float)czl * cellf);
+            const float4 Au = sA[min(u0 + k, W - 1)];  // columns past W are zero-filled (invalid)
+            const float dx = Au.x + Bv.x, dy = Au.y + Bv.y, dz = Au.z + Bv.z;
+            const float x = fmaf(z, dx, Tm.x), y = fmaf(z, dy, Tm.y), zz = fmaf(z, dz, Tm.z);
+            // first-order float32 error bound (x4 safety), see header; +1 ulp(0.5)
+            // for the folded face test below
+            const float ax = fabsf(x) + fabsf(y) + fabsf(zz);
+            const float err = 2.384185791015625e-07f * (2.0f * z * (Au.w + Bv.w) + Tm.w + 2.0f * ax) + 1e-9f;
+            const float margin = err * inv + 3.6e-7f;
+            const float qx = x * inv, qy = y * inv, qz = zz * inv;
+            const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+            // |frac - 1/2| > 1/2 - margin  <=>  within margin of a face (q - floor(q) and - 1/2 are exact)
+            const float dev = fmaxf(fmaxf(fabsf(qx - fx - 0.5f), fabsf(qy - fy - 0.5f)), fabsf(qz - fz - 0.5f));
+            const float qmax = fmaxf(fmaxf(fabsf(qx), fabsf(qy)), fabsf(qz));
+            valid[k] = z > 0.f && c > 0.f;
+            n_in += valid[k];
+            if (valid[k] && !(dev < 0.5f - margin && qmax <= 1.0e6f)) slow |= 1u << k;
+            // |q| <= 1e6 < 2^20: fast-path cells are always inside the key range
+            cx[k] = (int)fx; cy[k] = (int)fy; cz[k] = (int)fz;
+            ox[k] = x; oy[k] = y; oz[k] = zz;
+        }
+        if (slow) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!(slow & (1u << k))) continue;
+                long long cc[3];
+                exact_cells(a.slot_poses + 8 * slot, a.slot_globals + 8 * slot, ray_coef(u0 + k, a.cx, a.fx),
+                            ray_coef(v_band + r, a.cy, a.fy), zs[k], a.cell, cc);
+                ++n_slow;
+                if (cell_in_range(cc[0]) && cell_in_range(cc[1]) && cell_in_range(cc[2])) {
+                    cx[k] = (int)cc[0]; cy[k] = (int)cc[1]; cz[k] = (int)cc[2];
                 } else {
                     ++n_oor;
-                    valid = false;
+                    valid[k] = false;
                 }
             }
-            n_ovf += vb_insert_warp(a.vb, valid, cxl, cyl, czl, ox, oy, oz, c, 1u, cbk, cidx);
-            if (++u == W) { u = 0; ++r; }
+        }
+        unsigned long long bk[4];
+        int local[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float c = cs[k];
+            ox[k] = c * (ox[k] - (float)cx[k] * cellf);
+            oy[k] = c * (oy[k] - (float)cy[k] * cellf);
+            oz[k] = c * (oz[k] - (float)cz[k] * cellf);
+            bk[k] = valid[k] ? pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2) : kEmpty;
+            local[k] = (cx[k] & 3) | ((cy[k] & 3) << 2) | ((cz[k] & 3) << 4);
+        }
+        // phase B: block indices.  A lane reuses its previous block; lanes
+        // sharing a block elect one leader per pixel slot; the first probes of
+        // the 4 slots are in flight together, and only a first-probe miss
+        // walks the probe chain / inserts.
+        bool need[4];
+        int leader[4];
+        unsigned lead = 0;
+        {
+            unsigned long long prevk = cbk;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                need[k] = valid[k] && bk[k] != prevk;
+                if (valid[k]) prevk = bk[k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            leader[k] = -1;
+            if (__any_sync(0xffffffffu, need[k])) {
+                const unsigned peers = __match_any_sync(0xffffffffu, need[k] ? bk[k] : kEmpty);
+                leader[k] = __ffs(peers) - 1;
+                if (need[k] && lane == leader[k]) lead |= 1u << k;
+            }
+        }
+        int got[4];
+        unsigned long long ek[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            got[k] = -2;
+            ek[k] = kEmpty;
+#ifndef EC3R_EXP_NO_LOOKUP
+            if (lead & (1u << k)) load_entry(a.vb.table + (mix64(bk[k]) & a.vb.tmask), ek[k], got[k]);
+#else
+            if (lead & (1u << k)) { ek[k] = bk[k]; got[k] = (int)(mix64(bk[k]) % 100000ull); }
+#endif
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((lead & (1u << k)) && (ek[k] != bk[k] || got[k] == -1)) got[k] = vb_find_or_insert(a.vb, bk[k]);
+        int last = cidx;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (leader[k] >= 0) {
+                const int g = __shfl_sync(0xffffffffu, got[k], leader[k]);
+                if (need[k]) got[k] = g;
+            }
+            if (valid[k]) {
+                if (need[k]) last = got[k];
+                else got[k] = last;
+            }
+        }
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+            if (valid[k]) { cbk = bk[k]; break; }
+        cidx = last;
+        // phase C: fire-and-forget reductions into the pool
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!valid[k]) continue;
+            if (got[k] < 0) { ++n_ovf; continue; }
+            const size_t e = (size_t)got[k] * kBlockVox + local[k];
+#ifndef EC3R_EXP_NO_RED
+            red_add_v4(a.vb.sums + e, ox[k], oy[k], oz[k], cs[k]);
+#ifndef EC3R_EXP_NO_COUNT
+            atomicAdd(a.vb.counts + e, 1u);
+#endif
+#else
+            if (ox[k] == 12345.f) a.vb.counts[e] = 1;
+#endif
         }
     }
     // counters: warp reduce then one shared atomic per warp, one global per CTA
@@ -683,6 +848,7 @@ extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {
     cudaFree(h->sums);
     cudaFree(h->counts);
     cudaFree(h->counters);
+    cudaFree(h->ftab);
     delete h;
     return EC3R_OK;
 }
@@ -708,16 +874,31 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     if (n == 0) return EC3R_OK;
     FuseArgs a;
     a.depth = depth_pool; a.conf = conf_pool; a.slot_poses = slot_poses; a.slot_globals = slot_globals;
-    a.slots = slots; a.H = H; a.W = W;
+    a.slots = slots; a.n = n; a.H = H; a.W = W;
     a.fx = K4_h[0]; a.fy = K4_h[1]; a.cx = K4_h[2]; a.cy = K4_h[3];
     a.cell = h->cell; a.inv_cell_f = (float)(1.0 / h->cell); a.cell_f = (float)h->cell;
     a.vb = vb_of(h);
-    const size_t smem = (size_t)W * (sizeof(float4) + sizeof(double));
+    const int64_t need = (int64_t)n * (W + H + 1);
+    if (need > h->ftab_cap) {  // grows once per workload shape
+        cudaFree(h->ftab);
+        h->ftab = nullptr;
+        h->ftab_cap = 0;
+        if (cudaMalloc(&h->ftab, sizeof(float4) * (size_t)need) != cudaSuccess) {
+            set_last_error("cudaMalloc(vhash frame tables)", cudaGetLastError());
+            return EC3R_ENOMEM;
+        }
+        h->ftab_cap = need;
+    }
+    a.ftab = h->ftab;
+    cudaStream_t st = as_stream(stream);
+    vh_frame_tables_kernel<<<n, 256, 0, st>>>(a, h->ftab);
+    EC3R_CHECK_LAUNCH("vh_frame_tables_kernel");
+    const size_t smem = sizeof(float4) * (size_t)W;
     if (smem > 48 * 1024)
         EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
-    dim3 grid((H + FI_ROWS - 1) / FI_ROWS, n);
-    vh_insert_frames_kernel<<<grid, FI_NT, smem, as_stream(stream)>>>(a);
+    const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, n);
+    vh_insert_frames_kernel<<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
     return EC3R_OK;
 }
@@ -743,6 +924,7 @@ extern "C" int ec3r_vhash_stats_get(ec3r_vhash* h, ec3r_vhash_stats* out_h, void
     out_h->n_out_of_range = (int64_t)c[1];
     out_h->n_overflow = (int64_t)(c[2] + c[5]);  // dropped points + voxels beyond the emit capacity
     out_h->n_slow_path = (int64_t)c[3];
+    out_h->n_blocks = (int64_t)(c[4] < (unsigned long long)h->max_blocks ? c[4] : (unsigned long long)h->max_blocks);
     return EC3R_OK;
 }
 

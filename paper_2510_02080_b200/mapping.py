@@ -237,7 +237,7 @@ class VoxelMap:
         _lib.check(_lib.lib().ec3r_vhash_stats_get(self._h, C.byref(s), _lib.stream_ptr(stream)),
                    "ec3r_vhash_stats_get")
         return dict(n_points_in=s.n_points_in, n_out_of_range=s.n_out_of_range, n_overflow=s.n_overflow,
-                    n_slow_path=s.n_slow_path)
+                    n_slow_path=s.n_slow_path, n_blocks=s.n_blocks)
 
     def count(self, stream=None) -> int:
         """Number of fused voxels U (synchronises)."""

@@ -1,0 +1,27 @@
+#!/usr/bin/env bash
+# One GPU verification pass (run under gpurun from the repo root):
+#   tools/gpu_check.sh TAG [full]
+# gpu tests, a bench line, the ncu launch list of a short bench and, with
+# "full", one `ncu --set full` capture of the fusion / registration / matcher
+# kernels.  Everything lands in gpurun_out/TAG/.
+set -u
+TAG=${1:?tag}
+MODE=${2:-}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > "$OUT/smi.txt" 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/gpu_tests.log" 2>&1
+echo "tests_rc=$?"
+timeout 600 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.log" 2>&1
+echo "bench_rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k "regex:ec3r|cub" -c 600 --csv \
+    --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
+    > "$OUT/ncu_bench.log" 2>&1
+echo "ncu_rc=$?"
+if [ "$MODE" = "full" ]; then
+    timeout 900 ncu --set full --clock-control none --import-source on \
+        -k "regex:vh_insert_frames_kernel|register_edges_kernel|mt_tc_kernel" -c 3 \
+        -o "$OUT/prof" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+        > "$OUT/ncu_full.log" 2>&1
+    echo "full_rc=$?"
+fi
