@@ -149,7 +149,7 @@ EC3R_API int ec3r_umeyama_batched(const double* p, const double* q, const double
  * reference's float64 transform.  Voxel-block hash: an open-addressing
  * table of 4x4x4 block keys over a pool of dense blocks holding float32
  * sums of conf * (x - voxel corner), sum of conf and a uint32 count.
- * capacity (create) = expected voxels; the pool holds capacity / 8 blocks
+ * capacity (create) = expected voxels; the pool holds capacity / 4 blocks
  * and overflow is reported in n_overflow (grow and re-run).
  * ------------------------------------------------------------------- */
 typedef struct ec3r_vhash ec3r_vhash;

@@ -1,0 +1,199 @@
+"""Multi-GPU plumbing of the path (one process per GPU, torch.distributed).
+
+SURVEY.md §8(e) / DESIGN.md §5:
+
+* align + fuse shard by contiguous submap windows (``shard_window``): edges
+  are independent (mapping.py:171-183), so registration has no collective;
+* the global voxel map is partitioned by voxel key: every rank fuses its own
+  frames into a local hash, buckets the raw partial sums by owner rank
+  (``owner_of`` = mix64(key) mod world, the same hash as the device
+  partitioner in csrc/vhash.cu), exchanges them in one all-to-all
+  (``exchange_partials``) and merges what it owns (``fuse_global``);
+* the retrieval database shards by coarse keyframe rows; the per-shard
+  candidate lists come back in reference emission order when concatenated in
+  rank order (``retrieval_sharded``);
+* the matcher is replicas only (independent frame pairs).
+
+The exchange helpers take tensors on any device, so the protocol runs under
+``gloo`` on CPU in the tests and under NCCL on the GPUs.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+_M1 = 0xFF51AFD7ED558CCD
+_M2 = 0xC4CEB9FE1A85EC53
+
+
+def _world(group) -> tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def shard_window(n_items: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) window of n_items for rank (sizes differ by <= 1)."""
+    base, extra = divmod(int(n_items), int(world))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def mix64(keys) -> np.ndarray:
+    """The device's 64-bit finaliser (csrc/vhash.cu mix64) on uint64 keys."""
+    k = np.asarray(keys).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        k = k ^ (k >> np.uint64(33))
+        k = k * np.uint64(_M1)
+        k = k ^ (k >> np.uint64(33))
+        k = k * np.uint64(_M2)
+        k = k ^ (k >> np.uint64(33))
+    return k
+
+
+def owner_of(keys, world: int) -> np.ndarray:
+    """Owner rank of packed voxel keys: mix64(key) mod world (device rule)."""
+    return (mix64(keys) % np.uint64(world)).astype(np.int64)
+
+
+def gather_ragged(t: torch.Tensor, group=None) -> list[torch.Tensor]:
+    """All-gather tensors whose first dimension differs per rank."""
+    rank, world = _world(group)
+    if world == 1:
+        return [t]
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(max(sizes), 1)
+    pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return [b[:s] for b, s in zip(bufs, sizes)]
+
+
+def exchange_partials(keys: torch.Tensor, sums4: torch.Tensor, counts: torch.Tensor,
+                      rank_counts: Sequence[int], group=None):
+    """One all-to-all of owner-bucketed partials.
+
+    keys (n,) int64, sums4 (n, 4) float32, counts (n,) int32, laid out as
+    contiguous per-owner buckets of sizes rank_counts (the layout
+    ec3r_vhash_extract_partials writes).  Returns the partials this rank
+    owns, received from every rank (rank order)."""
+    rank, world = _world(group)
+    send = [int(c) for c in rank_counts]
+    if world == 1:
+        return keys[: send[0]], sums4[: send[0]], counts[: send[0]]
+    dev = keys.device
+    sc = torch.tensor(send, dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv = [int(x) for x in rc.tolist()]
+    n_in = sum(recv)
+    n_out = sum(send)
+    # one packed payload per row: key (2 x int32 words), 4 float sums, count
+    def pack(k, s, c):
+        return torch.cat([k.view(torch.int32).reshape(-1, 2), s.view(torch.int32).reshape(-1, 4),
+                          c.reshape(-1, 1).to(torch.int32)], dim=1)
+    payload = pack(keys[:n_out], sums4[:n_out], counts[:n_out])
+    out = torch.empty((n_in, 7), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(out, payload, output_split_sizes=recv, input_split_sizes=send, group=group)
+    k = out[:, 0:2].contiguous().view(torch.int64).reshape(-1)
+    s = out[:, 2:6].contiguous().view(torch.float32)
+    c = out[:, 6].contiguous()
+    return k, s, c
+
+
+class MapExchange:
+    """Owner-partitioned global voxel map from per-rank local maps: the
+    partials of a rank's local VoxelMap are bucketed by owner on the device
+    (ec3r_vhash_extract_partials), exchanged in one all-to-all and merged
+    into this rank's owned map (ec3r_vhash_merge_partials), whose sorted
+    emit is the rank's partition of the global map.  Buffers and the owned
+    map persist across calls (no allocation in steady state)."""
+
+    def __init__(self, cell: float, group=None):
+        self.cell = float(cell)
+        self.group = group
+        self.rank, self.world = _world(group)
+        self.owned = None
+        self._buf = None
+        self.out = None
+
+    def _buffers(self, n: int):
+        if self._buf is None or self._buf[0].shape[0] < n:
+            m = max(n, 1)
+            self._buf = (torch.empty(m, dtype=torch.int64, device="cuda"),
+                         torch.empty((m, 4), dtype=torch.float32, device="cuda"),
+                         torch.empty(m, dtype=torch.int32, device="cuda"),
+                         torch.zeros(self.world, dtype=torch.int64, device="cuda"))
+        return self._buf
+
+    def run(self, local, n_local: int, stream=None):
+        """local: this rank's fused VoxelMap holding n_local voxels."""
+        from . import _lib
+        from .mapping import VoxelMap
+
+        L = _lib.lib()
+        keys, sums4, cnt, rank_counts = self._buffers(n_local)
+        rank_counts.zero_()
+        wsb = L.ec3r_vhash_extract_workspace(local.handle) + 1024
+        ws = _lib.workspace(wsb, keys.device, "partials")
+        _lib.check(L.ec3r_vhash_extract_partials(local.handle, self.world, _lib.ptr(keys), _lib.ptr(sums4),
+                                                 _lib.ptr(cnt), _lib.ptr(rank_counts), _lib.ptr(ws), ws.numel(),
+                                                 _lib.stream_ptr(stream)), "ec3r_vhash_extract_partials")
+        rk, rs, rcnt = exchange_partials(keys, sums4, cnt, rank_counts.tolist(), self.group)
+        n = int(rk.shape[0])
+        while True:  # grow until neither the merge nor the emit overflows
+            if self.owned is None or self.owned.expected < n:
+                self.owned = VoxelMap(self.cell, capacity=max(2 * n, 1 << 16))
+            self.owned.clear(stream)
+            if n:
+                _lib.check(L.ec3r_vhash_merge_partials(self.owned.handle, _lib.ptr(rk), _lib.ptr(rs),
+                                                       _lib.ptr(rcnt), n, _lib.stream_ptr(stream)),
+                           "ec3r_vhash_merge_partials")
+            if self.owned.stats(stream)["n_overflow"] == 0:
+                if self.out is None or self.out[0].shape[0] < n:
+                    self.out = (torch.empty(max(n, 1), dtype=torch.int64, device="cuda"),
+                                torch.empty((max(n, 1), 3), dtype=torch.float32, device="cuda"),
+                                torch.empty(max(n, 1), dtype=torch.float32, device="cuda"),
+                                torch.empty(max(n, 1), dtype=torch.int32, device="cuda"))
+                res = self.owned.extract(sort=True, stream=stream, out=self.out)
+                if self.owned.stats(stream)["n_overflow"] == 0:
+                    return res
+            self.owned = VoxelMap(self.cell, capacity=4 * max(self.owned.expected, 2 * n))
+
+
+def fuse_global(pool, slots: torch.Tensor, cell: float, group=None, capacity: Optional[int] = None):
+    """Global voxel map over all ranks' frames: local fusion, owner-bucketed
+    partials, one all-to-all, owner-side merge.  Returns this rank's owned
+    partition (keys sorted ascending, centroid, wsum, count)."""
+    from .mapping import fuse_slots
+
+    local, out, _ = fuse_slots(pool, slots, cell, expected_voxels=capacity)
+    if _world(group)[1] == 1:
+        return out
+    return MapExchange(cell, group).run(local, int(out[0].shape[0]))
+
+
+def retrieval_sharded(db, stride: int, exclusion: int, tau_g: float, tau_l: float, group=None):
+    """Sharded K6: rank r scores the coarse rows of its window; the lists
+    concatenated in rank order are the single-GPU lists (reference emission
+    order).  Returns the six numpy arrays of loops.retrieval_device."""
+    rank, world = _world(group)
+    kc = (db.n + stride - 1) // stride
+    lo, hi = shard_window(kc, world, rank)
+    parts = db.score(stride, exclusion, tau_g, tau_l, lo, hi)
+    if world == 1:
+        return parts
+    dev = db.vec.device
+    merged = []
+    for a in parts:
+        t = torch.as_tensor(np.ascontiguousarray(a), device=dev)
+        merged.append(torch.cat(gather_ragged(t, group)).cpu().numpy())
+    return tuple(merged)

@@ -1,0 +1,211 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the N>1 host protocol:
+window sharding, ragged all-gather, the owner-bucketed all-to-all of voxel
+partials and the owner-side merge, checked against the single-process oracle
+fusion (oracle/fuse.py).  The device halves of the protocol
+(ec3r_vhash_extract_partials / merge_partials) are covered by the GPU tests."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import fuse as ofuse
+from paper_2510_02080_b200 import dist as D
+
+WORLD = 2
+CELL = 0.02
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn_name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, globals()[fn_name](rank, world)))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(fn_name, world=WORLD):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn_name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, v = q.get(timeout=120)
+        out[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        if isinstance(v, Exception):
+            raise v
+    return out
+
+
+# ---------------------------------------------------------------------------
+# helpers shared by the workers (module level: picklable under spawn)
+
+def _points(seed, n=20000):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-0.3, 0.3, size=(n, 3))
+    conf = rng.uniform(0.05, 1.0, size=n)
+    conf[rng.random(n) < 0.05] = 0.0  # dropped by rule (ii)
+    return x, conf
+
+
+def _local_partials(x, conf, world):
+    """What one rank's device hash holds after fusing its own points, as the
+    raw partials ec3r_vhash_extract_partials emits: (key, sum c*(x - corner),
+    sum c, count) bucketed by owner rank."""
+    live = conf > 0
+    x, conf = x[live], conf[live]
+    cells = ofuse.voxel_cells(x, CELL)
+    from oracle.ref_numpy import pack
+    keys = pack(cells)
+    uniq, inv = np.unique(keys, return_inverse=True)
+    corner = cells * CELL
+    s = np.zeros((len(uniq), 4))
+    np.add.at(s[:, :3], inv, conf[:, None] * (x - corner))
+    np.add.at(s[:, 3], inv, conf)
+    cnt = np.bincount(inv, minlength=len(uniq)).astype(np.int32)
+    own = D.owner_of(uniq, world)
+    order = np.argsort(own, kind="stable")
+    rank_counts = np.bincount(own, minlength=world)
+    return uniq[order].astype(np.int64), s[order].astype(np.float32), cnt[order], rank_counts
+
+
+def _merge(keys, sums4, cnt):
+    uniq, inv = np.unique(keys, return_inverse=True)
+    s = np.zeros((len(uniq), 4))
+    np.add.at(s, inv, sums4.astype(np.float64))
+    c = np.bincount(inv, weights=cnt, minlength=len(uniq)).astype(np.int64)
+    return uniq, s, c
+
+
+# ---------------------------------------------------------------------------
+# workers
+
+def w_exchange(rank, world):
+    rng = np.random.default_rng(rank)
+    n = 1000 + 337 * rank
+    keys = rng.integers(0, 1 << 62, size=n, dtype=np.int64)
+    sums = rng.standard_normal((n, 4)).astype(np.float32)
+    cnt = rng.integers(1, 50, size=n).astype(np.int32)
+    own = D.owner_of(keys, world)
+    order = np.argsort(own, kind="stable")
+    rc = np.bincount(own, minlength=world)
+    k, s, c = D.exchange_partials(torch.as_tensor(keys[order]), torch.as_tensor(sums[order]),
+                                  torch.as_tensor(cnt[order]), rc.tolist())
+    return k.numpy(), s.numpy(), c.numpy()
+
+
+def w_global_fusion(rank, world):
+    x, conf = _points(7, 30000)
+    lo, hi = D.shard_window(len(x), world, rank)
+    keys, sums4, cnt, rc = _local_partials(x[lo:hi], conf[lo:hi], world)
+    k, s, c = D.exchange_partials(torch.as_tensor(keys), torch.as_tensor(sums4), torch.as_tensor(cnt),
+                                  rc.tolist())
+    return _merge(k.numpy(), s.numpy(), c.numpy())
+
+
+def w_gather(rank, world):
+    t = torch.arange(3 + 4 * rank, dtype=torch.int64) + 100 * rank
+    return [g.numpy() for g in D.gather_ragged(t)]
+
+
+# ---------------------------------------------------------------------------
+# tests
+
+def test_shard_window_partitions():
+    for n in (0, 1, 5, 59, 60, 61, 1000):
+        for world in (1, 2, 3, 8):
+            ws = [D.shard_window(n, world, r) for r in range(world)]
+            assert ws[0][0] == 0 and ws[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(ws, ws[1:]))
+            sizes = [b - a for a, b in ws]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_owner_hash_matches_device_rule():
+    # mix64 of csrc/vhash.cu (murmur3 finaliser) on known values
+    k = np.array([0, 1, 2, (1 << 63) - 1], dtype=np.uint64)
+    m = D.mix64(k)
+    assert m[0] == 0
+    ref = []
+    for v in k.tolist():
+        v ^= v >> 33
+        v = (v * 0xFF51AFD7ED558CCD) & ((1 << 64) - 1)
+        v ^= v >> 33
+        v = (v * 0xC4CEB9FE1A85EC53) & ((1 << 64) - 1)
+        v ^= v >> 33
+        ref.append(v)
+    assert m.tolist() == ref
+    own = D.owner_of(np.arange(10000), 8)
+    assert set(own.tolist()) == set(range(8))
+
+
+def test_gather_ragged_gloo():
+    out = _spawn("w_gather")
+    for r in range(WORLD):
+        got = out[r]
+        assert len(got) == WORLD
+        for src in range(WORLD):
+            np.testing.assert_array_equal(got[src], np.arange(3 + 4 * src) + 100 * src)
+
+
+def test_exchange_partials_routes_every_row_to_its_owner_gloo():
+    out = _spawn("w_exchange")
+    # reconstruct what every rank sent
+    sent = []
+    for r in range(WORLD):
+        rng = np.random.default_rng(r)
+        n = 1000 + 337 * r
+        keys = rng.integers(0, 1 << 62, size=n, dtype=np.int64)
+        sums = rng.standard_normal((n, 4)).astype(np.float32)
+        cnt = rng.integers(1, 50, size=n).astype(np.int32)
+        sent.append((keys, sums, cnt))
+    for r in range(WORLD):
+        k, s, c = out[r]
+        assert np.all(D.owner_of(k, WORLD) == r)
+        exp_k = np.concatenate([kk[D.owner_of(kk, WORLD) == r] for kk, _, _ in sent])
+        exp_s = np.concatenate([ss[D.owner_of(kk, WORLD) == r] for kk, ss, _ in sent])
+        exp_c = np.concatenate([cc[D.owner_of(kk, WORLD) == r] for kk, _, cc in sent])
+        np.testing.assert_array_equal(k, exp_k)  # rank order, bucket order preserved
+        np.testing.assert_array_equal(s, exp_s)
+        np.testing.assert_array_equal(c, exp_c)
+
+
+def test_global_fusion_protocol_equals_single_process_oracle_gloo():
+    out = _spawn("w_global_fusion")
+    x, conf = _points(7, 30000)
+    ref = ofuse.fuse_points(x, conf, CELL)
+    keys = np.concatenate([out[r][0] for r in range(WORLD)])
+    sums = np.concatenate([out[r][1] for r in range(WORLD)])
+    cnt = np.concatenate([out[r][2] for r in range(WORLD)])
+    order = np.argsort(keys)
+    keys, sums, cnt = keys[order], sums[order], cnt[order]
+    # every voxel owned by exactly one rank, keys / counts bit-exact
+    np.testing.assert_array_equal(keys, ref["keys"])
+    np.testing.assert_array_equal(cnt, ref["count"])
+    np.testing.assert_allclose(sums[:, 3], ref["wsum"], rtol=1e-5)
+    from oracle.ref_numpy import unpack
+    corner = unpack(keys).astype(np.float64) * CELL
+    cen = corner + sums[:, :3] / sums[:, 3:4]
+    assert np.max(np.abs(cen - ref["centroid"])) < 1e-4

@@ -330,6 +330,60 @@ def test_voxel_points_api_and_extreme_coordinates():
     assert np.max(np.abs(c - o["centroid"])) < 1e-3  # float32 output at 2 km
 
 
+def test_voxel_partials_owner_buckets_and_merge_roundtrip():
+    """Multi-GPU device half: extract_partials buckets every voxel by
+    owner = mix64(key) mod n (dist.owner_of), and merging all buckets into a
+    fresh table reproduces the local map exactly (keys, counts) and within
+    float32 re-association (sums)."""
+    from paper_2510_02080_b200 import _lib, dist as pdist, mapping
+    rng = np.random.default_rng(11)
+    p = rng.normal(size=(200_000, 3)) * 0.5
+    conf = rng.uniform(0.1, 1.0, size=len(p))
+    vm = mapping.VoxelMap(0.02, 1 << 21)
+    vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"),
+                     [1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0])
+    k0, c0, w0, n0 = (x.cpu().numpy() for x in vm.extract())
+    U = len(k0)
+    for n_ranks in (1, 3, 8):
+        L = _lib.lib()
+        keys = torch.empty(U, dtype=torch.int64, device="cuda")
+        sums = torch.empty((U, 4), dtype=torch.float32, device="cuda")
+        cnt = torch.empty(U, dtype=torch.int32, device="cuda")
+        rc = torch.zeros(n_ranks, dtype=torch.int64, device="cuda")
+        ws = torch.empty(L.ec3r_vhash_extract_workspace(vm.handle) + 1024, dtype=torch.uint8, device="cuda")
+        _lib.check(L.ec3r_vhash_extract_partials(vm.handle, n_ranks, _lib.ptr(keys), _lib.ptr(sums), _lib.ptr(cnt),
+                                                 _lib.ptr(rc), _lib.ptr(ws), ws.numel(), None), "partials")
+        rcn = rc.cpu().numpy()
+        assert rcn.sum() == U
+        kn = keys.cpu().numpy()
+        off = np.concatenate([[0], np.cumsum(rcn)])
+        for r in range(n_ranks):
+            assert np.all(pdist.owner_of(kn[off[r]:off[r + 1]], n_ranks) == r)
+        merged = mapping.VoxelMap(0.02, 1 << 21)
+        _lib.check(L.ec3r_vhash_merge_partials(merged.handle, _lib.ptr(keys), _lib.ptr(sums), _lib.ptr(cnt), U,
+                                               None), "merge")
+        k1, c1, w1, n1 = (x.cpu().numpy() for x in merged.extract())
+        np.testing.assert_array_equal(k1, k0)
+        np.testing.assert_array_equal(n1, n0)
+        np.testing.assert_allclose(w1, w0, rtol=1e-6)
+        assert np.max(np.abs(c1 - c0)) < 1e-6
+
+
+def test_fuse_global_single_rank_equals_local():
+    from paper_2510_02080_b200 import dist as pdist, mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(6, cfg, seed=2, device="cuda")
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms = [dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    dm.register_chain(sms)
+    slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
+    k, c, w, n = (x.cpu().numpy() for x in pdist.fuse_global(dm.pool, slots, 0.02))
+    out = dm.fused_cloud(voxel=0.02)
+    np.testing.assert_array_equal(k, out["keys"])
+    np.testing.assert_array_equal(n, out["count"])
+
+
 # --------------------------------------------------------------------------
 # K5 matcher (bit-exact matches)
 

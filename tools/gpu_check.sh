@@ -14,7 +14,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/gpu_tests.log" 2>&1
 echo "tests_rc=$?"
 timeout 600 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.log" 2>&1
 echo "bench_rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k "regex:ec3r|cub" -c 600 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k "regex:ec3r::|CUB_200802" -c 600 --csv \
     --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
     > "$OUT/ncu_bench.log" 2>&1
 echo "ncu_rc=$?"
