@@ -21,12 +21,15 @@ void set_last_error(const char* where, cudaError_t e) {
 }
 void set_last_error_msg(const char* msg) { snprintf(g_last_error, sizeof(g_last_error), "%s", msg); }
 
-// tensor-core approximate pass (match_tc.cu)
-int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x, const int64_t* a_off_d,
-                 const int64_t* b_off_d, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
-                 int exact_dtype, double norm_bound, double ratio, MatchRowState* rs, int32_t* col_best,
-                 int32_t* flag_rows, int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes,
+// tensor-core approximate pass + certification (match_tc.cu)
+int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, const int64_t* b_off_d,
+                 const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
+                 double norm_bound, double ratio, MatchRowState* rs, int32_t* flag_rows, int32_t* flag_cols,
+                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, double* eps_out,
                  cudaStream_t st);
+int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
+                       const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
+                       int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st);
 size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs);
 
 }  // namespace ec3r
@@ -74,12 +77,26 @@ extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const vo
     EC3R_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 8, st));
     int rc;
     if (A != nullptr && B != nullptr && total_a > 0 && total_b > 0) {
-        // tensor-core pass: certifies most rows / columns and lists the rest
-        rc = match_tc_run(A, B, A_x, B_x, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound, ratio,
-                          rs, col_best, flag_rows, flag_cols, counters, tc_ws, tc_bytes, st);
+        // tensor-core pass: certifies most rows and lists the rest; the
+        // passing rows' mutual checks then list the columns they need
+        int tc_used = 0;
+        double eps_tc = 0.0;
+        rc = match_tc_run(A, B, a_off, b_off, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound, ratio, rs,
+                          flag_rows, flag_cols, counters, tc_ws, tc_bytes, &tc_used, &eps_tc, st);
         if (rc) return rc;
-        rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
-                                  flag_cols, counters + 1, 0, rs, col_best, st);
+        if (tc_used) {
+            rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
+                                      nullptr, nullptr, 0, rs, col_best, st);
+            if (rc) return rc;
+            rc = match_tc_need_cols(a_off, b_off, a_off_h, b_off_h, n_pairs, ratio, eps_tc, rs, col_best, flag_cols,
+                                    counters, tc_ws, st);
+            if (rc) return rc;
+            rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, nullptr, nullptr, 0,
+                                      flag_cols, counters + 1, 0, rs, col_best, st);
+        } else {
+            rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, flag_rows, counters + 0, 0,
+                                      flag_cols, counters + 1, 0, rs, col_best, st);
+        }
     } else {
         rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, n_pairs, nullptr, nullptr, total_a, nullptr,
                                   nullptr, total_b, rs, col_best, st);

@@ -11,6 +11,8 @@ struct MatchRowState {
     double d2;   // second order statistic of the row's d2 values
     int32_t best;  // best column within the pair (first index on ties), -1 if none
     int32_t ratio_ok;  // -1: decide from (d1, d2); 0 / 1: ratio test already certified reject / pass
+    int32_t mutual;    // -1: decide from col_best; 0 / 1: mutual check certified (tracking.py:160-162)
+    int32_t pad;
 };
 
 // 16-byte row chunks widened to float64 (rows are 16-byte aligned: D is

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A,
             rs[r].d1 = m1;
             rs[r].d2 = m2;
             rs[r].ratio_ok = -1;
+            rs[r].mutual = -1;
         }
         __syncthreads();
     }
@@ -173,11 +174,11 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
     const int64_t a0 = a_off[p], b0 = b_off[p], m = b_off[p + 1] - b0;
     int out = -1;
     const MatchRowState s = rs[r];
-    if (m > 0 && s.best >= 0 && col_best[b0 + s.best] == (int)(r - a0)) {
-        bool ok = true;
-        if (s.ratio_ok >= 0) ok = s.ratio_ok != 0;  // certified from the tensor-core values
-        else if (m > 1 && s.d1 > ratio2 * s.d2) ok = false;
-        if (ok) out = s.best;
+    if (m > 0 && s.best >= 0) {
+        bool keep;
+        if (s.ratio_ok >= 0) keep = s.ratio_ok != 0;  // certified from the tensor-core keys
+        else keep = !(m > 1 && s.d1 > ratio2 * s.d2);
+        if (keep && (s.mutual == 1 || (s.mutual == -1 && col_best[b0 + s.best] == (int)(r - a0)))) out = s.best;
     }
     match_b[r] = out;
     // one atomic per (warp, pair) instead of one per match

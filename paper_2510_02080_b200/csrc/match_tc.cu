@@ -1,5 +1,5 @@
 // K5 (tensor-core side): descriptor similarity on tcgen05 with a fused
-// top-k epilogue, sm_100a.
+// top-2 epilogue, sm_100a.
 //
 // Replaces the dgemm + argmin/partition of match_descriptors
 // (tracking.py:152-166).  One persistent CTA per SM walks work units
@@ -10,16 +10,24 @@
 //   warp 1    TMEM allocator + single-thread tcgen05.mma issuer
 //             (kind::f16, bf16 x bf16 -> fp32, M=128 N=128 K=16) into a
 //             double-buffered 2 x 256-column TMEM accumulator;
-//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> per-row running top-3
-//             (registers) and per-column top-2 over the unit's rows
-//             (REDUX.MAX on 32-bit keys that embed the lane), merged in
-//             shared memory and folded into global per-column state with
+//   warps 2-9 epilogue.  Each similarity becomes one 32-bit KEY: its fp32
+//             bits with the 11 low mantissa bits replaced by a code — the
+//             column within the 32-column chunk (row side) and the
+//             (A block, lane) of its row (column side) — so a plain float
+//             max/min returns the argmax with the value, and the epilogue is
+//             ~6 ALU ops per similarity: 1 LOP3 key, per-row top-2 over
+//             pairs (FMNMX / FMNMX3), per-column top-2 of the warp's 64 rows
+//             with two CREDUX.MAX.F32 per column; the 4 lane quarters merge
+//             in shared memory and fold into global per-column state with
 //             two atomics per column.
-// The N x M similarity matrix never exists in memory.  Approximate values
-// then go through certification (mt_certify_*): every decision is either
-// proven from the fp32 values plus an error bound or listed for the float64
-// re-scan of match_exact.cu, so the matches are bit-identical to the float64
-// reference.
+// The N x M similarity matrix never exists in memory.  The key values are
+// within eps_tc + 2^-12 |key| of the exact similarity, and certification
+// (mt_decide_rows / mt_need_cols) proves every decision from them or lists
+// it for the float64 re-scan of match_exact.cu, so the matches are
+// bit-identical to the float64 reference.  A row is only re-scanned when its
+// ratio test (tracking.py:167) is undecided, or it passes with an undecided
+// argmax; a column only when a passing row needs its argmax and the keys do
+// not settle it.
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -34,18 +42,22 @@ constexpr int TC_NA = 2;         // A blocks resident per unit
 constexpr int TC_BN = 128;       // columns per B tile (UMMA N)
 constexpr int TC_BK = 64;        // bf16 per 128-byte swizzle row
 constexpr int TC_STAGES = 4;     // B ring depth
-constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: one per A block
+constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: one per column half
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;  // producer + MMA + epilogue warps
 constexpr int TC_BOX_BYTES = TC_BM * TC_BK * 2;  // 16 KB (A box and B box alike)
 constexpr int TC_TMEM_COLS = 512;
 
-// Per A-row approximate top-4 (value, column): the first three are re-scored
-// in float64, the fourth bounds every other column.
-constexpr int TC_TOPK = 4;
+// Similarity keys: fp32 bits, low 11 mantissa bits = code.
+constexpr uint32_t KEY_MASK = 0xFFFFF800u;
+constexpr float KEY_NEG = -3.0e38f;  // invalid row / column: below every real key, finite after coding
+
+// Per A-row approximate top-2 keys and the best column (within the pair).
 struct __align__(16) RowCand {
-    float v[TC_TOPK];
-    int32_t c[TC_TOPK];
+    float k1;
+    float k2;
+    int32_t c1;
+    int32_t pad;
 };
 
 struct TcParams {
@@ -54,10 +66,9 @@ struct TcParams {
     const int2* units;  // (pair, first row of the unit within the packed A)
     int n_units;
     int kblocks;        // D / 64
-    float bias;         // makes every similarity + bias positive (ordered keys)
     RowCand* cand;
-    unsigned long long* col_key;
-    unsigned int* col_second;
+    unsigned long long* col_key;   // (ordered key << 32) | (~row): best row of the column
+    unsigned int* col_second;      // ordered key of the column's second row (0 = none)
 };
 
 // ---------------------------------------------------------------------------
@@ -124,7 +135,9 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// tcgen05.ld without the wait (the caller issues tcgen05.wait::ld before
+// touching the registers, then pins them with reg_fence)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
         "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
@@ -133,7 +146,51 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
+
+__device__ __forceinline__ void sts_f2(uint32_t addr, float a, float b) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float warp_max_f32(float x) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// key = value bits above bit 11, code below: bimm = KEY_MASK | column code
+// (an immediate), creg = KEY_MASK | row code; the two codes occupy disjoint
+// bits, so (a & b & c) | (b ^ c) is the whole key in one LOP3.
+__device__ __forceinline__ float make_key(uint32_t v, uint32_t bimm, uint32_t creg) {
+    return __uint_as_float((v & bimm & creg) | (bimm ^ creg));
+}
+
+// order-preserving float <-> uint32 (0 is below every finite key)
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o ^ 0x80000000u) : ~o);
 }
 
 // Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
@@ -154,7 +211,67 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-// ---------------------------------------------------------------------------
+// Epilogue of one 32-column chunk of the thread's two rows (r0: A block 0,
+// r1: A block 1).  Row side: the chunk's top-2 keys per row folded into the
+// running (best, second, chunk base of best).  Column side: per column the
+// top-2 keys over the warp's 64 rows, written to cb[j] by lane 0.
+struct RowTop2 {
+    float b, s;
+    int cb;  // column base of the chunk holding b (b's code has the column within the chunk)
+};
+
+__device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[32], uint32_t (&r1)[32], int nv0, int nv1, int cbase,
+                                               uint32_t creg0, uint32_t creg1, RowTop2& R0, RowTop2& R1,
+                                               uint32_t cb, int lane) {
+    // interior chunks (every row and column valid) skip the predicates
+    if (!__all_sync(0xffffffffu, nv0 == 32 && nv1 == 32)) {
+        const uint32_t neg = __float_as_uint(KEY_NEG);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j >= nv0) r0[j] = neg;
+            if (j >= nv1) r1[j] = neg;
+        }
+    }
+    float k0[32], k1[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        k0[j] = make_key(r0[j], KEY_MASK | ((uint32_t)j << 6), creg0);
+        k1[j] = make_key(r1[j], KEY_MASK | ((uint32_t)j << 6), creg1);
+    }
+    // row side: top-2 over pairs (hi, lo) — 5 ops per 2 keys per row
+    {
+        float m0 = fmaxf(k0[0], k0[1]), s0 = fminf(k0[0], k0[1]);
+        float m1 = fmaxf(k1[0], k1[1]), s1 = fminf(k1[0], k1[1]);
+#pragma unroll
+        for (int j = 2; j < 32; j += 2) {
+            const float h0 = fmaxf(k0[j], k0[j + 1]), l0 = fminf(k0[j], k0[j + 1]);
+            const float t0 = fminf(m0, h0);
+            m0 = fmaxf(m0, h0);
+            s0 = fmax3f(s0, l0, t0);
+            const float h1 = fmaxf(k1[j], k1[j + 1]), l1 = fminf(k1[j], k1[j + 1]);
+            const float t1 = fminf(m1, h1);
+            m1 = fmaxf(m1, h1);
+            s1 = fmax3f(s1, l1, t1);
+        }
+        const float t0 = fminf(R0.b, m0);
+        R0.cb = m0 > R0.b ? cbase : R0.cb;
+        R0.b = fmaxf(R0.b, m0);
+        R0.s = fmax3f(R0.s, s0, t0);
+        const float t1 = fminf(R1.b, m1);
+        R1.cb = m1 > R1.b ? cbase : R1.cb;
+        R1.b = fmaxf(R1.b, m1);
+        R1.s = fmax3f(R1.s, s1, t1);
+    }
+    // column side: fold the thread's two rows, then top-1 / top-2 over the
+    // warp (keys are unique within a column: the code holds block and lane)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const float hi = fmaxf(k0[j], k1[j]), lo = fminf(k0[j], k1[j]);
+        const float m = warp_max_f32(hi);
+        const float m2 = warp_max_f32(hi == m ? lo : hi);
+        if (lane == 0) sts_f2(cb + 8u * j, m, m2);
+    }
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
@@ -164,8 +281,9 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const int KB = p.kblocks;
     unsigned char* sA = smem;                                   // TC_NA * KB boxes
     unsigned char* sB = sA + (size_t)TC_NA * KB * TC_BOX_BYTES;  // TC_STAGES boxes
-    uint2* colbuf = (uint2*)(sB + (size_t)TC_STAGES * TC_BOX_BYTES);  // [TC_NA*4][TC_BN]
-    uint64_t* bars = (uint64_t*)(colbuf + TC_NA * 4 * TC_BN);
+    float2* colbuf = (float2*)(sB + (size_t)TC_STAGES * TC_BOX_BYTES);  // [2 tiles][4 quarters][TC_BN]
+    float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);                     // [TC_NA * TC_BM] half-row summaries
+    uint64_t* bars = (uint64_t*)(rsc + TC_NA * TC_BM);
     uint64_t* a_full = bars + 0;
     uint64_t* a_empty = bars + 1;
     uint64_t* b_full = bars + 2;
@@ -272,162 +390,110 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // ===================== epilogue (warps 2..9) =====================
         // warp -> (TMEM lane quarter q, column half h).  Each thread owns two
         // rows — row q*32+lane of both A blocks — over the tile's 64 columns
-        // [h*64, h*64+64): the two values of a column are folded in-thread
-        // (max / min) before the warp reductions, halving the CREDUX count.
-        // Column keys embed (block, lane) in their 6 low bits.
+        // [h*64, h*64+64), as two 32-column chunks (the second chunk's TMEM
+        // load is in flight while the first is reduced).
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
         const int et = threadIdx.x - 64;  // 0..255
-        const uint32_t code0 = 63u - (uint32_t)lane;        // block 0 (preferred on equal keys: smaller row)
-        const uint32_t code1 = 31u - (uint32_t)lane;        // block 1
+        const uint32_t creg0 = KEY_MASK | (uint32_t)lane;         // A block 0
+        const uint32_t creg1 = KEY_MASK | 32u | (uint32_t)lane;   // A block 1
         int acc = 0;
         uint32_t acc_phase = 0;
+        int tb = 0;  // colbuf double buffer (alternates over all tiles of the CTA)
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             const int2 un = p.units[u];
             const int64_t a1 = p.a_off[un.x + 1], a0 = p.a_off[un.x];
             const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (M + TC_BN - 1) / TC_BN;
-            // row state: best value / column and the second value (order
-            // statistic, duplicates count) — all the decision stage needs
-            float b0v = -INFINITY, s0v = -INFINITY, b1v = -INFINITY, s1v = -INFINITY;
-            int b0c = -1, b1c = -1;
+            RowTop2 R0{-INFINITY, -INFINITY, 0}, R1{-INFINITY, -INFINITY, 0};
             const int64_t row0 = (int64_t)un.y + q * 32 + lane, row1 = row0 + TC_BM;
             const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
                 const int col0 = t * TC_BN;
-#pragma unroll 1
-                for (int ch = 0; ch < 2; ++ch) {
-                    const int cl = h * 64 + ch * 32;  // column offset within the tile
-                    uint32_t r0[32], r1[32];
-                    const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + cl);
-                    tmem_ld32(ta, r0);
-                    tmem_ld32(ta + TC_BN, r1);
-                    const int cbase = col0 + cl;
-                    const int ncol = min(32, M - cbase);  // valid columns (may be <= 0)
-                    const int nv0 = rv0 ? ncol : 0, nv1 = rv1 ? ncol : 0;
-                    // interior chunks (every row and column valid) skip all
-                    // per-element predicates: warp-uniform fast path
-                    const bool full = __all_sync(0xffffffffu, nv0 == 32 && nv1 == 32);
-                    if (!full) {
-                        // invalid entries become -bias: below every real value
-                        // (|sim| <= bias / 2) and mapping to a zero-value key
-                        const uint32_t sentinel = __float_as_uint(-p.bias);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if (j >= nv0) r0[j] = sentinel;
-                            if (j >= nv1) r1[j] = sentinel;
-                        }
-                    }
-                    // row side, branch-free: second = max(second, min(v, best));
-                    // strict > keeps the first column on equal values
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float v0 = __uint_as_float(r0[j]), v1 = __uint_as_float(r1[j]);
-                        s0v = fmaxf(s0v, fminf(v0, b0v));
-                        b0c = v0 > b0v ? cbase + j : b0c;
-                        b0v = fmaxf(b0v, v0);
-                        s1v = fmaxf(s1v, fminf(v1, b1v));
-                        b1c = v1 > b1v ? cbase + j : b1c;
-                        b1v = fmaxf(b1v, v1);
-                    }
-                    // column side: per column fold the thread's two rows, then
-                    // top-1 and top-2 over the warp's 64 rows.  Invalid entries
-                    // (-bias) map to zero-value keys.  All 32 first reductions
-                    // are issued before the dependent second ones.
-                    uint32_t hi[32], lo[32], m[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t k0 = (__float_as_uint(__uint_as_float(r0[j]) + p.bias) & 0xFFFFFFC0u) | code0;
-                        const uint32_t k1 = (__float_as_uint(__uint_as_float(r1[j]) + p.bias) & 0xFFFFFFC0u) | code1;
-                        hi[j] = max(k0, k1);
-                        lo[j] = min(k0, k1);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) m[j] = __reduce_max_sync(0xffffffffu, hi[j]);
-                    uint32_t cm = 0, cm2 = 0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t m2 = __reduce_max_sync(0xffffffffu, hi[j] == m[j] ? lo[j] : hi[j]);
-                        cm = (lane == j) ? m[j] : cm;
-                        cm2 = (lane == j) ? m2 : cm2;
-                    }
-                    colbuf[q * TC_BN + cl + lane] = make_uint2(cm, cm2);
+                const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + h * 64);
+                const uint32_t cbq = smem_u32(colbuf + (size_t)(tb * 4 + q) * TC_BN + h * 64);
+                uint32_t ra[32], rb[32], rc[32], rd[32];
+                tmem_ld32_async(ta, ra);
+                tmem_ld32_async(ta + TC_BN, rb);
+                tmem_wait_ld();
+                reg_fence(ra);
+                reg_fence(rb);
+                tmem_ld32_async(ta + 32, rc);
+                tmem_ld32_async(ta + TC_BN + 32, rd);
+                {
+                    const int cbase = col0 + h * 64;
+                    const int ncol = min(32, M - cbase);
+                    chunk_epilogue(ra, rb, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq, lane);
                 }
+                tmem_wait_ld();
+                reg_fence(rc);
+                reg_fence(rd);
                 // accumulator drained: hand the TMEM buffer back to the MMA warp
                 tc_fence_before();
                 mbar_arrive(t_empty + acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                named_sync(1, TC_EPI_THREADS);
-                // merge the 4 quarter partials of column et and fold into the global state
-                if (et < TC_BN && col0 + et < M) {
-                    unsigned long long best = 0;
-                    uint32_t second = 0;
-#pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) {
-                        const uint2 c = colbuf[qq * TC_BN + et];
-                        if ((c.x & 0xFFFFFFC0u) == 0) continue;  // no valid row in this quarter
-                        const uint32_t code = c.x & 63u;
-                        const int bb = code >= 32 ? 0 : 1;
-                        const int lanew = (bb == 0 ? 63 : 31) - (int)code;
-                        const int64_t row = (int64_t)un.y - a0 + bb * TC_BM + qq * 32 + lanew;
-                        const unsigned long long gk =
-                            ((unsigned long long)(c.x & 0xFFFFFFC0u) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
-                        const uint32_t c2v = c.y & 0xFFFFFFC0u;  // zero-value keys contribute 0
-                        if (gk > best) {
-                            second = max(second, max(c2v, (uint32_t)(best >> 32)));
-                            best = gk;
-                        } else {
-                            second = max(second, c.x & 0xFFFFFFC0u);
-                        }
-                    }
-                    if (best) {
-                        const int64_t gc = b0 + col0 + et;
-                        const unsigned long long old = atomicMax(p.col_key + gc, best);
-                        const uint32_t loser = (uint32_t)((old > best ? best : old) >> 32);
-                        const uint32_t sec = max(second, loser);
-                        if (sec) atomicMax(p.col_second + gc, sec);
-                    }
+                {
+                    const int cbase = col0 + h * 64 + 32;
+                    const int ncol = min(32, M - cbase);
+                    chunk_epilogue(rc, rd, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq + 256u,
+                                   lane);
                 }
                 named_sync(1, TC_EPI_THREADS);
+                // merge the 4 quarter partials of column et and fold into the
+                // global state (colbuf is double-buffered: the next tile
+                // writes the other half, so one barrier per tile suffices)
+                if (et < TC_BN && col0 + et < M) {
+                    const uint32_t cb = smem_u32(colbuf + (size_t)tb * 4 * TC_BN + et);
+                    const float2 v0 = lds_f2(cb), v1 = lds_f2(cb + 8u * TC_BN), v2 = lds_f2(cb + 16u * TC_BN),
+                                 v3 = lds_f2(cb + 24u * TC_BN);
+                    const float h01 = fmaxf(v0.x, v1.x), l01 = fminf(v0.x, v1.x);
+                    const float h23 = fmaxf(v2.x, v3.x), l23 = fminf(v2.x, v3.x);
+                    const float bk = fmaxf(h01, h23);
+                    const float sk = fmax3f(fmax3f(l01, l23, fminf(h01, h23)), fmaxf(v0.y, v1.y), fmaxf(v2.y, v3.y));
+                    const int qs = v0.x == bk ? 0 : v1.x == bk ? 1 : v2.x == bk ? 2 : 3;
+                    const uint32_t code = __float_as_uint(bk) & 63u;
+                    const int64_t row = (int64_t)un.y - a0 + (int64_t)(code >> 5) * TC_BM + qs * 32 + (code & 31u);
+                    const unsigned long long gk =
+                        ((unsigned long long)f2ord(bk) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
+                    const int64_t gc = b0 + col0 + et;
+                    const unsigned long long old = atomicMax(p.col_key + gc, gk);
+                    const uint32_t loser = (uint32_t)((old < gk ? old : gk) >> 32);
+                    atomicMax(p.col_second + gc, max(f2ord(sk), loser));
+                }
+                tb ^= 1;
             }
             // the two column-half warps of a quarter hold partial states of
-            // the same rows: h = 1 hands its (best, column, second) over
-            float4* rsc = reinterpret_cast<float4*>(colbuf);
+            // the same rows: h = 1 hands its (best, second, column) over
             const int ti = q * 32 + lane;
+            const int c0 = R0.cb + (int)((__float_as_uint(R0.b) >> 6) & 31u);
+            const int c1 = R1.cb + (int)((__float_as_uint(R1.b) >> 6) & 31u);
             if (h == 1) {
-                rsc[ti] = make_float4(b0v, __int_as_float(b0c), s0v, 0.f);
-                rsc[TC_BM + ti] = make_float4(b1v, __int_as_float(b1c), s1v, 0.f);
+                rsc[ti] = make_float4(R0.b, R0.s, __int_as_float(c0), 0.f);
+                rsc[TC_BM + ti] = make_float4(R1.b, R1.s, __int_as_float(c1), 0.f);
             }
             named_sync(1, TC_EPI_THREADS);
             if (h == 0) {
                 const float4 o0 = rsc[ti], o1 = rsc[TC_BM + ti];
-                // merge two (best, column, second) summaries; h = 0 holds the
-                // smaller columns of every tile only per tile, so ties go to
-                // the smaller column explicitly
-                auto merge = [](float& bv, int& bc, float& sv, float ov, int oc, float os) {
-                    const bool take = ov > bv || (ov == bv && oc >= 0 && (bc < 0 || oc < bc));
-                    sv = fmaxf(fminf(bv, ov), fmaxf(sv, os));
-                    if (take) { bv = ov; bc = oc; }
-                };
-                merge(b0v, b0c, s0v, o0.x, __float_as_int(o0.y), o0.z);
-                merge(b1v, b1c, s1v, o1.x, __float_as_int(o1.y), o1.z);
                 if (rv0) {
                     RowCand rc;
-                    rc.v[0] = b0v; rc.v[1] = s0v; rc.v[2] = rc.v[3] = -INFINITY;
-                    rc.c[0] = b0c; rc.c[1] = rc.c[2] = rc.c[3] = -1;
+                    rc.k1 = fmaxf(R0.b, o0.x);
+                    rc.k2 = fmax3f(R0.s, o0.y, fminf(R0.b, o0.x));
+                    rc.c1 = o0.x > R0.b ? __float_as_int(o0.z) : c0;
+                    rc.pad = 0;
                     p.cand[row0] = rc;
                 }
                 if (rv1) {
                     RowCand rc;
-                    rc.v[0] = b1v; rc.v[1] = s1v; rc.v[2] = rc.v[3] = -INFINITY;
-                    rc.c[0] = b1c; rc.c[1] = rc.c[2] = rc.c[3] = -1;
+                    rc.k1 = fmaxf(R1.b, o1.x);
+                    rc.k2 = fmax3f(R1.s, o1.y, fminf(R1.b, o1.x));
+                    rc.c1 = o1.x > R1.b ? __float_as_int(o1.z) : c1;
+                    rc.pad = 0;
                     p.cand[row1] = rc;
                 }
             }
-            named_sync(1, TC_EPI_THREADS);
         }
     }
     tc_fence_before();
@@ -451,18 +517,26 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
     return lo;
 }
 
-__device__ __forceinline__ double d2x(double s) { return fmax(__dsub_rn(2.0, __dmul_rn(2.0, s)), 0.0); }
-
-// Stage 1 (one thread per row): decide from the approximate values alone.
-// Every true similarity is within eps of its tensor-core value, so the
-// approximate order statistics bound the true ones: the argmax is certain
-// when a1 - a2 > 2 eps (and the runner-up cannot clamp to d2 = 0), and the
-// ratio test d1 > r^2 d2 (tracking.py:167) is certain when its interval
-// bounds do not straddle.  Everything else goes to the float64 stages.
+// d2 = max(2 - 2 s, 0) (tracking.py:153) on interval end points
 __device__ __forceinline__ double d2c(double s) { return fmax(2.0 - 2.0 * s, 0.0); }
 
+// Bound on |key - exact similarity|: the tensor-core error eps_tc plus the
+// 2^11 ulps the code replaced (<= 2^-12 |key|).
+__device__ __forceinline__ double key_eps(double k, double eps_tc) { return eps_tc + ldexp(fabs(k), -12) + 1e-30; }
+
+// Relative slack on the ratio comparisons: covers the float64 rounding of
+// d2 and ratio^2 * d2 in the reference (tracking.py:153,167).
+constexpr double kRatioSlack = 1e-9;
+
+// Stage 1 (one thread per row).  The exact top-2 similarities lie within the
+// key bounds of the approximate ones, so
+//   * the ratio test's reject (d_first > r^2 second, tracking.py:167) is
+//     certain from the bounds alone — no argmax needed (most spurious rows);
+//   * a pass is certain when the argmax is (a1 - a2 beyond both bounds, and
+//     the runner-up cannot clamp to d2 = 0) and the bounds pass;
+// everything else is listed for the float64 row re-scan.
 __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                               int64_t total_a, const RowCand* __restrict__ cand, double eps, double ratio2,
+                               int64_t total_a, const RowCand* __restrict__ cand, double eps_tc, double ratio2,
                                MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
                                int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -470,101 +544,72 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
     const int p = pair_of(a_off, n_pairs, r);
     const int64_t M = b_off[p + 1] - b_off[p];
     MatchRowState s;
-    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = -1;
-    bool decided = false;
-    if (M == 0) {
-        decided = true;
-    } else {
-        const RowCand c = cand[r];
-        const double a1 = c.v[0];
-        if (M == 1) {
-            decided = c.c[0] >= 0;
-            s.best = c.c[0];
-            s.ratio_ok = 1;  // ratio test skipped for a single column (tracking.py:165)
-        } else {
-            const double a2 = c.v[1];
-            if (c.c[0] >= 0 && a1 - a2 > 2.0 * eps && a2 + eps < 1.0) {
-                const double d1_lo = d2c(a1 + eps), d1_hi = d2c(a1 - eps);
-                const double s_lo = d2c(a2 + eps), s_hi = d2c(a2 - eps);
-                if (d1_lo > ratio2 * s_hi) { decided = true; s.ratio_ok = 0; }
-                else if (d1_hi < ratio2 * s_lo) { decided = true; s.ratio_ok = 1; }
-                s.best = c.c[0];
-            }
-        }
+    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
+    if (M == 0) { rs[r] = s; return; }  // no columns: no match
+    const RowCand c = cand[r];
+    if (M == 1) {  // one column: argmax certain, ratio test skipped (tracking.py:165)
+        s.best = 0;
+        s.ratio_ok = 1;
+        rs[r] = s;
+        return;
     }
-    // undecided rows (~0.1-1%) go straight to the float64 full-row re-scan
-    if (decided) rs[r] = s;
-    else pending[atomicAdd((unsigned long long*)&counters[0], 1ull)] = (int32_t)r;
+    const double a1 = c.k1, a2 = c.k2;
+    const double e1 = key_eps(a1, eps_tc), e2 = key_eps(a2, eps_tc);
+    if (d2c(a1 + e1) > ratio2 * d2c(a2 - e2) * (1.0 + kRatioSlack)) { rs[r] = s; return; }  // certain reject
+    if (a1 - e1 > a2 + e2 && a2 + e2 < 1.0 && d2c(a1 - e1) < ratio2 * d2c(a2 + e2) * (1.0 - kRatioSlack)) {
+        s.best = c.c1;
+        s.ratio_ok = 1;
+        rs[r] = s;
+        return;
+    }
+    pending[atomicAdd((unsigned long long*)&counters[0], 1ull)] = (int32_t)r;
 }
 
-// Column side, stage 1: argmax certain when the best (quantised) key beats
-// the second by more than the bound and the runner-up cannot clamp.
-__global__ void mt_decide_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                               int64_t total_b, const unsigned long long* __restrict__ col_key,
-                               const unsigned int* __restrict__ col_second, double bias, double eps,
-                               int32_t* __restrict__ col_best, int32_t* __restrict__ pending,
-                               int64_t* __restrict__ counters) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= total_b) return;
-    const int p = pair_of(b_off, n_pairs, c);
-    const int64_t N = a_off[p + 1] - a_off[p];
-    if (N == 0) { col_best[c] = -1; return; }
-    const unsigned long long k = col_key[c];
-    const int64_t r1 = (int64_t)(0xFFFFFFFFull - (k & 0xFFFFFFFFull));
-    bool ok = k != 0 && r1 >= 0 && r1 < N;
-    if (ok && N >= 2) {
-        const unsigned int s2 = col_second[c];
-        if (s2 != 0) {
-            const double a1 = (double)__uint_as_float((unsigned int)(k >> 32)) - bias;
-            const double a2 = (double)__uint_as_float(s2) - bias;
-            ok = (a1 - eps > a2 + eps) && (a2 + eps < 1.0);
-        }
-    }
-    if (ok) col_best[c] = (int32_t)r1;
-    else pending[atomicAdd((unsigned long long*)&counters[3], 1ull)] = (int32_t)c;
-}
-
-// Column side, stage 2 (one warp per pending column): the best row is
-// re-scored; certified when the column's second value (plus the bound) is
-// below it and below 1 (d2 clamp), else listed for the full re-scan.
-template <typename T>
-__global__ void mt_certify_cols(const T* __restrict__ A, const T* __restrict__ B, int D,
-                                const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                                const int32_t* __restrict__ pending, const unsigned long long* __restrict__ col_key,
-                                const unsigned int* __restrict__ col_second, double bias, double eps,
-                                int32_t* __restrict__ col_best, int32_t* __restrict__ flag_cols,
-                                int64_t* __restrict__ counters) {
-    const int lane = threadIdx.x & 31;
-    const int64_t n_pend = counters[3];
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_pend;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t c = pending[t];
-    const int p = pair_of(b_off, n_pairs, c);
+// Stage 2 (one thread per row, after the float64 row re-scan): rows that
+// pass the ratio test need the mutual check best_a[best_b[i]] == i
+// (tracking.py:160-162).  It is settled from the column's top-2 keys when
+// they separate; otherwise the column is listed (once) for the float64
+// column re-scan, which writes col_best.
+__global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
+                             int64_t total_a, const RowCand* __restrict__ cand,
+                             const unsigned long long* __restrict__ col_key, const unsigned int* __restrict__ col_second,
+                             double eps_tc, double ratio2, MatchRowState* __restrict__ rs,
+                             int32_t* __restrict__ col_best, int32_t* __restrict__ pending,
+                             int64_t* __restrict__ counters) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= total_a) return;
+    const int p = pair_of(a_off, n_pairs, r);
     const int64_t a0 = a_off[p], N = a_off[p + 1] - a0;
-    const unsigned long long k = col_key[c];
-    bool ok = k != 0;
-    int64_t r1 = 0;
-    double e1 = 0;
-    if (ok) {
-        r1 = (int64_t)(0xFFFFFFFFull - (k & 0xFFFFFFFFull));
-        ok = r1 >= 0 && r1 < N;
-        if (ok) e1 = warp_dot16<T>(A + (a0 + r1) * D, B + c * D, D, lane);
-    }
-    if (ok && N >= 2) {
-        const unsigned int s2 = col_second[c];
-        if (s2 != 0) {
-            const double others = (double)__uint_as_float(s2) - bias + eps;
-            ok = others < e1 && others < 1.0;
+    const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
+    const MatchRowState s = rs[r];
+    if (M == 0 || s.best < 0) return;
+    const bool keep = s.ratio_ok == 1 || (s.ratio_ok == -1 && (M <= 1 || !(s.d1 > ratio2 * s.d2)));
+    if (!keep) return;
+    const int64_t c = b0 + s.best, lr = r - a0;
+    int mutual = -1;
+    const unsigned long long key = col_key[c];
+    if (key != 0) {
+        const double cv = ord2f((uint32_t)(key >> 32));
+        const int64_t rc = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+        const unsigned int sc = col_second[c];
+        if (rc == lr) {
+            const double sv = sc ? (double)ord2f(sc) : -INFINITY;
+            if (N == 1 || sv < -1e30) mutual = 1;
+            else if (cv - key_eps(cv, eps_tc) > sv + key_eps(sv, eps_tc) && sv + key_eps(sv, eps_tc) < 1.0)
+                mutual = 1;
+        } else if (rc >= 0 && rc < N) {
+            // an approximate value of (r, c): the row's best key when it is
+            // this element, else the exact similarity behind d1
+            const RowCand rcand = cand[r];
+            double kv = 0.0, ke = -1.0;
+            if (rcand.c1 == s.best) { kv = rcand.k1; ke = key_eps(kv, eps_tc); }
+            else if (s.ratio_ok == -1 && s.d1 > 0.0) { kv = 1.0 - 0.5 * s.d1; ke = 1e-12; }
+            if (ke >= 0.0 && cv - key_eps(cv, eps_tc) > kv + ke) mutual = 0;
         }
     }
-    if (lane == 0) {
-        if (ok) col_best[c] = (int32_t)r1;
-        else {
-            const unsigned long long i = atomicAdd((unsigned long long*)&counters[1], 1ull);
-            flag_cols[i] = (int32_t)c;
-        }
-    }
-    }
+    rs[r].mutual = mutual;
+    if (mutual == -1 && atomicCAS(col_best + c, -1, -2) == -1)
+        pending[atomicAdd((unsigned long long*)&counters[1], 1ull)] = (int32_t)c;
 }
 
 __global__ void mt_norm_kernel(const uint16_t* __restrict__ X, int64_t rows, int D, unsigned int* __restrict__ out) {
@@ -621,46 +666,46 @@ static bool make_map(CUtensorMap* m, const uint16_t* base, int64_t rows, int D) 
 
 static size_t tc_smem_bytes(int kblocks) {
     return 1024 + (size_t)TC_NA * kblocks * TC_BOX_BYTES + (size_t)TC_STAGES * TC_BOX_BYTES +
-           sizeof(uint2) * TC_NA * 4 * TC_BN + 8 * (2 + 2 * TC_STAGES + 4) + 16;
+           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * TC_NA * TC_BM + 8 * (2 + 2 * TC_STAGES + 4) + 16;
 }
 
 size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs) {
-    const int64_t max_units = total_a / TC_BM + n_pairs + 1;
+    const int64_t max_units = total_a / (TC_NA * TC_BM) + n_pairs + 1;
     return align256(sizeof(RowCand) * (size_t)total_a) + align256(8 * (size_t)total_b) +
-           align256(4 * (size_t)total_b) + align256(sizeof(int2) * (size_t)max_units) + align256(64) +
-           align256(4 * (size_t)total_a) + align256(4 * (size_t)total_b);
+           align256(4 * (size_t)total_b) + align256(sizeof(int2) * (size_t)max_units) + align256(64);
 }
 
-// Stage 1 on every row / column, then stage-2 float64 certification of the
-// pending ones.  The pending counts live on the device; stage 2 runs on a
-// fixed persistent grid that strides over the lists, so no host
-// synchronisation is needed.
-template <typename T>
-static int certify(const void* Ax, const void* Bx, int D, const int64_t* a_off, const int64_t* b_off, int n_pairs,
-                   int64_t ta, int64_t tb, const RowCand* cand, const unsigned long long* ck, const unsigned int* cs,
-                   double bias, double eps_row, double eps_col, double ratio2, MatchRowState* rs, int32_t* col_best,
-                   int32_t* pend_rows, int32_t* pend_cols, int32_t* flag_rows, int32_t* flag_cols,
-                   int64_t* counters, cudaStream_t st) {
-    (void)pend_rows;
-    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, ta, cand, eps_row, ratio2, rs,
-                                                                 flag_rows, counters);
-    EC3R_CHECK_LAUNCH("mt_decide_rows");
-    mt_decide_cols<<<(unsigned)((tb + 255) / 256), 256, 0, st>>>(a_off, b_off, n_pairs, tb, ck, cs, bias, eps_col,
-                                                                 col_best, pend_cols, counters);
-    EC3R_CHECK_LAUNCH("mt_decide_cols");
-    mt_certify_cols<T><<<kNumSMs * 4, 256, 0, st>>>(
-        (const T*)Ax, (const T*)Bx, D, a_off, b_off, n_pairs, pend_cols, ck, cs, bias, eps_col, col_best, flag_cols,
-        counters);
-    EC3R_CHECK_LAUNCH("mt_certify_cols");
-    return EC3R_OK;
+struct TcWs {
+    RowCand* cand;
+    unsigned long long* ck;
+    unsigned int* cs;
+    int2* units;
+    unsigned int* nb;
+    size_t used;
+};
+
+static TcWs carve_tc(void* tc_ws, int64_t ta, int64_t tb, int n_pairs) {
+    Carver cv{(char*)tc_ws, 0};
+    TcWs w;
+    w.cand = cv.take<RowCand>(ta);
+    w.ck = cv.take<unsigned long long>(tb);
+    w.cs = cv.take<unsigned int>(tb);
+    w.units = cv.take<int2>(ta / (TC_NA * TC_BM) + n_pairs + 1);
+    w.nb = cv.take<unsigned int>(16);
+    w.used = cv.used;
+    return w;
 }
 
-int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x, const int64_t* a_off_d,
-                 const int64_t* b_off_d, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D,
-                 int exact_dtype, double norm_bound, double ratio, MatchRowState* rs, int32_t* col_best,
-                 int32_t* flag_rows, int32_t* flag_cols, int64_t* counters, void* tc_ws, size_t tc_ws_bytes,
+// Tensor-core pass + stage-1 row decisions.  *tc_used = 0 when the shape or
+// alignment rules out the tensor cores: every row and column is then listed
+// for the float64 re-scan (counters[0] = rows, counters[1] = cols).
+int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, const int64_t* b_off_d,
+                 const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
+                 double norm_bound, double ratio, MatchRowState* rs, int32_t* flag_rows, int32_t* flag_cols,
+                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, double* eps_out,
                  cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
+    *tc_used = 0;
     const bool tc_ok = (D % TC_BK == 0) && D <= 256 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0 && ta > 0 &&
                        tb > 0 && get_encode() != nullptr;
     if (!tc_ok) {  // every decision goes to the float64 re-scan on the GPU
@@ -673,50 +718,39 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
         EC3R_CUDA_TRY(cudaStreamSynchronize(st));
         return EC3R_OK;
     }
-    Carver cv{(char*)tc_ws, 0};
-    RowCand* cand = cv.take<RowCand>(ta);
-    unsigned long long* ck = cv.take<unsigned long long>(tb);
-    unsigned int* cs = cv.take<unsigned int>(tb);
-    const int64_t max_units = ta / TC_BM + n_pairs + 1;
-    int2* units = cv.take<int2>(max_units);
-    unsigned int* nb = cv.take<unsigned int>(16);
-    int32_t* pend_rows = cv.take<int32_t>(ta);
-    int32_t* pend_cols = cv.take<int32_t>(tb);
-    if (cv.used > tc_ws_bytes) return EC3R_EWORKSPACE;
+    const TcWs w = carve_tc(tc_ws, ta, tb, n_pairs);
+    if (w.used > tc_ws_bytes) return EC3R_EWORKSPACE;
     std::vector<int2> hu;
-    hu.reserve(max_units);
+    hu.reserve(ta / (TC_NA * TC_BM) + n_pairs + 1);
     for (int pi = 0; pi < n_pairs; ++pi) {
         if (b_off_h[pi + 1] == b_off_h[pi]) continue;  // no columns: nothing to score
         for (int64_t r = a_off_h[pi]; r < a_off_h[pi + 1]; r += TC_NA * TC_BM) hu.push_back(make_int2(pi, (int)r));
     }
-    EC3R_CUDA_TRY(cudaMemsetAsync(ck, 0, 8 * (size_t)tb, st));
-    EC3R_CUDA_TRY(cudaMemsetAsync(cs, 0, 4 * (size_t)tb, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(w.ck, 0, 8 * (size_t)tb, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(w.cs, 0, 4 * (size_t)tb, st));
     if (!hu.empty())
-        EC3R_CUDA_TRY(cudaMemcpyAsync(units, hu.data(), sizeof(int2) * hu.size(), cudaMemcpyHostToDevice, st));
+        EC3R_CUDA_TRY(cudaMemcpyAsync(w.units, hu.data(), sizeof(int2) * hu.size(), cudaMemcpyHostToDevice, st));
     if (!(norm_bound > 0)) {
         // max squared row norms of A and B (float32, rounded up below)
-        EC3R_CUDA_TRY(cudaMemsetAsync(nb, 0, 8, st));
-        mt_norm_kernel<<<(unsigned)((ta * 32 + 255) / 256), 256, 0, st>>>(A, ta, D, nb);
+        EC3R_CUDA_TRY(cudaMemsetAsync(w.nb, 0, 8, st));
+        mt_norm_kernel<<<(unsigned)((ta * 32 + 255) / 256), 256, 0, st>>>(A, ta, D, w.nb);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
-        mt_norm_kernel<<<(unsigned)((tb * 32 + 255) / 256), 256, 0, st>>>(B, tb, D, nb + 1);
+        mt_norm_kernel<<<(unsigned)((tb * 32 + 255) / 256), 256, 0, st>>>(B, tb, D, w.nb + 1);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
         unsigned int h[2];
-        EC3R_CUDA_TRY(cudaMemcpyAsync(h, nb, 8, cudaMemcpyDeviceToHost, st));
+        EC3R_CUDA_TRY(cudaMemcpyAsync(h, w.nb, 8, cudaMemcpyDeviceToHost, st));
         EC3R_CUDA_TRY(cudaStreamSynchronize(st));
         float fa, fb;
         memcpy(&fa, &h[0], 4);
         memcpy(&fb, &h[1], 4);
         norm_bound = sqrt((double)fa * (1.0 + 1e-5)) * sqrt((double)fb * (1.0 + 1e-5)) + 1e-30;
     }
-    // error bounds (K5): fp32 tensor-core accumulation of exact
-    // bf16 products, + key quantisation (5 low bits) on the column side,
-    // + bf16 rounding of the inputs when the exact rows are wider.
-    const double Bn = norm_bound;
-    const float bias = (float)fmax(2.0, 2.0 * Bn);
-    double eps_row = ldexp(Bn, -14);
-    if (exact_dtype != 0) eps_row += ldexp(Bn, -7);
-    // column keys drop 6 low mantissa bits (64 ulps of a value < 2 (bias + Bn))
-    const double eps_col = eps_row + ldexp(2.0 * ((double)bias + Bn), -17);
+    // tensor-core error bound (K5): fp32 accumulation of exact
+    // bf16 products, + bf16 rounding of the inputs when the exact rows are
+    // wider.  The key quantisation is added per value (key_eps).
+    double eps_tc = ldexp(norm_bound, -14);
+    if (exact_dtype != 0) eps_tc += ldexp(norm_bound, -7);
+    *eps_out = eps_tc;
     CUtensorMap tmA, tmB;
     if (!make_map(&tmA, A, ta, D) || !make_map(&tmB, B, tb, D)) {
         set_last_error_msg("cuTensorMapEncodeTiled failed");
@@ -724,8 +758,8 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
     }
     TcParams prm;
     prm.a_off = a_off_d; prm.b_off = b_off_d;
-    prm.units = units; prm.n_units = (int)hu.size(); prm.kblocks = D / TC_BK; prm.bias = bias;
-    prm.cand = cand; prm.col_key = ck; prm.col_second = cs;
+    prm.units = w.units; prm.n_units = (int)hu.size(); prm.kblocks = D / TC_BK;
+    prm.cand = w.cand; prm.col_key = w.ck; prm.col_second = w.cs;
     if (prm.n_units > 0) {
         const size_t smem = tc_smem_bytes(prm.kblocks);
         EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -733,21 +767,26 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const void* A_x, const vo
         mt_tc_kernel<<<grid, TC_THREADS, smem, st>>>(tmA, tmB, prm);
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
     }
-    EC3R_CUDA_TRY(cudaMemsetAsync(counters, 0, 32, st));
-    const double ratio2 = ratio * ratio;  // tracking.py:158
-    switch (exact_dtype) {
-        case 0:
-            return certify<uint16_t>(A, B, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row, eps_col,
-                                     ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols, counters, st);
-        case 1:
-            return certify<float>(A_x, B_x, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row,
-                                  eps_col, ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols, counters,
-                                  st);
-        default:
-            return certify<double>(A_x, B_x, D, a_off_d, b_off_d, n_pairs, ta, tb, cand, ck, cs, bias, eps_row,
-                                   eps_col, ratio2, rs, col_best, pend_rows, pend_cols, flag_rows, flag_cols,
-                                   counters, st);
-    }
+    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, eps_tc,
+                                                                 ratio * ratio, rs, flag_rows, counters);
+    EC3R_CHECK_LAUNCH("mt_decide_rows");
+    *tc_used = 1;
+    return EC3R_OK;
+}
+
+// Mutual checks of the passing rows (after the row re-scan); lists the
+// columns that need the float64 column re-scan.  col_best is reset to -1.
+int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
+                       const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
+                       int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st) {
+    const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
+    const TcWs w = carve_tc(tc_ws, ta, tb, n_pairs);
+    EC3R_CUDA_TRY(cudaMemsetAsync(col_best, 0xFF, sizeof(int32_t) * (size_t)tb, st));
+    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.ck, w.cs,
+                                                               eps_tc, ratio * ratio, rs, col_best, flag_cols,
+                                                               counters);
+    EC3R_CHECK_LAUNCH("mt_need_cols");
+    return EC3R_OK;
 }
 
 }  // namespace ec3r

@@ -410,6 +410,92 @@ def test_match_random_vs_oracle(n, m, d, sigma):
         assert st["rows_rescanned"] < 0.05 * n and st["cols_rescanned"] < 0.05 * m, st
 
 
+def _bf16(x):
+    return torch.as_tensor(np.asarray(x, np.float64)).to(torch.bfloat16).double().numpy()
+
+
+def _unit(rng, n, d):
+    x = rng.normal(size=(n, d))
+    return x / np.linalg.norm(x, axis=1, keepdims=True)
+
+
+def _adversarial(case, rng, d=256):
+    """Inputs that stress the certification: exact ties (first-index rule),
+    similarities clamped to d2 = 0, near ties at bf16 resolution, negative
+    best similarities, non-unit norms."""
+    a = _unit(rng, 700, d)
+    b = _unit(rng, 900, d)
+    b[:500] = a[:500] + 0.05 * rng.normal(size=(500, d))
+    if case == "dup_cols":  # exact duplicate columns: row argmin ties
+        b[600:700] = b[100:200]
+    elif case == "dup_rows":  # exact duplicate rows: column argmin ties
+        a[550:650] = a[50:150]
+    elif case == "identical":  # sims == 1 -> d2 clamps to 0, duplicated on both sides
+        b[:500] = a[:500]
+        b[500:550] = a[:50]
+        a[600:650] = a[:50]
+    elif case == "near_ties":  # column pairs one bf16 ulp apart in one coordinate
+        b = _bf16(b)
+        b[500:700] = b[:200]
+        k = rng.integers(0, d, size=200)
+        b[np.arange(500, 700), k] *= 1 + 2.0 ** -7
+    elif case == "negative":  # partners anti-aligned: every best similarity is small
+        b[:500] = -b[:500]
+    elif case == "scaled":  # non-unit rows: sims up to ~2, clamp region exercised
+        a = a * 1.7
+        b = b * 1.2
+    return _bf16(a), _bf16(b)
+
+
+@pytest.mark.parametrize("case", ["dup_cols", "dup_rows", "identical", "near_ties", "negative", "scaled"])
+def test_match_adversarial_vs_oracle(case):
+    from paper_2510_02080_b200 import tracking
+    rng = np.random.default_rng(["dup_cols", "dup_rows", "identical", "near_ties", "negative", "scaled"].index(case))
+    a, b = _adversarial(case, rng)
+    exp = ref.match_descriptors_vec(a, b, 0.8)
+    got = np.array(tracking.match_descriptors(a, b, 0.8), np.int64).reshape(-1, 2)
+    np.testing.assert_array_equal(got, exp)
+    # the per-row reference loop agrees with the vectorised oracle on these
+    np.testing.assert_array_equal(np.array(ref.match_descriptors(a[:200], b, 0.8), np.int64).reshape(-1, 2),
+                                  ref.match_descriptors_vec(a[:200], b, 0.8))
+
+
+def test_match_tiny_pairs_vs_oracle():
+    """N or M of 1 and 2 (ratio test skipped for M == 1, tracking.py:165),
+    mixed with full tiles in one batch."""
+    from paper_2510_02080_b200 import tracking
+    rng = np.random.default_rng(11)
+    pairs = []
+    for n, m in ((1, 1), (1, 2), (2, 1), (2, 2), (1, 300), (300, 1), (129, 257), (256, 128), (3, 3)):
+        a = _unit(rng, n, 256)
+        b = _unit(rng, m, 256)
+        k = min(n, m)
+        b[:k] = a[:k] + 0.05 * rng.normal(size=(k, 256))
+        pairs.append((_bf16(a), _bf16(b)))
+    got = tracking.match_batched(pairs, 0.8)
+    for (a, b), g in zip(pairs, got):
+        np.testing.assert_array_equal(g, ref.match_descriptors_vec(a, b, 0.8))
+
+
+def test_match_bench_shape_vs_oracle():
+    """The bench workload's shape (1024 x 1024 x 256, 20 % spurious rows) over
+    several pairs in one launch, and the re-scan counts stay small."""
+    from paper_2510_02080_b200 import synth, tracking
+    A, B, ao, bo = synth.make_descriptor_pairs(6, 1024, 1024, 256, 0.05, seed=77)
+    mb, nm = tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)
+    mb = mb.cpu().numpy()
+    a = A.view(torch.bfloat16).double().cpu().numpy()
+    b = B.view(torch.bfloat16).double().cpu().numpy()
+    for p in range(6):
+        exp = ref.match_descriptors_vec(a[ao[p]:ao[p + 1]], b[bo[p]:bo[p + 1]], 0.8)
+        seg = mb[ao[p]:ao[p + 1]]
+        ia = np.flatnonzero(seg >= 0)
+        np.testing.assert_array_equal(np.stack([ia, seg[ia]], axis=1), exp)
+        assert int(nm[p]) == len(exp)
+    st = tracking.last_match_stats()
+    assert st["rows_rescanned"] < 0.01 * st["rows"] and st["cols_rescanned"] < 0.01 * st["cols"], st
+
+
 def test_match_batched_pairs_vs_oracle():
     from paper_2510_02080_b200 import tracking
     rng = np.random.default_rng(5)
