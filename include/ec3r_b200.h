@@ -212,7 +212,9 @@ EC3R_API int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, const
  * Output: match_b (sum N_p) int32 =
  * matched B row within the pair or -1; n_match (n_pairs) int32.
  * ------------------------------------------------------------------- */
-EC3R_API size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_pairs);
+/* Workspace bytes for ec3r_match_batched on these row offsets (host
+ * int64, n_pairs + 1 each): grows with sum_p ceil(N_p / 256) * M_p. */
+EC3R_API size_t ec3r_match_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs);
 EC3R_API int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
                        int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h,
                        int n_pairs, int D, double ratio, double norm_bound, int32_t* match_b,

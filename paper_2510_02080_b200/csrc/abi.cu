@@ -30,7 +30,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
 int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
                        const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
                        int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st);
-size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs);
+size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs);
 
 }  // namespace ec3r
 
@@ -44,11 +44,13 @@ extern "C" const char* ec3r_last_error(void) { return g_last_error; }
 //   a_off, b_off (n_pairs+1 int64 each), row state (total_a), col best
 //   (total_b), flagged rows / cols lists (total_a / total_b int32),
 //   counters (8 int64), then the tensor-core pass workspace.
-extern "C" size_t ec3r_match_workspace(int64_t total_a, int64_t total_b, int n_pairs) {
+extern "C" size_t ec3r_match_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
+    if (!a_off_h || !b_off_h || n_pairs < 0) return 0;
+    const int64_t total_a = a_off_h[n_pairs], total_b = b_off_h[n_pairs];
     return 2 * align256(sizeof(int64_t) * (size_t)(n_pairs + 1)) + align256(sizeof(MatchRowState) * (size_t)total_a) +
            align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int32_t) * (size_t)total_a) +
            align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int64_t) * 8) +
-           match_tc_workspace(total_a, total_b, n_pairs);
+           match_tc_workspace(a_off_h, b_off_h, n_pairs);
 }
 
 extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
@@ -58,7 +60,7 @@ extern "C" int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const vo
     if (n_pairs < 0 || D <= 0 || !a_off_h || !b_off_h || exact_dtype < 0 || exact_dtype > 2) return EC3R_EARG;
     if (n_pairs == 0) return EC3R_OK;
     const int64_t total_a = a_off_h[n_pairs], total_b = b_off_h[n_pairs];
-    if (!workspace || workspace_bytes < ec3r_match_workspace(total_a, total_b, n_pairs)) return EC3R_EWORKSPACE;
+    if (!workspace || workspace_bytes < ec3r_match_workspace(a_off_h, b_off_h, n_pairs)) return EC3R_EWORKSPACE;
     if (exact_dtype == 0) { A_x = A; B_x = B; }
     if ((total_a && !A_x) || (total_b && !B_x)) return EC3R_EARG;
     cudaStream_t st = as_stream(stream);

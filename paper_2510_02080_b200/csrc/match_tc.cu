@@ -60,15 +60,23 @@ struct __align__(16) RowCand {
     int32_t pad;
 };
 
+// One work unit: up to 256 rows of one pair against all its columns.  Its
+// per-column top-2 keys go to col_slots[slot + column] (plain stores: each
+// (unit, column) has its own slot; certification merges a pair's units).
+struct __align__(16) TcUnit {
+    int pair;
+    int row0;        // first row of the unit within the packed A
+    long long slot;  // first column slot of the unit
+};
+
 struct TcParams {
     const int64_t* a_off;
     const int64_t* b_off;
-    const int2* units;  // (pair, first row of the unit within the packed A)
+    const TcUnit* units;
     int n_units;
     int kblocks;        // D / 64
     RowCand* cand;
-    unsigned long long* col_key;   // (ordered key << 32) | (~row): best row of the column
-    unsigned int* col_second;      // ordered key of the column's second row (0 = none)
+    unsigned long long* col_slots;  // per unit and column: (ordered best key << 32) | ordered second key
 };
 
 // ---------------------------------------------------------------------------
@@ -180,8 +188,12 @@ __device__ __forceinline__ float warp_max_f32(float x) {
 // key = value bits above bit 11, code below: bimm = KEY_MASK | column code
 // (an immediate), creg = KEY_MASK | row code; the two codes occupy disjoint
 // bits, so (a & b & c) | (b ^ c) is the whole key in one LOP3.
-__device__ __forceinline__ float make_key(uint32_t v, uint32_t bimm, uint32_t creg) {
-    return __uint_as_float((v & bimm & creg) | (bimm ^ creg));
+// (inline PTX: left to itself the compiler splits it into two LOP3s)
+template <uint32_t BIMM>
+__device__ __forceinline__ float make_key(uint32_t v, uint32_t creg) {
+    uint32_t k;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE6;" : "=r"(k) : "r"(v), "n"(BIMM), "r"(creg));
+    return __uint_as_float(k);
 }
 
 // order-preserving float <-> uint32 (0 is below every finite key)
@@ -220,6 +232,16 @@ struct RowTop2 {
     int cb;  // column base of the chunk holding b (b's code has the column within the chunk)
 };
 
+template <int J>
+__device__ __forceinline__ void make_keys(const uint32_t (&r0)[32], const uint32_t (&r1)[32], uint32_t creg0,
+                                          uint32_t creg1, float (&k0)[32], float (&k1)[32]) {
+    if constexpr (J < 32) {
+        k0[J] = make_key<KEY_MASK | ((uint32_t)J << 6)>(r0[J], creg0);
+        k1[J] = make_key<KEY_MASK | ((uint32_t)J << 6)>(r1[J], creg1);
+        make_keys<J + 1>(r0, r1, creg0, creg1, k0, k1);
+    }
+}
+
 __device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[32], uint32_t (&r1)[32], int nv0, int nv1, int cbase,
                                                uint32_t creg0, uint32_t creg1, RowTop2& R0, RowTop2& R1,
                                                uint32_t cb, int lane) {
@@ -233,11 +255,7 @@ __device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[32], uint32_t (&r1
         }
     }
     float k0[32], k1[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        k0[j] = make_key(r0[j], KEY_MASK | ((uint32_t)j << 6), creg0);
-        k1[j] = make_key(r1[j], KEY_MASK | ((uint32_t)j << 6), creg1);
-    }
+    make_keys<0>(r0, r1, creg0, creg1, k0, k1);
     // row side: top-2 over pairs (hi, lo) — 5 ops per 2 keys per row
     {
         float m0 = fmaxf(k0[0], k0[1]), s0 = fminf(k0[0], k0[1]);
@@ -284,9 +302,9 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     float2* colbuf = (float2*)(sB + (size_t)TC_STAGES * TC_BOX_BYTES);  // [2 tiles][4 quarters][TC_BN]
     float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);                     // [TC_NA * TC_BM] half-row summaries
     uint64_t* bars = (uint64_t*)(rsc + TC_NA * TC_BM);
-    uint64_t* a_full = bars + 0;
-    uint64_t* a_empty = bars + 1;
-    uint64_t* b_full = bars + 2;
+    uint64_t* a_full = bars + 0;   // per k-block slice of the resident A (both blocks)
+    uint64_t* a_empty = bars + 4;
+    uint64_t* b_full = bars + 8;
     uint64_t* b_empty = b_full + TC_STAGES;
     uint64_t* t_full = b_empty + TC_STAGES;
     uint64_t* t_empty = t_full + 2;
@@ -295,8 +313,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(a_full, 1);
-        mbar_init(a_empty, 1);
+        for (int s = 0; s < 4; ++s) { mbar_init(a_full + s, 1); mbar_init(a_empty + s, 1); }
         for (int s = 0; s < TC_STAGES; ++s) { mbar_init(b_full + s, 1); mbar_init(b_empty + s, 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(t_full + s, 1); mbar_init(t_empty + s, TC_EPI_THREADS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -323,18 +340,21 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             int stage = 0;
             uint32_t phase = 0, a_phase = 0;
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                const int2 un = p.units[u];
-                const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
+                const TcUnit un = p.units[u];
+                const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
                 const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
-                mbar_wait_sleep(a_empty, a_phase ^ 1);
-                mbar_expect_tx(a_full, (uint32_t)(TC_NA * KB * TC_BOX_BYTES));
-                for (int b = 0; b < TC_NA; ++b)
-                    for (int kb = 0; kb < KB; ++kb)
-                        tma_load_2d(sA + (size_t)(b * KB + kb) * TC_BOX_BYTES, &tmA, a_full, kb * TC_BK,
-                                    un.y + b * TC_BM);
-                a_phase ^= 1;
+                // A slices are refilled one k-block at a time as the previous
+                // unit's last tile releases them, interleaved with the first
+                // tile's B k-blocks, so the unit switch does not drain the MMA
                 for (int t = 0; t < n_tiles; ++t) {
                     for (int kb = 0; kb < KB; ++kb) {
+                        if (t == 0) {
+                            mbar_wait_sleep(a_empty + kb, a_phase ^ 1);
+                            mbar_expect_tx(a_full + kb, (uint32_t)(TC_NA * TC_BOX_BYTES));
+                            for (int b = 0; b < TC_NA; ++b)
+                                tma_load_2d(sA + (size_t)(b * KB + kb) * TC_BOX_BYTES, &tmA, a_full + kb, kb * TC_BK,
+                                            un.row0 + b * TC_BM);
+                        }
                         mbar_wait_sleep(b_empty + stage, phase ^ 1);
                         mbar_expect_tx(b_full + stage, TC_BOX_BYTES);
                         tma_load_2d(sB + (size_t)stage * TC_BOX_BYTES, &tmB, b_full + stage, kb * TC_BK,
@@ -342,6 +362,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                         if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
+                a_phase ^= 1;
             }
         }
     } else if (warp == 1) {
@@ -353,17 +374,15 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             uint32_t acc_phase = 0;
             const uint32_t sA_addr = smem_u32(sA), sB_addr = smem_u32(sB);
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                const int2 un = p.units[u];
-                const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
+                const TcUnit un = p.units[u];
+                const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
                 const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
-                mbar_wait_sleep(a_full, a_phase);
-                a_phase ^= 1;
-                tc_fence_after();
                 for (int t = 0; t < n_tiles; ++t) {
                     mbar_wait_sleep(t_empty + acc, acc_phase ^ 1);
                     tc_fence_after();
                     const uint32_t d_base = tmem_base + (uint32_t)(acc * TC_NA * TC_BN);
                     for (int kb = 0; kb < KB; ++kb) {
+                        if (t == 0) mbar_wait_sleep(a_full + kb, a_phase);
                         mbar_wait_sleep(b_full + stage, phase);
                         tc_fence_after();
                         const uint32_t bB = sB_addr + (uint32_t)(stage * TC_BOX_BYTES);
@@ -378,12 +397,13 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                             }
                         }
                         tc_commit(b_empty + stage);
+                        if (t == n_tiles - 1) tc_commit(a_empty + kb);  // slice kb free for the next unit
                         if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
                     }
                     tc_commit(t_full + acc);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
-                tc_commit(a_empty);
+                a_phase ^= 1;
             }
         }
     } else {
@@ -401,13 +421,13 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         uint32_t acc_phase = 0;
         int tb = 0;  // colbuf double buffer (alternates over all tiles of the CTA)
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-            const int2 un = p.units[u];
-            const int64_t a1 = p.a_off[un.x + 1], a0 = p.a_off[un.x];
-            const int64_t b0 = p.b_off[un.x], b1 = p.b_off[un.x + 1];
+            const TcUnit un = p.units[u];
+            const int64_t a1 = p.a_off[un.pair + 1], a0 = p.a_off[un.pair];
+            const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (M + TC_BN - 1) / TC_BN;
             RowTop2 R0{-INFINITY, -INFINITY, 0}, R1{-INFINITY, -INFINITY, 0};
-            const int64_t row0 = (int64_t)un.y + q * 32 + lane, row1 = row0 + TC_BM;
+            const int64_t row0 = (int64_t)un.row0 + q * 32 + lane, row1 = row0 + TC_BM;
             const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
                 mbar_wait(t_full + acc, acc_phase);
@@ -453,15 +473,12 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     const float h23 = fmaxf(v2.x, v3.x), l23 = fminf(v2.x, v3.x);
                     const float bk = fmaxf(h01, h23);
                     const float sk = fmax3f(fmax3f(l01, l23, fminf(h01, h23)), fmaxf(v0.y, v1.y), fmaxf(v2.y, v3.y));
-                    const int qs = v0.x == bk ? 0 : v1.x == bk ? 1 : v2.x == bk ? 2 : 3;
-                    const uint32_t code = __float_as_uint(bk) & 63u;
-                    const int64_t row = (int64_t)un.y - a0 + (int64_t)(code >> 5) * TC_BM + qs * 32 + (code & 31u);
-                    const unsigned long long gk =
-                        ((unsigned long long)f2ord(bk) << 32) | (0xFFFFFFFFull - (unsigned long long)row);
-                    const int64_t gc = b0 + col0 + et;
-                    const unsigned long long old = atomicMax(p.col_key + gc, gk);
-                    const uint32_t loser = (uint32_t)((old < gk ? old : gk) >> 32);
-                    atomicMax(p.col_second + gc, max(f2ord(sk), loser));
+                    const uint32_t qs = v0.x == bk ? 0u : v1.x == bk ? 1u : v2.x == bk ? 2u : 3u;
+                    // bits 7..6 of the best key (column code, meaningless on
+                    // this side) now hold the quarter: bits 7..0 = row in unit
+                    const float bq = __uint_as_float((__float_as_uint(bk) & ~0xC0u) | (qs << 6));
+                    __stcg(p.col_slots + un.slot + col0 + et,
+                           ((unsigned long long)f2ord(bq) << 32) | (unsigned long long)f2ord(sk));
                 }
                 tb ^= 1;
             }
@@ -572,10 +589,10 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
 // column re-scan, which writes col_best.
 __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
                              int64_t total_a, const RowCand* __restrict__ cand,
-                             const unsigned long long* __restrict__ col_key, const unsigned int* __restrict__ col_second,
-                             double eps_tc, double ratio2, MatchRowState* __restrict__ rs,
-                             int32_t* __restrict__ col_best, int32_t* __restrict__ pending,
-                             int64_t* __restrict__ counters) {
+                             const unsigned long long* __restrict__ col_slots,
+                             const long long* __restrict__ pair_slot, double eps_tc, double ratio2,
+                             MatchRowState* __restrict__ rs, int32_t* __restrict__ col_best,
+                             int32_t* __restrict__ pending, int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= total_a) return;
     const int p = pair_of(a_off, n_pairs, r);
@@ -586,14 +603,27 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
     const bool keep = s.ratio_ok == 1 || (s.ratio_ok == -1 && (M <= 1 || !(s.d1 > ratio2 * s.d2)));
     if (!keep) return;
     const int64_t c = b0 + s.best, lr = r - a0;
+    // merge the column's per-unit top-2 keys (units = 256-row blocks)
+    uint32_t bo = 0, so = 0;
+    int64_t rc = -1;
+    const int n_rb = (int)((N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM));
+    const unsigned long long* sl = col_slots + pair_slot[p] + s.best;
+    for (int rb = 0; rb < n_rb; ++rb) {
+        const unsigned long long v = __ldcg(sl + (int64_t)rb * M);
+        const uint32_t vb = (uint32_t)(v >> 32), vs = (uint32_t)v;
+        so = max(max(so, vs), min(bo, vb));
+        if (vb > bo) {
+            bo = vb;
+            const uint32_t code = __float_as_uint(ord2f(vb));
+            rc = (int64_t)rb * (TC_NA * TC_BM) + (int64_t)((code >> 5) & 1u) * TC_BM + ((code >> 6) & 3u) * 32 +
+                 (code & 31u);
+        }
+    }
     int mutual = -1;
-    const unsigned long long key = col_key[c];
-    if (key != 0) {
-        const double cv = ord2f((uint32_t)(key >> 32));
-        const int64_t rc = (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
-        const unsigned int sc = col_second[c];
+    if (bo != 0) {
+        const double cv = ord2f(bo);
         if (rc == lr) {
-            const double sv = sc ? (double)ord2f(sc) : -INFINITY;
+            const double sv = so ? (double)ord2f(so) : -INFINITY;
             if (N == 1 || sv < -1e30) mutual = 1;
             else if (cv - key_eps(cv, eps_tc) > sv + key_eps(sv, eps_tc) && sv + key_eps(sv, eps_tc) < 1.0)
                 mutual = 1;
@@ -666,31 +696,44 @@ static bool make_map(CUtensorMap* m, const uint16_t* base, int64_t rows, int D) 
 
 static size_t tc_smem_bytes(int kblocks) {
     return 1024 + (size_t)TC_NA * kblocks * TC_BOX_BYTES + (size_t)TC_STAGES * TC_BOX_BYTES +
-           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * TC_NA * TC_BM + 8 * (2 + 2 * TC_STAGES + 4) + 16;
+           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * TC_NA * TC_BM + 8 * (8 + 2 * TC_STAGES + 4) + 16;
 }
 
-size_t match_tc_workspace(int64_t total_a, int64_t total_b, int n_pairs) {
-    const int64_t max_units = total_a / (TC_NA * TC_BM) + n_pairs + 1;
-    return align256(sizeof(RowCand) * (size_t)total_a) + align256(8 * (size_t)total_b) +
-           align256(4 * (size_t)total_b) + align256(sizeof(int2) * (size_t)max_units) + align256(64);
+// column slots: one per (unit, column) = sum over pairs of ceil(N/256) * M
+static int64_t n_col_slots(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
+    int64_t n = 0;
+    for (int p = 0; p < n_pairs; ++p)
+        n += (a_off_h[p + 1] - a_off_h[p] + TC_NA * TC_BM - 1) / (TC_NA * TC_BM) * (b_off_h[p + 1] - b_off_h[p]);
+    return n;
+}
+
+static int64_t max_units(int64_t ta, int n_pairs) { return ta / (TC_NA * TC_BM) + n_pairs + 1; }
+
+size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
+    const int64_t ta = a_off_h[n_pairs];
+    return align256(sizeof(RowCand) * (size_t)ta) +
+           align256(sizeof(unsigned long long) * (size_t)n_col_slots(a_off_h, b_off_h, n_pairs)) +
+           align256(sizeof(long long) * (size_t)(n_pairs + 1)) + align256(sizeof(TcUnit) * (size_t)max_units(ta, n_pairs)) +
+           align256(64);
 }
 
 struct TcWs {
     RowCand* cand;
-    unsigned long long* ck;
-    unsigned int* cs;
-    int2* units;
+    unsigned long long* slots;
+    long long* pair_slot;
+    TcUnit* units;
     unsigned int* nb;
     size_t used;
 };
 
-static TcWs carve_tc(void* tc_ws, int64_t ta, int64_t tb, int n_pairs) {
+static TcWs carve_tc(void* tc_ws, const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
+    const int64_t ta = a_off_h[n_pairs];
     Carver cv{(char*)tc_ws, 0};
     TcWs w;
     w.cand = cv.take<RowCand>(ta);
-    w.ck = cv.take<unsigned long long>(tb);
-    w.cs = cv.take<unsigned int>(tb);
-    w.units = cv.take<int2>(ta / (TC_NA * TC_BM) + n_pairs + 1);
+    w.slots = cv.take<unsigned long long>(n_col_slots(a_off_h, b_off_h, n_pairs));
+    w.pair_slot = cv.take<long long>(n_pairs + 1);
+    w.units = cv.take<TcUnit>(max_units(ta, n_pairs));
     w.nb = cv.take<unsigned int>(16);
     w.used = cv.used;
     return w;
@@ -718,18 +761,26 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         EC3R_CUDA_TRY(cudaStreamSynchronize(st));
         return EC3R_OK;
     }
-    const TcWs w = carve_tc(tc_ws, ta, tb, n_pairs);
+    const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     if (w.used > tc_ws_bytes) return EC3R_EWORKSPACE;
-    std::vector<int2> hu;
-    hu.reserve(ta / (TC_NA * TC_BM) + n_pairs + 1);
+    // units and column-slot bases; units + pair bases travel in one copy
+    std::vector<TcUnit> hu;
+    std::vector<long long> hp(n_pairs + 1);
+    hu.reserve(max_units(ta, n_pairs));
+    long long slot = 0;
     for (int pi = 0; pi < n_pairs; ++pi) {
-        if (b_off_h[pi + 1] == b_off_h[pi]) continue;  // no columns: nothing to score
-        for (int64_t r = a_off_h[pi]; r < a_off_h[pi + 1]; r += TC_NA * TC_BM) hu.push_back(make_int2(pi, (int)r));
+        hp[pi] = slot;
+        const int64_t M = b_off_h[pi + 1] - b_off_h[pi];
+        if (M == 0) continue;  // no columns: nothing to score
+        for (int64_t r = a_off_h[pi]; r < a_off_h[pi + 1]; r += TC_NA * TC_BM) {
+            hu.push_back(TcUnit{pi, (int)r, slot});
+            slot += M;
+        }
     }
-    EC3R_CUDA_TRY(cudaMemsetAsync(w.ck, 0, 8 * (size_t)tb, st));
-    EC3R_CUDA_TRY(cudaMemsetAsync(w.cs, 0, 4 * (size_t)tb, st));
+    hp[n_pairs] = slot;
+    EC3R_CUDA_TRY(cudaMemcpyAsync(w.pair_slot, hp.data(), sizeof(long long) * hp.size(), cudaMemcpyHostToDevice, st));
     if (!hu.empty())
-        EC3R_CUDA_TRY(cudaMemcpyAsync(w.units, hu.data(), sizeof(int2) * hu.size(), cudaMemcpyHostToDevice, st));
+        EC3R_CUDA_TRY(cudaMemcpyAsync(w.units, hu.data(), sizeof(TcUnit) * hu.size(), cudaMemcpyHostToDevice, st));
     if (!(norm_bound > 0)) {
         // max squared row norms of A and B (float32, rounded up below)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.nb, 0, 8, st));
@@ -759,7 +810,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     TcParams prm;
     prm.a_off = a_off_d; prm.b_off = b_off_d;
     prm.units = w.units; prm.n_units = (int)hu.size(); prm.kblocks = D / TC_BK;
-    prm.cand = w.cand; prm.col_key = w.ck; prm.col_second = w.cs;
+    prm.cand = w.cand; prm.col_slots = w.slots;
     if (prm.n_units > 0) {
         const size_t smem = tc_smem_bytes(prm.kblocks);
         EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -780,9 +831,9 @@ int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int
                        const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
                        int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
-    const TcWs w = carve_tc(tc_ws, ta, tb, n_pairs);
+    const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     EC3R_CUDA_TRY(cudaMemsetAsync(col_best, 0xFF, sizeof(int32_t) * (size_t)tb, st));
-    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.ck, w.cs,
+    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.slots, w.pair_slot,
                                                                eps_tc, ratio * ratio, rs, col_best, flag_cols,
                                                                counters);
     EC3R_CHECK_LAUNCH("mt_need_cols");

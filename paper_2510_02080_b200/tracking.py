@@ -52,7 +52,7 @@ def match_batched_device(A_bits: torch.Tensor, B_bits: torch.Tensor, A_x, B_x, e
     ta, tb = int(a_off[-1]), int(b_off[-1])
     match_b = torch.empty(max(ta, 1), dtype=torch.int32, device=dev)
     n_match = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
-    ws_bytes = L.ec3r_match_workspace(ta, tb, P)
+    ws_bytes = L.ec3r_match_workspace(a_off.ctypes.data, b_off.ctypes.data, P)
     ws = _lib.workspace(ws_bytes, dev, "match")
     _lib.check(L.ec3r_match_batched(_lib.ptr(A_bits), _lib.ptr(B_bits), _lib.ptr(A_x), _lib.ptr(B_x),
                                     int(exact_dtype), a_off.ctypes.data, b_off.ctypes.data, P, D, float(ratio),

@@ -35,7 +35,8 @@ def test_workspace_queries_without_gpu():
     from paper_2510_02080_b200 import _lib
     L = _lib.load()
     assert L.ec3r_inverse_project_workspace(5, 392, 518) > 0
-    assert L.ec3r_match_workspace(1024, 1024, 1) > 0
+    off = np.array([0, 1024], np.int64)
+    assert L.ec3r_match_workspace(off.ctypes.data, off.ctypes.data, 1) > 0
     assert L.ec3r_retrieval_workspace(1500, 5, 1 << 16) > 0
 
 
