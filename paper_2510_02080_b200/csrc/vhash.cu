@@ -81,6 +81,15 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
     return k;
 }
 
+// table position of a block key: a 32-bit mix (the table has < 2^32 entries)
+__device__ __forceinline__ unsigned long long table_slot(unsigned long long bk, unsigned long long tmask) {
+    uint32_t h = (uint32_t)bk * 0x9E3779B1u ^ (uint32_t)(bk >> 32) * 0x85EBCA77u;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return (unsigned long long)h & tmask;
+}
+
 __device__ __forceinline__ unsigned long long pack_cells(long long cx, long long cy, long long cz) {
     return ((unsigned long long)(cx + kPackOffset) << 42) | ((unsigned long long)(cy + kPackOffset) << 21) |
            (unsigned long long)(cz + kPackOffset);
@@ -126,7 +135,7 @@ __device__ __forceinline__ int load_idx(const BlockEntry* e) {
 // Find or allocate the pool block of block key bk (one thread).  Returns the
 // block index, or -2 when the pool or the table is full.
 __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk) {
-    unsigned long long h = mix64(bk) & v.tmask;
+    unsigned long long h = table_slot(bk, v.tmask);
     for (unsigned long long probe = 0; probe <= v.tmask; ++probe) {
         BlockEntry* e = v.table + h;
         unsigned long long k;
@@ -143,9 +152,8 @@ __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk
                 int got = -2;
                 if ((int64_t)slot < v.max_blocks) {
                     got = (int)slot;
-                    v.block_keys[slot] = bk;
+                    v.block_keys[slot] = bk;  // read by later kernels only: no fence needed
                 }
-                __threadfence();
                 atomicExch(&e->idx, got);
                 return got;
             }
@@ -304,11 +312,13 @@ __global__ void vh_frame_tables_kernel(FuseArgs a, float4* __restrict__ ftab) {
 // (frame-major ... all frames interleaved) and pool working set changed the
 // time by < 10%, so the pool's L2 residency is not the limiter.
 constexpr int ST_H = 8, ST_W = 16;
+constexpr int BC_BITS = 11;  // shared-memory block cache: 2048 entries (16 KB)
 
 __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
     extern __shared__ float4 sA[];  // A[W]
     __shared__ float4 sB[FI_ROWS];
     __shared__ unsigned long long cta_cnt[4];
+    __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
     const int W = a.W, H = a.H;
     const int HW = H * W;
     const int j = blockIdx.y;
@@ -319,7 +329,11 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     for (int u = threadIdx.x; u < W; u += FI_NT) sA[u] = __ldg(tab + u);
     if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
     if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < (1 << BC_BITS); i += FI_NT) bcache[i] = 0ull;
     const float4 Tm = __ldg(tab + W + H);
+    // cache keys are block coordinates relative to the camera centre's block
+    const int3 ob = make_int3((int)floorf(Tm.x * a.inv_cell_f * 0.25f), (int)floorf(Tm.y * a.inv_cell_f * 0.25f),
+                              (int)floorf(Tm.z * a.inv_cell_f * 0.25f));
     __syncthreads();
 
     const float inv = a.inv_cell_f, cellf = a.cell_f;
@@ -330,8 +344,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     const float* dbase = a.depth + (size_t)slot * HW;
     const float* cbase = a.conf + (size_t)slot * HW;
     unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
-    unsigned long long cbk = kEmpty;  // lane's last block
-    int cidx = -2;
 
     // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
     auto advance = [&](int& sy, int& sx) {
@@ -420,86 +432,94 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 }
             }
         }
-        unsigned long long bk[4];
-        int local[4];
+        // phase B: block indices.  The CTA's shared-memory block cache maps
+        // an exact 30-bit block key relative to the frame's camera block to
+        // the pool block; the four lookups of a lane are independent LDS.64.
+        // A miss (first touch of a block by this CTA, a block > 40 m from
+        // the camera, or a cache collision) resolves through the global
+        // table and refills the cache.
+        int got[4], local[4];
+        uint32_t tag[4], slot[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const float c = cs[k];
-            ox[k] = c * (ox[k] - (float)cx[k] * cellf);
-            oy[k] = c * (oy[k] - (float)cy[k] * cellf);
-            oz[k] = c * (oz[k] - (float)cz[k] * cellf);
-            bk[k] = valid[k] ? pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2) : kEmpty;
             local[k] = (cx[k] & 3) | ((cy[k] & 3) << 2) | ((cz[k] & 3) << 4);
+            const unsigned rx = (unsigned)((cx[k] >> 2) - ob.x + 512), ry = (unsigned)((cy[k] >> 2) - ob.y + 512),
+                           rz = (unsigned)((cz[k] >> 2) - ob.z + 512);
+            tag[k] = (valid[k] && (rx | ry | rz) < 1024u) ? (rx | (ry << 10) | (rz << 20)) + 1u : 0u;
+            slot[k] = (tag[k] * 0x9E3779B1u) >> (32 - BC_BITS);
+            const unsigned long long e = tag[k] ? bcache[slot[k]] : 0ull;
+            got[k] = ((uint32_t)(e >> 32) == tag[k] && tag[k]) ? (int)(uint32_t)e : -3;
         }
-        // phase B: block indices.  A lane reuses its previous block; lanes
-        // sharing a block elect one leader per pixel slot; the first probes of
-        // the 4 slots are in flight together, and only a first-probe miss
-        // walks the probe chain / inserts.
-        bool need[4];
+        // misses: lanes sharing a block elect one leader per pixel slot; the
+        // leaders' first probes of the 4 slots are in flight together and
+        // only a first-probe miss walks the probe chain / inserts
+        bool miss[4];
         int leader[4];
+        unsigned long long bk[4];
         unsigned lead = 0;
-        {
-            unsigned long long prevk = cbk;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            miss[k] = valid[k] && got[k] == -3;
+            leader[k] = -1;
+            bk[k] = pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2);
+            if (__any_sync(0xffffffffu, miss[k])) {
+                const unsigned peers = __match_any_sync(0xffffffffu, miss[k] ? bk[k] : kEmpty);
+                leader[k] = __ffs(peers) - 1;
+                if (miss[k] && lane == leader[k]) lead |= 1u << k;
+            }
+        }
+        if (lead) {
+            unsigned long long ek[4];
+            int gk[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                need[k] = valid[k] && bk[k] != prevk;
-                if (valid[k]) prevk = bk[k];
+                ek[k] = kEmpty;
+                gk[k] = -1;
+                if (lead & (1u << k)) load_entry(a.vb.table + table_slot(bk[k], a.vb.tmask), ek[k], gk[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!(lead & (1u << k))) continue;
+                if (ek[k] != bk[k] || gk[k] == -1) gk[k] = vb_find_or_insert(a.vb, bk[k]);
+                got[k] = gk[k];
+                if (tag[k] && gk[k] >= 0) bcache[slot[k]] = ((unsigned long long)tag[k] << 32) | (uint32_t)gk[k];
             }
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            leader[k] = -1;
-            if (__any_sync(0xffffffffu, need[k])) {
-                const unsigned peers = __match_any_sync(0xffffffffu, need[k] ? bk[k] : kEmpty);
-                leader[k] = __ffs(peers) - 1;
-                if (need[k] && lane == leader[k]) lead |= 1u << k;
-            }
-        }
-        int got[4];
-        unsigned long long ek[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            got[k] = -2;
-            ek[k] = kEmpty;
-#ifndef EC3R_EXP_NO_LOOKUP
-            if (lead & (1u << k)) load_entry(a.vb.table + (mix64(bk[k]) & a.vb.tmask), ek[k], got[k]);
-#else
-            if (lead & (1u << k)) { ek[k] = bk[k]; got[k] = (int)(mix64(bk[k]) % 100000ull); }
-#endif
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if ((lead & (1u << k)) && (ek[k] != bk[k] || got[k] == -1)) got[k] = vb_find_or_insert(a.vb, bk[k]);
-        int last = cidx;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (leader[k] >= 0) {
                 const int g = __shfl_sync(0xffffffffu, got[k], leader[k]);
-                if (need[k]) got[k] = g;
-            }
-            if (valid[k]) {
-                if (need[k]) last = got[k];
-                else got[k] = last;
+                if (miss[k]) got[k] = g;
             }
         }
-#pragma unroll
-        for (int k = 3; k >= 0; --k)
-            if (valid[k]) { cbk = bk[k]; break; }
-        cidx = last;
-        // phase C: fire-and-forget reductions into the pool
+        // phase C: reductions into the pool, consecutive pixels of the lane
+        // that land in the same voxel merged first (one update per run)
+        long long cur = -1;
+        float sx = 0.f, sy = 0.f, sz = 0.f, sw = 0.f;
+        unsigned sn = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+            const float c = cs[k];
+            const float wx = c * (ox[k] - (float)cx[k] * cellf);
+            const float wy = c * (oy[k] - (float)cy[k] * cellf);
+            const float wz = c * (oz[k] - (float)cz[k] * cellf);
             if (!valid[k]) continue;
             if (got[k] < 0) { ++n_ovf; continue; }
-            const size_t e = (size_t)got[k] * kBlockVox + local[k];
-#ifndef EC3R_EXP_NO_RED
-            red_add_v4(a.vb.sums + e, ox[k], oy[k], oz[k], cs[k]);
-#ifndef EC3R_EXP_NO_COUNT
-            atomicAdd(a.vb.counts + e, 1u);
-#endif
-#else
-            if (ox[k] == 12345.f) a.vb.counts[e] = 1;
-#endif
+            const long long e = (long long)got[k] * kBlockVox + local[k];
+            if (e != cur) {
+                if (cur >= 0) {
+                    red_add_v4(a.vb.sums + cur, sx, sy, sz, sw);
+                    atomicAdd(a.vb.counts + cur, sn);
+                }
+                cur = e;
+                sx = wx; sy = wy; sz = wz; sw = c; sn = 1;
+            } else {
+                sx += wx; sy += wy; sz += wz; sw += c; ++sn;
+            }
+        }
+        if (cur >= 0) {
+            red_add_v4(a.vb.sums + cur, sx, sy, sz, sw);
+            atomicAdd(a.vb.counts + cur, sn);
         }
     }
     // counters: warp reduce then one shared atomic per warp, one global per CTA
@@ -817,6 +837,8 @@ extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell
     // overflow, are reported and re-run on a larger handle)
     h->max_voxels = capacity > 65536 ? capacity : 65536;
     h->max_blocks = capacity / 4 > 4096 ? capacity / 4 : 4096;
+    // frame fusion addresses voxels as 32-bit (block << 6 | local) ids
+    if (h->max_blocks > (1 << 26) - 2) h->max_blocks = (1 << 26) - 2;
     int64_t tcap = 1;
     while (tcap < 2 * h->max_blocks) tcap <<= 1;
     h->tmask = (unsigned long long)(tcap - 1);
