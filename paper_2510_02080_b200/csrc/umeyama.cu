@@ -238,8 +238,7 @@ __device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, i
         const float* ca = a.conf + (size_t)sa * HW;
         const float* db = a.depth + (size_t)sb * HW;
         const float* cb = a.conf + (size_t)sb * HW;
-        for (int pix = 4 * (rank * UM_NT + threadIdx.x); pix < HW; pix += 4 * UM_CL * UM_NT) {
-            float4 za, wa, zb, wb;
+        auto load = [&](int pix, float4& za, float4& wa, float4& zb, float4& wb) {
             if (vec) {
                 za = __ldg(reinterpret_cast<const float4*>(da + pix));
                 wa = __ldg(reinterpret_cast<const float4*>(ca + pix));
@@ -255,7 +254,18 @@ __device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, i
                 za = make_float4(t0[0], t0[1], t0[2], t0[3]); wa = make_float4(t1[0], t1[1], t1[2], t1[3]);
                 zb = make_float4(t2[0], t2[1], t2[2], t2[3]); wb = make_float4(t3[0], t3[1], t3[2], t3[3]);
             }
+        };
+        // the next visit's four 16-byte loads are in flight while this one
+        // is reduced
+        constexpr int kStride = 4 * UM_CL * UM_NT;
+        int pix = 4 * (rank * UM_NT + threadIdx.x);
+        float4 za, wa, zb, wb;
+        if (pix < HW) load(pix, za, wa, zb, wb);
+        for (; pix < HW; pix += kStride) {
+            float4 nza, nwa, nzb, nwb;
+            if (pix + kStride < HW) load(pix + kStride, nza, nwa, nzb, nwb);
             f(sg, sa, sb, pix, za, wa, zb, wb);
+            za = nza; wa = nwa; zb = nzb; wb = nwb;
         }
     }
 }
