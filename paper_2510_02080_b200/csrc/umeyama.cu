@@ -538,30 +538,82 @@ __device__ void sim3_compose_dev(const double* a, const double* b, double* o) {
     for (int k = 0; k < 3; ++k) o[5 + k] = a[0] * r[k] + a[5 + k];
 }
 
-__global__ void chain_poses_kernel(const double* __restrict__ esim, const int64_t* __restrict__ ecount,
-                                   const int32_t* __restrict__ estatus, const int32_t* __restrict__ epartner,
-                                   const int32_t* __restrict__ sub_edge_off, int n_sub,
-                                   const int32_t* __restrict__ sub_slot_off, double* __restrict__ sub_globals,
-                                   double* __restrict__ slot_globals, int32_t* __restrict__ sub_status) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
+// The chain is sequential: thread 0 walks the submaps with every input and
+// the globals staged in shared memory (the dependent global round trips of
+// a direct walk cost ~1 us per submap); all threads then write back.
+constexpr int CHAIN_NT = 256;
+
+__host__ __device__ inline size_t chain_smem(int n_sub, int n_edges) {
+    return sizeof(double) * 8 * ((size_t)n_sub + n_edges) + sizeof(int64_t) * n_edges +
+           sizeof(int32_t) * (2 * (size_t)n_edges + 2 * n_sub + 1) + 16;
+}
+
+__global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
+    const double* __restrict__ esim, const int64_t* __restrict__ ecount, const int32_t* __restrict__ estatus,
+    const int32_t* __restrict__ epartner, const int32_t* __restrict__ sub_edge_off, int n_sub,
+    const int32_t* __restrict__ sub_slot_off, double* __restrict__ sub_globals, double* __restrict__ slot_globals,
+    int32_t* __restrict__ sub_status, size_t smem_cap) {
+    extern __shared__ double csh[];
+    const int n_edges = sub_edge_off[n_sub];
+    const bool staged = chain_smem(n_sub, n_edges) <= smem_cap;
+    // staged: everything in shared memory; else walk the global arrays
+    double* g = staged ? csh : sub_globals;
+    const double* es = esim;
+    const int64_t* ec = ecount;
+    const int32_t* est = estatus;
+    const int32_t* ep = epartner;
+    const int32_t* eo = sub_edge_off;
+    int32_t* sst = sub_status;
+    if (staged) {
+        double* es_s = g + 8 * (size_t)n_sub;
+        int64_t* ec_s = reinterpret_cast<int64_t*>(es_s + 8 * (size_t)n_edges);
+        int32_t* est_s = reinterpret_cast<int32_t*>(ec_s + n_edges);
+        int32_t* ep_s = est_s + n_edges;
+        int32_t* eo_s = ep_s + n_edges;
+        int32_t* sst_s = eo_s + n_sub + 1;
+        for (int i = threadIdx.x; i < 8 * n_sub; i += CHAIN_NT) g[i] = sub_globals[i];
+        for (int i = threadIdx.x; i < 8 * n_edges; i += CHAIN_NT) es_s[i] = esim[i];
+        for (int i = threadIdx.x; i < n_edges; i += CHAIN_NT) {
+            ec_s[i] = ecount[i];
+            est_s[i] = estatus[i];
+            ep_s[i] = epartner[i];
+        }
+        for (int i = threadIdx.x; i <= n_sub; i += CHAIN_NT) eo_s[i] = sub_edge_off[i];
+        es = es_s; ec = ec_s; est = est_s; ep = ep_s; eo = eo_s; sst = sst_s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         for (int j = 0; j < n_sub; ++j) {
-            const int e0 = sub_edge_off[j], e1 = sub_edge_off[j + 1];
+            const int e0 = eo[j], e1 = eo[j + 1];
             int best = -1;
             for (int e = e0; e < e1; ++e)
-                if (estatus[e] == EC3R_ST_OK && (best < 0 || ecount[e] > ecount[best])) best = e;
+                if (est[e] == EC3R_ST_OK && (best < 0 || ec[e] > ec[best])) best = e;
             int st = EC3R_ST_OK;
             if (e1 > e0) {
                 if (best < 0) st = EC3R_ST_SKIP;  // NoSharedKeyframes
-                else sim3_compose_dev(sub_globals + 8 * epartner[best], esim + 8 * best, sub_globals + 8 * j);
+                else sim3_compose_dev(g + 8 * ep[best], es + 8 * best, g + 8 * j);
             }
-            if (sub_status) sub_status[j] = st;
+            if (sst) sst[j] = st;
         }
     }
     __syncthreads();
-    for (int j = blockIdx.x; j < n_sub; j += gridDim.x)
-        for (int s = sub_slot_off[j] + threadIdx.x; s < sub_slot_off[j + 1]; s += blockDim.x)
-            for (int k = 0; k < 8; ++k) slot_globals[8 * s + k] = sub_globals[8 * j + k];
+    if (staged) {
+        for (int i = threadIdx.x; i < 8 * n_sub; i += CHAIN_NT) sub_globals[i] = g[i];
+        if (sub_status)
+            for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) sub_status[j] = sst[j];
+    }
+    const int s_end = sub_slot_off[n_sub];
+    for (int sidx = threadIdx.x; sidx < s_end; sidx += CHAIN_NT) {
+        // slot -> submap: slots of a submap are contiguous (sub_slot_off)
+        int lo = 0, hi = n_sub;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sub_slot_off[mid] <= sidx) lo = mid; else hi = mid;
+        }
+        for (int k = 0; k < 8; ++k) slot_globals[8 * sidx + k] = g[8 * lo + k];
+    }
 }
+
 
 }  // namespace ec3r
 
@@ -573,9 +625,13 @@ extern "C" int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_cou
                                 int32_t* sub_status, void* stream) {
     if (n_sub < 0 || !sub_edge_off || !sub_globals) return EC3R_EARG;
     if (n_sub == 0) return EC3R_OK;
-    chain_poses_kernel<<<1, 256, 0, as_stream(stream)>>>(edge_sim3, edge_count, edge_status, edge_partner,
-                                                         sub_edge_off, n_sub, sub_slot_off, sub_globals,
-                                                         slot_globals, sub_status);
+    // the edge count lives on the device: reserve the full opt-in shared
+    // memory; a chain that does not fit walks global memory instead
+    const size_t smem = 227 * 1024;
+    EC3R_CUDA_TRY(cudaFuncSetAttribute(chain_poses_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    chain_poses_kernel<<<1, CHAIN_NT, smem, as_stream(stream)>>>(edge_sim3, edge_count, edge_status, edge_partner,
+                                                                sub_edge_off, n_sub, sub_slot_off, sub_globals,
+                                                                slot_globals, sub_status, smem);
     EC3R_CHECK_LAUNCH("chain_poses_kernel");
     return EC3R_OK;
 }

@@ -25,6 +25,9 @@
 // is looked up once per distinct block per warp (__match_any_sync).
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -584,69 +587,6 @@ __global__ void vh_insert_points_kernel(const double* __restrict__ pts, const do
 // ---------------------------------------------------------------------------
 // extraction
 
-// Compact voxels with a non-zero count: (voxel key, pool index).
-// At most max_voxels are emitted; the excess is counted in counters[5]
-// (reported as overflow: the caller grows the handle and re-runs).
-// Also accumulates the cell bounding box bbox[6] = {min x,y,z, max x,y,z}
-// (pre-set to +/-inf) used to shrink the sort key.
-__global__ void vb_compact_kernel(const unsigned int* __restrict__ counts,
-                                  const unsigned long long* __restrict__ block_keys,
-                                  unsigned long long* __restrict__ counters, int64_t max_blocks,
-                                  int64_t max_voxels, unsigned long long* __restrict__ keys,
-                                  int64_t* __restrict__ idx, unsigned long long* __restrict__ cursor,
-                                  int* __restrict__ bbox) {
-    const int64_t n = min((int64_t)counters[4], max_blocks) * kBlockVox;
-    const int lane = threadIdx.x & 31;
-    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool occ = i < n && counts[i] != 0u;
-        const unsigned m = __ballot_sync(0xffffffffu, occ);
-        unsigned long long base = 0;
-        if (lane == 0 && m) base = atomicAdd(cursor, (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (occ) {
-            const unsigned long long o = base + __popc(m & ((1u << lane) - 1u));
-            if ((int64_t)o >= max_voxels) {
-                atomicAdd(&counters[5], 1ull);
-                continue;
-            }
-            long long bx, by, bz;
-            unpack_cells(block_keys[i / kBlockVox], bx, by, bz);
-            const int local = (int)(i % kBlockVox);
-            const long long c[3] = {bx * 4 + (local & 3), by * 4 + ((local >> 2) & 3), bz * 4 + (local >> 4)};
-            keys[o] = pack_cells(c[0], c[1], c[2]);
-            idx[o] = i;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) { mn[k] = min(mn[k], (int)c[k]); mx[k] = max(mx[k], (int)c[k]); }
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mn[k] = min(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
-            mx[k] = max(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
-        }
-        if (lane == 0 && mn[k] <= mx[k]) { atomicMin(&bbox[k], mn[k]); atomicMax(&bbox[3 + k], mx[k]); }
-    }
-}
-
-// Sort-key compaction: (cx, cy, cz) relative to the bounding box packed
-// into 32 bits preserve the lexicographic order of _pack keys.
-__global__ void vb_pack32_kernel(const unsigned long long* __restrict__ keys, const int64_t* __restrict__ idx,
-                                 const int64_t* __restrict__ n_ptr, const int* __restrict__ bbox, int by_bits,
-                                 int bz_bits, uint32_t* __restrict__ k32, uint32_t* __restrict__ i32) {
-    const int64_t n = *n_ptr;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        long long cx, cy, cz;
-        unpack_cells(keys[i], cx, cy, cz);
-        k32[i] = ((uint32_t)(cx - bbox[0]) << (by_bits + bz_bits)) | ((uint32_t)(cy - bbox[1]) << bz_bits) |
-                 (uint32_t)(cz - bbox[2]);
-        i32[i] = (uint32_t)idx[i];
-    }
-}
-
 __global__ void vb_gather32_kernel(const float4* __restrict__ sums, const unsigned int* __restrict__ counts,
                                    const unsigned long long* __restrict__ block_keys, const uint32_t* __restrict__ i32,
                                    const int64_t* __restrict__ n_ptr, double cell, int64_t* __restrict__ okeys,
@@ -741,15 +681,84 @@ static unsigned grid_for(int64_t n) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
-// compact + (optional) sort; n_out receives U, returns the arrays to gather from
-__global__ void clamp_count_kernel(const unsigned long long* __restrict__ cursor, int64_t cap,
-                                   int64_t* __restrict__ n_out) {
-    const int64_t c = (int64_t)*cursor;
-    *n_out = c < cap ? c : cap;
-}
-
 __global__ void bbox_init_kernel(int* bbox) {
     if (threadIdx.x < 3) { bbox[threadIdx.x] = INT_MAX; bbox[3 + threadIdx.x] = INT_MIN; }
+}
+
+// Compaction, pass 1 (one warp per pool block): occupied voxels per block
+// and the bounding box of the used blocks (cells, conservative to the block).
+__global__ void vb_block_count_kernel(const unsigned int* __restrict__ counts,
+                                      const unsigned long long* __restrict__ block_keys,
+                                      const unsigned long long* __restrict__ counters, int64_t max_blocks,
+                                      int* __restrict__ blk_cnt, int* __restrict__ bbox) {
+    const int lane = threadIdx.x & 31;
+    const int64_t used = min((int64_t)counters[4], max_blocks);
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < max_blocks;
+         b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int n = 0;
+        if (b < used) {
+            const unsigned m0 = __ballot_sync(0xffffffffu, counts[b * kBlockVox + lane] != 0u);
+            const unsigned m1 = __ballot_sync(0xffffffffu, counts[b * kBlockVox + 32 + lane] != 0u);
+            n = __popc(m0) + __popc(m1);
+            if (n && lane < 3) {
+                long long c[3];
+                unpack_cells(block_keys[b], c[0], c[1], c[2]);
+                mn[lane] = min(mn[lane], (int)(4 * c[lane]));
+                mx[lane] = max(mx[lane], (int)(4 * c[lane] + 3));
+            }
+        }
+        if (lane == 0) blk_cnt[b] = n;
+    }
+    if (lane < 3) {
+        if (mn[lane] <= mx[lane]) { atomicMin(&bbox[lane], mn[lane]); atomicMax(&bbox[3 + lane], mx[lane]); }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) blk_cnt[max_blocks] = 0;
+}
+
+// Compaction, pass 2 (one warp per pool block): voxel j of block b goes to
+// blk_off[b] + (occupied voxels before it in the block) -- block order, no
+// atomics.  pack32: keys relative to the box in 32 bits (lexicographic order
+// preserved), else _pack keys + int64 voxel indices.  At most max_voxels
+// are written; the excess is counted in counters[5].
+__global__ void vb_block_emit_kernel(const unsigned int* __restrict__ counts,
+                                     const unsigned long long* __restrict__ block_keys,
+                                     const unsigned long long* __restrict__ counters, int64_t max_blocks,
+                                     const int* __restrict__ blk_off, int64_t max_voxels, const int* __restrict__ bbox,
+                                     int pack32, int by_bits, int bz_bits, uint32_t* __restrict__ k32,
+                                     uint32_t* __restrict__ i32, unsigned long long* __restrict__ k64,
+                                     int64_t* __restrict__ i64, unsigned long long* __restrict__ ovf,
+                                     int64_t* __restrict__ n_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t used = min((int64_t)counters[4], max_blocks);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = min((int64_t)blk_off[max_blocks], max_voxels);
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < used;
+         b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const bool o0 = counts[b * kBlockVox + lane] != 0u, o1 = counts[b * kBlockVox + 32 + lane] != 0u;
+        const unsigned m0 = __ballot_sync(0xffffffffu, o0), m1 = __ballot_sync(0xffffffffu, o1);
+        if (!(m0 | m1)) continue;
+        long long bx, by, bz;
+        unpack_cells(block_keys[b], bx, by, bz);
+        const unsigned lt = (1u << lane) - 1u;
+        const int64_t base = blk_off[b];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!(h ? o1 : o0)) continue;
+            const int64_t o = base + (h ? __popc(m0) + __popc(m1 & lt) : __popc(m0 & lt));
+            if (o >= max_voxels) { atomicAdd(ovf, 1ull); continue; }
+            const int local = lane + 32 * h;
+            const long long cx = bx * 4 + (local & 3), cy = by * 4 + ((local >> 2) & 3), cz = bz * 4 + (local >> 4);
+            const int64_t v = b * kBlockVox + local;
+            if (pack32) {
+                k32[o] = ((uint32_t)(cx - bbox[0]) << (by_bits + bz_bits)) | ((uint32_t)(cy - bbox[1]) << bz_bits) |
+                         (uint32_t)(cz - bbox[2]);
+                i32[o] = (uint32_t)v;
+            } else {
+                k64[o] = pack_cells(cx, cy, cz);
+                i64[o] = v;
+            }
+        }
+    }
 }
 
 static int bits_for(int range) {  // bits to hold values 0..range
@@ -763,65 +772,90 @@ static int bits_for(int range) {  // bits to hold values 0..range
 // *i32 = nullptr; with the 32-bit key sort (bounding box fits 32 bits: the
 // usual case, 4 radix passes instead of 8) *i32 holds the sorted pool
 // indices.
+static size_t scan_temp_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (int*)nullptr, (int*)nullptr, (int)n);
+    return t;
+}
+
 static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t workspace_bytes, int64_t* n_out,
                           const unsigned long long** ks, const int64_t** is, const uint32_t** i32,
                           cudaStream_t st) {
     const size_t cap = (size_t)h->max_voxels;
+    const int64_t nb = h->max_blocks;
     Carver cv{(char*)workspace, 0};
     unsigned long long* k0 = cv.take<unsigned long long>(cap);
     int64_t* i0 = cv.take<int64_t>(cap);
     unsigned long long* k1 = cv.take<unsigned long long>(cap);
     int64_t* i1 = cv.take<int64_t>(cap);
-    unsigned long long* cursor = cv.take<unsigned long long>(8);  // [0] cursor, [1..3] bbox (6 ints)
+    unsigned long long* cursor = cv.take<unsigned long long>(8);  // [1..3] bbox (6 ints)
     int* bbox = reinterpret_cast<int*>(cursor + 1);
+    int* blk_cnt = cv.take<int>(nb + 1);
+    int* blk_off = cv.take<int>(nb + 1);
+    size_t scan_bytes = scan_temp_bytes(nb + 1);
+    void* scan_tmp = cv.take<char>(scan_bytes);
     size_t cub_bytes = workspace_bytes - cv.used;
     void* cub_tmp = cv.base + cv.used;
-    EC3R_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+    if (cv.used > workspace_bytes) return EC3R_EWORKSPACE;
     bbox_init_kernel<<<1, 32, 0, st>>>(bbox);
     EC3R_CHECK_LAUNCH("bbox_init_kernel");
-    vb_compact_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->counts, h->block_keys, h->counters, h->max_blocks,
-                                                   h->max_voxels, k0, i0, cursor, bbox);
-    EC3R_CHECK_LAUNCH("vb_compact_kernel");
-    clamp_count_kernel<<<1, 1, 0, st>>>(cursor, h->max_voxels, n_out);
-    EC3R_CHECK_LAUNCH("clamp_count_kernel");
+    const unsigned grid = (unsigned)std::min<int64_t>((nb * 32 + 255) / 256, (int64_t)kNumSMs * 16);
+    vb_block_count_kernel<<<grid, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, blk_cnt, bbox);
+    EC3R_CHECK_LAUNCH("vb_block_count_kernel");
+    if (cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, blk_cnt, blk_off, (int)(nb + 1), st) != cudaSuccess) {
+        set_last_error("cub::DeviceScan::ExclusiveSum", cudaGetLastError());
+        return EC3R_ECUDA;
+    }
     *ks = k0;
     *is = i0;
     *i32 = nullptr;
-    if (sort) {
-        unsigned long long hst[4] = {0, 0, 0, 0};
-        EC3R_CUDA_TRY(cudaMemcpyAsync(hst, cursor, sizeof(hst), cudaMemcpyDeviceToHost, st));
-        EC3R_CUDA_TRY(cudaStreamSynchronize(st));
-        unsigned long long nh = hst[0];
-        int bb[6];
-        memcpy(bb, hst + 1, sizeof(bb));
-        if ((int64_t)nh > h->max_voxels) nh = (unsigned long long)h->max_voxels;
-        if (nh > 0) {
-            const int bx = bits_for(bb[3] - bb[0]), by = bits_for(bb[4] - bb[1]), bz = bits_for(bb[5] - bb[2]);
-            const int total = bx + by + bz;
-            if (total <= 32 && cap <= 0xFFFFFFFFull) {
-                uint32_t* k32 = reinterpret_cast<uint32_t*>(k1);
-                uint32_t* v32 = reinterpret_cast<uint32_t*>(i1);
-                uint32_t* k32s = k32 + cap;
-                uint32_t* v32s = v32 + cap;
-                vb_pack32_kernel<<<kNumSMs * 8, 256, 0, st>>>(k0, i0, n_out, bbox, by, bz, k32, v32);
-                EC3R_CHECK_LAUNCH("vb_pack32_kernel");
-                if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k32, k32s, v32, v32s, (int)nh, 0,
-                                                    total > 0 ? total : 1, st) != cudaSuccess) {
-                    set_last_error("cub::DeviceRadixSort::SortPairs(u32)", cudaGetLastError());
-                    return EC3R_ECUDA;
-                }
-                *i32 = v32s;
-                return EC3R_OK;
-            }
-            if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k0, k1, i0, i1, (int)nh, 0, 63, st) !=
-                cudaSuccess) {
-                set_last_error("cub::DeviceRadixSort::SortPairs", cudaGetLastError());
-                return EC3R_ECUDA;
-            }
-        }
-        *ks = k1;
-        *is = i1;
+    if (!sort) {
+        vb_block_emit_kernel<<<grid, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, blk_off, h->max_voxels,
+                                                   bbox, 0, 0, 0, nullptr, nullptr, k0, i0, h->counters + 5, n_out);
+        EC3R_CHECK_LAUNCH("vb_block_emit_kernel");
+        return EC3R_OK;
     }
+    // one host round trip: the voxel count and the box decide the sort key
+    int hst[8];
+    EC3R_CUDA_TRY(cudaMemcpyAsync(hst, blk_off + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaMemcpyAsync(hst + 1, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t nh = std::min<int64_t>(hst[0], h->max_voxels);
+    const int* bb = hst + 1;
+    if (nh <= 0) {
+        vb_block_emit_kernel<<<1, 32, 0, st>>>(h->counts, h->block_keys, h->counters, 0, blk_off + nb, h->max_voxels,
+                                               bbox, 0, 0, 0, nullptr, nullptr, k0, i0, h->counters + 5, n_out);
+        EC3R_CHECK_LAUNCH("vb_block_emit_kernel");
+        return EC3R_OK;
+    }
+    const int bx = bits_for(bb[3] - bb[0]), by = bits_for(bb[4] - bb[1]), bz = bits_for(bb[5] - bb[2]);
+    const int total = bx + by + bz;
+    if (total <= 32 && cap <= 0xFFFFFFFFull) {
+        uint32_t* k32 = reinterpret_cast<uint32_t*>(k1);
+        uint32_t* v32 = reinterpret_cast<uint32_t*>(i1);
+        uint32_t* k32s = k32 + cap;
+        uint32_t* v32s = v32 + cap;
+        vb_block_emit_kernel<<<grid, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, blk_off, h->max_voxels,
+                                                   bbox, 1, by, bz, k32, v32, nullptr, nullptr, h->counters + 5,
+                                                   n_out);
+        EC3R_CHECK_LAUNCH("vb_block_emit_kernel");
+        if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k32, k32s, v32, v32s, (int)nh, 0,
+                                            total > 0 ? total : 1, st) != cudaSuccess) {
+            set_last_error("cub::DeviceRadixSort::SortPairs(u32)", cudaGetLastError());
+            return EC3R_ECUDA;
+        }
+        *i32 = v32s;
+        return EC3R_OK;
+    }
+    vb_block_emit_kernel<<<grid, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, blk_off, h->max_voxels, bbox,
+                                               0, 0, 0, nullptr, nullptr, k0, i0, h->counters + 5, n_out);
+    EC3R_CHECK_LAUNCH("vb_block_emit_kernel");
+    if (cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, k0, k1, i0, i1, (int)nh, 0, 63, st) != cudaSuccess) {
+        set_last_error("cub::DeviceRadixSort::SortPairs", cudaGetLastError());
+        return EC3R_ECUDA;
+    }
+    *ks = k1;
+    *is = i1;
     return EC3R_OK;
 }
 
@@ -981,7 +1015,9 @@ extern "C" size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h) {
     cub::DeviceRadixSort::SortPairs<uint32_t, uint32_t>(nullptr, cub32, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                                         (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cap, 0, 32);
     if (cub32 > cub_bytes) cub_bytes = cub32;
-    return 4 * align256(sizeof(int64_t) * cap) + align256(64) + align256(cub_bytes);
+    const int64_t nb = h->max_blocks;
+    return 4 * align256(sizeof(int64_t) * cap) + align256(64) + 2 * align256(sizeof(int) * (size_t)(nb + 1)) +
+           align256(scan_temp_bytes(nb + 1)) + align256(cub_bytes);
 }
 
 extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum, int32_t* count,
