@@ -119,6 +119,10 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                  : "memory");
 }
 
+__device__ __forceinline__ void red_add_u32(unsigned int* addr, uint32_t v) {
+    asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
 // One 16-byte L2 read of a table entry {key, idx} (relaxed, gpu scope: the
 // table is only written by this kernel's atomics, so L2 is the coherence
 // point; a volatile access would compile to .STRONG.SYS and two round trips).
@@ -495,34 +499,31 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 if (miss[k]) got[k] = g;
             }
         }
-        // phase C: reductions into the pool, consecutive pixels of the lane
-        // that land in the same voxel merged first (one update per run)
-        long long cur = -1;
-        float sx = 0.f, sy = 0.f, sz = 0.f, sw = 0.f;
-        unsigned sn = 0;
+        // phase C: reductions into the pool.  Consecutive pixels of the lane
+        // in the same voxel form a run whose sums ride along (FFMA with a
+        // 0/1 continuation flag); only a run's last pixel issues the two
+        // reductions (predicated, no branches).
+        uint32_t vid[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (valid[k] && got[k] < 0) ++n_ovf;
+            vid[k] = (valid[k] && got[k] >= 0) ? (((uint32_t)got[k] << 6) | (uint32_t)local[k]) : 0xFFFFFFFFu;
+        }
+        float rx = 0.f, ry = 0.f, rz = 0.f, rw = 0.f, rn = 0.f;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const float c = cs[k];
-            const float wx = c * (ox[k] - (float)cx[k] * cellf);
-            const float wy = c * (oy[k] - (float)cy[k] * cellf);
-            const float wz = c * (oz[k] - (float)cz[k] * cellf);
-            if (!valid[k]) continue;
-            if (got[k] < 0) { ++n_ovf; continue; }
-            const long long e = (long long)got[k] * kBlockVox + local[k];
-            if (e != cur) {
-                if (cur >= 0) {
-                    red_add_v4(a.vb.sums + cur, sx, sy, sz, sw);
-                    atomicAdd(a.vb.counts + cur, sn);
-                }
-                cur = e;
-                sx = wx; sy = wy; sz = wz; sw = c; sn = 1;
-            } else {
-                sx += wx; sy += wy; sz += wz; sw += c; ++sn;
+            const float cont = (k > 0 && vid[k] == vid[k - 1]) ? 1.f : 0.f;
+            rx = fmaf(cont, rx, c * (ox[k] - (float)cx[k] * cellf));
+            ry = fmaf(cont, ry, c * (oy[k] - (float)cy[k] * cellf));
+            rz = fmaf(cont, rz, c * (oz[k] - (float)cz[k] * cellf));
+            rw = fmaf(cont, rw, c);
+            rn = fmaf(cont, rn, 1.f);
+            const bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
+            if (last) {
+                red_add_v4(a.vb.sums + vid[k], rx, ry, rz, rw);
+                red_add_u32(a.vb.counts + vid[k], (uint32_t)rn);
             }
-        }
-        if (cur >= 0) {
-            red_add_v4(a.vb.sums + cur, sx, sy, sz, sw);
-            atomicAdd(a.vb.counts + cur, sn);
         }
     }
     // counters: warp reduce then one shared atomic per warp, one global per CTA
