@@ -32,6 +32,15 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 METRIC = "fused map points/sec and descriptor matches/sec at 1/2/4/8 B200 vs CPU ref"
 
 
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each hot
+    kernel, from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if os.path.exists(p):
+        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).get("kernels", {}).items()}
+    return {}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -242,7 +251,7 @@ def cpu_cores():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--keyframes", type=int, default=300)
@@ -284,6 +293,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = L.ec3r_kernel_launches()
+    _lib.kernel_times()  # drop anything recorded before the timed region
+    _lib.timing_enable(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -292,6 +303,8 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     launches = L.ec3r_kernel_launches() - launches0
+    _lib.timing_enable(False)
+    ktimes = _lib.kernel_times()  # per hot kernel: CUDA events on its launching stream
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -311,23 +324,29 @@ def main():
     P = int(n_points)
     U = step.n_voxels
     C = int(step.seg.shape[0]) * H * W  # overlap pixel pairs streamed by registration
-    fuse_ms = stages["insert"] + stages["emit"]
-    reg_ms = stages["reg"]
-    bytes_fuse = 8 * P + 28 * U
-    bytes_reg = 16 * C
-    achieved_fuse = bytes_fuse / (stages["insert"] * 1e-3) / 1e9
+    traffic = load_traffic()
+
+    def kms(name):  # average launch duration of a hot kernel over the timed region
+        t, n = ktimes.get(name, (0.0, 0))
+        return t / max(n, 1), n
+
+    bytes_fuse = 8 * P  # depth + confidence per streamed pixel
+    bytes_reg = 16 * C  # both frames' depth + confidence per overlap pixel pair
     flops_match = 2.0 * n_pairs_scored * 256
-    achieved_match = flops_match / (stages["match"] * 1e-3) / 1e12
-    roof = {
-        "fuse_insert": {"bound": "hbm", "achieved": achieved_fuse, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": achieved_fuse / peaks["hbm_gbs"], "traffic": None, "ms": stages["insert"],
-                        "alg_bytes": bytes_fuse},
-        "register": {"bound": "hbm", "achieved": bytes_reg / (reg_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": bytes_reg / (reg_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "ms": reg_ms,
-                     "alg_bytes": bytes_reg},
-        "match": {"bound": "tensor", "achieved": achieved_match, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                  "frac": achieved_match / peaks["bf16_tflops"], "ms": stages["match"], "alg_flops": flops_match},
-    }
+    roof = {}
+    for key, kname, alg, bound in (("fuse_insert", "vh_insert_frames_kernel", bytes_fuse, "hbm"),
+                                   ("register", "register_edges_kernel", bytes_reg, "hbm"),
+                                   ("match", "mt_tc_kernel", flops_match, "tensor")):
+        kt, n = kms(kname)
+        if bound == "hbm":
+            ach = alg / (kt * 1e-3) / 1e9 if kt > 0 else None
+            pk, unit = peaks["hbm_gbs"], "GB/s"
+        else:
+            ach = alg / (kt * 1e-3) / 1e12 if kt > 0 else None
+            pk, unit = peaks["bf16_tflops"], "TFLOP/s"
+        roof[key] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit,
+                     "frac": (ach / pk) if ach else None, "traffic": traffic.get(kname), "ms": kt,
+                     "launches": n, "kernel": kname, ("alg_bytes" if bound == "hbm" else "alg_flops"): alg}
     dominant = max(roof, key=lambda k: roof[k]["ms"])
     value = P * world / (ms * 1e-3)
 
@@ -361,7 +380,8 @@ def main():
             "matches_per_s": n_pairs_scored * world / (ms * 1e-3), "matches_unit": "candidate descriptor pairs/s",
             "emitted_matches_per_s": n_matches * world / (ms * 1e-3),
             "stages_ms": stages,
-            "roofline": dict(roof[dominant], kernel=dominant, peak_source=f"{peak_src} MEASURED_PEAKS.json"),
+            "roofline": dict(roof[dominant], stage=dominant, peak_source=f"{peak_src} MEASURED_PEAKS.json",
+                             traffic_source="profiles/kernel_traffic.json (ncu --set full, dram bytes per launch)"),
             "rooflines": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -59,6 +59,12 @@ EC3R_API int ec3r_abi_version(void);
 /* Process-wide count of kernels this library has launched (diagnostic; the
  * benchmark reports the delta over its timed region as gpu_launches). */
 EC3R_API uint64_t ec3r_kernel_launches(void);
+/* Kernel timing diagnostics: when enabled, CUDA events are recorded on the
+ * launching stream around the tensor-core matcher pass (kernel 0), the pool
+ * registration (1) and the frame fusion (2); ec3r_timing_get sums and clears
+ * them (synchronizing on the events). */
+EC3R_API void ec3r_timing_enable(int on);
+EC3R_API int ec3r_timing_get(int kernel, double* ms_total, int64_t* n_launches);
 /* Last CUDA error string of the calling thread's most recent failing call. */
 EC3R_API const char* ec3r_last_error(void);
 

@@ -24,6 +24,8 @@ _SZ = C.c_size_t
 _PROTOS = {
     "ec3r_abi_version": (_I, []),
     "ec3r_kernel_launches": (C.c_uint64, []),
+    "ec3r_timing_enable": (None, [_I]),
+    "ec3r_timing_get": (_I, [_I, _P, _P]),
     "ec3r_sim3_apply": (_I, [_P, _I64, _P, _P, _P]),
     "ec3r_last_error": (C.c_char_p, []),
     "ec3r_inverse_project_workspace": (_SZ, [_I, _I, _I]),
@@ -126,3 +128,24 @@ def workspace(nbytes: int, device=None, tag: str = "default") -> torch.Tensor:
         buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         _ws_cache[key] = buf
     return buf
+
+
+TIMED_KERNELS = ("mt_tc_kernel", "register_edges_kernel", "vh_insert_frames_kernel")
+
+
+def timing_enable(on: bool = True) -> None:
+    """Record CUDA events around the three hot kernels' launches (on their
+    launching streams); read and clear with kernel_times()."""
+    lib().ec3r_timing_enable(1 if on else 0)
+
+
+def kernel_times() -> dict:
+    """{kernel name: (total ms, launches)} since the last call."""
+    L = lib()
+    out = {}
+    for k, name in enumerate(TIMED_KERNELS):
+        ms, n = C.c_double(), C.c_int64()
+        check(L.ec3r_timing_get(k, C.byref(ms), C.byref(n)), "ec3r_timing_get")
+        out[name] = (ms.value, n.value)
+    return out
+

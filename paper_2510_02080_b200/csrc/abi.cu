@@ -5,6 +5,9 @@
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "match.cuh"
@@ -15,6 +18,26 @@ static thread_local char g_last_error[512] = "";
 static std::atomic<unsigned long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static std::atomic<int> g_timing{0};
+static std::mutex g_timing_mu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timed[TK_COUNT];
+
+KernelTimer::KernelTimer(int kernel, cudaStream_t stream) : k(kernel), st(stream) {
+    if (!g_timing.load(std::memory_order_relaxed)) return;
+    if (cudaEventCreate(&e0) != cudaSuccess) { e0 = nullptr; return; }
+    cudaEventRecord(e0, st);
+}
+
+void KernelTimer::stop() {
+    if (!e0) return;
+    cudaEvent_t e1;
+    if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); e0 = nullptr; return; }
+    cudaEventRecord(e1, st);
+    std::lock_guard<std::mutex> g(g_timing_mu);
+    g_timed[k].emplace_back(e0, e1);
+    e0 = nullptr;
+}
 
 void set_last_error(const char* where, cudaError_t e) {
     snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
@@ -39,6 +62,32 @@ using namespace ec3r;
 extern "C" int ec3r_abi_version(void) { return EC3R_ABI_VERSION; }
 extern "C" uint64_t ec3r_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 extern "C" const char* ec3r_last_error(void) { return g_last_error; }
+
+extern "C" void ec3r_timing_enable(int on) { g_timing.store(on ? 1 : 0); }
+
+// Sums the recorded launches of one timed kernel (0 match tensor-core pass,
+// 1 pool registration, 2 frame fusion) and forgets them.  Synchronizes on the
+// recorded events.
+extern "C" int ec3r_timing_get(int kernel, double* ms_total, int64_t* n_launches) {
+    if (kernel < 0 || kernel >= TK_COUNT || !ms_total || !n_launches) return EC3R_EARG;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    {
+        std::lock_guard<std::mutex> g(g_timing_mu);
+        ev.swap(g_timed[kernel]);
+    }
+    double tot = 0.0;
+    for (auto& e : ev) {
+        float ms = 0.f;
+        EC3R_CUDA_TRY(cudaEventSynchronize(e.second));
+        EC3R_CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+        tot += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    *ms_total = tot;
+    *n_launches = (int64_t)ev.size();
+    return EC3R_OK;
+}
 
 // Workspace of ec3r_match_batched:
 //   a_off, b_off (n_pairs+1 int64 each), row state (total_a), col best

@@ -19,6 +19,17 @@ void set_last_error(const char* where, cudaError_t e);
 void set_last_error_msg(const char* msg);
 void count_launch();  // diagnostic counter behind ec3r_kernel_launches()
 
+// Optional kernel timing (ec3r_timing_enable): CUDA events recorded on the
+// launching stream around the hot kernels, summed by ec3r_timing_get.
+enum TimedKernel { TK_MATCH_TC = 0, TK_REGISTER = 1, TK_FUSE_INSERT = 2, TK_COUNT = 3 };
+struct KernelTimer {
+    cudaEvent_t e0 = nullptr;
+    int k = -1;
+    cudaStream_t st = nullptr;
+    KernelTimer(int kernel, cudaStream_t stream);  // records the start event when timing is on
+    void stop();                                  // records the end event
+};
+
 // Every kernel launch of the library is followed by this check (it also
 // feeds the launch counter the benchmark reports as gpu_launches).
 #define EC3R_CHECK_LAUNCH(where)                          \

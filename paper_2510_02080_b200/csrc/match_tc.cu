@@ -815,8 +815,10 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         const size_t smem = tc_smem_bytes(prm.kblocks);
         EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int grid = prm.n_units < kNumSMs ? prm.n_units : kNumSMs;
+        KernelTimer tk(TK_MATCH_TC, st);
         mt_tc_kernel<<<grid, TC_THREADS, smem, st>>>(tmA, tmB, prm);
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
+        tk.stop();
     }
     mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, eps_tc,
                                                                  ratio * ratio, rs, flag_rows, counters);

@@ -677,8 +677,10 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
         EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
     }
+    KernelTimer tk(TK_REGISTER, as_stream(stream));
     register_edges_kernel<<<n_edges * UM_CL, UM_NT, smem, as_stream(stream)>>>(a, out_sim3, out_rms, out_count,
                                                                                out_npairs, out_status, keep_masks);
     EC3R_CHECK_LAUNCH("register_edges_kernel");
+    tk.stop();
     return EC3R_OK;
 }

@@ -955,8 +955,10 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
         EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
     const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, n);
+    KernelTimer tk(TK_FUSE_INSERT, st);
     vh_insert_frames_kernel<<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
+    tk.stop();
     return EC3R_OK;
 }
 

@@ -25,3 +25,11 @@ if [ "$MODE" = "full" ]; then
         > "$OUT/ncu_full.log" 2>&1
     echo "full_rc=$?"
 fi
+if [ "$MODE" = "full" ] && [ -f "$OUT/prof.ncu-rep" ]; then
+    python tools/ncu_traffic.py "$OUT/prof.ncu-rep" > "$OUT/kernel_traffic.json" 2> "$OUT/traffic.err"
+    tools/ncu_metrics.sh "$OUT/prof.ncu-rep" > "$OUT/full_metrics.txt" 2>&1
+    ncu -i "$OUT/prof.ncu-rep" --page source --csv --print-source sass > "$OUT/source.csv" 2>/dev/null
+    python tools/ncu_stalls.py "$OUT/source.csv" 25 > "$OUT/stalls.txt" 2>&1
+    rm -f "$OUT/source.csv"
+    python tools/launch_summary.py "$OUT/launches.csv" > "$OUT/launch_summary.txt" 2>&1
+fi
