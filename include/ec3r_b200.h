@@ -254,6 +254,27 @@ EC3R_API int ec3r_retrieval(const double* pooled, int K, int D, int stride, int 
                    int k_end, void* workspace, size_t workspace_bytes, void* stream);
 EC3R_API size_t ec3r_retrieval_workspace(int K, int stride, int64_t cap_refine);
 
+/* ---------------------------------------------------------------------
+ * K7  the reference's native-kernel plugin slot (_kernels/__init__.py:
+ *     12-33: raycast, nn_query, nn_dists with the semantics of
+ *     _kernels/_numpy.py), results bit-identical to it.
+ * ec3r_nn_query replaces nn_query / nn_dists (_numpy.py:66-137): directed
+ * nearest neighbours query -> ref through the grid hash of cell size
+ * `cell`; query (n_query x 3) and ref (n_ref x 3) float64 row-major.
+ * Output out_dist (n_query) float64 and out_idx (n_query) int64 (index into
+ * ref; inf / -1 when ref is empty).  n_ref <= 2^31 - 1.
+ * ec3r_raycast replaces raycast (_numpy.py:29-47): first-hit parameter of
+ * each ray (origins, dirs: n x 3 float64) against the room shell and solid
+ * boxes solids_h (HOST, n_solids x 6 float64 {min xyz, max xyz}, room
+ * first); 0 where nothing is hit.  n_solids <= 64.
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_nn_workspace(int64_t n_ref, int64_t n_query);
+EC3R_API int ec3r_nn_query(const double* query, int64_t n_query, const double* ref, int64_t n_ref,
+                           double cell, double* out_dist, int64_t* out_idx, void* workspace,
+                           size_t workspace_bytes, void* stream);
+EC3R_API int ec3r_raycast(const double* origins, const double* dirs, int64_t n, const double* solids_h,
+                          int n_solids, double* out_t, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

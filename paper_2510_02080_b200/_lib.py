@@ -54,6 +54,9 @@ _PROTOS = {
     "ec3r_retrieval": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _P, _P, _P, _P, _P, _I64, _P, _I, _I, _P,
                             _SZ, _P]),
     "ec3r_retrieval_workspace": (_SZ, [_I, _I, _I64]),
+    "ec3r_nn_workspace": (_SZ, [_I64, _I64]),
+    "ec3r_nn_query": (_I, [_P, _I64, _P, _I64, _D, _P, _P, _P, _SZ, _P]),
+    "ec3r_raycast": (_I, [_P, _P, _I64, _P, _I, _P, _P]),
 }
 
 EXPORTED = tuple(_PROTOS)

@@ -310,8 +310,66 @@ def gen_retrieval():
     np.savez_compressed(os.path.join(OUT, "retrieval.npz"), **out)
 
 
+# ---------------------------------------------------------------------------
+# 5. The native-kernel plugin slot (_kernels/_numpy.py): nn_query / raycast
+#    on seeded clouds and rays, including exact ties, stray queries past the
+#    last ring, empty inputs and axis-parallel rays.
+
+def gen_kernels():
+    from submap_slam._kernels import _numpy as rk
+
+    rng = np.random.default_rng(404)
+    out = {}
+    cases = []
+    # uniform cloud, queries inside
+    cases.append((rng.uniform(-1, 1, (2000, 3)), rng.uniform(-1, 1, (500, 3)), 0.1))
+    # surface-like cloud with exact duplicates; queries on and near it
+    u = rng.uniform(0, 2, (1500, 2))
+    surf = np.stack([u[:, 0], u[:, 1], 0.3 * np.sin(2 * u[:, 0])], axis=1)
+    surf = np.concatenate([surf, surf[:200]])
+    q = np.concatenate([surf[:100], surf[100:300] + 0.01 * rng.normal(size=(200, 3))])
+    cases.append((surf, q, 0.05))
+    # stray queries beyond ring 8 (brute-force path) and far negative coordinates
+    cases.append((rng.uniform(-3, -2, (800, 3)), np.concatenate([rng.uniform(-3, -2, (50, 3)),
+                                                                 rng.uniform(5, 9, (30, 3))]), 0.02))
+    # integer lattice, queries at cell centres / midpoints: many equal distances
+    g = np.stack(np.meshgrid(np.arange(6), np.arange(6), np.arange(6), indexing="ij"), -1).reshape(-1, 3) * 0.25
+    qq = np.concatenate([g[:40] + 0.125, g[40:80] + np.array([0.125, 0.0, 0.0]), g[80:100]])
+    cases.append((g.astype(float), qq, 0.25))
+    # float32-representable inputs (the device path's common case)
+    cases.append((f32(rng.normal(size=(3000, 3))), f32(rng.normal(size=(700, 3))), 0.15))
+    for i, (ref, qry, cell) in enumerate(cases):
+        d, ix = rk.nn_query(qry, ref, cell)
+        out[f"nn{i}_ref"], out[f"nn{i}_query"], out[f"nn{i}_cell"] = ref, qry, np.float64(cell)
+        out[f"nn{i}_dist"], out[f"nn{i}_idx"] = d, ix
+    out["n_nn"] = np.int64(len(cases))
+    d, ix = rk.nn_query(np.zeros((3, 3)), np.zeros((0, 3)), 0.1)
+    out["nn_empty_ref_dist"], out["nn_empty_ref_idx"] = d, ix
+
+    # raycast: room + interior boxes (scenesim.cast_depth call shape)
+    room_min, room_max = np.array([0.0, 0.0, 0.0]), np.array([8.0, 8.0, 4.0])
+    boxes = [(np.array([2.0, 2.0, 0.0]), np.array([3.0, 3.5, 1.0])),
+             (np.array([5.0, 1.0, 0.0]), np.array([6.5, 2.0, 2.0])),
+             (np.array([1.0, 6.0, 0.5]), np.array([2.0, 7.0, 1.5]))]
+    n = 3000
+    org = np.concatenate([rng.uniform([0.5, 0.5, 0.5], [7.5, 7.5, 3.5], (n, 3)),
+                          rng.uniform(-2, 10, (500, 3))])
+    dirs = rng.normal(size=(len(org), 3))
+    dirs[:300, rng.integers(0, 3, 300)] = 0.0          # axis-parallel components
+    dirs[300:350] = np.array([1.0, 0.0, 0.0])
+    dirs[350:400] = np.array([0.0, -1.0, 0.0])
+    dirs[400:420] = 0.0                               # degenerate zero rays
+    org[420:440] = np.array([2.0, 2.5, 0.5])           # on a box face
+    t = rk.raycast(org, dirs, room_min, room_max, boxes)
+    out["rc_origins"], out["rc_dirs"], out["rc_t"] = org, dirs, t
+    out["rc_room_min"], out["rc_room_max"] = room_min, room_max
+    out["rc_boxes"] = np.stack([np.stack(b) for b in boxes])
+    np.savez_compressed(os.path.join(OUT, "kernels.npz"), **out)
+
+
 if __name__ == "__main__":
     gen_registration()
     gen_mapping()
     gen_match()
     gen_retrieval()
+    gen_kernels()

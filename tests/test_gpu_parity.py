@@ -551,3 +551,68 @@ def test_retrieval_sharded_equals_single():
     adm = loops.admit(mat, np.arange(1500), full[2], full[3])
     assert [p for p, _ in adm] == [p for p, _ in exp]
     assert len(exp) > 0
+
+
+# --------------------------------------------------------------------------
+# K7 native-kernel plugin slot: nn_query / nn_dists / raycast (bit-exact)
+
+def test_kernels_nn_query_golden(golden):
+    from paper_2510_02080_b200 import kernels
+    g = golden("kernels")
+    for i in range(int(g["n_nn"])):
+        d, ix = kernels.nn_query(g[f"nn{i}_query"], g[f"nn{i}_ref"], float(g[f"nn{i}_cell"]))
+        np.testing.assert_array_equal(ix, g[f"nn{i}_idx"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(d, g[f"nn{i}_dist"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(kernels.nn_dists(g[f"nn{i}_query"], g[f"nn{i}_ref"],
+                                                       float(g[f"nn{i}_cell"])), g[f"nn{i}_dist"])
+    d, ix = kernels.nn_query(np.zeros((3, 3)), np.zeros((0, 3)), 0.1)
+    np.testing.assert_array_equal(d, g["nn_empty_ref_dist"])
+    np.testing.assert_array_equal(ix, g["nn_empty_ref_idx"])
+    d, ix = kernels.nn_query(np.zeros((0, 3)), np.ones((5, 3)), 0.1)
+    assert d.shape == (0,) and ix.shape == (0,) and ix.dtype == np.int64
+
+
+def test_kernels_nn_query_large_vs_oracle():
+    """A cloud_metrics-sized and a larger problem: the first queries against
+    the oracle (bit-exact), every query against a float64 brute force."""
+    from oracle import kernels as ok
+    from paper_2510_02080_b200 import kernels
+    rng = np.random.default_rng(77)
+    u = rng.uniform(0, 4, (300000, 2))
+    ref_pts = np.stack([u[:, 0], u[:, 1], 0.2 * np.sin(3 * u[:, 0]) * np.cos(2 * u[:, 1])], axis=1)
+    qry = ref_pts[rng.integers(0, len(ref_pts), 40000)] + 0.01 * rng.normal(size=(40000, 3))
+    qry[:50] += 3.0  # strays past ring 8
+    cell = 0.02
+    d, ix = kernels.nn_query(qry, ref_pts, cell)
+    de, ie = ok.nn_query(qry[:300], ref_pts, cell)
+    np.testing.assert_array_equal(d[:300], de)
+    np.testing.assert_array_equal(ix[:300], ie)
+    # consistency + optimality over all queries (GPU float64 brute force)
+    np.testing.assert_array_equal(d, np.sqrt(((ref_pts[ix] - qry) ** 2).sum(axis=1)))
+    R = torch.as_tensor(ref_pts, device="cuda")
+    mins = []
+    for q0 in range(0, len(qry), 500):
+        Q = torch.as_tensor(qry[q0:q0 + 500], device="cuda")
+        mins.append(torch.cdist(Q, R, compute_mode="donot_use_mm_for_euclid_dist").min(dim=1).values.cpu().numpy())
+    np.testing.assert_allclose(d, np.concatenate(mins), rtol=1e-14, atol=0)
+
+
+def test_kernels_raycast_golden_and_render(golden):
+    from oracle import kernels as ok
+    from paper_2510_02080_b200 import kernels
+    g = golden("kernels")
+    boxes = [(b[0], b[1]) for b in g["rc_boxes"]]
+    t = kernels.raycast(g["rc_origins"], g["rc_dirs"], g["rc_room_min"], g["rc_room_max"], boxes)
+    np.testing.assert_array_equal(t, g["rc_t"])
+    # a full 518 x 392 perspective render (scenesim.render_depth's ray layout)
+    h, w, f = 392, 518, 400.0
+    uu, vv = np.meshgrid(np.arange(w, dtype=float), np.arange(h, dtype=float))
+    dirs = np.stack([(uu - w / 2) / f, (vv - h / 2) / f, np.ones_like(uu)], -1).reshape(-1, 3)
+    c, s_ = np.cos(0.7), np.sin(0.7)
+    Rw = np.array([[c, 0, s_], [0, 1, 0], [-s_, 0, c]]) @ np.array([[1, 0, 0], [0, 0, 1], [0, -1, 0]])
+    dw = dirs @ Rw.T
+    org = np.broadcast_to(np.array([4.0, 3.0, 1.5]), dw.shape)
+    t = kernels.raycast(org, dw, g["rc_room_min"], g["rc_room_max"], boxes)
+    sel = np.random.default_rng(3).integers(0, len(dw), 3000)
+    np.testing.assert_array_equal(t[sel], ok.raycast(org[sel], dw[sel], g["rc_room_min"], g["rc_room_max"], boxes))
+    assert (t > 0).all()

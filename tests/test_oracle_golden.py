@@ -114,3 +114,26 @@ def test_retrieval_cases(golden):
                                        rtol=0, atol=1e-15)
         keys = np.array(sorted(st.scores), np.int64).reshape(-1, 2)
         np.testing.assert_array_equal(keys, g[f"c{i}_matrix_keys"])
+
+
+# --------------------------------------------------------------------------
+# native-kernel plugin slot (_kernels/_numpy.py): nn_query / raycast
+
+def test_kernels_nn_query_cases(golden):
+    from oracle import kernels as ok
+    g = golden("kernels")
+    for i in range(int(g["n_nn"])):
+        d, ix = ok.nn_query(g[f"nn{i}_query"], g[f"nn{i}_ref"], float(g[f"nn{i}_cell"]))
+        np.testing.assert_array_equal(ix, g[f"nn{i}_idx"], err_msg=f"case {i}")
+        np.testing.assert_array_equal(d, g[f"nn{i}_dist"], err_msg=f"case {i}")
+    d, ix = ok.nn_query(np.zeros((3, 3)), np.zeros((0, 3)), 0.1)
+    np.testing.assert_array_equal(d, g["nn_empty_ref_dist"])
+    np.testing.assert_array_equal(ix, g["nn_empty_ref_idx"])
+
+
+def test_kernels_raycast_case(golden):
+    from oracle import kernels as ok
+    g = golden("kernels")
+    boxes = [(b[0], b[1]) for b in g["rc_boxes"]]
+    t = ok.raycast(g["rc_origins"], g["rc_dirs"], g["rc_room_min"], g["rc_room_max"], boxes)
+    np.testing.assert_array_equal(t, g["rc_t"])
