@@ -169,6 +169,10 @@ typedef struct {
 } ec3r_vhash_stats;
 
 EC3R_API int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream);
+/* As ec3r_vhash_create with the pool's block count chosen explicitly (a map
+ * refused with overflow can be re-created from its stats: n_blocks, voxels). */
+EC3R_API int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks,
+                                     double cell_size, void* stream);
 EC3R_API int ec3r_vhash_destroy(ec3r_vhash* h);
 EC3R_API int64_t ec3r_vhash_capacity(const ec3r_vhash* h);
 EC3R_API int ec3r_vhash_clear(ec3r_vhash* h, void* stream);

@@ -864,14 +864,12 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
 
 using namespace ec3r;
 
-extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream) {
-    if (!out || capacity < 2 || !(cell_size > 0)) return EC3R_EARG;
+extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks, double cell_size,
+                                       void* stream) {
+    if (!out || max_voxels < 2 || max_blocks < 1 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
-    // capacity = voxels to emit at most; the pool holds capacity / 4 blocks
-    // (surface blocks are far fuller than 4 of 64 voxels; sparse inputs
-    // overflow, are reported and re-run on a larger handle)
-    h->max_voxels = capacity > 65536 ? capacity : 65536;
-    h->max_blocks = capacity / 4 > 4096 ? capacity / 4 : 4096;
+    h->max_voxels = max_voxels > 65536 ? max_voxels : 65536;
+    h->max_blocks = max_blocks > 4096 ? max_blocks : 4096;
     // frame fusion addresses voxels as 32-bit (block << 6 | local) ids
     if (h->max_blocks > (1 << 26) - 2) h->max_blocks = (1 << 26) - 2;
     int64_t tcap = 1;
@@ -896,6 +894,14 @@ extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell
     EC3R_CUDA_TRY(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, st));
     *out = h;
     return ec3r_vhash_clear(h, stream);
+}
+
+// capacity = voxels to emit at most; the pool holds capacity / 4 blocks
+// (surface blocks are far fuller than 4 of 64 voxels; sparse inputs
+// overflow, are reported and re-run on a larger handle)
+extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream) {
+    if (capacity < 2) return EC3R_EARG;
+    return ec3r_vhash_create_sized(out, capacity, capacity / 4 > 1 ? capacity / 4 : 1, cell_size, stream);
 }
 
 extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {

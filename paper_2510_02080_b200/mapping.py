@@ -190,12 +190,18 @@ class ChainPlan:
 class VoxelMap:
     """Owner of one ec3r_vhash handle (K4)."""
 
-    def __init__(self, cell: float = 0.02, capacity: int = 1 << 20, stream=None):
+    def __init__(self, cell: float = 0.02, capacity: int = 1 << 20, stream=None, max_blocks: Optional[int] = None):
+        """capacity: voxels the emit can hold; max_blocks: 4x4x4 pool blocks
+        (default capacity / 4; size it from a previous fill's n_blocks)."""
         L = _lib.lib()
         self.cell = float(cell)
         h = C.c_void_p()
-        _lib.check(L.ec3r_vhash_create(C.byref(h), int(capacity), self.cell, _lib.stream_ptr(stream)),
-                   "ec3r_vhash_create")
+        if max_blocks is None:
+            _lib.check(L.ec3r_vhash_create(C.byref(h), int(capacity), self.cell, _lib.stream_ptr(stream)),
+                       "ec3r_vhash_create")
+        else:
+            _lib.check(L.ec3r_vhash_create_sized(C.byref(h), int(capacity), int(max_blocks), self.cell,
+                                                 _lib.stream_ptr(stream)), "ec3r_vhash_create_sized")
         self._h = h
         self.capacity = int(L.ec3r_vhash_capacity(h))  # voxel slots of the block pool
         self.expected = int(capacity)
@@ -267,13 +273,15 @@ class VoxelMap:
 
 
 def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional[VoxelMap] = None,
-               expected_voxels: Optional[int] = None, sort: bool = True):
+               expected_voxels: Optional[int] = None, sort: bool = True, expected_blocks: Optional[int] = None):
     """Voxel fusion of pool slots with overflow-safe capacity growth.
-    Returns (VoxelMap, (keys, centroid, wsum, count), stats)."""
+    Returns (VoxelMap, (keys, centroid, wsum, count), stats).  With the
+    expected voxel and block counts of a previous fill the map is sized at 2x
+    both (a small pool and table keep the per-fill clear and emit cheap)."""
     if vmap is None or vmap.cell != cell:
         n_px = int(slots.numel()) * pool.H * pool.W
         cap = expected_voxels * 2 if expected_voxels else max(1 << 16, n_px // 8)
-        vmap = VoxelMap(cell, cap)
+        vmap = VoxelMap(cell, cap, max_blocks=2 * expected_blocks if expected_blocks else None)
     while True:
         vmap.clear()
         vmap.insert_frames(pool, slots)
@@ -283,7 +291,7 @@ def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional
             st = vmap.stats()  # the emit may overflow the voxel capacity too
             if st["n_overflow"] == 0:
                 break
-        vmap = VoxelMap(cell, vmap.expected * 4)
+        vmap = VoxelMap(cell, vmap.expected * 4)  # default block sizing (capacity / 4)
     return vmap, out, st
 
 
