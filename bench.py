@@ -260,6 +260,7 @@ def main():
     ap.add_argument("--desc", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -356,6 +357,10 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(step, dm, desc, args, world)
 
+    extras = None
+    if rank == 0 and not args.no_extras:
+        extras = run_extras(peaks)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         c = cpu_sample()
@@ -389,6 +394,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "extras": extras,
         }
         print(json.dumps(line))
     if world > 1:
@@ -471,6 +477,77 @@ def run_e2e(step, dm, desc, args, world):
             "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(out_bytes), "steps": steps,
             "pipelined": "inputs double-buffered: step i+1 H2D overlaps step i compute",
             "h2d_pinned_gbs": h2d_gbs}
+
+
+def _time_ms(fn, reps=5, warm=2):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def run_extras(peaks):
+    """Side measurements outside the step (not part of `value`):
+    * configs[2]: the matcher sweep, one N = M pair per size and the
+      local-loop batch (1 query x 7 window keyframes) at 4k, D = 256, with
+      the tensor-core kernel's own CUDA-event time;
+    * K7: nn_query at the cloud_metrics size (20k x 20k) and
+      at 1M x 1M points, raycast of 100 full 518x392 frames."""
+    import torch
+
+    from paper_2510_02080_b200 import _lib, kernels, synth, tracking
+
+    out = {"matcher_sweep": [], "nn_query": [], "raycast": None}
+    for n in (2048, 8192, 32768):
+        A, B, ao, bo = synth.make_descriptor_pairs(1, n, n, 256, 0.05, seed=n, device="cuda")
+        run = lambda: tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)  # noqa: E731
+        run()
+        _lib.kernel_times()
+        _lib.timing_enable(True)
+        ms = _time_ms(run)
+        _lib.timing_enable(False)
+        kt, kn = _lib.kernel_times()["mt_tc_kernel"]
+        kms = kt / max(kn, 1)
+        fl = 2.0 * n * n * 256
+        st = tracking.last_match_stats()
+        out["matcher_sweep"].append({"n": n, "m": n, "ms": ms, "pairs_per_s": n * n / (ms * 1e-3),
+                                     "tc_kernel_ms": kms, "tc_tflops": fl / (kms * 1e-3) / 1e12,
+                                     "tc_frac": fl / (kms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                                     "rows_rescanned": st["rows_rescanned"], "cols_rescanned": st["cols_rescanned"]})
+    A, B, ao, bo = synth.make_descriptor_pairs(7, 4096, 4096, 256, 0.05, seed=7, device="cuda")
+    A = A[:4096].repeat(7, 1)  # one query frame against 7 window keyframes
+    run = lambda: tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)  # noqa: E731
+    ms = _time_ms(run)
+    out["local_loop_batch"] = {"pairs": 7, "n": 4096, "m": 4096, "ms": ms, "pairs_per_s": 7 * 4096 * 4096 / (ms * 1e-3)}
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    for n, cell in ((20000, 0.05), (1 << 20, 0.01)):
+        ref = torch.rand((n, 3), generator=g, device="cuda", dtype=torch.float64) * torch.tensor(
+            [4.0, 4.0, 0.0], device="cuda", dtype=torch.float64)
+        ref[:, 2] = 0.2 * torch.sin(3 * ref[:, 0])
+        qry = ref[torch.randperm(n, generator=g, device="cuda")] + 0.003 * torch.randn(
+            (n, 3), generator=g, device="cuda", dtype=torch.float64)
+        ms = _time_ms(lambda: kernels.nn_query_device(qry, ref, cell))
+        out["nn_query"].append({"n_query": n, "n_ref": n, "cell": cell, "ms": ms, "queries_per_s": n / (ms * 1e-3)})
+    h, w = 392, 518
+    uu, vv = torch.meshgrid(torch.arange(w, device="cuda", dtype=torch.float64),
+                            torch.arange(h, device="cuda", dtype=torch.float64), indexing="xy")
+    d = torch.stack([(uu - w / 2) / 400.0, (vv - h / 2) / 400.0, torch.ones_like(uu)], -1).reshape(-1, 3)
+    d = d.repeat(100, 1)
+    o = torch.tensor([4.0, 3.0, 1.5], device="cuda", dtype=torch.float64).expand_as(d).contiguous()
+    boxes = [((2.0, 2.0, 0.0), (3.0, 3.5, 1.0)), ((5.0, 1.0, 0.0), (6.5, 2.0, 2.0))]
+    ms = _time_ms(lambda: kernels.raycast_device(o, d, (0.0, 0.0, 0.0), (8.0, 8.0, 4.0), boxes))
+    out["raycast"] = {"rays": int(d.shape[0]), "ms": ms, "rays_per_s": d.shape[0] / (ms * 1e-3)}
+    return out
 
 
 def run_reference(args, rank, world):

@@ -616,3 +616,29 @@ def test_kernels_raycast_golden_and_render(golden):
     sel = np.random.default_rng(3).integers(0, len(dw), 3000)
     np.testing.assert_array_equal(t[sel], ok.raycast(org[sel], dw[sel], g["rc_room_min"], g["rc_room_max"], boxes))
     assert (t > 0).all()
+
+
+def test_match_sweep_32k_vs_oracle():
+    """configs[2] top size: one 32768 x 32768 x 256 pair.  Checked row by row
+    against the float64 reference decisions on a sample of rows (their full
+    rows, and the full columns of the sampled rows' matches)."""
+    from paper_2510_02080_b200 import synth, tracking
+    n = 32768
+    A, B, ao, bo = synth.make_descriptor_pairs(1, n, n, 256, 0.05, seed=32)
+    mb, nm = tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)
+    mb = mb.cpu().numpy()
+    a = A.view(torch.bfloat16).double()
+    b = B.view(torch.bfloat16).double()
+    rows = torch.as_tensor(np.random.default_rng(1).choice(n, 600, replace=False), device="cuda")
+    sim = a[rows] @ b.T                                   # exact: bf16 products, fp64 sums
+    d2 = torch.clamp(2.0 - 2.0 * sim, min=0.0)
+    best = torch.argmin(d2, dim=1)
+    second = torch.topk(d2, 2, dim=1, largest=False).values[:, 1]
+    d1 = d2.gather(1, best[:, None])[:, 0]
+    col_best = torch.argmin(torch.clamp(2.0 - 2.0 * (a @ b[best].T), min=0.0), dim=0)
+    keep = (col_best == rows) & ~(d1 > 0.64 * second)
+    exp = torch.where(keep, best, torch.full_like(best, -1)).cpu().numpy()
+    np.testing.assert_array_equal(mb[rows.cpu().numpy()], exp)
+    assert int(nm[0]) == int((mb >= 0).sum())
+    st = tracking.last_match_stats()
+    assert st["rows_rescanned"] < 0.01 * n and st["cols_rescanned"] < 0.01 * n, st
