@@ -32,6 +32,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "match.cuh"
 
@@ -66,7 +68,11 @@ struct __align__(16) RowCand {
 struct __align__(16) TcUnit {
     int pair;
     int row0;        // first row of the unit within the packed A
-    long long slot;  // first column slot of the unit
+    int col0;        // column range [col0, col1) within the pair (multiples of TC_BN)
+    int col1;
+    long long slot;  // column slot of the unit's first column
+    int split;       // which column range (row candidates: cand[row * n_split + split])
+    int pad;
 };
 
 struct TcParams {
@@ -76,6 +82,7 @@ struct TcParams {
     int n_units;
     int kblocks;        // D / 64
     RowCand* cand;
+    int n_split;
     unsigned long long* col_slots;  // per unit and column: (ordered best key << 32) | ordered second key
 };
 
@@ -341,8 +348,8 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             uint32_t phase = 0, a_phase = 0;
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
                 const TcUnit un = p.units[u];
-                const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
-                const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
+                const int64_t b0 = p.b_off[un.pair] + un.col0;
+                const int n_tiles = (un.col1 - un.col0) / TC_BN;
                 // A slices are refilled one k-block at a time as the previous
                 // unit's last tile releases them, interleaved with the first
                 // tile's B k-blocks, so the unit switch does not drain the MMA
@@ -358,7 +365,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                         mbar_wait_sleep(b_empty + stage, phase ^ 1);
                         mbar_expect_tx(b_full + stage, TC_BOX_BYTES);
                         tma_load_2d(sB + (size_t)stage * TC_BOX_BYTES, &tmB, b_full + stage, kb * TC_BK,
-                                    (int)(b0 + t * TC_BN));
+                                    (int)(b0 + t * TC_BN));  // past the pair: rows of the next pair or TMA zero fill
                         if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -375,8 +382,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const uint32_t sA_addr = smem_u32(sA), sB_addr = smem_u32(sB);
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
                 const TcUnit un = p.units[u];
-                const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
-                const int n_tiles = (int)((b1 - b0 + TC_BN - 1) / TC_BN);
+                const int n_tiles = (un.col1 - un.col0) / TC_BN;
                 for (int t = 0; t < n_tiles; ++t) {
                     mbar_wait_sleep(t_empty + acc, acc_phase ^ 1);
                     tc_fence_after();
@@ -425,14 +431,14 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int64_t a1 = p.a_off[un.pair + 1], a0 = p.a_off[un.pair];
             const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
             const int M = (int)(b1 - b0);
-            const int n_tiles = (M + TC_BN - 1) / TC_BN;
+            const int n_tiles = (un.col1 - un.col0) / TC_BN;
             RowTop2 R0{-INFINITY, -INFINITY, 0}, R1{-INFINITY, -INFINITY, 0};
             const int64_t row0 = (int64_t)un.row0 + q * 32 + lane, row1 = row0 + TC_BM;
             const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
-                const int col0 = t * TC_BN;
+                const int col0 = un.col0 + t * TC_BN;
                 const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + h * 64);
                 const uint32_t cbq = smem_u32(colbuf + (size_t)(tb * 4 + q) * TC_BN + h * 64);
                 uint32_t ra[32], rb[32], rc[32], rd[32];
@@ -477,7 +483,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     // bits 7..6 of the best key (column code, meaningless on
                     // this side) now hold the quarter: bits 7..0 = row in unit
                     const float bq = __uint_as_float((__float_as_uint(bk) & ~0xC0u) | (qs << 6));
-                    __stcg(p.col_slots + un.slot + col0 + et,
+                    __stcg(p.col_slots + un.slot + (col0 - un.col0) + et,
                            ((unsigned long long)f2ord(bq) << 32) | (unsigned long long)f2ord(sk));
                 }
                 tb ^= 1;
@@ -500,7 +506,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     rc.k2 = fmax3f(R0.s, o0.y, fminf(R0.b, o0.x));
                     rc.c1 = o0.x > R0.b ? __float_as_int(o0.z) : c0;
                     rc.pad = 0;
-                    p.cand[row0] = rc;
+                    p.cand[row0 * p.n_split + un.split] = rc;
                 }
                 if (rv1) {
                     RowCand rc;
@@ -508,7 +514,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     rc.k2 = fmax3f(R1.s, o1.y, fminf(R1.b, o1.x));
                     rc.c1 = o1.x > R1.b ? __float_as_int(o1.z) : c1;
                     rc.pad = 0;
-                    p.cand[row1] = rc;
+                    p.cand[row1 * p.n_split + un.split] = rc;
                 }
             }
         }
@@ -553,7 +559,7 @@ constexpr double kRatioSlack = 1e-9;
 //     the runner-up cannot clamp to d2 = 0) and the bounds pass;
 // everything else is listed for the float64 row re-scan.
 __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                               int64_t total_a, const RowCand* __restrict__ cand, double eps_tc, double ratio2,
+                               int64_t total_a, RowCand* __restrict__ cand, int n_split, double eps_tc, double ratio2,
                                MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
                                int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -563,7 +569,16 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
     MatchRowState s;
     s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
     if (M == 0) { rs[r] = s; return; }  // no columns: no match
-    const RowCand c = cand[r];
+    // merge the row's column-range candidates (top-2 keys, best column);
+    // the merged candidate goes back to split 0 for the column stage
+    RowCand c = cand[r * n_split];
+    for (int sp = 1; sp < n_split; ++sp) {
+        const RowCand o = cand[r * n_split + sp];
+        if (o.c1 < 0) continue;  // range entirely past the pair's columns
+        c.k2 = fmax3f(c.k2, o.k2, fminf(c.k1, o.k1));
+        if (o.k1 > c.k1) { c.k1 = o.k1; c.c1 = o.c1; }
+    }
+    if (n_split > 1) cand[r * n_split] = c;
     if (M == 1) {  // one column: argmax certain, ratio test skipped (tracking.py:165)
         s.best = 0;
         s.ratio_ok = 1;
@@ -588,7 +603,7 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
 // they separate; otherwise the column is listed (once) for the float64
 // column re-scan, which writes col_best.
 __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                             int64_t total_a, const RowCand* __restrict__ cand,
+                             int64_t total_a, const RowCand* __restrict__ cand, int n_split,
                              const unsigned long long* __restrict__ col_slots,
                              const long long* __restrict__ pair_slot, double eps_tc, double ratio2,
                              MatchRowState* __restrict__ rs, int32_t* __restrict__ col_best,
@@ -630,7 +645,7 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
         } else if (rc >= 0 && rc < N) {
             // an approximate value of (r, c): the row's best key when it is
             // this element, else the exact similarity behind d1
-            const RowCand rcand = cand[r];
+            const RowCand rcand = cand[r * n_split];
             double kv = 0.0, ke = -1.0;
             if (rcand.c1 == s.best) { kv = rcand.k1; ke = key_eps(kv, eps_tc); }
             else if (s.ratio_ok == -1 && s.d1 > 0.0) { kv = 1.0 - 0.5 * s.d1; ke = 1e-12; }
@@ -707,18 +722,39 @@ static int64_t n_col_slots(const int64_t* a_off_h, const int64_t* b_off_h, int n
     return n;
 }
 
-static int64_t max_units(int64_t ta, int n_pairs) { return ta / (TC_NA * TC_BM) + n_pairs + 1; }
+// Column ranges per row block: enough units for eight waves of CTAs when the
+// batch has few row blocks (the configs[2] sweep's single pairs); 1 for
+// batches of many pairs.  Row candidates are then merged across ranges.
+static int choose_split(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
+    int64_t rb = 0, max_tiles = 1;
+    for (int p = 0; p < n_pairs; ++p) {
+        const int64_t N = a_off_h[p + 1] - a_off_h[p], M = b_off_h[p + 1] - b_off_h[p];
+        if (M == 0 || N == 0) continue;
+        rb += (N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM);
+        max_tiles = std::max<int64_t>(max_tiles, (M + TC_BN - 1) / TC_BN);
+    }
+    if (rb == 0) return 1;
+    int64_t sp = (8 * kNumSMs + rb - 1) / rb;  // >= 8 waves: <= 1/8 wave quantization
+    sp = std::min<int64_t>(std::min<int64_t>(sp, max_tiles), 64);
+    return (int)std::max<int64_t>(sp, 1);
+}
+
+static int64_t max_units(int64_t ta, int n_pairs, int n_split) {
+    return (ta / (TC_NA * TC_BM) + n_pairs + 1) * n_split;
+}
 
 size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs) {
     const int64_t ta = a_off_h[n_pairs];
-    return align256(sizeof(RowCand) * (size_t)ta) +
+    const int sp = choose_split(a_off_h, b_off_h, n_pairs);
+    return align256(sizeof(RowCand) * (size_t)ta * sp) +
            align256(sizeof(unsigned long long) * (size_t)n_col_slots(a_off_h, b_off_h, n_pairs)) +
-           align256(sizeof(long long) * (size_t)(n_pairs + 1)) + align256(sizeof(TcUnit) * (size_t)max_units(ta, n_pairs)) +
+           align256(sizeof(long long) * (size_t)(n_pairs + 1)) + align256(sizeof(TcUnit) * (size_t)max_units(ta, n_pairs, sp)) +
            align256(64);
 }
 
 struct TcWs {
     RowCand* cand;
+    int n_split;
     unsigned long long* slots;
     long long* pair_slot;
     TcUnit* units;
@@ -730,10 +766,11 @@ static TcWs carve_tc(void* tc_ws, const int64_t* a_off_h, const int64_t* b_off_h
     const int64_t ta = a_off_h[n_pairs];
     Carver cv{(char*)tc_ws, 0};
     TcWs w;
-    w.cand = cv.take<RowCand>(ta);
+    w.n_split = choose_split(a_off_h, b_off_h, n_pairs);
+    w.cand = cv.take<RowCand>(ta * w.n_split);
     w.slots = cv.take<unsigned long long>(n_col_slots(a_off_h, b_off_h, n_pairs));
     w.pair_slot = cv.take<long long>(n_pairs + 1);
-    w.units = cv.take<TcUnit>(max_units(ta, n_pairs));
+    w.units = cv.take<TcUnit>(max_units(ta, n_pairs, w.n_split));
     w.nb = cv.take<unsigned int>(16);
     w.used = cv.used;
     return w;
@@ -766,14 +803,18 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     // units and column-slot bases; units + pair bases travel in one copy
     std::vector<TcUnit> hu;
     std::vector<long long> hp(n_pairs + 1);
-    hu.reserve(max_units(ta, n_pairs));
+    hu.reserve(max_units(ta, n_pairs, w.n_split));
     long long slot = 0;
     for (int pi = 0; pi < n_pairs; ++pi) {
         hp[pi] = slot;
         const int64_t M = b_off_h[pi + 1] - b_off_h[pi];
         if (M == 0) continue;  // no columns: nothing to score
+        const int tiles = (int)((M + TC_BN - 1) / TC_BN);
         for (int64_t r = a_off_h[pi]; r < a_off_h[pi + 1]; r += TC_NA * TC_BM) {
-            hu.push_back(TcUnit{pi, (int)r, slot});
+            for (int sp = 0; sp < w.n_split; ++sp) {
+                const int t0 = (int)((int64_t)tiles * sp / w.n_split), t1 = (int)((int64_t)tiles * (sp + 1) / w.n_split);
+                if (t1 > t0) hu.push_back(TcUnit{pi, (int)r, t0 * TC_BN, t1 * TC_BN, slot + t0 * TC_BN, sp, 0});
+            }
             slot += M;
         }
     }
@@ -810,7 +851,9 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     TcParams prm;
     prm.a_off = a_off_d; prm.b_off = b_off_d;
     prm.units = w.units; prm.n_units = (int)hu.size(); prm.kblocks = D / TC_BK;
-    prm.cand = w.cand; prm.col_slots = w.slots;
+    prm.cand = w.cand; prm.n_split = w.n_split; prm.col_slots = w.slots;
+    if (w.n_split > 1)  // ranges past a short pair's columns stay invalid (c1 = -1)
+        EC3R_CUDA_TRY(cudaMemsetAsync(w.cand, 0xFF, sizeof(RowCand) * (size_t)ta * w.n_split, st));
     if (prm.n_units > 0) {
         const size_t smem = tc_smem_bytes(prm.kblocks);
         EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -820,8 +863,8 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
         tk.stop();
     }
-    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, eps_tc,
-                                                                 ratio * ratio, rs, flag_rows, counters);
+    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split,
+                                                                 eps_tc, ratio * ratio, rs, flag_rows, counters);
     EC3R_CHECK_LAUNCH("mt_decide_rows");
     *tc_used = 1;
     return EC3R_OK;
@@ -835,7 +878,7 @@ int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
     const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     EC3R_CUDA_TRY(cudaMemsetAsync(col_best, 0xFF, sizeof(int32_t) * (size_t)tb, st));
-    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.slots, w.pair_slot,
+    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split, w.slots, w.pair_slot,
                                                                eps_tc, ratio * ratio, rs, col_best, flag_cols,
                                                                counters);
     EC3R_CHECK_LAUNCH("mt_need_cols");
