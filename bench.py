@@ -261,6 +261,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: validation of the N>1 path with ranks sharing a GPU (not a measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -274,9 +276,14 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # --dist-backend gloo (validation only): several ranks may share a GPU
+    dev_index = local % max(torch.cuda.device_count(), 1) if args.dist_backend == "gloo" else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2510_02080_b200 import _lib
 
     L = _lib.lib()
@@ -312,7 +319,7 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], device="cuda")
+    ms_t = torch.tensor([ms], device="cuda" if args.dist_backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -432,7 +439,7 @@ def run_e2e(step, dm, desc, args, world):
             b.copy_(h_in[4], non_blocking=True)
             ready[i % 2].record(cs)
 
-    U0 = int(step.out[0].shape[0])
+    U0 = int(max(step.out[0].shape[0], step.n_voxels) * 1.25) + 1  # N > 1: the owned partition may be larger
     h_out = [torch.empty((U0,) + tuple(x.shape[1:]), dtype=x.dtype).pin_memory() for x in step.out]
     h_match = torch.empty(int(ao[-1]), dtype=torch.int32).pin_memory()
     steps = max(2, min(args.steps, 5))

@@ -60,11 +60,20 @@ def owner_of(keys, world: int) -> np.ndarray:
     return (mix64(keys) % np.uint64(world)).astype(np.int64)
 
 
+def _host_staged(group, dev) -> bool:
+    """gloo moves CPU tensors only: CUDA payloads are staged through host
+    memory (validation runs with several ranks per GPU); NCCL moves them
+    directly over NVLink."""
+    return dev.type == "cuda" and dist.get_backend(group) == "gloo"
+
+
 def gather_ragged(t: torch.Tensor, group=None) -> list[torch.Tensor]:
     """All-gather tensors whose first dimension differs per rank."""
     rank, world = _world(group)
     if world == 1:
         return [t]
+    if _host_staged(group, t.device):
+        return [x.to(t.device) for x in gather_ragged(t.cpu(), group)]
     n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
@@ -90,6 +99,9 @@ def exchange_partials(keys: torch.Tensor, sums4: torch.Tensor, counts: torch.Ten
     if world == 1:
         return keys[: send[0]], sums4[: send[0]], counts[: send[0]]
     dev = keys.device
+    if _host_staged(group, dev):
+        k, s_, c = exchange_partials(keys.cpu(), sums4.cpu(), counts.cpu(), rank_counts, group)
+        return k.to(dev), s_.to(dev), c.to(dev)
     sc = torch.tensor(send, dtype=torch.int64, device=dev)
     rc = torch.empty_like(sc)
     dist.all_to_all_single(rc, sc, group=group)
