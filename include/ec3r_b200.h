@@ -279,6 +279,22 @@ EC3R_API int ec3r_nn_query(const double* query, int64_t n_query, const double* r
 EC3R_API int ec3r_raycast(const double* origins, const double* dirs, int64_t n, const double* solids_h,
                           int n_solids, double* out_t, void* stream);
 
+/* ---------------------------------------------------------------------
+ * K8  local loop candidates: replaces the projection count of
+ * detect_local_candidates (loops.py:114-133 -> project_points,
+ * geometry.py:87-109) for a whole window of keyframes in one launch.
+ * positions (n_points x 3 float64), world_from_cam (n_keyframes x 8 float64
+ * {s, q, t}), intrinsics_h (HOST, 6 doubles {fx, fy, cx, cy, width,
+ * height}).  out_counts (n_keyframes int64, optional): points projecting
+ * inside the image in front of the camera; out_cand (n_keyframes int32):
+ * count / n_points > tau_p.
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_local_candidates_workspace(int n_keyframes);
+EC3R_API int ec3r_local_candidates(const double* positions, int64_t n_points, const double* world_from_cam,
+                                   int n_keyframes, const double* intrinsics_h, double tau_p,
+                                   int64_t* out_counts, int32_t* out_cand, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,8 @@ _PROTOS = {
     "ec3r_nn_workspace": (_SZ, [_I64, _I64]),
     "ec3r_nn_query": (_I, [_P, _I64, _P, _I64, _D, _P, _P, _P, _SZ, _P]),
     "ec3r_raycast": (_I, [_P, _P, _I64, _P, _I, _P, _P]),
+    "ec3r_local_candidates_workspace": (_SZ, [_I]),
+    "ec3r_local_candidates": (_I, [_P, _I64, _P, _I, _P, _D, _P, _P, _P, _SZ, _P]),
 }
 
 EXPORTED = tuple(_PROTOS)

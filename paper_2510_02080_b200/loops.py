@@ -168,3 +168,42 @@ class RetrievalDB:
         _populate(matrix, kfs, cp, cs)
         _populate(matrix, kfs, ep, es)
         return admit(matrix, kfs, qp, qs)
+
+
+# ---------------------------------------------------------------------------
+# Local loop candidates (loops.py:114-133; K8, csrc/local_cand.cu)
+
+def local_candidates_device(positions: torch.Tensor, world_from_cam: torch.Tensor, intrinsics, tau_p: float,
+                            stream=None):
+    """Projection counts of the map points (N, 3) float64 into K keyframes
+    (world_from_cam: (K, 8) float64 {s, q, t}) in one launch.  Returns
+    (counts (K,) int64, candidate (K,) int32) CUDA tensors; intrinsics =
+    (fx, fy, cx, cy, width, height)."""
+    L = _lib.lib()
+    pts = positions.reshape(-1, 3).to(torch.float64).contiguous()
+    poses = world_from_cam.reshape(-1, 8).to(torch.float64).contiguous()
+    K = int(poses.shape[0])
+    counts = torch.empty(max(K, 1), dtype=torch.int64, device=poses.device)
+    cand = torch.empty(max(K, 1), dtype=torch.int32, device=poses.device)
+    intr = np.ascontiguousarray(np.asarray(intrinsics, dtype=np.float64).reshape(6))
+    ws = _lib.workspace(L.ec3r_local_candidates_workspace(K), poses.device, "local_cand")
+    _lib.check(L.ec3r_local_candidates(_lib.ptr(pts) if pts.shape[0] else None, int(pts.shape[0]), _lib.ptr(poses),
+                                       K, intr.ctypes.data, float(tau_p), _lib.ptr(counts), _lib.ptr(cand),
+                                       _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)), "ec3r_local_candidates")
+    return counts[:K], cand[:K]
+
+
+def detect_local_candidates(sparse_map, window, k, cfg) -> list:
+    """loops.py:114-133 — keyframes of `window` ((kf_id, world_from_cam)
+    pairs) that see more than cfg.tau_p of the live map's points."""
+    from .types import sim3_to_vec
+
+    _lib.lib()
+    positions = sparse_map.positions()
+    if len(positions) == 0 or len(window) == 0:
+        return []
+    pts = torch.as_tensor(np.ascontiguousarray(np.asarray(positions, dtype=np.float64)), device="cuda")
+    poses = torch.as_tensor(np.stack([sim3_to_vec(p) for _, p in window]), device="cuda")
+    _, cand = local_candidates_device(pts, poses, (k.fx, k.fy, k.cx, k.cy, k.width, k.height), cfg.tau_p)
+    c = cand.cpu().numpy()
+    return [kf for (kf, _), ok in zip(window, c) if ok]

@@ -367,9 +367,71 @@ def gen_kernels():
     np.savez_compressed(os.path.join(OUT, "kernels.npz"), **out)
 
 
+# ---------------------------------------------------------------------------
+# 6. Local loop candidates (loops.py:114-133 with project_points,
+#    geometry.py:87-109): visible counts and decisions on the reference's own
+#    test scenes (pkg/tests/test_loops.py:115-157) and a random window.
+
+def gen_local():
+    from submap_slam.backend import GroundTruthBackend
+    from submap_slam.geometry import project_points
+    from submap_slam.loops import LoopConfig, detect_local_candidates
+    from submap_slam.tracking import LocalSparseMap, SparseMapPoint
+
+    out = {}
+    cases = []
+    for seed, frames, stride, extra in ((1, 25, 12, dict(step_bound=0.6)), (2, 60, 3, {})):
+        world = generate_world(WorldConfig(room_size=(8.0, 8.0, 4.0), landmark_count=500), seed)
+        spec = TrajectorySpec(kind="circle", frame_count=frames, radius=2.0, look_at="forward", **extra)
+        traj = generate_trajectory(spec, world)
+        be = GroundTruthBackend(world, traj)
+        obs0 = be.extract_features(0)
+        m = LocalSparseMap()
+        lids = obs0.landmark_ids[obs0.landmark_ids >= 0]
+        m.insert_batch([SparseMapPoint(i, world.landmarks[l].copy(), world.tags[l].copy(), 1.0, 0)
+                        for i, l in enumerate(lids)])
+        window = [(i, traj[i]) for i in range(0, frames, stride)]
+        cases.append((m.positions(), window, be.intrinsics))
+    # random map points, random window poses around the origin
+    rng = np.random.default_rng(606)
+    pts = rng.uniform([-1.5, -1.5, 1.0], [1.5, 1.5, 5.0], (3000, 3))
+    from submap_slam.liegroups import Pose3, Rotation3
+
+    window = []
+    for i in range(12):
+        q = rng.normal(size=4)
+        q[0] = abs(q[0]) + 3.0  # mostly looking down +z, where the points are
+        window.append((100 + i, Pose3(Rotation3(q / np.linalg.norm(q)), rng.uniform(-0.5, 0.5, 3))))
+    cases.append((pts, window, cases[0][2]))
+    cfg = LoopConfig()
+    for i, (pos, window, k) in enumerate(cases):
+        counts = [int(project_points(p.inverse(), k, pos)[2].sum()) for _, p in window]
+        cand = detect_local_candidates(_SM(pos), window, k, cfg)
+        out[f"c{i}_pos"] = pos
+        out[f"c{i}_kf"] = np.array([kf for kf, _ in window], np.int64)
+        out[f"c{i}_poses"] = np.stack([np.concatenate([[1.0], p.rotation.q, p.translation]) for _, p in window])
+        out[f"c{i}_intr"] = np.array([k.fx, k.fy, k.cx, k.cy, k.width, k.height], float)
+        out[f"c{i}_counts"] = np.array(counts, np.int64)
+        out[f"c{i}_cand"] = np.array(cand, np.int64)
+    out["n_cases"] = np.int64(len(cases))
+    out["tau_p"] = np.float64(cfg.tau_p)
+    np.savez_compressed(os.path.join(OUT, "local.npz"), **out)
+
+
+class _SM:
+    """The sparse map surface detect_local_candidates uses (positions())."""
+
+    def __init__(self, pos):
+        self._pos = pos
+
+    def positions(self):
+        return self._pos
+
+
 if __name__ == "__main__":
     gen_registration()
     gen_mapping()
     gen_match()
     gen_retrieval()
     gen_kernels()
+    gen_local()

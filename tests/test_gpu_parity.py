@@ -642,3 +642,33 @@ def test_match_sweep_32k_vs_oracle():
     assert int(nm[0]) == int((mb >= 0).sum())
     st = tracking.last_match_stats()
     assert st["rows_rescanned"] < 0.01 * n and st["cols_rescanned"] < 0.01 * n, st
+
+
+# --------------------------------------------------------------------------
+# K8 local loop candidates (projection counts, decisions)
+
+def test_local_candidates_golden_and_batch(golden):
+    from oracle import local as ol
+    from paper_2510_02080_b200 import loops
+    g = golden("local")
+    tau = float(g["tau_p"])
+    for i in range(int(g["n_cases"])):
+        pos = torch.as_tensor(g[f"c{i}_pos"], device="cuda")
+        poses = torch.as_tensor(g[f"c{i}_poses"], device="cuda")
+        counts, cand = loops.local_candidates_device(pos, poses, g[f"c{i}_intr"], tau)
+        np.testing.assert_array_equal(counts.cpu().numpy(), g[f"c{i}_counts"], err_msg=f"case {i}")
+        kf = g[f"c{i}_kf"]
+        assert kf[cand.cpu().numpy() == 1].tolist() == g[f"c{i}_cand"].tolist()
+    # a large map against a 64-keyframe window, against the oracle
+    rng = np.random.default_rng(9)
+    pts = rng.uniform([-2, -2, 0.5], [2, 2, 6], (200000, 3))
+    q = rng.normal(size=(64, 4))
+    q[:, 0] = np.abs(q[:, 0]) + 2.5
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    poses8 = np.concatenate([np.ones((64, 1)), q, rng.uniform(-0.5, 0.5, (64, 3))], axis=1)
+    intr = np.array([400.0, 400.0, 259.0, 196.0, 518.0, 392.0])
+    counts, cand = loops.local_candidates_device(torch.as_tensor(pts, device="cuda"),
+                                                 torch.as_tensor(poses8, device="cuda"), intr, 0.3)
+    exp = ol.visible_counts(pts, poses8, intr)
+    np.testing.assert_array_equal(counts.cpu().numpy(), exp)
+    np.testing.assert_array_equal(cand.cpu().numpy(), (exp / len(pts) > 0.3).astype(np.int32))

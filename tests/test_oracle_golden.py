@@ -137,3 +137,13 @@ def test_kernels_raycast_case(golden):
     boxes = [(b[0], b[1]) for b in g["rc_boxes"]]
     t = ok.raycast(g["rc_origins"], g["rc_dirs"], g["rc_room_min"], g["rc_room_max"], boxes)
     np.testing.assert_array_equal(t, g["rc_t"])
+
+
+def test_local_candidates_cases(golden):
+    from oracle import local as ol
+    g = golden("local")
+    for i in range(int(g["n_cases"])):
+        np.testing.assert_array_equal(ol.visible_counts(g[f"c{i}_pos"], g[f"c{i}_poses"], g[f"c{i}_intr"]),
+                                      g[f"c{i}_counts"], err_msg=f"case {i}")
+        assert ol.local_candidates(g[f"c{i}_pos"], g[f"c{i}_kf"], g[f"c{i}_poses"], g[f"c{i}_intr"],
+                                   float(g["tau_p"])) == g[f"c{i}_cand"].tolist()
