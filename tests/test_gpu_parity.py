@@ -672,3 +672,57 @@ def test_local_candidates_golden_and_batch(golden):
     exp = ol.visible_counts(pts, poses8, intr)
     np.testing.assert_array_equal(counts.cpu().numpy(), exp)
     np.testing.assert_array_equal(cand.cpu().numpy(), (exp / len(pts) > 0.3).astype(np.int32))
+
+
+# --------------------------------------------------------------------------
+# pool registration: gate / error statuses against the oracle
+
+def test_registration_edges_status_paths(golden):
+    """Edges whose shared frame is empty (no pairs), has < 10 valid pairs,
+    carries zero confidence everywhere (AllZeroConfidence) or only collinear
+    points (DegenerateConfiguration): statuses and counts as the reference."""
+    from paper_2510_02080_b200 import _lib, mapping
+    g = golden("mapping")
+    gs, _ = mapping_submaps(g)
+    a, b = gs[1], gs[0]
+    sh = [i for i, kf in enumerate(a["frame_ids"]) if kf in list(b["frame_ids"])][0]
+    fb = list(b["frame_ids"]).index(a["frame_ids"][sh])
+    H, W = a["depth"].shape[1:]
+
+    def variant(kind):
+        da, ca, db, cb = (x.copy() for x in (a["depth"], a["conf"], b["depth"], b["conf"]))
+        if kind == "empty":
+            db[fb] = 0.0
+            cb[fb] = 0.0
+        elif kind == "few":
+            keep = np.zeros((H, W), bool)
+            keep[H // 2, W // 4:W // 4 + 5] = True
+            da[sh][~keep] = 0.0
+            ca[sh][~keep] = 0.0
+        elif kind == "zero_conf":
+            ca[sh] = 0.0
+            cb[fb] = 0.0
+        elif kind == "collinear":
+            row = np.zeros((H, W), bool)
+            row[H // 2, 2:W - 2] = True
+            da[sh] = np.where(row, 2.0, 0.0)
+            ca[sh] = np.where(row, 0.9, 0.0)
+            db[fb] = np.where(row, 2.5, 0.0)
+            cb[fb] = np.where(row, 0.8, 0.0)
+        return dict(a, depth=da, conf=ca), dict(b, depth=db, conf=cb)
+
+    names = {0: ref.STATUS_OK, _lib.ST_SKIP: ref.STATUS_SKIP, _lib.ST_TOO_FEW: ref.STATUS_TOO_FEW,
+             _lib.ST_ALL_ZERO: ref.STATUS_ALL_ZERO, _lib.ST_DEGENERATE: ref.STATUS_DEGENERATE}
+    for kind, expect in (("empty", ref.STATUS_SKIP), ("few", ref.STATUS_SKIP), ("zero_conf", ref.STATUS_ALL_ZERO),
+                         ("collinear", ref.STATUS_DEGENERATE)):
+        sa, sb = variant(kind)
+        e = ref.registration_edge(sa, sb)
+        assert e["status"] == expect, (kind, e["status"])
+        dm = mapping.DenseMapping(H, W, a["K"])
+        subs = []
+        for s in (sb, sa):
+            poses8 = np.concatenate([np.ones((len(s["frame_ids"]), 1)), s["pose_q"], s["pose_t"]], axis=1)
+            subs.append(dm.add_submap(s["frame_ids"], s["depth"], s["conf"], list(poses8)))
+        (r,), _ = mapping.register_edges(dm.pool, [(subs[1], subs[0])], with_keep_masks=True)
+        assert names[r.status] == expect, (kind, r.status)
+        assert r.count == e["count"], (kind, r.count, e["count"])
