@@ -52,6 +52,7 @@ struct ec3r_vhash {
     double cell;
     ec3r::BlockEntry* table;
     unsigned long long* block_keys;  // max_blocks
+    uint32_t* block_slot;            // max_blocks: table position of each allocated block
     float4* sums;                    // max_blocks * 64
     unsigned int* counts;            // max_blocks * 64
     unsigned long long* counters;    // [n_in, n_oor, n_overflow, n_slow, blocks_used, ...]
@@ -65,6 +66,7 @@ struct VB {
     BlockEntry* table;
     unsigned long long tmask;
     unsigned long long* block_keys;
+    uint32_t* block_slot;
     float4* sums;
     unsigned int* counts;
     unsigned long long* counters;
@@ -72,7 +74,7 @@ struct VB {
 };
 
 static VB vb_of(const ec3r_vhash* h) {
-    return VB{h->table, h->tmask, h->block_keys, h->sums, h->counts, h->counters, h->max_blocks};
+    return VB{h->table, h->tmask, h->block_keys, h->block_slot, h->sums, h->counts, h->counters, h->max_blocks};
 }
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
@@ -160,6 +162,7 @@ __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk
                 if ((int64_t)slot < v.max_blocks) {
                     got = (int)slot;
                     v.block_keys[slot] = bk;  // read by later kernels only: no fence needed
+                    v.block_slot[slot] = (uint32_t)h;
                 }
                 atomicExch(&e->idx, got);
                 return got;
@@ -222,11 +225,21 @@ __global__ void vb_clear_table_kernel(BlockEntry* __restrict__ t, int64_t n) {
     }
 }
 
-// zero the pool blocks used by the previous fill (count read on the device)
-__global__ void vb_clear_pool_kernel(float4* __restrict__ sums, unsigned int* __restrict__ counts,
+__global__ void vb_clear_used_kernel(BlockEntry* __restrict__ table, int64_t tcap, const uint32_t* __restrict__ block_slot,
+                                     float4* __restrict__ sums, unsigned int* __restrict__ counts,
                                      const unsigned long long* __restrict__ counters, int64_t max_blocks) {
-    const int64_t used = min((int64_t)counters[4], max_blocks) * kBlockVox;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long used_raw = counters[4];
+    const bool full = (int64_t)used_raw > max_blocks;
+    const int64_t used = full ? max_blocks : (int64_t)used_raw;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    BlockEntry empty;
+    empty.key = kEmpty;
+    empty.idx = -1;
+    empty.pad = 0;
+    const int64_t n_tab = full ? tcap : used;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_tab; i += stride)
+        table[full ? i : (int64_t)block_slot[i]] = empty;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used * kBlockVox; i += stride) {
         sums[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         counts[i] = 0u;
     }
@@ -879,12 +892,13 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     const size_t nv = (size_t)h->max_blocks * kBlockVox;
     bool ok = cudaMalloc(&h->table, sizeof(BlockEntry) * (size_t)tcap) == cudaSuccess &&
               cudaMalloc(&h->block_keys, sizeof(unsigned long long) * (size_t)h->max_blocks) == cudaSuccess &&
+              cudaMalloc(&h->block_slot, sizeof(uint32_t) * (size_t)h->max_blocks) == cudaSuccess &&
               cudaMalloc(&h->sums, sizeof(float4) * nv) == cudaSuccess &&
               cudaMalloc(&h->counts, sizeof(unsigned int) * nv) == cudaSuccess &&
               cudaMalloc(&h->counters, sizeof(unsigned long long) * 8) == cudaSuccess;
     if (!ok) {
         set_last_error("cudaMalloc(vhash)", cudaGetLastError());
-        cudaFree(h->table); cudaFree(h->block_keys); cudaFree(h->sums); cudaFree(h->counts); cudaFree(h->counters);
+        cudaFree(h->table); cudaFree(h->block_keys); cudaFree(h->block_slot); cudaFree(h->sums); cudaFree(h->counts); cudaFree(h->counters);
         delete h;
         return EC3R_ENOMEM;
     }
@@ -892,8 +906,11 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     EC3R_CUDA_TRY(cudaMemsetAsync(h->sums, 0, sizeof(float4) * nv, st));
     EC3R_CUDA_TRY(cudaMemsetAsync(h->counts, 0, sizeof(unsigned int) * nv, st));
     EC3R_CUDA_TRY(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, st));
+    // the whole table starts empty (later clears touch only the used entries)
+    vb_clear_table_kernel<<<(unsigned)((tcap + 255) / 256), 256, 0, st>>>(h->table, tcap);
+    EC3R_CHECK_LAUNCH("vb_clear_table_kernel");
     *out = h;
-    return ec3r_vhash_clear(h, stream);
+    return EC3R_OK;
 }
 
 // capacity = voxels to emit at most; the pool holds capacity / 4 blocks
@@ -908,6 +925,7 @@ extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {
     if (!h) return EC3R_OK;
     cudaFree(h->table);
     cudaFree(h->block_keys);
+    cudaFree(h->block_slot);
     cudaFree(h->sums);
     cudaFree(h->counts);
     cudaFree(h->counters);
@@ -922,10 +940,11 @@ extern "C" int ec3r_vhash_clear(ec3r_vhash* h, void* stream) {
     if (!h) return EC3R_EARG;
     cudaStream_t st = as_stream(stream);
     const int64_t tcap = (int64_t)h->tmask + 1;
-    vb_clear_table_kernel<<<(unsigned)((tcap + 255) / 256), 256, 0, st>>>(h->table, tcap);
-    EC3R_CHECK_LAUNCH("vb_clear_table_kernel");
-    vb_clear_pool_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->sums, h->counts, h->counters, h->max_blocks);
-    EC3R_CHECK_LAUNCH("vb_clear_pool_kernel");
+    // only the entries and pool blocks the last fill used (the whole table
+    // when that fill overflowed the pool and left unallocated entries)
+    vb_clear_used_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->table, tcap, h->block_slot, h->sums, h->counts, h->counters,
+                                                      h->max_blocks);
+    EC3R_CHECK_LAUNCH("vb_clear_used_kernel");
     EC3R_CUDA_TRY(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, st));
     return EC3R_OK;
 }
