@@ -678,6 +678,82 @@ __global__ void mt_flag_all_kernel(int32_t* __restrict__ list, int64_t n) {
     if (i < n) list[i] = (int32_t)i;
 }
 
+// Work units from the device row offsets.  mt_unit_scan (one CTA): per pair
+// the unit and column-slot counts, exclusive-scanned in chunks of the CTA's
+// threads; mt_units_kernel (one thread per unit): the unit's pair by binary
+// search, then its (row block, column range).  A pair with `tiles` column
+// tiles has min(tiles, n_split) ranges per row block; range j covers tiles
+// [tiles * j / ns, tiles * (j + 1) / ns) (the host's count in match_tc_run).
+__global__ void __launch_bounds__(1024) mt_unit_scan(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off,
+                                                    int n_pairs, int n_split, long long* __restrict__ unit_base,
+                                                    long long* __restrict__ pair_slot) {
+    __shared__ long long s_u[1024], s_s[1024];
+    __shared__ long long base_u, base_s;
+    if (threadIdx.x == 0) { base_u = 0; base_s = 0; }
+    __syncthreads();
+    for (int p0 = 0; p0 < n_pairs; p0 += 1024) {
+        const int p = p0 + threadIdx.x;
+        long long nu = 0, ns = 0;
+        if (p < n_pairs) {
+            const int64_t M = b_off[p + 1] - b_off[p], N = a_off[p + 1] - a_off[p];
+            if (M > 0) {
+                const long long tiles = (M + TC_BN - 1) / TC_BN;
+                const long long rb = (N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM);
+                nu = rb * (tiles < n_split ? tiles : n_split);
+                ns = rb * M;
+            }
+        }
+        s_u[threadIdx.x] = nu;
+        s_s[threadIdx.x] = ns;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan
+            const long long au = threadIdx.x >= o ? s_u[threadIdx.x - o] : 0;
+            const long long as = threadIdx.x >= o ? s_s[threadIdx.x - o] : 0;
+            __syncthreads();
+            s_u[threadIdx.x] += au;
+            s_s[threadIdx.x] += as;
+            __syncthreads();
+        }
+        if (p < n_pairs) {
+            unit_base[p] = base_u + s_u[threadIdx.x] - nu;
+            pair_slot[p] = base_s + s_s[threadIdx.x] - ns;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            base_u += s_u[1023];
+            base_s += s_s[1023];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        unit_base[n_pairs] = base_u;
+        pair_slot[n_pairs] = base_s;
+    }
+}
+
+__global__ void mt_units_kernel(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
+                                int n_split, const long long* __restrict__ unit_base,
+                                const long long* __restrict__ pair_slot, int64_t n_units, TcUnit* __restrict__ units) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n_units) return;
+    int lo = 0, hi = n_pairs;  // unit_base[lo] <= u < unit_base[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (unit_base[mid] <= u) lo = mid; else hi = mid;
+    }
+    while (lo + 1 < n_pairs && unit_base[lo + 1] <= u) ++lo;  // skip pairs without units
+    const int p = lo;
+    const int64_t M = b_off[p + 1] - b_off[p];
+    const int tiles = (int)((M + TC_BN - 1) / TC_BN);
+    const int ns = tiles < n_split ? tiles : n_split;
+    const long long local = u - unit_base[p];
+    const long long b = local / ns;
+    const int j = (int)(local - b * ns);
+    const int t0 = (int)((int64_t)tiles * j / ns), t1 = (int)((int64_t)tiles * (j + 1) / ns);
+    units[u] = TcUnit{p, (int)(a_off[p] + b * TC_NA * TC_BM), t0 * TC_BN, t1 * TC_BN,
+                      pair_slot[p] + b * M + t0 * TC_BN, j, 0};
+}
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -748,7 +824,8 @@ size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_
     const int sp = choose_split(a_off_h, b_off_h, n_pairs);
     return align256(sizeof(RowCand) * (size_t)ta * sp) +
            align256(sizeof(unsigned long long) * (size_t)n_col_slots(a_off_h, b_off_h, n_pairs)) +
-           align256(sizeof(long long) * (size_t)(n_pairs + 1)) + align256(sizeof(TcUnit) * (size_t)max_units(ta, n_pairs, sp)) +
+           2 * align256(sizeof(long long) * (size_t)(n_pairs + 1)) +
+           align256(sizeof(TcUnit) * (size_t)max_units(ta, n_pairs, sp)) +
            align256(64);
 }
 
@@ -757,6 +834,7 @@ struct TcWs {
     int n_split;
     unsigned long long* slots;
     long long* pair_slot;
+    long long* unit_base;
     TcUnit* units;
     unsigned int* nb;
     size_t used;
@@ -770,6 +848,7 @@ static TcWs carve_tc(void* tc_ws, const int64_t* a_off_h, const int64_t* b_off_h
     w.cand = cv.take<RowCand>(ta * w.n_split);
     w.slots = cv.take<unsigned long long>(n_col_slots(a_off_h, b_off_h, n_pairs));
     w.pair_slot = cv.take<long long>(n_pairs + 1);
+    w.unit_base = cv.take<long long>(n_pairs + 1);
     w.units = cv.take<TcUnit>(max_units(ta, n_pairs, w.n_split));
     w.nb = cv.take<unsigned int>(16);
     w.used = cv.used;
@@ -801,27 +880,23 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     if (w.used > tc_ws_bytes) return EC3R_EWORKSPACE;
     // units and column-slot bases; units + pair bases travel in one copy
-    std::vector<TcUnit> hu;
-    std::vector<long long> hp(n_pairs + 1);
-    hu.reserve(max_units(ta, n_pairs, w.n_split));
-    long long slot = 0;
+    // unit count on the host (grid size); the units themselves and the
+    // pairs' column-slot bases are written on the device from the offsets
+    int64_t n_units = 0;
     for (int pi = 0; pi < n_pairs; ++pi) {
-        hp[pi] = slot;
-        const int64_t M = b_off_h[pi + 1] - b_off_h[pi];
-        if (M == 0) continue;  // no columns: nothing to score
-        const int tiles = (int)((M + TC_BN - 1) / TC_BN);
-        for (int64_t r = a_off_h[pi]; r < a_off_h[pi + 1]; r += TC_NA * TC_BM) {
-            for (int sp = 0; sp < w.n_split; ++sp) {
-                const int t0 = (int)((int64_t)tiles * sp / w.n_split), t1 = (int)((int64_t)tiles * (sp + 1) / w.n_split);
-                if (t1 > t0) hu.push_back(TcUnit{pi, (int)r, t0 * TC_BN, t1 * TC_BN, slot + t0 * TC_BN, sp, 0});
-            }
-            slot += M;
-        }
+        const int64_t M = b_off_h[pi + 1] - b_off_h[pi], N = a_off_h[pi + 1] - a_off_h[pi];
+        if (M == 0) continue;
+        const int64_t tiles = (M + TC_BN - 1) / TC_BN;
+        n_units += (N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM) * std::min<int64_t>(tiles, w.n_split);
     }
-    hp[n_pairs] = slot;
-    EC3R_CUDA_TRY(cudaMemcpyAsync(w.pair_slot, hp.data(), sizeof(long long) * hp.size(), cudaMemcpyHostToDevice, st));
-    if (!hu.empty())
-        EC3R_CUDA_TRY(cudaMemcpyAsync(w.units, hu.data(), sizeof(TcUnit) * hu.size(), cudaMemcpyHostToDevice, st));
+    mt_unit_scan<<<1, 1024, 0, st>>>(a_off_d, b_off_d, n_pairs, w.n_split, w.unit_base, w.pair_slot);
+    EC3R_CHECK_LAUNCH("mt_unit_scan");
+    if (n_units > 0) {
+        mt_units_kernel<<<(unsigned)((n_units + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, w.n_split,
+                                                                           w.unit_base, w.pair_slot, n_units,
+                                                                           w.units);
+        EC3R_CHECK_LAUNCH("mt_units_kernel");
+    }
     if (!(norm_bound > 0)) {
         // max squared row norms of A and B (float32, rounded up below)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.nb, 0, 8, st));
@@ -850,7 +925,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     }
     TcParams prm;
     prm.a_off = a_off_d; prm.b_off = b_off_d;
-    prm.units = w.units; prm.n_units = (int)hu.size(); prm.kblocks = D / TC_BK;
+    prm.units = w.units; prm.n_units = (int)n_units; prm.kblocks = D / TC_BK;
     prm.cand = w.cand; prm.n_split = w.n_split; prm.col_slots = w.slots;
     if (w.n_split > 1)  // ranges past a short pair's columns stay invalid (c1 = -1)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.cand, 0xFF, sizeof(RowCand) * (size_t)ta * w.n_split, st));
