@@ -198,6 +198,9 @@ EC3R_API int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream);
 EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum,
                        int32_t* count, int64_t* n_out, int sort, void* workspace,
                        size_t workspace_bytes, void* stream);
+/* Voxel count of the last sorted extract on this handle (already known on
+ * the host), or -1: lets a caller size its outputs without a device read. */
+EC3R_API int64_t ec3r_vhash_extract_count(const ec3r_vhash* h);
 /* Multi-GPU: emit raw partial sums (key, sum w*dx, sum w, count) bucketed
  * by owner rank = hash(key) mod n_ranks for the all-to-all (outputs hold
  * U rows; workspace = ec3r_vhash_extract_workspace + 1 KB), and merge

@@ -47,6 +47,7 @@ _PROTOS = {
     "ec3r_vhash_count": (_I, [_P, _P, _P]),
     "ec3r_vhash_extract_workspace": (_SZ, [_P]),
     "ec3r_vhash_extract": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P]),
+    "ec3r_vhash_extract_count": (_I64, [_P]),
     "ec3r_vhash_extract_partials": (_I, [_P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
     "ec3r_vhash_merge_partials": (_I, [_P, _P, _P, _P, _I64, _P]),
     "ec3r_match_workspace": (_SZ, [_P, _P, _I]),

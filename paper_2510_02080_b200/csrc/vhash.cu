@@ -58,6 +58,7 @@ struct ec3r_vhash {
     unsigned long long* counters;    // [n_in, n_oor, n_overflow, n_slow, blocks_used, ...]
     float4* ftab;                    // per-frame affine tables of the last insert_frames
     int64_t ftab_cap;                // float4 entries
+    int64_t last_count;              // voxels of the last sorted extract (host-known), -1 if unknown
 };
 
 namespace ec3r {
@@ -797,6 +798,7 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
                           cudaStream_t st) {
     const size_t cap = (size_t)h->max_voxels;
     const int64_t nb = h->max_blocks;
+    h->last_count = -1;
     Carver cv{(char*)workspace, 0};
     unsigned long long* k0 = cv.take<unsigned long long>(cap);
     int64_t* i0 = cv.take<int64_t>(cap);
@@ -835,6 +837,7 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
     EC3R_CUDA_TRY(cudaMemcpyAsync(hst + 1, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, st));
     EC3R_CUDA_TRY(cudaStreamSynchronize(st));
     const int64_t nh = std::min<int64_t>(hst[0], h->max_voxels);
+    h->last_count = nh;
     const int* bb = hst + 1;
     if (nh <= 0) {
         vb_block_emit_kernel<<<1, 32, 0, st>>>(h->counts, h->block_keys, h->counters, 0, blk_off + nb, h->max_voxels,
@@ -881,6 +884,7 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
                                        void* stream) {
     if (!out || max_voxels < 2 || max_blocks < 1 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
+    h->last_count = -1;
     h->max_voxels = max_voxels > 65536 ? max_voxels : 65536;
     h->max_blocks = max_blocks > 4096 ? max_blocks : 4096;
     // frame fusion addresses voxels as 32-bit (block << 6 | local) ids
@@ -1069,6 +1073,11 @@ extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid,
     EC3R_CHECK_LAUNCH("vb_gather_kernel");
     return EC3R_OK;
 }
+
+// Voxel count of the last sorted ec3r_vhash_extract on this handle (the
+// library read it on the host to size the sort), or -1.  Saves the caller a
+// device round trip.
+extern "C" int64_t ec3r_vhash_extract_count(const ec3r_vhash* h) { return h ? h->last_count : -1; }
 
 extern "C" int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* keys, float* sums4, int32_t* count,
                                            int64_t* rank_counts, void* workspace, size_t workspace_bytes,

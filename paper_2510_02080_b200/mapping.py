@@ -268,7 +268,9 @@ class VoxelMap:
         _lib.check(L.ec3r_vhash_extract(self._h, _lib.ptr(keys), _lib.ptr(cen), _lib.ptr(ws_), _lib.ptr(cnt),
                                         _lib.ptr(self._n), int(bool(sort)), _lib.ptr(ws), ws.numel(),
                                         _lib.stream_ptr(stream)), "ec3r_vhash_extract")
-        U = int(self._n.item())
+        U = int(L.ec3r_vhash_extract_count(self._h)) if sort else -1
+        if U < 0:
+            U = int(self._n.item())
         return keys[:U], cen[:U], ws_[:U], cnt[:U]
 
 
