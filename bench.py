@@ -170,8 +170,9 @@ class Step:
             # size the block pool once from a first fusion (outside the timed region)
             self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell)
             U = int(out[0].numel())
-            # (a pool / table sized to 2x the blocks used measured 10% slower
-            # insertion: the sparse default table spreads insert contention)
+            # re-size: pool for 2x the blocks this fill used, sparse table
+            self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell, expected_voxels=U,
+                                                          expected_blocks=stt["n_blocks"])
             self.out = tuple(torch.empty((U,) + tuple(x.shape[1:]), dtype=x.dtype, device="cuda") for x in out)
         self.vmap.clear()
         self.vmap.insert_frames(self.dm.pool, self.slots)

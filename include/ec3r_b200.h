@@ -169,10 +169,13 @@ typedef struct {
 } ec3r_vhash_stats;
 
 EC3R_API int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream);
-/* As ec3r_vhash_create with the pool's block count chosen explicitly (a map
- * refused with overflow can be re-created from its stats: n_blocks, voxels). */
+/* As ec3r_vhash_create with the pool's block count and the block table's
+ * entry count chosen explicitly (table_entries 0: 2x the pool, rounded up to
+ * a power of two).  A map sized from a previous fill's stats (n_blocks,
+ * voxels) with a sparse table keeps the per-fill clear and emit small while
+ * inserting as fast as an oversized map. */
 EC3R_API int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks,
-                                     double cell_size, void* stream);
+                                     int64_t table_entries, double cell_size, void* stream);
 EC3R_API int ec3r_vhash_destroy(ec3r_vhash* h);
 EC3R_API int64_t ec3r_vhash_capacity(const ec3r_vhash* h);
 EC3R_API int ec3r_vhash_clear(ec3r_vhash* h, void* stream);

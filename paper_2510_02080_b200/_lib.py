@@ -37,7 +37,7 @@ _PROTOS = {
     "ec3r_umeyama_workspace": (_SZ, [_I]),
     "ec3r_umeyama_batched": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _SZ, _P]),
     "ec3r_vhash_create": (_I, [C.POINTER(_P), _I64, _D, _P]),
-    "ec3r_vhash_create_sized": (_I, [C.POINTER(_P), _I64, _I64, _D, _P]),
+    "ec3r_vhash_create_sized": (_I, [C.POINTER(_P), _I64, _I64, _I64, _D, _P]),
     "ec3r_vhash_destroy": (_I, [_P]),
     "ec3r_vhash_capacity": (_I64, [_P]),
     "ec3r_vhash_clear": (_I, [_P, _P]),

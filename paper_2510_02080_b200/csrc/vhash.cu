@@ -880,8 +880,8 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
 
 using namespace ec3r;
 
-extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks, double cell_size,
-                                       void* stream) {
+extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks,
+                                       int64_t table_entries, double cell_size, void* stream) {
     if (!out || max_voxels < 2 || max_blocks < 1 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
     h->last_count = -1;
@@ -889,8 +889,13 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     h->max_blocks = max_blocks > 4096 ? max_blocks : 4096;
     // frame fusion addresses voxels as 32-bit (block << 6 | local) ids
     if (h->max_blocks > (1 << 26) - 2) h->max_blocks = (1 << 26) - 2;
+    // table: a power of two >= 2x the pool (or the caller's, larger, choice:
+    // a sparse table inserts faster — concurrent first touches of neighbouring
+    // blocks contend less for L2 lines)
     int64_t tcap = 1;
-    while (tcap < 2 * h->max_blocks) tcap <<= 1;
+    const int64_t want = table_entries > 2 * h->max_blocks ? table_entries : 2 * h->max_blocks;
+    while (tcap < want) tcap <<= 1;
+    if (tcap > (int64_t)1 << 32) return EC3R_EARG;
     h->tmask = (unsigned long long)(tcap - 1);
     h->cell = cell_size;
     const size_t nv = (size_t)h->max_blocks * kBlockVox;
@@ -922,7 +927,7 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
 // overflow, are reported and re-run on a larger handle)
 extern "C" int ec3r_vhash_create(ec3r_vhash** out, int64_t capacity, double cell_size, void* stream) {
     if (capacity < 2) return EC3R_EARG;
-    return ec3r_vhash_create_sized(out, capacity, capacity / 4 > 1 ? capacity / 4 : 1, cell_size, stream);
+    return ec3r_vhash_create_sized(out, capacity, capacity / 4 > 1 ? capacity / 4 : 1, 0, cell_size, stream);
 }
 
 extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {

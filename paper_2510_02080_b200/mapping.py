@@ -190,9 +190,11 @@ class ChainPlan:
 class VoxelMap:
     """Owner of one ec3r_vhash handle (K4)."""
 
-    def __init__(self, cell: float = 0.02, capacity: int = 1 << 20, stream=None, max_blocks: Optional[int] = None):
+    def __init__(self, cell: float = 0.02, capacity: int = 1 << 20, stream=None, max_blocks: Optional[int] = None,
+                 table_entries: int = 0):
         """capacity: voxels the emit can hold; max_blocks: 4x4x4 pool blocks
-        (default capacity / 4; size it from a previous fill's n_blocks)."""
+        (default capacity / 4; size it from a previous fill's n_blocks);
+        table_entries: block-table size (0: 2x the pool)."""
         L = _lib.lib()
         self.cell = float(cell)
         h = C.c_void_p()
@@ -200,8 +202,8 @@ class VoxelMap:
             _lib.check(L.ec3r_vhash_create(C.byref(h), int(capacity), self.cell, _lib.stream_ptr(stream)),
                        "ec3r_vhash_create")
         else:
-            _lib.check(L.ec3r_vhash_create_sized(C.byref(h), int(capacity), int(max_blocks), self.cell,
-                                                 _lib.stream_ptr(stream)), "ec3r_vhash_create_sized")
+            _lib.check(L.ec3r_vhash_create_sized(C.byref(h), int(capacity), int(max_blocks), int(table_entries),
+                                                 self.cell, _lib.stream_ptr(stream)), "ec3r_vhash_create_sized")
         self._h = h
         self.capacity = int(L.ec3r_vhash_capacity(h))  # voxel slots of the block pool
         self.expected = int(capacity)
@@ -279,11 +281,13 @@ def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional
     """Voxel fusion of pool slots with overflow-safe capacity growth.
     Returns (VoxelMap, (keys, centroid, wsum, count), stats).  With the
     expected voxel and block counts of a previous fill the map is sized at 2x
-    both (a small pool and table keep the per-fill clear and emit cheap)."""
+    both, with a sparse block table (64 entries per block: the insert speed
+    of an oversized map, the clear and emit cost of a small one)."""
     if vmap is None or vmap.cell != cell:
         n_px = int(slots.numel()) * pool.H * pool.W
         cap = expected_voxels * 2 if expected_voxels else max(1 << 16, n_px // 8)
-        vmap = VoxelMap(cell, cap, max_blocks=2 * expected_blocks if expected_blocks else None)
+        vmap = VoxelMap(cell, cap, max_blocks=2 * expected_blocks if expected_blocks else None,
+                        table_entries=64 * expected_blocks if expected_blocks else 0)
     while True:
         vmap.clear()
         vmap.insert_frames(pool, slots)
