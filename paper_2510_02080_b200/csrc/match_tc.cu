@@ -84,6 +84,11 @@ struct TcParams {
     RowCand* cand;
     int n_split;
     unsigned long long* col_slots;  // per unit and column: (ordered best key << 32) | ordered second key
+    // n_split == 1: the stage-1 row decision is made here (no decide kernel)
+    MatchRowState* rs;
+    int32_t* pending;
+    int64_t* counters;
+    double eps_tc, ratio2;
 };
 
 // ---------------------------------------------------------------------------
@@ -229,6 +234,39 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
                             ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// d2 = max(2 - 2 s, 0) (tracking.py:153) on interval end points
+__device__ __forceinline__ double d2c(double s) { return fmax(2.0 - 2.0 * s, 0.0); }
+
+// Bound on |key - exact similarity|: the tensor-core error eps_tc plus the
+// 2^11 ulps the code replaced (<= 2^-12 |key|).
+__device__ __forceinline__ double key_eps(double k, double eps_tc) { return eps_tc + ldexp(fabs(k), -12) + 1e-30; }
+
+// Relative slack on the ratio comparisons: covers the float64 rounding of
+// d2 and ratio^2 * d2 in the reference (tracking.py:153,167).
+constexpr double kRatioSlack = 1e-9;
+
+// Stage-1 decision of one row from its merged candidate (see mt_decide_rows).
+// Returns false when the row needs the float64 re-scan.
+__device__ __forceinline__ bool row_decision(const RowCand& c, int64_t M, double eps_tc, double ratio2,
+                                             MatchRowState& s) {
+    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
+    if (M == 0) return true;  // no columns: no match
+    if (M == 1) {             // one column: argmax certain, ratio test skipped (tracking.py:165)
+        s.best = 0;
+        s.ratio_ok = 1;
+        return true;
+    }
+    const double a1 = c.k1, a2 = c.k2;
+    const double e1 = key_eps(a1, eps_tc), e2 = key_eps(a2, eps_tc);
+    if (d2c(a1 + e1) > ratio2 * d2c(a2 - e2) * (1.0 + kRatioSlack)) return true;  // certain reject
+    if (a1 - e1 > a2 + e2 && a2 + e2 < 1.0 && d2c(a1 - e1) < ratio2 * d2c(a2 + e2) * (1.0 - kRatioSlack)) {
+        s.best = c.c1;
+        s.ratio_ok = 1;
+        return true;
+    }
+    return false;
+}
 
 // Epilogue of one 32-column chunk of the thread's two rows (r0: A block 0,
 // r1: A block 1).  Row side: the chunk's top-2 keys per row folded into the
@@ -507,6 +545,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     rc.c1 = o0.x > R0.b ? __float_as_int(o0.z) : c0;
                     rc.pad = 0;
                     p.cand[row0 * p.n_split + un.split] = rc;
+                    if (p.n_split == 1) {
+                        MatchRowState st;
+                        if (row_decision(rc, M, p.eps_tc, p.ratio2, st)) p.rs[row0] = st;
+                        else p.pending[atomicAdd((unsigned long long*)&p.counters[0], 1ull)] = (int32_t)row0;
+                    }
                 }
                 if (rv1) {
                     RowCand rc;
@@ -515,6 +558,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     rc.c1 = o1.x > R1.b ? __float_as_int(o1.z) : c1;
                     rc.pad = 0;
                     p.cand[row1 * p.n_split + un.split] = rc;
+                    if (p.n_split == 1) {
+                        MatchRowState st;
+                        if (row_decision(rc, M, p.eps_tc, p.ratio2, st)) p.rs[row1] = st;
+                        else p.pending[atomicAdd((unsigned long long*)&p.counters[0], 1ull)] = (int32_t)row1;
+                    }
                 }
             }
         }
@@ -540,16 +588,6 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
     return lo;
 }
 
-// d2 = max(2 - 2 s, 0) (tracking.py:153) on interval end points
-__device__ __forceinline__ double d2c(double s) { return fmax(2.0 - 2.0 * s, 0.0); }
-
-// Bound on |key - exact similarity|: the tensor-core error eps_tc plus the
-// 2^11 ulps the code replaced (<= 2^-12 |key|).
-__device__ __forceinline__ double key_eps(double k, double eps_tc) { return eps_tc + ldexp(fabs(k), -12) + 1e-30; }
-
-// Relative slack on the ratio comparisons: covers the float64 rounding of
-// d2 and ratio^2 * d2 in the reference (tracking.py:153,167).
-constexpr double kRatioSlack = 1e-9;
 
 // Stage 1 (one thread per row).  The exact top-2 similarities lie within the
 // key bounds of the approximate ones, so
@@ -561,14 +599,18 @@ constexpr double kRatioSlack = 1e-9;
 __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
                                int64_t total_a, RowCand* __restrict__ cand, int n_split, double eps_tc, double ratio2,
                                MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
-                               int64_t* __restrict__ counters) {
+                               int64_t* __restrict__ counters, int only_empty) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= total_a) return;
     const int p = pair_of(a_off, n_pairs, r);
     const int64_t M = b_off[p + 1] - b_off[p];
+    if (only_empty && M != 0) return;  // decided in the tensor-core epilogue
     MatchRowState s;
-    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
-    if (M == 0) { rs[r] = s; return; }  // no columns: no match
+    if (M == 0) {  // no columns: no match (no unit wrote a candidate)
+        row_decision(RowCand{}, 0, eps_tc, ratio2, s);
+        rs[r] = s;
+        return;
+    }
     // merge the row's column-range candidates (top-2 keys, best column);
     // the merged candidate goes back to split 0 for the column stage
     RowCand c = cand[r * n_split];
@@ -579,18 +621,7 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
         if (o.k1 > c.k1) { c.k1 = o.k1; c.c1 = o.c1; }
     }
     if (n_split > 1) cand[r * n_split] = c;
-    if (M == 1) {  // one column: argmax certain, ratio test skipped (tracking.py:165)
-        s.best = 0;
-        s.ratio_ok = 1;
-        rs[r] = s;
-        return;
-    }
-    const double a1 = c.k1, a2 = c.k2;
-    const double e1 = key_eps(a1, eps_tc), e2 = key_eps(a2, eps_tc);
-    if (d2c(a1 + e1) > ratio2 * d2c(a2 - e2) * (1.0 + kRatioSlack)) { rs[r] = s; return; }  // certain reject
-    if (a1 - e1 > a2 + e2 && a2 + e2 < 1.0 && d2c(a1 - e1) < ratio2 * d2c(a2 + e2) * (1.0 - kRatioSlack)) {
-        s.best = c.c1;
-        s.ratio_ok = 1;
+    if (row_decision(c, M, eps_tc, ratio2, s)) {
         rs[r] = s;
         return;
     }
@@ -927,6 +958,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     prm.a_off = a_off_d; prm.b_off = b_off_d;
     prm.units = w.units; prm.n_units = (int)n_units; prm.kblocks = D / TC_BK;
     prm.cand = w.cand; prm.n_split = w.n_split; prm.col_slots = w.slots;
+    prm.rs = rs; prm.pending = flag_rows; prm.counters = counters; prm.eps_tc = eps_tc; prm.ratio2 = ratio * ratio;
     if (w.n_split > 1)  // ranges past a short pair's columns stay invalid (c1 = -1)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.cand, 0xFF, sizeof(RowCand) * (size_t)ta * w.n_split, st));
     if (prm.n_units > 0) {
@@ -938,9 +970,17 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
         tk.stop();
     }
-    mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split,
-                                                                 eps_tc, ratio * ratio, rs, flag_rows, counters);
-    EC3R_CHECK_LAUNCH("mt_decide_rows");
+    // with one column range the epilogue already decided every row of a pair
+    // with columns; the kernel then only covers rows of column-less pairs
+    bool any_empty = false;
+    for (int pi = 0; pi < n_pairs && !any_empty; ++pi)
+        any_empty = b_off_h[pi + 1] == b_off_h[pi] && a_off_h[pi + 1] > a_off_h[pi];
+    if (w.n_split > 1 || any_empty) {
+        mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand,
+                                                                     w.n_split, eps_tc, ratio * ratio, rs, flag_rows,
+                                                                     counters, w.n_split == 1 ? 1 : 0);
+        EC3R_CHECK_LAUNCH("mt_decide_rows");
+    }
     *tc_used = 1;
     return EC3R_OK;
 }

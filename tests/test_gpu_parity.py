@@ -466,9 +466,10 @@ def test_match_tiny_pairs_vs_oracle():
     from paper_2510_02080_b200 import tracking
     rng = np.random.default_rng(11)
     pairs = []
-    for n, m in ((1, 1), (1, 2), (2, 1), (2, 2), (1, 300), (300, 1), (129, 257), (256, 128), (3, 3)):
-        a = _unit(rng, n, 256)
-        b = _unit(rng, m, 256)
+    for n, m in ((1, 1), (1, 2), (2, 1), (2, 2), (1, 300), (300, 1), (129, 257), (256, 128), (3, 3), (40, 0),
+                 (0, 40), (0, 0)):
+        a = _unit(rng, n, 256) if n else np.zeros((0, 256))
+        b = _unit(rng, m, 256) if m else np.zeros((0, 256))
         k = min(n, m)
         b[:k] = a[:k] + 0.05 * rng.normal(size=(k, 256))
         pairs.append((_bf16(a), _bf16(b)))
