@@ -191,9 +191,12 @@ __device__ __forceinline__ float fmax3f(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
     return r;
 }
+// not volatile: a pure function of the warp's values, so the compiler may
+// overlap the column reductions of a chunk (volatile asm would serialise
+// every CREDUX behind the previous column's dependent second reduction)
 __device__ __forceinline__ float warp_max_f32(float x) {
     float r;
-    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
+    asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
     return r;
 }
 
