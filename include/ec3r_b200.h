@@ -218,7 +218,7 @@ EC3R_API int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, const
  * K5  brute-force mutual-NN + Lowe-ratio descriptor matching
  * replaces match_descriptors (tracking.py:143-170) for a batch of frame
  * pairs.  A: (sum N_p, D) and B: (sum M_p, D) bf16 rows (ld = D, D % 8 == 0
- * after zero padding); a_off/b_off: n_pairs+1 int64 row offsets (device).
+ * after zero padding); a_off_h/b_off_h: n_pairs+1 int64 row offsets (HOST).
  * The approximate similarity pass runs on tcgen05 tensor cores (fp32 TMEM
  * accumulators); every decision is certified against an error bound and
  * re-scored in float64 from the exact rows (A_x/B_x, dtype exact_dtype:

@@ -3,7 +3,8 @@
 //
 // Replaces the dgemm + argmin/partition of match_descriptors
 // (tracking.py:152-166).  One persistent CTA per SM walks work units
-// (pair, 256-row super-block):
+// (pair, 256-row super-block, column range; the range is the whole pair
+// unless the batch has too few row blocks to fill the GPU):
 //   warp 0    TMA producer: the unit's two 128-row A blocks (K-major,
 //             SWIZZLE_128B, resident for the unit) and a 4-stage ring of
 //             128-column B k-blocks;
@@ -18,8 +19,8 @@
 //             ~6 ALU ops per similarity: 1 LOP3 key, per-row top-2 over
 //             pairs (FMNMX / FMNMX3), per-column top-2 of the warp's 64 rows
 //             with two CREDUX.MAX.F32 per column; the 4 lane quarters merge
-//             in shared memory and fold into global per-column state with
-//             two atomics per column.
+//             in shared memory and each column's top-2 keys go to the
+//             unit's own 8-byte slot with a plain store (no atomics).
 // The N x M similarity matrix never exists in memory.  The key values are
 // within eps_tc + 2^-12 |key| of the exact similarity, and certification
 // (mt_decide_rows / mt_need_cols) proves every decision from them or lists
