@@ -358,6 +358,20 @@ def main():
         roof[key] = {"bound": bound, "achieved": ach, "peak": pk, "unit": unit,
                      "frac": (ach / pk) if ach else None, "traffic": traffic.get(kname), "ms": kt,
                      "launches": n, "kernel": kname, ("alg_bytes" if bound == "hbm" else "alg_flops"): alg}
+    # the north star's stage-level figures: align + fuse (registration, pose
+    # chain, fusion, sorted emit) against HBM with SURVEY §8(d)'s bytes
+    # (depth-input variant: 8 B/px + 16 B per overlap pair + 24 B per voxel),
+    # and the whole matcher (tensor pass + certification) against bf16
+    af_ms = stages["reg"] + stages["chain"] + stages["insert"] + stages["emit"]
+    af_bytes = 8 * P + 16 * C + 24 * U
+    stage_roof = {
+        "align_fuse": {"bound": "hbm", "ms": af_ms, "alg_bytes": af_bytes, "unit": "GB/s",
+                       "achieved": af_bytes / (af_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                       "frac": af_bytes / (af_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+        "match": {"bound": "tensor", "ms": stages["match"], "alg_flops": flops_match, "unit": "TFLOP/s",
+                  "achieved": flops_match / (stages["match"] * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
+                  "frac": flops_match / (stages["match"] * 1e-3) / 1e12 / peaks["bf16_tflops"]},
+    }
     dominant = max(roof, key=lambda k: roof[k]["ms"])
     value = P * world / (ms * 1e-3)
 
@@ -398,6 +412,7 @@ def main():
             "roofline": dict(roof[dominant], stage=dominant, peak_source=f"{peak_src} MEASURED_PEAKS.json",
                              traffic_source="profiles/kernel_traffic.json (ncu --set full, dram bytes per launch)"),
             "rooflines": roof,
+            "stage_rooflines": stage_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
