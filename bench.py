@@ -570,6 +570,19 @@ def run_extras(peaks):
     boxes = [((2.0, 2.0, 0.0), (3.0, 3.5, 1.0)), ((5.0, 1.0, 0.0), (6.5, 2.0, 2.0))]
     ms = _time_ms(lambda: kernels.raycast_device(o, d, (0.0, 0.0, 0.0), (8.0, 8.0, 4.0), boxes))
     out["raycast"] = {"rays": int(d.shape[0]), "ms": ms, "rays_per_s": d.shape[0] / (ms * 1e-3)}
+    # K6 global retrieval (configs[3]/[4] databases): latency of one
+    # update_similarity scoring call through the public device API (host
+    # list assembly included), and the scored (coarse + refined) pairs
+    from paper_2510_02080_b200 import loops
+
+    out["retrieval"] = []
+    for K in (1500, 4000):
+        pooled = synth.pooled_embeddings(K, seed=K)
+        res = loops.retrieval_device(pooled, 5, 15, 0.93, 0.96)
+        scored = int(len(res[0]) + len(res[4]))
+        ms = _time_ms(lambda: loops.retrieval_device(pooled, 5, 15, 0.93, 0.96), reps=5, warm=1)
+        out["retrieval"].append({"keyframes": K, "ms": ms, "scored_pairs": scored,
+                                 "scored_pairs_per_s": scored / (ms * 1e-3), "candidates": int(len(res[2]))})
     return out
 
 
