@@ -11,7 +11,10 @@
 // the coarse rows ai in [k_begin, k_end); the per-rank lists concatenated in
 // rank order equal the single-GPU lists.
 
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -39,48 +42,6 @@ __global__ void rt_coarse_kernel(const double* __restrict__ P, int K, int D, int
     }
     dense_s[o] = s;
     dense_f[o] = f;
-}
-
-// Ordered compaction of the dense coarse grid (one CTA, row-major order).
-constexpr int RT_NT = 1024;
-__global__ void __launch_bounds__(RT_NT) rt_coarse_compact_kernel(const double* __restrict__ dense_s,
-                                                                  const uint8_t* __restrict__ dense_f, int64_t n,
-                                                                  int Kc, int kb, int stride, int32_t* __restrict__ cp,
-                                                                  double* __restrict__ cs, int64_t cap_c,
-                                                                  int32_t* __restrict__ hits, int64_t cap_h,
-                                                                  int64_t* __restrict__ counts) {
-    typedef cub::BlockScan<int, RT_NT> BS;
-    __shared__ typename BS::TempStorage tmp;
-    __shared__ int64_t carry_c, carry_h;
-    if (threadIdx.x == 0) { carry_c = 0; carry_h = 0; }
-    __syncthreads();
-    for (int64_t b = 0; b < n; b += RT_NT) {
-        const int64_t i = b + threadIdx.x;
-        const uint8_t f = i < n ? dense_f[i] : 0;
-        int ex_c, ex_h, ag_c, ag_h;
-        BS(tmp).ExclusiveSum(f >= 1 ? 1 : 0, ex_c, ag_c);
-        __syncthreads();
-        BS(tmp).ExclusiveSum(f == 2 ? 1 : 0, ex_h, ag_h);
-        if (f >= 1) {
-            const int64_t o = carry_c + ex_c;
-            if (o < cap_c) {
-                cp[2 * o] = (int32_t)((kb + i / Kc) * stride);
-                cp[2 * o + 1] = (int32_t)((i % Kc) * stride);
-                cs[o] = dense_s[i];
-            }
-        }
-        if (f == 2) {
-            const int64_t o = carry_h + ex_h;
-            if (o < cap_h) hits[o] = (int32_t)i;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) { carry_c += ag_c; carry_h += ag_h; }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        counts[0] = carry_c;
-        counts[3] = carry_h;  // scratch slot: number of coarse hits
-    }
 }
 
 // Refinement windows: hit h, offset r -> (da, db) = (r / (2s-1), r % (2s-1)) - (s-1)
@@ -113,43 +74,117 @@ __global__ void rt_refine_kernel(const double* __restrict__ P, int K, int D, int
     }
 }
 
-__global__ void __launch_bounds__(RT_NT) rt_refine_compact_kernel(const double* __restrict__ rs,
-                                                                  const uint8_t* __restrict__ rf,
-                                                                  const int32_t* __restrict__ rpair, int stride,
-                                                                  int64_t cap_h, int32_t* __restrict__ candp,
-                                                                  double* __restrict__ cands,
-                                                                  int32_t* __restrict__ evp, double* __restrict__ evs,
-                                                                  int64_t cap, int64_t* __restrict__ counts) {
-    typedef cub::BlockScan<int, RT_NT> BS;
+// ---------------------------------------------------------------------------
+// Multi-CTA ordered compaction of a flag array (0 / 1 / 2): per 4096-element
+// chunk the counts of (f >= 1) and (f == 2), one exclusive scan over the
+// chunks, then every chunk scatters its elements in order.  The single-CTA
+// block-scan loops above it replaced cost ~6 ms at K = 4000.
+constexpr int RC_NT = 256, RC_PER = 16, RC_CH = RC_NT * RC_PER;
+
+__device__ __forceinline__ int64_t rc_len(int64_t n_static, const int64_t* n_dev, int64_t cap, int64_t mul) {
+    return n_dev ? min(*n_dev, cap) * mul : n_static;
+}
+
+__global__ void __launch_bounds__(RC_NT) rt_chunk_count_kernel(const uint8_t* __restrict__ f, int64_t n_static,
+                                                               const int64_t* __restrict__ n_dev, int64_t cap,
+                                                               int64_t mul, int* __restrict__ c1,
+                                                               int* __restrict__ c2) {
+    typedef cub::BlockReduce<int, RC_NT> BR;
+    __shared__ typename BR::TempStorage t1, t2;
+    const int64_t n = rc_len(n_static, n_dev, cap, mul);
+    const int64_t i0 = (int64_t)blockIdx.x * RC_CH + (int64_t)threadIdx.x * RC_PER;
+    int a = 0, b = 0;
+    for (int k = 0; k < RC_PER; ++k) {
+        const int64_t i = i0 + k;
+        const uint8_t v = i < n ? f[i] : 0;
+        a += v >= 1;
+        b += v == 2;
+    }
+    const int ta = BR(t1).Sum(a);
+    const int tb = BR(t2).Sum(b);
+    if (threadIdx.x == 0) { c1[blockIdx.x] = ta; c2[blockIdx.x] = tb; }
+}
+
+// in-place exclusive scan of both chunk-count arrays (one CTA); totals to
+// out1 / out2
+__global__ void __launch_bounds__(1024) rt_chunk_scan_kernel(int* __restrict__ c1, int* __restrict__ c2, int nchunks,
+                                                             int64_t* __restrict__ out1, int64_t* __restrict__ out2) {
+    typedef cub::BlockScan<int, 1024> BS;
     __shared__ typename BS::TempStorage tmp;
-    __shared__ int64_t carry_e, carry_c;
-    const int w = 2 * stride - 1;
-    const int64_t n = min(counts[3], cap_h) * (int64_t)(w * w);
-    if (threadIdx.x == 0) { carry_e = 0; carry_c = 0; }
+    __shared__ int carry1, carry2;
+    if (threadIdx.x == 0) { carry1 = 0; carry2 = 0; }
     __syncthreads();
-    for (int64_t b = 0; b < n; b += RT_NT) {
-        const int64_t i = b + threadIdx.x;
-        const uint8_t f = i < n ? rf[i] : 0;
-        int ex_e, ex_c, ag_e, ag_c;
-        BS(tmp).ExclusiveSum(f >= 1 ? 1 : 0, ex_e, ag_e);
+    for (int b = 0; b < nchunks; b += 1024) {
+        const int i = b + threadIdx.x;
+        const int v1 = i < nchunks ? c1[i] : 0, v2 = i < nchunks ? c2[i] : 0;
+        int e1, e2, t1, t2;
+        BS(tmp).ExclusiveSum(v1, e1, t1);
         __syncthreads();
-        BS(tmp).ExclusiveSum(f == 2 ? 1 : 0, ex_c, ag_c);
-        if (f >= 1) {
-            const int64_t o = carry_e + ex_e;
-            if (o < cap) { evp[2 * o] = rpair[2 * i]; evp[2 * o + 1] = rpair[2 * i + 1]; evs[o] = rs[i]; }
-        }
-        if (f == 2) {
-            const int64_t o = carry_c + ex_c;
-            if (o < cap) { candp[2 * o] = rpair[2 * i]; candp[2 * o + 1] = rpair[2 * i + 1]; cands[o] = rs[i]; }
-        }
+        BS(tmp).ExclusiveSum(v2, e2, t2);
+        if (i < nchunks) { c1[i] = carry1 + e1; c2[i] = carry2 + e2; }
         __syncthreads();
-        if (threadIdx.x == 0) { carry_e += ag_e; carry_c += ag_c; }
+        if (threadIdx.x == 0) { carry1 += t1; carry2 += t2; }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        counts[1] = carry_c;
-        counts[2] = carry_e;
+    if (threadIdx.x == 0) { *out1 = carry1; *out2 = carry2; }
+}
+
+// scatter: thread-local prefix over its 16 elements + block scan + chunk base
+template <typename F>
+__device__ __forceinline__ void rc_scatter(const uint8_t* __restrict__ f, int64_t n, const int* __restrict__ b1,
+                                           const int* __restrict__ b2, F&& emit) {
+    typedef cub::BlockScan<int, RC_NT> BS;
+    __shared__ typename BS::TempStorage s1, s2;
+    const int64_t i0 = (int64_t)blockIdx.x * RC_CH + (int64_t)threadIdx.x * RC_PER;
+    uint8_t v[RC_PER];
+    int a = 0, b = 0;
+#pragma unroll
+    for (int k = 0; k < RC_PER; ++k) {
+        v[k] = i0 + k < n ? f[i0 + k] : 0;
+        a += v[k] >= 1;
+        b += v[k] == 2;
     }
+    int ea, eb;
+    BS(s1).ExclusiveSum(a, ea);
+    BS(s2).ExclusiveSum(b, eb);
+    int64_t o1 = (int64_t)b1[blockIdx.x] + ea, o2 = (int64_t)b2[blockIdx.x] + eb;
+#pragma unroll
+    for (int k = 0; k < RC_PER; ++k) {
+        if (v[k] >= 1) emit(i0 + k, o1++, v[k] == 2 ? o2++ : (int64_t)-1);
+    }
+}
+
+__global__ void __launch_bounds__(RC_NT) rt_coarse_scatter_kernel(const double* __restrict__ dense_s,
+                                                                  const uint8_t* __restrict__ dense_f, int64_t n,
+                                                                  int Kc, int kb, int stride, const int* __restrict__ b1,
+                                                                  const int* __restrict__ b2,
+                                                                  int32_t* __restrict__ cp, double* __restrict__ cs,
+                                                                  int64_t cap_c, int32_t* __restrict__ hits,
+                                                                  int64_t cap_h) {
+    rc_scatter(dense_f, n, b1, b2, [&](int64_t i, int64_t o, int64_t oh) {
+        if (o < cap_c) {
+            cp[2 * o] = (int32_t)((kb + i / Kc) * stride);
+            cp[2 * o + 1] = (int32_t)((i % Kc) * stride);
+            cs[o] = dense_s[i];
+        }
+        if (oh >= 0 && oh < cap_h) hits[oh] = (int32_t)i;
+    });
+}
+
+__global__ void __launch_bounds__(RC_NT) rt_refine_scatter_kernel(const double* __restrict__ rs,
+                                                                  const uint8_t* __restrict__ rf,
+                                                                  const int32_t* __restrict__ rpair,
+                                                                  const int64_t* __restrict__ counts, int64_t cap_h,
+                                                                  int64_t R, const int* __restrict__ b1,
+                                                                  const int* __restrict__ b2,
+                                                                  int32_t* __restrict__ candp,
+                                                                  double* __restrict__ cands, int32_t* __restrict__ evp,
+                                                                  double* __restrict__ evs, int64_t cap) {
+    const int64_t n = min(counts[3], cap_h) * R;
+    rc_scatter(rf, n, b1, b2, [&](int64_t i, int64_t o, int64_t oh) {
+        if (o < cap) { evp[2 * o] = rpair[2 * i]; evp[2 * o + 1] = rpair[2 * i + 1]; evs[o] = rs[i]; }
+        if (oh >= 0 && oh < cap) { candp[2 * oh] = rpair[2 * i]; candp[2 * oh + 1] = rpair[2 * i + 1]; cands[oh] = rs[i]; }
+    });
 }
 
 }  // namespace ec3r
@@ -164,8 +199,10 @@ extern "C" size_t ec3r_retrieval_workspace(int K, int stride, int64_t cap_refine
     const int64_t dense = Kc * Kc;
     const int64_t R = (int64_t)(2 * stride - 1) * (2 * stride - 1);
     const int64_t cap_h = cap_refine / R + 1;
+    const int64_t nch = (std::max<int64_t>(dense, cap_h * R) + RC_CH - 1) / RC_CH + 1;
     return align256(8 * dense) + align256(dense) + align256(4 * (size_t)cap_h) + align256(8 * (size_t)(cap_h * R)) +
-           align256((size_t)(cap_h * R)) + align256(8 * (size_t)(cap_h * R)) + align256(64);
+           align256((size_t)(cap_h * R)) + align256(8 * (size_t)(cap_h * R)) + align256(64) +
+           2 * align256(4 * (size_t)nch);
 }
 
 extern "C" int ec3r_retrieval(const double* pooled, int K, int D, int stride, int exclusion, double tau_g,
@@ -196,14 +233,30 @@ extern "C" int ec3r_retrieval(const double* pooled, int K, int D, int stride, in
     rt_coarse_kernel<<<g1, 128, 0, st>>>(pooled, K, D, stride, exclusion, tau_g, Kc, k_begin, dense_s, dense_f);
     EC3R_CHECK_LAUNCH("rt_coarse_kernel");
     const int64_t cap_c = (int64_t)rows * Kc;
-    rt_coarse_compact_kernel<<<1, RT_NT, 0, st>>>(dense_s, dense_f, (int64_t)rows * Kc, Kc, k_begin, stride,
-                                                  coarse_pairs, coarse_scores, cap_c, hits, cap_h, counts);
-    EC3R_CHECK_LAUNCH("rt_coarse_compact_kernel");
+    const int64_t n_c = (int64_t)rows * Kc;
+    const int64_t nch_max = (std::max<int64_t>((int64_t)Kc * Kc, cap_h * R) + RC_CH - 1) / RC_CH + 1;
+    int* cb1 = cv.take<int>(nch_max);
+    int* cb2 = cv.take<int>(nch_max);
+    // coarse grid -> coarse pairs (scored) and hits, in row-major order
+    const int nch_c = (int)((n_c + RC_CH - 1) / RC_CH);
+    rt_chunk_count_kernel<<<nch_c, RC_NT, 0, st>>>(dense_f, n_c, nullptr, 0, 1, cb1, cb2);
+    EC3R_CHECK_LAUNCH("rt_chunk_count_kernel");
+    rt_chunk_scan_kernel<<<1, 1024, 0, st>>>(cb1, cb2, nch_c, counts + 0, counts + 3);
+    EC3R_CHECK_LAUNCH("rt_chunk_scan_kernel");
+    rt_coarse_scatter_kernel<<<nch_c, RC_NT, 0, st>>>(dense_s, dense_f, n_c, Kc, k_begin, stride, cb1, cb2,
+                                                      coarse_pairs, coarse_scores, cap_c, hits, cap_h);
+    EC3R_CHECK_LAUNCH("rt_coarse_scatter_kernel");
     rt_refine_kernel<<<kNumSMs * 4, 128, 0, st>>>(pooled, K, D, stride, exclusion, tau_l, Kc, k_begin, hits, counts,
                                                   cap_h, rs, rf, rpair);
     EC3R_CHECK_LAUNCH("rt_refine_kernel");
-    rt_refine_compact_kernel<<<1, RT_NT, 0, st>>>(rs, rf, rpair, stride, cap_h, cand_pairs, cand_scores, eval_pairs,
-                                                  eval_scores, cap_refine, counts);
-    EC3R_CHECK_LAUNCH("rt_refine_compact_kernel");
+    // refinement windows -> evaluated pairs and admitted-candidate pairs
+    const int nch_r = (int)((cap_h * R + RC_CH - 1) / RC_CH);
+    rt_chunk_count_kernel<<<nch_r, RC_NT, 0, st>>>(rf, 0, counts + 3, cap_h, R, cb1, cb2);
+    EC3R_CHECK_LAUNCH("rt_chunk_count_kernel");
+    rt_chunk_scan_kernel<<<1, 1024, 0, st>>>(cb1, cb2, nch_r, counts + 2, counts + 1);
+    EC3R_CHECK_LAUNCH("rt_chunk_scan_kernel");
+    rt_refine_scatter_kernel<<<nch_r, RC_NT, 0, st>>>(rs, rf, rpair, counts, cap_h, R, cb1, cb2, cand_pairs,
+                                                      cand_scores, eval_pairs, eval_scores, cap_refine);
+    EC3R_CHECK_LAUNCH("rt_refine_scatter_kernel");
     return EC3R_OK;
 }

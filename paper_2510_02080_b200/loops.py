@@ -43,6 +43,9 @@ class SimilarityMatrix:
         return self._scores.items()
 
 
+_cap_cache: dict = {}  # (K, stride, k_begin, k_end) -> refinement capacity that sufficed
+
+
 def retrieval_device(pooled: torch.Tensor, stride: int, exclusion: int, tau_g: float, tau_l: float,
                      k_begin: int = 0, k_end: int = -1, cap_refine: int = 1 << 16, stream=None):
     """Run K6 on a (K, D) float64 CUDA tensor.  Returns numpy arrays
@@ -57,6 +60,8 @@ def retrieval_device(pooled: torch.Tensor, stride: int, exclusion: int, tau_g: f
     ke = Kc if k_end is None or k_end < 0 or k_end > Kc else k_end
     rows = max(ke - kb, 0)
     R = (2 * stride - 1) ** 2
+    key = (int(K), int(stride), kb, ke)
+    cap_refine = max(int(cap_refine), _cap_cache.get(key, 0))  # start from the last call's need
     while True:
         cap_c = max(rows * Kc, 1)
         cp = torch.empty((cap_c, 2), dtype=torch.int32, device=dev)
@@ -76,8 +81,27 @@ def retrieval_device(pooled: torch.Tensor, stride: int, exclusion: int, tau_g: f
         if n_q <= cap_refine and n_e <= cap_refine and n_h <= cap_refine // R + 1:
             break
         cap_refine = max(cap_refine * 4, (n_h + 1) * R, n_e)
-    return (cp[:n_c].cpu().numpy(), cs[:n_c].cpu().numpy(), qp[:n_q].cpu().numpy(), qs[:n_q].cpu().numpy(),
-            ep[:n_e].cpu().numpy(), es[:n_e].cpu().numpy())
+    _cap_cache[key] = cap_refine
+    outs = (cp[:n_c], cs[:n_c], qp[:n_q], qs[:n_q], ep[:n_e], es[:n_e])
+    return tuple(_to_host(x) for x in outs) if outs[0].is_cuda else tuple(x.numpy() for x in outs)
+
+
+_pinned: dict = {}
+
+
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """D2H through a cached pinned buffer (pageable copies of the multi-MB
+    lists ran at ~3.5 GB/s)."""
+    n = t.numel() * t.element_size()
+    buf = _pinned.get(t.dtype)
+    if buf is None or buf.numel() < t.numel():
+        buf = torch.empty(max(t.numel(), 1 << 16), dtype=t.dtype, pin_memory=True)
+        _pinned[t.dtype] = buf
+    view = buf[: t.numel()]
+    if n:
+        view.copy_(t.reshape(-1), non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+    return view.numpy().reshape(t.shape).copy()
 
 
 def _populate(matrix, kfs: np.ndarray, pairs: np.ndarray, scores: np.ndarray):
