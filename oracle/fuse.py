@@ -20,7 +20,8 @@ Declared rule (``fuse_points``):
         count = number of points,
   (v)   output sorted by key ascending.
 Parity: keys and counts bit-exact, centroids within 1e-4 m, wsum within
-1e-5 relative (the GPU accumulates in float32 relative to the voxel corner).
+1e-4 relative (the GPU accumulates in float32 relative to the voxel corner,
+in arbitrary order).
 """
 
 from __future__ import annotations
