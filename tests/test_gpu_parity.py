@@ -727,3 +727,30 @@ def test_registration_edges_status_paths(golden):
         (r,), _ = mapping.register_edges(dm.pool, [(subs[1], subs[0])], with_keep_masks=True)
         assert names[r.status] == expect, (kind, r.status)
         assert r.count == e["count"], (kind, r.count, e["count"])
+
+
+def test_registration_full_resolution_edges_vs_oracle():
+    """Four 518x392 edges of the bench generator (one launch): keep counts
+    exact, Sim(3) within 1e-5 relative of the oracle's float64 Umeyama."""
+    from paper_2510_02080_b200 import mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(26, cfg, seed=9, device="cuda")
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms = [dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    pairs = [(sms[j], sms[j - 1]) for j in range(1, len(sms))]
+    res, _ = mapping.register_edges(dm.pool, pairs, with_keep_masks=True)
+    dense = []
+    for ids, o in zip(sb.frame_ids, sb.slot_offsets):
+        F = len(ids)
+        dense.append(dict(depth=sb.depth[o:o + F].cpu().numpy(), conf=sb.conf[o:o + F].cpu().numpy(),
+                          frame_ids=np.array(ids), pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:],
+                          K=sb.K4))
+    assert len(res) >= 4
+    for j, r in zip(range(1, len(sms)), res):
+        e = ref.registration_edge(dense[j], dense[j - 1])
+        assert e["status"] == ref.STATUS_OK and r.status == 0, (j, e["status"], r.status)
+        assert r.count == e["count"], (j, r.count, e["count"])
+        tr = r.transform
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, e["s"], e["q"], e["t"])
+        assert abs(r.rms - e["rms"]) <= 1e-5 * max(1.0, e["rms"])
