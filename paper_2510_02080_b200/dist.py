@@ -209,3 +209,140 @@ def retrieval_sharded(db, stride: int, exclusion: int, tau_g: float, tau_l: floa
         t = torch.as_tensor(np.ascontiguousarray(a), device=dev)
         merged.append(torch.cat(gather_ragged(t, group)).cpu().numpy())
     return tuple(merged)
+
+
+# -- align windows with a shared-frame halo (SURVEY.md §8(e), row (a)+(b)) --
+#
+# Rank r owns a contiguous window of submaps.  Its first submap shares a
+# keyframe with the last submap of rank r-1 (KeyframeBuffer flush order,
+# loops.py:89-111), so registering it needs the predecessor's copy of that
+# frame: a halo of one 392x518 depth + confidence plane (1.6 MB) and its
+# local pose.  Each rank registers [halo stub] + window with the stub fixed
+# at identity (mapping.py:190-211 semantics), which gives every submap's
+# pose relative to the predecessor's last submap; one all-gather of the
+# windows' last poses (8 f64 per rank) and a prefix composition in rank
+# order turn those into global poses.  Edge measurements never depend on
+# global poses, so the result equals single-process registration up to the
+# association order of the Sim(3) compositions.
+
+HALO_MAX = 16  # keyframes one submap may share with its predecessor
+
+
+def _peer(group, r: int) -> int:
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+def shift(send: Sequence[torch.Tensor], recv: Sequence[torch.Tensor], step: int = 1, group=None) -> None:
+    """Grouped P2P: rank r sends `send` to rank r+step and receives `recv`
+    (preallocated, same shapes as the sender's) from rank r-step; ranks at
+    the ends skip the side that does not exist."""
+    rank, world = _world(group)
+    if world == 1:
+        return
+    ops = []
+    dst, src = rank + step, rank - step
+    if 0 <= dst < world:
+        ops += [dist.P2POp(dist.isend, t.contiguous(), _peer(group, dst), group) for t in send]
+    if 0 <= src < world:
+        ops += [dist.P2POp(dist.irecv, t, _peer(group, src), group) for t in recv]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def window_halo(mapping, window: Sequence, group=None):
+    """Fetch the predecessor's halo and add it to `mapping` as a stub submap.
+
+    Two point-to-point rounds: rank r sends the keyframe ids of its first
+    submap to rank r-1; rank r-1 answers with the frames of its last submap
+    holding those keyframes (ids, depth, confidence, local pose).  Returns the
+    stub (None on rank 0, or when nothing is shared)."""
+    rank, world = _world(group)
+    if world == 1:
+        return None
+    pool = mapping.pool
+    dev = pool.device
+    tdev = torch.device("cpu") if _host_staged(group, dev) else dev
+    H, W = pool.H, pool.W
+    i64 = dict(dtype=torch.int64, device=tdev)
+    # round 1 (backwards): requested keyframe ids, -1 padded
+    req = torch.full((HALO_MAX,), -1, **i64)
+    if window:
+        ids = list(window[0].keyframe_ids)[:HALO_MAX]
+        req[: len(ids)] = torch.tensor(ids, dtype=torch.int64)
+    want = torch.full((HALO_MAX,), -1, **i64)
+    shift([req], [want], step=-1, group=group)
+    # round 2 (forwards): header (count, ids) then the frames
+    send = []
+    if rank + 1 < world:
+        wanted = {int(x) for x in want.tolist() if x >= 0}
+        last = window[-1]
+        pick = [k for k, f in enumerate(last.keyframe_ids) if f in wanted]
+        hdr = torch.full((1 + HALO_MAX,), -1, **i64)
+        hdr[0] = len(pick)
+        hdr[1: 1 + len(pick)] = torch.tensor([last.keyframe_ids[k] for k in pick], dtype=torch.int64)
+        sl = torch.as_tensor(np.asarray(last.slots, np.int64)[pick], device=dev)
+        send = [hdr, pool.depth.index_select(0, sl).to(tdev), pool.conf.index_select(0, sl).to(tdev),
+                pool.poses.index_select(0, sl).to(tdev)]
+        n_send = len(pick)
+    hdr_in = torch.full((1 + HALO_MAX,), -1, **i64)
+    shift(send[:1], [hdr_in] if rank > 0 else [], step=1, group=group)
+    n_in = int(hdr_in[0]) if rank > 0 else 0
+    recv = []
+    if rank > 0 and n_in > 0:
+        recv = [torch.empty((n_in, H, W), dtype=pool.depth.dtype, device=tdev),
+                torch.empty((n_in, H, W), dtype=pool.conf.dtype, device=tdev),
+                torch.empty((n_in, 8), dtype=torch.float64, device=tdev)]
+    shift(send[1:] if rank + 1 < world and n_send > 0 else [], recv, step=1, group=group)
+    if rank == 0 or n_in == 0:
+        return None
+    ids = [int(x) for x in hdr_in[1: 1 + n_in].tolist()]
+    return mapping.add_submap(ids, recv[0].to(dev), recv[1].to(dev), list(recv[2].cpu().numpy()))
+
+
+def prefix_offsets(window_last: Sequence) -> list:
+    """O_0 = identity, O_r = O_{r-1} o W_{r-1}: the global pose of each
+    window's reference frame from the windows' last-submap poses W_r (each
+    expressed in its own window's frame).  Sim(3) 8-vectors."""
+    from .types import Sim3Transform, sim3_to_vec, vec_to_sim3
+
+    out = [sim3_to_vec(Sim3Transform.identity())]
+    for w in list(window_last)[:-1]:
+        out.append(sim3_to_vec(vec_to_sim3(out[-1]).compose(vec_to_sim3(np.asarray(w, np.float64)))))
+    return [np.asarray(o, np.float64) for o in out]
+
+
+def window_offset(last_local, group=None, device=None) -> np.ndarray:
+    """All-gather every window's last-submap pose (8 f64 per rank) and return
+    this rank's prefix offset (prefix_offsets)."""
+    rank, world = _world(group)
+    v = np.asarray(last_local, np.float64).reshape(8)
+    if world == 1:
+        return prefix_offsets([v])[0]
+    dev = torch.device("cpu") if device is None else torch.device(device)
+    if _host_staged(group, dev):
+        dev = torch.device("cpu")
+    t = torch.as_tensor(v, device=dev)
+    bufs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(bufs, t, group=group)
+    return prefix_offsets([b.cpu().numpy() for b in bufs])[rank]
+
+
+def register_window(mapping, window: Sequence, group=None):
+    """Register this rank's window of submaps into global poses.
+
+    `mapping` holds only this rank's submaps (window, in order).  The halo
+    stub is registered first (identity), used as the first submap's partner
+    and then forgotten, so fusion never sees the predecessor's frames twice.
+    Returns the window offset (Sim3Transform)."""
+    from .types import sim3_to_vec, vec_to_sim3
+
+    stub = window_halo(mapping, window, group)
+    mapping.register_chain(([stub] if stub is not None else []) + list(window))
+    off = vec_to_sim3(window_offset(sim3_to_vec(window[-1].global_pose), group, mapping.pool.device))
+    if stub is not None:
+        mapping.forget(stub)
+    for sm in window:
+        sm.global_pose = off.compose(sm.global_pose)
+        mapping._commit(sm)
+    return off

@@ -375,6 +375,15 @@ class DenseMapping:
             if sm.id not in lst:
                 lst.append(sm.id)
 
+    def forget(self, sm):
+        """Drop a submap from the map (its pool slots stay allocated): used
+        for the halo stub of a sharded window (dist.register_window)."""
+        self.submaps.pop(sm.id, None)
+        for kf in sm.keyframe_ids:
+            lst = self.kf_submaps.get(kf, [])
+            if sm.id in lst:
+                lst.remove(sm.id)
+
     def register_submap(self, sm):
         """mapping.py:190-211."""
         if not self.submaps:

@@ -209,3 +209,77 @@ def test_global_fusion_protocol_equals_single_process_oracle_gloo():
     corner = unpack(keys).astype(np.float64) * CELL
     cen = corner + sums[:, :3] / sums[:, 3:4]
     assert np.max(np.abs(cen - ref["centroid"])) < 1e-4
+
+
+# --------------------------------------------------------------------------
+# align windows: halo exchange + prefix composition of window offsets
+
+class _FakePool:
+    def __init__(self, rank, n_frames=12, H=4, W=5):
+        self.H, self.W, self.device = H, W, torch.device("cpu")
+        g = torch.Generator().manual_seed(100 + rank)
+        self.depth = torch.rand((n_frames, H, W), generator=g)
+        self.conf = torch.rand((n_frames, H, W), generator=g)
+        self.poses = torch.rand((n_frames, 8), generator=g, dtype=torch.float64)
+
+
+class _FakeSubmap:
+    def __init__(self, kf_ids, slots):
+        self.keyframe_ids, self.slots = tuple(kf_ids), np.asarray(slots)
+
+
+class _FakeMapping:
+    def __init__(self, rank):
+        self.pool = _FakePool(rank)
+        self.added = None
+
+    def add_submap(self, ids, depth, conf, poses):
+        self.added = (list(ids), depth.clone(), conf.clone(), np.stack(poses))
+        return self.added
+
+
+def _windows(rank):
+    # flush order (new..., old): rank 0 = [(0..5), (6..10, 5)], rank 1 = [(11..15, 10), (16..20, 15)]
+    if rank == 0:
+        return [_FakeSubmap(range(6), range(6)), _FakeSubmap(list(range(6, 11)) + [5], range(6, 12))]
+    return [_FakeSubmap(list(range(11, 16)) + [10], range(6)), _FakeSubmap(list(range(16, 21)) + [15], range(6, 12))]
+
+
+def w_halo(rank, world):
+    m = _FakeMapping(rank)
+    D.window_halo(m, _windows(rank))
+    return m.added
+
+
+def _tf(rng):
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    return np.concatenate([[rng.uniform(0.5, 2.0)], q, rng.normal(size=3)])
+
+
+def w_offset(rank, world):
+    rng = np.random.default_rng(rank)
+    return D.window_offset(_tf(rng))
+
+
+def test_window_halo_sends_the_shared_keyframe_frame_gloo():
+    out = _spawn("w_halo")
+    assert out[0] is None
+    ids, depth, conf, poses = out[1]
+    assert ids == [10]  # rank 1's first submap shares keyframe 10 with rank 0's last submap
+    src = _FakePool(0)
+    k = 4 + 6  # keyframe 10 is frame 4 of rank 0's last submap, pool slot 10
+    np.testing.assert_array_equal(depth.numpy(), src.depth[k:k + 1].numpy())
+    np.testing.assert_array_equal(conf.numpy(), src.conf[k:k + 1].numpy())
+    np.testing.assert_array_equal(poses, src.poses[k:k + 1].numpy())
+
+
+def test_window_offsets_prefix_compose_gloo():
+    from paper_2510_02080_b200.types import vec_to_sim3
+    out = _spawn("w_offset")
+    w0 = _tf(np.random.default_rng(0))
+    np.testing.assert_allclose(out[0], [1, 1, 0, 0, 0, 0, 0, 0], atol=0)
+    exp = vec_to_sim3(D.prefix_offsets([w0, w0])[1])
+    got = vec_to_sim3(out[1])
+    assert abs(got.scale - vec_to_sim3(w0).scale) < 1e-15 and abs(exp.scale - got.scale) == 0
+    np.testing.assert_allclose(got.translation, vec_to_sim3(w0).translation, atol=1e-15)

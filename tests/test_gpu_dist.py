@@ -1,0 +1,109 @@
+"""Two ranks on one GPU (gloo, CUDA payloads staged through the host) running
+the sharded align protocol end to end: each rank registers its own window of
+full-resolution synthetic submaps plus the predecessor's shared-frame halo
+(dist.register_window); the resulting global poses must equal single-process
+registration of the whole sequence, and the fused map of the two windows the
+single-process fused map."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+N_KF = 31  # 6 submaps of 6 frames
+SEED = 4
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _build(ids_sel=None):
+    from paper_2510_02080_b200 import mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(N_KF, cfg, seed=SEED, device="cuda")
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    idx = range(len(sb.frame_ids)) if ids_sel is None else ids_sel
+    sms = []
+    for i in idx:
+        ids, o = sb.frame_ids[i], sb.slot_offsets[i]
+        sms.append(dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)],
+                                 list(sb.poses8[o:o + len(ids)])))
+    return dm, sms, len(sb.frame_ids)
+
+
+def _poses(sms):
+    from paper_2510_02080_b200.types import sim3_to_vec
+    return np.stack([sim3_to_vec(sm.global_pose) for sm in sms])
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_02080_b200 import dist as D
+        torch.cuda.set_device(0)
+        from paper_2510_02080_b200 import synth
+        S = len(synth.flush_batches(N_KF))
+        lo, hi = D.shard_window(S, world, rank)
+        dm, sms, _ = _build(range(lo, hi))
+        D.register_window(dm, sms)
+        cloud = dm.fused_cloud(voxel=0.02)
+        q.put((rank, (lo, hi, _poses(sms), len(dm.submaps), cloud["keys"], cloud["count"])))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_register_window_two_ranks_equals_single_process():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, v = q.get(timeout=240)
+        out[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    for v in out.values():
+        if isinstance(v, Exception):
+            raise v
+    dm, sms, S = _build()
+    dm.register_chain(sms)
+    full = _poses(sms)
+    from oracle import ref_numpy as ref
+    for r in range(world):
+        lo, hi, poses, n_sub, _, _ = out[r]
+        assert n_sub == hi - lo  # the halo stub is not part of the map
+        for j in range(lo, hi):
+            a, b = poses[j - lo], full[j]
+            assert abs(a[0] - b[0]) <= 1e-9 * b[0]
+            np.testing.assert_allclose(ref.canonical_quat(a[1:5]), ref.canonical_quat(b[1:5]), atol=1e-9)
+            np.testing.assert_allclose(a[5:], b[5:], atol=1e-9 * max(1.0, float(np.abs(b[5:]).max())))
+    # the union of the windows' voxel maps covers the single-process map
+    ref_map = dm.fused_cloud(voxel=0.02)
+    keys = np.unique(np.concatenate([out[r][4] for r in range(world)]))
+    cnt = {}
+    for r in range(world):
+        for k, c in zip(out[r][4], out[r][5]):
+            cnt[int(k)] = cnt.get(int(k), 0) + int(c)
+    np.testing.assert_array_equal(keys, ref_map["keys"])
+    assert sum(cnt.values()) == int(ref_map["count"].sum())
