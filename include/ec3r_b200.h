@@ -301,6 +301,38 @@ EC3R_API int ec3r_local_candidates(const double* positions, int64_t n_points, co
                                    int64_t* out_counts, int32_t* out_cand, void* workspace,
                                    size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------
+ * K9 (§8f rank 4): batched homography RANSAC (loop verification).
+ * Replaces estimate_homography_ransac (geometry.py:594-640), called per
+ * candidate by verify_candidate (loops.py:136-153).
+ *
+ * P problems; problem p owns matches [offsets[p], offsets[p+1]) of src / dst
+ * ((total, 2) float64 pixels, DEVICE; offsets DEVICE int64).  rng_state
+ * (DEVICE, P x 6 uint64): numpy PCG64 state of default_rng(seed) as
+ * (state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger).
+ *
+ * ec3r_homography_ransac_score replays rng.choice(n, 4, replace=False) for
+ * `iters` (= cfg.max_iterations) iterations and writes out_counts (P x iters
+ * int32): the inlier count of each iteration's hypothesis, -1 where the
+ * reference skips it (degenerate sample or failed DLT).  out_samples
+ * (nullable, P x iters x 4 int32) receives the drawn indices.  The caller
+ * walks the counts with the reference's acceptance / adaptive-stop rule and
+ * passes each problem's chosen iteration (or -1) in `best` to
+ * ec3r_homography_ransac_refit, with the SAME workspace: it writes the final
+ * model (P x 9 float64, row-major, h22 = 1), the inlier mask (total uint8)
+ * and the inlier count (P int32).
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_homography_workspace(int n_problems, int iters);
+EC3R_API int ec3r_homography_ransac_score(const double* src, const double* dst, const int64_t* offsets,
+                                          int n_problems, const uint64_t* rng_state, int iters,
+                                          double pixel_threshold, int32_t* out_counts, int32_t* out_samples,
+                                          void* workspace, size_t workspace_bytes, void* stream);
+EC3R_API int ec3r_homography_ransac_refit(const double* src, const double* dst, const int64_t* offsets,
+                                          int n_problems, const int32_t* best, int iters,
+                                          double pixel_threshold, double* out_model, uint8_t* out_mask,
+                                          int32_t* out_count, void* workspace, size_t workspace_bytes,
+                                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -218,6 +218,29 @@ except ImportError:
 
 
 try:  # pragma: no cover
+    from submap_slam.geometry import RansacConfig, RansacResult
+except ImportError:
+    @dataclass
+    class RansacConfig:
+        """geometry.py:59-66."""
+
+        pixel_threshold: float = 2.0
+        confidence: float = 0.999
+        max_iterations: int = 1000
+        min_inliers: int = 10
+        min_parallax_deg: float = 1.0
+        seed: int = 0
+
+    @dataclass
+    class RansacResult:
+        """geometry.py:69-73."""
+
+        model: object
+        inlier_mask: np.ndarray
+        inlier_ratio: float
+
+
+try:  # pragma: no cover
     from submap_slam.geometry import Correspondence2D3D
 except ImportError:
     @dataclass(frozen=True, eq=False)

@@ -418,6 +418,90 @@ def gen_local():
     np.savez_compressed(os.path.join(OUT, "local.npz"), **out)
 
 
+# --------------------------------------------------------------------------
+# §8(f) rank 4: homography RANSAC (geometry.py:594-640) on the reference's own
+# test scenes (test_geometry.py:222-280, test_loops.py:144-200) plus random
+# mixtures, noisy inliers and degenerate sets
+
+def _homog(h, src):
+    sh = np.concatenate([src, np.ones((len(src), 1))], axis=1) @ h.T
+    return sh[:, :2] / sh[:, 2:3]
+
+
+def gen_ransac():
+    from submap_slam.geometry import RansacConfig, estimate_homography_ransac
+
+    cases = []  # (src, dst, cfg)
+    rng = np.random.default_rng(39)                       # test_homography_exact
+    h = np.array([[1.2, 0.1, 5.0], [-0.05, 0.9, -3.0], [1e-4, -2e-4, 1.0]])
+    src = rng.uniform(0, 640, size=(60, 2))
+    cases.append((src, _homog(h, src), RansacConfig(seed=4)))
+    rng = np.random.default_rng(40)                       # test_homography_null_distribution
+    for trial in range(20):
+        src = rng.uniform(0, 640, size=(100, 2))
+        dst = rng.uniform(0, 640, size=(100, 2))
+        cases.append((src, dst, RansacConfig(seed=trial)))
+    rng = np.random.default_rng(41)                       # test_homography_mixture_ratio
+    h = np.array([[1.0, 0.02, 10.0], [0.01, 1.05, -4.0], [0.0, 0.0, 1.0]])
+    src = rng.uniform(50, 600, size=(100, 2))
+    dst = _homog(h, src)
+    bad = rng.choice(100, size=40, replace=False)
+    dst[bad] = rng.uniform(0, 640, size=(40, 2))
+    cases.append((src, dst, RansacConfig(seed=5)))
+    rng = np.random.default_rng(42)                       # test_homography_invariant_to_uniform_rescale
+    h = np.array([[0.9, 0.05, 20.0], [-0.02, 1.1, 7.0], [5e-5, 1e-4, 1.0]])
+    src = rng.uniform(0, 640, size=(40, 2))
+    dst = _homog(h, src)
+    cases.append((src, dst, RansacConfig(seed=6)))
+    cases.append((src * 3.0, dst * 3.0, RansacConfig(seed=6, pixel_threshold=6.0)))
+    for n_in, seed in ((35, 73), (30, 74), (40, 75)):     # test_loops._synthetic_homography_obs
+        rng = np.random.default_rng(seed)
+        h = np.array([[1.05, 0.02, 4.0], [-0.01, 0.98, -2.0], [1e-5, 0.0, 1.0]])
+        src = rng.uniform(20, 600, size=(100, 2))
+        dst = _homog(h, src)
+        dst[n_in:] = rng.uniform(0, 640, size=(100 - n_in, 2))
+        dst[n_in:] += 50.0 * np.sign(dst[n_in:] - 320.0)
+        dst[n_in:] = np.clip(dst[n_in:], 0, 640)
+        cases.append((src, dst, RansacConfig(seed=3)))
+    rng = np.random.default_rng(777)                      # random mixtures with pixel noise
+    for n, frac, noise, cfg in ((4, 1.0, 0.0, RansacConfig(seed=1)), (5, 0.8, 0.3, RansacConfig(seed=2)),
+                                (8, 0.5, 0.5, RansacConfig(seed=3)), (25, 0.6, 0.8, RansacConfig(seed=4)),
+                                (200, 0.3, 0.7, RansacConfig(seed=5)), (200, 0.9, 1.2, RansacConfig(seed=6)),
+                                (600, 0.45, 0.6, RansacConfig(seed=7, pixel_threshold=1.5)),
+                                (1500, 0.25, 0.5, RansacConfig(seed=8)),
+                                (300, 0.15, 0.4, RansacConfig(seed=9, max_iterations=200)),
+                                (120, 0.5, 0.5, RansacConfig(seed=10, confidence=0.99, pixel_threshold=3.0))):
+        h = np.eye(3) + np.array([[0.1, 0.05, 0], [-0.04, 0.08, 0], [0, 0, 0]]) * rng.normal(size=(3, 3))
+        h[:2, 2] = rng.uniform(-30, 30, 2)
+        h[2, :2] = rng.uniform(-2e-4, 2e-4, 2)
+        src = rng.uniform(0, 640, size=(n, 2))
+        dst = _homog(h, src) + noise * rng.normal(size=(n, 2))
+        k = int(round(frac * n))
+        dst[k:] = rng.uniform(0, 640, size=(n - k, 2))
+        cases.append((src, dst, cfg))
+    t = np.linspace(0, 600, 30)                           # degenerate: every point on one line
+    line = np.stack([t, 0.5 * t + 3.0], axis=1)
+    cases.append((line, line + 1.0, RansacConfig(seed=11)))
+    dup = np.repeat(rng.uniform(0, 640, size=(3, 2)), 4, axis=0)   # 3 distinct points only
+    cases.append((dup, dup * 1.1, RansacConfig(seed=12)))
+    out = {}
+    for i, (src, dst, cfg) in enumerate(cases):
+        res = estimate_homography_ransac(list(zip(src, dst)), cfg)
+        out[f"c{i}_src"] = src
+        out[f"c{i}_dst"] = dst
+        out[f"c{i}_cfg"] = np.array([cfg.pixel_threshold, cfg.confidence, cfg.max_iterations, cfg.seed], float)
+        out[f"c{i}_model"] = np.asarray(res.model, float)
+        out[f"c{i}_mask"] = np.asarray(res.inlier_mask, bool)
+        out[f"c{i}_ratio"] = np.float64(res.inlier_ratio)
+    # the reference's hypothesis order: the first draws of rng.choice (geometry.py:612)
+    for n, seed in ((4, 0), (60, 4), (100, 7), (1500, 8), (70000, 3)):
+        r = np.random.default_rng(seed)
+        out[f"draws_{n}_{seed}"] = np.stack([r.choice(n, size=4, replace=False) for _ in range(64)])
+    out["n_cases"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(OUT, "ransac.npz"), **out)
+    print("ransac:", len(cases), "cases")
+
+
 class _SM:
     """The sparse map surface detect_local_candidates uses (positions())."""
 
@@ -435,3 +519,4 @@ if __name__ == "__main__":
     gen_retrieval()
     gen_kernels()
     gen_local()
+    gen_ransac()

@@ -754,3 +754,91 @@ def test_registration_full_resolution_edges_vs_oracle():
         tr = r.transform
         _assert_sim3(tr.scale, tr.rotation.q, tr.translation, e["s"], e["q"], e["t"])
         assert abs(r.rms - e["rms"]) <= 1e-5 * max(1.0, e["rms"])
+
+
+# --------------------------------------------------------------------------
+# K9 (§8f rank 4): batched homography RANSAC
+
+def _ransac_groups(g):
+    from paper_2510_02080_b200.types import RansacConfig
+    groups = {}
+    for i in range(int(g["n_cases"])):
+        c = g[f"c{i}_cfg"]
+        groups.setdefault((float(c[0]), float(c[1]), int(c[2])), []).append((i, int(c[3])))
+    for (thr, conf, iters), items in groups.items():
+        yield RansacConfig(pixel_threshold=thr, confidence=conf, max_iterations=iters), items
+
+
+def test_homography_ransac_golden_batched(golden):
+    """Every reference case (its own test scenes, mixtures, degenerate sets)
+    in batched launches: masks and ratios equal, models to rounding."""
+    from paper_2510_02080_b200 import geometry
+    g = golden("ransac")
+    seen = 0
+    for cfg, items in _ransac_groups(g):
+        probs = [(g[f"c{i}_src"], g[f"c{i}_dst"]) for i, _ in items]
+        res = geometry.estimate_homography_ransac_batch(probs, cfg, seeds=[s for _, s in items])
+        for (i, _), r in zip(items, res):
+            np.testing.assert_array_equal(r.inlier_mask, g[f"c{i}_mask"], err_msg=f"case {i}")
+            assert r.inlier_ratio == float(g[f"c{i}_ratio"]), i
+            np.testing.assert_allclose(r.model, g[f"c{i}_model"], rtol=0, atol=1e-8 * np.abs(r.model).max())
+            seen += 1
+    assert seen == int(g["n_cases"])
+
+
+def test_homography_ransac_hypothesis_order_and_counts(golden):
+    """The device replays rng.choice exactly, and every iteration's inlier
+    count equals the oracle's (-1 where the reference skips)."""
+    from oracle import ransac as orr
+    from paper_2510_02080_b200 import geometry
+    from paper_2510_02080_b200.types import RansacConfig
+    g = golden("ransac")
+    for i in (0, 21, 31, 35, 37):
+        c = g[f"c{i}_cfg"]
+        cfg = RansacConfig(pixel_threshold=float(c[0]), confidence=float(c[1]), max_iterations=int(c[2]),
+                           seed=int(c[3]))
+        src, dst = g[f"c{i}_src"], g[f"c{i}_dst"]
+        _, counts, samples = geometry.estimate_homography_ransac_batch([(src, dst)], cfg, return_samples=True)
+        rng = np.random.default_rng(cfg.seed)
+        draws = np.stack([rng.choice(len(src), size=4, replace=False) for _ in range(cfg.max_iterations)])
+        np.testing.assert_array_equal(samples[0], draws, err_msg=f"case {i}")
+        np.testing.assert_array_equal(counts[0], orr.hypotheses(src, dst, cfg.pixel_threshold, cfg.max_iterations,
+                                                                cfg.seed), err_msg=f"case {i}")
+
+
+def test_homography_ransac_random_batch_vs_oracle():
+    """64 loop-verification-sized problems (40-800 matches, 10-90 % inliers,
+    pixel noise) in one batch against the oracle."""
+    from oracle import ransac as orr
+    from paper_2510_02080_b200 import geometry
+    from paper_2510_02080_b200.types import RansacConfig
+    rng = np.random.default_rng(31337)
+    probs, seeds = [], []
+    for p in range(64):
+        n = int(rng.integers(40, 800))
+        h = np.eye(3) + 0.05 * rng.normal(size=(3, 3))
+        h[:2, 2] = rng.uniform(-40, 40, 2)
+        h[2, :2] = rng.uniform(-3e-4, 3e-4, 2)
+        h[2, 2] = 1.0
+        src = rng.uniform(0, 640, size=(n, 2))
+        sh = np.concatenate([src, np.ones((n, 1))], axis=1) @ h.T
+        dst = sh[:, :2] / sh[:, 2:3] + rng.uniform(0.0, 1.0) * rng.normal(size=(n, 2))
+        k = int(n * rng.uniform(0.1, 0.9))
+        dst[k:] = rng.uniform(0, 640, size=(n - k, 2))
+        probs.append((src, dst))
+        seeds.append(p)
+    cfg = RansacConfig()
+    res = geometry.estimate_homography_ransac_batch(probs, cfg, seeds=seeds)
+    for (src, dst), s, r in zip(probs, seeds, res):
+        h, m, ratio = orr.estimate_homography_ransac(src, dst, seed=s)
+        np.testing.assert_array_equal(r.inlier_mask, m)
+        assert r.inlier_ratio == ratio
+        np.testing.assert_allclose(r.model, h, rtol=0, atol=1e-8 * np.abs(h).max())
+
+
+def test_homography_ransac_errors():
+    from paper_2510_02080_b200 import geometry
+    from paper_2510_02080_b200.types import TooFewCorrespondences
+    with pytest.raises(TooFewCorrespondences):
+        geometry.estimate_homography_ransac([(np.zeros(2), np.zeros(2))] * 3)
+    assert geometry.estimate_homography_ransac_batch([]) == []

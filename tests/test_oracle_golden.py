@@ -147,3 +147,58 @@ def test_local_candidates_cases(golden):
                                       g[f"c{i}_counts"], err_msg=f"case {i}")
         assert ol.local_candidates(g[f"c{i}_pos"], g[f"c{i}_kf"], g[f"c{i}_poses"], g[f"c{i}_intr"],
                                    float(g["tau_p"])) == g[f"c{i}_cand"].tolist()
+
+
+def _ransac_case(g, i):
+    c = g[f"c{i}_cfg"]
+    return g[f"c{i}_src"], g[f"c{i}_dst"], float(c[0]), float(c[1]), int(c[2]), int(c[3])
+
+
+def test_ransac_homography_cases(golden):
+    """oracle/ransac.py == the reference on its own test scenes + mixtures."""
+    from oracle import ransac as orr
+    g = golden("ransac")
+    for i in range(int(g["n_cases"])):
+        src, dst, thr, conf, iters, seed = _ransac_case(g, i)
+        h, m, r = orr.estimate_homography_ransac(src, dst, thr, conf, iters, seed)
+        np.testing.assert_array_equal(m, g[f"c{i}_mask"], err_msg=f"case {i}")
+        assert r == float(g[f"c{i}_ratio"])
+        np.testing.assert_allclose(h, g[f"c{i}_model"], rtol=0, atol=1e-9 * np.abs(h).max())
+
+
+def test_ransac_rng_replay_matches_numpy_choice(golden):
+    """The PCG64 + Generator.choice replay K9 runs on the device reproduces
+    the reference's hypothesis order (geometry.py:612)."""
+    from oracle import ransac as orr
+    g = golden("ransac")
+    keys = [k for k in g.files if k.startswith("draws_")]
+    assert len(keys) == 5
+    for k in keys:
+        _, n, seed = k.split("_")
+        rp = orr.Pcg64Replay(int(seed))
+        np.testing.assert_array_equal(np.array([rp.choice4(int(n)) for _ in range(len(g[k]))]), g[k], err_msg=k)
+
+
+def test_ransac_host_walk_reproduces_sequential_loop(golden):
+    """geometry.walk_counts over the full-budget counts picks the hypothesis
+    the reference's adaptive loop keeps."""
+    from oracle import ransac as orr
+    from paper_2510_02080_b200.geometry import walk_counts
+    from paper_2510_02080_b200.types import RansacConfig
+    g = golden("ransac")
+    for i in (0, 1, 21, 24, 28, 30, 35, 36, 37):
+        src, dst, thr, conf, iters, seed = _ransac_case(g, i)
+        counts = orr.hypotheses(src, dst, thr, iters, seed)
+        b = walk_counts(counts, len(src), RansacConfig(pixel_threshold=thr, confidence=conf, max_iterations=iters,
+                                                       seed=seed))
+        if b < 0:
+            assert float(g[f"c{i}_ratio"]) == 0.0
+            continue
+        rng = np.random.default_rng(seed)
+        for _ in range(b + 1):
+            smp = rng.choice(len(src), size=4, replace=False)
+        h = orr.dlt(src[smp], dst[smp])
+        best = orr.transfer_errors(h, src, dst) < thr
+        assert int(best.sum()) == counts[b]
+        # the reference's final mask is the refit's when it keeps at least as many
+        assert g[f"c{i}_mask"].sum() >= best.sum()
