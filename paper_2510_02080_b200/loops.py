@@ -231,3 +231,71 @@ def detect_local_candidates(sparse_map, window, k, cfg) -> list:
     _, cand = local_candidates_device(pts, poses, (k.fx, k.fy, k.cx, k.cy, k.width, k.height), cfg.tau_p)
     c = cand.cpu().numpy()
     return [kf for (kf, _), ok in zip(window, c) if ok]
+
+
+# -- loop verification (loops.py:136-153) on K5 + K9 -----------------------
+
+try:  # pragma: no cover - exercised when the reference is installed
+    from submap_slam.loops import APPEND, REJECT, REPLACE, LoopConfig, LoopVerdict
+except ImportError:
+    from dataclasses import dataclass, field
+
+    from .types import RansacConfig
+
+    REJECT, APPEND, REPLACE = "Reject", "AppendToBuffer", "ReplaceCurrent"  # loops.py:24-26
+
+    @dataclass(frozen=True, eq=False)
+    class LoopConfig:
+        """loops.py:29-43."""
+
+        tau1: float = 0.4
+        tau2: float = 0.3
+        tau_p: float = 0.7
+        tau_global: float = 0.93
+        tau_local: float = 0.96
+        buffer_capacity: int = 5
+        r_local: int = 3
+        match_ratio: float = 0.8
+        ransac: RansacConfig = field(default_factory=RansacConfig)
+
+        def exclusion_zone(self) -> int:
+            return 3 * self.buffer_capacity
+
+    @dataclass
+    class LoopVerdict:
+        """loops.py:54-57."""
+
+        verdict: str
+        inlier_ratio: float
+
+
+def verify_candidates(query_obs, candidate_obs, cfg) -> list:
+    """verify_candidate (loops.py:136-153) for many candidates of one query:
+    one matcher launch (K5, mutual NN + ratio test) over every (query,
+    candidate) pair, then one batched homography RANSAC (K9) over the
+    candidates with >= 4 matches; the tau_2 / tau_1 bands as the reference."""
+    from .geometry import estimate_homography_ransac_batch
+    from .tracking import match_batched
+
+    cands = list(candidate_obs)
+    if not cands:
+        return []
+    qd = np.asarray(query_obs.descriptors)
+    live = [i for i, c in enumerate(cands) if len(qd) and len(c.descriptors)]
+    pairs = match_batched([(qd, cands[i].descriptors) for i in live], cfg.match_ratio) if live else []
+    probs, owners = [], []
+    for i, m in zip(live, pairs):
+        if len(m) >= 4:
+            probs.append((np.asarray(query_obs.keypoints, float)[m[:, 0]],
+                          np.asarray(cands[i].keypoints, float)[m[:, 1]]))
+            owners.append(i)
+    out = [LoopVerdict(REJECT, 0.0) for _ in cands]
+    for i, res in zip(owners, estimate_homography_ransac_batch(probs, cfg.ransac)):
+        r = res.inlier_ratio
+        out[i] = LoopVerdict(REJECT if r <= cfg.tau2 else APPEND if r <= cfg.tau1 else REPLACE, r)
+    return out
+
+
+def verify_candidate(query_obs, candidate_obs, cfg):
+    """loops.py:136-153 (one candidate)."""
+    return verify_candidates(query_obs, [candidate_obs], cfg)[0]

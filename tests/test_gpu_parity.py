@@ -842,3 +842,48 @@ def test_homography_ransac_errors():
     with pytest.raises(TooFewCorrespondences):
         geometry.estimate_homography_ransac([(np.zeros(2), np.zeros(2))] * 3)
     assert geometry.estimate_homography_ransac_batch([]) == []
+
+
+class _Obs:
+    def __init__(self, fid, kp, desc):
+        self.frame_id, self.keypoints, self.descriptors = fid, np.asarray(kp, float), np.asarray(desc, float)
+
+
+def _synthetic_homography_obs(n_total, n_inlier, seed):
+    """test_loops.py:144-160 scene: n_inlier pairs on a homography, the rest
+    pushed far off; identity descriptors."""
+    rng = np.random.default_rng(seed)
+    h = np.array([[1.05, 0.02, 4.0], [-0.01, 0.98, -2.0], [1e-5, 0.0, 1.0]])
+    src = rng.uniform(20, 600, size=(n_total, 2))
+    sh = np.concatenate([src, np.ones((n_total, 1))], axis=1) @ h.T
+    dst = sh[:, :2] / sh[:, 2:3]
+    dst[n_inlier:] = rng.uniform(0, 640, size=(n_total - n_inlier, 2))
+    dst[n_inlier:] += 50.0 * np.sign(dst[n_inlier:] - 320.0)
+    dst[n_inlier:] = np.clip(dst[n_inlier:], 0, 640)
+    desc = np.eye(n_total, 128)
+    return _Obs(0, src, desc), _Obs(1, dst, desc)
+
+
+def test_verify_candidates_reference_bands():
+    """The reference's test_loops.py:163-200 verification cases through the
+    batched K5 + K9 path (one query, all candidates in one call)."""
+    from paper_2510_02080_b200 import loops
+    from paper_2510_02080_b200.types import RansacConfig
+    cfg = loops.LoopConfig(ransac=RansacConfig(seed=3))
+    qs, cs = zip(*[_synthetic_homography_obs(100, k, s) for k, s in ((35, 73), (30, 74), (40, 75))])
+    for q, c, ratio, verdict in zip(qs, cs, (0.35, 0.3, 0.4), (loops.APPEND, loops.REJECT, loops.APPEND)):
+        v = loops.verify_candidate(q, c, cfg)
+        assert v.inlier_ratio == ratio and v.verdict == verdict
+    rng = np.random.default_rng(71)  # test_verify_identical_observations_replace
+    pix = rng.uniform(0, 63, size=(50, 2))
+    desc = rng.normal(size=(50, 64))
+    desc /= np.linalg.norm(desc, axis=1, keepdims=True)
+    a, b = _Obs(0, pix, desc), _Obs(1, pix.copy(), desc.copy())
+    rng = np.random.default_rng(72)  # test_verify_unrelated_observations_reject
+    u0 = _Obs(0, rng.uniform(0, 640, (60, 2)), np.eye(60, 80))
+    u1 = _Obs(1, rng.uniform(0, 640, (60, 2)), np.eye(60, 80))
+    out = loops.verify_candidates(a, [b, _Obs(2, np.zeros((0, 2)), np.zeros((0, 64))), b], loops.LoopConfig())
+    assert out[0].verdict == loops.REPLACE and out[0].inlier_ratio > 0.95
+    assert out[1].verdict == loops.REJECT and out[1].inlier_ratio == 0.0
+    assert out[2].verdict == out[0].verdict and out[2].inlier_ratio == out[0].inlier_ratio
+    assert loops.verify_candidate(u0, u1, loops.LoopConfig()).verdict == loops.REJECT
