@@ -583,6 +583,33 @@ def run_extras(peaks):
         ms = _time_ms(lambda: loops.retrieval_device(pooled, 5, 15, 0.93, 0.96), reps=5, warm=1)
         out["retrieval"].append({"keyframes": K, "ms": ms, "scored_pairs": scored,
                                  "scored_pairs_per_s": scored / (ms * 1e-3), "candidates": int(len(res[2]))})
+    # K9 loop verification (§8f rank 4): 64 candidates x 500 matches, 40 %
+    # inliers, full 1000-iteration budget scored on the device; the reference
+    # loop (oracle port) on 4 of them on the host for scale
+    from oracle import ransac as orr  # cpu_baseline leg only
+    from paper_2510_02080_b200 import geometry
+
+    rng = np.random.default_rng(99)
+    probs = []
+    for _ in range(64):
+        h = np.eye(3) + 0.05 * rng.normal(size=(3, 3))
+        h[2, :2] = rng.uniform(-3e-4, 3e-4, 2)
+        h[2, 2] = 1.0
+        src = rng.uniform(0, 640, size=(500, 2))
+        sh = np.concatenate([src, np.ones((500, 1))], axis=1) @ h.T
+        dst = sh[:, :2] / sh[:, 2:3] + 0.5 * rng.normal(size=(500, 2))
+        dst[200:] = rng.uniform(0, 640, size=(300, 2))
+        probs.append((src, dst))
+    seeds = list(range(64))
+    ms = _time_ms(lambda: geometry.estimate_homography_ransac_batch(probs, seeds=seeds), reps=3, warm=1)
+    t0 = time.perf_counter()
+    for (src, dst), sd in zip(probs[:4], seeds[:4]):
+        orr.estimate_homography_ransac(src, dst, seed=sd)
+    cpu_ms = (time.perf_counter() - t0) * 1e3 / 4
+    out["homography_ransac"] = {"problems": 64, "matches": 500, "iterations_scored": 64 * 1000, "ms": ms,
+                                "problems_per_s": 64 / (ms * 1e-3),
+                                "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "problems/s", "cores": 1, "kind": "port",
+                                                 "sample": "the reference loop on 4 of the 64 problems"}}
     return out
 
 
