@@ -104,8 +104,28 @@ def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
     from paper_2510_02080_b200 import mapping, synth
 
     cfg = synth.SceneConfig()
-    sb = synth.make_submaps(n_kf, cfg, seed=rank, device=device)
-    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8))
+    stub, send_pos = None, []
+    if world == 1:
+        sb = synth.make_submaps(n_kf, cfg, seed=rank, device=device)
+        dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8))
+    else:
+        # one sequence of n_kf x world keyframes (world x the laps, so every
+        # window has the N = 1 geometry), rank r decoding its contiguous
+        # window of flush batches; the first submap's shared keyframe comes
+        # from rank r-1 as a halo every step (dist.WindowChain)
+        from paper_2510_02080_b200 import dist as pdist
+
+        cfg = synth.SceneConfig(laps=cfg.laps * world)
+        batches = synth.flush_batches(n_kf * world)
+        lo, hi = pdist.shard_window(len(batches), world, rank)
+        send_pos, recv_ids = pdist.halo_handshake(batches[lo], batches[hi - 1])
+        sb = synth.make_submaps(n_kf * world, cfg, seed=0, device=device, batch_range=(lo, hi))
+        dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8) + len(recv_ids))
+        if recv_ids:  # stub slots first: a ChainPlan walks contiguous slots
+            n = len(recv_ids)
+            z = torch.zeros((n, cfg.height, cfg.width), dtype=torch.float32, device=device)
+            ident = np.tile(np.array([1.0, 1.0, 0, 0, 0, 0, 0, 0]), (n, 1))
+            stub = dm.add_submap(recv_ids, z, z, list(ident), -1)
     sms = []
     for j, ids in enumerate(sb.frame_ids):
         o = sb.slot_offsets[j]
@@ -116,13 +136,13 @@ def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
     A, B, a_off, b_off = synth.make_descriptor_pairs(n_frames, n_desc, n_desc, 256, 0.05, seed=100 + rank,
                                                      device=device)
     torch.cuda.synchronize()
-    return dm, sms, (A, B, a_off, b_off)
+    return dm, sms, (A, B, a_off, b_off), (stub, send_pos)
 
 
 class Step:
     """One pass of the hot path over the resident workload."""
 
-    def __init__(self, dm, sms, desc, cell=0.02):
+    def __init__(self, dm, sms, desc, cell=0.02, halo=(None, [])):
         import torch
 
         from paper_2510_02080_b200 import mapping, tracking
@@ -130,7 +150,14 @@ class Step:
         self.torch, self.mapping, self.tracking = torch, mapping, tracking
         self.dm, self.sms, self.desc, self.cell = dm, sms, desc, cell
         self.slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
-        self.plan = mapping.ChainPlan(sms)
+        self.chain = None
+        if torch.distributed.is_available() and torch.distributed.is_initialized() \
+                and torch.distributed.get_world_size() > 1:
+            from paper_2510_02080_b200 import dist as pdist
+            self.chain = pdist.WindowChain(dm, halo[0], sms, halo[1])
+            self.plan = self.chain.plan
+        else:
+            self.plan = mapping.ChainPlan(sms)
         self.pairs = self.plan.pairs
         self.seg = self.plan.seg
         self.vmap = None
@@ -162,7 +189,7 @@ class Step:
         self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8, self.norm_bound)
         ev["t_match"] = self._event()
         # registration of all edges (one launch) + device pose chain (one launch)
-        out = self.plan.run(self.dm.pool)
+        out = self.plan.run(self.dm.pool) if self.chain is None else self.chain.run()
         ev["t_reg"] = self._event()  # both launches: stage "reg" = registration + chain
         self.edge_status, self.sub_status = out[4], out[6]
         ev["t_chain"] = self._event()
@@ -288,8 +315,8 @@ def main():
     from paper_2510_02080_b200 import _lib
 
     L = _lib.lib()
-    dm, sms, desc = build_workload(rank, world, args.keyframes, args.desc, "cuda")
-    step = Step(dm, sms, desc)
+    dm, sms, desc, halo = build_workload(rank, world, args.keyframes, args.desc, "cuda")
+    step = Step(dm, sms, desc, halo=halo)
     for _ in range(args.warmup):
         step.run()
     torch.cuda.synchronize()
@@ -403,8 +430,9 @@ def main():
                        "l2": "inputs larger than L2 (pool %.0f MB, descriptors %.0f MB)" %
                              (dm.pool.nbytes() / 1e6, (A.numel() + B.numel()) * 2 / 1e6),
                        "parallelism": f"submap windows x{world}" + (
-                           ", global map partitioned by voxel key (one NCCL all-to-all of partials per step)"
-                           if world > 1 else ""),
+                           ": one sequence sharded by flush batches, shared-frame halo by P2P and an all-gather "
+                           "of window poses per step; global map partitioned by voxel key (one NCCL all-to-all "
+                           "of partials per step)" if world > 1 else ""),
                        "matcher_float64_rescans": rescans},
             "matches_per_s": n_pairs_scored * world / (ms * 1e-3), "matches_unit": "candidate descriptor pairs/s",
             "emitted_matches_per_s": n_matches * world / (ms * 1e-3),

@@ -133,6 +133,15 @@ EC3R_API int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_count
                               double* sub_globals, double* slot_globals, int32_t* sub_status,
                               void* stream);
 
+/* Sharded chain (SURVEY §8(e), row (a)+(b)): rank `rank` of `world` chained
+ * its window relative to the predecessor's halo submap; window_last (DEVICE,
+ * world x 8, all-gathered) holds every window's last-submap pose in its own
+ * frame.  Left-composes O = W_0 o ... o W_{rank-1} into sub_globals (n_sub x 8)
+ * and slot_globals (n_slots x 8) in place; offset_out (nullable, 8) gets O. */
+EC3R_API int ec3r_apply_window_offset(const double* window_last, int world, int rank, double* sub_globals,
+                                      int n_sub, double* slot_globals, int64_t n_slots, double* offset_out,
+                                      void* stream);
+
 /* ---------------------------------------------------------------------
  * K2+K3  batched weighted Umeyama on explicit correspondences
  * replaces align_point_sets (registration.py:38-102) / weighted_umeyama

@@ -684,3 +684,45 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
     tk.stop();
     return EC3R_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Sharded chain (dist.WindowChain): rank r's chain is computed relative to
+// its halo stub (the predecessor's last submap); the offset
+// O_r = W_0 o W_1 o ... o W_{r-1} (W_q = window q's last-submap pose in its
+// own frame, all-gathered) turns it into global poses.  Every thread
+// recomputes the (<= world-long) prefix and left-composes its globals.
+namespace ec3r {
+__global__ void window_offset_kernel(const double* __restrict__ window_last, int rank, double* __restrict__ sub_globals,
+                                     int n_sub, double* __restrict__ slot_globals, int64_t n_slots,
+                                     double* __restrict__ offset_out) {
+    double o[8] = {1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < rank; ++q) {
+        double t[8];
+        sim3_compose_dev(o, window_last + 8 * q, t);
+        for (int k = 0; k < 8; ++k) o[k] = t[k];
+    }
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && offset_out)
+        for (int k = 0; k < 8; ++k) offset_out[k] = o[k];
+    double* g = i < n_sub ? sub_globals + 8 * i : (i - n_sub < n_slots ? slot_globals + 8 * (i - n_sub) : nullptr);
+    if (!g) return;
+    double in[8], out[8];
+    for (int k = 0; k < 8; ++k) in[k] = g[k];
+    sim3_compose_dev(o, in, out);
+    for (int k = 0; k < 8; ++k) g[k] = out[k];
+}
+}  // namespace ec3r
+
+extern "C" int ec3r_apply_window_offset(const double* window_last, int world, int rank, double* sub_globals,
+                                        int n_sub, double* slot_globals, int64_t n_slots, double* offset_out,
+                                        void* stream) {
+    if (world < 1 || rank < 0 || rank >= world || n_sub < 0 || n_slots < 0) return EC3R_EARG;
+    if ((rank > 0 && !window_last) || (n_sub && !sub_globals) || (n_slots && !slot_globals)) return EC3R_EARG;
+    const int64_t n = (int64_t)n_sub + n_slots;
+    if (n == 0 && !offset_out) return EC3R_OK;
+    const int64_t blocks = (n + 127) / 128 > 0 ? (n + 127) / 128 : 1;
+    window_offset_kernel<<<(unsigned)blocks, 128, 0, as_stream(stream)>>>(window_last, rank, sub_globals, n_sub,
+                                                                        slot_globals, n_slots, offset_out);
+    EC3R_CHECK_LAUNCH("window_offset_kernel");
+    return EC3R_OK;
+}

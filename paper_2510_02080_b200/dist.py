@@ -346,3 +346,105 @@ def register_window(mapping, window: Sequence, group=None):
         sm.global_pose = off.compose(sm.global_pose)
         mapping._commit(sm)
     return off
+
+
+def halo_handshake(first_ids: Sequence[int], last_ids: Sequence[int], group=None):
+    """Agree on the halo once, before the pools are filled.  Rank r sends the
+    keyframe ids of its first submap back to rank r-1, which answers with the
+    ones its last submap holds.  Returns (send_pos, recv_ids): positions in
+    this rank's last submap to send forward each step, and the keyframe ids
+    of the frames arriving from the predecessor (empty on rank 0)."""
+    rank, world = _world(group)
+    if world == 1:
+        return [], []
+    dev = torch.device("cpu")
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    req = torch.full((HALO_MAX,), -1, dtype=torch.int64, device=dev)
+    ids = list(first_ids)[:HALO_MAX]
+    if ids:
+        req[: len(ids)] = torch.tensor(ids, dtype=torch.int64)
+    want = torch.full_like(req, -1)
+    shift([req], [want], step=-1, group=group)
+    send_pos = []
+    hdr = torch.full((HALO_MAX,), -1, dtype=torch.int64, device=dev)
+    if rank + 1 < world:
+        wanted = {int(x) for x in want.tolist() if x >= 0}
+        send_pos = [k for k, f in enumerate(last_ids) if int(f) in wanted][:HALO_MAX]
+        if send_pos:
+            hdr[: len(send_pos)] = torch.tensor([int(last_ids[k]) for k in send_pos], dtype=torch.int64)
+    got = torch.full_like(hdr, -1)
+    shift([hdr], [got], step=1, group=group)
+    recv_ids = [int(x) for x in got.tolist() if x >= 0] if rank > 0 else []
+    return send_pos, recv_ids
+
+
+class WindowChain:
+    """Device-resident sharded registration chain (ChainPlan over
+    [halo stub] + window) with the per-step exchange steps of SURVEY §8(e):
+
+    1. grouped isend / irecv of the halo frames (depth, confidence, local
+       pose) from rank r-1's last submap into this rank's stub slots;
+    2. registration of every edge + device pose chain (ChainPlan.run), the
+       stub fixed at identity;
+    3. all-gather of each window's last-submap pose (8 f64 per rank) and
+       ec3r_apply_window_offset, which left-composes the prefix offset into
+       the submap and slot globals.
+
+    No host synchronisation; with NCCL all transfers stay on the device."""
+
+    def __init__(self, dm, stub, window: Sequence, send_pos: Sequence[int], group=None):
+        from .mapping import ChainPlan
+
+        self.rank, self.world = _world(group)
+        self.group, self.dm, self.stub, self.window = group, dm, stub, list(window)
+        self.plan = ChainPlan(([stub] if stub is not None else []) + self.window, device=dm.pool.device)
+        pool = dm.pool
+        self.send_slots = [int(self.window[-1].slots[k]) for k in send_pos] if self.window else []
+        self.staged = self.world > 1 and _host_staged(group, pool.device)
+        self.last = torch.zeros(8, dtype=torch.float64, device=pool.device)
+        self.gathered = torch.zeros((max(self.world, 1), 8), dtype=torch.float64, device=pool.device)
+        self.offset = torch.zeros(8, dtype=torch.float64, device=pool.device)
+        self.n_slots = sum(len(sm.slots) for sm in self.plan.sms)
+
+    def _halo(self):
+        pool = self.dm.pool
+        send, recv = [], []
+        for s in self.send_slots:
+            send += [pool.depth[s:s + 1], pool.conf[s:s + 1], pool.poses[s:s + 1]]
+        if self.stub is not None:
+            s0, s1 = int(self.stub.slots[0]), int(self.stub.slots[-1]) + 1
+            recv = [t[s:s + 1] for s in range(s0, s1) for t in (pool.depth, pool.conf, pool.poses)]
+        if self.staged:
+            hs = [t.cpu() for t in send]
+            hr = [torch.empty_like(t, device="cpu") for t in recv]
+            shift(hs, hr, step=1, group=self.group)
+            for d, h in zip(recv, hr):
+                d.copy_(h)
+        else:
+            shift(send, recv, step=1, group=self.group)
+
+    def run(self, config=None, stream=None):
+        from . import _lib
+        from .mapping import MappingConfig
+
+        if self.world > 1:
+            self._halo()
+        out = self.plan.run(self.dm.pool, config or MappingConfig(), stream=stream)
+        sub_globals = out[5]
+        if self.world > 1:
+            self.last.copy_(sub_globals[-1])
+            if self.staged:
+                bufs = [torch.empty(8, dtype=torch.float64) for _ in range(self.world)]
+                dist.all_gather(bufs, self.last.cpu(), group=self.group)
+                self.gathered.copy_(torch.stack(bufs))
+            else:
+                dist.all_gather_into_tensor(self.gathered, self.last, group=self.group)
+            pool = self.dm.pool
+            slot_g = pool.globals[self.plan.slot0:]
+            n_slots = self.n_slots
+            _lib.check(_lib.lib().ec3r_apply_window_offset(_lib.ptr(self.gathered), self.world, self.rank,
+                                                           _lib.ptr(sub_globals), int(sub_globals.shape[0]),
+                                                           _lib.ptr(slot_g), n_slots, _lib.ptr(self.offset),
+                                                           _lib.stream_ptr(stream)), "ec3r_apply_window_offset")
+        return out

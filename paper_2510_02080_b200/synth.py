@@ -142,10 +142,14 @@ def flush_batches(n_keyframes: int, capacity: int = 5):
 
 
 def make_submaps(n_keyframes: int, cfg: SceneConfig = SceneConfig(), seed: int = 0, device="cuda",
-                 invalid_fraction: float = 0.0) -> SubmapBatch:
-    """Decoded submaps of a run of n_keyframes (synthetic decode, backend.py:228-281)."""
+                 invalid_fraction: float = 0.0, batch_range=None) -> SubmapBatch:
+    """Decoded submaps of a run of n_keyframes (synthetic decode, backend.py:228-281).
+    batch_range=(b0, b1) decodes only those flush batches of the run (a
+    rank's window of a sharded sequence); keyframe ids stay global."""
     Rw, tw = trajectory(n_keyframes, cfg, seed)
     batches = flush_batches(n_keyframes)
+    if batch_range is not None:
+        batches = batches[batch_range[0]:batch_range[1]]
     gen = torch.Generator(device=device)
     gen.manual_seed(1000 + seed)
     rng = np.random.default_rng(2000 + seed)

@@ -107,3 +107,76 @@ def test_register_window_two_ranks_equals_single_process():
             cnt[int(k)] = cnt.get(int(k), 0) + int(c)
     np.testing.assert_array_equal(keys, ref_map["keys"])
     assert sum(cnt.values()) == int(ref_map["count"].sum())
+
+
+def _chain_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_02080_b200 import dist as D
+        from paper_2510_02080_b200 import mapping, synth
+        torch.cuda.set_device(0)
+        cfg = synth.SceneConfig()
+        sb = synth.make_submaps(N_KF, cfg, seed=SEED, device="cuda")
+        S = len(sb.frame_ids)
+        lo, hi = D.shard_window(S, world, rank)
+        send_pos, recv_ids = D.halo_handshake(sb.frame_ids[lo], sb.frame_ids[hi - 1])
+        dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+        stub = None
+        if recv_ids:  # zero planes: the halo must fill them
+            z = torch.zeros((len(recv_ids), cfg.height, cfg.width), dtype=torch.float32, device="cuda")
+            stub = dm.add_submap(recv_ids, z, z, [np.array([1.0, 1, 0, 0, 0, 0, 0, 0])] * len(recv_ids))
+        sms = []
+        for i in range(lo, hi):
+            ids, o = sb.frame_ids[i], sb.slot_offsets[i]
+            sms.append(dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)],
+                                     list(sb.poses8[o:o + len(ids)])))
+        wc = D.WindowChain(dm, stub, sms, send_pos)
+        for _ in range(2):  # repeated steps give the same poses
+            out = wc.run()
+        torch.cuda.synchronize()
+        sub_g = out[5].cpu().numpy()[(1 if stub is not None else 0):]
+        slot_g = dm.pool.globals[int(sms[0].slots[0]):int(sms[-1].slots[-1]) + 1].cpu().numpy()
+        q.put((rank, (lo, hi, sub_g, slot_g, [len(sm.slots) for sm in sms], (out[6].cpu().numpy() == 0).sum())))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_window_chain_device_two_ranks_equals_single_chain():
+    """The bench's N > 1 registration step (dist.WindowChain: halo P2P,
+    ChainPlan, all-gather of window poses, ec3r_apply_window_offset) on two
+    ranks equals the single-process device chain over the whole sequence."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, v = q.get(timeout=240)
+        out[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    for v in out.values():
+        if isinstance(v, Exception):
+            raise v
+    from oracle import ref_numpy as ref
+    from paper_2510_02080_b200 import mapping
+    dm, sms, S = _build()
+    full = mapping.ChainPlan(sms).run(dm.pool)[5].cpu().numpy()
+    for r in range(world):
+        lo, hi, sub_g, slot_g, lens, n_ok = out[r]
+        assert n_ok >= hi - lo - (1 if r == 0 else 0)
+        for j in range(lo, hi):
+            a, b = sub_g[j - lo], full[j]
+            assert abs(a[0] - b[0]) <= 1e-9 * b[0]
+            np.testing.assert_allclose(ref.canonical_quat(a[1:5]), ref.canonical_quat(b[1:5]), atol=1e-9)
+            np.testing.assert_allclose(a[5:], b[5:], atol=1e-9 * max(1.0, float(np.abs(b[5:]).max())))
+        np.testing.assert_array_equal(slot_g, np.repeat(sub_g, lens, axis=0))

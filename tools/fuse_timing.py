@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--keyframes", type=int, default=300)
     args = ap.parse_args()
-    dm, sms, desc = bench.build_workload(0, 1, args.keyframes, 1024, "cuda")
+    dm, sms, desc, _ = bench.build_workload(0, 1, args.keyframes, 1024, "cuda")
     slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
     plan = mapping.ChainPlan(sms)
     plan.run(dm.pool)
