@@ -470,7 +470,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         int tb = 0;  // colbuf double buffer (alternates over all tiles of the CTA)
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             const TcUnit un = p.units[u];
-            const int64_t a1 = p.a_off[un.pair + 1], a0 = p.a_off[un.pair];
+            const int64_t a1 = p.a_off[un.pair + 1];
             const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
             const int M = (int)(b1 - b0);
             const int n_tiles = (un.col1 - un.col0) / TC_BN;
