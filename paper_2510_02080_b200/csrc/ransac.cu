@@ -69,8 +69,10 @@ __device__ __forceinline__ uint32_t pcg_next32(Pcg64& g) {
     return (uint32_t)n;
 }
 
-// random_bounded_uint64(off=0, rng=r, use_masked=false) for r < 2^32: Lemire
-__device__ __forceinline__ uint32_t pcg_bounded(Pcg64& g, uint32_t r) {
+// random_bounded_uint64(off=0, rng=r, use_masked=false) for r < 2^32: Lemire.
+// `extra` is set when a rejection drew another 32-bit word (probability
+// < (r+1) / 2^32 per call).
+__device__ __forceinline__ uint32_t pcg_bounded(Pcg64& g, uint32_t r, bool& extra) {
     if (r == 0) return 0;
     if (r == 0xFFFFFFFFu) return pcg_next32(g);
     const uint32_t ex = r + 1;
@@ -79,6 +81,7 @@ __device__ __forceinline__ uint32_t pcg_bounded(Pcg64& g, uint32_t r) {
     if (left < ex) {
         const uint32_t thr = (0xFFFFFFFFu - r) % ex;
         while (left < thr) {
+            extra = true;
             m = (uint64_t)pcg_next32(g) * ex;
             left = (uint32_t)m;
         }
@@ -86,36 +89,115 @@ __device__ __forceinline__ uint32_t pcg_bounded(Pcg64& g, uint32_t r) {
     return (uint32_t)(m >> 32);
 }
 
-__global__ void hg_draw_kernel(const int64_t* __restrict__ off, int P, const uint64_t* __restrict__ state, int iters,
-                               int32_t* __restrict__ samples) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const int64_t n = off[p + 1] - off[p];
-    int32_t* out = samples + (size_t)p * iters * 4;
-    if (n < 4) return;
-    Pcg64 g;
-    const uint64_t* st = state + 6 * (size_t)p;
+// LCG jump-ahead (state after k steps) in O(log k) 128-bit multiplies
+__device__ __forceinline__ unsigned __int128 pcg_advance(unsigned __int128 s, unsigned __int128 inc, uint64_t k) {
+    unsigned __int128 cur_m = ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    unsigned __int128 cur_p = inc, acc_m = 1, acc_p = 0;
+    while (k) {
+        if (k & 1) {
+            acc_m *= cur_m;
+            acc_p = acc_p * cur_m + cur_p;
+        }
+        cur_p = (cur_m + 1) * cur_p;
+        cur_m *= cur_m;
+        k >>= 1;
+    }
+    return acc_m * s + acc_p;
+}
+
+// one Generator.choice(n, 4, replace=False) draw (Floyd + shuffle), in
+// registers only
+__device__ __forceinline__ int4 choice4(Pcg64& g, uint32_t j0, bool& extra) {
+    uint32_t i0 = pcg_bounded(g, j0, extra);
+    uint32_t i1 = pcg_bounded(g, j0 + 1, extra);
+    i1 = (i1 == i0) ? j0 + 1 : i1;
+    uint32_t i2 = pcg_bounded(g, j0 + 2, extra);
+    i2 = (i2 == i0 || i2 == i1) ? j0 + 2 : i2;
+    uint32_t i3 = pcg_bounded(g, j0 + 3, extra);
+    i3 = (i3 == i0 || i3 == i1 || i3 == i2) ? j0 + 3 : i3;
+    {  // _shuffle_int(4, 1, idx): i = 3, 2, 1 swaps idx[i] with idx[bounded(i)]
+        const uint32_t r = pcg_bounded(g, 3u, extra), t = i3;
+        i3 = r == 0 ? i0 : r == 1 ? i1 : r == 2 ? i2 : i3;
+        i0 = r == 0 ? t : i0;
+        i1 = r == 1 ? t : i1;
+        i2 = r == 2 ? t : i2;
+    }
+    {
+        const uint32_t r = pcg_bounded(g, 2u, extra), t = i2;
+        i2 = r == 0 ? i0 : r == 1 ? i1 : i2;
+        i0 = r == 0 ? t : i0;
+        i1 = r == 1 ? t : i1;
+    }
+    {
+        const uint32_t r = pcg_bounded(g, 1u, extra), t = i1;
+        i1 = r == 0 ? i0 : i1;
+        i0 = r == 0 ? t : i0;
+    }
+    return make_int4((int)i0, (int)i1, (int)i2, (int)i3);
+}
+
+__device__ __forceinline__ void load_pcg(const uint64_t* st, Pcg64& g) {
     g.s = ((unsigned __int128)st[0] << 64) | st[1];
     g.inc = ((unsigned __int128)st[2] << 64) | st[3];
     g.has32 = (int)st[4];
     g.u32 = (uint32_t)st[5];
-    for (int it = 0; it < iters; ++it) {
-        uint32_t idx[4];
-        for (int k = 0; k < 4; ++k) {  // Floyd: j = n-4 .. n-1
-            const uint32_t j = (uint32_t)(n - 4 + k);
-            uint32_t v = pcg_bounded(g, j);
-            for (int q = 0; q < k; ++q)
-                if (idx[q] == v) v = j;
-            idx[k] = v;
-        }
-        for (int i = 3; i > 0; --i) {  // _shuffle_int(4, 1, idx)
-            const uint32_t jj = pcg_bounded(g, (uint32_t)i);
-            const uint32_t t = idx[i];
-            idx[i] = idx[jj];
-            idx[jj] = t;
-        }
-        for (int k = 0; k < 4; ++k) out[4 * it + k] = (int32_t)idx[k];
+}
+
+// Parallel replay.  Without rejections every draw consumes exactly seven
+// 32-bit words (4 Floyd + 3 shuffle; six when n == 4), so iteration `it`
+// starts at word 7 it of the stream: thread t jumps the LCG to its first word and replays its
+// iterations.  A thread that meets a rejection flags the problem, which the
+// serial kernel below then redoes from the start.
+constexpr int HG_DRAW_NT = 64;
+
+__global__ void __launch_bounds__(HG_DRAW_NT) hg_draw_par_kernel(const int64_t* __restrict__ off, int iters,
+                                                                 const uint64_t* __restrict__ state,
+                                                                 int32_t* __restrict__ samples,
+                                                                 int32_t* __restrict__ redo) {
+    const int p = blockIdx.x;
+    const int64_t n = off[p + 1] - off[p];
+    if (threadIdx.x == 0) redo[p] = 0;
+    if (n < 4) return;
+    Pcg64 g;
+    load_pcg(state + 6 * (size_t)p, g);
+    __shared__ int flag;
+    if (threadIdx.x == 0) flag = g.has32 ? 1 : 0;  // a buffered word shifts the stream: serial
+    __syncthreads();
+    if (flag) {
+        if (threadIdx.x == 0) redo[p] = 1;
+        return;
     }
+    const int per = (iters + HG_DRAW_NT - 1) / HG_DRAW_NT;
+    const int it0 = threadIdx.x * per, it1 = min(iters, it0 + per);
+    bool extra = false;
+    if (it0 < it1) {
+        // bounded(0) draws nothing: with n == 4 a draw takes six words
+        const uint64_t w = (n == 4 ? 6ull : 7ull) * (uint64_t)it0;  // first 32-bit word
+        g.s = pcg_advance(g.s, g.inc, w >> 1);     // outputs before the word's
+        g.has32 = 0;
+        if (w & 1) (void)pcg_next32(g);            // odd word: the high half of the next output
+        const uint32_t j0 = (uint32_t)(n - 4);
+        int4* out = reinterpret_cast<int4*>(samples + (size_t)p * iters * 4);
+        for (int it = it0; it < it1; ++it) out[it] = choice4(g, j0, extra);
+    }
+    if (extra) atomicOr(&flag, 1);
+    __syncthreads();
+    if (threadIdx.x == 0 && flag) redo[p] = 1;
+}
+
+// serial replay for flagged problems (rejections or a buffered word)
+__global__ void hg_draw_serial_kernel(const int64_t* __restrict__ off, int P, const uint64_t* __restrict__ state,
+                                      int iters, const int32_t* __restrict__ redo, int32_t* __restrict__ samples) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P || !redo[p]) return;
+    const int64_t n = off[p + 1] - off[p];
+    if (n < 4) return;
+    Pcg64 g;
+    load_pcg(state + 6 * (size_t)p, g);
+    const uint32_t j0 = (uint32_t)(n - 4);
+    bool extra = false;
+    int4* out = reinterpret_cast<int4*>(samples + (size_t)p * iters * 4);
+    for (int it = 0; it < iters; ++it) out[it] = choice4(g, j0, extra);
 }
 
 // ---------------------------------------------------------------------------
@@ -320,9 +402,38 @@ __device__ __forceinline__ bool is_inlier(const double* h, const double* hi, con
     return __dsqrt_rn(xm(0.5, xa(d1, d2))) < thr;
 }
 
+// Fast path of is_inlier: one reciprocal per transfer instead of two
+// divisions and no square root.  x = 0.5 (d1 + d2) is within
+// 2e-14 M^2 of the exact value (M = the largest coordinate involved), and
+// sqrt_rn(x) < thr is decided by x against thr^2 outside a band of
+// 1e-13 M^2 + 1e-14 thr^2; inside the band the exact numpy-order test runs.
+__device__ __forceinline__ void transfer_fast(const double* m, double x, double y, double& ox, double& oy) {
+    const double px = xa(xa(xm(x, m[0]), xm(y, m[1])), m[2]);
+    const double py = xa(xa(xm(x, m[3]), xm(y, m[4])), m[5]);
+    const double w = xa(xa(xm(x, m[6]), xm(y, m[7])), m[8]);
+    const bool bad = fabs(w) < 1e-12;
+    const double r = __drcp_rn(bad ? 1.0 : w);
+    ox = bad ? 1e9 : px * r;
+    oy = bad ? 1e9 : py * r;
+}
+
+__device__ __forceinline__ bool is_inlier_fast(const double* h, const double* hi, const double* s, const double* d,
+                                               double thr, double thr2, double cmax) {
+    double ax, ay, bx, by;
+    transfer_fast(h, s[0], s[1], ax, ay);
+    transfer_fast(hi, d[0], d[1], bx, by);
+    const double e0 = ax - d[0], e1 = ay - d[1], f0 = bx - s[0], f1 = by - s[1];
+    const double x = 0.5 * ((e0 * e0 + e1 * e1) + (f0 * f0 + f1 * f1));
+    const double m = fmax(fmax(fmax(fabs(ax), fabs(ay)), fmax(fabs(bx), fabs(by))), cmax);
+    const double band = 1e-13 * m * m + 1e-14 * thr2;
+    if (x < thr2 - band) return true;
+    if (x > thr2 + band) return false;
+    return is_inlier(h, hi, s, d, thr);
+}
+
 __global__ void hg_count_kernel(const double* __restrict__ src, const double* __restrict__ dst,
                                 const int64_t* __restrict__ off, int P, int iters, const double* __restrict__ hyps,
-                                double thr, int32_t* __restrict__ counts) {
+                                const double* __restrict__ cmax_p, double thr, int32_t* __restrict__ counts) {
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= (int64_t)P * iters) return;
@@ -339,8 +450,10 @@ __global__ void hg_count_kernel(const double* __restrict__ src, const double* __
         hi[j] = hy[10 + j];
     }
     const int64_t o = off[p], n = off[p + 1] - o;
+    const double cmax = cmax_p[p], thr2 = thr * thr;
     int c = 0;
-    for (int64_t i = lane; i < n; i += 32) c += is_inlier(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr) ? 1 : 0;
+    for (int64_t i = lane; i < n; i += 32)
+        c += is_inlier_fast(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr, thr2, cmax) ? 1 : 0;
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
     if (lane == 0) counts[w] = c;
@@ -401,7 +514,8 @@ __device__ __forceinline__ double hg_sum(double x, double* red) {
 
 __global__ void __launch_bounds__(HG_REFIT_THREADS)
 hg_refit_kernel(const double* __restrict__ src, const double* __restrict__ dst, const int64_t* __restrict__ off,
-                int iters, const double* __restrict__ hyps, const int32_t* __restrict__ best, double thr,
+                int iters, const double* __restrict__ hyps, const int32_t* __restrict__ best,
+                const double* __restrict__ cmax, double thr,
                 double* __restrict__ out_model, uint8_t* __restrict__ out_mask, int32_t* __restrict__ out_count) {
     const int p = blockIdx.x;
     const int64_t o = off[p], n = off[p + 1] - o;
@@ -425,7 +539,7 @@ hg_refit_kernel(const double* __restrict__ src, const double* __restrict__ dst, 
     }
     double c0 = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const bool in = is_inlier(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr);
+        const bool in = is_inlier_fast(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr, thr * thr, cmax[p]);
         mask[i] = in ? 1 : 0;
         c0 += in ? 1.0 : 0.0;
     }
@@ -474,11 +588,23 @@ hg_refit_kernel(const double* __restrict__ src, const double* __restrict__ dst, 
 #pragma unroll
                 for (int c = a; c < 9; ++c) g[k++] += r0[a] * r0[c] + r1[a] * r1[c];
         }
+    // the 45 sums: warp shuffles, then one pass over the warps' partials
+    __shared__ double gw[HG_REFIT_THREADS / 32][45];
     __shared__ double gs[45];
+#pragma unroll
     for (int k = 0; k < 45; ++k) {
-        const double t = hg_sum<HG_REFIT_THREADS>(g[k], &red);
-        if (threadIdx.x == 0) gs[k] = t;
+        double t = g[k];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o2);
+        if ((threadIdx.x & 31) == 0) gw[threadIdx.x >> 5][k] = t;
     }
+    __syncthreads();
+    if (threadIdx.x < 45) {
+        double t = 0.0;
+        for (int w = 0; w < HG_REFIT_THREADS / 32; ++w) t += gw[w][threadIdx.x];
+        gs[threadIdx.x] = t;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         double A[9][9], V[9][9];
         int k = 0;
@@ -516,13 +642,33 @@ hg_refit_kernel(const double* __restrict__ src, const double* __restrict__ dst, 
         hi[j] = hsh[9 + j];
     }
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        c2 += is_inlier(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr) ? 1.0 : 0.0;
+        c2 += is_inlier_fast(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr, thr * thr, cmax[p]) ? 1.0 : 0.0;
     const int count2 = (int)hg_sum<HG_REFIT_THREADS>(c2, &red);
     if (count2 < best_count) return;  // keep the minimal hypothesis (:637)
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        mask[i] = is_inlier(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr) ? 1 : 0;
+        mask[i] = is_inlier_fast(h, hi, src + 2 * (o + i), dst + 2 * (o + i), thr, thr * thr, cmax[p]) ? 1 : 0;
     if (threadIdx.x < 9) model[threadIdx.x] = h[threadIdx.x];
     if (threadIdx.x == 0) out_count[p] = count2;
+}
+
+// per problem: the largest |coordinate| of its matches (the fast path's
+// error scale)
+__global__ void hg_cmax_kernel(const double* __restrict__ src, const double* __restrict__ dst,
+                               const int64_t* __restrict__ off, double* __restrict__ cmax) {
+    const int p = blockIdx.x;
+    const int64_t o = off[p], n = off[p + 1] - o;
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < 2 * n; i += blockDim.x)
+        m = fmax(m, fmax(fabs(src[2 * o + i]), fabs(dst[2 * o + i])));
+    for (int s = 16; s > 0; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+    __shared__ double wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+        m = fmax(m, wm[0]);
+        cmax[p] = m;
+    }
 }
 
 static size_t hg_hyp_bytes(int P, int iters) { return align256(sizeof(double) * HYP_STRIDE * (size_t)P * iters); }
@@ -532,9 +678,12 @@ static size_t hg_sample_bytes(int P, int iters) { return align256(sizeof(int32_t
 
 using namespace ec3r;
 
+static size_t hg_cmax_bytes(int P) { return align256(sizeof(double) * (size_t)P); }
+
 extern "C" size_t ec3r_homography_workspace(int n_problems, int iters) {
     if (n_problems <= 0 || iters <= 0) return 256;
-    return hg_hyp_bytes(n_problems, iters) + hg_sample_bytes(n_problems, iters);
+    return hg_hyp_bytes(n_problems, iters) + hg_sample_bytes(n_problems, iters) + hg_cmax_bytes(n_problems) +
+           align256(sizeof(int32_t) * (size_t)n_problems);
 }
 
 extern "C" int ec3r_homography_ransac_score(const double* src, const double* dst, const int64_t* offsets,
@@ -548,13 +697,21 @@ extern "C" int ec3r_homography_ransac_score(const double* src, const double* dst
     cudaStream_t st = as_stream(stream);
     double* hyps = (double*)workspace;
     int32_t* samples = out_samples ? out_samples : (int32_t*)((char*)workspace + hg_hyp_bytes(n_problems, iters));
-    hg_draw_kernel<<<(n_problems + 63) / 64, 64, 0, st>>>(offsets, n_problems, rng_state, iters, samples);
-    EC3R_CHECK_LAUNCH("hg_draw_kernel");
+    int32_t* redo = (int32_t*)((char*)workspace + hg_hyp_bytes(n_problems, iters) +
+                               hg_sample_bytes(n_problems, iters) + hg_cmax_bytes(n_problems));
+    hg_draw_par_kernel<<<n_problems, HG_DRAW_NT, 0, st>>>(offsets, iters, rng_state, samples, redo);
+    EC3R_CHECK_LAUNCH("hg_draw_par_kernel");
+    hg_draw_serial_kernel<<<(n_problems + 63) / 64, 64, 0, st>>>(offsets, n_problems, rng_state, iters, redo,
+                                                                 samples);
+    EC3R_CHECK_LAUNCH("hg_draw_serial_kernel");
     const int64_t nh = (int64_t)n_problems * iters;
     hg_hyp_kernel<<<(unsigned)((nh + 127) / 128), 128, 0, st>>>(src, dst, offsets, n_problems, iters, samples, hyps);
     EC3R_CHECK_LAUNCH("hg_hyp_kernel");
+    double* cmax = (double*)((char*)workspace + hg_hyp_bytes(n_problems, iters) + hg_sample_bytes(n_problems, iters));
+    hg_cmax_kernel<<<n_problems, 256, 0, st>>>(src, dst, offsets, cmax);
+    EC3R_CHECK_LAUNCH("hg_cmax_kernel");
     hg_count_kernel<<<(unsigned)((nh * 32 + 255) / 256), 256, 0, st>>>(src, dst, offsets, n_problems, iters, hyps,
-                                                                       pixel_threshold, out_counts);
+                                                                       cmax, pixel_threshold, out_counts);
     EC3R_CHECK_LAUNCH("hg_count_kernel");
     return EC3R_OK;
 }
@@ -567,8 +724,11 @@ extern "C" int ec3r_homography_ransac_refit(const double* src, const double* dst
     if (n_problems == 0) return EC3R_OK;
     if (!src || !dst || !offsets || !best || !out_model || !out_mask || !out_count) return EC3R_EARG;
     if (!workspace || workspace_bytes < ec3r_homography_workspace(n_problems, iters)) return EC3R_EWORKSPACE;
+    const double* cmax =
+        (const double*)((const char*)workspace + hg_hyp_bytes(n_problems, iters) + hg_sample_bytes(n_problems, iters));
     hg_refit_kernel<<<n_problems, HG_REFIT_THREADS, 0, as_stream(stream)>>>(
-        src, dst, offsets, iters, (const double*)workspace, best, pixel_threshold, out_model, out_mask, out_count);
+        src, dst, offsets, iters, (const double*)workspace, best, cmax, pixel_threshold, out_model, out_mask,
+        out_count);
     EC3R_CHECK_LAUNCH("hg_refit_kernel");
     return EC3R_OK;
 }

@@ -15,6 +15,7 @@ There is no CPU fallback.
 
 from __future__ import annotations
 
+import functools
 import math
 from typing import Optional, Sequence
 
@@ -25,28 +26,35 @@ from . import _lib
 from .types import RansacConfig, RansacResult, TooFewCorrespondences
 
 
+@functools.lru_cache(maxsize=4096)
+def _pcg_state_cached(seed: int) -> tuple:
+    return tuple(int(x) for x in _pcg_state(seed))
+
+
 def pcg_state(seed) -> np.ndarray:
     """numpy PCG64 state of default_rng(seed) as 6 uint64 (state hi/lo, inc
-    hi/lo, has_uint32, uinteger) — the stream K9 replays."""
+    hi/lo, has_uint32, uinteger) — the stream K9 replays.  Integer seeds are
+    cached (SeedSequence hashing costs ~20 us per generator)."""
+    if isinstance(seed, (int, np.integer)):
+        return np.array(_pcg_state_cached(int(seed)), np.uint64)
+    return _pcg_state(seed)
+
+
+def _pcg_state(seed) -> np.ndarray:
     st = np.random.default_rng(seed).bit_generator.state
     s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
     m = (1 << 64) - 1
     return np.array([s >> 64, s & m, inc >> 64, inc & m, int(st["has_uint32"]), int(st["uinteger"])], np.uint64)
 
 
-def walk_counts(counts: np.ndarray, n: int, cfg: RansacConfig) -> int:
-    """The reference's sequential RANSAC loop (geometry.py:607-625) over the
-    per-iteration inlier counts (-1 = skipped).  Returns the 0-based
-    iteration whose hypothesis wins, or -1."""
-    counts = np.asarray(counts)
-    prev = np.concatenate([[0], np.maximum.accumulate(np.maximum(counts, 0))[:-1]])
-    best, best_i, max_iters = 0, -1, int(cfg.max_iterations)
-    for i in np.flatnonzero(counts > prev):
+def _walk(improvements, counts_row, n: int, cfg: RansacConfig) -> int:
+    best_i, max_iters = -1, int(cfg.max_iterations)
+    for i in improvements:
         it = int(i) + 1
         if it > max_iters:
             break
-        c = int(counts[i])
-        best, best_i = c, int(i)
+        c = int(counts_row[i])
+        best_i = int(i)
         if c > 4:
             w = c / n
             denom = math.log(max(1e-12, 1.0 - w ** 4))
@@ -54,6 +62,31 @@ def walk_counts(counts: np.ndarray, n: int, cfg: RansacConfig) -> int:
                 needed = math.log(max(1e-300, 1.0 - cfg.confidence)) / denom
                 max_iters = min(cfg.max_iterations, max(it, int(math.ceil(needed))))
     return best_i
+
+
+def _improvements(counts: np.ndarray) -> np.ndarray:
+    """Mask of iterations whose count beats every earlier one (and 0): the
+    only places the reference's loop changes state."""
+    c = np.maximum(counts, 0)
+    prev = np.zeros_like(c)
+    prev[..., 1:] = np.maximum.accumulate(c, axis=-1)[..., :-1]
+    return counts > prev
+
+
+def walk_counts(counts: np.ndarray, n: int, cfg: RansacConfig) -> int:
+    """The reference's sequential RANSAC loop (geometry.py:607-625) over the
+    per-iteration inlier counts (-1 = skipped).  Returns the 0-based
+    iteration whose hypothesis wins, or -1."""
+    counts = np.asarray(counts)
+    return _walk(np.flatnonzero(_improvements(counts)), counts, n, cfg)
+
+
+def walk_counts_batch(counts: np.ndarray, ns, cfg: RansacConfig) -> np.ndarray:
+    """walk_counts for every row of a (P, iters) count matrix."""
+    rows, cols = np.nonzero(_improvements(counts))
+    starts = np.searchsorted(rows, np.arange(len(ns) + 1))
+    return np.array([_walk(cols[starts[p]:starts[p + 1]], counts[p], int(ns[p]), cfg) for p in range(len(ns))],
+                    np.int32)
 
 
 def estimate_homography_ransac_batch(problems: Sequence, cfg: RansacConfig = RansacConfig(),
@@ -97,7 +130,7 @@ def estimate_homography_ransac_batch(problems: Sequence, cfg: RansacConfig = Ran
                                               float(cfg.pixel_threshold), _lib.ptr(counts), _lib.ptr(samples),
                                               _lib.ptr(ws), ws.numel(), st), "ec3r_homography_ransac_score")
     counts_h = counts.cpu().numpy()
-    best = np.array([walk_counts(counts_h[p, :iters], int(ns[p]), cfg) for p in range(P)], np.int32)
+    best = walk_counts_batch(counts_h[:, :iters], ns, cfg)
     best_d = h2d(best)
     model = torch.empty((P, 9), dtype=torch.float64, device=dev)
     mask = torch.empty(int(off_h[-1]), dtype=torch.uint8, device=dev)

@@ -793,7 +793,7 @@ def test_homography_ransac_hypothesis_order_and_counts(golden):
     from paper_2510_02080_b200 import geometry
     from paper_2510_02080_b200.types import RansacConfig
     g = golden("ransac")
-    for i in (0, 21, 31, 35, 37):
+    for i in (0, 21, 27, 28, 31, 35, 37):
         c = g[f"c{i}_cfg"]
         cfg = RansacConfig(pixel_threshold=float(c[0]), confidence=float(c[1]), max_iterations=int(c[2]),
                            seed=int(c[3]))
@@ -804,6 +804,25 @@ def test_homography_ransac_hypothesis_order_and_counts(golden):
         np.testing.assert_array_equal(samples[0], draws, err_msg=f"case {i}")
         np.testing.assert_array_equal(counts[0], orr.hypotheses(src, dst, cfg.pixel_threshold, cfg.max_iterations,
                                                                 cfg.seed), err_msg=f"case {i}")
+
+
+def test_homography_ransac_draws_large_n_with_rejections():
+    """n = 70,000 matches, 2,000 iterations, 16 seeds: Lemire rejections occur
+    (p ~ n / 2^32 per draw) and shift the word stream; the device falls back
+    to the serial replay for those problems.  Every draw equals rng.choice."""
+    from paper_2510_02080_b200 import geometry
+    from paper_2510_02080_b200.types import RansacConfig
+    n, iters = 70000, 2000
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(0, 640, size=(n, 2))
+    probs = [(pts, pts + 1.0)] * 16
+    cfg = RansacConfig(max_iterations=iters)
+    _, _, samples = geometry.estimate_homography_ransac_batch(probs, cfg, seeds=list(range(16)),
+                                                              return_samples=True)
+    for sd in range(16):
+        r = np.random.default_rng(sd)
+        np.testing.assert_array_equal(samples[sd], np.stack([r.choice(n, size=4, replace=False)
+                                                             for _ in range(iters)]), err_msg=f"seed {sd}")
 
 
 def test_homography_ransac_random_batch_vs_oracle():

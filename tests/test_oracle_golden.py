@@ -202,3 +202,16 @@ def test_ransac_host_walk_reproduces_sequential_loop(golden):
         assert int(best.sum()) == counts[b]
         # the reference's final mask is the refit's when it keeps at least as many
         assert g[f"c{i}_mask"].sum() >= best.sum()
+
+
+def test_ransac_batched_walk_equals_per_row_walk():
+    from paper_2510_02080_b200.geometry import walk_counts, walk_counts_batch
+    from paper_2510_02080_b200.types import RansacConfig
+    rng = np.random.default_rng(3)
+    counts = rng.integers(-1, 60, size=(40, 300))
+    counts[5] = -1
+    counts[7, :] = 0
+    ns = rng.integers(60, 200, size=40)
+    cfg = RansacConfig(max_iterations=300)
+    np.testing.assert_array_equal(walk_counts_batch(counts, ns, cfg),
+                                  [walk_counts(counts[p], int(ns[p]), cfg) for p in range(40)])
