@@ -275,7 +275,10 @@ __device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s
     for_each_pixel4_seg(a, s0, s1, rank, [](int, int) {}, f);
 }
 
-__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT, 2)
+#ifndef EC3R_RE_MINB
+#define EC3R_RE_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT, EC3R_RE_MINB)
 register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restrict__ out_rms,
                       int64_t* __restrict__ out_count, int64_t* __restrict__ out_npairs,
                       int32_t* __restrict__ out_status, uint8_t* __restrict__ keep_masks) {
