@@ -335,6 +335,11 @@ __global__ void vh_frame_tables_kernel(FuseArgs a, float4* __restrict__ ftab) {
 constexpr int ST_H = 8, ST_W = 16;
 constexpr int BC_BITS = 11;  // shared-memory block cache: 2048 entries (16 KB)
 
+#ifndef EC3R_FI_G
+#define EC3R_FI_G 1  // consecutive listed frames per CTA (same band): the block cache carries over
+#endif
+constexpr int FI_G = EC3R_FI_G;
+
 __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
     extern __shared__ float4 sA[];  // A[W]
     __shared__ float4 sB[FI_ROWS];
@@ -342,29 +347,34 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
     const int W = a.W, H = a.H;
     const int HW = H * W;
-    const int j = blockIdx.y;
-    const int slot = a.slots[j];
     const int v_band = blockIdx.x * FI_ROWS;
     const int rows = min(FI_ROWS, H - v_band);
-    const float4* tab = a.ftab + (size_t)j * (W + H + 1);
-    for (int u = threadIdx.x; u < W; u += FI_NT) sA[u] = __ldg(tab + u);
-    if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
     if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
     for (int i = threadIdx.x; i < (1 << BC_BITS); i += FI_NT) bcache[i] = 0ull;
-    const float4 Tm = __ldg(tab + W + H);
-    // cache keys are block coordinates relative to the camera centre's block
-    const int3 ob = make_int3((int)floorf(Tm.x * a.inv_cell_f * 0.25f), (int)floorf(Tm.y * a.inv_cell_f * 0.25f),
-                              (int)floorf(Tm.z * a.inv_cell_f * 0.25f));
-    __syncthreads();
-
+    // cache keys are block coordinates relative to the first frame's camera block
+    int3 ob;
+    {
+        const float4 T0 = __ldg(a.ftab + (size_t)(blockIdx.y * FI_G) * (W + H + 1) + W + H);
+        ob = make_int3((int)floorf(T0.x * a.inv_cell_f * 0.25f), (int)floorf(T0.y * a.inv_cell_f * 0.25f),
+                       (int)floorf(T0.z * a.inv_cell_f * 0.25f));
+    }
     const float inv = a.inv_cell_f, cellf = a.cell_f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int dv = lane >> 2, du = 4 * (lane & 3);
     const int stx = (W + ST_W - 1) / ST_W;
     const bool pairs = (W & 1) == 0;
+    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
+    const int j_end = min(a.n, (int)(blockIdx.y + 1) * FI_G);
+    for (int j = blockIdx.y * FI_G; j < j_end; ++j) {
+    const int slot = a.slots[j];
+    const float4* tab = a.ftab + (size_t)j * (W + H + 1);
+    __syncthreads();  // the previous frame's tables are no longer read
+    for (int u = threadIdx.x; u < W; u += FI_NT) sA[u] = __ldg(tab + u);
+    if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
+    const float4 Tm = __ldg(tab + W + H);
+    __syncthreads();
     const float* dbase = a.depth + (size_t)slot * HW;
     const float* cbase = a.conf + (size_t)slot * HW;
-    unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
 
     // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
     auto advance = [&](int& sy, int& sx) {
@@ -540,6 +550,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             }
         }
     }
+    }  // frames of this CTA
     // counters: warp reduce then one shared atomic per warp, one global per CTA
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -988,7 +999,7 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     if (smem > 48 * 1024)
         EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
-    const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, n);
+    const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, (n + FI_G - 1) / FI_G);
     KernelTimer tk(TK_FUSE_INSERT, st);
     vh_insert_frames_kernel<<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
