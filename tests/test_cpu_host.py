@@ -38,6 +38,26 @@ def test_workspace_queries_without_gpu():
     off = np.array([0, 1024], np.int64)
     assert L.ec3r_match_workspace(off.ctypes.data, off.ctypes.data, 1) > 0
     assert L.ec3r_retrieval_workspace(1500, 5, 1 << 16) > 0
+    assert L.ec3r_homography_workspace(64, 1000) >= 64 * 1000 * (19 * 8 + 16)
+    assert L.ec3r_local_candidates_workspace(7) > 0
+    assert L.ec3r_nn_workspace(1000, 1000) > 0
+
+
+def test_argument_errors_without_gpu():
+    """Argument checks run before any CUDA call: the error codes the host
+    mirror turns into exceptions (INTEGRATION.md error column)."""
+    from paper_2510_02080_b200 import _lib
+    L = _lib.load()
+    EARG = -2
+    assert L.ec3r_apply_window_offset(None, 0, 0, None, 0, None, 0, None, None) == EARG   # world < 1
+    assert L.ec3r_apply_window_offset(None, 2, 2, None, 0, None, 0, None, None) == EARG   # rank >= world
+    assert L.ec3r_apply_window_offset(None, 2, 1, None, 0, None, 0, None, None) == EARG   # rank > 0 needs poses
+    assert L.ec3r_apply_window_offset(None, 1, 0, None, 0, None, 0, None, None) == 0      # nothing to do
+    assert L.ec3r_homography_ransac_score(None, None, None, -1, None, 10, 2.0, None, None, None, 0, None) == EARG
+    assert L.ec3r_homography_ransac_score(None, None, None, 0, None, 10, 2.0, None, None, None, 0, None) == 0
+    assert L.ec3r_homography_ransac_refit(None, None, None, 3, None, 10, 2.0, None, None, None, None, 0,
+                                          None) == EARG
+    assert L.ec3r_local_candidates(None, -1, None, 1, None, 0.7, None, None, None, 0, None) == EARG
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
