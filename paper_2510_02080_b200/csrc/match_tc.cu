@@ -592,6 +592,20 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
     return lo;
 }
 
+// pair_of for one thread per row: thread 0 searches the CTA's first row and
+// every thread steps forward from there (a CTA spans few pairs).  Call from
+// all threads of the CTA (it contains a barrier).
+__device__ __forceinline__ int pair_of_cta(const int64_t* __restrict__ off, int n_pairs, int64_t r, int64_t total) {
+    __shared__ int p0;
+    if (threadIdx.x == 0) p0 = pair_of(off, n_pairs, (int64_t)blockIdx.x * blockDim.x < total
+                                                          ? (int64_t)blockIdx.x * blockDim.x : total - 1);
+    __syncthreads();
+    int p = p0;
+    if (r < total)
+        while (p + 1 < n_pairs && off[p + 1] <= r) ++p;
+    return p;
+}
+
 
 // Stage 1 (one thread per row).  The exact top-2 similarities lie within the
 // key bounds of the approximate ones, so
@@ -605,8 +619,8 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
                                MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
                                int64_t* __restrict__ counters, int only_empty) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = pair_of_cta(a_off, n_pairs, r, total_a);
     if (r >= total_a) return;
-    const int p = pair_of(a_off, n_pairs, r);
     const int64_t M = b_off[p + 1] - b_off[p];
     if (only_empty && M != 0) return;  // decided in the tensor-core epilogue
     MatchRowState s;
@@ -644,8 +658,8 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
                              MatchRowState* __restrict__ rs, int32_t* __restrict__ col_best,
                              int32_t* __restrict__ pending, int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = pair_of_cta(a_off, n_pairs, r, total_a);
     if (r >= total_a) return;
-    const int p = pair_of(a_off, n_pairs, r);
     const int64_t a0 = a_off[p], N = a_off[p + 1] - a0;
     const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
     const MatchRowState s = rs[r];
@@ -658,15 +672,22 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
     int64_t rc = -1;
     const int n_rb = (int)((N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM));
     const unsigned long long* sl = col_slots + pair_slot[p] + s.best;
-    for (int rb = 0; rb < n_rb; ++rb) {
-        const unsigned long long v = __ldcg(sl + (int64_t)rb * M);
-        const uint32_t vb = (uint32_t)(v >> 32), vs = (uint32_t)v;
-        so = max(max(so, vs), min(bo, vb));
-        if (vb > bo) {
-            bo = vb;
-            const uint32_t code = __float_as_uint(ord2f(vb));
-            rc = (int64_t)rb * (TC_NA * TC_BM) + (int64_t)((code >> 5) & 1u) * TC_BM + ((code >> 6) & 3u) * 32 +
-                 (code & 31u);
+    constexpr int kBatch = 4;  // independent slot loads in flight
+    for (int rb0 = 0; rb0 < n_rb; rb0 += kBatch) {
+        unsigned long long vv[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) vv[q] = rb0 + q < n_rb ? __ldcg(sl + (int64_t)(rb0 + q) * M) : 0ull;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+            const int rb = rb0 + q;
+            const uint32_t vb = (uint32_t)(vv[q] >> 32), vs = (uint32_t)vv[q];
+            so = max(max(so, vs), min(bo, vb));
+            if (vb > bo) {
+                bo = vb;
+                const uint32_t code = __float_as_uint(ord2f(vb));
+                rc = (int64_t)rb * (TC_NA * TC_BM) + (int64_t)((code >> 5) & 1u) * TC_BM +
+                     ((code >> 6) & 3u) * 32 + (code & 31u);
+            }
         }
     }
     int mutual = -1;
