@@ -261,12 +261,25 @@ struct Solution {
 // registration.py:78-98 from the moments.  Degeneracy is decided from the
 // eigenvalues of M (sv of sqrt(w) dp squared); callers refine it with a
 // rotated-basis pass when the ratio is suspicious (see umeyama.cu).
+// The closed form after the two 3x3 decompositions (split out so that a
+// caller can run the covariance SVD and the source eigen-decomposition in
+// two threads at once).
+__device__ inline void umeyama_finish(const Moments& mo, int with_scale, const double U[3][3], const double sig[3],
+                                      const double V[3][3], const double lam[3], const double Vm[3][3],
+                                      Solution& out);
+
 __device__ inline void umeyama_solve(const Moments& mo, int with_scale, Solution& out) {
-    out.status = EC3R_ST_OK;
     double U[3][3], sig[3], V[3][3];
     svd3_jacobi(mo.C, U, sig, V);
     double Vm[3][3], Um[3][3], lam[3];
     svd3_jacobi(mo.M, Um, lam, Vm);  // symmetric PSD: singular values = eigenvalues
+    umeyama_finish(mo, with_scale, U, sig, V, lam, Vm, out);
+}
+
+__device__ inline void umeyama_finish(const Moments& mo, int with_scale, const double U[3][3], const double sig[3],
+                                      const double V[3][3], const double lam[3], const double Vm[3][3],
+                                      Solution& out) {
+    out.status = EC3R_ST_OK;
     for (int k = 0; k < 3; ++k) out.src_lambda[k] = fabs(lam[k]);
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) out.src_V[i][j] = Vm[i][j];

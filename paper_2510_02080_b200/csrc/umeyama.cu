@@ -457,10 +457,14 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         cl.sync();
         return;
     }
-    if (threadIdx.x == 0) {
-        Moments mo;
+    // the closed form: thread 32 decomposes the source moments while thread 0
+    // decomposes the covariance (two serial 3x3 Jacobi runs in parallel)
+    __shared__ double eig_sh[12];  // lam[3], Vm[3][3]
+    Moments mo;
+    double U[3][3], sig[3], V[3][3], mp[3];
+    if (threadIdx.x == 0 || threadIdx.x == 32) {
         mo.W = Wsum;
-        double mp[3], mq[3];
+        double mq[3];
         for (int k = 0; k < 3; ++k) { mp[k] = tot2[2 + k] / Wsum; mq[k] = tot2[5 + k] / Wsum; }
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j) mo.C[i][j] = tot2[8 + 3 * i + j] / Wsum - mq[i] * mp[j];
@@ -471,7 +475,23 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         mo.M[1][1] = m11; mo.M[1][2] = mo.M[2][1] = m12; mo.M[2][2] = m22;
         mo.varq = tot2[23] / Wsum - (mq[0] * mq[0] + mq[1] * mq[1] + mq[2] * mq[2]);
         for (int k = 0; k < 3; ++k) { mo.pbar[k] = shp[k] + mp[k]; mo.qbar[k] = shq[k] + mq[k]; }
-        umeyama_solve(mo, a.with_scale, sol);
+        if (threadIdx.x == 32) {
+            double Um[3][3], Vm[3][3], lam[3];
+            svd3_jacobi(mo.M, Um, lam, Vm);  // symmetric PSD: singular values = eigenvalues
+            for (int k = 0; k < 3; ++k) eig_sh[k] = lam[k];
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) eig_sh[3 + 3 * i + j] = Vm[i][j];
+        } else {
+            svd3_jacobi(mo.C, U, sig, V);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double lam[3], Vm[3][3];
+        for (int k = 0; k < 3; ++k) lam[k] = eig_sh[k];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) Vm[i][j] = eig_sh[3 + 3 * i + j];
+        umeyama_finish(mo, a.with_scale, U, sig, V, lam, Vm, sol);
         // stash the in-shift source centroid for the refinement pass
         sol.rms2_closed = fmax(sol.rms2_closed, 0.0);
         tot3[0] = mp[0]; tot3[1] = mp[1]; tot3[2] = mp[2];
