@@ -158,7 +158,12 @@ __device__ __noinline__ int vb_find_or_insert(const VB& v, unsigned long long bk
         if (k == kEmpty) {
             const unsigned long long prev = atomicCAS(&e->key, kEmpty, bk);
             if (prev == kEmpty) {
-                const unsigned long long slot = atomicAdd(&v.counters[4], 1ull);
+                // warp-aggregated allocation: the lanes that won a CAS together
+                // share one atomic on the (single, contended) block counter
+                cg::coalesced_group g = cg::coalesced_threads();
+                unsigned long long base = 0;
+                if (g.thread_rank() == 0) base = atomicAdd(&v.counters[4], (unsigned long long)g.size());
+                const unsigned long long slot = g.shfl(base, 0) + g.thread_rank();
                 int got = -2;
                 if ((int64_t)slot < v.max_blocks) {
                     got = (int)slot;
