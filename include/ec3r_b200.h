@@ -214,9 +214,9 @@ EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, f
  * the host), or -1: lets a caller size its outputs without a device read. */
 EC3R_API int64_t ec3r_vhash_extract_count(const ec3r_vhash* h);
 /* Multi-GPU: emit raw partial sums (key, sum w*dx, sum w, count) bucketed
- * by owner rank = hash(key) mod n_ranks for the all-to-all (outputs hold
- * U rows; workspace = ec3r_vhash_extract_workspace + 1 KB), and merge
- * received partials into a table. */
+ * by owner rank = hash(key) mod n_ranks (1 <= n_ranks <= 64) for the
+ * all-to-all (outputs hold U rows; workspace = ec3r_vhash_extract_workspace
+ * + 1 KB), and merge received partials into a table. */
 EC3R_API int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* keys, float* sums4,
                                 int32_t* count, int64_t* rank_counts, void* workspace,
                                 size_t workspace_bytes, void* stream);

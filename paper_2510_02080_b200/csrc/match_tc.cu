@@ -713,20 +713,31 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
         pending[atomicAdd((unsigned long long*)&counters[1], 1ull)] = (int32_t)c;
 }
 
+// max squared row norm: one warp per row (grid-stride), the CTA's maximum in
+// shared memory, one global atomic per CTA (a per-row atomic on one word
+// serialises at L2)
 __global__ void mt_norm_kernel(const uint16_t* __restrict__ X, int64_t rows, int D, unsigned int* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (r >= rows) return;
-    float s = 0.f;
-    for (int k = lane * 8; k < D; k += 256) {
-        double x[8];
-        Vec16<uint16_t>::load(X + r * D + k, x);
+    __shared__ unsigned int smax;
+    if (threadIdx.x == 0) smax = 0u;
+    __syncthreads();
+    unsigned int best = 0u;  // non-negative floats order like their bits
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        float s = 0.f;
+        for (int k = lane * 8; k < D; k += 256) {
+            double x[8];
+            Vec16<uint16_t>::load(X + r * D + k, x);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s = fmaf((float)x[i], (float)x[i], s);
+            for (int i = 0; i < 8; ++i) s = fmaf((float)x[i], (float)x[i], s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        best = max(best, __float_as_uint(s));
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) atomicMax(out, __float_as_uint(s));
+    if (lane == 0 && best) atomicMax(&smax, best);
+    __syncthreads();
+    if (threadIdx.x == 0 && smax) atomicMax(out, smax);
 }
 
 __global__ void mt_flag_all_kernel(int32_t* __restrict__ list, int64_t n) {
@@ -956,9 +967,12 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     if (!(norm_bound > 0)) {
         // max squared row norms of A and B (float32, rounded up below)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.nb, 0, 8, st));
-        mt_norm_kernel<<<(unsigned)((ta * 32 + 255) / 256), 256, 0, st>>>(A, ta, D, w.nb);
+        const auto norm_grid = [](int64_t rows) {
+            return (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows * 32 + 255) / 256, (int64_t)kNumSMs * 8));
+        };
+        mt_norm_kernel<<<norm_grid(ta), 256, 0, st>>>(A, ta, D, w.nb);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
-        mt_norm_kernel<<<(unsigned)((tb * 32 + 255) / 256), 256, 0, st>>>(B, tb, D, w.nb + 1);
+        mt_norm_kernel<<<norm_grid(tb), 256, 0, st>>>(B, tb, D, w.nb + 1);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
         unsigned int h[2];
         EC3R_CUDA_TRY(cudaMemcpyAsync(h, w.nb, 8, cudaMemcpyDeviceToHost, st));

@@ -663,9 +663,17 @@ __global__ void vb_gather_kernel(const float4* __restrict__ sums, const unsigned
 // partial sums for the multi-GPU all-to-all: owner = mix64(key) % n_ranks
 __global__ void vb_partition_count_kernel(const unsigned long long* __restrict__ keys, const int64_t* __restrict__ n_ptr,
                                           int n_ranks, unsigned long long* __restrict__ rank_counts) {
+    // per-CTA histogram in shared memory, one global add per (CTA, rank):
+    // a global atomic per voxel on <= n_ranks words serialises at L2
+    __shared__ unsigned int hist[64];
+    for (int r = threadIdx.x; r < n_ranks; r += blockDim.x) hist[r] = 0u;
+    __syncthreads();
     const int64_t n = *n_ptr;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&rank_counts[mix64(keys[i]) % (unsigned long long)n_ranks], 1ull);
+        atomicAdd(&hist[mix64(keys[i]) % (unsigned long long)n_ranks], 1u);
+    __syncthreads();
+    for (int r = threadIdx.x; r < n_ranks; r += blockDim.x)
+        if (hist[r]) atomicAdd(&rank_counts[r], (unsigned long long)hist[r]);
 }
 
 __global__ void vb_partition_write_kernel(const float4* __restrict__ sums, const unsigned int* __restrict__ counts,
@@ -678,7 +686,14 @@ __global__ void vb_partition_write_kernel(const float4* __restrict__ sums, const
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long k = keys[i];
         const int r = (int)(mix64(k) % (unsigned long long)n_ranks);
-        const unsigned long long o = rank_base[r] + atomicAdd(&cursors[r], 1ull);
+        // warp-aggregated cursor: one atomic per (warp, owner rank)
+        const unsigned peers = __match_any_sync(__activemask(), r);
+        const int lead = __ffs(peers) - 1;
+        const unsigned lanes_below = peers & ((1u << (threadIdx.x & 31)) - 1u);
+        unsigned long long base = 0;
+        if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(&cursors[r], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, lead);
+        const unsigned long long o = rank_base[r] + base + __popc(lanes_below);
         okeys[o] = (int64_t)k;
         reinterpret_cast<float4*>(sums4)[o] = sums[idx[i]];
         cnt[o] = (int32_t)counts[idx[i]];
@@ -741,8 +756,20 @@ __global__ void vb_block_count_kernel(const unsigned int* __restrict__ counts,
         }
         if (lane == 0) blk_cnt[b] = n;
     }
-    if (lane < 3) {
-        if (mn[lane] <= mx[lane]) { atomicMin(&bbox[lane], mn[lane]); atomicMax(&bbox[3 + lane], mx[lane]); }
+    // bounding box: shared-memory reduction first, then one global atomic
+    // per CTA and component (every warp hitting the six global words
+    // serialised them at L2)
+    __shared__ int sbox[6];
+    if (threadIdx.x < 3) { sbox[threadIdx.x] = INT_MAX; sbox[3 + threadIdx.x] = INT_MIN; }
+    __syncthreads();
+    if (lane < 3 && mn[lane] <= mx[lane]) {
+        atomicMin(&sbox[lane], mn[lane]);
+        atomicMax(&sbox[3 + lane], mx[lane]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && sbox[threadIdx.x] <= sbox[3 + threadIdx.x]) {
+        atomicMin(&bbox[threadIdx.x], sbox[threadIdx.x]);
+        atomicMax(&bbox[3 + threadIdx.x], sbox[3 + threadIdx.x]);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) blk_cnt[max_blocks] = 0;
 }
@@ -1103,7 +1130,7 @@ extern "C" int64_t ec3r_vhash_extract_count(const ec3r_vhash* h) { return h ? h-
 extern "C" int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* keys, float* sums4, int32_t* count,
                                            int64_t* rank_counts, void* workspace, size_t workspace_bytes,
                                            void* stream) {
-    if (!h || n_ranks < 1 || !keys || !sums4 || !count || !rank_counts) return EC3R_EARG;
+    if (!h || n_ranks < 1 || n_ranks > 64 || !keys || !sums4 || !count || !rank_counts) return EC3R_EARG;
     const size_t need = ec3r_vhash_extract_workspace(h) + 4 * align256(sizeof(unsigned long long) * n_ranks);
     if (!workspace || workspace_bytes < need) return EC3R_EWORKSPACE;
     cudaStream_t st = as_stream(stream);
