@@ -65,7 +65,13 @@ __global__ void lc_count_kernel(const double* __restrict__ pts, int64_t n, const
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0 && local) atomicAdd(counts + k, (unsigned long long)local);
+    // one global atomic per CTA: warps add into shared memory first
+    __shared__ unsigned int cta;
+    if (threadIdx.x == 0) cta = 0u;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(&cta, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta) atomicAdd(counts + k, (unsigned long long)cta);
 }
 
 __global__ void lc_decide_kernel(const unsigned long long* __restrict__ counts, int K, int64_t n, double tau_p,
