@@ -17,6 +17,8 @@ fused map (stage c), mirroring ``submap_slam.mapping`` (mapping.py:1-338).
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -276,6 +278,11 @@ class VoxelMap:
         return keys[:U], cen[:U], ws_[:U], cnt[:U]
 
 
+# block-table entries per expected block for a re-sized map (sparse: fewer
+# probe collisions at insert time; env override for A/B measurements)
+TABLE_PER_BLOCK = int(os.environ.get("EC3R_TABLE_PER_BLOCK", "64"))
+
+
 def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional[VoxelMap] = None,
                expected_voxels: Optional[int] = None, sort: bool = True, expected_blocks: Optional[int] = None):
     """Voxel fusion of pool slots with overflow-safe capacity growth.
@@ -287,7 +294,7 @@ def fuse_slots(pool: FramePool, slots: torch.Tensor, cell: float, vmap: Optional
         n_px = int(slots.numel()) * pool.H * pool.W
         cap = expected_voxels * 2 if expected_voxels else max(1 << 16, n_px // 8)
         vmap = VoxelMap(cell, cap, max_blocks=2 * expected_blocks if expected_blocks else None,
-                        table_entries=64 * expected_blocks if expected_blocks else 0)
+                        table_entries=TABLE_PER_BLOCK * expected_blocks if expected_blocks else 0)
     while True:
         vmap.clear()
         vmap.insert_frames(pool, slots)
