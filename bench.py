@@ -3,8 +3,9 @@ fused map points/sec and descriptor matches/sec vs the CPU reference).
 
 Workload (N=1): BASELINE configs[1] — synthetic TUM-style sequence, 300
 keyframes / 60 submaps (5 new + 1 shared frame each, 518x392), 1024 x 256-d
-descriptors per frame; one step = tracking match of 1500 frames against a
-1024-point map + registration of all 59 edges (one launch) + pose chaining +
+descriptors per frame; one step = tracking match of 1500 frames, each against
+its keyframe interval's resident 1024-point local map (300 maps, 5 frames per
+map) + registration of all 59 edges (one launch) + pose chaining +
 voxel-hash fusion at 2 cm of all 360 frames + sorted emit.  Inputs are
 resident in HBM and larger than L2 (126 MB).  Under torchrun each rank owns a
 contiguous window of the sequence (weak scaling).
@@ -133,10 +134,12 @@ def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
         sms.append(dm.add_submap(ids, sb.depth[o:o + F], sb.conf[o:o + F], list(sb.poses8[o:o + F]), j))
     del sb
     n_frames = 5 * n_kf  # tracked frames: 5 per keyframe
-    A, B, a_off, b_off = synth.make_descriptor_pairs(n_frames, n_desc, n_desc, 256, 0.05, seed=100 + rank,
-                                                     device=device)
+    # frames tracked against resident local maps: the 5 frames of a keyframe
+    # interval share one map (tracking.py:173-194), uploaded once
+    A, B, a_off, b_off, b_row = synth.make_descriptor_maps(n_frames, 5, n_desc, n_desc, 256, 0.05,
+                                                           seed=100 + rank, device=device)
     torch.cuda.synchronize()
-    return dm, sms, (A, B, a_off, b_off), (stub, send_pos)
+    return dm, sms, (A, B, a_off, b_off, b_row), (stub, send_pos)
 
 
 class Step:
@@ -185,8 +188,9 @@ class Step:
         torch = self.torch
         ev = {}
         ev["t0"] = self._event()
-        A, B, ao, bo = self.desc
-        self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8, self.norm_bound)
+        A, B, ao, bo, b_row = self.desc
+        self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8, self.norm_bound,
+                                                              b_row=b_row)
         ev["t_match"] = self._event()
         # registration of all edges (one launch) + device pose chain (one launch)
         out = self.plan.run(self.dm.pool) if self.chain is None else self.chain.run()
@@ -321,7 +325,7 @@ def main():
         step.run()
     torch.cuda.synchronize()
     n_points = step.vmap.stats()["n_points_in"]
-    A, B, ao, bo = desc
+    A, B, ao, bo = desc[:4]
     n_pairs_scored = int(np.sum(np.diff(ao) * np.diff(bo)))
 
     sampler = ClockSampler(local)
@@ -425,6 +429,7 @@ def main():
             "config": {"workload": "configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
                                    "tracking match + align + fuse",
                        "keyframes_per_gpu": args.keyframes, "frames_tracked_per_gpu": int(len(ao) - 1),
+                       "local_maps_per_gpu": int(B.shape[0]) // args.desc,
                        "resolution": [W, H], "voxel_m": 0.02, "submaps_per_gpu": len(sms),
                        "edges_per_gpu": len(step.pairs), "points_per_step_per_gpu": P, "voxels_per_gpu": U,
                        "l2": "inputs larger than L2 (pool %.0f MB, descriptors %.0f MB)" %
@@ -463,7 +468,7 @@ def run_e2e(step, dm, desc, args, world):
 
     pool = dm.pool
     n = pool.n
-    A, B, ao, bo = desc
+    A, B, ao, bo, b_row = desc
     h_in = [x.cpu().pin_memory() for x in (pool.depth[:n], pool.conf[:n], pool.poses[:n], A, B)]
     bufs = [(pool.depth, pool.conf, pool.poses, A, B),
             (pool.depth.clone(), pool.conf.clone(), pool.poses.clone(), A.clone(), B.clone())]
@@ -499,7 +504,7 @@ def run_e2e(step, dm, desc, args, world):
         main.wait_event(ready[i % 2])
         d, c, po, a, b = bufs[i % 2]
         pool.depth, pool.conf, pool.poses = d, c, po
-        step.desc = (a, b, ao, bo)
+        step.desc = (a, b, ao, bo, b_row)
         res = step.run()
         free[i % 2].record(main)
         out_bytes = 0

@@ -244,6 +244,16 @@ EC3R_API int ec3r_match_batched(const uint16_t* A, const uint16_t* B, const void
                        int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h,
                        int n_pairs, int D, double ratio, double norm_bound, int32_t* match_b,
                        int32_t* n_match, void* workspace, size_t workspace_bytes, void* stream);
+/* Shared maps: pair p's M_p = b_off_h[p+1] - b_off_h[p] columns are rows
+ * [b_row_h[p], b_row_h[p] + M_p) of B (host int64 per pair; n_b_rows rows
+ * in B), so consecutive frames tracked against one local map
+ * (tracking.py:173-194) share its rows.  b_off_h stays the per-pair column
+ * prefix (column state and outputs).  b_row_h = NULL: ec3r_match_batched. */
+EC3R_API int ec3r_match_batched_rows(const uint16_t* A, const uint16_t* B, const void* A_x, const void* B_x,
+                                     int exact_dtype, const int64_t* a_off_h, const int64_t* b_off_h,
+                                     const int64_t* b_row_h, int64_t n_b_rows, int n_pairs, int D, double ratio,
+                                     double norm_bound, int32_t* match_b, int32_t* n_match, void* workspace,
+                                     size_t workspace_bytes, void* stream);
 /* Diagnostics of the last ec3r_match_batched on this workspace (device
  * counters copied to host; synchronizes): rows / columns that needed the
  * float64 full rescan. */

@@ -70,7 +70,7 @@ __device__ __forceinline__ double warp_dot16(const T* a, const T* b, int D, int 
 }
 
 int match_exact_dispatch(const void* A, const void* B, int dtype, int D, const int64_t* a_off, const int64_t* b_off,
-                         int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
+                         const int64_t* b_row, int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
                          const int32_t* cols, const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs,
                          int32_t* col_best, cudaStream_t st);
 

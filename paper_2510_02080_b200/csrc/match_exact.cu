@@ -75,7 +75,8 @@ constexpr int MX_WARPS = MX_NT / 32;
 template <typename T>
 __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
                                                         const int64_t* __restrict__ a_off,
-                                                        const int64_t* __restrict__ b_off, int n_pairs,
+                                                        const int64_t* __restrict__ b_off,
+                                                        const int64_t* __restrict__ b_row, int n_pairs,
                                                         const int32_t* __restrict__ rows,
                                                         const int64_t* __restrict__ n_rows_ptr, int64_t n_rows_all,
                                                         MatchRowState* __restrict__ rs) {
@@ -87,11 +88,13 @@ __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A,
         const int64_t r = rows ? (int64_t)rows[t] : t;
         const int p = find_pair(a_off, n_pairs, r);
         const int64_t b0 = b_off[p], b1 = b_off[p + 1];
+        // the pair's B rows start at b_row[p] (shared maps) : shift the base
+        const T* Bp = B + (b_row[p] - b0) * (int64_t)D;
         double d1 = INFINITY, d2nd = INFINITY;
         int i1 = INT_MAX;
         for (int64_t j = b0 + 4 * warp; j < b1; j += 4 * MX_WARPS) {
             double s[4];
-            warp_dot4<T>(A + r * D, B, j, b1, D, lane, s);
+            warp_dot4<T>(A + r * D, Bp, j, b1, D, lane, s);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (j + u >= b1) break;
@@ -125,7 +128,8 @@ __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A,
 template <typename T>
 __global__ void __launch_bounds__(MX_NT) mx_cols_kernel(const T* __restrict__ A, const T* __restrict__ B, int D,
                                                         const int64_t* __restrict__ a_off,
-                                                        const int64_t* __restrict__ b_off, int n_pairs,
+                                                        const int64_t* __restrict__ b_off,
+                                                        const int64_t* __restrict__ b_row, int n_pairs,
                                                         const int32_t* __restrict__ cols,
                                                         const int64_t* __restrict__ n_cols_ptr, int64_t n_cols_all,
                                                         int32_t* __restrict__ col_best) {
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(MX_NT) mx_cols_kernel(const T* __restrict__ A,
         int i1 = INT_MAX;
         for (int64_t i = a0 + 4 * warp; i < a1; i += 4 * MX_WARPS) {
             double s[4];
-            warp_dot4<T>(B + c * D, A, i, a1, D, lane, s);
+            warp_dot4<T>(B + (b_row[p] + (c - b_off[p])) * D, A, i, a1, D, lane, s);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (i + u >= a1) break;
@@ -188,7 +192,8 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
 }
 
 template <typename T>
-int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int64_t* b_off, int n_pairs,
+int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int64_t* b_off, const int64_t* b_row,
+                 int n_pairs,
                  const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all, const int32_t* cols,
                  const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs, int32_t* col_best,
                  cudaStream_t st) {
@@ -196,11 +201,12 @@ int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int6
     const size_t smem = 0;
     const unsigned grid = kNumSMs * 8;
     if (rows != nullptr || n_rows_all > 0) {
-        mx_rows_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, n_pairs, rows, n_rows_ptr, n_rows_all, rs);
+        mx_rows_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, b_row, n_pairs, rows, n_rows_ptr, n_rows_all,
+                                                    rs);
         EC3R_CHECK_LAUNCH("mx_rows_kernel");
     }
     if (cols != nullptr || n_cols_all > 0) {
-        mx_cols_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, n_pairs, cols, n_cols_ptr, n_cols_all,
+        mx_cols_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, b_row, n_pairs, cols, n_cols_ptr, n_cols_all,
                                                     col_best);
         EC3R_CHECK_LAUNCH("mx_cols_kernel");
     }
@@ -208,18 +214,18 @@ int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int6
 }
 
 int match_exact_dispatch(const void* A, const void* B, int dtype, int D, const int64_t* a_off, const int64_t* b_off,
-                         int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
+                         const int64_t* b_row, int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
                          const int32_t* cols, const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs,
                          int32_t* col_best, cudaStream_t st) {
     switch (dtype) {
         case 0:
-            return launch_exact<uint16_t>((const uint16_t*)A, (const uint16_t*)B, D, a_off, b_off, n_pairs, rows,
+            return launch_exact<uint16_t>((const uint16_t*)A, (const uint16_t*)B, D, a_off, b_off, b_row, n_pairs, rows,
                                           n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
         case 1:
-            return launch_exact<float>((const float*)A, (const float*)B, D, a_off, b_off, n_pairs, rows, n_rows_ptr,
+            return launch_exact<float>((const float*)A, (const float*)B, D, a_off, b_off, b_row, n_pairs, rows, n_rows_ptr,
                                        n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
         case 2:
-            return launch_exact<double>((const double*)A, (const double*)B, D, a_off, b_off, n_pairs, rows,
+            return launch_exact<double>((const double*)A, (const double*)B, D, a_off, b_off, b_row, n_pairs, rows,
                                         n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
     }
     return EC3R_EARG;

@@ -78,7 +78,8 @@ struct __align__(16) TcUnit {
 
 struct TcParams {
     const int64_t* a_off;
-    const int64_t* b_off;
+    const int64_t* b_off;   // virtual column prefix (per-pair column state)
+    const int64_t* b_row;   // first B row of each pair (pairs may share a map's rows)
     const TcUnit* units;
     int n_units;
     int kblocks;        // D / 64
@@ -390,7 +391,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             uint32_t phase = 0, a_phase = 0;
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
                 const TcUnit un = p.units[u];
-                const int64_t b0 = p.b_off[un.pair] + un.col0;
+                const int64_t b0 = p.b_row[un.pair] + un.col0;
                 const int n_tiles = (un.col1 - un.col0) / TC_BN;
                 // A slices are refilled one k-block at a time as the previous
                 // unit's last tile releases them, interleaved with the first
@@ -926,6 +927,7 @@ static TcWs carve_tc(void* tc_ws, const int64_t* a_off_h, const int64_t* b_off_h
 // alignment rules out the tensor cores: every row and column is then listed
 // for the float64 re-scan (counters[0] = rows, counters[1] = cols).
 int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, const int64_t* b_off_d,
+                 const int64_t* b_row_d, int64_t n_b_rows,
                  const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
                  double norm_bound, double ratio, MatchRowState* rs, int32_t* flag_rows, int32_t* flag_cols,
                  int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, double* eps_out,
@@ -972,7 +974,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         };
         mt_norm_kernel<<<norm_grid(ta), 256, 0, st>>>(A, ta, D, w.nb);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
-        mt_norm_kernel<<<norm_grid(tb), 256, 0, st>>>(B, tb, D, w.nb + 1);
+        mt_norm_kernel<<<norm_grid(n_b_rows), 256, 0, st>>>(B, n_b_rows, D, w.nb + 1);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
         unsigned int h[2];
         EC3R_CUDA_TRY(cudaMemcpyAsync(h, w.nb, 8, cudaMemcpyDeviceToHost, st));
@@ -989,12 +991,12 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     if (exact_dtype != 0) eps_tc += ldexp(norm_bound, -7);
     *eps_out = eps_tc;
     CUtensorMap tmA, tmB;
-    if (!make_map(&tmA, A, ta, D) || !make_map(&tmB, B, tb, D)) {
+    if (!make_map(&tmA, A, ta, D) || !make_map(&tmB, B, n_b_rows, D)) {
         set_last_error_msg("cuTensorMapEncodeTiled failed");
         return EC3R_ECUDA;
     }
     TcParams prm;
-    prm.a_off = a_off_d; prm.b_off = b_off_d;
+    prm.a_off = a_off_d; prm.b_off = b_off_d; prm.b_row = b_row_d;
     prm.units = w.units; prm.n_units = (int)n_units; prm.kblocks = D / TC_BK;
     prm.cand = w.cand; prm.n_split = w.n_split; prm.col_slots = w.slots;
     prm.rs = rs; prm.pending = flag_rows; prm.counters = counters; prm.eps_tc = eps_tc; prm.ratio2 = ratio * ratio;

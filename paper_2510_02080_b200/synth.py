@@ -227,6 +227,36 @@ def make_descriptor_pairs(n_pairs: int, n: int, m: int, d: int = 256, sigma: flo
     return A.view(torch.int16), B.view(torch.int16), a_off, b_off
 
 
+def make_descriptor_maps(n_frames: int, frames_per_map: int, n: int, m: int, d: int = 256, sigma: float = 0.05,
+                         spurious: float = 0.2, seed: int = 0, device="cuda"):
+    """Tracking workload with resident local maps: frame f is matched
+    against map f // frames_per_map (tracking.py:173-194: consecutive frames
+    of a keyframe interval see the same local map).  Returns (A_bits,
+    B_bits, a_off, b_off, b_row) for tracking.match_batched_device: B holds
+    each map once, b_off is the per-frame column prefix (m per frame) and
+    b_row[f] the first row of frame f's map in B."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    n_maps = (n_frames + frames_per_map - 1) // frames_per_map
+    A = torch.empty((n_frames * n, d), dtype=torch.bfloat16, device=device)
+    B = torch.empty((n_maps * m, d), dtype=torch.bfloat16, device=device)
+    for k in range(n_maps):
+        tags = torch.randn((max(n, m), d), generator=g, device=device, dtype=torch.float32)
+        tags = tags / tags.norm(dim=1, keepdim=True)
+        B[k * m:(k + 1) * m] = tags[torch.randperm(tags.shape[0], generator=g, device=device)[:m]].to(torch.bfloat16)
+        for f in range(k * frames_per_map, min(n_frames, (k + 1) * frames_per_map)):
+            sel = torch.randperm(tags.shape[0], generator=g, device=device)[:n]
+            obs = tags[sel] + sigma * torch.randn((n, d), generator=g, device=device)
+            spur = torch.rand(n, generator=g, device=device) < spurious
+            fresh = torch.randn((n, d), generator=g, device=device)
+            obs = torch.where(spur[:, None], fresh, obs)
+            A[f * n:(f + 1) * n] = (obs / obs.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+    a_off = np.arange(n_frames + 1, dtype=np.int64) * n
+    b_off = np.arange(n_frames + 1, dtype=np.int64) * m
+    b_row = (np.arange(n_frames, dtype=np.int64) // frames_per_map) * m
+    return A.view(torch.int16), B.view(torch.int16), a_off, b_off, b_row
+
+
 def pooled_embeddings(n: int, cfg: SceneConfig = SceneConfig(), dim: int = 64, tokens: int = 16,
                       noise: float = 0.02, seed: int = 0, device="cuda") -> torch.Tensor:
     """Pooled unit retrieval vectors of a keyframe run (backend.py:216-226:

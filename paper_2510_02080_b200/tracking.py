@@ -9,7 +9,7 @@ pairs (tracking frames, a local-loop window) in one launch.
 
 from __future__ import annotations
 
-from typing import Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch
@@ -36,13 +36,17 @@ def to_bf16_bits(x: torch.Tensor) -> torch.Tensor:
 
 
 def match_batched_device(A_bits: torch.Tensor, B_bits: torch.Tensor, A_x, B_x, exact_dtype: int,
-                         a_off: np.ndarray, b_off: np.ndarray, ratio: float, norm_bound: float = 0.0, stream=None):
+                         a_off: np.ndarray, b_off: np.ndarray, ratio: float, norm_bound: float = 0.0, stream=None,
+                         b_row: Optional[np.ndarray] = None):
     """One launch sequence of ec3r_match_batched.
 
     A_bits/B_bits: (rows, D) int16 bf16 bits (D % 16 == 0); A_x/B_x: exact
     rows (None when exact_dtype == 0, else float32/float64 (rows, D));
-    a_off/b_off: host int64 (P+1) row offsets.  Returns (match_b (sumN,)
-    int32, n_match (P,) int32) CUDA tensors."""
+    a_off/b_off: host int64 (P+1) row offsets.  b_row (host int64 per pair,
+    optional): pair p's map rows start at B row b_row[p] instead of
+    b_off[p], so frames tracked against the same local map share its rows
+    (ec3r_match_batched_rows).  Returns (match_b (sumN,) int32, n_match (P,)
+    int32) CUDA tensors."""
     L = _lib.lib()
     P = len(a_off) - 1
     D = A_bits.shape[1]
@@ -54,10 +58,18 @@ def match_batched_device(A_bits: torch.Tensor, B_bits: torch.Tensor, A_x, B_x, e
     n_match = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
     ws_bytes = L.ec3r_match_workspace(a_off.ctypes.data, b_off.ctypes.data, P)
     ws = _lib.workspace(ws_bytes, dev, "match")
-    _lib.check(L.ec3r_match_batched(_lib.ptr(A_bits), _lib.ptr(B_bits), _lib.ptr(A_x), _lib.ptr(B_x),
-                                    int(exact_dtype), a_off.ctypes.data, b_off.ctypes.data, P, D, float(ratio),
-                                    float(norm_bound), _lib.ptr(match_b), _lib.ptr(n_match), _lib.ptr(ws), ws.numel(),
-                                    _lib.stream_ptr(stream)), "ec3r_match_batched")
+    if b_row is None:
+        _lib.check(L.ec3r_match_batched(_lib.ptr(A_bits), _lib.ptr(B_bits), _lib.ptr(A_x), _lib.ptr(B_x),
+                                        int(exact_dtype), a_off.ctypes.data, b_off.ctypes.data, P, D, float(ratio),
+                                        float(norm_bound), _lib.ptr(match_b), _lib.ptr(n_match), _lib.ptr(ws),
+                                        ws.numel(), _lib.stream_ptr(stream)), "ec3r_match_batched")
+    else:
+        b_row = np.ascontiguousarray(np.asarray(b_row, np.int64))
+        _lib.check(L.ec3r_match_batched_rows(_lib.ptr(A_bits), _lib.ptr(B_bits), _lib.ptr(A_x), _lib.ptr(B_x),
+                                             int(exact_dtype), a_off.ctypes.data, b_off.ctypes.data,
+                                             b_row.ctypes.data, int(B_bits.shape[0]), P, D, float(ratio),
+                                             float(norm_bound), _lib.ptr(match_b), _lib.ptr(n_match), _lib.ptr(ws),
+                                             ws.numel(), _lib.stream_ptr(stream)), "ec3r_match_batched_rows")
     _last.update(ws=ws, ta=ta, tb=tb, P=P)
     return match_b[:ta], n_match[:P]
 

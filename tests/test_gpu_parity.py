@@ -906,3 +906,34 @@ def test_verify_candidates_reference_bands():
     assert out[1].verdict == loops.REJECT and out[1].inlier_ratio == 0.0
     assert out[2].verdict == out[0].verdict and out[2].inlier_ratio == out[0].inlier_ratio
     assert loops.verify_candidate(u0, u1, loops.LoopConfig()).verdict == loops.REJECT
+
+
+def test_matcher_shared_map_rows_equal_expanded_copies():
+    """ec3r_match_batched_rows: frames tracked against the same local map
+    read its rows in place; the matches equal those of per-pair copies of
+    the map, on the tensor-core path (D = 256) and on the float64 re-scan
+    path (D = 48, not a tensor-core shape)."""
+    from paper_2510_02080_b200 import synth, tracking
+    for D, n_maps, per in ((256, 6, 5), (48, 3, 4)):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(D)
+        maps = torch.randn((n_maps * 300, D), generator=g, device="cuda")
+        maps = synth.bf16_round(maps / maps.norm(dim=1, keepdim=True))
+        P = n_maps * per
+        A = []
+        for p in range(P):
+            base = maps[(p // per) * 300:(p // per + 1) * 300]
+            obs = base[torch.randperm(300, generator=g, device="cuda")[:257]] + 0.05 * torch.randn(
+                (257, D), generator=g, device="cuda")
+            A.append(synth.bf16_round(obs / obs.norm(dim=1, keepdim=True)))
+        A = torch.cat(A)
+        a_off = np.arange(P + 1, dtype=np.int64) * 257
+        b_off = np.arange(P + 1, dtype=np.int64) * 300
+        b_row = (np.arange(P, dtype=np.int64) // per) * 300
+        bits = lambda x: x.to(torch.bfloat16).view(torch.int16)  # noqa: E731
+        Bx = torch.cat([maps[r:r + 300] for r in b_row])
+        m1, n1 = tracking.match_batched_device(bits(A), bits(Bx), None, None, 0, a_off, b_off, 0.8)
+        m2, n2 = tracking.match_batched_device(bits(A), bits(maps), None, None, 0, a_off, b_off, 0.8, b_row=b_row)
+        np.testing.assert_array_equal(m1.cpu().numpy(), m2.cpu().numpy())
+        np.testing.assert_array_equal(n1.cpu().numpy(), n2.cpu().numpy())
+        assert int(n1.sum()) > P * 50
