@@ -58,6 +58,17 @@ def test_argument_errors_without_gpu():
     assert L.ec3r_homography_ransac_refit(None, None, None, 3, None, 10, 2.0, None, None, None, None, 0,
                                           None) == EARG
     assert L.ec3r_local_candidates(None, -1, None, 1, None, 0.7, None, None, None, 0, None) == EARG
+    # shared map rows: every pair's rows must lie inside B
+    a_off = np.array([0, 4, 8], np.int64)
+    b_off = np.array([0, 3, 6], np.int64)
+    ok_rows = np.array([0, 0], np.int64)
+    bad_rows = np.array([0, 2], np.int64)   # rows 2..4 of a 3-row B
+    assert L.ec3r_match_batched_rows(None, None, None, None, 0, a_off.ctypes.data, b_off.ctypes.data,
+                                     bad_rows.ctypes.data, 3, 2, 16, 0.8, 0.0, None, None, None, 0,
+                                     None) == EARG
+    assert L.ec3r_match_batched_rows(None, None, None, None, 0, a_off.ctypes.data, b_off.ctypes.data,
+                                     ok_rows.ctypes.data, 3, 2, 16, 0.8, 0.0, None, None, None, 0,
+                                     None) == -3  # passes the row check, then needs a workspace
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
