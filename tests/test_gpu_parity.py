@@ -937,3 +937,48 @@ def test_matcher_shared_map_rows_equal_expanded_copies():
         np.testing.assert_array_equal(m1.cpu().numpy(), m2.cpu().numpy())
         np.testing.assert_array_equal(n1.cpu().numpy(), n2.cpu().numpy())
         assert int(n1.sum()) > P * 50
+
+
+def test_verify_candidates_batch_vs_oracle():
+    """One query against 12 candidates (0-90 % of its keypoints on a
+    homography, bf16-exact descriptors): the batched K5 + K9 verdicts equal
+    the oracle's match_descriptors + estimate_homography_ransac + bands."""
+    from oracle import ransac as orr
+    from paper_2510_02080_b200 import loops, synth
+    rng = np.random.default_rng(2024)
+    n, D = 160, 64
+    qd = synth.bf16_round(torch.as_tensor(rng.normal(size=(n, D)))).numpy()
+    qd /= np.linalg.norm(qd, axis=1, keepdims=True)
+    qd = synth.bf16_round(torch.as_tensor(qd)).numpy()
+    qk = rng.uniform(0, 640, size=(n, 2))
+    cands = []
+    for c in range(12):
+        frac = c / 12.0
+        k = int(frac * n)
+        h = np.eye(3) + 0.03 * rng.normal(size=(3, 3))
+        h[2, :2] *= 1e-3
+        h[2, 2] = 1.0
+        sh = np.concatenate([qk, np.ones((n, 1))], axis=1) @ h.T
+        kp = sh[:, :2] / sh[:, 2:3] + 0.3 * rng.normal(size=(n, 2))
+        kp[k:] = rng.uniform(0, 640, size=(n - k, 2))
+        dd = qd + 0.02 * rng.normal(size=(n, D))
+        dd[int(0.8 * n):] = rng.normal(size=(n - int(0.8 * n), D))
+        dd /= np.linalg.norm(dd, axis=1, keepdims=True)
+        dd = synth.bf16_round(torch.as_tensor(dd)).numpy()
+        perm = rng.permutation(n)
+        cands.append(_Obs(c + 1, kp[perm], dd[perm]))
+    cfg = loops.LoopConfig()
+    got = loops.verify_candidates(_Obs(0, qk, qd), cands, cfg)
+    for cobs, v in zip(cands, got):
+        pairs = ref.match_descriptors(qd, cobs.descriptors, cfg.match_ratio)
+        if len(pairs) < 4:
+            exp_v, exp_r = loops.REJECT, 0.0
+        else:
+            a = np.array([p[0] for p in pairs])
+            b = np.array([p[1] for p in pairs])
+            _, _, r = orr.estimate_homography_ransac(qk[a], cobs.keypoints[b], cfg.ransac.pixel_threshold,
+                                                     cfg.ransac.confidence, cfg.ransac.max_iterations, cfg.ransac.seed)
+            exp_r = r
+            exp_v = loops.REJECT if r <= cfg.tau2 else loops.APPEND if r <= cfg.tau1 else loops.REPLACE
+        assert v.inlier_ratio == exp_r and v.verdict == exp_v, (cobs.frame_id, v, exp_v, exp_r)
+    assert {v.verdict for v in got} >= {loops.REJECT, loops.REPLACE}
