@@ -616,6 +616,25 @@ def run_extras(peaks):
         ms = _time_ms(lambda: loops.retrieval_device(pooled, 5, 15, 0.93, 0.96), reps=5, warm=1)
         out["retrieval"].append({"keyframes": K, "ms": ms, "scored_pairs": scored,
                                  "scored_pairs_per_s": scored / (ms * 1e-3), "candidates": int(len(res[2]))})
+    # K1 inverse projection (§8(a) a2, backend.py:78-101; off the fusion step,
+    # which reads the pool planes directly): one 6-frame full-resolution
+    # submap per call, float64 points + conf + frame ids + pixels out
+    from paper_2510_02080_b200 import backend
+
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(11, cfg, seed=3, device="cuda")
+    o, ids = sb.slot_offsets[0], sb.frame_ids[0]
+    dsub, csub = sb.depth[o:o + len(ids)].contiguous(), sb.conf[o:o + len(ids)].contiguous()
+    psub = sb.poses8[o:o + len(ids)]
+    res = backend.inverse_project_device(dsub, csub, sb.K4, psub, ids)
+    n_valid = int(res[0].shape[0])
+    ms = _time_ms(lambda: backend.inverse_project_device(dsub, csub, sb.K4, psub, ids), reps=10, warm=2)
+    px = int(dsub.numel())
+    out["inverse_project"] = {"frames": len(ids), "pixels": px, "points": n_valid, "ms": ms,
+                              "points_per_s": n_valid / (ms * 1e-3),
+                              "gbs": (8 * px + 56 * n_valid) / (ms * 1e-3) / 1e9,
+                              "note": "8 B/px in + 56 B/point out; includes the one D2H of the point count"}
+    del sb, dsub, csub
     # K9 loop verification (§8f rank 4): 64 candidates x 500 matches, 40 %
     # inliers, full 1000-iteration budget scored on the device; the reference
     # loop (oracle port) on 4 of them on the host for scale
