@@ -239,6 +239,13 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_
                             ((uint32_t)(TC_BM >> 4) << 24);
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+#ifndef EC3R_MT_SPLITBAR
+#define EC3R_MT_SPLITBAR 1  // per-tile colbuf handoff: only the merging warps wait
+#endif
 
 // d2 = max(2 - 2 s, 0) (tracking.py:153) on interval end points
 __device__ __forceinline__ double d2c(double s) { return fmax(2.0 - 2.0 * s, 0.0); }
@@ -469,6 +476,12 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         int acc = 0;
         uint32_t acc_phase = 0;
         int tb = 0;  // colbuf double buffer (alternates over all tiles of the CTA)
+        // warps 2-5 merge the 4 quarter partials of the tile's columns; with
+        // EC3R_MT_SPLITBAR the other warps only arrive at the tile's "full"
+        // barrier (ids 2 + buffer) and wait on "merged" (ids 4 + buffer)
+        // before reusing that buffer two tiles later
+        const bool merger = et < TC_BN;
+        int ttile = 0;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             const TcUnit un = p.units[u];
             const int64_t a1 = p.a_off[un.pair + 1];
@@ -479,6 +492,9 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             const int64_t row0 = (int64_t)un.row0 + q * 32 + lane, row1 = row0 + TC_BM;
             const bool rv0 = row0 < a1, rv1 = row1 < a1;
             for (int t = 0; t < n_tiles; ++t) {
+#if EC3R_MT_SPLITBAR
+                if (!merger && ttile >= 2) named_sync(4 + tb, TC_EPI_THREADS);  // tile ttile-2 merged
+#endif
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
                 const int col0 = un.col0 + t * TC_BN;
@@ -510,11 +526,16 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     chunk_epilogue(rc, rd, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq + 256u,
                                    lane);
                 }
+#if EC3R_MT_SPLITBAR
+                if (merger) named_sync(2 + tb, TC_EPI_THREADS);
+                else named_arrive(2 + tb, TC_EPI_THREADS);
+#else
                 named_sync(1, TC_EPI_THREADS);
+#endif
                 // merge the 4 quarter partials of column et and fold into the
                 // global state (colbuf is double-buffered: the next tile
                 // writes the other half, so one barrier per tile suffices)
-                if (et < TC_BN && col0 + et < M) {
+                if (merger && col0 + et < M) {
                     const uint32_t cb = smem_u32(colbuf + (size_t)tb * 4 * TC_BN + et);
                     const float2 v0 = lds_f2(cb), v1 = lds_f2(cb + 8u * TC_BN), v2 = lds_f2(cb + 16u * TC_BN),
                                  v3 = lds_f2(cb + 24u * TC_BN);
@@ -529,7 +550,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     __stcg(p.col_slots + un.slot + (col0 - un.col0) + et,
                            ((unsigned long long)f2ord(bq) << 32) | (unsigned long long)f2ord(sk));
                 }
+#if EC3R_MT_SPLITBAR
+                if (merger) named_arrive(4 + tb, TC_EPI_THREADS);
+#endif
                 tb ^= 1;
+                ++ttile;
             }
             // the two column-half warps of a quarter hold partial states of
             // the same rows: h = 1 hands its (best, second, column) over
@@ -571,6 +596,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 }
             }
         }
+#if EC3R_MT_SPLITBAR
+        // consume the "merged" arrivals of the last two tiles
+        if (!merger)
+            for (int k = ttile >= 2 ? ttile - 2 : 0; k < ttile; ++k) named_sync(4 + (k & 1), TC_EPI_THREADS);
+#endif
     }
     tc_fence_before();
     __syncthreads();
