@@ -283,3 +283,20 @@ def test_window_offsets_prefix_compose_gloo():
     got = vec_to_sim3(out[1])
     assert abs(got.scale - vec_to_sim3(w0).scale) < 1e-15 and abs(exp.scale - got.scale) == 0
     np.testing.assert_allclose(got.translation, vec_to_sim3(w0).translation, atol=1e-15)
+
+
+def test_prefix_offsets_compose_in_rank_order():
+    """O_r = W_0 o ... o W_{r-1}: the global pose of window r's reference
+    frame, for any number of windows (pure host math of window_offset)."""
+    from paper_2510_02080_b200.types import Sim3Transform, sim3_to_vec, vec_to_sim3
+    rng = np.random.default_rng(11)
+    W = [_tf(rng) for _ in range(5)]
+    offs = D.prefix_offsets(W)
+    acc = Sim3Transform.identity()
+    for r in range(5):
+        got = vec_to_sim3(offs[r])
+        assert abs(got.scale - acc.scale) <= 1e-12 * acc.scale
+        np.testing.assert_allclose(got.translation, acc.translation, atol=1e-9)
+        np.testing.assert_allclose(np.abs(np.dot(got.rotation.q, acc.rotation.q)), 1.0, atol=1e-12)
+        acc = acc.compose(vec_to_sim3(W[r]))
+    np.testing.assert_array_equal(offs[0], sim3_to_vec(Sim3Transform.identity()))
