@@ -338,7 +338,10 @@ __global__ void vh_frame_tables_kernel(FuseArgs a, float4* __restrict__ ftab) {
 // (frame-major ... all frames interleaved) and pool working set changed the
 // time by < 10%, so the pool's L2 residency is not the limiter.
 constexpr int ST_H = 8, ST_W = 16;
-constexpr int BC_BITS = 11;  // shared-memory block cache: 2048 entries (16 KB)
+#ifndef EC3R_BC_BITS
+#define EC3R_BC_BITS 11
+#endif
+constexpr int BC_BITS = EC3R_BC_BITS;  // shared-memory block cache: 2048 entries (16 KB)
 
 #ifndef EC3R_FI_G
 #define EC3R_FI_G 1  // consecutive listed frames per CTA (same band): the block cache carries over
