@@ -19,7 +19,10 @@
 
 namespace ec3r {
 
-constexpr int UM_CL = 8;    // CTAs per cluster (portable maximum)
+#ifndef EC3R_UM_CL
+#define EC3R_UM_CL 8
+#endif
+constexpr int UM_CL = EC3R_UM_CL;  // CTAs per cluster (portable maximum 8)
 constexpr int UM_NT = 256;  // threads per CTA
 
 // Reduce K doubles across the CTA: result valid in out[0..K) for all threads
