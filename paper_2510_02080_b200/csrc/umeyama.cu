@@ -569,6 +569,9 @@ __device__ void sim3_compose_dev(const double* a, const double* b, double* o) {
 // a direct walk cost ~1 us per submap); all threads then write back.
 constexpr int CHAIN_NT = 256;
 
+__host__ __device__ inline size_t chain_par_extra(int n_sub) {
+    return 16 + sizeof(double) * 16 * (size_t)n_sub + sizeof(int) * 4 * (size_t)n_sub;
+}
 __host__ __device__ inline size_t chain_smem(int n_sub, int n_edges) {
     return sizeof(double) * 8 * ((size_t)n_sub + n_edges) + sizeof(int64_t) * n_edges +
            sizeof(int32_t) * (2 * (size_t)n_edges + 2 * n_sub + 1) + 16;
@@ -608,7 +611,62 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
         es = es_s; ec = ec_s; est = est_s; ep = ep_s; eo = eo_s; sst = sst_s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // parallel form (pointer jumping over the partner tree) when its extra
+    // arrays fit next to the staged inputs: every submap's strongest edge is
+    // known up front, so global_j = global_root o (T_a o ... o T_j) and the
+    // chain takes log2(depth) rounds instead of n_sub dependent steps
+    const size_t base_b = chain_smem(n_sub, n_edges);
+    const bool par = staged && base_b + chain_par_extra(n_sub) <= smem_cap;
+    if (par) {
+        double* T0 = (double*)((char*)csh + ((base_b + 15) & ~(size_t)15));
+        double* T1 = T0 + 8 * (size_t)n_sub;
+        int* an0 = (int*)(T1 + 8 * (size_t)n_sub);
+        int* an1 = an0 + n_sub;
+        int* rt0 = an1 + n_sub;
+        int* rt1 = rt0 + n_sub;
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
+            const int e0 = eo[j], e1 = eo[j + 1];
+            int best = -1;
+            for (int e = e0; e < e1; ++e)
+                if (est[e] == EC3R_ST_OK && (best < 0 || ec[e] > ec[best])) best = e;
+            const bool linked = e1 > e0 && best >= 0;
+            if (sst) sst[j] = (e1 > e0 && best < 0) ? EC3R_ST_SKIP : EC3R_ST_OK;  // SKIP: NoSharedKeyframes
+            an0[j] = linked ? ep[best] : -1;
+            rt0[j] = linked ? -1 : j;
+            for (int k = 0; k < 8; ++k) T0[8 * j + k] = linked ? es[8 * best + k] : (k < 2 ? 1.0 : 0.0);
+        }
+        __syncthreads();
+        for (int span = 1; span < n_sub; span <<= 1) {
+            for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
+                const int a = an0[j];
+                if (a >= 0) {
+                    sim3_compose_dev(T0 + 8 * a, T0 + 8 * j, T1 + 8 * j);
+                    an1[j] = an0[a];
+                    rt1[j] = an0[a] < 0 ? rt0[a] : -1;
+                } else {
+                    for (int k = 0; k < 8; ++k) T1[8 * j + k] = T0[8 * j + k];
+                    an1[j] = -1;
+                    rt1[j] = rt0[j];
+                }
+            }
+            __syncthreads();
+            double* tt = T0; T0 = T1; T1 = tt;
+            int* ta = an0; an0 = an1; an1 = ta;
+            int* tr = rt0; rt0 = rt1; rt1 = tr;
+        }
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
+            const int r = rt0[j];
+            if (r != j) {  // roots keep their given global
+                double o[8];
+                sim3_compose_dev(g + 8 * r, T0 + 8 * j, o);
+                for (int k = 0; k < 8; ++k) T1[8 * j + k] = o[k];
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT)
+            if (rt0[j] != j)
+                for (int k = 0; k < 8; ++k) g[8 * j + k] = T1[8 * j + k];
+    } else if (threadIdx.x == 0) {
         for (int j = 0; j < n_sub; ++j) {
             const int e0 = eo[j], e1 = eo[j + 1];
             int best = -1;
