@@ -6,8 +6,10 @@
 // across the cluster through distributed shared memory (fixed rank order), so
 // results are deterministic and independent of scheduling.  The 3x3 closed
 // form (one-sided Jacobi SVD, reflection guard, scale, translation,
-// Shepperd quaternion) runs redundantly in one thread of every CTA from the
-// identical cluster totals, so no extra broadcast round is needed.
+// Shepperd quaternion) runs redundantly in every CTA from the identical
+// cluster totals, so no extra broadcast round is needed; in the pool kernel
+// the covariance SVD and the source eigen-decomposition run in two threads
+// at once.
 //
 // Reference: registration.py:38-102 (align_point_sets), mapping.py:138-183
 // (_shared_correspondences + gate/floor of _registration_edges).
@@ -547,9 +549,10 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
 // ---------------------------------------------------------------------------
 // Pose chaining of register_submap (mapping.py:200-204): the strongest edge
 // (max count, first on ties — Python max()) sets
-// global_j = global_partner o T (sim3_compose, liegroups.py:275-281).  One
-// thread; the chain is sequential and tiny, but keeping it on the device
-// removes the host round trip between registration and fusion.
+// global_j = global_partner o T (sim3_compose, liegroups.py:275-281).  The
+// strongest edges are known before chaining, so the chain is pointer jumping
+// over the partner tree (log2 rounds of parallel compositions); keeping it on
+// the device removes the host round trip between registration and fusion.
 __device__ void sim3_compose_dev(const double* a, const double* b, double* o) {
     const double aw = a[1], ax = a[2], ay = a[3], az = a[4];
     const double bw = b[1], bx = b[2], by = b[3], bz = b[4];
