@@ -35,6 +35,8 @@
 
 #include <algorithm>
 
+#include <cub/block/block_scan.cuh>
+
 #include "common.cuh"
 #include "match.cuh"
 
@@ -785,7 +787,8 @@ __global__ void mt_flag_all_kernel(int32_t* __restrict__ list, int64_t n) {
 __global__ void __launch_bounds__(1024) mt_unit_scan(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off,
                                                     int n_pairs, int n_split, long long* __restrict__ unit_base,
                                                     long long* __restrict__ pair_slot) {
-    __shared__ long long s_u[1024], s_s[1024];
+    using BScan = cub::BlockScan<long long, 1024>;
+    __shared__ typename BScan::TempStorage scan_tmp;
     __shared__ long long base_u, base_s;
     if (threadIdx.x == 0) { base_u = 0; base_s = 0; }
     __syncthreads();
@@ -801,25 +804,19 @@ __global__ void __launch_bounds__(1024) mt_unit_scan(const int64_t* __restrict__
                 ns = rb * M;
             }
         }
-        s_u[threadIdx.x] = nu;
-        s_s[threadIdx.x] = ns;
+        // exclusive block scans (warp shuffles; one barrier pair per scan)
+        long long eu, es, tu, ts;
+        BScan(scan_tmp).ExclusiveSum(nu, eu, tu);
         __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan
-            const long long au = threadIdx.x >= o ? s_u[threadIdx.x - o] : 0;
-            const long long as = threadIdx.x >= o ? s_s[threadIdx.x - o] : 0;
-            __syncthreads();
-            s_u[threadIdx.x] += au;
-            s_s[threadIdx.x] += as;
-            __syncthreads();
-        }
+        BScan(scan_tmp).ExclusiveSum(ns, es, ts);
         if (p < n_pairs) {
-            unit_base[p] = base_u + s_u[threadIdx.x] - nu;
-            pair_slot[p] = base_s + s_s[threadIdx.x] - ns;
+            unit_base[p] = base_u + eu;
+            pair_slot[p] = base_s + es;
         }
         __syncthreads();
-        if (threadIdx.x == 1023) {
-            base_u += s_u[1023];
-            base_s += s_s[1023];
+        if (threadIdx.x == 0) {
+            base_u += tu;
+            base_s += ts;
         }
         __syncthreads();
     }
