@@ -118,15 +118,21 @@ EC3R_API int ec3r_register_edges(const float* depth_pool, const float* conf_pool
                         int64_t* out_npairs, int32_t* out_status, uint8_t* keep_masks,
                         void* workspace, size_t workspace_bytes, void* stream);
 
-/* Pose chaining of register_submap (mapping.py:200-204) on the device:
- * submaps 0..n_sub-1 in registration order; submap j's edges are
- * [sub_edge_off[j], sub_edge_off[j+1]) with edge_partner[e] < j the partner
- * submap index.  The OK edge with the largest count (first on ties) sets
- * sub_globals[j] = sub_globals[partner] o edge_sim3[e]; submaps with an
- * empty edge range keep the caller's sub_globals entry (gauge / already
- * registered); sub_status[j] = EC3R_ST_SKIP when no edge survived
- * (NoSharedKeyframes).  slot_globals[s] for s in
- * [sub_slot_off[j], sub_slot_off[j+1]) receives sub_globals[j]. */
+/* Pose chaining of register_submap (mapping.py:190-211) on the device:
+ * submaps 0..n_sub-1 in registration order; submap 0 is the fixed root (the
+ * first submap, or a sharded window's halo stub) and keeps the caller's
+ * sub_globals[0].  Submap j's edges are [sub_edge_off[j], sub_edge_off[j+1])
+ * with edge_partner[e] < j the partner submap index.  Edges to partners that
+ * were not committed (sub_status != OK) are ignored, SKIP edges are dropped,
+ * the first error edge status aborts the submap (sub_status[j] = that status,
+ * as align_point_sets raises out of the reference loop), and no surviving edge
+ * gives sub_status[j] = EC3R_ST_SKIP (NoSharedKeyframes); such submaps keep
+ * the caller's sub_globals entry.  Otherwise the OK edge with the largest
+ * count (first on ties) sets sub_globals[j] = sub_globals[partner] o
+ * edge_sim3[e].  slot_globals[s] for s in [sub_slot_off[j], sub_slot_off[j+1])
+ * receives sub_globals[j].  sub_status (DEVICE, n_sub) is required.
+ * Env EC3R_CHAIN_SMEM_CAP (bytes) caps the shared-memory staging (tests use
+ * it to force the sequential walk). */
 EC3R_API int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_count,
                               const int32_t* edge_status, const int32_t* edge_partner,
                               const int32_t* sub_edge_off, int n_sub, const int32_t* sub_slot_off,
@@ -319,6 +325,18 @@ EC3R_API int ec3r_local_candidates(const double* positions, int64_t n_points, co
                                    int n_keyframes, const double* intrinsics_h, double tau_p,
                                    int64_t* out_counts, int32_t* out_cand, void* workspace,
                                    size_t workspace_bytes, void* stream);
+/* As ec3r_local_candidates, plus the margin guard: every (keyframe, point)
+ * whose visibility lies within 1e-6 px of the image border or 1e-12 of
+ * Z_MIN is listed in amb_out (DEVICE, amb_cap x 3 int32: keyframe, point,
+ * device decision); amb_count (DEVICE u64) receives the total (may exceed
+ * amb_cap: re-run larger).  The host re-decides those points with the
+ * reference's numpy expression (pts @ R.T + t, geometry.py:96-108) and
+ * corrects the counts. */
+EC3R_API int ec3r_local_candidates_ex(const double* positions, int64_t n_points, const double* world_from_cam,
+                                      int n_keyframes, const double* intrinsics_h, double tau_p,
+                                      int64_t* out_counts, int32_t* out_cand, int32_t* amb_out, int64_t amb_cap,
+                                      unsigned long long* amb_count, void* workspace, size_t workspace_bytes,
+                                      void* stream);
 
 /* ---------------------------------------------------------------------
  * K9 (§8f rank 4): batched homography RANSAC (loop verification).

@@ -11,7 +11,11 @@
 // safe_z + cx (geometry.py:99-102), all with _rn intrinsics (no FMA).  The
 // matmul pts @ R.T runs in BLAS on the reference side, whose summation order
 // is not pinned: a visibility decision can differ only for a point whose
-// projection lies within an ulp of the image border or of z = Z_MIN.
+// projection lies within an ulp of the image border or of z = Z_MIN.  Such
+// points are listed (margin guard: a band of 1e-6 px around the border and
+// 1e-12 around Z_MIN, far above the ~1e-12 px disagreement of the two
+// summation orders) with the device's decision, and the host re-decides
+// them with the reference's own numpy expression.
 
 #include "common.cuh"
 
@@ -45,7 +49,8 @@ __device__ __forceinline__ void lc_camera(const double* wfc, LcCam& c) {
 
 __global__ void lc_count_kernel(const double* __restrict__ pts, int64_t n, const double* __restrict__ poses,
                                 double fx, double fy, double cx, double cy, double wmax, double hmax,
-                                unsigned long long* __restrict__ counts) {
+                                unsigned long long* __restrict__ counts, int32_t* __restrict__ amb,
+                                int64_t amb_cap, unsigned long long* __restrict__ amb_count) {
     __shared__ LcCam cam;
     const int k = blockIdx.y;
     if (threadIdx.x == 0) lc_camera(poses + 8 * (size_t)k, cam);
@@ -61,7 +66,23 @@ __global__ void lc_count_kernel(const double* __restrict__ pts, int64_t n, const
         const double sz = fabs(z) > LC_Z_MIN ? z : 1.0;
         const double u = xa(__ddiv_rn(xm(fx, pc[0]), sz), cx);
         const double v = xa(__ddiv_rn(xm(fy, pc[1]), sz), cy);
-        local += (z > LC_Z_MIN && u >= 0.0 && u <= wmax && v >= 0.0 && v <= hmax) ? 1u : 0u;
+        const bool vis = z > LC_Z_MIN && u >= 0.0 && u <= wmax && v >= 0.0 && v <= hmax;
+        local += vis ? 1u : 0u;
+        if (amb) {
+            const double bp = 1e-6;
+            const bool near_z = fabs(z - LC_Z_MIN) < 1e-12;
+            const bool in_z = z > LC_Z_MIN - 1e-12;
+            const bool near_uv = fabs(u) < bp || fabs(u - wmax) < bp || fabs(v) < bp || fabs(v - hmax) < bp;
+            const bool in_uv = u > -bp && u < wmax + bp && v > -bp && v < hmax + bp;
+            if ((near_z && in_uv) || (near_uv && in_z && in_uv)) {
+                const unsigned long long o = atomicAdd(amb_count, 1ull);
+                if ((int64_t)o < amb_cap) {
+                    amb[3 * o] = k;
+                    amb[3 * o + 1] = (int32_t)i;
+                    amb[3 * o + 2] = vis ? 1 : 0;
+                }
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -91,9 +112,11 @@ extern "C" size_t ec3r_local_candidates_workspace(int n_keyframes) {
     return align256(sizeof(unsigned long long) * (size_t)(n_keyframes > 0 ? n_keyframes : 1));
 }
 
-extern "C" int ec3r_local_candidates(const double* positions, int64_t n_points, const double* world_from_cam,
-                                     int n_keyframes, const double* intrinsics_h, double tau_p, int64_t* out_counts,
-                                     int32_t* out_cand, void* workspace, size_t workspace_bytes, void* stream) {
+extern "C" int ec3r_local_candidates_ex(const double* positions, int64_t n_points, const double* world_from_cam,
+                                        int n_keyframes, const double* intrinsics_h, double tau_p, int64_t* out_counts,
+                                        int32_t* out_cand, int32_t* amb_out, int64_t amb_cap,
+                                        unsigned long long* amb_count, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
     if (n_points < 0 || n_keyframes < 0 || !intrinsics_h) return EC3R_EARG;
     if (n_keyframes == 0) return EC3R_OK;
     if (!world_from_cam || !out_cand || (n_points && !positions)) return EC3R_EARG;
@@ -101,6 +124,8 @@ extern "C" int ec3r_local_candidates(const double* positions, int64_t n_points, 
     cudaStream_t st = as_stream(stream);
     unsigned long long* counts = (unsigned long long*)workspace;
     EC3R_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * (size_t)n_keyframes, st));
+    if (amb_out && !amb_count) return EC3R_EARG;
+    if (amb_count) EC3R_CUDA_TRY(cudaMemsetAsync(amb_count, 0, sizeof(unsigned long long), st));
     if (n_points > 0) {
         int64_t gx = (n_points + 255) / 256;
         if (gx > 4 * kNumSMs) gx = 4 * kNumSMs;
@@ -108,11 +133,18 @@ extern "C" int ec3r_local_candidates(const double* positions, int64_t n_points, 
         // width - 1, height - 1 as the reference compares against ints
         lc_count_kernel<<<grid, 256, 0, st>>>(positions, n_points, world_from_cam, intrinsics_h[0], intrinsics_h[1],
                                               intrinsics_h[2], intrinsics_h[3], intrinsics_h[4] - 1.0,
-                                              intrinsics_h[5] - 1.0, counts);
+                                              intrinsics_h[5] - 1.0, counts, amb_out, amb_cap, amb_count);
         EC3R_CHECK_LAUNCH("lc_count_kernel");
     }
     lc_decide_kernel<<<(n_keyframes + 127) / 128, 128, 0, st>>>(counts, n_keyframes, n_points, tau_p, out_counts,
                                                                out_cand);
     EC3R_CHECK_LAUNCH("lc_decide_kernel");
     return EC3R_OK;
+}
+
+extern "C" int ec3r_local_candidates(const double* positions, int64_t n_points, const double* world_from_cam,
+                                     int n_keyframes, const double* intrinsics_h, double tau_p, int64_t* out_counts,
+                                     int32_t* out_cand, void* workspace, size_t workspace_bytes, void* stream) {
+    return ec3r_local_candidates_ex(positions, n_points, world_from_cam, n_keyframes, intrinsics_h, tau_p, out_counts,
+                                    out_cand, nullptr, 0, nullptr, workspace, workspace_bytes, stream);
 }

@@ -359,8 +359,8 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     unsigned char* sA = smem;                                   // TC_NA * KB boxes
     unsigned char* sB = sA + (size_t)TC_NA * KB * TC_BOX_BYTES;  // TC_STAGES boxes
     float2* colbuf = (float2*)(sB + (size_t)TC_STAGES * TC_BOX_BYTES);  // [2 tiles][4 quarters][TC_BN]
-    float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);                     // [TC_NA * TC_BM] half-row summaries
-    uint64_t* bars = (uint64_t*)(rsc + TC_NA * TC_BM);
+    float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);                     // [2 units][TC_NA * TC_BM] half-row summaries
+    uint64_t* bars = (uint64_t*)(rsc + 2 * TC_NA * TC_BM);
     uint64_t* a_full = bars + 0;   // per k-block slice of the resident A (both blocks)
     uint64_t* a_empty = bars + 4;
     uint64_t* b_full = bars + 8;
@@ -484,7 +484,8 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // before reusing that buffer two tiles later
         const bool merger = et < TC_BN;
         int ttile = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        int uiter = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++uiter) {
             const TcUnit un = p.units[u];
             const int64_t a1 = p.a_off[un.pair + 1];
             const int64_t b0 = p.b_off[un.pair], b1 = p.b_off[un.pair + 1];
@@ -560,7 +561,11 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             }
             // the two column-half warps of a quarter hold partial states of
             // the same rows: h = 1 hands its (best, second, column) over
-            const int ti = q * 32 + lane;
+            // rsc is double-buffered by unit parity: with split barriers the
+            // h = 1 warps can finish a 1-2 tile unit and write its summaries
+            // while the h = 0 warps still read the previous unit's; the buffer
+            // they reuse two units later is ordered by the named_sync(1) in between
+            const int ti = q * 32 + lane + (uiter & 1) * (TC_NA * TC_BM);
             const int c0 = R0.cb + (int)((__float_as_uint(R0.b) >> 6) & 31u);
             const int c1 = R1.cb + (int)((__float_as_uint(R1.b) >> 6) & 31u);
             if (h == 1) {
@@ -882,7 +887,7 @@ static bool make_map(CUtensorMap* m, const uint16_t* base, int64_t rows, int D) 
 
 static size_t tc_smem_bytes(int kblocks) {
     return 1024 + (size_t)TC_NA * kblocks * TC_BOX_BYTES + (size_t)TC_STAGES * TC_BOX_BYTES +
-           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * TC_NA * TC_BM + 8 * (8 + 2 * TC_STAGES + 4) + 16;
+           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * 2 * TC_NA * TC_BM + 8 * (8 + 2 * TC_STAGES + 4) + 16;
 }
 
 // column slots: one per (unit, column) = sum over pairs of ceil(N/256) * M

@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ec3r {
@@ -580,6 +583,29 @@ __host__ __device__ inline size_t chain_smem(int n_sub, int n_edges) {
            sizeof(int32_t) * (2 * (size_t)n_edges + 2 * n_sub + 1) + 16;
 }
 
+// Submap j's registration outcome (mapping.py:162-211): submap 0 is the
+// chain's fixed root (the first submap, or a sharded window's halo stub).
+// For j > 0 the partners are the earlier submaps that were committed
+// (status OK); edges to them are walked in partner order: SKIP edges
+// (< min_correspondences) are dropped, the first error status aborts the
+// submap (align_point_sets raises out of the loop), and no surviving edge
+// means NoSharedKeyframes (SKIP).  Returns the strongest edge (max count,
+// first on ties) or -1.
+__device__ inline int chain_select(int j, const int32_t* eo, const int32_t* est, const int64_t* ec,
+                                   const int32_t* ep, const int32_t* sst, int* st_out) {
+    *st_out = EC3R_ST_OK;
+    if (j == 0) return -1;
+    int best = -1;
+    for (int e = eo[j]; e < eo[j + 1]; ++e) {
+        if (sst[ep[e]] != EC3R_ST_OK) continue;
+        if (est[e] == EC3R_ST_SKIP) continue;
+        if (est[e] != EC3R_ST_OK) { *st_out = est[e]; return -1; }
+        if (best < 0 || ec[e] > ec[best]) best = e;
+    }
+    if (best < 0) *st_out = EC3R_ST_SKIP;
+    return best;
+}
+
 __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
     const double* __restrict__ esim, const int64_t* __restrict__ ecount, const int32_t* __restrict__ estatus,
     const int32_t* __restrict__ epartner, const int32_t* __restrict__ sub_edge_off, int n_sub,
@@ -618,6 +644,7 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
     // arrays fit next to the staged inputs: every submap's strongest edge is
     // known up front, so global_j = global_root o (T_a o ... o T_j) and the
     // chain takes log2(depth) rounds instead of n_sub dependent steps
+    int32_t* sst_w = sst;
     const size_t base_b = chain_smem(n_sub, n_edges);
     const bool par = staged && base_b + chain_par_extra(n_sub) <= smem_cap;
     if (par) {
@@ -627,16 +654,21 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
         int* an1 = an0 + n_sub;
         int* rt0 = an1 + n_sub;
         int* rt1 = rt0 + n_sub;
+        // statuses and strongest edges first (sequential: a submap that is
+        // not committed is not a partner of later submaps)
+        if (threadIdx.x == 0)
+            for (int j = 0; j < n_sub; ++j) {
+                int st;
+                const int best = chain_select(j, eo, est, ec, ep, sst_w, &st);
+                sst_w[j] = st;
+                an0[j] = best >= 0 ? ep[best] : -1;
+                rt0[j] = best >= 0 ? -1 : j;
+                rt1[j] = best;
+            }
+        __syncthreads();
         for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
-            const int e0 = eo[j], e1 = eo[j + 1];
-            int best = -1;
-            for (int e = e0; e < e1; ++e)
-                if (est[e] == EC3R_ST_OK && (best < 0 || ec[e] > ec[best])) best = e;
-            const bool linked = e1 > e0 && best >= 0;
-            if (sst) sst[j] = (e1 > e0 && best < 0) ? EC3R_ST_SKIP : EC3R_ST_OK;  // SKIP: NoSharedKeyframes
-            an0[j] = linked ? ep[best] : -1;
-            rt0[j] = linked ? -1 : j;
-            for (int k = 0; k < 8; ++k) T0[8 * j + k] = linked ? es[8 * best + k] : (k < 2 ? 1.0 : 0.0);
+            const int best = rt1[j];
+            for (int k = 0; k < 8; ++k) T0[8 * j + k] = best >= 0 ? es[8 * best + k] : (k < 2 ? 1.0 : 0.0);
         }
         __syncthreads();
         for (int span = 1; span < n_sub; span <<= 1) {
@@ -671,23 +703,16 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
                 for (int k = 0; k < 8; ++k) g[8 * j + k] = T1[8 * j + k];
     } else if (threadIdx.x == 0) {
         for (int j = 0; j < n_sub; ++j) {
-            const int e0 = eo[j], e1 = eo[j + 1];
-            int best = -1;
-            for (int e = e0; e < e1; ++e)
-                if (est[e] == EC3R_ST_OK && (best < 0 || ec[e] > ec[best])) best = e;
-            int st = EC3R_ST_OK;
-            if (e1 > e0) {
-                if (best < 0) st = EC3R_ST_SKIP;  // NoSharedKeyframes
-                else sim3_compose_dev(g + 8 * ep[best], es + 8 * best, g + 8 * j);
-            }
-            if (sst) sst[j] = st;
+            int st;
+            const int best = chain_select(j, eo, est, ec, ep, sst_w, &st);
+            sst_w[j] = st;
+            if (best >= 0) sim3_compose_dev(g + 8 * ep[best], es + 8 * best, g + 8 * j);
         }
     }
     __syncthreads();
     if (staged) {
         for (int i = threadIdx.x; i < 8 * n_sub; i += CHAIN_NT) sub_globals[i] = g[i];
-        if (sub_status)
-            for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) sub_status[j] = sst[j];
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) sub_status[j] = sst[j];
     }
     const int s_end = sub_slot_off[n_sub];
     for (int sidx = threadIdx.x; sidx < s_end; sidx += CHAIN_NT) {
@@ -710,15 +735,18 @@ extern "C" int ec3r_chain_poses(const double* edge_sim3, const int64_t* edge_cou
                                 const int32_t* edge_partner, const int32_t* sub_edge_off, int n_sub,
                                 const int32_t* sub_slot_off, double* sub_globals, double* slot_globals,
                                 int32_t* sub_status, void* stream) {
-    if (n_sub < 0 || !sub_edge_off || !sub_globals) return EC3R_EARG;
+    if (n_sub < 0 || !sub_edge_off || !sub_globals || !sub_status) return EC3R_EARG;
     if (n_sub == 0) return EC3R_OK;
     // the edge count lives on the device: reserve the full opt-in shared
     // memory; a chain that does not fit walks global memory instead
     const size_t smem = 227 * 1024;
+    // test knob: a smaller cap forces the staged-sequential or the global walk
+    size_t cap = smem;
+    if (const char* e = getenv("EC3R_CHAIN_SMEM_CAP")) cap = std::min(smem, (size_t)strtoull(e, nullptr, 10));
     EC3R_CUDA_TRY(cudaFuncSetAttribute(chain_poses_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     chain_poses_kernel<<<1, CHAIN_NT, smem, as_stream(stream)>>>(edge_sim3, edge_count, edge_status, edge_partner,
                                                                 sub_edge_off, n_sub, sub_slot_off, sub_globals,
-                                                                slot_globals, sub_status, smem);
+                                                                slot_globals, sub_status, cap);
     EC3R_CHECK_LAUNCH("chain_poses_kernel");
     return EC3R_OK;
 }

@@ -86,6 +86,85 @@ def retrieval_device(pooled: torch.Tensor, stride: int, exclusion: int, tau_g: f
     return tuple(_to_host(x) for x in outs) if outs[0].is_cuda else tuple(x.numpy() for x in outs)
 
 
+# Margin guard.  The device scores with a sequential fma dot, the reference
+# with numpy's BLAS ddot (loops.py:205): the two agree to a few ulps
+# (|error| <= D * 2^-52 * sum|a_k b_k| ~ 1e-14 for unit vectors), so only a
+# score within GUARD_BAND of tau_global / tau_local can be decided
+# differently.  Those pairs are re-scored on the host with the reference's
+# own expression, float(pa @ pb), and every decision is taken on that score.
+GUARD_BAND = 1e-12
+_guard_stats = {"coarse_rescored": 0, "refine_rescored": 0, "coarse_flips": 0, "refine_flips": 0}
+
+
+def last_guard_stats() -> dict:
+    return dict(_guard_stats)
+
+
+def _window_pairs(a: int, b: int, stride: int, exclusion: int, K: int):
+    """Refinement window of a coarse hit in the reference's order
+    (loops.py:228-238): (da, db) ascending, in bounds, outside exclusion."""
+    out = []
+    for da in range(-(stride - 1), stride):
+        for db in range(-(stride - 1), stride):
+            ia, ib = a + da, b + db
+            if 0 <= ia < K and 0 <= ib < K and abs(ia - ib) >= exclusion:
+                out.append((ia, ib))
+    return out
+
+
+def guard_retrieval(host_pooled: np.ndarray, outs, stride: int, exclusion: int, tau_g: float, tau_l: float,
+                    band: float = GUARD_BAND):
+    """Apply the margin guard to retrieval_device's lists (ORDER indices).
+    host_pooled: (K, D) float64, the vectors the reference multiplies."""
+    cp, cs, qp, qs, ep, es = outs
+    for k in _guard_stats:
+        _guard_stats[k] = 0
+    P = host_pooled
+    K = P.shape[0]
+
+    def rescore(pairs):
+        return np.array([float(P[i] @ P[j]) for i, j in pairs], dtype=np.float64)
+
+    near = np.flatnonzero(np.abs(cs - tau_g) < band)
+    flips = []
+    if near.size:
+        cs = cs.copy()
+        old = cs[near] > tau_g
+        cs[near] = rescore(cp[near])
+        _guard_stats["coarse_rescored"] = int(near.size)
+        flips = near[(cs[near] > tau_g) != old].tolist()
+        _guard_stats["coarse_flips"] = len(flips)
+    if flips:
+        # rebuild the refinement groups in coarse emission order: unchanged
+        # hits keep the device's scored group, flipped-in hits are scored here
+        dev_hits = np.flatnonzero(np.where(np.isin(np.arange(len(cs)), flips), ~(cs > tau_g), cs > tau_g))
+        sizes = [len(_window_pairs(int(cp[h, 0]), int(cp[h, 1]), stride, exclusion, K)) for h in dev_hits]
+        groups = dict(zip(dev_hits.tolist(), np.split(np.arange(len(ep)), np.cumsum(sizes)[:-1]) if sizes else []))
+        new_p, new_s = [], []
+        for h in np.flatnonzero(cs > tau_g).tolist():
+            if h in groups:
+                idx = groups[h]
+                new_p.append(ep[idx])
+                new_s.append(es[idx])
+            else:
+                w = _window_pairs(int(cp[h, 0]), int(cp[h, 1]), stride, exclusion, K)
+                new_p.append(np.asarray(w, np.int32).reshape(-1, 2))
+                new_s.append(rescore(w))
+        ep = np.concatenate(new_p) if new_p else np.zeros((0, 2), np.int32)
+        es = np.concatenate(new_s) if new_s else np.zeros(0)
+    near_r = np.flatnonzero(np.abs(es - tau_l) < band)
+    if near_r.size:
+        es = es.copy()
+        old = es[near_r] > tau_l
+        es[near_r] = rescore(ep[near_r])
+        _guard_stats["refine_rescored"] = int(near_r.size)
+        _guard_stats["refine_flips"] = int(((es[near_r] > tau_l) != old).sum())
+    if flips or near_r.size:
+        keep = es > tau_l
+        qp, qs = ep[keep], es[keep]
+    return cp, cs, qp, qs, ep, es
+
+
 _pinned: dict = {}
 
 
@@ -145,10 +224,13 @@ def update_similarity(matrix, database, stride: int, cfg) -> list:
     if not order:
         return []
     pooled = torch.as_tensor(np.stack([np.asarray(database.get(kf).pooled, np.float64) for kf in order]),
-                             device="cuda")
+                             device="cuda")  # the host stack is kept for the margin guard
     kfs = np.asarray(order, dtype=np.int64)
-    cp, cs, qp, qs, ep, es = retrieval_device(pooled, int(stride), int(cfg.exclusion_zone()),
-                                              float(cfg.tau_global), float(cfg.tau_local))
+    host = np.stack([np.asarray(database.get(kf).pooled, np.float64) for kf in order])
+    outs = retrieval_device(pooled, int(stride), int(cfg.exclusion_zone()), float(cfg.tau_global),
+                            float(cfg.tau_local))
+    cp, cs, qp, qs, ep, es = guard_retrieval(host, outs, int(stride), int(cfg.exclusion_zone()),
+                                             float(cfg.tau_global), float(cfg.tau_local))
     _populate(matrix, kfs, cp, cs)
     _populate(matrix, kfs, ep, es)
     return admit(matrix, kfs, qp, qs)
@@ -163,10 +245,12 @@ class RetrievalDB:
         self.dim = int(dim)
         self.vec = torch.zeros((capacity, self.dim), dtype=torch.float64, device=self.device)
         self.kf = np.zeros(capacity, dtype=np.int64)
+        self.host = np.zeros((capacity, self.dim), dtype=np.float64)  # margin-guard copy (host side of append)
         self.n = 0
 
     def append(self, kf_ids, pooled):
-        pooled = torch.as_tensor(np.asarray(pooled, np.float64).reshape(-1, self.dim), device=self.device)
+        pooled_h = np.asarray(pooled, np.float64).reshape(-1, self.dim)
+        pooled = torch.as_tensor(pooled_h, device=self.device)
         k = pooled.shape[0]
         if self.n + k > self.vec.shape[0]:
             cap = self.vec.shape[0]
@@ -178,12 +262,20 @@ class RetrievalDB:
             kf = np.zeros(cap, np.int64)
             kf[: self.n] = self.kf[: self.n]
             self.kf = kf
+            hv = np.zeros((cap, self.dim), np.float64)
+            hv[: self.n] = self.host[: self.n]
+            self.host = hv
         self.vec[self.n:self.n + k] = pooled
+        self.host[self.n:self.n + k] = pooled_h
         self.kf[self.n:self.n + k] = np.asarray(kf_ids, np.int64)
         self.n += k
 
-    def score(self, stride: int, exclusion: int, tau_g: float, tau_l: float, k_begin: int = 0, k_end: int = -1):
-        return retrieval_device(self.vec[: self.n], stride, exclusion, tau_g, tau_l, k_begin, k_end)
+    def score(self, stride: int, exclusion: int, tau_g: float, tau_l: float, k_begin: int = 0, k_end: int = -1,
+              guard: bool = True):
+        outs = retrieval_device(self.vec[: self.n], stride, exclusion, tau_g, tau_l, k_begin, k_end)
+        if not guard:
+            return outs
+        return guard_retrieval(self.host[: self.n], outs, stride, exclusion, tau_g, tau_l)
 
     def update(self, matrix, stride: int, cfg, k_begin: int = 0, k_end: int = -1) -> list:
         cp, cs, qp, qs, ep, es = self.score(stride, cfg.exclusion_zone(), cfg.tau_global, cfg.tau_local,
@@ -198,11 +290,12 @@ class RetrievalDB:
 # Local loop candidates (loops.py:114-133; K8, csrc/local_cand.cu)
 
 def local_candidates_device(positions: torch.Tensor, world_from_cam: torch.Tensor, intrinsics, tau_p: float,
-                            stream=None):
+                            stream=None, ambiguous: bool = False, amb_cap: int = 4096):
     """Projection counts of the map points (N, 3) float64 into K keyframes
     (world_from_cam: (K, 8) float64 {s, q, t}) in one launch.  Returns
     (counts (K,) int64, candidate (K,) int32) CUDA tensors; intrinsics =
-    (fx, fy, cx, cy, width, height)."""
+    (fx, fy, cx, cy, width, height).  ambiguous=True also returns the
+    margin-guard list (n, 3) int32 numpy (keyframe, point, device decision)."""
     L = _lib.lib()
     pts = positions.reshape(-1, 3).to(torch.float64).contiguous()
     poses = world_from_cam.reshape(-1, 8).to(torch.float64).contiguous()
@@ -211,26 +304,74 @@ def local_candidates_device(positions: torch.Tensor, world_from_cam: torch.Tenso
     cand = torch.empty(max(K, 1), dtype=torch.int32, device=poses.device)
     intr = np.ascontiguousarray(np.asarray(intrinsics, dtype=np.float64).reshape(6))
     ws = _lib.workspace(L.ec3r_local_candidates_workspace(K), poses.device, "local_cand")
-    _lib.check(L.ec3r_local_candidates(_lib.ptr(pts) if pts.shape[0] else None, int(pts.shape[0]), _lib.ptr(poses),
-                                       K, intr.ctypes.data, float(tau_p), _lib.ptr(counts), _lib.ptr(cand),
-                                       _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)), "ec3r_local_candidates")
-    return counts[:K], cand[:K]
+    while True:
+        amb = torch.empty((max(amb_cap, 1), 3), dtype=torch.int32, device=poses.device) if ambiguous else None
+        n_amb = torch.zeros(1, dtype=torch.int64, device=poses.device) if ambiguous else None
+        _lib.check(L.ec3r_local_candidates_ex(_lib.ptr(pts) if pts.shape[0] else None, int(pts.shape[0]),
+                                              _lib.ptr(poses), K, intr.ctypes.data, float(tau_p), _lib.ptr(counts),
+                                              _lib.ptr(cand), _lib.ptr(amb), int(amb_cap), _lib.ptr(n_amb),
+                                              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
+                   "ec3r_local_candidates_ex")
+        if not ambiguous:
+            return counts[:K], cand[:K]
+        n = int(n_amb.item())
+        if n <= amb_cap:
+            return counts[:K], cand[:K], amb[:n].cpu().numpy()
+        amb_cap = 2 * n
+
+
+def _reference_visible(world_from_cam, k, positions: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """Visibility of positions[idx] exactly as project_points computes it
+    (geometry.py:87-109 under world_from_cam.inverse(), loops.py:129): the
+    matmul runs over the whole array, as the reference's does."""
+    pose = world_from_cam.inverse()
+    pc = positions @ pose.rotation.matrix().T + pose.translation
+    pc = pc[idx]
+    z = pc[:, 2]
+    safe_z = np.where(np.abs(z) > 1e-6, z, 1.0)
+    u = k.fx * pc[:, 0] / safe_z + k.cx
+    v = k.fy * pc[:, 1] / safe_z + k.cy
+    return (z > 1e-6) & (u >= 0.0) & (u <= k.width - 1) & (v >= 0.0) & (v <= k.height - 1)
+
+
+_local_guard_stats = {"ambiguous": 0, "flips": 0}
 
 
 def detect_local_candidates(sparse_map, window, k, cfg) -> list:
     """loops.py:114-133 — keyframes of `window` ((kf_id, world_from_cam)
-    pairs) that see more than cfg.tau_p of the live map's points."""
+    pairs) that see more than cfg.tau_p of the live map's points.  Points
+    within the margin band of the image border are re-decided on the host
+    with the reference's expression (the device's summation order differs
+    from BLAS's by ulps)."""
     from .types import sim3_to_vec
 
     _lib.lib()
     positions = sparse_map.positions()
     if len(positions) == 0 or len(window) == 0:
         return []
-    pts = torch.as_tensor(np.ascontiguousarray(np.asarray(positions, dtype=np.float64)), device="cuda")
+    pos = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+    pts = torch.as_tensor(pos, device="cuda")
     poses = torch.as_tensor(np.stack([sim3_to_vec(p) for _, p in window]), device="cuda")
-    _, cand = local_candidates_device(pts, poses, (k.fx, k.fy, k.cx, k.cy, k.width, k.height), cfg.tau_p)
-    c = cand.cpu().numpy()
+    counts, cand, amb = local_candidates_device(pts, poses, (k.fx, k.fy, k.cx, k.cy, k.width, k.height),
+                                                cfg.tau_p, ambiguous=True)
+    c = cand.cpu().numpy().astype(bool)
+    _local_guard_stats["ambiguous"] = int(len(amb))
+    _local_guard_stats["flips"] = 0
+    if len(amb):
+        cnt = counts.cpu().numpy().astype(np.int64)
+        for kk in np.unique(amb[:, 0]).tolist():
+            rows = amb[amb[:, 0] == kk]
+            vis = _reference_visible(window[kk][1], k, pos, rows[:, 1])
+            delta = int(vis.sum()) - int(rows[:, 2].sum())
+            if delta:
+                _local_guard_stats["flips"] += int((vis != rows[:, 2].astype(bool)).sum())
+                cnt[kk] += delta
+                c[kk] = cnt[kk] / len(pos) > cfg.tau_p
     return [kf for (kf, _), ok in zip(window, c) if ok]
+
+
+def last_local_guard_stats() -> dict:
+    return dict(_local_guard_stats)
 
 
 # -- loop verification (loops.py:136-153) on K5 + K9 -----------------------

@@ -164,6 +164,12 @@ class ChainPlan:
         self.sub_edge_off = t(sub_edge_off)
         self.sub_slot_off = t(np.concatenate([[0], np.cumsum([len(sm.slots) for sm in self.sms])]))
         self.slot0 = int(self.sms[0].slots[0]) if self.sms else 0
+        # the chain kernel writes slot globals through sub_slot_off from slot0:
+        # the submaps' slots must be contiguous and in order
+        if self.sms:
+            all_slots = np.concatenate([np.asarray(sm.slots, np.int64) for sm in self.sms])
+            if not np.array_equal(all_slots, np.arange(self.slot0, self.slot0 + all_slots.size)):
+                raise ValueError("ChainPlan needs the submaps' pool slots contiguous and in registration order")
         self.n_edges = len(pairs)
 
     def run(self, pool: FramePool, config: MappingConfig = MappingConfig(), sub_globals: Optional[torch.Tensor] = None,

@@ -300,3 +300,69 @@ def test_prefix_offsets_compose_in_rank_order():
         np.testing.assert_allclose(np.abs(np.dot(got.rotation.q, acc.rotation.q)), 1.0, atol=1e-12)
         acc = acc.compose(vec_to_sim3(W[r]))
     np.testing.assert_array_equal(offs[0], sim3_to_vec(Sim3Transform.identity()))
+
+
+# --------------------------------------------------------------------------
+# sharded retrieval (dist.retrieval_sharded): per-rank coarse rows, ragged
+# all-gather in rank order == the single-process lists
+
+def _shard_lists(P, stride, excl, tau_g, tau_l, kb, ke):
+    """Test-side restatement of the six K6 lists for coarse rows [kb, ke)
+    in the reference's emission order (loops.py:218-243)."""
+    K = P.shape[0]
+    Kc = (K + stride - 1) // stride
+    cp, cs, qp, qs, ep, es = [], [], [], [], [], []
+    for ai in range(kb, ke):
+        for bi in range(ai + 1, Kc):
+            a, b = ai * stride, bi * stride
+            if abs(a - b) < excl:
+                continue
+            s = float(P[a] @ P[b])
+            cp.append((a, b))
+            cs.append(s)
+            if s <= tau_g:
+                continue
+            for da in range(-(stride - 1), stride):
+                for db in range(-(stride - 1), stride):
+                    ia, ib = a + da, b + db
+                    if 0 <= ia < K and 0 <= ib < K and abs(ia - ib) >= excl:
+                        sn = float(P[ia] @ P[ib])
+                        ep.append((ia, ib))
+                        es.append(sn)
+                        if sn > tau_l:
+                            qp.append((ia, ib))
+                            qs.append(sn)
+    f = lambda p: np.asarray(p, np.int32).reshape(-1, 2)  # noqa: E731
+    return f(cp), np.asarray(cs), f(qp), np.asarray(qs), f(ep), np.asarray(es)
+
+
+def _retrieval_db(K=300):
+    from paper_2510_02080_b200 import synth
+    return synth.pooled_embeddings(K, device="cpu").numpy()
+
+
+class _HostShardDB:
+    """RetrievalDB stand-in whose score() is the restated lists (CPU)."""
+
+    def __init__(self, P):
+        self.P, self.n = P, P.shape[0]
+        self.vec = torch.as_tensor(P)
+
+    def score(self, stride, excl, tau_g, tau_l, kb, ke):
+        return _shard_lists(self.P, stride, excl, tau_g, tau_l, kb, ke)
+
+
+def w_retrieval(rank, world):
+    db = _HostShardDB(_retrieval_db())
+    return D.retrieval_sharded(db, 5, 15, 0.93, 0.96)
+
+
+def test_retrieval_sharded_merge_equals_single_gloo():
+    out = _spawn("w_retrieval")
+    P = _retrieval_db()
+    Kc = (P.shape[0] + 4) // 5
+    exp = _shard_lists(P, 5, 15, 0.93, 0.96, 0, Kc)
+    assert len(exp[2]) > 0 and len(exp[0]) > 0  # the case has candidates
+    for r in range(WORLD):
+        for got, want in zip(out[r], exp):
+            np.testing.assert_array_equal(got, want)

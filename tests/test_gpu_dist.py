@@ -180,3 +180,57 @@ def test_window_chain_device_two_ranks_equals_single_chain():
             np.testing.assert_allclose(ref.canonical_quat(a[1:5]), ref.canonical_quat(b[1:5]), atol=1e-9)
             np.testing.assert_allclose(a[5:], b[5:], atol=1e-9 * max(1.0, float(np.abs(b[5:]).max())))
         np.testing.assert_array_equal(slot_g, np.repeat(sub_g, lens, axis=0))
+
+
+K_RET = 1200
+
+
+def _ret_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_02080_b200 import dist as D
+        from paper_2510_02080_b200 import loops, synth
+        torch.cuda.set_device(0)
+        pooled = synth.pooled_embeddings(K_RET, device="cpu").numpy()
+        db = loops.RetrievalDB(pooled.shape[1], 256)
+        db.append(np.arange(K_RET) * 3 + 7, pooled)
+        q.put((rank, D.retrieval_sharded(db, 5, 15, 0.93, 0.96)))
+    except Exception as e:
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_retrieval_sharded_two_ranks_equals_single_and_oracle():
+    """dist.retrieval_sharded with two ranks (gloo, one GPU): each rank scores
+    its coarse rows on the device; the gathered lists equal the single-GPU
+    lists, and the admitted pairs equal the oracle's update_similarity."""
+    from oracle import ref_numpy as ref
+    from paper_2510_02080_b200 import loops, synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ret_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for v in out.values():
+        if isinstance(v, Exception):
+            raise v
+    pooled = synth.pooled_embeddings(K_RET, device="cpu").numpy()
+    db = loops.RetrievalDB(pooled.shape[1], 256)
+    kfs = np.arange(K_RET) * 3 + 7
+    db.append(kfs, pooled)
+    single = db.score(5, 15, 0.93, 0.96)
+    for r in range(2):
+        for a, b in zip(out[r], single):
+            np.testing.assert_array_equal(a, b)
+    mat = loops.SimilarityMatrix()
+    got = loops.admit(mat, kfs, out[0][2], out[0][3])
+    exp = ref.update_similarity(ref.SimilarityState(), kfs, pooled, 5, 15, 0.93, 0.96)
+    assert [p for p, _ in got] == [p for p, _ in exp]
+    assert len(got) > 0

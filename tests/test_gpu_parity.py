@@ -497,6 +497,24 @@ def test_match_bench_shape_vs_oracle():
     assert st["rows_rescanned"] < 0.01 * st["rows"] and st["cols_rescanned"] < 0.01 * st["cols"], st
 
 
+def test_match_many_small_pairs_vs_oracle():
+    """Hundreds of pairs with M <= 256 give one- and two-tile units on every
+    CTA (> 148 units), the case where the epilogue's half-row summaries of
+    consecutive units could collide (match_tc.cu rsc double buffer)."""
+    from paper_2510_02080_b200 import synth, tracking
+    for n, m, n_pairs in ((200, 128, 600), (256, 256, 400), (97, 250, 333)):
+        A, B, ao, bo = synth.make_descriptor_pairs(n_pairs, n, m, 256, 0.05, seed=n * m)
+        mb, nm = tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)
+        mb = mb.cpu().numpy()
+        a = A.view(torch.bfloat16).double().cpu().numpy()
+        b = B.view(torch.bfloat16).double().cpu().numpy()
+        for p in range(n_pairs):
+            exp = ref.match_descriptors_vec(a[ao[p]:ao[p + 1]], b[bo[p]:bo[p + 1]], 0.8)
+            seg = mb[ao[p]:ao[p + 1]]
+            ia = np.flatnonzero(seg >= 0)
+            np.testing.assert_array_equal(np.stack([ia, seg[ia]], axis=1), exp, err_msg=f"{n}x{m} pair {p}")
+
+
 def test_match_batched_pairs_vs_oracle():
     from paper_2510_02080_b200 import tracking
     rng = np.random.default_rng(5)
