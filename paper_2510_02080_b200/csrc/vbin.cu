@@ -1,0 +1,1100 @@
+// K4: binned super-block voxel fusion (stage c) on sm_100a.
+//
+// Replaces Submap.world_points / Mapping.fused_cloud (mapping.py:56-57,
+// 332-338) under the declared fusion rule of oracle/fuse.py: keys are
+// _pack(floor(x / cell)) (_kernels/_numpy.py:50-55) of the exact float64
+// chain (fuse_common.cuh), per key sum conf, conf-weighted centroid and
+// count, output sorted by key.
+//
+// Why binned: the bench map has 18.7 points per voxel, almost all of it
+// reuse ACROSS frames (1.37 points per voxel inside one frame), so a
+// per-pixel hash update is one scattered L2 reduction per point.  Here the
+// points are first grouped by 8x8x8-voxel super-block ("bin", 16 cm at 2 cm)
+// and every bin is then accumulated in shared memory over all frames:
+//
+//  1. bf_bin_kernel (one pass over depth + confidence, 8 B/px): exact cells,
+//     then per warp iteration (128 pixels) a warp-local multisplit by bin
+//     (match.any + a short slot list), payload staged in shared memory and
+//     written coalesced into the CTA's own region (12 B/point: conf,
+//     9-bit voxel-in-bin index, 3 x 18-bit in-voxel offsets), and one
+//     segment record (start, count, bin id) per (iteration, bin).  Bin ids
+//     come from a small open-addressing table of super-block keys (a
+//     per-warp cache in front).  No global atomics per point.
+//  2. segments are counting-sorted by bin (scan + scatter).
+//  3. bf_aggregate_kernel (one CTA per bin): reads the bin's segments and
+//     accumulates every point into 512 shared-memory voxels with 64-bit
+//     fixed-point integer sums (exact, so the result is independent of the
+//     order -- run-to-run deterministic), then writes the occupied voxels
+//     once, in in-bin (x, y, z) order, with per-(bin, x, y) column counts.
+//  4. ordered emit: bins are sorted by key; for bins grouped by x then y,
+//     the global key order of the voxel columns is a closed-form
+//     interleave of (bin x, voxel x, bin y, voxel y, bin z); one exclusive
+//     scan of the column counts in that order gives every column its output
+//     offset and bf_permute_kernel writes the sorted map (no voxel sort).
+
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "vbin.cuh"
+
+namespace ec3r {
+
+constexpr int BF_NT = 256;
+constexpr int BF_WARPS = BF_NT / 32;
+#ifndef EC3R_BF_ROWS
+#define EC3R_BF_ROWS 32
+#endif
+constexpr int BF_ROWS = EC3R_BF_ROWS;  // image rows per CTA
+constexpr int BF_MAXS = 128;           // slots per warp iteration (<= its points)
+constexpr int BF_WC = 128;             // per-warp bin-id cache entries
+constexpr int BF_SBV = 512;            // voxels per bin (8^3)
+constexpr int BF_PTS_CTA = 4096;       // explicit-point kernel: points per CTA region
+constexpr int BF_QBITS = 18;           // in-voxel offset bits per axis
+#ifndef EC3R_BF_MINB
+#define EC3R_BF_MINB 2
+#endif
+
+struct __align__(16) BinEntry {
+    unsigned long long key;  // pack of super-block coordinates (cell >> 3)
+    int id;                  // bin id; -1 while being published, -2 overflow
+    int pad;
+};
+
+struct CtaDesc {
+    uint32_t base;  // first payload / segment entry of the CTA's region
+    uint32_t nseg;  // segment records the CTA wrote at base..
+};
+
+// counters
+enum { C_IN = 0, C_OOR, C_OVF, C_SLOW, C_BINS, C_VOX, C_VOX_OVF, C_SEGS, C_N };
+
+struct BinGroup {
+    int start_x, n_x, off_xy, n_xy, r_z, pad;
+};
+
+// Workspace layout of the aggregation + emit (grown on demand, owned here).
+struct BfWs {
+    uint32_t* seg_off;      // n_bins + 1
+    uint32_t* cursor;       // n_bins
+    unsigned long long* sorted;  // segments
+    unsigned long long* st_key;
+    float4* st_sum;
+    int32_t* st_cnt;
+    uint32_t* st_tag;
+    uint8_t* colcnt;        // n_bins * 64
+    unsigned long long* skeys;   // n_bins (sorted)
+    uint32_t* ids;          // n_bins
+    uint32_t* sids;         // n_bins
+    BinGroup* grp;          // n_bins
+    uint32_t* scan_in;      // n_bins * 64
+    uint32_t* col_base;     // n_bins * 64
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+
+struct BinFuse {
+    int64_t max_voxels = 0, max_bins = 0;
+    double cell = 0.02;
+    unsigned long long tmask = 0;
+    BinEntry* table = nullptr;
+    unsigned long long* bin_keys = nullptr;
+    uint32_t* bin_slot = nullptr;
+    uint32_t* bin_nseg = nullptr;
+    unsigned long long* ctr = nullptr;
+    // payload (3 u32 per entry) and segment records share one index space
+    uint32_t* pay = nullptr;
+    unsigned long long* seg = nullptr;
+    int64_t cap = 0, used = 0;  // entries
+    CtaDesc* cta = nullptr;
+    int64_t cta_cap = 0, cta_used = 0;
+    // aggregation / emit state
+    bool dirty = true;
+    int64_t n_bins = 0, U = 0;
+    char* ws = nullptr;
+    size_t ws_cap = 0;
+    BfWs view;  // carved views of ws (valid after aggregation)
+};
+
+// ---------------------------------------------------------------------------
+// bin table
+
+__device__ __forceinline__ void bf_load_entry(const BinEntry* e, unsigned long long& key, int& id) {
+    unsigned long long lo, hi;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(e) : "memory");
+    key = lo;
+    id = (int)(unsigned)(hi & 0xFFFFFFFFull);
+}
+
+__device__ __forceinline__ int bf_load_id(const BinEntry* e) {
+    int id;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(id) : "l"(&e->id) : "memory");
+    return id;
+}
+
+struct BinTab {
+    BinEntry* table;
+    unsigned long long tmask;
+    unsigned long long* bin_keys;
+    uint32_t* bin_slot;
+    unsigned long long* ctr;
+    int64_t max_bins;
+};
+
+// Find or allocate the bin of super-block key k (one thread).  Returns the
+// bin id or -2 when the table or the bin arrays are full.
+__device__ __noinline__ int bf_find_or_insert(const BinTab& t, unsigned long long k) {
+    unsigned long long h = table_slot(k, t.tmask);
+    for (unsigned long long probe = 0; probe <= t.tmask; ++probe) {
+        BinEntry* e = t.table + h;
+        unsigned long long ek;
+        int id;
+        bf_load_entry(e, ek, id);
+        if (ek == k) {
+            while (id == -1) id = bf_load_id(e);  // winner is publishing
+            return id;
+        }
+        if (ek == kEmpty) {
+            const unsigned long long prev = atomicCAS(&e->key, kEmpty, k);
+            if (prev == kEmpty) {
+                const unsigned long long slot = atomicAdd(&t.ctr[C_BINS], 1ull);
+                int got = -2;
+                if ((int64_t)slot < t.max_bins) {
+                    got = (int)slot;
+                    t.bin_keys[slot] = k;  // read by later kernels only
+                    t.bin_slot[slot] = (uint32_t)h;
+                }
+                atomicExch(&e->id, got);
+                return got;
+            }
+            if (prev == k) {
+                int i2 = bf_load_id(e);
+                while (i2 == -1) i2 = bf_load_id(e);
+                return i2;
+            }
+        }
+        h = (h + 1) & t.tmask;
+    }
+    return -2;
+}
+
+// ---------------------------------------------------------------------------
+// warp-level multisplit of one iteration's points by bin
+
+struct WarpSmem {
+    unsigned long long keys[BF_MAXS];  // slot -> bin key
+    uint32_t cnt[BF_MAXS];             // slot -> point count, then exclusive offset
+    uint32_t stage[3 * BF_MAXS];       // payload in slot order
+    unsigned long long ckey[BF_WC];    // bin-id cache (key, id), one writer per entry
+    int cid[BF_WC];
+};
+
+struct BinOut {
+    BinTab tab;
+    uint32_t* bin_nseg;
+    uint32_t* pay;
+    unsigned long long* seg;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Points k = 0..3 of each lane: valid, bin key bk, payload (w0 = conf bits,
+// pv = in-bin index | offsets).  Appends the valid points to the CTA region
+// (cursor *cta_pay, region base rbase) grouped by bin and one segment record
+// per bin.  Returns the number of points dropped (bin table overflow).
+__device__ __forceinline__ unsigned bf_warp_emit(const BinOut& o, WarpSmem& w, const bool (&valid)[4],
+                                                 const unsigned long long (&bk)[4], const uint32_t (&w0)[4],
+                                                 const unsigned long long (&pv)[4], uint32_t rbase,
+                                                 unsigned* cta_pay, unsigned* cta_seg) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    int ns = 0;  // warp-uniform
+    int slot[4];
+    unsigned rank[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        slot[k] = -1;
+        rank[k] = 0;
+        if (!__any_sync(0xffffffffu, valid[k])) continue;
+        const unsigned peers = __match_any_sync(0xffffffffu, valid[k] ? bk[k] : kEmpty);
+        const int leader = __ffs(peers) - 1;
+        const bool lead = valid[k] && lane == leader;
+        int s = -1;
+        if (lead)
+            for (int i = 0; i < ns; ++i)
+                if (w.keys[i] == bk[k]) { s = i; break; }
+        const unsigned nm = __ballot_sync(0xffffffffu, lead && s < 0);
+        if (lead && s < 0) {
+            s = ns + __popc(nm & lt);
+            w.keys[s] = bk[k];
+            w.cnt[s] = 0u;
+        }
+        ns += __popc(nm);
+        unsigned base = 0;
+        if (lead) {  // leaders hold distinct slots: plain read-modify-write
+            base = w.cnt[s];
+            w.cnt[s] = base + __popc(peers);
+        }
+        s = __shfl_sync(0xffffffffu, s, leader);
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (valid[k]) {
+            slot[k] = s;
+            rank[k] = base + __popc(peers & lt);
+        }
+    }
+    if (ns == 0) return 0u;
+    __syncwarp();
+    // exclusive scan of the slot counts (in place)
+    unsigned carry = 0;
+    for (int b0 = 0; b0 < ns; b0 += 32) {
+        const int i = b0 + lane;
+        const unsigned v = i < ns ? w.cnt[i] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (i < ns) w.cnt[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncwarp();
+    const unsigned total = carry;
+    // stage in slot order
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (slot[k] < 0) continue;
+        const unsigned p = w.cnt[slot[k]] + rank[k];
+        w.stage[3 * p] = w0[k];
+        w.stage[3 * p + 1] = (uint32_t)pv[k];
+        w.stage[3 * p + 2] = (uint32_t)(pv[k] >> 32);
+    }
+    unsigned gb = 0, sb = 0;
+    if (lane == 0) {
+        gb = atomicAdd(cta_pay, total);
+        sb = atomicAdd(cta_seg, (unsigned)ns);
+    }
+    gb = __shfl_sync(0xffffffffu, gb, 0);
+    sb = __shfl_sync(0xffffffffu, sb, 0);
+    __syncwarp();
+    uint32_t* dst = o.pay + 3 * (size_t)(rbase + gb);
+    for (unsigned i = lane; i < 3 * total; i += 32) dst[i] = w.stage[i];
+    // one segment record per slot: bin ids through the per-warp cache
+    unsigned dropped = 0;
+    for (int b0 = 0; b0 < ns; b0 += 32) {
+        const int s = b0 + lane;
+        const bool act = s < ns;
+        const unsigned long long key = act ? w.keys[s] : kEmpty;
+        const int ce = (int)(mix64(key) & (BF_WC - 1));
+        int id = -3;
+        if (act && w.ckey[ce] == key) id = w.cid[ce];
+        const bool miss = act && id == -3;
+        if (miss) id = bf_find_or_insert(o.tab, key);
+        // one writer per cache entry
+        const unsigned same = __match_any_sync(0xffffffffu, miss ? ce : -1);
+        __syncwarp();
+        if (miss && lane == __ffs(same) - 1 && id >= 0) {
+            w.ckey[ce] = key;
+            w.cid[ce] = id;
+        }
+        if (act) {
+            const unsigned beg = w.cnt[s];
+            const unsigned end = s + 1 < ns ? w.cnt[s + 1] : total;
+            if (id >= 0) {
+                o.seg[rbase + sb + s] = (unsigned long long)(rbase + gb + beg) |
+                                        ((unsigned long long)(end - beg - 1) << 32) | ((unsigned long long)id << 40);
+                atomicAdd(&o.bin_nseg[id], 1u);
+            } else {
+                // bins full: the segment is recorded empty (bin 0, count 0 is
+                // not representable) -- mark it with the all-ones id and drop
+                o.seg[rbase + sb + s] = ~0ull;
+                dropped += end - beg;
+            }
+        }
+        __syncwarp();
+    }
+    return dropped;
+}
+
+// payload of one point: in-bin voxel index (x major) and 18-bit offsets
+__device__ __forceinline__ unsigned long long bf_payload(int cx, int cy, int cz, float fx, float fy, float fz) {
+    const unsigned l = (unsigned)(cz & 7) | ((unsigned)(cy & 7) << 3) | ((unsigned)(cx & 7) << 6);
+    const float qs = (float)(1 << BF_QBITS);
+    const unsigned qx = min((unsigned)(fmaxf(fx, 0.f) * qs), (1u << BF_QBITS) - 1u);
+    const unsigned qy = min((unsigned)(fmaxf(fy, 0.f) * qs), (1u << BF_QBITS) - 1u);
+    const unsigned qz = min((unsigned)(fmaxf(fz, 0.f) * qs), (1u << BF_QBITS) - 1u);
+    return (unsigned long long)l | ((unsigned long long)qx << 9) | ((unsigned long long)qy << 27) |
+           ((unsigned long long)qz << 45);
+}
+
+// ---------------------------------------------------------------------------
+// 1. frame binning
+
+struct BinArgs {
+    BinOut out;
+    CtaDesc* cta;       // descriptor per CTA of this launch
+    uint32_t region0;   // first entry of this launch
+    uint32_t region;    // entries per CTA region
+    unsigned long long* ctr;
+};
+
+__global__ void __launch_bounds__(BF_NT, EC3R_BF_MINB) bf_bin_kernel(FrameGeom a, BinArgs b) {
+    extern __shared__ float4 sA[];  // A[W]
+    __shared__ float4 sB[BF_ROWS];
+    __shared__ WarpSmem wsm[BF_WARPS];
+    __shared__ unsigned cta_pay, cta_seg;
+    __shared__ unsigned long long cta_cnt[4];
+    const int W = a.W, H = a.H;
+    const int HW = H * W;
+    const int v_band = blockIdx.x * BF_ROWS;
+    const int rows = min(BF_ROWS, H - v_band);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpSmem& w = wsm[warp];
+    for (int i = lane; i < BF_WC; i += 32) w.ckey[i] = kEmpty;
+    if (threadIdx.x == 0) { cta_pay = 0u; cta_seg = 0u; }
+    if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0ull;
+    const int j = blockIdx.y;
+    const int slot = a.slots[j];
+    const float4* tab = a.ftab + (size_t)j * (W + H + 1);
+    for (int u = threadIdx.x; u < W; u += BF_NT) sA[u] = __ldg(tab + u);
+    if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
+    const float4 Tm = __ldg(tab + W + H);
+    __syncthreads();
+    const uint32_t rbase = b.region0 + (uint32_t)(blockIdx.y * gridDim.x + blockIdx.x) * b.region;
+    const float* dbase = a.depth + (size_t)slot * HW;
+    const float* cbase = a.conf + (size_t)slot * HW;
+    const float inv = a.inv_cell_f, cellf = a.cell_f;
+    constexpr int ST_H = 8, ST_W = 16;
+    const int dv = lane >> 2, du = 4 * (lane & 3);
+    const int stx = (W + ST_W - 1) / ST_W;
+    const bool pairs = (W & 1) == 0;
+    unsigned n_in = 0, n_oor = 0, n_slow = 0, n_drop = 0;
+    auto advance = [&](int& sy, int& sx) {
+        sx += BF_WARPS;
+        while (sx >= stx) { sx -= stx; ++sy; }
+    };
+    auto load4 = [&](int sy, int sx, float (&z)[4], float (&c)[4]) {
+        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { z[k] = 0.f; c[k] = 0.f; }
+        if (r >= rows) return;
+        const size_t off = (size_t)(v_band + r) * W + u0;
+        if (pairs) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (u0 + 2 * h + 1 < W) {
+                    const float2 z2 = __ldcs(reinterpret_cast<const float2*>(dbase + off + 2 * h));
+                    const float2 c2 = __ldcs(reinterpret_cast<const float2*>(cbase + off + 2 * h));
+                    z[2 * h] = z2.x; z[2 * h + 1] = z2.y;
+                    c[2 * h] = c2.x; c[2 * h + 1] = c2.y;
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (u0 + k < W) { z[k] = __ldcs(dbase + off + k); c[k] = __ldcs(cbase + off + k); }
+        }
+    };
+    const int n_sy = (rows + ST_H - 1) / ST_H;
+    int sy = 0, sx = warp;
+    while (sx >= stx) { sx -= stx; ++sy; }
+    int py = sy, px = sx;
+    float nz[4], nc[4];
+    if (py < n_sy) load4(py, px, nz, nc);
+    for (; sy < n_sy; advance(sy, sx)) {
+        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+        float zs[4], cs[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
+        advance(py, px);
+        if (py < n_sy) load4(py, px, nz, nc);
+        const float4 Bv = sB[min(r, rows - 1)];
+        Cells4 ce;
+        frame_cells4(a, sA, Bv, Tm, slot, u0, v_band + r, zs, cs, ce, n_in, n_oor, n_slow);
+        bool valid[4];
+        unsigned long long bk[4], pv[4];
+        uint32_t w0[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            valid[k] = ce.valid[k] && r < rows;
+            bk[k] = pack_block(ce.cx[k] >> 3, ce.cy[k] >> 3, ce.cz[k] >> 3);
+            pv[k] = bf_payload(ce.cx[k], ce.cy[k], ce.cz[k], (ce.x[k] - (float)ce.cx[k] * cellf) * inv,
+                               (ce.y[k] - (float)ce.cy[k] * cellf) * inv, (ce.z[k] - (float)ce.cz[k] * cellf) * inv);
+            w0[k] = __float_as_uint(cs[k]);
+        }
+        n_drop += bf_warp_emit(b.out, w, valid, bk, w0, pv, rbase, &cta_pay, &cta_seg);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
+        n_oor += __shfl_xor_sync(0xffffffffu, n_oor, o);
+        n_slow += __shfl_xor_sync(0xffffffffu, n_slow, o);
+        n_drop += __shfl_xor_sync(0xffffffffu, n_drop, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&cta_cnt[0], (unsigned long long)n_in);
+        atomicAdd(&cta_cnt[1], (unsigned long long)n_oor);
+        atomicAdd(&cta_cnt[2], (unsigned long long)n_drop);
+        atomicAdd(&cta_cnt[3], (unsigned long long)n_slow);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && cta_cnt[threadIdx.x]) atomicAdd(&b.ctr[threadIdx.x], cta_cnt[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        b.cta[blockIdx.y * gridDim.x + blockIdx.x] = CtaDesc{rbase, cta_seg};
+        if (cta_seg) atomicAdd(&b.ctr[C_SEGS], (unsigned long long)cta_seg);
+    }
+}
+
+// Explicit float64 points under one Sim(3) (exact transform): one point per
+// lane, BF_PTS_CTA points per CTA region.
+__global__ void __launch_bounds__(BF_NT) bf_points_kernel(const double* __restrict__ pts,
+                                                          const double* __restrict__ conf, int64_t n, Sim3Arg g,
+                                                          double cell, BinArgs b) {
+    __shared__ WarpSmem wsm[BF_WARPS];
+    __shared__ unsigned cta_pay, cta_seg;
+    __shared__ unsigned long long cta_cnt[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpSmem& w = wsm[warp];
+    for (int i = lane; i < BF_WC; i += 32) w.ckey[i] = kEmpty;
+    if (threadIdx.x == 0) { cta_pay = 0u; cta_seg = 0u; }
+    if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0ull;
+    __syncthreads();
+    const uint32_t rbase = b.region0 + (uint32_t)blockIdx.x * b.region;
+    const int64_t p0 = (int64_t)blockIdx.x * BF_PTS_CTA, p1 = min(n, p0 + BF_PTS_CTA);
+    unsigned n_in = 0, n_oor = 0, n_drop = 0;
+    for (int64_t i0 = p0 + warp * 32; i0 < p1; i0 += BF_NT) {
+        const int64_t i = i0 + lane;
+        bool valid[4] = {false, false, false, false};
+        unsigned long long bk[4] = {kEmpty, kEmpty, kEmpty, kEmpty}, pv[4] = {0, 0, 0, 0};
+        uint32_t w0[4] = {0, 0, 0, 0};
+        if (i < p1) {
+            const double c = conf[i];
+            if (c > 0) {
+                ++n_in;
+                const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+                double x[3];
+                sim3_apply_exact(g.v, p, x);
+                long long cc[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cc[k] = (long long)floor(__ddiv_rn(x[k], cell));
+                if (cell_in_range(cc[0]) && cell_in_range(cc[1]) && cell_in_range(cc[2])) {
+                    valid[0] = true;
+                    bk[0] = pack_block((int)(cc[0] >> 3), (int)(cc[1] >> 3), (int)(cc[2] >> 3));
+                    pv[0] = bf_payload((int)cc[0], (int)cc[1], (int)cc[2], (float)((x[0] - (double)cc[0] * cell) / cell),
+                                       (float)((x[1] - (double)cc[1] * cell) / cell),
+                                       (float)((x[2] - (double)cc[2] * cell) / cell));
+                    w0[0] = __float_as_uint((float)c);
+                } else {
+                    ++n_oor;
+                }
+            }
+        }
+        n_drop += bf_warp_emit(b.out, w, valid, bk, w0, pv, rbase, &cta_pay, &cta_seg);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_in += __shfl_xor_sync(0xffffffffu, n_in, o);
+        n_oor += __shfl_xor_sync(0xffffffffu, n_oor, o);
+        n_drop += __shfl_xor_sync(0xffffffffu, n_drop, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&cta_cnt[0], (unsigned long long)n_in);
+        atomicAdd(&cta_cnt[1], (unsigned long long)n_oor);
+        atomicAdd(&cta_cnt[2], (unsigned long long)n_drop);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && cta_cnt[threadIdx.x]) atomicAdd(&b.ctr[threadIdx.x], cta_cnt[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        b.cta[blockIdx.x] = CtaDesc{rbase, cta_seg};
+        if (cta_seg) atomicAdd(&b.ctr[C_SEGS], (unsigned long long)cta_seg);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 2. segments by bin (counting sort: offsets from a scan of bin_nseg)
+
+__global__ void bf_seg_scatter_kernel(const CtaDesc* __restrict__ cta, int64_t n_cta,
+                                      const unsigned long long* __restrict__ seg, const uint32_t* __restrict__ seg_off,
+                                      uint32_t* __restrict__ cursor, unsigned long long* __restrict__ sorted) {
+    for (int64_t c = blockIdx.x; c < n_cta; c += gridDim.x) {
+        const CtaDesc d = cta[c];
+        for (uint32_t i = threadIdx.x; i < d.nseg; i += blockDim.x) {
+            const unsigned long long r = seg[d.base + i];
+            if (r == ~0ull) continue;
+            const uint32_t id = (uint32_t)(r >> 40);
+            sorted[seg_off[id] + atomicAdd(&cursor[id], 1u)] = r;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 3. per-bin aggregation (one CTA per bin)
+
+__device__ __forceinline__ void add64(uint32_t* lo, uint32_t* hi, unsigned long long t) {
+    const uint32_t tl = (uint32_t)t, th = (uint32_t)(t >> 32);
+    const uint32_t old = atomicAdd(lo, tl);
+    const uint32_t carry = (old + tl < old) ? 1u : 0u;
+    if (th + carry) atomicAdd(hi, th + carry);
+}
+
+__global__ void __launch_bounds__(BF_NT) bf_aggregate_kernel(
+    const unsigned long long* __restrict__ bin_keys, const uint32_t* __restrict__ seg_off,
+    const unsigned long long* __restrict__ sorted, const uint32_t* __restrict__ pay, double cell, int64_t max_voxels,
+    unsigned long long* __restrict__ ctr, unsigned long long* __restrict__ st_key, float4* __restrict__ st_sum,
+    int32_t* __restrict__ st_cnt, uint32_t* __restrict__ st_tag, uint8_t* __restrict__ colcnt) {
+    __shared__ uint32_t lo[4][BF_SBV], hi[4][BF_SBV], cnt[BF_SBV];
+    __shared__ uint32_t ex[BF_SBV + 1];
+    __shared__ unsigned long long base_s;
+    typedef cub::BlockScan<uint32_t, BF_NT> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    const int b = blockIdx.x;
+    for (int i = threadIdx.x; i < BF_SBV; i += BF_NT) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { lo[k][i] = 0u; hi[k][i] = 0u; }
+        cnt[i] = 0u;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t s0 = seg_off[b], s1 = seg_off[b + 1];
+    for (uint32_t s = s0 + warp; s < s1; s += BF_WARPS) {
+        const unsigned long long r = sorted[s];
+        const uint32_t start = (uint32_t)r, n = (uint32_t)((r >> 32) & 0xFF) + 1u;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t* e = pay + 3 * (size_t)(start + i);
+            const float c = __uint_as_float(__ldcs(e));
+            const unsigned long long v = (unsigned long long)__ldcs(e + 1) | ((unsigned long long)__ldcs(e + 2) << 32);
+            const int l = (int)(v & 511u);
+            const float qx = (float)((v >> 9) & 0x3FFFFu) + 0.5f, qy = (float)((v >> 27) & 0x3FFFFu) + 0.5f,
+                        qz = (float)((v >> 45) & 0x3FFFFu) + 0.5f;
+            // fixed point: conf * 2^31, conf * frac * 2^31 (frac = q / 2^18)
+            add64(&lo[0][l], &hi[0][l], __float2ull_rn(c * 2147483648.f));
+            add64(&lo[1][l], &hi[1][l], __float2ull_rn(c * qx * 8192.f));
+            add64(&lo[2][l], &hi[2][l], __float2ull_rn(c * qy * 8192.f));
+            add64(&lo[3][l], &hi[3][l], __float2ull_rn(c * qz * 8192.f));
+            atomicAdd(&cnt[l], 1u);
+        }
+    }
+    __syncthreads();
+    // occupied voxels in in-bin order (x major): exclusive positions
+    const int l0 = 2 * threadIdx.x;
+    uint32_t f[2] = {cnt[l0] ? 1u : 0u, cnt[l0 + 1] ? 1u : 0u};
+    uint32_t e[2], total;
+    BS(scan_tmp).ExclusiveSum(f, e, total);
+    ex[l0] = e[0];
+    ex[l0 + 1] = e[1];
+    if (threadIdx.x == 0) {
+        ex[BF_SBV] = total;
+        base_s = atomicAdd(&ctr[C_VOX], (unsigned long long)total);
+    }
+    __syncthreads();
+    const unsigned long long base = base_s;
+    const long long room = max_voxels - (long long)base;
+    const uint32_t kept = room <= 0 ? 0u : (room < (long long)total ? (uint32_t)room : total);
+    if (threadIdx.x == 0 && kept < total) atomicAdd(&ctr[C_VOX_OVF], (unsigned long long)(total - kept));
+    if (threadIdx.x < 64) {
+        // column (x, y) of the bin: voxels 8*col .. 8*col+7 (z ascending),
+        // counted only where staged
+        const uint32_t a0 = min(ex[8 * threadIdx.x], kept), a1 = min(ex[8 * threadIdx.x + 8], kept);
+        colcnt[(size_t)b * 64 + threadIdx.x] = (uint8_t)(a1 - a0);
+    }
+    long long bx, by, bz;
+    unpack_cells(bin_keys[b], bx, by, bz);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int l = l0 + h;
+        if (!f[h] || e[h] >= kept) continue;
+        const unsigned long long o = base + e[h];
+        const long long cx = 8 * bx + (l >> 6), cy = 8 * by + ((l >> 3) & 7), cz = 8 * bz + (l & 7);
+        const double sc = (double)(((unsigned long long)hi[0][l] << 32) | lo[0][l]);
+        const double sx = (double)(((unsigned long long)hi[1][l] << 32) | lo[1][l]);
+        const double sy = (double)(((unsigned long long)hi[2][l] << 32) | lo[2][l]);
+        const double sz = (double)(((unsigned long long)hi[3][l] << 32) | lo[3][l]);
+        const double k = cell * 4.656612873077392578125e-10;  // cell / 2^31
+        st_key[o] = pack_cells(cx, cy, cz);
+        st_sum[o] = make_float4((float)(sx * k), (float)(sy * k), (float)(sz * k),
+                                (float)(sc * 4.656612873077392578125e-10));
+        st_cnt[o] = (int32_t)cnt[l];
+        st_tag[o] = ((uint32_t)b << 9) | ((uint32_t)(l >> 3) << 3) | (e[h] - ex[l & ~7]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 4. ordered emit
+
+__device__ __forceinline__ int lower_bound_u64(const unsigned long long* a, int n, unsigned long long v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void bf_iota_kernel(uint32_t* v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (uint32_t)i;
+}
+
+__global__ void bf_groups_kernel(const unsigned long long* __restrict__ skeys, const uint32_t* __restrict__ sids,
+                                 int n, BinGroup* __restrict__ grp) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = skeys[i];
+    const unsigned long long x = k >> 42, xy = k >> 21;
+    const int sx = lower_bound_u64(skeys, n, x << 42), ex_ = lower_bound_u64(skeys, n, (x + 1) << 42);
+    const int sxy = lower_bound_u64(skeys, n, xy << 21), exy = lower_bound_u64(skeys, n, (xy + 1) << 21);
+    grp[sids[i]] = BinGroup{sx, ex_ - sx, sxy - sx, exy - sxy, i - sxy, 0};
+}
+
+__device__ __forceinline__ int64_t col_pos(const BinGroup& g, int col) {
+    const int lx = col >> 3, ly = col & 7;
+    return (int64_t)g.start_x * 64 + (int64_t)lx * 8 * g.n_x + (int64_t)g.off_xy * 8 + (int64_t)ly * g.n_xy + g.r_z;
+}
+
+__global__ void bf_colpos_kernel(const BinGroup* __restrict__ grp, const uint8_t* __restrict__ colcnt, int n,
+                                 uint32_t* __restrict__ scan_in) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * 64) return;
+    const int b = (int)(t >> 6), col = (int)(t & 63);
+    scan_in[col_pos(grp[b], col)] = colcnt[t];
+}
+
+__global__ void bf_permute_kernel(const unsigned long long* __restrict__ ctr, int64_t max_voxels,
+                                  const BinGroup* __restrict__ grp, const uint32_t* __restrict__ col_base,
+                                  const unsigned long long* __restrict__ st_key, const float4* __restrict__ st_sum,
+                                  const int32_t* __restrict__ st_cnt, const uint32_t* __restrict__ st_tag, double cell,
+                                  int64_t* __restrict__ keys, float* __restrict__ cen, float* __restrict__ wsum,
+                                  int32_t* __restrict__ count, int64_t* __restrict__ n_out) {
+    const int64_t U = min((int64_t)ctr[C_VOX], max_voxels);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n_out) *n_out = U;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < U; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t tag = st_tag[i];
+        const int b = (int)(tag >> 9), col = (int)((tag >> 3) & 63);
+        const int64_t d = (int64_t)col_base[col_pos(grp[b], col)] + (tag & 7);
+        const unsigned long long k = st_key[i];
+        const float4 s = st_sum[i];
+        long long cx, cy, cz;
+        unpack_cells(k, cx, cy, cz);
+        const double w = s.w;
+        keys[d] = (int64_t)k;
+        cen[3 * d + 0] = (float)((double)cx * cell + (double)s.x / w);
+        cen[3 * d + 1] = (float)((double)cy * cell + (double)s.y / w);
+        cen[3 * d + 2] = (float)((double)cz * cell + (double)s.z / w);
+        wsum[d] = s.w;
+        count[d] = st_cnt[i];
+    }
+}
+
+// owner = mix64(key) % n_ranks (dist.owner_of)
+__global__ void bf_owner_count_kernel(const unsigned long long* __restrict__ keys, const unsigned long long* ctr,
+                                      int64_t max_voxels, int n_ranks, unsigned long long* __restrict__ rank_counts) {
+    __shared__ unsigned int hist[64];
+    for (int r = threadIdx.x; r < n_ranks; r += blockDim.x) hist[r] = 0u;
+    __syncthreads();
+    const int64_t n = min((int64_t)ctr[C_VOX], max_voxels);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[mix64(keys[i]) % (unsigned long long)n_ranks], 1u);
+    __syncthreads();
+    for (int r = threadIdx.x; r < n_ranks; r += blockDim.x)
+        if (hist[r]) atomicAdd(&rank_counts[r], (unsigned long long)hist[r]);
+}
+
+__global__ void bf_owner_write_kernel(const unsigned long long* __restrict__ skeys, const float4* __restrict__ ssum,
+                                      const int32_t* __restrict__ scnt, const unsigned long long* ctr,
+                                      int64_t max_voxels, int n_ranks, const unsigned long long* __restrict__ rank_base,
+                                      unsigned long long* __restrict__ cursors, int64_t* __restrict__ okeys,
+                                      float* __restrict__ sums4, int32_t* __restrict__ cnt) {
+    const int64_t n = min((int64_t)ctr[C_VOX], max_voxels);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = skeys[i];
+        const int r = (int)(mix64(k) % (unsigned long long)n_ranks);
+        const unsigned peers = __match_any_sync(__activemask(), r);
+        const int lead = __ffs(peers) - 1;
+        const unsigned below = peers & ((1u << (threadIdx.x & 31)) - 1u);
+        unsigned long long base = 0;
+        if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(&cursors[r], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, lead);
+        const unsigned long long o = rank_base[r] + base + __popc(below);
+        okeys[o] = (int64_t)k;
+        reinterpret_cast<float4*>(sums4)[o] = ssum[i];
+        cnt[o] = scnt[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// clearing
+
+__global__ void bf_clear_table_kernel(BinEntry* __restrict__ t, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        BinEntry e;
+        e.key = kEmpty;
+        e.id = -1;
+        e.pad = 0;
+        t[i] = e;
+    }
+}
+
+__global__ void bf_clear_used_kernel(BinEntry* __restrict__ table, int64_t tcap, const uint32_t* __restrict__ bin_slot,
+                                     uint32_t* __restrict__ bin_nseg, const unsigned long long* __restrict__ ctr,
+                                     int64_t max_bins) {
+    const unsigned long long used_raw = ctr[C_BINS];
+    const bool full = (int64_t)used_raw > max_bins;
+    const int64_t used = full ? max_bins : (int64_t)used_raw;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    BinEntry empty;
+    empty.key = kEmpty;
+    empty.id = -1;
+    empty.pad = 0;
+    const int64_t n_tab = full ? tcap : used;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_tab; i += stride)
+        table[full ? i : (int64_t)bin_slot[i]] = empty;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used; i += stride) bin_nseg[i] = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static BinTab tab_of(const BinFuse* b) {
+    return BinTab{b->table, b->tmask, b->bin_keys, b->bin_slot, b->ctr, b->max_bins};
+}
+
+BinFuse* bf_create(int64_t max_voxels, int64_t max_bins, double cell, cudaStream_t st, int* rc) {
+    BinFuse* b = new BinFuse();
+    b->max_voxels = max_voxels;
+    b->max_bins = std::min<int64_t>(std::max<int64_t>(max_bins, 8192), (1 << 23) - 2);  // st_tag holds bin << 9
+    b->cell = cell;
+    int64_t tcap = 1;
+    while (tcap < 4 * b->max_bins) tcap <<= 1;
+    b->tmask = (unsigned long long)(tcap - 1);
+    bool ok = cudaMalloc(&b->table, sizeof(BinEntry) * (size_t)tcap) == cudaSuccess &&
+              cudaMalloc(&b->bin_keys, sizeof(unsigned long long) * (size_t)b->max_bins) == cudaSuccess &&
+              cudaMalloc(&b->bin_slot, sizeof(uint32_t) * (size_t)b->max_bins) == cudaSuccess &&
+              cudaMalloc(&b->bin_nseg, sizeof(uint32_t) * (size_t)(b->max_bins + 1)) == cudaSuccess &&
+              cudaMalloc(&b->ctr, sizeof(unsigned long long) * 16) == cudaSuccess;
+    if (!ok) {
+        set_last_error("cudaMalloc(binned fusion)", cudaGetLastError());
+        bf_destroy(b);
+        *rc = EC3R_ENOMEM;
+        return nullptr;
+    }
+    cudaMemsetAsync(b->bin_nseg, 0, sizeof(uint32_t) * (size_t)(b->max_bins + 1), st);
+    cudaMemsetAsync(b->ctr, 0, sizeof(unsigned long long) * 16, st);
+    bf_clear_table_kernel<<<(unsigned)((tcap + 255) / 256), 256, 0, st>>>(b->table, tcap);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) {
+        bf_destroy(b);
+        *rc = EC3R_ECUDA;
+        return nullptr;
+    }
+    *rc = EC3R_OK;
+    return b;
+}
+
+void bf_destroy(BinFuse* b) {
+    if (!b) return;
+    cudaFree(b->table);
+    cudaFree(b->bin_keys);
+    cudaFree(b->bin_slot);
+    cudaFree(b->bin_nseg);
+    cudaFree(b->ctr);
+    cudaFree(b->pay);
+    cudaFree(b->seg);
+    cudaFree(b->cta);
+    cudaFree(b->ws);
+    delete b;
+}
+
+int bf_clear(BinFuse* b, cudaStream_t st) {
+    bf_clear_used_kernel<<<kNumSMs * 4, 256, 0, st>>>(b->table, (int64_t)b->tmask + 1, b->bin_slot, b->bin_nseg,
+                                                      b->ctr, b->max_bins);
+    EC3R_CHECK_LAUNCH("bf_clear_used_kernel");
+    EC3R_CUDA_TRY(cudaMemsetAsync(b->ctr, 0, sizeof(unsigned long long) * 16, st));
+    b->used = 0;
+    b->cta_used = 0;
+    b->dirty = true;
+    return EC3R_OK;
+}
+
+// room for `entries` more payload entries and `ctas` more CTA descriptors
+static int bf_reserve(BinFuse* b, int64_t entries, int64_t ctas, cudaStream_t st) {
+    if (b->used + entries > (int64_t)0xFFFFFFFFll) {
+        set_last_error_msg("binned fusion: more than 2^32 points in one map");
+        return EC3R_EARG;
+    }
+    if (b->used + entries > b->cap) {
+        const int64_t cap = std::max<int64_t>(b->used + entries, b->cap + b->cap / 2);
+        uint32_t* pay = nullptr;
+        unsigned long long* seg = nullptr;
+        if (cudaMalloc(&pay, sizeof(uint32_t) * 3 * (size_t)cap) != cudaSuccess ||
+            cudaMalloc(&seg, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess) {
+            cudaFree(pay);
+            set_last_error("cudaMalloc(binned fusion payload)", cudaGetLastError());
+            return EC3R_ENOMEM;
+        }
+        if (b->used) {
+            EC3R_CUDA_TRY(cudaMemcpyAsync(pay, b->pay, sizeof(uint32_t) * 3 * (size_t)b->used,
+                                          cudaMemcpyDeviceToDevice, st));
+            EC3R_CUDA_TRY(cudaMemcpyAsync(seg, b->seg, sizeof(unsigned long long) * (size_t)b->used,
+                                          cudaMemcpyDeviceToDevice, st));
+            EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        cudaFree(b->pay);
+        cudaFree(b->seg);
+        b->pay = pay;
+        b->seg = seg;
+        b->cap = cap;
+    }
+    if (b->cta_used + ctas > b->cta_cap) {
+        const int64_t cap = std::max<int64_t>(b->cta_used + ctas, b->cta_cap * 2);
+        CtaDesc* d = nullptr;
+        if (cudaMalloc(&d, sizeof(CtaDesc) * (size_t)cap) != cudaSuccess) {
+            set_last_error("cudaMalloc(binned fusion descriptors)", cudaGetLastError());
+            return EC3R_ENOMEM;
+        }
+        if (b->cta_used) {
+            EC3R_CUDA_TRY(cudaMemcpyAsync(d, b->cta, sizeof(CtaDesc) * (size_t)b->cta_used, cudaMemcpyDeviceToDevice,
+                                          st));
+            EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        cudaFree(b->cta);
+        b->cta = d;
+        b->cta_cap = cap;
+    }
+    return EC3R_OK;
+}
+
+static BinArgs args_of(BinFuse* b, uint32_t region) {
+    BinArgs a;
+    a.out.tab = tab_of(b);
+    a.out.bin_nseg = b->bin_nseg;
+    a.out.pay = b->pay;
+    a.out.seg = b->seg;
+    a.cta = b->cta + b->cta_used;
+    a.region0 = (uint32_t)b->used;
+    a.region = region;
+    a.ctr = b->ctr;
+    return a;
+}
+
+int bf_insert_frames(BinFuse* b, const FrameGeom& g, cudaStream_t st) {
+    const int bands = (g.H + BF_ROWS - 1) / BF_ROWS;
+    const int64_t n_cta = (int64_t)bands * g.n;
+    const uint32_t region = (uint32_t)(BF_ROWS * g.W);
+    int rc = bf_reserve(b, n_cta * region, n_cta, st);
+    if (rc) return rc;
+    const BinArgs a = args_of(b, region);
+    const size_t smem = sizeof(float4) * (size_t)g.W;
+    static bool attr = false;
+    if (!attr) {
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(bf_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    if (smem > 64 * 1024) {
+        set_last_error_msg("binned fusion: image wider than 4096 px");
+        return EC3R_EARG;
+    }
+    KernelTimer tk(TK_FUSE_INSERT, st);
+    bf_bin_kernel<<<dim3(bands, g.n), BF_NT, smem, st>>>(g, a);
+    EC3R_CHECK_LAUNCH("bf_bin_kernel");
+    tk.stop();
+    b->used += n_cta * region;
+    b->cta_used += n_cta;
+    b->dirty = true;
+    return EC3R_OK;
+}
+
+int bf_insert_points(BinFuse* b, const double* pts, const double* conf, int64_t n, const double* sim3_h,
+                     cudaStream_t st) {
+    const int64_t n_cta = (n + BF_PTS_CTA - 1) / BF_PTS_CTA;
+    int rc = bf_reserve(b, n_cta * BF_PTS_CTA, n_cta, st);
+    if (rc) return rc;
+    const BinArgs a = args_of(b, BF_PTS_CTA);
+    Sim3Arg g;
+    for (int k = 0; k < 8; ++k) g.v[k] = sim3_h[k];
+    bf_points_kernel<<<(unsigned)n_cta, BF_NT, 0, st>>>(pts, conf, n, g, b->cell, a);
+    EC3R_CHECK_LAUNCH("bf_points_kernel");
+    b->used += n_cta * BF_PTS_CTA;
+    b->cta_used += n_cta;
+    b->dirty = true;
+    return EC3R_OK;
+}
+
+int bf_stats(BinFuse* b, int64_t out[5], cudaStream_t st) {
+    unsigned long long c[16];
+    EC3R_CUDA_TRY(cudaMemcpyAsync(c, b->ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    out[0] = (int64_t)c[C_IN];
+    out[1] = (int64_t)c[C_OOR];
+    out[2] = (int64_t)(c[C_OVF] + c[C_VOX_OVF]);
+    out[3] = (int64_t)c[C_SLOW];
+    out[4] = (int64_t)std::min<unsigned long long>(c[C_BINS], (unsigned long long)b->max_bins);
+    return EC3R_OK;
+}
+
+static size_t bf_ws_layout(BinFuse* b, int64_t nb, int64_t nseg, BfWs* w) {
+    size_t cub1 = 0, cub2 = 0, cub3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cub1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(nb + 1));
+    cub::DeviceRadixSort::SortPairs(nullptr, cub2, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (uint32_t*)nullptr, (uint32_t*)nullptr, (int)std::max<int64_t>(nb, 1), 0, 63);
+    cub::DeviceScan::ExclusiveSum(nullptr, cub3, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int)std::max<int64_t>(nb * 64, 1));
+    const size_t cubb = std::max(cub1, std::max(cub2, cub3));
+    Carver cv{w ? b->ws : nullptr, 0};
+    const size_t V = (size_t)b->max_voxels;
+    BfWs t;
+    t.seg_off = cv.take<uint32_t>(nb + 1);
+    t.cursor = cv.take<uint32_t>(nb + 1);
+    t.sorted = cv.take<unsigned long long>(std::max<int64_t>(nseg, 1));
+    t.st_key = cv.take<unsigned long long>(V);
+    t.st_sum = cv.take<float4>(V);
+    t.st_cnt = cv.take<int32_t>(V);
+    t.st_tag = cv.take<uint32_t>(V);
+    t.colcnt = cv.take<uint8_t>(nb * 64 + 64);
+    t.skeys = cv.take<unsigned long long>(nb + 1);
+    t.ids = cv.take<uint32_t>(nb + 1);
+    t.sids = cv.take<uint32_t>(nb + 1);
+    t.grp = cv.take<BinGroup>(nb + 1);
+    t.scan_in = cv.take<uint32_t>(nb * 64 + 1);
+    t.col_base = cv.take<uint32_t>(nb * 64 + 1);
+    t.cub_tmp = cv.take<char>(cubb);
+    t.cub_bytes = cubb;
+    if (w) *w = t;
+    return cv.used;
+}
+
+// Aggregation (phase A): sorted segments -> per-bin voxels in staging.  One
+// host round trip (bin and segment counts size the launches).
+static int bf_aggregate(BinFuse* b, BfWs* w, cudaStream_t st) {
+    unsigned long long c[16];
+    EC3R_CUDA_TRY(cudaMemcpyAsync(c, b->ctr, sizeof(c), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t nb = std::min<int64_t>((int64_t)c[C_BINS], b->max_bins);
+    const int64_t nseg_cap = std::max<int64_t>((int64_t)c[C_SEGS], 1);  // records written (>= sorted)
+    const size_t need = bf_ws_layout(b, nb, nseg_cap, nullptr);
+    if (need > b->ws_cap) {
+        cudaFree(b->ws);
+        b->ws = nullptr;
+        b->ws_cap = 0;
+        const size_t cap = need + need / 4;
+        if (cudaMalloc(&b->ws, cap) != cudaSuccess) {
+            set_last_error("cudaMalloc(binned fusion workspace)", cudaGetLastError());
+            return EC3R_ENOMEM;
+        }
+        b->ws_cap = cap;
+    }
+    bf_ws_layout(b, nb, nseg_cap, &b->view);
+    *w = b->view;
+    b->n_bins = nb;
+    EC3R_CUDA_TRY(cudaMemsetAsync(b->ctr + C_VOX, 0, sizeof(unsigned long long) * 2, st));
+    if (nb == 0) {
+        b->dirty = false;
+        return EC3R_OK;
+    }
+    size_t tb = w->cub_bytes;
+    if (cub::DeviceScan::ExclusiveSum(w->cub_tmp, tb, b->bin_nseg, w->seg_off, (int)(nb + 1), st) != cudaSuccess) {
+        set_last_error("cub::DeviceScan::ExclusiveSum(bins)", cudaGetLastError());
+        return EC3R_ECUDA;
+    }
+    EC3R_CUDA_TRY(cudaMemsetAsync(w->cursor, 0, sizeof(uint32_t) * (size_t)nb, st));
+    bf_seg_scatter_kernel<<<(unsigned)std::min<int64_t>(b->cta_used, (int64_t)kNumSMs * 16), 256, 0, st>>>(
+        b->cta, b->cta_used, b->seg, w->seg_off, w->cursor, w->sorted);
+    EC3R_CHECK_LAUNCH("bf_seg_scatter_kernel");
+    bf_aggregate_kernel<<<(unsigned)nb, BF_NT, 0, st>>>(b->bin_keys, w->seg_off, w->sorted, b->pay, b->cell,
+                                                       b->max_voxels, b->ctr, w->st_key, w->st_sum, w->st_cnt,
+                                                       w->st_tag, w->colcnt);
+    EC3R_CHECK_LAUNCH("bf_aggregate_kernel");
+    b->dirty = false;
+    return EC3R_OK;
+}
+
+static int bf_ensure_aggregated(BinFuse* b, BfWs* w, cudaStream_t st) {
+    if (b->dirty) return bf_aggregate(b, w, st);
+    *w = b->view;
+    return EC3R_OK;
+}
+
+int bf_count(BinFuse* b, int64_t* U, cudaStream_t st) {
+    BfWs w;
+    int rc = bf_ensure_aggregated(b, &w, st);
+    if (rc) return rc;
+    unsigned long long v = 0;
+    EC3R_CUDA_TRY(cudaMemcpyAsync(&v, b->ctr + C_VOX, sizeof(v), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    *U = std::min<int64_t>((int64_t)v, b->max_voxels);
+    return EC3R_OK;
+}
+
+int bf_extract(BinFuse* b, int64_t* keys, float* centroid, float* wsum, int32_t* count, int64_t* n_out,
+               int64_t* U_host, cudaStream_t st) {
+    BfWs w;
+    int rc = bf_ensure_aggregated(b, &w, st);
+    if (rc) return rc;
+    const int64_t nb = b->n_bins;
+    if (nb > 0) {
+        bf_iota_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(w.ids, (int)nb);
+        EC3R_CHECK_LAUNCH("bf_iota_kernel");
+        size_t tb = w.cub_bytes;
+        if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, b->bin_keys, w.skeys, w.ids, w.sids, (int)nb, 0, 63, st) !=
+            cudaSuccess) {
+            set_last_error("cub::DeviceRadixSort::SortPairs(bins)", cudaGetLastError());
+            return EC3R_ECUDA;
+        }
+        bf_groups_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(w.skeys, w.sids, (int)nb, w.grp);
+        EC3R_CHECK_LAUNCH("bf_groups_kernel");
+        const int64_t ncol = nb * 64;
+        bf_colpos_kernel<<<(unsigned)((ncol + 255) / 256), 256, 0, st>>>(w.grp, w.colcnt, (int)nb, w.scan_in);
+        EC3R_CHECK_LAUNCH("bf_colpos_kernel");
+        tb = w.cub_bytes;
+        if (cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.scan_in, w.col_base, (int)ncol, st) != cudaSuccess) {
+            set_last_error("cub::DeviceScan::ExclusiveSum(columns)", cudaGetLastError());
+            return EC3R_ECUDA;
+        }
+    }
+    bf_permute_kernel<<<kNumSMs * 8, 256, 0, st>>>(b->ctr, b->max_voxels, w.grp, w.col_base, w.st_key, w.st_sum,
+                                                  w.st_cnt, w.st_tag, b->cell, keys, centroid, wsum, count, n_out);
+    EC3R_CHECK_LAUNCH("bf_permute_kernel");
+    if (U_host) {
+        unsigned long long v = 0;
+        EC3R_CUDA_TRY(cudaMemcpyAsync(&v, b->ctr + C_VOX, sizeof(v), cudaMemcpyDeviceToHost, st));
+        EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        *U_host = std::min<int64_t>((int64_t)v, b->max_voxels);
+    }
+    return EC3R_OK;
+}
+
+int bf_extract_partials(BinFuse* b, int n_ranks, int64_t* keys, float* sums4, int32_t* count, int64_t* rank_counts,
+                        cudaStream_t st) {
+    BfWs w;
+    int rc = bf_ensure_aggregated(b, &w, st);
+    if (rc) return rc;
+    unsigned long long* base = nullptr;
+    EC3R_CUDA_TRY(cudaMallocAsync((void**)&base, sizeof(unsigned long long) * 2 * n_ranks, st));
+    unsigned long long* cursors = base + n_ranks;
+    EC3R_CUDA_TRY(cudaMemsetAsync(rank_counts, 0, sizeof(int64_t) * n_ranks, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(cursors, 0, sizeof(unsigned long long) * n_ranks, st));
+    bf_owner_count_kernel<<<kNumSMs * 8, 256, 0, st>>>(w.st_key, b->ctr, b->max_voxels, n_ranks,
+                                                      (unsigned long long*)rank_counts);
+    EC3R_CHECK_LAUNCH("bf_owner_count_kernel");
+    std::vector<unsigned long long> rc_h(n_ranks), rb(n_ranks);
+    EC3R_CUDA_TRY(cudaMemcpyAsync(rc_h.data(), rank_counts, sizeof(int64_t) * n_ranks, cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long acc = 0;
+    for (int r = 0; r < n_ranks; ++r) { rb[r] = acc; acc += rc_h[r]; }
+    EC3R_CUDA_TRY(cudaMemcpyAsync(base, rb.data(), sizeof(unsigned long long) * n_ranks, cudaMemcpyHostToDevice, st));
+    bf_owner_write_kernel<<<kNumSMs * 8, 256, 0, st>>>(w.st_key, w.st_sum, w.st_cnt, b->ctr, b->max_voxels, n_ranks,
+                                                      base, cursors, keys, sums4, count);
+    EC3R_CHECK_LAUNCH("bf_owner_write_kernel");
+    EC3R_CUDA_TRY(cudaFreeAsync(base, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));  // rb is a host temporary
+    return EC3R_OK;
+}
+
+}  // namespace ec3r

@@ -30,11 +30,11 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "fuse_common.cuh"
+#include "vbin.cuh"
 
 namespace ec3r {
 
-constexpr unsigned long long kEmpty = ~0ull;  // never a _pack key (max is 2^63-1)
-constexpr int64_t kPackOffset = 1 << 20;
 constexpr int kBlockVox = 64;                 // 4 x 4 x 4
 
 struct __align__(16) BlockEntry {
@@ -59,6 +59,12 @@ struct ec3r_vhash {
     float4* ftab;                    // per-frame affine tables of the last insert_frames
     int64_t ftab_cap;                // float4 entries
     int64_t last_count;              // voxels of the last sorted extract (host-known), -1 if unknown
+    // binned super-block engine (vbin.cu): frame and point inserts go there
+    // unless EC3R_FUSE_LEGACY=1; partial merges (multi-GPU owner maps) use
+    // the block hash.  A map holds one kind of content between clears.
+    ec3r::BinFuse* bf;
+    bool binned;
+    bool bf_active, legacy_active;
 };
 
 namespace ec3r {
@@ -77,45 +83,6 @@ struct VB {
 static VB vb_of(const ec3r_vhash* h) {
     return VB{h->table, h->tmask, h->block_keys, h->block_slot, h->sums, h->counts, h->counters, h->max_blocks};
 }
-
-__device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdull;
-    k ^= k >> 33;
-    k *= 0xc4ceb9fe1a85ec53ull;
-    k ^= k >> 33;
-    return k;
-}
-
-// table position of a block key: a 32-bit mix (the table has < 2^32 entries)
-__device__ __forceinline__ unsigned long long table_slot(unsigned long long bk, unsigned long long tmask) {
-    uint32_t h = (uint32_t)bk * 0x9E3779B1u ^ (uint32_t)(bk >> 32) * 0x85EBCA77u;
-    h ^= h >> 15;
-    h *= 0x2C1B3C6Du;
-    h ^= h >> 13;
-    return (unsigned long long)h & tmask;
-}
-
-__device__ __forceinline__ unsigned long long pack_cells(long long cx, long long cy, long long cz) {
-    return ((unsigned long long)(cx + kPackOffset) << 42) | ((unsigned long long)(cy + kPackOffset) << 21) |
-           (unsigned long long)(cz + kPackOffset);
-}
-
-// pack_cells of int32 block coordinates with 32-bit operations
-__device__ __forceinline__ unsigned long long pack_block(int bx, int by, int bz) {
-    const unsigned X = (unsigned)(bx + (int)kPackOffset), Y = (unsigned)(by + (int)kPackOffset),
-                   Z = (unsigned)(bz + (int)kPackOffset);
-    const unsigned lo = (Y << 21) | Z, hi = (X << 10) | (Y >> 11);
-    return ((unsigned long long)hi << 32) | lo;
-}
-
-__device__ __forceinline__ void unpack_cells(unsigned long long k, long long& cx, long long& cy, long long& cz) {
-    cx = (long long)((k >> 42) & 0x1FFFFF) - kPackOffset;
-    cy = (long long)((k >> 21) & 0x1FFFFF) - kPackOffset;
-    cz = (long long)(k & 0x1FFFFF) - kPackOffset;
-}
-
-__device__ __forceinline__ bool cell_in_range(long long c) { return c >= -kPackOffset && c < kPackOffset; }
 
 __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -263,36 +230,14 @@ constexpr int FI_ROWS = EC3R_FI_ROWS;
 #define EC3R_FI_MINB 2  // resident CTAs per SM the register budget is sized for
 #endif
 
-struct FuseArgs {
-    const float* depth;
-    const float* conf;
-    const double* slot_poses;    // anchor_from_cam per slot
-    const double* slot_globals;  // world_from_anchor (submap global Sim3) per slot
-    const int32_t* slots;        // slot ids to fuse
-    const float4* ftab;          // per listed frame: A[W], B[H], T (see vh_frame_tables_kernel)
-    int n, H, W;
-    double fx, fy, cx, cy;
-    double cell;
-    float inv_cell_f, cell_f;
+struct FuseArgs : FrameGeom {
     VB vb;
 };
-
-// Exact reference chain for one pixel: cells of  G.apply(P.apply(ray)).
-__device__ __noinline__ void exact_cells(const double* P, const double* G, double xcoef, double ycoef, float zf,
-                                         double cell, long long c[3]) {
-    const double z = (double)zf;
-    const double ray[3] = {xm(xcoef, z), xm(ycoef, z), z};
-    double pa[3], pw[3];
-    pose_apply_exact(P, ray, pa);
-    sim3_apply_exact(G, pa, pw);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) c[k] = (long long)floor(__ddiv_rn(pw[k], cell));
-}
 
 // Per listed frame j, the composite G o P_f folded into a float32 affine map
 // x = z * (A[u] + B[v]) + T: A[u] = M[:,0] x_u + M[:,2], B[v] = M[:,1] y_v,
 // each with its |.|-sum in .w for the rounding bound; T = (t, |t|-sum).
-__global__ void vh_frame_tables_kernel(FuseArgs a, float4* __restrict__ ftab) {
+__global__ void vh_frame_tables_kernel(FrameGeom a, float4* __restrict__ ftab) {
     const int j = blockIdx.x;
     const int slot = a.slots[j];
     const double* P = a.slot_poses + 8 * slot;
@@ -926,11 +871,22 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
 
 using namespace ec3r;
 
+static int mixed_error() {
+    set_last_error_msg("ec3r_vhash: frame/point inserts and partial merges cannot share a map between clears");
+    return EC3R_EARG;
+}
+
 extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int64_t max_blocks,
                                        int64_t table_entries, double cell_size, void* stream) {
     if (!out || max_voxels < 2 || max_blocks < 1 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
     h->last_count = -1;
+    h->bf = nullptr;
+    h->bf_active = h->legacy_active = false;
+    {
+        const char* e = getenv("EC3R_FUSE_LEGACY");
+        h->binned = !(e && e[0] == '1');
+    }
     h->max_voxels = max_voxels > 65536 ? max_voxels : 65536;
     h->max_blocks = max_blocks > 4096 ? max_blocks : 4096;
     // frame fusion addresses voxels as 32-bit (block << 6 | local) ids
@@ -964,6 +920,14 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     // the whole table starts empty (later clears touch only the used entries)
     vb_clear_table_kernel<<<(unsigned)((tcap + 255) / 256), 256, 0, st>>>(h->table, tcap);
     EC3R_CHECK_LAUNCH("vb_clear_table_kernel");
+    if (h->binned) {
+        int rc = EC3R_OK;
+        h->bf = bf_create(h->max_voxels, h->max_blocks, cell_size, st, &rc);
+        if (!h->bf) {
+            ec3r_vhash_destroy(h);
+            return rc;
+        }
+    }
     *out = h;
     return EC3R_OK;
 }
@@ -985,6 +949,7 @@ extern "C" int ec3r_vhash_destroy(ec3r_vhash* h) {
     cudaFree(h->counts);
     cudaFree(h->counters);
     cudaFree(h->ftab);
+    bf_destroy(h->bf);
     delete h;
     return EC3R_OK;
 }
@@ -1001,6 +966,13 @@ extern "C" int ec3r_vhash_clear(ec3r_vhash* h, void* stream) {
                                                       h->max_blocks);
     EC3R_CHECK_LAUNCH("vb_clear_used_kernel");
     EC3R_CUDA_TRY(cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 8, st));
+    h->last_count = -1;
+    h->legacy_active = false;
+    if (h->bf) {
+        const int rc = bf_clear(h->bf, st);
+        if (rc) return rc;
+    }
+    h->bf_active = false;
     return EC3R_OK;
 }
 
@@ -1030,6 +1002,12 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     cudaStream_t st = as_stream(stream);
     vh_frame_tables_kernel<<<n, 256, 0, st>>>(a, h->ftab);
     EC3R_CHECK_LAUNCH("vh_frame_tables_kernel");
+    if (h->bf) {
+        if (h->legacy_active) return mixed_error();
+        h->bf_active = true;
+        return bf_insert_frames(h->bf, a, st);
+    }
+    h->legacy_active = true;
     const size_t smem = sizeof(float4) * (size_t)W;
     if (smem > 48 * 1024)
         EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1046,6 +1024,12 @@ extern "C" int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, con
                                         const double* sim3_h, void* stream) {
     if (!h || n < 0 || !sim3_h) return EC3R_EARG;
     if (n == 0) return EC3R_OK;
+    if (h->bf) {
+        if (h->legacy_active) return mixed_error();
+        h->bf_active = true;
+        return bf_insert_points(h->bf, points, conf, n, sim3_h, as_stream(stream));
+    }
+    h->legacy_active = true;
     Sim3Arg g;
     for (int k = 0; k < 8; ++k) g.v[k] = sim3_h[k];
     vh_insert_points_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(points, conf, n, g, h->cell, vb_of(h));
@@ -1055,6 +1039,17 @@ extern "C" int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, con
 
 extern "C" int ec3r_vhash_stats_get(ec3r_vhash* h, ec3r_vhash_stats* out_h, void* stream) {
     if (!h || !out_h) return EC3R_EARG;
+    if (h->bf_active) {
+        int64_t v[5];
+        const int rc = bf_stats(h->bf, v, as_stream(stream));
+        if (rc) return rc;
+        out_h->n_points_in = v[0];
+        out_h->n_out_of_range = v[1];
+        out_h->n_overflow = v[2];
+        out_h->n_slow_path = v[3];
+        out_h->n_blocks = v[4];
+        return EC3R_OK;
+    }
     unsigned long long c[8];
     cudaStream_t st = as_stream(stream);
     EC3R_CUDA_TRY(cudaMemcpyAsync(c, h->counters, sizeof(c), cudaMemcpyDeviceToHost, st));
@@ -1081,6 +1076,14 @@ __global__ void vb_count_kernel(const unsigned int* __restrict__ counts, const u
 extern "C" int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream) {
     if (!h || !n_out) return EC3R_EARG;
     cudaStream_t st = as_stream(stream);
+    if (h->bf_active) {
+        int64_t U = 0;
+        const int rc = bf_count(h->bf, &U, st);
+        if (rc) return rc;
+        EC3R_CUDA_TRY(cudaMemcpyAsync(n_out, &U, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+        return EC3R_OK;
+    }
     EC3R_CUDA_TRY(cudaMemsetAsync(n_out, 0, sizeof(int64_t), st));
     vb_count_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->counts, h->counters, h->max_blocks, (unsigned long long*)n_out);
     EC3R_CHECK_LAUNCH("vb_count_kernel");
@@ -1106,8 +1109,14 @@ extern "C" size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h) {
 extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum, int32_t* count,
                                   int64_t* n_out, int sort, void* workspace, size_t workspace_bytes, void* stream) {
     if (!h || !keys || !centroid || !wsum || !count || !n_out) return EC3R_EARG;
-    if (!workspace || workspace_bytes < ec3r_vhash_extract_workspace(h)) return EC3R_EWORKSPACE;
     cudaStream_t st = as_stream(stream);
+    if (h->bf_active) {  // always key-sorted; the workspace is the engine's own
+        int64_t U = -1;
+        const int rc = bf_extract(h->bf, keys, centroid, wsum, count, n_out, &U, st);
+        h->last_count = U;
+        return rc;
+    }
+    if (!workspace || workspace_bytes < ec3r_vhash_extract_workspace(h)) return EC3R_EWORKSPACE;
     const unsigned long long* ks;
     const int64_t* is;
     const uint32_t* i32;
@@ -1134,6 +1143,7 @@ extern "C" int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* 
                                            int64_t* rank_counts, void* workspace, size_t workspace_bytes,
                                            void* stream) {
     if (!h || n_ranks < 1 || n_ranks > 64 || !keys || !sums4 || !count || !rank_counts) return EC3R_EARG;
+    if (h->bf_active) return bf_extract_partials(h->bf, n_ranks, keys, sums4, count, rank_counts, as_stream(stream));
     const size_t need = ec3r_vhash_extract_workspace(h) + 4 * align256(sizeof(unsigned long long) * n_ranks);
     if (!workspace || workspace_bytes < need) return EC3R_EWORKSPACE;
     cudaStream_t st = as_stream(stream);
@@ -1168,6 +1178,8 @@ extern "C" int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, con
                                          int64_t n, void* stream) {
     if (!h || n < 0) return EC3R_EARG;
     if (n == 0) return EC3R_OK;
+    if (h->bf_active) return mixed_error();
+    h->legacy_active = true;
     vb_merge_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(keys, sums4, count, n, vb_of(h));
     EC3R_CHECK_LAUNCH("vb_merge_kernel");
     return EC3R_OK;
