@@ -80,7 +80,14 @@ struct FrameGeom {
 __global__ void vh_frame_tables_kernel(FrameGeom a, float4* __restrict__ ftab);
 
 // Exact reference chain for one pixel: cells of  G.apply(P.apply(ray)).
-__device__ __noinline__ inline void exact_cells(const double* P, const double* G, double xcoef, double ycoef,
+// Out of line by default (rare path, keeps the caller's registers free);
+// EC3R_EXACT_INLINE=1 inlines it (needed under tight register caps).
+#if defined(EC3R_EXACT_INLINE) && EC3R_EXACT_INLINE
+#define EC3R_EXACT_ATTR __forceinline__
+#else
+#define EC3R_EXACT_ATTR __noinline__ inline
+#endif
+__device__ EC3R_EXACT_ATTR void exact_cells(const double* P, const double* G, double xcoef, double ycoef,
                                                 float zf, double cell, long long c[3]) {
     const double z = (double)zf;
     const double ray[3] = {xm(xcoef, z), xm(ycoef, z), z};

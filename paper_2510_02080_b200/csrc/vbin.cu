@@ -80,7 +80,7 @@ struct BinGroup {
 struct BfWs {
     uint32_t* seg_off;      // n_bins + 1
     uint32_t* cursor;       // n_bins
-    unsigned long long* sorted;  // segments
+    uint4* sorted;          // group records by bin
     unsigned long long* st_key;
     float4* st_sum;
     int32_t* st_cnt;
@@ -108,7 +108,7 @@ struct BinFuse {
     unsigned long long* ctr = nullptr;
     // payload (3 u32 per entry) and segment records share one index space
     uint32_t* pay = nullptr;
-    unsigned long long* seg = nullptr;
+    uint4* seg = nullptr;
     int64_t cap = 0, used = 0;  // entries
     CtaDesc* cta = nullptr;
     int64_t cta_cap = 0, cta_used = 0;
@@ -186,10 +186,7 @@ __device__ __noinline__ int bf_find_or_insert(const BinTab& t, unsigned long lon
 // warp-level multisplit of one iteration's points by bin
 
 struct WarpSmem {
-    unsigned long long keys[BF_MAXS];  // slot -> bin key
-    uint32_t cnt[BF_MAXS];             // slot -> point count, then exclusive offset
-    uint32_t stage[3 * BF_MAXS];       // payload in slot order
-    unsigned long long ckey[BF_WC];    // bin-id cache (key, id), one writer per entry
+    unsigned long long ckey[BF_WC];  // bin-id cache (key, id), one writer per entry
     int cid[BF_WC];
 };
 
@@ -197,7 +194,7 @@ struct BinOut {
     BinTab tab;
     uint32_t* bin_nseg;
     uint32_t* pay;
-    unsigned long long* seg;
+    uint4* seg;
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -206,120 +203,85 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-// Points k = 0..3 of each lane: valid, bin key bk, payload (w0 = conf bits,
-// pv = in-bin index | offsets).  Appends the valid points to the CTA region
-// (cursor *cta_pay, region base rbase) grouped by bin and one segment record
-// per bin.  Returns the number of points dropped (bin table overflow).
-__device__ __forceinline__ unsigned bf_warp_emit(const BinOut& o, WarpSmem& w, const bool (&valid)[4],
-                                                 const unsigned long long (&bk)[4], const uint32_t (&w0)[4],
-                                                 const unsigned long long (&pv)[4], uint32_t rbase,
-                                                 unsigned* cta_pay, unsigned* cta_seg) {
+// Bin id of key through the warp's direct-mapped cache (entry from the low
+// bits of the bin coordinates: neighbouring bins never share an entry).
+// Lanes with act resolve; every lane of the warp must call.  Misses go to
+// the global table; one lane per cache entry refills it.
+__device__ __forceinline__ int bf_bin_id(const BinTab& t, WarpSmem& w, bool act, unsigned long long key) {
     const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    int ns = 0;  // warp-uniform
-    int slot[4];
-    unsigned rank[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        slot[k] = -1;
-        rank[k] = 0;
-        if (!__any_sync(0xffffffffu, valid[k])) continue;
-        const unsigned peers = __match_any_sync(0xffffffffu, valid[k] ? bk[k] : kEmpty);
-        const int leader = __ffs(peers) - 1;
-        const bool lead = valid[k] && lane == leader;
-        int s = -1;
-        if (lead)
-            for (int i = 0; i < ns; ++i)
-                if (w.keys[i] == bk[k]) { s = i; break; }
-        const unsigned nm = __ballot_sync(0xffffffffu, lead && s < 0);
-        if (lead && s < 0) {
-            s = ns + __popc(nm & lt);
-            w.keys[s] = bk[k];
-            w.cnt[s] = 0u;
-        }
-        ns += __popc(nm);
-        unsigned base = 0;
-        if (lead) {  // leaders hold distinct slots: plain read-modify-write
-            base = w.cnt[s];
-            w.cnt[s] = base + __popc(peers);
-        }
-        s = __shfl_sync(0xffffffffu, s, leader);
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (valid[k]) {
-            slot[k] = s;
-            rank[k] = base + __popc(peers & lt);
-        }
-    }
-    if (ns == 0) return 0u;
-    __syncwarp();
-    // exclusive scan of the slot counts (in place)
-    unsigned carry = 0;
-    for (int b0 = 0; b0 < ns; b0 += 32) {
-        const int i = b0 + lane;
-        const unsigned v = i < ns ? w.cnt[i] : 0u;
-        unsigned x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        if (i < ns) w.cnt[i] = carry + x - v;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    __syncwarp();
-    const unsigned total = carry;
-    // stage in slot order
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (slot[k] < 0) continue;
-        const unsigned p = w.cnt[slot[k]] + rank[k];
-        w.stage[3 * p] = w0[k];
-        w.stage[3 * p + 1] = (uint32_t)pv[k];
-        w.stage[3 * p + 2] = (uint32_t)(pv[k] >> 32);
-    }
-    unsigned gb = 0, sb = 0;
-    if (lane == 0) {
-        gb = atomicAdd(cta_pay, total);
-        sb = atomicAdd(cta_seg, (unsigned)ns);
-    }
-    gb = __shfl_sync(0xffffffffu, gb, 0);
-    sb = __shfl_sync(0xffffffffu, sb, 0);
-    __syncwarp();
-    uint32_t* dst = o.pay + 3 * (size_t)(rbase + gb);
-    for (unsigned i = lane; i < 3 * total; i += 32) dst[i] = w.stage[i];
-    // one segment record per slot: bin ids through the per-warp cache
-    unsigned dropped = 0;
-    for (int b0 = 0; b0 < ns; b0 += 32) {
-        const int s = b0 + lane;
-        const bool act = s < ns;
-        const unsigned long long key = act ? w.keys[s] : kEmpty;
-        const int ce = (int)(mix64(key) & (BF_WC - 1));
-        int id = -3;
-        if (act && w.ckey[ce] == key) id = w.cid[ce];
-        const bool miss = act && id == -3;
-        if (miss) id = bf_find_or_insert(o.tab, key);
-        // one writer per cache entry
+    const int ce = (int)(((key >> 42) & 7u) | (((key >> 21) & 3u) << 3) | ((key & 3u) << 5));
+    int id = -3;
+    if (act && w.ckey[ce] == key) id = w.cid[ce];
+    const bool miss = act && id == -3;
+    if (__any_sync(0xffffffffu, miss)) {
+        if (miss) id = bf_find_or_insert(t, key);
         const unsigned same = __match_any_sync(0xffffffffu, miss ? ce : -1);
         __syncwarp();
         if (miss && lane == __ffs(same) - 1 && id >= 0) {
             w.ckey[ce] = key;
             w.cid[ce] = id;
         }
-        if (act) {
-            const unsigned beg = w.cnt[s];
-            const unsigned end = s + 1 < ns ? w.cnt[s + 1] : total;
+        __syncwarp();
+    }
+    return id;
+}
+
+// Points k = 0..3 of each lane: valid, bin key bk, payload (w0 = conf bits,
+// pv = in-bin index | offsets).  Per k the valid points are written in lane
+// order, contiguously into the CTA region (cursor *cta_pay, region base
+// rbase): fully coalesced, no reordering.  The lanes sharing a bin form a
+// group (match.any) described by one record {first entry of the k-slice,
+// valid-lane mask, group-lane mask, bin id}: the entry of group lane j is
+// first + popc(valid & lanes below j).  Returns the number of points dropped
+// (bin table overflow).
+__device__ __forceinline__ unsigned bf_warp_emit(const BinOut& o, WarpSmem& w, const bool (&valid)[4],
+                                                 const unsigned long long (&bk)[4], const uint32_t (&w0)[4],
+                                                 const unsigned long long (&pv)[4], uint32_t rbase,
+                                                 unsigned* cta_pay, unsigned* cta_seg) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    unsigned peers[4], vm[4], lm[4];
+    unsigned tot_v = 0, tot_g = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        vm[k] = __ballot_sync(0xffffffffu, valid[k]);
+        peers[k] = __match_any_sync(0xffffffffu, valid[k] ? bk[k] : kEmpty);
+        lm[k] = __ballot_sync(0xffffffffu, valid[k] && lane == __ffs(peers[k]) - 1);
+        tot_v += __popc(vm[k]);
+        tot_g += __popc(lm[k]);
+    }
+    if (tot_v == 0) return 0u;
+    unsigned gb = 0, sb = 0;
+    if (lane == 0) {
+        gb = atomicAdd(cta_pay, tot_v);
+        sb = atomicAdd(cta_seg, tot_g);
+    }
+    uint32_t pbase = rbase + __shfl_sync(0xffffffffu, gb, 0);
+    uint32_t sbase = rbase + __shfl_sync(0xffffffffu, sb, 0);
+    unsigned dropped = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (vm[k] == 0) continue;
+        if (valid[k]) {
+            uint32_t* dst = o.pay + 3 * (size_t)(pbase + __popc(vm[k] & lt));
+            dst[0] = w0[k];
+            dst[1] = (uint32_t)pv[k];
+            dst[2] = (uint32_t)(pv[k] >> 32);
+        }
+        const bool lead = (lm[k] >> lane) & 1u;
+        const int id = bf_bin_id(o.tab, w, lead, bk[k]);
+        if (lead) {
+            const uint32_t si = sbase + __popc(lm[k] & lt);
             if (id >= 0) {
-                o.seg[rbase + sb + s] = (unsigned long long)(rbase + gb + beg) |
-                                        ((unsigned long long)(end - beg - 1) << 32) | ((unsigned long long)id << 40);
+                o.seg[si] = make_uint4(pbase, vm[k], peers[k], (uint32_t)id);
                 atomicAdd(&o.bin_nseg[id], 1u);
             } else {
-                // bins full: the segment is recorded empty (bin 0, count 0 is
-                // not representable) -- mark it with the all-ones id and drop
-                o.seg[rbase + sb + s] = ~0ull;
-                dropped += end - beg;
+                o.seg[si] = make_uint4(0u, 0u, 0u, 0xFFFFFFFFu);  // bins full: the group is dropped (counted)
+                dropped += __popc(peers[k]);
             }
         }
-        __syncwarp();
+        pbase += __popc(vm[k]);
+        sbase += __popc(lm[k]);
     }
     return dropped;
 }
@@ -520,22 +482,30 @@ __global__ void __launch_bounds__(BF_NT) bf_points_kernel(const double* __restri
 // ---------------------------------------------------------------------------
 // 2. segments by bin (counting sort: offsets from a scan of bin_nseg)
 
-__global__ void bf_seg_scatter_kernel(const CtaDesc* __restrict__ cta, int64_t n_cta,
-                                      const unsigned long long* __restrict__ seg, const uint32_t* __restrict__ seg_off,
-                                      uint32_t* __restrict__ cursor, unsigned long long* __restrict__ sorted) {
+__global__ void bf_seg_scatter_kernel(const CtaDesc* __restrict__ cta, int64_t n_cta, const uint4* __restrict__ seg,
+                                      const uint32_t* __restrict__ seg_off, uint32_t* __restrict__ cursor,
+                                      uint4* __restrict__ sorted) {
     for (int64_t c = blockIdx.x; c < n_cta; c += gridDim.x) {
         const CtaDesc d = cta[c];
         for (uint32_t i = threadIdx.x; i < d.nseg; i += blockDim.x) {
-            const unsigned long long r = seg[d.base + i];
-            if (r == ~0ull) continue;
-            const uint32_t id = (uint32_t)(r >> 40);
-            sorted[seg_off[id] + atomicAdd(&cursor[id], 1u)] = r;
+            const uint4 r = seg[d.base + i];
+            if (r.w == 0xFFFFFFFFu) continue;
+            sorted[seg_off[r.w] + atomicAdd(&cursor[r.w], 1u)] = r;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
 // 3. per-bin aggregation (one CTA per bin)
+//
+// A warp takes the bin's group records 32 at a time (one coalesced load),
+// then walks them with the next record's payload already in flight: lane j
+// of a record holds the group's point j (if any).  Lanes of the record that
+// share a voxel are summed by their leader through a per-warp scratch, and
+// the leader adds into the bin's 512 shared-memory voxels: 64-bit
+// fixed-point sums (conf * 2^31 and conf * frac * 2^31, frac = offset / cell)
+// kept as two 32-bit words updated with native shared atomics (carry into
+// the high word).  Integer sums make the result independent of the order.
 
 __device__ __forceinline__ void add64(uint32_t* lo, uint32_t* hi, unsigned long long t) {
     const uint32_t tl = (uint32_t)t, th = (uint32_t)(t >> 32);
@@ -546,39 +516,81 @@ __device__ __forceinline__ void add64(uint32_t* lo, uint32_t* hi, unsigned long 
 
 __global__ void __launch_bounds__(BF_NT) bf_aggregate_kernel(
     const unsigned long long* __restrict__ bin_keys, const uint32_t* __restrict__ seg_off,
-    const unsigned long long* __restrict__ sorted, const uint32_t* __restrict__ pay, double cell, int64_t max_voxels,
+    const uint4* __restrict__ sorted, const uint32_t* __restrict__ pay, double cell, int64_t max_voxels,
     unsigned long long* __restrict__ ctr, unsigned long long* __restrict__ st_key, float4* __restrict__ st_sum,
     int32_t* __restrict__ st_cnt, uint32_t* __restrict__ st_tag, uint8_t* __restrict__ colcnt) {
     __shared__ uint32_t lo[4][BF_SBV], hi[4][BF_SBV], cnt[BF_SBV];
     __shared__ uint32_t ex[BF_SBV + 1];
+    __shared__ uint32_t scr[BF_WARPS][4][32];
     __shared__ unsigned long long base_s;
     typedef cub::BlockScan<uint32_t, BF_NT> BS;
     __shared__ typename BS::TempStorage scan_tmp;
     const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
     for (int i = threadIdx.x; i < BF_SBV; i += BF_NT) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) { lo[k][i] = 0u; hi[k][i] = 0u; }
         cnt[i] = 0u;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t s0 = seg_off[b], s1 = seg_off[b + 1];
-    for (uint32_t s = s0 + warp; s < s1; s += BF_WARPS) {
-        const unsigned long long r = sorted[s];
-        const uint32_t start = (uint32_t)r, n = (uint32_t)((r >> 32) & 0xFF) + 1u;
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint32_t* e = pay + 3 * (size_t)(start + i);
-            const float c = __uint_as_float(__ldcs(e));
-            const unsigned long long v = (unsigned long long)__ldcs(e + 1) | ((unsigned long long)__ldcs(e + 2) << 32);
-            const int l = (int)(v & 511u);
-            const float qx = (float)((v >> 9) & 0x3FFFFu) + 0.5f, qy = (float)((v >> 27) & 0x3FFFFu) + 0.5f,
-                        qz = (float)((v >> 45) & 0x3FFFFu) + 0.5f;
-            // fixed point: conf * 2^31, conf * frac * 2^31 (frac = q / 2^18)
-            add64(&lo[0][l], &hi[0][l], __float2ull_rn(c * 2147483648.f));
-            add64(&lo[1][l], &hi[1][l], __float2ull_rn(c * qx * 8192.f));
-            add64(&lo[2][l], &hi[2][l], __float2ull_rn(c * qy * 8192.f));
-            add64(&lo[3][l], &hi[3][l], __float2ull_rn(c * qz * 8192.f));
-            atomicAdd(&cnt[l], 1u);
+    uint32_t (&sc)[4][32] = scr[warp];
+    for (uint32_t r0 = s0 + 32 * warp; r0 < s1; r0 += 32 * BF_WARPS) {
+        const int nr = (int)min(32u, s1 - r0);
+        uint4 mine = make_uint4(0u, 0u, 0u, 0u);
+        if (lane < nr) mine = sorted[r0 + lane];
+        // payload of record j for this lane (entry of group lane `lane`)
+        auto fetch = [&](int j, uint32_t& e0, uint32_t& e1, uint32_t& e2, bool& act) {
+            const uint32_t x = __shfl_sync(0xffffffffu, mine.x, j), y = __shfl_sync(0xffffffffu, mine.y, j),
+                           z = __shfl_sync(0xffffffffu, mine.z, j);
+            act = (z >> lane) & 1u;
+            e0 = e1 = e2 = 0u;
+            if (act) {
+                const uint32_t* e = pay + 3 * (size_t)(x + __popc(y & lt));
+                e0 = __ldcs(e);
+                e1 = __ldcs(e + 1);
+                e2 = __ldcs(e + 2);
+            }
+        };
+        uint32_t n0, n1, n2;
+        bool nact;
+        fetch(0, n0, n1, n2, nact);
+        for (int j = 0; j < nr; ++j) {
+            const uint32_t e0 = n0, e1 = n1, e2 = n2;
+            const bool act = nact;
+            if (j + 1 < nr) fetch(j + 1, n0, n1, n2, nact);
+            const float c = __uint_as_float(e0);
+            const unsigned long long v = (unsigned long long)e1 | ((unsigned long long)e2 << 32);
+            const int l = act ? (int)(e1 & 511u) : -1;
+            const unsigned long long t[4] = {
+                __float2ull_rn(c * 2147483648.f), __float2ull_rn(c * ((float)((v >> 9) & 0x3FFFFu) + 0.5f) * 8192.f),
+                __float2ull_rn(c * ((float)((v >> 27) & 0x3FFFFu) + 0.5f) * 8192.f),
+                __float2ull_rn(c * ((float)((v >> 45) & 0x3FFFFu) + 0.5f) * 8192.f)};
+            if (__any_sync(0xffffffffu, t[0] >> 32)) {  // conf > 1 somewhere: per-lane 64-bit adds
+                if (act) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) add64(&lo[k][l], &hi[k][l], t[k]);
+                    atomicAdd(&cnt[l], 1u);
+                }
+                continue;
+            }
+            const unsigned sub = __match_any_sync(0xffffffffu, l);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sc[k][lane] = (uint32_t)t[k];
+            __syncwarp();
+            if (act && lane == __ffs(sub) - 1) {
+                unsigned long long a[4] = {0ull, 0ull, 0ull, 0ull};
+                for (unsigned m = sub; m; m &= m - 1) {
+                    const int q = __ffs(m) - 1;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) a[k] += sc[k][q];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) add64(&lo[k][l], &hi[k][l], a[k]);
+                atomicAdd(&cnt[l], (uint32_t)__popc(sub));
+            }
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -612,14 +624,13 @@ __global__ void __launch_bounds__(BF_NT) bf_aggregate_kernel(
         if (!f[h] || e[h] >= kept) continue;
         const unsigned long long o = base + e[h];
         const long long cx = 8 * bx + (l >> 6), cy = 8 * by + ((l >> 3) & 7), cz = 8 * bz + (l & 7);
-        const double sc = (double)(((unsigned long long)hi[0][l] << 32) | lo[0][l]);
-        const double sx = (double)(((unsigned long long)hi[1][l] << 32) | lo[1][l]);
-        const double sy = (double)(((unsigned long long)hi[2][l] << 32) | lo[2][l]);
-        const double sz = (double)(((unsigned long long)hi[3][l] << 32) | lo[3][l]);
         const double k = cell * 4.656612873077392578125e-10;  // cell / 2^31
         st_key[o] = pack_cells(cx, cy, cz);
-        st_sum[o] = make_float4((float)(sx * k), (float)(sy * k), (float)(sz * k),
-                                (float)(sc * 4.656612873077392578125e-10));
+        double a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = (double)(((unsigned long long)hi[q][l] << 32) | lo[q][l]);
+        st_sum[o] = make_float4((float)(a[1] * k), (float)(a[2] * k), (float)(a[3] * k),
+                                (float)(a[0] * 4.656612873077392578125e-10));
         st_cnt[o] = (int32_t)cnt[l];
         st_tag[o] = ((uint32_t)b << 9) | ((uint32_t)(l >> 3) << 3) | (e[h] - ex[l & ~7]);
     }
@@ -832,9 +843,9 @@ static int bf_reserve(BinFuse* b, int64_t entries, int64_t ctas, cudaStream_t st
     if (b->used + entries > b->cap) {
         const int64_t cap = std::max<int64_t>(b->used + entries, b->cap + b->cap / 2);
         uint32_t* pay = nullptr;
-        unsigned long long* seg = nullptr;
+        uint4* seg = nullptr;
         if (cudaMalloc(&pay, sizeof(uint32_t) * 3 * (size_t)cap) != cudaSuccess ||
-            cudaMalloc(&seg, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess) {
+            cudaMalloc(&seg, sizeof(uint4) * (size_t)cap) != cudaSuccess) {
             cudaFree(pay);
             set_last_error("cudaMalloc(binned fusion payload)", cudaGetLastError());
             return EC3R_ENOMEM;
@@ -842,7 +853,7 @@ static int bf_reserve(BinFuse* b, int64_t entries, int64_t ctas, cudaStream_t st
         if (b->used) {
             EC3R_CUDA_TRY(cudaMemcpyAsync(pay, b->pay, sizeof(uint32_t) * 3 * (size_t)b->used,
                                           cudaMemcpyDeviceToDevice, st));
-            EC3R_CUDA_TRY(cudaMemcpyAsync(seg, b->seg, sizeof(unsigned long long) * (size_t)b->used,
+            EC3R_CUDA_TRY(cudaMemcpyAsync(seg, b->seg, sizeof(uint4) * (size_t)b->used,
                                           cudaMemcpyDeviceToDevice, st));
             EC3R_CUDA_TRY(cudaStreamSynchronize(st));
         }
@@ -952,7 +963,7 @@ static size_t bf_ws_layout(BinFuse* b, int64_t nb, int64_t nseg, BfWs* w) {
     BfWs t;
     t.seg_off = cv.take<uint32_t>(nb + 1);
     t.cursor = cv.take<uint32_t>(nb + 1);
-    t.sorted = cv.take<unsigned long long>(std::max<int64_t>(nseg, 1));
+    t.sorted = cv.take<uint4>(std::max<int64_t>(nseg, 1));
     t.st_key = cv.take<unsigned long long>(V);
     t.st_sum = cv.take<float4>(V);
     t.st_cnt = cv.take<int32_t>(V);

@@ -1,8 +1,8 @@
 """A/B of the two fusion engines on the bench workload (configs[1] by
-default): the binned super-block engine (default) against the legacy
-voxel-block hash (EC3R_FUSE_LEGACY=1 at map creation).  Checks that keys and
-counts are identical and centroids / wsum agree, and times insert + sorted
-extract of each with CUDA events.  Run on the GPU box:
+default): the binned super-block engine (EC3R_FUSE_ENGINE=binned at map
+creation) against the default voxel-block hash.  Checks that keys and counts
+are identical and centroids / wsum agree, and times insert + sorted extract of
+each with CUDA events.  Run on the GPU box:
 
     python tools/fuse_ab.py [--keyframes 300] [--reps 10]
 """
@@ -22,13 +22,13 @@ from paper_2510_02080_b200 import _lib, mapping  # noqa: E402
 
 def run(dm, slots, legacy, reps, U_hint=None):
     if legacy:
-        os.environ["EC3R_FUSE_LEGACY"] = "1"
+        os.environ.pop("EC3R_FUSE_ENGINE", None)
     else:
-        os.environ.pop("EC3R_FUSE_LEGACY", None)
+        os.environ["EC3R_FUSE_ENGINE"] = "binned"
     vmap, out, st = mapping.fuse_slots(dm.pool, slots, 0.02)
     U = int(out[0].numel())
     vmap, out, st = mapping.fuse_slots(dm.pool, slots, 0.02, expected_voxels=U, expected_blocks=st["n_blocks"])
-    os.environ.pop("EC3R_FUSE_LEGACY", None)
+    os.environ.pop("EC3R_FUSE_ENGINE", None)
     bufs = tuple(torch.empty_like(x) for x in out)
     ti, te = [], []
     L = _lib.lib()

@@ -8,7 +8,7 @@ import sys
 
 def main(path, top=25):
     agg, src, f = collections.Counter(), {}, None
-    with open(path) as fh:
+    with open(path, errors="replace") as fh:
         for line in csv.reader(fh):
             if len(line) == 2 and line[0] in ("File Path", "File Name"):
                 f = line[1].split("/")[-1]
