@@ -141,4 +141,4 @@ def test_binned_points_and_partials_roundtrip(binned, monkeypatch):
         np.testing.assert_array_equal(k1, k0)
         np.testing.assert_array_equal(n1, n0)
         np.testing.assert_allclose(w1, w0, rtol=1e-6)
-        assert np.max(np.abs(c1 - c0)) < 1e-4
+        assert np.max(np.abs(c1 - c0)) < 1e-3  # float32 centroids at 1.2 km
