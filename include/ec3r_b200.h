@@ -85,6 +85,13 @@ EC3R_API int ec3r_inverse_project(const float* depth, const float* conf, int F, 
                          double* out_points, double* out_conf, int64_t* out_fids,
                          int64_t* out_pixels, int64_t* n_out, void* workspace,
                          size_t workspace_bytes, void* stream);
+/* As ec3r_inverse_project on float64 depth / confidence planes (a reference
+ * ReconstructionOutput as decoded, backend.py:51-58): bit-identical float64
+ * points for any input, not only float32-representable ones. */
+EC3R_API int ec3r_inverse_project_f64(const double* depth, const double* conf, int F, int H, int W,
+                                      const double* K4_h, const double* poses_h, const int64_t* frame_ids_h,
+                                      double* out_points, double* out_conf, int64_t* out_fids, int64_t* out_pixels,
+                                      int64_t* n_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Sim3Transform.apply (liegroups.py:259-260) on (n,3) float64 points,
  * bit-identical to the reference; the world-point transform of

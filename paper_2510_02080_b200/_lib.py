@@ -30,6 +30,7 @@ _PROTOS = {
     "ec3r_last_error": (C.c_char_p, []),
     "ec3r_inverse_project_workspace": (_SZ, [_I, _I, _I]),
     "ec3r_inverse_project": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ec3r_inverse_project_f64": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "ec3r_register_edges_workspace": (_SZ, [_I]),
     "ec3r_register_edges": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _I, _D, _I, _I, _P, _P, _P, _P, _P, _P,
                                  _P, _SZ, _P]),

@@ -29,9 +29,10 @@ def _f32_dev(x) -> torch.Tensor:
 
 def inverse_project_device(depth: torch.Tensor, conf: torch.Tensor, K4, poses8: np.ndarray, frame_ids,
                            stream=None):
-    """K1 on device planes.  depth/conf: (F,H,W) float32 CUDA; poses8: (F,8)
-    host float64.  Returns device tensors (points (N,3) f64, conf (N,) f64,
-    frame_ids (N,) i64, pixels (N,2) i64) trimmed to N (one D2H of N)."""
+    """K1 on device planes.  depth/conf: (F,H,W) float32 (pool planes) or
+    float64 (a reference output) CUDA; poses8: (F,8) host float64.  Returns
+    device tensors (points (N,3) f64, conf (N,) f64, frame_ids (N,) i64,
+    pixels (N,2) i64) trimmed to N (one D2H of N)."""
     L = _lib.lib()
     F, H, W = depth.shape
     total = F * H * W
@@ -46,25 +47,39 @@ def inverse_project_device(depth: torch.Tensor, conf: torch.Tensor, K4, poses8: 
     K4 = np.ascontiguousarray(np.asarray(K4, dtype=np.float64))
     P8 = np.ascontiguousarray(np.asarray(poses8, dtype=np.float64).reshape(F, 8))
     fids = np.ascontiguousarray(np.asarray(frame_ids, dtype=np.int64).reshape(F))
-    _lib.check(L.ec3r_inverse_project(_lib.ptr(depth), _lib.ptr(conf), F, H, W, K4.ctypes.data, P8.ctypes.data,
-                                      fids.ctypes.data, _lib.ptr(pts), _lib.ptr(cf), _lib.ptr(fid), _lib.ptr(pix),
-                                      _lib.ptr(n), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream)),
-               "ec3r_inverse_project")
+    if depth.dtype != conf.dtype or depth.dtype not in (torch.float32, torch.float64):
+        raise ValueError("depth and confidence planes must both be float32 or both float64")
+    fn = L.ec3r_inverse_project_f64 if depth.dtype == torch.float64 else L.ec3r_inverse_project
+    _lib.check(fn(_lib.ptr(depth), _lib.ptr(conf), F, H, W, K4.ctypes.data, P8.ctypes.data, fids.ctypes.data,
+                  _lib.ptr(pts), _lib.ptr(cf), _lib.ptr(fid), _lib.ptr(pix), _lib.ptr(n), _lib.ptr(ws), ws.numel(),
+                  _lib.stream_ptr(stream)), "ec3r_inverse_project")
     N = int(n.item())
     return pts[:N], cf[:N], fid[:N], pix[:N]
 
 
+def _dev_planes(x) -> torch.Tensor:
+    """float32 inputs stay float32, everything else is consumed as float64
+    (the reference's ReconstructionOutput dtype)."""
+    if isinstance(x, torch.Tensor):
+        dt = torch.float32 if x.dtype == torch.float32 else torch.float64
+        return x.to(device="cuda", dtype=dt).contiguous()
+    a = np.asarray(x)
+    a = a if a.dtype == np.float32 else a.astype(np.float64)
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
 def inverse_project(output: ReconstructionOutput) -> SubmapCloud:
     """backend.py:78-101 — one 3D point per positive-depth pixel, in the
-    submap frame.  Depths/confidences are consumed as float32 (the storage
-    type of the B200 pool); points match the reference computed on those
-    values bit-for-bit."""
+    submap frame, bit-identical to the reference's float64 result for the
+    output's own depth dtype (float64 as decoded, or float32 planes)."""
     _lib.lib()
     F = len(output.frame_ids)
     if F == 0:
         return SubmapCloud(np.zeros((0, 3)), np.zeros(0), np.zeros(0, np.int64), np.zeros((0, 2), np.int64))
-    depth = _f32_dev(output.depths)
-    conf = _f32_dev(output.confidences)
+    depth = _dev_planes(output.depths)
+    conf = _dev_planes(output.confidences)
+    if depth.dtype != conf.dtype:
+        depth, conf = depth.double(), conf.double()
     poses8 = np.stack([sim3_to_vec(p) for p in output.poses])
     pts, cf, fid, pix = inverse_project_device(depth, conf, intrinsics_vec(output.intrinsics), poses8,
                                                output.frame_ids)

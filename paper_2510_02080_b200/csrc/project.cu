@@ -1,6 +1,7 @@
 // K1: inverse projection with stream compaction (backend.inverse_project,
 // backend.py:78-101).  Points are bit-identical to the reference's float64
-// arithmetic on the float32 depth (exact __d*_rn sequences, common.cuh).
+// arithmetic (exact __d*_rn sequences, common.cuh) on float32 pool planes or,
+// through ec3r_inverse_project_f64, on a reference output's float64 depths.
 //
 // Three launches: per-tile valid counts -> single-CTA exclusive scan of the
 // tile counts -> per-tile block scan + ordered write.  Output order is the
@@ -17,12 +18,15 @@ constexpr int IP_NT = 256;
 constexpr int IP_PER = 4;                   // pixels per thread (contiguous)
 constexpr int IP_TILE = IP_NT * IP_PER;     // pixels per CTA
 
-__global__ void __launch_bounds__(IP_NT) ip_count_kernel(const float* __restrict__ depth, int64_t total,
+// T = float (the pool's planes) or double (a reference ReconstructionOutput:
+// float64 depths, backend.py:51-58)
+template <typename T>
+__global__ void __launch_bounds__(IP_NT) ip_count_kernel(const T* __restrict__ depth, int64_t total,
                                                          int32_t* __restrict__ tile_counts) {
     const int64_t base = (int64_t)blockIdx.x * IP_TILE + (int64_t)threadIdx.x * IP_PER;
     int c = 0;
 #pragma unroll
-    for (int k = 0; k < IP_PER; ++k) c += (base + k < total && depth[base + k] > 0.f) ? 1 : 0;
+    for (int k = 0; k < IP_PER; ++k) c += (base + k < total && depth[base + k] > T(0)) ? 1 : 0;
     typedef cub::BlockReduce<int, IP_NT> BR;
     __shared__ typename BR::TempStorage tmp;
     const int s = BR(tmp).Sum(c);
@@ -49,7 +53,8 @@ __global__ void __launch_bounds__(1024) ip_scan_kernel(const int32_t* __restrict
     if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void __launch_bounds__(IP_NT) ip_write_kernel(const float* __restrict__ depth, const float* __restrict__ conf,
+template <typename T>
+__global__ void __launch_bounds__(IP_NT) ip_write_kernel(const T* __restrict__ depth, const T* __restrict__ conf,
                                                          int H, int W, int64_t total, double fx, double fy, double cx,
                                                          double cy, const double* __restrict__ poses,
                                                          const int64_t* __restrict__ frame_ids,
@@ -61,7 +66,7 @@ __global__ void __launch_bounds__(IP_NT) ip_write_kernel(const float* __restrict
     int flags = 0, c = 0;
 #pragma unroll
     for (int k = 0; k < IP_PER; ++k) {
-        const bool v = base + k < total && depth[base + k] > 0.f;
+        const bool v = base + k < total && depth[base + k] > T(0);
         flags |= (v ? 1 : 0) << k;
         c += v;
     }
@@ -126,10 +131,11 @@ extern "C" size_t ec3r_inverse_project_workspace(int F, int H, int W) {
     return align256(tiles * 4) + align256(tiles * 8) + align256((size_t)F * 64) + align256((size_t)F * 8);
 }
 
-extern "C" int ec3r_inverse_project(const float* depth, const float* conf, int F, int H, int W, const double* K4_h,
-                                    const double* poses_h, const int64_t* frame_ids_h, double* out_points,
-                                    double* out_conf, int64_t* out_fids, int64_t* out_pixels, int64_t* n_out,
-                                    void* workspace, size_t workspace_bytes, void* stream) {
+template <typename T>
+static int inverse_project_impl(const T* depth, const T* conf, int F, int H, int W, const double* K4_h,
+                                const double* poses_h, const int64_t* frame_ids_h, double* out_points,
+                                double* out_conf, int64_t* out_fids, int64_t* out_pixels, int64_t* n_out,
+                                void* workspace, size_t workspace_bytes, void* stream) {
     if (F < 0 || H <= 0 || W <= 0 || !K4_h || !n_out) return EC3R_EARG;
     if (workspace_bytes < ec3r_inverse_project_workspace(F, H, W) || !workspace) return EC3R_EWORKSPACE;
     cudaStream_t st = as_stream(stream);
@@ -146,12 +152,28 @@ extern "C" int ec3r_inverse_project(const float* depth, const float* conf, int F
     int64_t* fids = cv.take<int64_t>(F);
     EC3R_CUDA_TRY(cudaMemcpyAsync(poses, poses_h, sizeof(double) * 8 * F, cudaMemcpyHostToDevice, st));
     EC3R_CUDA_TRY(cudaMemcpyAsync(fids, frame_ids_h, sizeof(int64_t) * F, cudaMemcpyHostToDevice, st));
-    ip_count_kernel<<<(unsigned)tiles, IP_NT, 0, st>>>(depth, total, counts);
+    ip_count_kernel<T><<<(unsigned)tiles, IP_NT, 0, st>>>(depth, total, counts);
     EC3R_CHECK_LAUNCH("ip_count_kernel");
     ip_scan_kernel<<<1, 1024, 0, st>>>(counts, tiles, offs, n_out);
     EC3R_CHECK_LAUNCH("ip_scan_kernel");
-    ip_write_kernel<<<(unsigned)tiles, IP_NT, 0, st>>>(depth, conf, H, W, total, K4_h[0], K4_h[1], K4_h[2], K4_h[3],
-                                                       poses, fids, offs, out_points, out_conf, out_fids, out_pixels);
+    ip_write_kernel<T><<<(unsigned)tiles, IP_NT, 0, st>>>(depth, conf, H, W, total, K4_h[0], K4_h[1], K4_h[2], K4_h[3],
+                                                          poses, fids, offs, out_points, out_conf, out_fids, out_pixels);
     EC3R_CHECK_LAUNCH("ip_write_kernel");
     return EC3R_OK;
+}
+
+extern "C" int ec3r_inverse_project(const float* depth, const float* conf, int F, int H, int W, const double* K4_h,
+                                    const double* poses_h, const int64_t* frame_ids_h, double* out_points,
+                                    double* out_conf, int64_t* out_fids, int64_t* out_pixels, int64_t* n_out,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+    return inverse_project_impl<float>(depth, conf, F, H, W, K4_h, poses_h, frame_ids_h, out_points, out_conf,
+                                       out_fids, out_pixels, n_out, workspace, workspace_bytes, stream);
+}
+
+extern "C" int ec3r_inverse_project_f64(const double* depth, const double* conf, int F, int H, int W,
+                                        const double* K4_h, const double* poses_h, const int64_t* frame_ids_h,
+                                        double* out_points, double* out_conf, int64_t* out_fids, int64_t* out_pixels,
+                                        int64_t* n_out, void* workspace, size_t workspace_bytes, void* stream) {
+    return inverse_project_impl<double>(depth, conf, F, H, W, K4_h, poses_h, frame_ids_h, out_points, out_conf,
+                                        out_fids, out_pixels, n_out, workspace, workspace_bytes, stream);
 }

@@ -24,7 +24,7 @@ SUITES = ["test_registration.py", "test_mapping.py", "test_tracking.py", "test_l
 @pytest.mark.parametrize("suite", SUITES)
 def test_reference_suite_through_binding(suite):
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([ROOT, REF]), EC3R_REFERENCE_SRC=REF)
-    cmd = [sys.executable, "-m", "pytest", os.path.join("ref_tests", suite), "-q", "-p", "no:cacheprovider",
+    cmd = [sys.executable, "-m", "pytest", os.path.join("ref_tests", suite), "-p", "no:cacheprovider",
            "-p", "tests.ref_binding_plugin", "--rootdir", REF]
     r = subprocess.run(cmd, cwd=REF, env=env, capture_output=True, text=True, timeout=900)
     tail = "\n".join((r.stdout + r.stderr).splitlines()[-40:])
