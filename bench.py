@@ -99,7 +99,20 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # workload
 
-def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
+CONFIGS = {
+    1: dict(keyframes=300, invalid=0.0,
+            workload="configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
+                     "tracking match + align + fuse"),
+    3: dict(keyframes=1500, invalid=0.0,
+            workload="configs[3]: large indoor map, 1500 keyframes / 300 submaps per GPU, 2 cm voxel-hash fusion, "
+                     "1024 descriptors per frame"),
+    4: dict(keyframes=500, invalid=0.5,
+            workload="configs[4]: 4000-keyframe long trajectory sharded 500 keyframes per GPU (8 x B200), ~50% "
+                     "invalid pixels (~400M raw points at 8 GPUs), submap-sharded align + fuse"),
+}
+
+
+def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device, invalid: float = 0.0):
     import torch
 
     from paper_2510_02080_b200 import mapping, synth
@@ -107,7 +120,7 @@ def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
     cfg = synth.SceneConfig()
     stub, send_pos = None, []
     if world == 1:
-        sb = synth.make_submaps(n_kf, cfg, seed=rank, device=device)
+        sb = synth.make_submaps(n_kf, cfg, seed=rank, device=device, invalid_fraction=invalid)
         dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8))
     else:
         # one sequence of n_kf x world keyframes (world x the laps, so every
@@ -120,7 +133,8 @@ def build_workload(rank: int, world: int, n_kf: int, n_desc: int, device):
         batches = synth.flush_batches(n_kf * world)
         lo, hi = pdist.shard_window(len(batches), world, rank)
         send_pos, recv_ids = pdist.halo_handshake(batches[lo], batches[hi - 1])
-        sb = synth.make_submaps(n_kf * world, cfg, seed=0, device=device, batch_range=(lo, hi))
+        sb = synth.make_submaps(n_kf * world, cfg, seed=0, device=device, batch_range=(lo, hi),
+                                invalid_fraction=invalid)
         dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4, slot_capacity=len(sb.poses8) + len(recv_ids))
         if recv_ids:  # stub slots first: a ChainPlan walks contiguous slots
             n = len(recv_ids)
@@ -230,12 +244,58 @@ def stage_ms(records):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port) on a bounded sample
+# CPU reference on a bounded sample, scaled to the GPU step's per-step mix
 
-def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: float = 20.0):
-    """Times the oracle port of the path on a bounded sample: registration of
-    n_submaps-1 edges + voxel fusion of n_submaps submaps (points/s), and
-    n_match tracking matches of 1024 x 1024 x 256 (pairs/s)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_module():
+    """The unmodified reference package (installed into baseline/_ref by
+    tools/install_reference.sh; it travels to the GPU box), or None."""
+    if os.path.isdir(os.path.join(REF_DIR, "submap_slam")) and REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import submap_slam  # noqa: F401
+        return submap_slam
+    except ImportError:
+        return None
+
+
+def _ref_submaps(sb, cfg, n_submaps):
+    """Reference Submap objects (mapping.py:30-62) of the first n synthetic
+    submaps, through the reference's own inverse_project (backend.py:78-101);
+    returns (submaps, seconds spent in inverse_project)."""
+    from submap_slam.backend import ReconstructionOutput, inverse_project
+    from submap_slam.geometry import CameraIntrinsics
+    from submap_slam.liegroups import Pose3, Rotation3, Sim3Transform
+    from submap_slam.mapping import Submap
+
+    K = CameraIntrinsics(float(sb.K4[0]), float(sb.K4[1]), float(sb.K4[2]), float(sb.K4[3]), cfg.width, cfg.height)
+    out, t_ip = [], 0.0
+    for j, ids in enumerate(sb.frame_ids[:n_submaps]):
+        o, F = sb.slot_offsets[j], len(ids)
+        poses = tuple(Pose3(Rotation3(p[1:5]), p[5:].copy()) for p in sb.poses8[o:o + F])
+        ro = ReconstructionOutput(tuple(ids), sb.depth[o:o + F].double().numpy(), sb.conf[o:o + F].double().numpy(),
+                                  poses, K, j)
+        t0 = time.perf_counter()
+        cloud = inverse_project(ro)
+        t_ip += time.perf_counter() - t0
+        out.append(Submap(j, tuple(ids), cloud, {f: p for f, p in zip(ids, poses)}, K, Sim3Transform.identity(), j))
+    return out, t_ip
+
+
+def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: float = 20.0, use_reference=True):
+    """Times the reference CPU path on a bounded sample of the configs[1]
+    workload and scales it to the GPU step's mix (60 submaps decoded and
+    fused, 59 registration edges, 1500 tracking matches of 1024 x 1024 x 256):
+    step time = 60 x t(submap) + 59 x t(edge) + 1500 x t(match).
+
+    With the reference importable (baseline/_ref): its own inverse_project,
+    Mapping._shared_correspondences + the gate of _registration_edges +
+    align_point_sets (mapping.py:138-188, registration.py:38-102),
+    Submap.world_points concatenation (fused_cloud, mapping.py:332-338) and
+    match_descriptors (tracking.py:143-170); the voxel rule, which the
+    reference does not have, is oracle/fuse.py.  Else the oracle port."""
     import torch
 
     from oracle import fuse as ofuse
@@ -244,33 +304,71 @@ def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: fl
 
     cfg = synth.SceneConfig()
     sb = synth.make_submaps(5 * n_submaps + 1, cfg, seed=seed, device="cpu")
-    dense = []
-    for j, ids in enumerate(sb.frame_ids[:n_submaps]):
-        o, F = sb.slot_offsets[j], len(ids)
-        dense.append(dict(depth=sb.depth[o:o + F].numpy(), conf=sb.conf[o:o + F].numpy(), frame_ids=np.array(ids),
-                          pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:], K=sb.K4))
-    t0 = time.perf_counter()
-    globs = [(1.0, np.array([1.0, 0, 0, 0]), np.zeros(3))]
-    for j in range(1, len(dense)):
-        e = ref.registration_edge(dense[j], dense[j - 1])
-        globs.append(ref.sim3_compose(globs[j - 1], (e["s"], e["q"], e["t"])))
-    f = ofuse.fuse_submaps(dense, globs, 0.02)
-    t_fuse = time.perf_counter() - t0
-    pts = f["n_in"]
     A, B, ao, bo = synth.make_descriptor_pairs(n_match, 1024, 1024, 256, 0.05, seed=seed, device="cpu")
     a = A.view(torch.bfloat16).double().numpy()
     b = B.view(torch.bfloat16).double().numpy()
+    rm = reference_module() if use_reference else None
+    if rm is not None:
+        from submap_slam.mapping import Mapping, MappingConfig
+        from submap_slam.registration import align_point_sets
+        from submap_slam.tracking import match_descriptors
+
+        kind = "reference"
+        mcfg = MappingConfig()
+        sms, t_ip = _ref_submaps(sb, cfg, n_submaps)
+        mp = Mapping.__new__(Mapping)  # only the config and _shared_correspondences are used
+        mp.config = mcfg
+        t0 = time.perf_counter()
+        for j in range(1, len(sms)):
+            p, q, w = mp._shared_correspondences(sms[j], sms[j - 1])
+            floor = mcfg.confidence_floor_frac * float(w.max())
+            keep = w >= floor
+            tr, _ = align_point_sets(p[keep], q[keep], w[keep])
+            sms[j].global_pose = sms[j - 1].global_pose.compose(tr)
+        t_edges = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        x = np.concatenate([sm.world_points() for sm in sms])
+        c = np.concatenate([sm.cloud.confidences for sm in sms])
+        f = ofuse.fuse_points(x, c, 0.02)
+        t_fuse = time.perf_counter() - t0 + t_ip
+        match = match_descriptors
+    else:
+        kind = "port"
+        dense = []
+        for j, ids in enumerate(sb.frame_ids[:n_submaps]):
+            o, F = sb.slot_offsets[j], len(ids)
+            dense.append(dict(depth=sb.depth[o:o + F].numpy(), conf=sb.conf[o:o + F].numpy(), frame_ids=np.array(ids),
+                              pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:], K=sb.K4))
+        t0 = time.perf_counter()
+        globs = [(1.0, np.array([1.0, 0, 0, 0]), np.zeros(3))]
+        for j in range(1, len(dense)):
+            e = ref.registration_edge(dense[j], dense[j - 1])
+            globs.append(ref.sim3_compose(globs[j - 1], (e["s"], e["q"], e["t"])))
+        t_edges = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        f = ofuse.fuse_submaps(dense, globs, 0.02)
+        t_fuse = time.perf_counter() - t0
+        match = ref.match_descriptors
+    pts = f["n_in"]
     t1 = time.perf_counter()
+    done = 0
     for p in range(n_match):
-        ref.match_descriptors(a[ao[p]:ao[p + 1]], b[bo[p]:bo[p + 1]], 0.8)
-        if time.perf_counter() - t0 > budget_s:
-            n_match = p + 1
+        match(a[ao[p]:ao[p + 1]], b[bo[p]:bo[p + 1]], 0.8)
+        done = p + 1
+        if time.perf_counter() - t1 > budget_s:
             break
     t_match = time.perf_counter() - t1
-    return {"points": pts, "t_fuse": t_fuse, "points_per_s": pts / t_fuse, "pairs": n_match * 1024 * 1024,
-            "t_match": t_match, "pairs_per_s": n_match * 1024 * 1024 / t_match,
-            "sample": f"oracle port: {n_submaps - 1} registration edges + 2 cm voxel fusion of {n_submaps} submaps "
-                      f"({pts} points, 518x392) and {n_match} matches of 1024x1024x256 (reference per-row loop)"}
+    n_edges = max(n_submaps - 1, 1)
+    t_sub, t_edge, t_m = t_fuse / n_submaps, t_edges / n_edges, t_match / done
+    step_s = 60 * t_sub + 59 * t_edge + 1500 * t_m
+    step_pts = pts / n_submaps * 60
+    return {"kind": kind, "points": pts, "points_per_s": step_pts / step_s, "step_s": step_s,
+            "t_submap_s": t_sub, "t_edge_s": t_edge, "t_match_s": t_m,
+            "pairs_per_s": 1024 * 1024 / t_m,
+            "sample": f"{'unmodified reference (baseline/_ref)' if kind == 'reference' else 'oracle port'}: "
+                      f"{n_submaps} submaps decoded + fused at 2 cm ({pts} points, 518x392), {n_edges} registration "
+                      f"edge(s), {done} match(es) of 1024x1024x256; scaled to the GPU step's mix "
+                      f"(60 submaps, 59 edges, 1500 matches): step = 60 t_submap + 59 t_edge + 1500 t_match"}
 
 
 def cpu_cores():
@@ -288,7 +386,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--keyframes", type=int, default=300)
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
+                    help="BASELINE configs[i] preset (1: the headline, 3: 1500-keyframe map, 4: 500 keyframes per "
+                         "GPU with ~50%% invalid pixels)")
+    ap.add_argument("--keyframes", type=int, default=None, help="override the preset's keyframes per GPU")
     ap.add_argument("--desc", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -297,6 +398,12 @@ def main():
                     help="gloo: validation of the N>1 path with ranks sharing a GPU (not a measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    preset = CONFIGS[args.config]
+    if args.keyframes is None:
+        args.keyframes = preset["keyframes"]
+    args.invalid = preset["invalid"]
+    args.workload = preset["workload"] if args.keyframes == preset["keyframes"] else (
+        f"configs[{args.config}] shape at {args.keyframes} keyframes per GPU")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -319,7 +426,7 @@ def main():
     from paper_2510_02080_b200 import _lib
 
     L = _lib.lib()
-    dm, sms, desc, halo = build_workload(rank, world, args.keyframes, args.desc, "cuda")
+    dm, sms, desc, halo = build_workload(rank, world, args.keyframes, args.desc, "cuda", args.invalid)
     step = Step(dm, sms, desc, halo=halo)
     for _ in range(args.warmup):
         step.run()
@@ -417,8 +524,9 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         c = cpu_sample()
-        cpu = {"value": c["points_per_s"], "unit": "points/s", "cores": cpu_cores(), "kind": "port",
-               "sample": c["sample"], "matches_value": c["pairs_per_s"], "matches_unit": "candidate pairs/s"}
+        cpu = {"value": c["points_per_s"], "unit": "fused map points/s", "cores": cpu_cores(), "kind": c["kind"],
+               "sample": c["sample"], "step_s": c["step_s"], "matches_value": c["pairs_per_s"],
+               "matches_unit": "candidate pairs/s", "same_config": True}
 
     if rank == 0:
         line = {
@@ -426,8 +534,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 planes / f64 transforms+moments / bf16 tensor-core matcher",
             "data": "synthetic (device ray-cast box room, seeded)",
-            "config": {"workload": "configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
-                                   "tracking match + align + fuse",
+            "config": {"workload": args.workload, "invalid_pixel_fraction": args.invalid,
                        "keyframes_per_gpu": args.keyframes, "frames_tracked_per_gpu": int(len(ao) - 1),
                        "local_maps_per_gpu": int(B.shape[0]) // args.desc,
                        "resolution": [W, H], "voxel_m": 0.02, "submaps_per_gpu": len(sms),
@@ -666,27 +773,31 @@ def run_extras(peaks):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the
-    host cores, rank 0 only, bounded samples of the same workload."""
+    """--impl reference: the reference's own CPU implementation (the
+    unmodified package from baseline/_ref; the oracle port only when it is
+    absent) on the host cores, rank 0 only.  Each step is a bounded sample
+    of the configs[1] workload scaled to the GPU step's mix (cpu_sample)."""
     if rank != 0:
         return
-    vals, mvals = [], []
+    vals, mvals, steps_s = [], [], []
     c = None
     for k in range(args.warmup + args.steps):
         c = cpu_sample(n_submaps=2, n_match=1, seed=k, budget_s=15.0)
         if k >= args.warmup:
             vals.append(c["points_per_s"])
             mvals.append(c["pairs_per_s"])
+            steps_s.append(c["step_s"])
     v = float(np.median(vals))
     line = {"metric": METRIC, "value": v, "unit": "fused map points/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (same generator, CPU)", "impl": "reference",
+            "warmup": args.warmup, "ms_per_step": float(np.median(steps_s)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator, CPU)",
+            "impl": "reference",
             "config": {"workload": "configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
                                    "tracking match + align + fuse",
-                       "sample": "each step a bounded sample of that workload: 1 registration edge + 2 cm fusion "
-                                 "of 2 submaps and one 1024x1024x256 match", "voxel_m": 0.02},
+                       "sample": "each step a bounded sample (2 submaps, 1 edge, 1 match) scaled to the full "
+                                 "step's mix: 60 submaps decoded + fused, 59 edges, 1500 matches", "voxel_m": 0.02},
             "matches_per_s": float(np.median(mvals)), "matches_unit": "candidate descriptor pairs/s",
-            "cpu_baseline": {"value": v, "unit": "points/s", "cores": cpu_cores(), "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "fused map points/s", "cores": cpu_cores(), "kind": c["kind"],
                              "sample": c["sample"]},
             "e2e": {"value": v, "unit": "fused map points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
