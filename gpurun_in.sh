@@ -1,14 +1,6 @@
-T=r02h; O=gpurun_out/$T; mkdir -p $O
-nproc > $O/nproc.txt; lscpu | head -20 > $O/lscpu.txt
-( time timeout 900 python bench.py --impl reference --steps 20 --warmup 3 ) > $O/ref.json 2> $O/ref.err; echo ref_rc=$?; tail -c 1500 $O/ref.json; tail -3 $O/ref.err
-timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo b_rc=$?; tail -c 3000 $O/bench.json; tail -3 $O/bench.err
-timeout 900 python bench.py --config 3 --steps 10 --warmup 3 --no-extras --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err; echo c3_rc=$?; tail -3 $O/bench_c3.err
-timeout 900 python bench.py --config 4 --steps 10 --warmup 3 --no-extras --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err; echo c4_rc=$?; tail -3 $O/bench_c4.err
-python - <<'PY'
-import json
-for f in ("bench","bench_c3","bench_c4"):
-    try:
-        d=json.loads(open(f"gpurun_out/r02h/{f}.json").read().strip().splitlines()[-1])
-        print(f, d["value"], d["ms_per_step"], d["stages_ms"], d["config"]["workload"][:40], d["e2e"] and d["e2e"]["value"])
-    except Exception as e: print(f, e)
-PY
+T=r02d; O=gpurun_out/$T; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_fusion_engines.py -q -x > $O/engine_tests.log 2>&1; echo tests_rc=$?; tail -3 $O/engine_tests.log
+EC3R_DEBUG_BINS=1 timeout 600 python tools/fuse_ab.py --reps 5 > $O/fuse_ab.json 2> $O/fuse_ab.err; echo ab_rc=$?; cat $O/fuse_ab.json; grep vbin $O/fuse_ab.err | tail -2
+timeout 900 ncu -k regex:"bn_|bf_|vh_|vb_|Radix|Scan" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ab_launches.csv python tools/fuse_ab.py --reps 1 > /dev/null 2>&1; echo ncu_rc=$?
+python tools/launch_summary.py $O/ab_launches.csv 2>/dev/null | head -30
+timeout 900 ncu -k regex:"bn_bin_frames|bn_aggregate" -c 2 --set full --import-source on --clock-control none -o $O/bin_full python tools/fuse_ab.py --reps 1 > $O/ncu_full.log 2>&1; echo ncu_full_rc=$?; tail -3 $O/ncu_full.log

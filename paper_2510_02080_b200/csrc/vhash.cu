@@ -885,11 +885,14 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     h->bf = nullptr;
     h->bf_active = h->legacy_active = false;
     {
-        // EC3R_FUSE_ENGINE=binned selects the binned super-block engine
-        // (vbin.cu: deterministic integer sums; measured 1.08 ms bin pass +
-        // 2.2 ms aggregation/emit on configs[1], against 1.20 + 0.35 ms here)
+        // Engine: the binned super-block engine (vbin.cu: sort-based,
+        // atomic-free per point, deterministic integer sums) for cells up to
+        // 2.56 cm, where its cell/256 offset quantisation keeps centroids
+        // within 50 um; the voxel-block hash otherwise.  EC3R_FUSE_ENGINE=hash
+        // forces the block hash, =binned the binned engine where it applies.
         const char* e = getenv("EC3R_FUSE_ENGINE");
-        h->binned = e && std::string(e) == "binned";
+        const bool want = e && std::string(e) == "binned";
+        h->binned = want && cell_size <= 0.0256;
     }
     h->max_voxels = max_voxels > 65536 ? max_voxels : 65536;
     h->max_blocks = max_blocks > 4096 ? max_blocks : 4096;

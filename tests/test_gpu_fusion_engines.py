@@ -95,7 +95,8 @@ def test_binned_equals_block_hash_engine(golden, monkeypatch):
     kb, cb, wb, nb = (x.cpu().numpy() for x in b.extract())
     np.testing.assert_array_equal(ka, kb)
     np.testing.assert_array_equal(na, nb)
-    assert np.max(np.abs(ca - cb)) < 1e-5
+    # binned in-voxel offsets are quantised to cell/256: <= cell/512 = 39 um
+    assert np.max(np.abs(ca - cb)) < 0.02 / 512 + 2e-6
     np.testing.assert_allclose(wa, wb, rtol=1e-5)
 
 
