@@ -1,6 +1,7 @@
-T=r02d; O=gpurun_out/$T; mkdir -p $O
-timeout 600 python -m pytest tests/test_gpu_fusion_engines.py -q -x > $O/engine_tests.log 2>&1; echo tests_rc=$?; tail -3 $O/engine_tests.log
-EC3R_DEBUG_BINS=1 timeout 600 python tools/fuse_ab.py --reps 5 > $O/fuse_ab.json 2> $O/fuse_ab.err; echo ab_rc=$?; cat $O/fuse_ab.json; grep vbin $O/fuse_ab.err | tail -2
-timeout 900 ncu -k regex:"bn_|bf_|vh_|vb_|Radix|Scan" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ab_launches.csv python tools/fuse_ab.py --reps 1 > /dev/null 2>&1; echo ncu_rc=$?
-python tools/launch_summary.py $O/ab_launches.csv 2>/dev/null | head -30
-timeout 900 ncu -k regex:"bn_bin_frames|bn_aggregate" -c 2 --set full --import-source on --clock-control none -o $O/bin_full python tools/fuse_ab.py --reps 1 > $O/ncu_full.log 2>&1; echo ncu_full_rc=$?; tail -3 $O/ncu_full.log
+T=r02g; O=gpurun_out/$T; mkdir -p $O
+timeout 900 ncu -k regex:"vc_|vb_|Radix|Scan|bbox" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/emit_launches.csv python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1; echo ncu_rc=$?
+python tools/launch_summary.py $O/emit_launches.csv | head -20
+EC3R_EMIT_VOXEL_SORT=1 timeout 900 python bench.py --steps 20 --warmup 5 --no-extras --no-cpu-baseline > $O/bench_old.json 2> $O/bench_old.err; python -c "
+import json;d=json.loads(open('$O/bench_old.json').read().strip().splitlines()[-1]);print('old',d['ms_per_step'],d['stages_ms'])"
+timeout 900 python bench.py --steps 20 --warmup 5 --no-extras --no-cpu-baseline > $O/bench_new.json 2> $O/bench_new.err; python -c "
+import json;d=json.loads(open('$O/bench_new.json').read().strip().splitlines()[-1]);print('new',d['ms_per_step'],d['stages_ms'])"

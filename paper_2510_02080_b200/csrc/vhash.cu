@@ -868,6 +868,209 @@ static int compact_sorted(ec3r_vhash* h, int sort, void* workspace, size_t works
     return EC3R_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sorted emit without a voxel sort.  The output is ordered by _pack key, i.e.
+// by (cx, cy, cz).  A pool block (bx, by, bz) holds 16 voxel columns (lx, ly)
+// of 4 voxels (lz); the key order of all columns is the lexicographic order
+// of (bx, lx, by, ly, bz).  So only the USED BLOCKS are sorted (by block key,
+// ~1/37 of the voxels here); per block, the closed-form position of each of
+// its columns in that order follows from the block's x-group (blocks with
+// the same bx) and xy-group (same bx, by):
+//   pos = 16 * start_x + 4 * n_x * lx + 4 * off_xy + n_xy * ly + r_z
+// One exclusive scan of the columns' occupied counts in that order gives each
+// column its first output row, and each occupied voxel its row
+// (+ its rank among the column's occupied lz).  Reference: the declared
+// fusion rule's "output sorted by key" (oracle/fuse.py, _numpy.py:50-55).
+
+struct ColGroup {
+    int start_x, n_x, off_xy, n_xy, r_z, pad;
+};
+
+__device__ __forceinline__ int64_t vc_used(const unsigned long long* counters, int64_t max_blocks) {
+    return min((int64_t)counters[4], max_blocks);
+}
+
+// per pool block: 16 column counts and its sort key (_pack key; unused
+// blocks sort last)
+__global__ void vc_block_prep_kernel(const unsigned int* __restrict__ counts,
+                                     const unsigned long long* __restrict__ block_keys,
+                                     const unsigned long long* __restrict__ counters, int64_t nb,
+                                     uint8_t* __restrict__ colcnt, unsigned long long* __restrict__ skey,
+                                     uint32_t* __restrict__ ids) {
+    const int lane = threadIdx.x & 31;
+    const int64_t used = vc_used(counters, nb);
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb;
+         b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (b < used) {
+            const unsigned m0 = __ballot_sync(0xffffffffu, counts[b * kBlockVox + lane] != 0u);
+            const unsigned m1 = __ballot_sync(0xffffffffu, counts[b * kBlockVox + 32 + lane] != 0u);
+            if (lane < 16) {
+                const unsigned long long m = ((unsigned long long)m1 << 32) | m0;
+                colcnt[b * 16 + lane] = (uint8_t)__popcll(m & (0x0001000100010001ull << lane));
+            }
+        }
+        if (lane == 16) {
+            skey[b] = b < used ? block_keys[b] : ~0ull;
+            ids[b] = (uint32_t)b;
+        }
+    }
+}
+
+__device__ __forceinline__ int64_t lb_u64(const unsigned long long* a, int64_t n, unsigned long long v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void vc_groups_kernel(const unsigned long long* __restrict__ skeys, const uint32_t* __restrict__ sids,
+                                 const unsigned long long* __restrict__ counters, int64_t nb,
+                                 ColGroup* __restrict__ grp) {
+    const int64_t n = vc_used(counters, nb);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = skeys[i];
+        const unsigned long long x = k >> 42, xy = k >> 21;
+        const int64_t s_x = lb_u64(skeys, n, x << 42), e_x = lb_u64(skeys, n, (x + 1) << 42);
+        const int64_t s_xy = lb_u64(skeys, n, xy << 21), e_xy = lb_u64(skeys, n, (xy + 1) << 21);
+        grp[sids[i]] = ColGroup{(int)s_x, (int)(e_x - s_x), (int)(s_xy - s_x), (int)(e_xy - s_xy), (int)(i - s_xy), 0};
+    }
+}
+
+__device__ __forceinline__ int64_t vc_col_pos(const ColGroup& g, int col) {
+    const int lx = col & 3, ly = col >> 2;
+    return (int64_t)g.start_x * 16 + (int64_t)lx * 4 * g.n_x + (int64_t)g.off_xy * 4 + (int64_t)ly * g.n_xy + g.r_z;
+}
+
+// column counts in key order (scan input) and the column behind each position
+__global__ void vc_colpos_kernel(const ColGroup* __restrict__ grp, const uint8_t* __restrict__ colcnt,
+                                 const unsigned long long* __restrict__ counters, int64_t nb,
+                                 uint32_t* __restrict__ scan_in, uint32_t* __restrict__ colsrc) {
+    const int64_t n16 = vc_used(counters, nb) * 16;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n16; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = vc_col_pos(grp[t >> 4], (int)(t & 15));
+        scan_in[p] = colcnt[t];
+        colsrc[p] = (uint32_t)t;
+    }
+}
+
+// one thread per column position, in key order: the column's occupied voxels
+// go to consecutive output rows (coalesced writes)
+__global__ void vc_gather_kernel(const float4* __restrict__ sums, const unsigned int* __restrict__ counts,
+                                 const unsigned long long* __restrict__ block_keys,
+                                 const unsigned long long* __restrict__ counters, int64_t nb,
+                                 const uint32_t* __restrict__ colsrc, const uint32_t* __restrict__ scan_in,
+                                 const uint32_t* __restrict__ col_base, int64_t max_voxels, double cell,
+                                 int64_t* __restrict__ okeys, float* __restrict__ cen, float* __restrict__ wsum,
+                                 int32_t* __restrict__ cnt, unsigned long long* __restrict__ ovf,
+                                 int64_t* __restrict__ n_out) {
+    const int64_t n16 = vc_used(counters, nb) * 16;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = min((int64_t)col_base[n16], max_voxels);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n16; p += (int64_t)gridDim.x * blockDim.x) {
+        if (!scan_in[p]) continue;
+        const uint32_t t = colsrc[p];
+        const int64_t b = t >> 4;
+        const int col = (int)(t & 15);
+        int64_t d = col_base[p];
+        long long bx, by, bz;
+        unpack_cells(block_keys[b], bx, by, bz);
+        const long long cx = bx * 4 + (col & 3), cy = by * 4 + (col >> 2);
+#pragma unroll
+        for (int lz = 0; lz < 4; ++lz) {
+            const int64_t v = b * kBlockVox + col + 16 * lz;
+            const unsigned c = counts[v];
+            if (!c) continue;
+            if (d >= max_voxels) { atomicAdd(ovf, 1ull); continue; }
+            const float4 s = sums[v];
+            const long long cz = bz * 4 + lz;
+            okeys[d] = (int64_t)pack_cells(cx, cy, cz);
+            const double w = s.w;
+            cen[3 * d + 0] = (float)((double)cx * cell + (double)s.x / w);
+            cen[3 * d + 1] = (float)((double)cy * cell + (double)s.y / w);
+            cen[3 * d + 2] = (float)((double)cz * cell + (double)s.z / w);
+            wsum[d] = s.w;
+            cnt[d] = (int32_t)c;
+            ++d;
+        }
+    }
+}
+
+struct ColWs {
+    uint8_t* colcnt;
+    unsigned long long *skey, *skey_s;
+    uint32_t *ids, *ids_s;
+    ColGroup* grp;
+    uint32_t *scan_in, *colsrc, *col_base;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+static size_t col_ws_layout(int64_t nb, char* base, ColWs* w) {
+    size_t cs = 0, cc = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cs, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nb, 0, 64);
+    cub::DeviceScan::ExclusiveSum(nullptr, cc, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(nb * 16 + 1));
+    Carver cv{base, 0};
+    ColWs t;
+    t.colcnt = cv.take<uint8_t>(nb * 16);
+    t.skey = cv.take<unsigned long long>(nb);
+    t.skey_s = cv.take<unsigned long long>(nb);
+    t.ids = cv.take<uint32_t>(nb);
+    t.ids_s = cv.take<uint32_t>(nb);
+    t.grp = cv.take<ColGroup>(nb);
+    t.scan_in = cv.take<uint32_t>(nb * 16 + 1);
+    t.colsrc = cv.take<uint32_t>(nb * 16);
+    t.col_base = cv.take<uint32_t>(nb * 16 + 1);
+    t.cub_bytes = std::max(cs, cc);
+    t.cub_tmp = cv.take<char>(t.cub_bytes);
+    if (w) *w = t;
+    return cv.used;
+}
+
+// No host round trip until the end (the caller needs U): every launch is
+// sized by the map's capacity and reads the used-block count on the device.
+static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum, int32_t* count, int64_t* n_out,
+                       void* workspace, size_t workspace_bytes, cudaStream_t st) {
+    const int64_t nb = h->max_blocks;
+    ColWs w;
+    if (col_ws_layout(nb, (char*)workspace, &w) > workspace_bytes) return EC3R_EWORKSPACE;
+    h->last_count = -1;
+    EC3R_CUDA_TRY(cudaMemsetAsync(w.scan_in, 0, sizeof(uint32_t) * (size_t)(nb * 16 + 1), st));
+    const unsigned gw = (unsigned)std::min<int64_t>((nb * 32 + 255) / 256, (int64_t)kNumSMs * 16);
+    vc_block_prep_kernel<<<gw, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, w.colcnt, w.skey, w.ids);
+    EC3R_CHECK_LAUNCH("vc_block_prep_kernel");
+    size_t cb = w.cub_bytes;
+    if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.skey, w.skey_s, w.ids, w.ids_s, (int)nb, 0, 64, st) !=
+        cudaSuccess) {
+        set_last_error("cub::DeviceRadixSort::SortPairs(blocks)", cudaGetLastError());
+        return EC3R_ECUDA;
+    }
+    count_launch();
+    const unsigned gt = (unsigned)std::min<int64_t>((nb + 255) / 256, (int64_t)kNumSMs * 8);
+    vc_groups_kernel<<<gt, 256, 0, st>>>(w.skey_s, w.ids_s, h->counters, nb, w.grp);
+    EC3R_CHECK_LAUNCH("vc_groups_kernel");
+    const unsigned gc = (unsigned)std::min<int64_t>((nb * 16 + 255) / 256, (int64_t)kNumSMs * 16);
+    vc_colpos_kernel<<<gc, 256, 0, st>>>(w.grp, w.colcnt, h->counters, nb, w.scan_in, w.colsrc);
+    EC3R_CHECK_LAUNCH("vc_colpos_kernel");
+    cb = w.cub_bytes;
+    if (cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.scan_in, w.col_base, (int)(nb * 16 + 1), st) != cudaSuccess) {
+        set_last_error("cub::DeviceScan::ExclusiveSum(columns)", cudaGetLastError());
+        return EC3R_ECUDA;
+    }
+    count_launch();
+    vc_gather_kernel<<<gc, 256, 0, st>>>(h->sums, h->counts, h->block_keys, h->counters, nb, w.colsrc, w.scan_in,
+                                         w.col_base, h->max_voxels, h->cell, keys, centroid, wsum, count,
+                                         h->counters + 5, n_out);
+    EC3R_CHECK_LAUNCH("vc_gather_kernel");
+    int64_t U = 0;
+    EC3R_CUDA_TRY(cudaMemcpyAsync(&U, n_out, sizeof(U), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    h->last_count = U;
+    return EC3R_OK;
+}
+
 }  // namespace ec3r
 
 using namespace ec3r;
@@ -1109,8 +1312,10 @@ extern "C" size_t ec3r_vhash_extract_workspace(const ec3r_vhash* h) {
                                                         (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cap, 0, 32);
     if (cub32 > cub_bytes) cub_bytes = cub32;
     const int64_t nb = h->max_blocks;
-    return 4 * align256(sizeof(int64_t) * cap) + align256(64) + 2 * align256(sizeof(int) * (size_t)(nb + 1)) +
-           align256(scan_temp_bytes(nb + 1)) + align256(cub_bytes);
+    const size_t legacy = 4 * align256(sizeof(int64_t) * cap) + align256(64) +
+                          2 * align256(sizeof(int) * (size_t)(nb + 1)) + align256(scan_temp_bytes(nb + 1)) +
+                          align256(cub_bytes);
+    return std::max(legacy, col_ws_layout(nb, nullptr, nullptr));
 }
 
 extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum, int32_t* count,
@@ -1124,6 +1329,8 @@ extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid,
         return rc;
     }
     if (!workspace || workspace_bytes < ec3r_vhash_extract_workspace(h)) return EC3R_EWORKSPACE;
+    if (sort && !getenv("EC3R_EMIT_VOXEL_SORT")) return column_emit(h, keys, centroid, wsum, count, n_out, workspace,
+                                                                   workspace_bytes, st);
     const unsigned long long* ks;
     const int64_t* is;
     const uint32_t* i32;
