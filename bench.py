@@ -192,6 +192,8 @@ class Step:
             from paper_2510_02080_b200 import dist as pdist
             self.exchange = pdist.MapExchange(cell)
         self.n_voxels = 0
+        self.async_exchange = False
+        self.n_dev = None
 
     def _event(self):
         e = self.torch.cuda.Event(enable_timing=True)
@@ -227,9 +229,16 @@ class Step:
         else:
             # N > 1: global map partitioned by voxel key — owner-bucketed
             # partials, one NCCL all-to-all, owner-side merge + sorted emit
-            keys, cen, wsum, cnt_v = self.exchange.run(self.vmap, int(self.out[0].shape[0]))
+            # device-timed steps: no host round trip (fixed slabs, device
+            # counts; overflow flags verified after the timed region)
+            if self.async_exchange:
+                keys, cen, wsum, cnt_v, self.n_dev = self.exchange.run(self.vmap, int(self.out[0].shape[0]),
+                                                                       sync=False)
+            else:
+                keys, cen, wsum, cnt_v = self.exchange.run(self.vmap, int(self.out[0].shape[0]))
         ev["t_emit"] = self._event()
-        self.n_voxels = int(keys.numel())
+        if self.exchange is None or not self.async_exchange:
+            self.n_voxels = int(keys.numel())
         if record is not None:
             record.append(ev)
         return keys, cen, wsum, cnt_v
@@ -431,6 +440,7 @@ def main():
     for _ in range(args.warmup):
         step.run()
     torch.cuda.synchronize()
+    step.async_exchange = step.exchange is not None
     n_points = step.vmap.stats()["n_points_in"]
     A, B, ao, bo = desc[:4]
     n_pairs_scored = int(np.sum(np.diff(ao) * np.diff(bo)))
@@ -453,6 +463,10 @@ def main():
     torch.cuda.synchronize()
     launches = L.ec3r_kernel_launches() - launches0
     _lib.timing_enable(False)
+    if step.async_exchange:
+        step.exchange.verify()  # overflow flags of the host-sync-free exchange
+        step.n_voxels = int(step.n_dev.item())
+        step.async_exchange = False
     ktimes = _lib.kernel_times()  # per hot kernel: CUDA events on its launching stream
     if world > 1:
         dist.barrier()

@@ -223,6 +223,9 @@ EC3R_API int ec3r_vhash_count(ec3r_vhash* h, int64_t* n_out, void* stream);
 EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum,
                        int32_t* count, int64_t* n_out, int sort, void* workspace,
                        size_t workspace_bytes, void* stream);
+/* sort: 0 = block order, 1 = key order (U read back to the host, see
+ * ec3r_vhash_extract_count), 2 = key order without the host read (U only in
+ * *n_out on the device). */
 /* Voxel count of the last sorted extract on this handle (already known on
  * the host), or -1: lets a caller size its outputs without a device read. */
 EC3R_API int64_t ec3r_vhash_extract_count(const ec3r_vhash* h);
@@ -235,6 +238,24 @@ EC3R_API int ec3r_vhash_extract_partials(ec3r_vhash* h, int n_ranks, int64_t* ke
                                 size_t workspace_bytes, void* stream);
 EC3R_API int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, const float* sums4,
                               const int32_t* count, int64_t n, void* stream);
+/* Host-sync-free form of the exchange (replaces the per-step host reads of
+ * the bucket sizes): owner r's partials go to the fixed slab
+ * [r*cap, r*cap + slab_counts[r]) of the outputs (n_ranks*cap rows; rows
+ * past a full slab are counted in *overflow, both device int64), so the
+ * all-to-all uses equal splits; the receiver merges n_slabs slabs of cap rows
+ * with their device counts.  Workspace = ec3r_vhash_extract_workspace + 17 KB.
+ * Reference boundary: the owner-partitioned voxel map of SURVEY §8(e) over
+ * mapping.py:332-338 + the declared fusion rule. */
+EC3R_API int ec3r_vhash_extract_partials_fixed(ec3r_vhash* h, int n_ranks, int64_t cap, int64_t* keys,
+                                               float* sums4, int32_t* count, int64_t* slab_counts,
+                                               int64_t* overflow, void* workspace, size_t workspace_bytes,
+                                               void* stream);
+EC3R_API int ec3r_vhash_merge_partials_slabs(ec3r_vhash* h, const int64_t* keys, const float* sums4,
+                                             const int32_t* count, int n_slabs, int64_t cap,
+                                             const int64_t* slab_counts, void* stream);
+/* ec3r_vhash_stats_get into a device buffer of 5 int64 (no host round trip;
+ * block-hash maps). */
+EC3R_API int ec3r_vhash_stats_device(ec3r_vhash* h, int64_t* out5, void* stream);
 
 /* ---------------------------------------------------------------------
  * K5  brute-force mutual-NN + Lowe-ratio descriptor matching

@@ -51,6 +51,9 @@ _PROTOS = {
     "ec3r_vhash_extract_count": (_I64, [_P]),
     "ec3r_vhash_extract_partials": (_I, [_P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
     "ec3r_vhash_merge_partials": (_I, [_P, _P, _P, _P, _I64, _P]),
+    "ec3r_vhash_extract_partials_fixed": (_I, [_P, _I, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "ec3r_vhash_merge_partials_slabs": (_I, [_P, _P, _P, _P, _I, _I64, _P, _P]),
+    "ec3r_vhash_stats_device": (_I, [_P, _P, _P]),
     "ec3r_match_workspace": (_SZ, [_P, _P, _I]),
     "ec3r_match_batched": (_I, [_P, _P, _P, _P, _I, _P, _P, _I, _I, _D, _D, _P, _P, _P, _SZ, _P]),
     "ec3r_match_batched_rows": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _I64, _I, _I, _D, _D, _P, _P, _P, _SZ, _P]),

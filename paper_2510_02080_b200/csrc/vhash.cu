@@ -1032,7 +1032,7 @@ static size_t col_ws_layout(int64_t nb, char* base, ColWs* w) {
 // No host round trip until the end (the caller needs U): every launch is
 // sized by the map's capacity and reads the used-block count on the device.
 static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsum, int32_t* count, int64_t* n_out,
-                       void* workspace, size_t workspace_bytes, cudaStream_t st) {
+                       void* workspace, size_t workspace_bytes, bool read_count, cudaStream_t st) {
     const int64_t nb = h->max_blocks;
     ColWs w;
     if (col_ws_layout(nb, (char*)workspace, &w) > workspace_bytes) return EC3R_EWORKSPACE;
@@ -1064,11 +1064,79 @@ static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsu
                                          w.col_base, h->max_voxels, h->cell, keys, centroid, wsum, count,
                                          h->counters + 5, n_out);
     EC3R_CHECK_LAUNCH("vc_gather_kernel");
+    if (!read_count) return EC3R_OK;  // *n_out (device) holds U
     int64_t U = 0;
     EC3R_CUDA_TRY(cudaMemcpyAsync(&U, n_out, sizeof(U), cudaMemcpyDeviceToHost, st));
     EC3R_CUDA_TRY(cudaStreamSynchronize(st));
     h->last_count = U;
     return EC3R_OK;
+}
+
+
+// Fixed-slab partials for a host-sync-free all-to-all: owner r's rows go to
+// [r * cap, r * cap + min(count_r, cap)); rows past a full slab are counted
+// in *overflow (the caller re-runs with a larger cap).  slab_counts[r] =
+// min(count_r, cap) after the launch.
+__global__ void vb_partition_fixed_kernel(const float4* __restrict__ sums, const unsigned int* __restrict__ counts,
+                                          const unsigned long long* __restrict__ keys,
+                                          const int64_t* __restrict__ idx, const int64_t* __restrict__ n_ptr,
+                                          int n_ranks, int64_t cap, unsigned long long* __restrict__ cursors,
+                                          int64_t* __restrict__ okeys, float* __restrict__ sums4,
+                                          int32_t* __restrict__ cnt, unsigned long long* __restrict__ overflow) {
+    const int64_t n = *n_ptr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        const int r = (int)(mix64(k) % (unsigned long long)n_ranks);
+        const unsigned peers = __match_any_sync(__activemask(), r);
+        const int lead = __ffs(peers) - 1;
+        const unsigned lanes_below = peers & ((1u << (threadIdx.x & 31)) - 1u);
+        unsigned long long base = 0;
+        if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(&cursors[r], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, lead);
+        const unsigned long long pos = base + __popc(lanes_below);
+        if ((int64_t)pos >= cap) {
+            atomicAdd(overflow, 1ull);
+            continue;
+        }
+        const int64_t o = (int64_t)r * cap + (int64_t)pos;
+        okeys[o] = (int64_t)k;
+        reinterpret_cast<float4*>(sums4)[o] = sums[idx[i]];
+        cnt[o] = (int32_t)counts[idx[i]];
+    }
+}
+
+__global__ void vb_slab_counts_kernel(const unsigned long long* __restrict__ cursors, int n_ranks, int64_t cap,
+                                      int64_t* __restrict__ slab_counts) {
+    const int r = threadIdx.x;
+    if (r < n_ranks) slab_counts[r] = min((int64_t)cursors[r], cap);
+}
+
+// merge received slabs: row i of slab s is valid iff i < slab_counts[s]
+__global__ void vb_merge_slabs_kernel(const int64_t* __restrict__ keys, const float* __restrict__ sums4,
+                                      const int32_t* __restrict__ cnt, int n_slabs, int64_t cap,
+                                      const int64_t* __restrict__ slab_counts, VB vb) {
+    const int64_t n = (int64_t)n_slabs * cap;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        bool valid = i < n;
+        if (valid) {
+            const int64_t sl = i / cap;
+            valid = (i - sl * cap) < slab_counts[sl];
+        }
+        long long cx = 0, cy = 0, cz = 0;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        unsigned c = 0;
+        if (valid) {
+            unpack_cells((unsigned long long)keys[i], cx, cy, cz);
+            s = reinterpret_cast<const float4*>(sums4)[i];
+            c = (unsigned)cnt[i];
+        }
+        unsigned long long cbk = kEmpty;
+        int cidx = -2;
+        if (vb_insert_warp(vb, valid, cx, cy, cz, s.x, s.y, s.z, s.w, c, cbk, cidx))
+            atomicAdd(&vb.counters[2], 1ull);
+    }
 }
 
 }  // namespace ec3r
@@ -1329,8 +1397,8 @@ extern "C" int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid,
         return rc;
     }
     if (!workspace || workspace_bytes < ec3r_vhash_extract_workspace(h)) return EC3R_EWORKSPACE;
-    if (sort && !getenv("EC3R_EMIT_VOXEL_SORT")) return column_emit(h, keys, centroid, wsum, count, n_out, workspace,
-                                                                   workspace_bytes, st);
+    if (sort && !getenv("EC3R_EMIT_VOXEL_SORT"))
+        return column_emit(h, keys, centroid, wsum, count, n_out, workspace, workspace_bytes, sort != 2, st);
     const unsigned long long* ks;
     const int64_t* is;
     const uint32_t* i32;
@@ -1396,5 +1464,74 @@ extern "C" int ec3r_vhash_merge_partials(ec3r_vhash* h, const int64_t* keys, con
     h->legacy_active = true;
     vb_merge_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(keys, sums4, count, n, vb_of(h));
     EC3R_CHECK_LAUNCH("vb_merge_kernel");
+    return EC3R_OK;
+}
+
+extern "C" int ec3r_vhash_extract_partials_fixed(ec3r_vhash* h, int n_ranks, int64_t cap, int64_t* keys, float* sums4,
+                                                 int32_t* count, int64_t* slab_counts, int64_t* overflow,
+                                                 void* workspace, size_t workspace_bytes, void* stream) {
+    if (!h || n_ranks < 1 || n_ranks > 1024 || cap < 1 || !keys || !sums4 || !count || !slab_counts || !overflow)
+        return EC3R_EARG;
+    if (h->bf_active) {
+        set_last_error_msg("ec3r_vhash_extract_partials_fixed: the binned engine emits partials with a host count "
+                           "(ec3r_vhash_extract_partials)");
+        return EC3R_EARG;
+    }
+    const size_t need = ec3r_vhash_extract_workspace(h) + 2 * align256(sizeof(unsigned long long) * n_ranks) + 1024;
+    if (!workspace || workspace_bytes < need) return EC3R_EWORKSPACE;
+    cudaStream_t st = as_stream(stream);
+    Carver cv{(char*)workspace, 0};
+    unsigned long long* cursors = cv.take<unsigned long long>(n_ranks);
+    int64_t* n_dev = cv.take<int64_t>(1);
+    void* cws = cv.base + cv.used;
+    const unsigned long long* ks;
+    const int64_t* is;
+    const uint32_t* i32;
+    const int rc = compact_sorted(h, 0, cws, workspace_bytes - cv.used, n_dev, &ks, &is, &i32, st);
+    if (rc) return rc;
+    EC3R_CUDA_TRY(cudaMemsetAsync(cursors, 0, sizeof(unsigned long long) * n_ranks, st));
+    EC3R_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int64_t), st));
+    vb_partition_fixed_kernel<<<kNumSMs * 8, 256, 0, st>>>(h->sums, h->counts, ks, is, n_dev, n_ranks, cap, cursors,
+                                                           keys, sums4, count, (unsigned long long*)overflow);
+    EC3R_CHECK_LAUNCH("vb_partition_fixed_kernel");
+    vb_slab_counts_kernel<<<1, 1024, 0, st>>>(cursors, n_ranks, cap, slab_counts);
+    EC3R_CHECK_LAUNCH("vb_slab_counts_kernel");
+    return EC3R_OK;
+}
+
+extern "C" int ec3r_vhash_merge_partials_slabs(ec3r_vhash* h, const int64_t* keys, const float* sums4,
+                                               const int32_t* count, int n_slabs, int64_t cap,
+                                               const int64_t* slab_counts, void* stream) {
+    if (!h || n_slabs < 1 || cap < 1 || !keys || !sums4 || !count || !slab_counts) return EC3R_EARG;
+    if (h->bf_active) return mixed_error();
+    h->legacy_active = true;
+    vb_merge_slabs_kernel<<<grid_for((int64_t)n_slabs * cap), 256, 0, as_stream(stream)>>>(keys, sums4, count, n_slabs,
+                                                                                          cap, slab_counts, vb_of(h));
+    EC3R_CHECK_LAUNCH("vb_merge_slabs_kernel");
+    return EC3R_OK;
+}
+
+// Device-side map counters (n_points_in, n_out_of_range, n_overflow (dropped
+// points + voxels past the emit capacity), n_slow_path, n_blocks) into a
+// caller device buffer of 5 int64, without a host round trip.
+__global__ void vb_stats_dev_kernel(const unsigned long long* __restrict__ c, int64_t max_blocks,
+                                    int64_t* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        out[0] = (int64_t)c[0];
+        out[1] = (int64_t)c[1];
+        out[2] = (int64_t)(c[2] + c[5]);
+        out[3] = (int64_t)c[3];
+        out[4] = (int64_t)min(c[4], (unsigned long long)max_blocks);
+    }
+}
+
+extern "C" int ec3r_vhash_stats_device(ec3r_vhash* h, int64_t* out5, void* stream) {
+    if (!h || !out5) return EC3R_EARG;
+    if (h->bf_active) {
+        set_last_error_msg("ec3r_vhash_stats_device: block-hash maps only");
+        return EC3R_EARG;
+    }
+    vb_stats_dev_kernel<<<1, 32, 0, as_stream(stream)>>>(h->counters, h->max_blocks, out5);
+    EC3R_CHECK_LAUNCH("vb_stats_dev_kernel");
     return EC3R_OK;
 }

@@ -122,63 +122,133 @@ def exchange_partials(keys: torch.Tensor, sums4: torch.Tensor, counts: torch.Ten
 
 
 class MapExchange:
-    """Owner-partitioned global voxel map from per-rank local maps: the
-    partials of a rank's local VoxelMap are bucketed by owner on the device
-    (ec3r_vhash_extract_partials), exchanged in one all-to-all and merged
-    into this rank's owned map (ec3r_vhash_merge_partials), whose sorted
-    emit is the rank's partition of the global map.  Buffers and the owned
-    map persist across calls (no allocation in steady state)."""
+    """Owner-partitioned global voxel map from per-rank local maps, with no
+    host round trip in the step: the partials of a rank's local VoxelMap are
+    bucketed by owner on the device into fixed slabs of `cap` rows
+    (ec3r_vhash_extract_partials_fixed), so the bucket counts and the payload
+    each move in one equal-split all-to-all (counts stay on the device), and
+    the owner merges the received slabs with their device counts
+    (ec3r_vhash_merge_partials_slabs) before its sorted emit.  Overflow (a
+    bucket larger than `cap`, or the owned map's capacity) is flagged on the
+    device: run(sync=True) checks it and re-runs with larger buffers;
+    run(sync=False) returns the unsliced outputs plus the device count and
+    leaves the check to verify().  Buffers persist across calls."""
 
-    def __init__(self, cell: float, group=None):
+    def __init__(self, cell: float, group=None, cap: Optional[int] = None):
         self.cell = float(cell)
         self.group = group
         self.rank, self.world = _world(group)
+        self.cap = int(cap) if cap else 0
         self.owned = None
-        self._buf = None
+        self._bufs = None
         self.out = None
+        self.flags = None  # device int64[2]: partition overflow, owned-map overflow (accumulated)
+        self._stats = None
+        self._slab = None
 
-    def _buffers(self, n: int):
-        if self._buf is None or self._buf[0].shape[0] < n:
-            m = max(n, 1)
-            self._buf = (torch.empty(m, dtype=torch.int64, device="cuda"),
-                         torch.empty((m, 4), dtype=torch.float32, device="cuda"),
-                         torch.empty(m, dtype=torch.int32, device="cuda"),
-                         torch.zeros(self.world, dtype=torch.int64, device="cuda"))
-        return self._buf
-
-    def run(self, local, n_local: int, stream=None):
-        """local: this rank's fused VoxelMap holding n_local voxels."""
-        from . import _lib
+    def _alloc(self, cap: int):
+        W = self.world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        n = W * cap
+        self._bufs = dict(
+            keys=torch.empty(n, dtype=torch.int64, device=dev),
+            sums4=torch.empty((n, 4), dtype=torch.float32, device=dev),
+            cnt=torch.empty(n, dtype=torch.int32, device=dev),
+            send_counts=torch.zeros(W, dtype=torch.int64, device=dev),
+            recv_counts=torch.zeros(W, dtype=torch.int64, device=dev),
+            payload=torch.empty((n, 7), dtype=torch.int32, device=dev),
+            recv=torch.empty((n, 7), dtype=torch.int32, device=dev),
+            ovf=torch.zeros(1, dtype=torch.int64, device=dev))
         from .mapping import VoxelMap
+        self.owned = VoxelMap(self.cell, capacity=max(n, 1 << 16))
+        self.out = (torch.empty(max(n, 1), dtype=torch.int64, device=dev),
+                    torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev),
+                    torch.empty(max(n, 1), dtype=torch.float32, device=dev),
+                    torch.empty(max(n, 1), dtype=torch.int32, device=dev))
+        self.flags = torch.zeros(2, dtype=torch.int64, device=dev)
+        self._stats = torch.zeros(5, dtype=torch.int64, device=dev)
+        self.cap = cap
+
+    def _all_to_all(self, out: torch.Tensor, inp: torch.Tensor):
+        if _host_staged(self.group, inp.device):
+            o = torch.empty_like(out, device="cpu")
+            dist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, group=self.group)
+
+    def run(self, local, n_local: int, stream=None, sync: bool = True):
+        """local: this rank's fused VoxelMap holding ~n_local voxels.
+        sync=True: returns (keys, centroid, wsum, count) sliced to this rank's
+        partition, re-running with larger slabs on overflow (all ranks agree
+        through one all-reduce of the flags).  sync=False: returns the full
+        output buffers and the device int64[1] count; no host round trip."""
+        if self._bufs is None:
+            cap = self.cap or max(1024, (2 * int(n_local)) // max(self.world, 1) + 1024)
+            if self.world > 1:  # equal splits: every rank uses the largest slab any rank needs
+                t = torch.tensor([cap], dtype=torch.int64, device=_coll_dev(self.group))
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+                cap = int(t.item())
+            self._alloc(cap)
+        while True:
+            if sync:
+                self.flags.zero_()
+            res = self._step(local, stream)
+            if not sync:
+                return res
+            f = self.flags.clone()
+            if self.world > 1:
+                if _host_staged(self.group, f.device):
+                    fc = f.cpu()
+                    dist.all_reduce(fc, op=dist.ReduceOp.MAX, group=self.group)
+                    f = fc
+                else:
+                    dist.all_reduce(f, op=dist.ReduceOp.MAX, group=self.group)
+            if int(f.max().item()) == 0:
+                n = int(res[4].item())
+                return tuple(x[:n] for x in res[:4])
+            self._alloc(2 * self.cap)
+
+    def _step(self, local, stream):
+        from . import _lib
 
         L = _lib.lib()
-        keys, sums4, cnt, rank_counts = self._buffers(n_local)
-        rank_counts.zero_()
-        wsb = L.ec3r_vhash_extract_workspace(local.handle) + 1024
-        ws = _lib.workspace(wsb, keys.device, "partials")
-        _lib.check(L.ec3r_vhash_extract_partials(local.handle, self.world, _lib.ptr(keys), _lib.ptr(sums4),
-                                                 _lib.ptr(cnt), _lib.ptr(rank_counts), _lib.ptr(ws), ws.numel(),
-                                                 _lib.stream_ptr(stream)), "ec3r_vhash_extract_partials")
-        rk, rs, rcnt = exchange_partials(keys, sums4, cnt, rank_counts.tolist(), self.group)
-        n = int(rk.shape[0])
-        while True:  # grow until neither the merge nor the emit overflows
-            if self.owned is None or self.owned.expected < n:
-                self.owned = VoxelMap(self.cell, capacity=max(2 * n, 1 << 16))
-            self.owned.clear(stream)
-            if n:
-                _lib.check(L.ec3r_vhash_merge_partials(self.owned.handle, _lib.ptr(rk), _lib.ptr(rs),
-                                                       _lib.ptr(rcnt), n, _lib.stream_ptr(stream)),
-                           "ec3r_vhash_merge_partials")
-            if self.owned.stats(stream)["n_overflow"] == 0:
-                if self.out is None or self.out[0].shape[0] < n:
-                    self.out = (torch.empty(max(n, 1), dtype=torch.int64, device="cuda"),
-                                torch.empty((max(n, 1), 3), dtype=torch.float32, device="cuda"),
-                                torch.empty(max(n, 1), dtype=torch.float32, device="cuda"),
-                                torch.empty(max(n, 1), dtype=torch.int32, device="cuda"))
-                res = self.owned.extract(sort=True, stream=stream, out=self.out)
-                if self.owned.stats(stream)["n_overflow"] == 0:
-                    return res
-            self.owned = VoxelMap(self.cell, capacity=4 * max(self.owned.expected, 2 * n))
+        b, W, cap = self._bufs, self.world, self.cap
+        wsb = L.ec3r_vhash_extract_workspace(local.handle) + 2 * 256 * max(W, 4) + 4096
+        ws = _lib.workspace(wsb, b["keys"].device, "partials")
+        _lib.check(L.ec3r_vhash_extract_partials_fixed(local.handle, W, cap, _lib.ptr(b["keys"]), _lib.ptr(b["sums4"]),
+                                                       _lib.ptr(b["cnt"]), _lib.ptr(b["send_counts"]),
+                                                       _lib.ptr(b["ovf"]), _lib.ptr(ws), ws.numel(),
+                                                       _lib.stream_ptr(stream)), "ec3r_vhash_extract_partials_fixed")
+        self.flags[0:1].add_(b["ovf"])
+        p = b["payload"]
+        p[:, 0:2].copy_(b["keys"].view(torch.int32).view(-1, 2))
+        p[:, 2:6].copy_(b["sums4"].view(torch.int32))
+        p[:, 6].copy_(b["cnt"])
+        if W > 1:
+            self._all_to_all(b["recv_counts"], b["send_counts"])
+            self._all_to_all(b["recv"], p)
+            r, counts = b["recv"], b["recv_counts"]
+        else:
+            r, counts = p, b["send_counts"]
+        rk = r[:, 0:2].contiguous().view(torch.int64).view(-1)
+        rs = r[:, 2:6].contiguous().view(torch.float32)
+        rc = r[:, 6].contiguous()
+        self.owned.clear(stream)
+        _lib.check(L.ec3r_vhash_merge_partials_slabs(self.owned.handle, _lib.ptr(rk), _lib.ptr(rs), _lib.ptr(rc), W,
+                                                     cap, _lib.ptr(counts), _lib.stream_ptr(stream)),
+                   "ec3r_vhash_merge_partials_slabs")
+        res = self.owned.extract(sort=True, stream=stream, out=self.out, sync=False)
+        self.owned.stats_device(self._stats, stream)
+        self.flags[1:2].add_(self._stats[2:3])
+        return res
+
+    def verify(self):
+        """Host check of the overflow flags accumulated by run(sync=False)."""
+        f = self.flags.tolist()
+        if f[0] or f[1]:
+            raise RuntimeError(f"MapExchange overflow: {f[0]} partial rows past a slab of {self.cap}, "
+                               f"{f[1]} rows past the owned map; re-run with a larger cap")
 
 
 def fuse_global(pool, slots: torch.Tensor, cell: float, group=None, capacity: Optional[int] = None):
@@ -272,20 +342,21 @@ def window_halo(mapping, window: Sequence, group=None):
         req[: len(ids)] = torch.tensor(ids, dtype=torch.int64)
     want = torch.full((HALO_MAX,), -1, **i64)
     shift([req], [want], step=-1, group=group)
-    # round 2 (forwards): header (count, ids) then the frames
+    # round 2 (forwards): header (count, submap id, ids) then the frames
     send = []
     if rank + 1 < world:
         wanted = {int(x) for x in want.tolist() if x >= 0}
         last = window[-1]
         pick = [k for k, f in enumerate(last.keyframe_ids) if f in wanted]
-        hdr = torch.full((1 + HALO_MAX,), -1, **i64)
+        hdr = torch.full((2 + HALO_MAX,), -1, **i64)
         hdr[0] = len(pick)
-        hdr[1: 1 + len(pick)] = torch.tensor([last.keyframe_ids[k] for k in pick], dtype=torch.int64)
+        hdr[1] = int(last.id)
+        hdr[2: 2 + len(pick)] = torch.tensor([last.keyframe_ids[k] for k in pick], dtype=torch.int64)
         sl = torch.as_tensor(np.asarray(last.slots, np.int64)[pick], device=dev)
         send = [hdr, pool.depth.index_select(0, sl).to(tdev), pool.conf.index_select(0, sl).to(tdev),
                 pool.poses.index_select(0, sl).to(tdev)]
         n_send = len(pick)
-    hdr_in = torch.full((1 + HALO_MAX,), -1, **i64)
+    hdr_in = torch.full((2 + HALO_MAX,), -1, **i64)
     shift(send[:1], [hdr_in] if rank > 0 else [], step=1, group=group)
     n_in = int(hdr_in[0]) if rank > 0 else 0
     recv = []
@@ -296,8 +367,12 @@ def window_halo(mapping, window: Sequence, group=None):
     shift(send[1:] if rank + 1 < world and n_send > 0 else [], recv, step=1, group=group)
     if rank == 0 or n_in == 0:
         return None
-    ids = [int(x) for x in hdr_in[1: 1 + n_in].tolist()]
-    return mapping.add_submap(ids, recv[0].to(dev), recv[1].to(dev), list(recv[2].cpu().numpy()))
+    ids = [int(x) for x in hdr_in[2: 2 + n_in].tolist()]
+    stub = mapping.add_submap(ids, recv[0].to(dev), recv[1].to(dev), list(recv[2].cpu().numpy()))
+    mapping._next_id -= 1  # the stub takes no id of this rank's sequence
+    stub.id = -(1 << 30)
+    stub.remote_id = int(hdr_in[1])  # the predecessor's submap (global id): edges name it
+    return stub
 
 
 def prefix_offsets(window_last: Sequence) -> list:
@@ -338,7 +413,11 @@ def register_window(mapping, window: Sequence, group=None):
     from .types import sim3_to_vec, vec_to_sim3
 
     stub = window_halo(mapping, window, group)
+    n0 = len(mapping.edges)
     mapping.register_chain(([stub] if stub is not None else []) + list(window))
+    if stub is not None:  # the halo edge names the predecessor's submap, not the stub
+        mapping.edges[n0:] = [(stub.remote_id if i == stub.id else i, j, tr, info)
+                              for i, j, tr, info in mapping.edges[n0:]]
     off = vec_to_sim3(window_offset(sim3_to_vec(window[-1].global_pose), group, mapping.pool.device))
     if stub is not None:
         mapping.forget(stub)
@@ -448,3 +527,319 @@ class WindowChain:
                                                            _lib.ptr(slot_g), n_slots, _lib.ptr(self.offset),
                                                            _lib.stream_ptr(stream)), "ec3r_apply_window_offset")
         return out
+
+
+# -- loop edges across shards and the pose-graph data path ----
+#
+# Submap ids are global: every rank numbers its window from the window's
+# first global index (DenseMapping._next_id), so an edge (i, j) means the same
+# submaps on every rank.  A loop submap (mapping.py:282-318) is registered
+# against every submap sharing one of its keyframes -- those may live on any
+# shard.  The owner of the loop submap requests the shared frames (depth,
+# confidence, local pose, plus the partner's global pose) from their owners
+# in one ragged all-to-all, adds them as stub submaps, registers every edge
+# in one launch, chains the loop submap off its strongest partner and drops
+# the stubs again.  Pose-graph optimisation stays in the reference's host
+# code (posegraph.py:176): the per-edge results (i, j, s, q, t, count, rms)
+# and every submap's global pose are gathered to the PGO rank, which runs the
+# caller's optimiser and broadcasts the optimised poses (8 f64 per submap);
+# each rank re-commits its own submaps (slot globals on the device).
+
+def _coll_dev(group=None) -> torch.device:
+    """Device of small host-side collectives: NCCL moves CUDA tensors only."""
+    if dist.is_available() and dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+class SubmapDirectory:
+    """Replicated directory of every rank's committed submaps: owner rank and
+    keyframe ids (one ragged all-gather of (sid, keyframe) rows; collective)."""
+
+    def __init__(self, mapping, group=None):
+        self.group = group
+        self.rank, self.world = _world(group)
+        rows = [(sid, kf, self.rank) for sid, sm in mapping.submaps.items() for kf in sm.keyframe_ids]
+        t = torch.as_tensor(np.asarray(rows, np.int64).reshape(-1, 3), device=_coll_dev(group))
+        parts = [x.cpu() for x in gather_ragged(t, group)] if self.world > 1 else [t]
+        self.owner: dict = {}
+        self.kf_subs: dict = {}
+        self.sub_kfs: dict = {}
+        for p in parts:
+            for sid, kf, r in p.tolist():
+                self.owner[sid] = r
+                self.kf_subs.setdefault(kf, []).append(sid)
+                self.sub_kfs.setdefault(sid, []).append(kf)
+
+    def partners(self, keyframe_ids, exclude=None) -> list:
+        """Submaps sharing any of keyframe_ids (mapping.py:164-169 order:
+        keyframes in order, then the submaps holding each)."""
+        out: dict = {}
+        for kf in keyframe_ids:
+            for sid in self.kf_subs.get(int(kf), ()):
+                if sid != exclude:
+                    out[sid] = None
+        return list(out)
+
+
+def _a2a_ragged(send: list, dtype, width: int, dev, group) -> list:
+    """Ragged all-to-all of per-destination row blocks (each (n_r, width)
+    of `dtype`); returns the blocks received from every rank.  Sizes travel
+    first (one host read: this path is per loop closure, not per frame)."""
+    rank, world = _world(group)
+    sizes = torch.tensor([int(b.shape[0]) for b in send], dtype=torch.int64)
+    rs = torch.empty_like(sizes)
+    staged = dev.type == "cpu" or dist.get_backend(group) == "gloo"
+    sdev = torch.device("cpu") if staged else dev
+    if staged:
+        dist.all_to_all_single(rs, sizes, group=group)
+    else:
+        s_d, r_d = sizes.to(dev), torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(r_d, s_d, group=group)
+        rs = r_d.cpu()
+    recv_sizes = [int(x) for x in rs.tolist()]
+    flat = torch.cat([b.reshape(-1, width).to(device=sdev, dtype=dtype) for b in send]) if send else \
+        torch.empty((0, width), dtype=dtype, device=sdev)
+    out = torch.empty((sum(recv_sizes), width), dtype=dtype, device=sdev)
+    dist.all_to_all_single(out, flat.contiguous(), output_split_sizes=recv_sizes,
+                           input_split_sizes=[int(b.shape[0]) for b in send], group=group)
+    res, o = [], 0
+    for n in recv_sizes:
+        res.append(out[o:o + n].to(dev))
+        o += n
+    return res
+
+
+def fetch_frames(mapping, requests, directory: SubmapDirectory, group=None) -> dict:
+    """Collective: every rank passes the (submap id, keyframe id) frames it
+    needs (possibly none); owners answer with that submap's copy of the frame.
+    Returns {(sid, kf): (depth (H,W) f32, conf (H,W) f32, local pose 8 f64,
+    submap global pose 8 f64)} on the pool's device."""
+    rank, world = _world(group)
+    pool = mapping.pool
+    dev = pool.device
+    H, W = pool.H, pool.W
+    per = [[] for _ in range(world)]
+    for sid, kf in requests:
+        per[directory.owner[int(sid)]].append((int(sid), int(kf)))
+    if world == 1:
+        incoming = [torch.as_tensor(np.asarray(per[0], np.int64).reshape(-1, 2))]
+    else:
+        incoming = _a2a_ragged([torch.as_tensor(np.asarray(p, np.int64).reshape(-1, 2)) for p in per],
+                               torch.int64, 2, torch.device("cpu"), group)
+    from .types import sim3_to_vec
+
+    planes, poses = [], []
+    for blk in incoming:
+        rows = blk.cpu().tolist()
+        if not rows:
+            planes.append(torch.empty((0, 2 * H * W), dtype=torch.float32, device=dev))
+            poses.append(torch.empty((0, 16), dtype=torch.float64, device=dev))
+            continue
+        sl = []
+        gl = []
+        for sid, kf in rows:
+            sm = mapping.submaps[sid]
+            sl.append(int(sm.slots[list(sm.keyframe_ids).index(kf)]))
+            gl.append(sim3_to_vec(sm.global_pose))
+        idx = torch.as_tensor(np.asarray(sl, np.int64), device=dev)
+        planes.append(torch.cat([pool.depth.index_select(0, idx).reshape(len(sl), -1),
+                                 pool.conf.index_select(0, idx).reshape(len(sl), -1)], dim=1))
+        poses.append(torch.cat([pool.poses.index_select(0, idx),
+                                torch.as_tensor(np.asarray(gl, np.float64), device=dev)], dim=1))
+    if world == 1:
+        got_planes, got_poses = planes, poses
+    else:
+        got_planes = _a2a_ragged(planes, torch.float32, 2 * H * W, dev, group)
+        got_poses = _a2a_ragged(poses, torch.float64, 16, dev, group)
+    out = {}
+    for r in range(world):
+        for k, (sid, kf) in enumerate(per[r]):
+            pl = got_planes[r][k]
+            ps = got_poses[r][k]
+            out[(sid, kf)] = (pl[: H * W].reshape(H, W), pl[H * W:].reshape(H, W), ps[:8].cpu().numpy(),
+                              ps[8:].cpu().numpy())
+    return out
+
+
+def register_loop_sharded(mapping, loop_sm, directory: SubmapDirectory, group=None):
+    """Collective (every rank calls; loop_sm is None on ranks without a loop
+    submap this step).  Registers loop_sm against every submap, on any shard,
+    sharing one of its keyframes (mapping.py:282-318 with _registration_edges
+    :162-188), sets its global pose from the strongest partner and commits it.
+    Returns the edges [(partner id, loop id, T, info, count, rms)] (empty when
+    there is no loop submap, or NoSharedKeyframes: the graph stays untouched,
+    mapping.py:309-311)."""
+    from .types import NoSharedKeyframes, vec_to_sim3
+
+    rank, world = _world(group)
+    requests, local_p, remote_p = [], [], {}
+    if loop_sm is not None:
+        for sid in directory.partners(loop_sm.keyframe_ids, exclude=loop_sm.id):
+            if directory.owner[sid] == rank and sid in mapping.submaps:
+                local_p.append(sid)
+            else:
+                shared = [kf for kf in directory.sub_kfs[sid] if kf in loop_sm.keyframe_ids]
+                remote_p[sid] = shared
+                requests += [(sid, kf) for kf in shared]
+    frames = fetch_frames(mapping, requests, directory, group)
+    if loop_sm is None:
+        return []
+    stubs, order = {}, []
+    for sid in directory.partners(loop_sm.keyframe_ids, exclude=loop_sm.id):
+        if sid in remote_p:
+            kfs = remote_p[sid]
+            d = torch.stack([frames[(sid, kf)][0] for kf in kfs])
+            c = torch.stack([frames[(sid, kf)][1] for kf in kfs])
+            p8 = [frames[(sid, kf)][2] for kf in kfs]
+            st = mapping.add_submap(kfs, d, c, p8)
+            mapping._next_id -= 1  # stubs take no id of this rank's sequence
+            st.id = -1 - len(stubs)
+            st.global_pose = vec_to_sim3(frames[(sid, kfs[0])][3])
+            mapping.submaps[st.id] = st  # a partner for this registration only
+            stubs[st.id] = sid
+            order.append(st.id)
+        else:
+            order.append(sid)
+    try:
+        edges = mapping.registration_edges(loop_sm, partner_ids=order)
+    except NoSharedKeyframes:
+        edges = []
+    best = max(edges, key=lambda e: e[3]) if edges else None
+    if best is not None:
+        loop_sm.global_pose = mapping.submaps[best[0]].global_pose.compose(best[1])
+    for st_id in stubs:
+        mapping.submaps.pop(st_id, None)
+    if best is None:
+        return []
+    mapping._commit(loop_sm)
+    out = []
+    for sid, tr, info, count, rms in edges:
+        gid = stubs.get(sid, sid)
+        mapping.edges.append((gid, loop_sm.id, tr, info))
+        out.append((gid, loop_sm.id, tr, info, count, rms))
+    return out
+
+
+EDGE_COLS = 12  # i, j, s, qw, qx, qy, qz, tx, ty, tz, information scale, (pad)
+
+
+def edge_rows(edges) -> np.ndarray:
+    """(i, j, T, info, ...) tuples -> (n, EDGE_COLS) float64 rows."""
+    from .types import sim3_to_vec
+
+    rows = np.zeros((len(edges), EDGE_COLS), np.float64)
+    for k, e in enumerate(edges):
+        i, j, tr, info = e[:4]
+        rows[k, 0], rows[k, 1] = i, j
+        rows[k, 2:10] = sim3_to_vec(tr)
+        rows[k, 10] = float(np.asarray(info)[0, 0]) if np.ndim(info) == 2 else float(info)
+    return rows
+
+
+def gather_graph(mapping, edges, group=None, root: int = 0):
+    """Collective: (node poses {sid: 8 f64}, edge rows (n, EDGE_COLS)) of all
+    ranks, on `root` (None elsewhere)."""
+    from .types import sim3_to_vec
+
+    rank, world = _world(group)
+    nodes = np.asarray([[sid, *sim3_to_vec(sm.global_pose)] for sid, sm in mapping.submaps.items()],
+                       np.float64).reshape(-1, 9)
+    er = edge_rows(edges)
+    if world == 1:
+        return {int(r[0]): r[1:] for r in nodes}, er
+    cd = _coll_dev(group)
+    n_parts = [x.cpu() for x in gather_ragged(torch.as_tensor(nodes, device=cd), group)]
+    e_parts = [x.cpu() for x in gather_ragged(torch.as_tensor(er, device=cd), group)]
+    if rank != root:
+        return None, None
+    allnodes = {int(r[0]): r[1:].copy() for p in n_parts for r in p.numpy()}
+    return allnodes, np.concatenate([p.numpy() for p in e_parts]) if e_parts else er[:0]
+
+
+def broadcast_poses(poses, ids, group=None, root: int = 0) -> dict:
+    """Collective: the root's {sid: 8 f64} for the listed ids to every rank."""
+    rank, world = _world(group)
+    t = torch.zeros((len(ids), 8), dtype=torch.float64)
+    if rank == root and ids:
+        t[:] = torch.as_tensor(np.stack([np.asarray(poses[i], np.float64) for i in ids]))
+    if world > 1:
+        td = t.to(_coll_dev(group))
+        dist.broadcast(td, src=_peer(group, root), group=group)
+        t = td.cpu()
+    return {int(i): t[k].numpy() for k, i in enumerate(ids)}
+
+
+def optimize_sharded(mapping, edges, optimize_fn, group=None, root: int = 0) -> dict:
+    """Collective pose-graph step: gather every node and edge to `root`, run
+    optimize_fn(nodes {sid: 8 f64}, edge_rows) -> {sid: 8 f64} there (the
+    reference's host PGO, posegraph.py:176), broadcast the result and
+    re-commit this rank's submaps (their pool slot globals on the device).
+    Returns the optimised poses of all submaps."""
+    from .types import vec_to_sim3
+
+    rank, world = _world(group)
+    nodes, rows = gather_graph(mapping, edges, group, root)
+    ids = None
+    if rank == root:
+        new = optimize_fn(nodes, rows)
+        ids = sorted(new)
+    cd = _coll_dev(group)
+    idt = torch.as_tensor(np.asarray(ids if ids is not None else [], np.int64), device=cd)
+    if world > 1:
+        n = torch.tensor([idt.numel()], dtype=torch.int64, device=cd)
+        dist.broadcast(n, src=_peer(group, root), group=group)
+        if rank != root:
+            idt = torch.zeros(int(n.item()), dtype=torch.int64, device=cd)
+        dist.broadcast(idt, src=_peer(group, root), group=group)
+    ids = [int(x) for x in idt.cpu().tolist()]
+    out = broadcast_poses(new if rank == root else None, ids, group, root)
+    for sid, v in out.items():
+        sm = mapping.submaps.get(sid)
+        if sm is not None:
+            sm.global_pose = vec_to_sim3(v)
+            mapping._commit(sm)
+    return out
+
+
+def _reference_posegraph():
+    """submap_slam.posegraph / liegroups: importable as installed, or from
+    EC3R_REFERENCE_SRC, or from the offline install under baseline/_ref."""
+    import importlib
+    import os
+    import sys
+
+    try:
+        return importlib.import_module("submap_slam.posegraph"), importlib.import_module("submap_slam.liegroups")
+    except ImportError:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        for p in (os.environ.get("EC3R_REFERENCE_SRC"), os.path.join(root, "baseline", "_ref")):
+            if p and os.path.isdir(p) and p not in sys.path:
+                sys.path.append(p)
+        return importlib.import_module("submap_slam.posegraph"), importlib.import_module("submap_slam.liegroups")
+
+
+def reference_pgo(lm_config=None):
+    """optimize_fn running the reference's own PoseGraph (posegraph.py:93-255,
+    host code by design) on reference Sim3Transform values built from the
+    8-vectors: the first node (smallest id) is fixed, as the reference fixes
+    its first submap (mapping.py:194-197).  Raises ImportError without the
+    reference."""
+    pg, lg = _reference_posegraph()
+
+    def to_ref(v):
+        v = np.asarray(v, np.float64)
+        return lg.Sim3Transform(float(v[0]), lg.Rotation3(v[1:5]), v[5:8])
+
+    def fn(nodes, rows):
+        g = pg.PoseGraph()
+        first = min(nodes)
+        for sid in sorted(nodes):
+            g.add_node(sid, to_ref(nodes[sid]), fixed=(sid == first))
+        for r in rows:
+            g.add_edge(int(r[0]), int(r[1]), to_ref(r[2:10]), np.eye(7) * float(r[10]))
+        g.optimize(lm_config or pg.LmConfig())
+        return {sid: np.concatenate([[float(n.pose.scale)], np.asarray(n.pose.rotation.q, float),
+                                     np.asarray(n.pose.translation, float)]) for sid, n in g.nodes.items()}
+
+    return fn

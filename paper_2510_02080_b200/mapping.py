@@ -261,12 +261,22 @@ class VoxelMap:
                    "ec3r_vhash_count")
         return int(self._n.item())
 
-    def extract(self, sort: bool = True, stream=None, out=None):
+    def stats_device(self, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """The stats() counters into a device int64[5] (no host round trip)."""
+        _lib.check(_lib.lib().ec3r_vhash_stats_device(self._h, _lib.ptr(out), _lib.stream_ptr(stream)),
+                   "ec3r_vhash_stats_device")
+        return out
+
+    def extract(self, sort: bool = True, stream=None, out=None, sync: bool = True):
         """Returns (keys int64, centroid (U,3) f32, wsum f32, count i32) CUDA
         tensors of length U (sorted by key when sort=True).  `out` may hold
-        preallocated buffers of at least U rows."""
+        preallocated buffers of at least U rows.  sync=False (sorted only):
+        no host read of U; returns the full `out` buffers plus the device
+        int64[1] count instead."""
         L = _lib.lib()
         if out is None:
+            if not sync:
+                raise ValueError("extract(sync=False) needs preallocated out buffers")
             cap = self.count(stream)
             out = (torch.empty(cap, dtype=torch.int64, device="cuda"),
                    torch.empty((cap, 3), dtype=torch.float32, device="cuda"),
@@ -275,9 +285,12 @@ class VoxelMap:
         keys, cen, ws_, cnt = out
         wsb = L.ec3r_vhash_extract_workspace(self._h)
         ws = _lib.workspace(wsb, None, "vhash_extract")
+        mode = (1 if sync else 2) if sort else 0
         _lib.check(L.ec3r_vhash_extract(self._h, _lib.ptr(keys), _lib.ptr(cen), _lib.ptr(ws_), _lib.ptr(cnt),
-                                        _lib.ptr(self._n), int(bool(sort)), _lib.ptr(ws), ws.numel(),
+                                        _lib.ptr(self._n), mode, _lib.ptr(ws), ws.numel(),
                                         _lib.stream_ptr(stream)), "ec3r_vhash_extract")
+        if sort and not sync:
+            return keys, cen, ws_, cnt, self._n
         U = int(L.ec3r_vhash_extract_count(self._h)) if sort else -1
         if U < 0:
             U = int(self._n.item())

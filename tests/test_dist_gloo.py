@@ -224,30 +224,37 @@ class _FakePool:
 
 
 class _FakeSubmap:
-    def __init__(self, kf_ids, slots):
-        self.keyframe_ids, self.slots = tuple(kf_ids), np.asarray(slots)
+    def __init__(self, kf_ids, slots, sid=0):
+        self.keyframe_ids, self.slots, self.id = tuple(kf_ids), np.asarray(slots), sid
 
 
 class _FakeMapping:
     def __init__(self, rank):
         self.pool = _FakePool(rank)
         self.added = None
+        self._next_id = 50
 
     def add_submap(self, ids, depth, conf, poses):
         self.added = (list(ids), depth.clone(), conf.clone(), np.stack(poses))
-        return self.added
+        sm = _FakeSubmap(ids, [], self._next_id)
+        self._next_id += 1
+        return sm
 
 
 def _windows(rank):
     # flush order (new..., old): rank 0 = [(0..5), (6..10, 5)], rank 1 = [(11..15, 10), (16..20, 15)]
     if rank == 0:
-        return [_FakeSubmap(range(6), range(6)), _FakeSubmap(list(range(6, 11)) + [5], range(6, 12))]
-    return [_FakeSubmap(list(range(11, 16)) + [10], range(6)), _FakeSubmap(list(range(16, 21)) + [15], range(6, 12))]
+        return [_FakeSubmap(range(6), range(6), 0), _FakeSubmap(list(range(6, 11)) + [5], range(6, 12), 1)]
+    return [_FakeSubmap(list(range(11, 16)) + [10], range(6), 2),
+            _FakeSubmap(list(range(16, 21)) + [15], range(6, 12), 3)]
 
 
 def w_halo(rank, world):
     m = _FakeMapping(rank)
-    D.window_halo(m, _windows(rank))
+    stub = D.window_halo(m, _windows(rank))
+    # the stub names the predecessor's submap (global id 1) and takes no id
+    # of this rank's sequence
+    assert stub is None or (stub.remote_id == 1 and stub.id < 0 and m._next_id == 50)
     return m.added
 
 
@@ -366,3 +373,107 @@ def test_retrieval_sharded_merge_equals_single_gloo():
     for r in range(WORLD):
         for got, want in zip(out[r], exp):
             np.testing.assert_array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# loop edges across shards + the pose-graph data path (dist.SubmapDirectory,
+# fetch_frames, gather_graph, optimize_sharded): a CPU "mapping" with a frame
+# pool on the host -- the registration launch itself is covered on the GPU
+# (tests/test_gpu_dist.py)
+
+class _Pool:
+    def __init__(self, H, W):
+        self.H, self.W, self.device = H, W, torch.device("cpu")
+        self.depth = torch.zeros((0, H, W))
+        self.conf = torch.zeros((0, H, W))
+        self.poses = torch.zeros((0, 8), dtype=torch.float64)
+
+
+class _Sub:
+    def __init__(self, sid, kfs, slots, g):
+        from paper_2510_02080_b200.types import vec_to_sim3
+        self.id, self.keyframe_ids, self.slots = sid, tuple(kfs), np.asarray(slots)
+        self.global_pose = vec_to_sim3(g)
+
+
+class _Mapping:
+    """Rank r owns submaps 10r .. 10r+2; submap i holds keyframes (3i, 3i+1,
+    3i+2); frame planes encode (submap, keyframe) so the test can check who
+    answered."""
+
+    def __init__(self, rank, H=4, W=5):
+        self.pool = _Pool(H, W)
+        self.submaps, self.edges, self.committed = {}, [], []
+        d, c, p = [], [], []
+        for i in range(3):
+            sid = 10 * rank + i
+            kfs = [3 * sid, 3 * sid + 1, 3 * sid + 2]
+            slots = list(range(len(d), len(d) + 3))
+            for kf in kfs:
+                d.append(torch.full((H, W), float(1000 * sid + kf)))
+                c.append(torch.full((H, W), 0.5 + 0.01 * kf))
+                p.append(torch.tensor([1.0, 1, 0, 0, 0, kf, sid, 0], dtype=torch.float64))
+            g = np.array([1.0 + 0.1 * sid, 1, 0, 0, 0, sid, 0, 0])
+            self.submaps[sid] = _Sub(sid, kfs, slots, g)
+        self.pool.depth, self.pool.conf, self.pool.poses = torch.stack(d), torch.stack(c), torch.stack(p)
+
+    def _commit(self, sm):
+        self.committed.append(sm.id)
+
+
+def w_directory_fetch(rank, world):
+    m = _Mapping(rank)
+    dr = D.SubmapDirectory(m)
+    # each rank asks for one frame of every other rank's middle submap, plus one of its own
+    req = [(10 * r + 1, 3 * (10 * r + 1) + 2) for r in range(world) if r != rank] + [(10 * rank, 3 * 10 * rank)]
+    got = D.fetch_frames(m, req, dr)
+    out = {}
+    for (sid, kf), (dep, cf, pose, glob) in got.items():
+        out[(sid, kf)] = (float(dep[0, 0]), float(cf[1, 2]), pose.tolist(), glob.tolist())
+    return dr.owner, dr.partners([3, 31, 4]), out
+
+
+def test_directory_and_fetch_frames_gloo():
+    out = _spawn("w_directory_fetch")
+    for rank, (owner, partners, got) in out.items():
+        assert owner == {0: 0, 1: 0, 2: 0, 10: 1, 11: 1, 12: 1}
+        assert partners == [1, 10]  # keyframes 3, 31 (submap 10 holds 30..32), 4 (submap 1): first-seen order
+        for (sid, kf), (dep, cf, pose, glob) in got.items():
+            assert dep == 1000 * sid + kf  # the owner's copy of that submap's frame
+            assert abs(cf - (0.5 + 0.01 * kf)) < 1e-6
+            assert pose[5] == kf and pose[6] == sid
+            assert abs(glob[0] - (1.0 + 0.1 * sid)) < 1e-12 and glob[5] == sid
+        assert len(got) == 2
+
+
+def w_pgo_path(rank, world):
+    from paper_2510_02080_b200.types import vec_to_sim3
+    m = _Mapping(rank)
+    info = np.eye(7) * (5.0 + rank)
+    edges = [(10 * rank, 10 * rank + 1, vec_to_sim3([1.0, 1, 0, 0, 0, 0.5, 0, 0]), info)]
+    seen = {}
+
+    def fn(nodes, rows):  # a stand-in optimiser: shift every translation by the edge count
+        seen["nodes"] = sorted(nodes)
+        seen["rows"] = rows.copy()
+        return {sid: np.concatenate([v[:5], v[5:] + len(rows)]) for sid, v in nodes.items()}
+
+    res = D.optimize_sharded(m, edges, fn)
+    return seen, {k: v.tolist() for k, v in res.items()}, sorted(m.committed), \
+        {sid: float(sm.global_pose.translation[0]) for sid, sm in m.submaps.items()}
+
+
+def test_pose_graph_gather_and_broadcast_gloo():
+    out = _spawn("w_pgo_path")
+    seen0 = out[0][0]
+    assert seen0["nodes"] == [0, 1, 2, 10, 11, 12]
+    rows = seen0["rows"]
+    assert rows.shape == (2, D.EDGE_COLS)
+    assert rows[:, :2].tolist() == [[0, 1], [10, 11]]
+    assert rows[:, 10].tolist() == [5.0, 6.0]
+    assert out[1][0] == {}  # only the root runs the optimiser
+    for rank, (_, res, committed, tx) in out.items():
+        assert sorted(res) == [0, 1, 2, 10, 11, 12]
+        assert committed == [10 * rank, 10 * rank + 1, 10 * rank + 2]  # own submaps re-committed
+        for sid, x in tx.items():
+            assert x == sid + 2  # translation x = sid, shifted by the 2 gathered edges
