@@ -398,6 +398,34 @@ EC3R_API int ec3r_homography_ransac_refit(const double* src, const double* dst, 
                                           int32_t* out_count, void* workspace, size_t workspace_bytes,
                                           void* stream);
 
+/* -------------------------------------------------------------------
+ * §8f rank 4, the tracking half: PnP RANSAC scoring.  Replaces the
+ * per-hypothesis _reprojection_errors pass of solve_pnp_ransac
+ * (geometry.py:414-474, called by tracking.py:208); the minimal EPnP
+ * hypotheses stay in the reference's host solver (LAPACK null-space bases,
+ * geometry.py:134-210).
+ *
+ * ec3r_ransac_draws: the replay of rng.choice(n, 4, replace=False) for
+ * `iters` iterations of each problem (as ec3r_homography_ransac_score) into
+ * out_samples (P x iters x 4 int32, DEVICE); workspace
+ * ec3r_ransac_draws_workspace(P).
+ *
+ * ec3r_pnp_score: n_hyp hypotheses (hyp: n_hyp x 12 float64, R row-major
+ * then t; hyp_problem: problem of each) scored over their problem's
+ * correspondences (pts (total,3), pix (total,2) float64, offsets P+1,
+ * K4 P x 4 {fx, fy, cx, cy}; all DEVICE): inlier count, sum of the inlier
+ * errors, and an ambiguity flag (an error within guard * threshold of the
+ * threshold, or a depth within 1e-12 of Z_MIN) the host resolves with the
+ * reference expression.
+ * ------------------------------------------------------------------- */
+EC3R_API size_t ec3r_ransac_draws_workspace(int n_problems);
+EC3R_API int ec3r_ransac_draws(const int64_t* offsets, int n_problems, const uint64_t* rng_state, int iters,
+                               int32_t* out_samples, void* workspace, size_t workspace_bytes, void* stream);
+EC3R_API int ec3r_pnp_score(const double* pts, const double* pix, const int64_t* offsets, const double* K4,
+                            const double* hyp, const int32_t* hyp_problem, int n_hyp, double pixel_threshold,
+                            double guard, int32_t* out_count, double* out_errsum, int32_t* out_ambiguous,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

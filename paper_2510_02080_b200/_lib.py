@@ -68,6 +68,9 @@ _PROTOS = {
     "ec3r_homography_workspace": (_SZ, [_I, _I]),
     "ec3r_homography_ransac_score": (_I, [_P, _P, _P, _I, _P, _I, _D, _P, _P, _P, _SZ, _P]),
     "ec3r_homography_ransac_refit": (_I, [_P, _P, _P, _I, _P, _I, _D, _P, _P, _P, _P, _SZ, _P]),
+    "ec3r_ransac_draws_workspace": (_SZ, [_I]),
+    "ec3r_ransac_draws": (_I, [_P, _I, _P, _I, _P, _P, _SZ, _P]),
+    "ec3r_pnp_score": (_I, [_P, _P, _P, _P, _P, _P, _I, _D, _D, _P, _P, _P, _P]),
     "ec3r_local_candidates_workspace": (_SZ, [_I]),
     "ec3r_local_candidates": (_I, [_P, _I64, _P, _I, _P, _D, _P, _P, _P, _SZ, _P]),
     "ec3r_local_candidates_ex": (_I, [_P, _I64, _P, _I, _P, _D, _P, _P, _P, _I64, _P, _P, _SZ, _P]),

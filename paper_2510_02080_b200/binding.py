@@ -16,6 +16,8 @@ Bindings (reference file:line -> this package):
       (loops.py:114-153,184-243)               -> loops.*
   geometry.estimate_homography_ransac (geometry.py:594-640)
                                                -> geometry.estimate_homography_ransac
+  geometry.solve_pnp_ransac (geometry.py:414-474, its EPnP / Gauss-Newton
+      helpers stay the reference's)            -> geometry.solve_pnp_ransac
   _kernels.nn_query / nn_dists / raycast (_kernels/__init__.py:12-33)
                                                -> kernels.*
   mapping.Mapping (mapping.py:80-338)          -> mapping.b200_mapping_class(Mapping)
@@ -45,6 +47,7 @@ def _targets():
         ("loops", "detect_local_candidates", loops.detect_local_candidates, ("loops", "pipeline")),
         ("loops", "verify_candidate", loops.verify_candidate, ("loops", "pipeline")),
         ("geometry", "estimate_homography_ransac", geometry.estimate_homography_ransac, ("geometry", "loops")),
+        ("geometry", "solve_pnp_ransac", geometry.solve_pnp_ransac, ("geometry", "tracking")),
         ("_kernels", "nn_query", kernels.nn_query, ("_kernels", "evaluation")),
         ("_kernels", "nn_dists", kernels.nn_dists, ("_kernels", "evaluation")),
         ("_kernels", "raycast", kernels.raycast, ("_kernels",)),

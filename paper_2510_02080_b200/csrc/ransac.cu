@@ -732,3 +732,107 @@ extern "C" int ec3r_homography_ransac_refit(const double* src, const double* dst
     EC3R_CHECK_LAUNCH("hg_refit_kernel");
     return EC3R_OK;
 }
+
+// ---------------------------------------------------------------------------
+// PnP RANSAC scoring (§8f rank 4, the tracking half: geometry.py:414-474,
+// called by tracking.py:208).  The hypotheses (EPnP on each 4-point draw)
+// come from the reference's host solver; the draws themselves are the
+// device replay above.  One warp scores one hypothesis over all of its
+// problem's correspondences with _reprojection_errors' operation order
+// (geometry.py:117-126): pc = R p + t, z > Z_MIN, u = fx pc0 / z + cx,
+// v = fy pc1 / z + cy, err = hypot(u - pix_u, v - pix_v), inlier = err < thr.
+// A point whose error lies within `guard` (relative) of the threshold, or
+// whose depth lies within 1e-12 of Z_MIN, flags the hypothesis ambiguous:
+// the host re-scores it with the reference expression (BLAS summation order
+// of pts @ R.T is not pinned).  The inlier error sum (fixed shuffle tree:
+// deterministic) feeds the mean-error tie break, guarded the same way.
+
+constexpr double kZMin = 1e-6;  // geometry.py:23
+
+__global__ void pnp_score_kernel(const double* __restrict__ pts, const double* __restrict__ pix,
+                                 const int64_t* __restrict__ off, const double* __restrict__ K4,
+                                 const double* __restrict__ hyp, const int32_t* __restrict__ hyp_prob, int H,
+                                 double thr, double guard, int32_t* __restrict__ out_count,
+                                 double* __restrict__ out_errsum, int32_t* __restrict__ out_amb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= H) return;
+    const int p = hyp_prob[w];
+    const double* h = hyp + 12 * w;
+    double R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = h[k];
+    t[0] = h[9]; t[1] = h[10]; t[2] = h[11];
+    const double fx = K4[4 * p], fy = K4[4 * p + 1], cx = K4[4 * p + 2], cy = K4[4 * p + 3];
+    const int64_t n0 = off[p], n1 = off[p + 1];
+    int cnt = 0, amb = 0;
+    double sum = 0.0;
+    for (int64_t i = n0 + lane; i < n1; i += 32) {
+        const double X = pts[3 * i], Y = pts[3 * i + 1], Z = pts[3 * i + 2];
+        double pc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            pc[k] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(X, R[3 * k]), __dmul_rn(Y, R[3 * k + 1])),
+                                        __dmul_rn(Z, R[3 * k + 2])),
+                              t[k]);
+        const double z = pc[2];
+        if (fabs(z - kZMin) <= 1e-12) amb = 1;
+        if (z > kZMin) {
+            const double u = __dadd_rn(__ddiv_rn(__dmul_rn(fx, pc[0]), z), cx);
+            const double v = __dadd_rn(__ddiv_rn(__dmul_rn(fy, pc[1]), z), cy);
+            const double err = hypot(__dsub_rn(u, pix[2 * i]), __dsub_rn(v, pix[2 * i + 1]));
+            if (fabs(err - thr) <= guard * thr) amb = 1;
+            if (err < thr) {
+                ++cnt;
+                sum += err;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        amb |= __shfl_xor_sync(0xffffffffu, amb, o);
+    }
+    if (lane == 0) {
+        out_count[w] = cnt;
+        out_errsum[w] = sum;
+        out_amb[w] = amb;
+    }
+}
+
+extern "C" size_t ec3r_ransac_draws_workspace(int n_problems) {
+    return align256(sizeof(int32_t) * (size_t)(n_problems > 0 ? n_problems : 1));
+}
+
+extern "C" int ec3r_ransac_draws(const int64_t* offsets, int n_problems, const uint64_t* rng_state, int iters,
+                                 int32_t* out_samples, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_problems < 0 || iters < 0) return EC3R_EARG;
+    if (n_problems == 0 || iters == 0) return EC3R_OK;
+    if (!offsets || !rng_state || !out_samples) return EC3R_EARG;
+    if (!workspace || workspace_bytes < ec3r_ransac_draws_workspace(n_problems)) return EC3R_EWORKSPACE;
+    cudaStream_t st = as_stream(stream);
+    int32_t* redo = (int32_t*)workspace;
+    hg_draw_par_kernel<<<n_problems, HG_DRAW_NT, 0, st>>>(offsets, iters, rng_state, out_samples, redo);
+    EC3R_CHECK_LAUNCH("hg_draw_par_kernel");
+    hg_draw_serial_kernel<<<(n_problems + 63) / 64, 64, 0, st>>>(offsets, n_problems, rng_state, iters, redo,
+                                                                 out_samples);
+    EC3R_CHECK_LAUNCH("hg_draw_serial_kernel");
+    return EC3R_OK;
+}
+
+extern "C" int ec3r_pnp_score(const double* pts, const double* pix, const int64_t* offsets, const double* K4,
+                              const double* hyp, const int32_t* hyp_problem, int n_hyp, double pixel_threshold,
+                              double guard, int32_t* out_count, double* out_errsum, int32_t* out_ambiguous,
+                              void* stream) {
+    if (n_hyp < 0 || !(pixel_threshold > 0) || guard < 0) return EC3R_EARG;
+    if (n_hyp == 0) return EC3R_OK;
+    if (!pts || !pix || !offsets || !K4 || !hyp || !hyp_problem || !out_count || !out_errsum || !out_ambiguous)
+        return EC3R_EARG;
+    const int64_t threads = (int64_t)n_hyp * 32;
+    pnp_score_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+        pts, pix, offsets, K4, hyp, hyp_problem, n_hyp, pixel_threshold, guard, out_count, out_errsum,
+        out_ambiguous);
+    EC3R_CHECK_LAUNCH("pnp_score_kernel");
+    return EC3R_OK;
+}

@@ -37,6 +37,7 @@ try:  # pragma: no cover - exercised when the reference is installed
     AllZeroConfidence = _ref_errors.AllZeroConfidence
     NoSharedKeyframes = _ref_errors.NoSharedKeyframes
     MissingEmbedding = _ref_errors.MissingEmbedding
+    NoConsensus = _ref_errors.NoConsensus
     REFERENCE_TYPES = True
 except ImportError:
     REFERENCE_TYPES = False
@@ -58,6 +59,9 @@ except ImportError:
 
     class MissingEmbedding(SubmapSlamError):
         """errors.py:48"""
+
+    class NoConsensus(SubmapSlamError):
+        """errors.py:16"""
 
     def _quat_mul(a, b):
         aw, ax, ay, az = a
@@ -265,3 +269,19 @@ def vec_to_sim3(v) -> "Sim3Transform":
 
 def intrinsics_vec(k) -> np.ndarray:
     return np.array([k.fx, k.fy, k.cx, k.cy], dtype=np.float64)
+
+
+def reference_module(name: str):
+    """A module of the reference package (host code this path delegates to:
+    EPnP / Gauss-Newton, pose-graph LM), importable as installed, from
+    EC3R_REFERENCE_SRC, or from the offline install under baseline/_ref."""
+    import importlib
+
+    try:
+        return importlib.import_module(name)
+    except ImportError:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        for p in (os.environ.get("EC3R_REFERENCE_SRC"), os.path.join(root, "baseline", "_ref")):
+            if p and os.path.isdir(p) and p not in sys.path:
+                sys.path.append(p)
+        return importlib.import_module(name)

@@ -502,6 +502,92 @@ def gen_ransac():
     print("ransac:", len(cases), "cases")
 
 
+
+def _pnp_scene(rng, n, k, outlier_frac=0.0, noise=0.0, planar=False):
+    """test_geometry.py:27-37 (_looking_at_points) + noise / outliers."""
+    from helpers import random_pose
+    pose = random_pose(rng, max_angle=0.8)
+    inv = pose.inverse()
+    u = rng.uniform(5, k.width - 6, size=n)
+    v = rng.uniform(5, k.height - 6, size=n)
+    z = rng.uniform(2.0, 8.0, size=n)
+    rays = np.stack([(u - k.cx) / k.fx * z, (v - k.cy) / k.fy * z, z], axis=1)
+    pts = rays @ inv.rotation.matrix().T + inv.translation
+    if planar:  # points on the world plane z = 0 seen by the camera
+        pts[:, 2] = 0.0
+        pc = pts @ pose.rotation.matrix().T + pose.translation
+        keep = pc[:, 2] > 0.5
+        pts, pc = pts[keep], pc[keep]
+        u, v = k.fx * pc[:, 0] / pc[:, 2] + k.cx, k.fy * pc[:, 1] / pc[:, 2] + k.cy
+    pix = np.stack([u, v], axis=1)
+    if noise:
+        pix = pix + rng.normal(scale=noise, size=pix.shape)
+    if outlier_frac:
+        bad = rng.choice(len(pix), size=int(outlier_frac * len(pix)), replace=False)
+        pix[bad] = rng.uniform([0, 0], [k.width, k.height], size=(len(bad), 2))
+    return pts, pix
+
+
+def gen_pnp():
+    """solve_pnp_ransac (geometry.py:414-474) on the reference's own
+    test_geometry.py scenes (:79-133) plus larger noisy / outlier / planar /
+    degenerate problems: masks, models and ratios, or the exception."""
+    from submap_slam.geometry import CameraIntrinsics, Correspondence2D3D, RansacConfig, solve_pnp_ransac
+    K = CameraIntrinsics(fx=100.0, fy=100.0, cx=50.0, cy=50.0, width=100, height=100)
+    KV = CameraIntrinsics(fx=500.0, fy=500.0, cx=320.0, cy=240.0, width=640, height=480)
+    cases = []
+    # the reference's tests, verbatim inputs
+    rng = np.random.default_rng(32)
+    pts, pix = _pnp_scene(rng, 50, KV)
+    cases.append((pts, pix, KV, RansacConfig(seed=1)))
+    rng = np.random.default_rng(33)
+    pts, pix = _pnp_scene(rng, 50, KV)
+    pix = pix + rng.normal(scale=0.5, size=pix.shape)
+    for i in rng.choice(50, size=15, replace=False):
+        pix[i] = rng.uniform([0, 0], [KV.width, KV.height])
+    cases.append((pts, pix, KV, RansacConfig(seed=2)))
+    rng = np.random.default_rng(34)
+    g_pix, g_pts = [], []
+    for i in range(20):
+        g_pix.append(rng.uniform(0, 99, size=2))
+        g_pts.append(rng.normal(size=3) * 10 + [0, 0, 50])
+    cases.append((np.array(g_pts), np.array(g_pix), K, RansacConfig(seed=3, min_inliers=10)))
+    rng = np.random.default_rng(35)
+    pts, pix = _pnp_scene(rng, 40, KV)
+    pix = pix + rng.normal(scale=0.5, size=pix.shape)
+    cases.append((pts, pix, KV, RansacConfig(seed=7)))
+    cases.append((np.zeros((3, 3)), np.zeros((3, 2)), K, RansacConfig()))  # too few
+    # larger problems
+    for n, fr, noise, seed in ((200, 0.3, 0.5, 11), (600, 0.5, 0.7, 12), (1500, 0.2, 0.4, 13), (120, 0.6, 1.0, 14)):
+        rng = np.random.default_rng(900 + seed)
+        pts, pix = _pnp_scene(rng, n, KV, outlier_frac=fr, noise=noise)
+        cases.append((pts, pix, KV, RansacConfig(seed=seed)))
+    rng = np.random.default_rng(950)
+    pts, pix = _pnp_scene(rng, 300, KV, outlier_frac=0.25, noise=0.3, planar=True)
+    cases.append((pts, pix, KV, RansacConfig(seed=21)))
+    rng = np.random.default_rng(951)
+    pts, pix = _pnp_scene(rng, 12, KV)  # exact, few points: many count ties (mean-error tie break)
+    cases.append((pts, pix, KV, RansacConfig(seed=22, min_inliers=4)))
+    out = {}
+    for c, (pts, pix, k, cfg) in enumerate(cases):
+        corrs = [Correspondence2D3D(pix[i], pts[i], i) for i in range(len(pts))]
+        out[f"c{c}_pts"], out[f"c{c}_pix"] = pts, pix
+        out[f"c{c}_K"] = np.array([k.fx, k.fy, k.cx, k.cy, k.width, k.height], np.float64)
+        out[f"c{c}_cfg"] = np.array([cfg.seed, cfg.min_inliers, cfg.pixel_threshold, cfg.max_iterations,
+                                     cfg.confidence], np.float64)
+        try:
+            r = solve_pnp_ransac(corrs, k, cfg)
+            out[f"c{c}_status"] = np.array("ok")
+            out[f"c{c}_mask"] = np.asarray(r.inlier_mask, bool)
+            out[f"c{c}_q"] = np.asarray(r.model.rotation.q, np.float64)
+            out[f"c{c}_t"] = np.asarray(r.model.translation, np.float64)
+            out[f"c{c}_ratio"] = np.float64(r.inlier_ratio)
+        except SubmapSlamError as e:
+            out[f"c{c}_status"] = np.array(type(e).__name__)
+    out["n_cases"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(OUT, "pnp.npz"), **out)
+    print("pnp:", len(cases), "cases", [str(out[f"c{c}_status"]) for c in range(len(cases))])
+
 class _SM:
     """The sparse map surface detect_local_candidates uses (positions())."""
 
@@ -513,10 +599,8 @@ class _SM:
 
 
 if __name__ == "__main__":
-    gen_registration()
-    gen_mapping()
-    gen_match()
-    gen_retrieval()
-    gen_kernels()
-    gen_local()
-    gen_ransac()
+    gens = [gen_registration, gen_mapping, gen_match, gen_retrieval, gen_kernels, gen_local, gen_ransac, gen_pnp]
+    want = set(sys.argv[1:])  # e.g. `make_golden.py pnp`: only those fixtures
+    for g in gens:
+        if not want or g.__name__[4:] in want:
+            g()

@@ -280,6 +280,7 @@ def _loop_worker(rank, world, port, q):
             loop_sm = dm.add_submap([kf_a, kf_b], torch.stack([f[0] for f in fr]), torch.stack([f[1] for f in fr]),
                                     [f[2] for f in fr])
         edges = D.register_loop_sharded(dm, loop_sm, directory)
+        loop_pose = None if loop_sm is None else D.edge_rows([(0, 0, loop_sm.global_pose, 1.0)])[0][2:10]
         all_edges = [e[:4] for e in dm.edges]
         try:
             fn = D.reference_pgo()
@@ -295,7 +296,7 @@ def _loop_worker(rank, world, port, q):
         n = int(a[4].item())
         b = D.MapExchange(0.02).run(local, int(out[0].shape[0]))
         res = dict(edges=[(i, j, D.edge_rows([(i, j, t, inf)])[0], c, r) for i, j, t, inf, c, r in edges],
-                   loop=None if loop_sm is None else D.edge_rows([(0, 0, loop_sm.global_pose, 1.0)])[0][2:10],
+                   loop=loop_pose,
                    pgo=pgo, async_map=tuple(x[:n].cpu().numpy() for x in a[:4]),
                    sync_map=tuple(x.cpu().numpy() for x in b), n_edges=len(all_edges),
                    final={sid: D.edge_rows([(0, 0, sm.global_pose, 1.0)])[0][2:10] for sid, sm in dm.submaps.items()})
