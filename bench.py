@@ -202,14 +202,19 @@ class Step:
 
     def run(self, record=None):
         torch = self.torch
+        nvtx = torch.cuda.nvtx
         ev = {}
         ev["t0"] = self._event()
         A, B, ao, bo, b_row = self.desc
+        nvtx.range_push("match")
         self.mb, self.nm = self.tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8, self.norm_bound,
                                                               b_row=b_row)
+        nvtx.range_pop()
         ev["t_match"] = self._event()
         # registration of all edges (one launch) + device pose chain (one launch)
+        nvtx.range_push("register+chain")
         out = self.plan.run(self.dm.pool) if self.chain is None else self.chain.run()
+        nvtx.range_pop()
         ev["t_reg"] = self._event()  # both launches: stage "reg" = registration + chain
         self.edge_status, self.sub_status = out[4], out[6]
         ev["t_chain"] = self._event()
@@ -221,9 +226,12 @@ class Step:
             self.vmap, out, stt = self.mapping.fuse_slots(self.dm.pool, self.slots, self.cell, expected_voxels=U,
                                                           expected_blocks=stt["n_blocks"])
             self.out = tuple(torch.empty((U,) + tuple(x.shape[1:]), dtype=x.dtype, device="cuda") for x in out)
+        nvtx.range_push("fuse")
         self.vmap.clear()
         self.vmap.insert_frames(self.dm.pool, self.slots)
+        nvtx.range_pop()
         ev["t_insert"] = self._event()
+        nvtx.range_push("emit" if self.exchange is None else "exchange+emit")
         if self.exchange is None:
             keys, cen, wsum, cnt_v = self.vmap.extract(sort=True, out=self.out)
         else:
@@ -236,6 +244,7 @@ class Step:
                                                                        sync=False)
             else:
                 keys, cen, wsum, cnt_v = self.exchange.run(self.vmap, int(self.out[0].shape[0]))
+        nvtx.range_pop()
         ev["t_emit"] = self._event()
         if self.exchange is None or not self.async_exchange:
             self.n_voxels = int(keys.numel())
@@ -783,6 +792,43 @@ def run_extras(peaks):
                                 "problems_per_s": 64 / (ms * 1e-3),
                                 "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "problems/s", "cores": 1, "kind": "port",
                                                  "sample": "the reference loop on 4 of the 64 problems"}}
+    # PnP RANSAC (tracking, geometry.py:414-474): 16 frames x 1,000 2D-3D
+    # correspondences (30 % outliers); device draws + scoring, the
+    # reference's host EPnP per hypothesis; against the unmodified reference
+    # solve_pnp_ransac on the same problems (host, 1 core)
+    try:
+        from paper_2510_02080_b200.types import reference_module
+        rg = reference_module("submap_slam.geometry")
+    except ImportError:
+        rg = None
+    if rg is not None:
+        KV = rg.CameraIntrinsics(fx=500.0, fy=500.0, cx=320.0, cy=240.0, width=640, height=480)
+        rng = np.random.default_rng(7)
+        pp = []
+        for f in range(16):
+            n = 1000
+            u, v, z = rng.uniform(5, 634, n), rng.uniform(5, 474, n), rng.uniform(2, 8, n)
+            cam = np.stack([(u - 320) / 500 * z, (v - 240) / 500 * z, z], axis=1)
+            pts = cam + rng.normal(size=3) * 0.2
+            pix = np.stack([u, v], axis=1) + 0.4 * rng.normal(size=(n, 2))
+            bad = rng.choice(n, size=300, replace=False)
+            pix[bad] = rng.uniform([0, 0], [640, 480], size=(300, 2))
+            pp.append([rg.Correspondence2D3D(pix[i], pts[i], i) for i in range(n)])
+        cfg = rg.RansacConfig(seed=3)
+        stats = {}
+        ms = _time_ms(lambda: geometry.solve_pnp_ransac_batch([(c, KV) for c in pp], cfg, stats=stats), reps=3,
+                      warm=1)
+        t0 = time.perf_counter()
+        for c in pp[:4]:
+            rg.solve_pnp_ransac(c, KV, cfg)
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / 4
+        out["pnp_ransac"] = {"problems": 16, "correspondences": 1000, "ms": ms, "problems_per_s": 16 / (ms * 1e-3),
+                             "hypotheses_scored": stats.get("hypotheses_scored"),
+                             "host_rescored": stats.get("host_rescored"),
+                             "note": "device draws + scoring; EPnP per hypothesis is the reference's host code",
+                             "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "problems/s", "cores": 1,
+                                              "kind": "reference",
+                                              "sample": "the unmodified reference solve_pnp_ransac on 4 of the 16"}}
     return out
 
 

@@ -184,7 +184,7 @@ def _pnp_problem(corrs, k):
     return pts, pix, norm_pix
 
 
-def solve_pnp_ransac_batch(problems: Sequence, cfg: RansacConfig = RansacConfig(), seeds=None, chunk: int = 32,
+def solve_pnp_ransac_batch(problems: Sequence, cfg: RansacConfig = RansacConfig(), seeds=None, chunk: int = 8,
                            stream=None, stats: Optional[dict] = None) -> list:
     """problems: sequence of (corrs, intrinsics).  One RansacResult per
     problem, or the exception instance the reference raises for it
@@ -305,7 +305,7 @@ def solve_pnp_ransac_batch(problems: Sequence, cfg: RansacConfig = RansacConfig(
                     if denom < 0:
                         needed = math.log(max(1e-300, 1.0 - cfg.confidence)) / denom
                         s["max_iters"] = min(cfg.max_iterations, max(it + 1, int(math.ceil(needed))))
-        width = min(4 * width, 256)
+        width = min(2 * width, 128)  # the adaptive stop usually lands early: grow the chunk gently
     for li, p in enumerate(live):
         s = S[li]
         pts, pix, norm_pix = data[p]
