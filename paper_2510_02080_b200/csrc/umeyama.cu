@@ -221,7 +221,23 @@ struct PoolArgs {
     double fx, fy, cx, cy;
     double floor_frac;
     int min_corr, with_scale;
+    float inv_w;  // 1/W for the division-free row split (images < 2^21 pixels)
 };
+
+// Row / column of pixel px without an integer division: floor((px + 1/2) / W)
+// through a float reciprocal is exact while px < 2^21 (relative error 2^-22
+// against a fractional-part distance of at least 1/(2W)); larger images take
+// the integer division.
+__device__ __forceinline__ void pix_uv(const PoolArgs& a, int px, int& u, int& v) {
+    if (a.inv_w > 0.f) v = __float2int_rd(__fmul_rn((float)px + 0.5f, a.inv_w));
+    else v = px / a.W;
+    u = px - v * a.W;
+}
+
+// Shared column tables are stored by (u mod 4, u / 4): the lanes of a warp
+// visit pixels 4 apart in each of their four sub-steps, so this layout puts
+// them on consecutive doubles (no bank conflicts) instead of 32 bytes apart.
+__device__ __forceinline__ int col_ix(int u, int Wq) { return (u & 3) * Wq + (u >> 2); }
 
 __device__ __forceinline__ void load_rot(const double* x8, double R[3][3], double t[3]) {
     quat_to_mat(x8 + 1, R);
@@ -290,9 +306,10 @@ __global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT, EC3R_RE_M
 register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restrict__ out_rms,
                       int64_t* __restrict__ out_count, int64_t* __restrict__ out_npairs,
                       int32_t* __restrict__ out_status, uint8_t* __restrict__ keep_masks) {
-    extern __shared__ double tabs[];  // xc[W], yc[H]  (ray coefficients, backend.py:89)
+    extern __shared__ double tabs[];  // xc[4 Wq], yc[H]  (ray coefficients, backend.py:89)
+    const int Wq = (a.W + 3) >> 2, Wp = 4 * Wq;
     double* xc = tabs;
-    double* yc = tabs + a.W;
+    double* yc = tabs + Wp;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     const int e = blockIdx.x / UM_CL;
@@ -303,7 +320,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     __shared__ float wmax_warp[UM_NT / 32];
     __shared__ float part_wmax;
     __shared__ Solution sol;
-    for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[u] = (u - a.cx) / a.fx;
+    for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[col_ix(u, Wq)] = (u - a.cx) / a.fx;
     for (int v = threadIdx.x; v < a.H; v += UM_NT) yc[v] = (v - a.cy) / a.fy;
     __syncthreads();
     const int W = a.W;
@@ -327,11 +344,14 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
         float sp[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
         int nv = 0;
+        int u0, v0;
+        pix_uv(a, pix, u0, v0);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (zA[k] > 0.f && zB[k] > 0.f) {
-                const int px = pix + k, v = px / W, u = px - v * W;
-                const float x = (float)xc[u], y = (float)yc[v];
+                int u = u0 + k, v = v0;
+                if (u >= W) pix_uv(a, pix + k, u, v);  // the group crosses a row end
+                const float x = (float)xc[col_ix(u, Wq)], y = (float)yc[v];
                 wmax = fmaxf(wmax, fminf(cA[k], cB[k]));
                 ++nv;
 #pragma unroll
@@ -385,10 +405,10 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     double a2[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) a2[k] = 0;
-    double* colA = yc + a.H;          // [3][W]
-    double* rowA = colA + 3 * W;      // [3][H]
-    double* colB = rowA + 3 * a.H;    // [3][W]
-    double* rowB = colB + 3 * W;      // [3][H]
+    double* colA = yc + a.H;          // [3][4 Wq] (col_ix layout)
+    double* rowA = colA + 3 * Wp;     // [3][H]
+    double* colB = rowA + 3 * a.H;    // [3][4 Wq]
+    double* rowB = colB + 3 * Wp;     // [3][H]
     __shared__ double tAB[6];
     auto build = [&](int sa, int sb) {
         double Ra[3][3], ta_[3], Rb[3][3], tb_[3];
@@ -396,8 +416,8 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         load_rot(a.slot_poses + 8 * sb, Rb, tb_);
         for (int u = threadIdx.x; u < W; u += UM_NT)
             for (int i = 0; i < 3; ++i) {
-                colA[i * W + u] = Ra[i][0] * xc[u] + Ra[i][2];
-                colB[i * W + u] = Rb[i][0] * xc[u] + Rb[i][2];
+                colA[i * Wp + col_ix(u, Wq)] = Ra[i][0] * xc[col_ix(u, Wq)] + Ra[i][2];
+                colB[i * Wp + col_ix(u, Wq)] = Rb[i][0] * xc[col_ix(u, Wq)] + Rb[i][2];
             }
         for (int v = threadIdx.x; v < a.H; v += UM_NT)
             for (int i = 0; i < 3; ++i) {
@@ -414,6 +434,8 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
         const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
         uint32_t kbits = 0;
+        int u0, v0;
+        pix_uv(a, pix, u0, v0);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const bool valid = zA[k] > 0.f && zB[k] > 0.f;
@@ -421,14 +443,16 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             const bool keep = valid && ((double)wf >= floorv);  // mapping.py:177
             if (keep) {
                 kbits |= 1u << (8 * k);
-                const int px = pix + k, v = px / W, u = px - v * W;
+                int u = u0 + k, v = v0;
+                if (u >= W) pix_uv(a, pix + k, u, v);
+                const int cu = col_ix(u, Wq);
                 const double wi = (double)wf;
                 const double zaa = zA[k], zbb = zB[k];
                 double pp[3], qq[3];
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    pp[i] = zaa * (colA[i * W + u] + rowA[i * a.H + v]) + tAB[i];
-                    qq[i] = zbb * (colB[i * W + u] + rowB[i * a.H + v]) + tAB[3 + i];
+                    pp[i] = zaa * (colA[i * Wp + cu] + rowA[i * a.H + v]) + tAB[i];
+                    qq[i] = zbb * (colB[i * Wp + cu] + rowB[i * a.H + v]) + tAB[3 + i];
                 }
                 a2[0] += wi;
                 a2[1] += 1.0;
@@ -520,10 +544,11 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             for (int k = 0; k < 4; ++k) {
                 const float wf = fminf(cA[k], cB[k]);
                 if (zA[k] > 0.f && zB[k] > 0.f && (double)wf >= floorv) {
-                    const int px = pix + k, v = px / W, u = px - v * W;
+                    int u, v;
+                    pix_uv(a, pix + k, u, v);
                     const double z = zA[k];
                     double d[3];
-                    for (int i = 0; i < 3; ++i) d[i] = z * (colA[i * W + u] + rowA[i * a.H + v]) + tAB[i];
+                    for (int i = 0; i < 3; ++i) d[i] = z * (colA[i * Wp + col_ix(u, Wq)] + rowA[i * a.H + v]) + tAB[i];
                     d[0] -= mp0; d[1] -= mp1; d[2] -= mp2;
                     const double y0 = v0[0] * d[0] + v0[1] * d[1] + v0[2] * d[2];
                     const double y1 = v1[0] * d[0] + v1[1] * d[1] + v1[2] * d[2];
@@ -787,7 +812,9 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
     a.edge_seg = edge_seg; a.H = H; a.W = W;
     a.fx = K4_h[0]; a.fy = K4_h[1]; a.cx = K4_h[2]; a.cy = K4_h[3];
     a.floor_frac = floor_frac; a.min_corr = min_corr; a.with_scale = with_scale;
-    const size_t smem = sizeof(double) * 7 * (size_t)(H + W);  // xc, yc + two frames' col/row tables
+    a.inv_w = (int64_t)H * W < (1 << 21) ? 1.0f / (float)W : 0.f;
+    const size_t Wp = 4 * (size_t)((W + 3) / 4);
+    const size_t smem = sizeof(double) * 7 * (size_t)(H + Wp);  // xc, yc + two frames' col/row tables
     if (smem > 48 * 1024) {
         EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
