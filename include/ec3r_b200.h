@@ -337,6 +337,18 @@ EC3R_API int ec3r_nn_query(const double* query, int64_t n_query, const double* r
                            size_t workspace_bytes, void* stream);
 EC3R_API int ec3r_raycast(const double* origins, const double* dirs, int64_t n, const double* solids_h,
                           int n_solids, double* out_t, void* stream);
+/* §8(f) rank 3: SyntheticBackend.decode (backend.py:228-281) over
+ * render_depth (scenesim.py:145-163) on the device.  solids_h (HOST):
+ * n_solids x {lo xyz, hi xyz} (room shell first, then the interior boxes);
+ * frames (DEVICE): n_frames x 12 float64 {R_wc row-major, t_wc}; K4_h (HOST)
+ * {fx, fy, cx, cy}.  Writes depth = first_hit * scale (x exp(sigma xi) when
+ * sigma > 0) and conf = 1/(1+|xi|) (1 without noise, 0 where depth <= 0) as
+ * float32 (n_frames, H, W) planes.  xi: Philox normals keyed by `key`
+ * (same distribution as the reference's, not the same stream); with
+ * sigma = 0 the output is the reference decode rounded to float32. */
+EC3R_API int ec3r_synthetic_decode(const double* solids_h, int n_solids, const double* frames, int n_frames, int H,
+                                   int W, const double* K4_h, double scale, double sigma, uint64_t key,
+                                   float* out_depth, float* out_conf, void* stream);
 
 /* ---------------------------------------------------------------------
  * K8  local loop candidates: replaces the projection count of

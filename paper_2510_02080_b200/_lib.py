@@ -64,6 +64,7 @@ _PROTOS = {
     "ec3r_nn_workspace": (_SZ, [_I64, _I64]),
     "ec3r_nn_query": (_I, [_P, _I64, _P, _I64, _D, _P, _P, _P, _SZ, _P]),
     "ec3r_raycast": (_I, [_P, _P, _I64, _P, _I, _P, _P]),
+    "ec3r_synthetic_decode": (_I, [_P, _I, _P, _I, _I, _I, _P, _D, _D, C.c_uint64, _P, _P, _P]),
     "ec3r_apply_window_offset": (_I, [_P, _I, _I, _P, _I, _P, _I64, _P, _P]),
     "ec3r_homography_workspace": (_SZ, [_I, _I]),
     "ec3r_homography_ransac_score": (_I, [_P, _P, _P, _I, _P, _I, _D, _P, _P, _P, _SZ, _P]),

@@ -24,6 +24,7 @@
 #include <climits>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <curand_kernel.h>
 
 #include "common.cuh"
 
@@ -202,35 +203,85 @@ struct RcSolids {
     int n;
 };
 
+// first hit of one ray (_numpy.py:29-47 for one row), 0 for none
+__device__ __forceinline__ double rc_first_hit(const double (&o)[3], const double (&d)[3], const RcSolids& s) {
+    constexpr double EPS = 1e-9;
+    double inv[3];
+    for (int a = 0; a < 3; ++a) inv[a] = __ddiv_rn(1.0, d[a]);
+    double best = INFINITY;
+    for (int b = 0; b < s.n; ++b) {
+        double near = -INFINITY, far = INFINITY;
+        for (int a = 0; a < 3; ++a) {
+            double t1, t2;
+            if (d[a] == 0.0) {
+                const bool inside = o[a] >= s.lo[b][a] && o[a] <= s.hi[b][a];
+                t1 = inside ? -INFINITY : INFINITY;
+                t2 = inside ? INFINITY : -INFINITY;
+            } else {
+                t1 = __dmul_rn(__dsub_rn(s.lo[b][a], o[a]), inv[a]);
+                t2 = __dmul_rn(__dsub_rn(s.hi[b][a], o[a]), inv[a]);
+            }
+            near = np_max(near, np_min(t1, t2));
+            far = np_min(far, np_max(t1, t2));
+        }
+        if (near <= far && far > EPS) best = fmin(best, near > EPS ? near : far);
+    }
+    return isfinite(best) ? best : 0.0;
+}
+
 __global__ void rc_kernel(const double* __restrict__ org, const double* __restrict__ dir, int64_t n, RcSolids s,
                           double* __restrict__ out_t) {
-    constexpr double EPS = 1e-9;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double o[3], d[3], inv[3];
+        double o[3], d[3];
         for (int a = 0; a < 3; ++a) {
             o[a] = org[3 * i + a];
             d[a] = dir[3 * i + a];
-            inv[a] = __ddiv_rn(1.0, d[a]);
         }
-        double best = INFINITY;
-        for (int b = 0; b < s.n; ++b) {
-            double near = -INFINITY, far = INFINITY;
-            for (int a = 0; a < 3; ++a) {
-                double t1, t2;
-                if (d[a] == 0.0) {
-                    const bool inside = o[a] >= s.lo[b][a] && o[a] <= s.hi[b][a];
-                    t1 = inside ? -INFINITY : INFINITY;
-                    t2 = inside ? INFINITY : -INFINITY;
-                } else {
-                    t1 = __dmul_rn(__dsub_rn(s.lo[b][a], o[a]), inv[a]);
-                    t2 = __dmul_rn(__dsub_rn(s.hi[b][a], o[a]), inv[a]);
-                }
-                near = np_max(near, np_min(t1, t2));
-                far = np_min(far, np_max(t1, t2));
-            }
-            if (near <= far && far > EPS) best = fmin(best, near > EPS ? near : far);
+        out_t[i] = rc_first_hit(o, d, s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// §8(f) rank 3: the synthetic producer on the device -- SyntheticBackend.decode
+// (backend.py:228-281) over render_depth (scenesim.py:145-163).  One thread
+// per pixel of every listed frame:
+//   dir_cam = ((u - cx) / fx, (v - cy) / fy, 1)           (scenesim.py:155-158)
+//   dir_world = dir_cam @ R_wc^T  as numpy's BLAS evaluates it here: an FMA
+//               chain in column order (d0 r0, + d1 r1, + d2 r2)   (:159)
+//   t = first hit (rc_first_hit, bit-exact with _kernels raycast)  (:161)
+//   depth = t * scale; with sigma > 0: depth *= exp(sigma xi), conf =
+//   1 / (1 + |xi|); conf = 0 where depth <= 0              (backend.py:253-262)
+// xi is a standard normal from a counter-based Philox stream keyed by
+// (seed, decode call) and indexed by (frame, pixel): the same distribution as
+// the reference's default_rng normals, not the same numbers (numpy's
+// ziggurat over PCG64 is sequential).  With sigma = 0 the decode is
+// bit-exact (depth rounded to float32, the pool's format).
+__global__ void dec_kernel(RcSolids s, const double* __restrict__ frames, int F, int H, int W, double fx, double fy,
+                           double cx, double cy, double scale, double sigma, unsigned long long key,
+                           float* __restrict__ depth, float* __restrict__ conf) {
+    const int64_t HW = (int64_t)H * W, n = HW * F;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(p / HW);
+        const int64_t q = p - (int64_t)f * HW;
+        const int v = (int)(q / W), u = (int)(q - (int64_t)v * W);
+        const double* R = frames + 12 * f;
+        const double dc[3] = {__ddiv_rn(__dsub_rn((double)u, cx), fx), __ddiv_rn(__dsub_rn((double)v, cy), fy), 1.0};
+        double o[3], d[3];
+        for (int i = 0; i < 3; ++i) {
+            d[i] = __fma_rn(dc[2], R[3 * i + 2], __fma_rn(dc[1], R[3 * i + 1], __dmul_rn(dc[0], R[3 * i])));
+            o[i] = R[9 + i];
         }
-        out_t[i] = isfinite(best) ? best : 0.0;
+        double z = __dmul_rn(rc_first_hit(o, d, s), scale);
+        double c = 1.0;
+        if (sigma > 0.0) {
+            curandStatePhilox4_32_10_t st;
+            curand_init(key, (unsigned long long)p, 0ull, &st);
+            const double xi = curand_normal_double(&st);
+            z = __dmul_rn(z, exp(__dmul_rn(sigma, xi)));
+            c = __ddiv_rn(1.0, __dadd_rn(1.0, fabs(xi)));
+        }
+        depth[p] = (float)z;
+        conf[p] = z > 0.0 ? (float)c : 0.f;
     }
 }
 
@@ -321,5 +372,28 @@ extern "C" int ec3r_raycast(const double* origins, const double* dirs, int64_t n
         }
     rc_kernel<<<nn_grid(n, 256), 256, 0, as_stream(stream)>>>(origins, dirs, n, s, out_t);
     EC3R_CHECK_LAUNCH("rc_kernel");
+    return EC3R_OK;
+}
+
+extern "C" int ec3r_synthetic_decode(const double* solids_h, int n_solids, const double* frames, int n_frames, int H,
+                                     int W, const double* K4_h, double scale, double sigma, uint64_t key,
+                                     float* out_depth, float* out_conf, void* stream) {
+    if (n_frames < 0 || H <= 0 || W <= 0 || n_solids < 0 || n_solids > RC_MAX_SOLIDS || (n_solids && !solids_h) ||
+        !K4_h || !(sigma >= 0.0))
+        return EC3R_EARG;
+    if (n_frames == 0) return EC3R_OK;
+    if (!frames || !out_depth || !out_conf) return EC3R_EARG;
+    RcSolids s;
+    s.n = n_solids;
+    for (int b = 0; b < n_solids; ++b)
+        for (int a = 0; a < 3; ++a) {
+            s.lo[b][a] = solids_h[6 * b + a];
+            s.hi[b][a] = solids_h[6 * b + 3 + a];
+        }
+    const int64_t n = (int64_t)n_frames * H * W;
+    dec_kernel<<<nn_grid(n, 256), 256, 0, as_stream(stream)>>>(s, frames, n_frames, H, W, K4_h[0], K4_h[1], K4_h[2],
+                                                               K4_h[3], scale, sigma, (unsigned long long)key,
+                                                               out_depth, out_conf);
+    EC3R_CHECK_LAUNCH("dec_kernel");
     return EC3R_OK;
 }

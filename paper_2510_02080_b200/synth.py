@@ -271,3 +271,80 @@ def pooled_embeddings(n: int, cfg: SceneConfig = SceneConfig(), dim: int = 64, t
     pooled = tok.mean(axis=1)
     pooled /= np.linalg.norm(pooled, axis=1, keepdims=True)
     return torch.as_tensor(pooled, device=device)
+
+
+class DeviceDecoder:
+    """SyntheticBackend.decode (backend.py:228-281) on the device, §8(f) rank 3.
+
+    Wraps the reference's own SyntheticBackend (its world, trajectory,
+    config, seed and decode-call counter): the gauge scale comes from the
+    reference's own generator (default_rng([seed, 303, call_index]).uniform,
+    backend.py:241-244, bit-exact), the relative poses are the reference's
+    expressions (:265-266), and the frames are rendered and decoded by
+    ec3r_synthetic_decode in one launch: render_depth's ray layout and BLAS
+    FMA order, the bit-exact slab ray cast, log-normal depth noise with
+    conf = 1/(1+|xi|), conf = 0 where depth <= 0.  The noise xi is a Philox
+    stream (same distribution, different numbers than numpy's sequential
+    ziggurat); with depth_noise_sigma = 0 the planes equal the reference's
+    decode rounded to float32.  Depths / confidences come back as CUDA
+    float32 tensors (the FramePool's format): DenseMapping.add_output takes
+    them without a host copy."""
+
+    DECODE_SALT = 303  # backend.py:33
+
+    def __init__(self, backend, stream=None):
+        self.b = backend
+        self.stream = stream
+        w = backend.world
+        sol = [np.concatenate([np.asarray(w.room_min, float), np.asarray(w.room_max, float)])]
+        for lo, hi in w.config.interior_boxes:
+            sol.append(np.concatenate([np.asarray(lo, float), np.asarray(hi, float)]))
+        self.solids = np.ascontiguousarray(np.stack(sol), np.float64)
+        k = backend.intrinsics
+        self.K4 = np.array([k.fx, k.fy, k.cx, k.cy], np.float64)
+
+    def decode(self, embeddings):
+        from . import _lib
+        from .types import reference_module
+
+        rb = reference_module("submap_slam.backend")
+        rl = reference_module("submap_slam.liegroups")
+        b, cfg = self.b, self.b.config
+        if len(embeddings) < 2:
+            raise rb.BatchTooSmall(f"decoder needs >= 2 embeddings, got {len(embeddings)}")
+        if len(embeddings) > cfg.max_batch:
+            raise rb.BatchTooLarge(f"decoder batch {len(embeddings)} exceeds max {cfg.max_batch}")
+        frame_ids = tuple(int(getattr(e, "keyframe_id", e)) for e in embeddings)
+        for fid in frame_ids:
+            b._check_frame(fid)
+        call_index = b._decode_calls
+        b._decode_calls += 1
+        rng = np.random.default_rng([b.seed, self.DECODE_SALT, call_index])
+        lo, hi = cfg.gauge_scale_range
+        scale = float(rng.uniform(lo, hi)) if hi > lo else float(lo)
+        anchor = frame_ids[0]
+        anchor_world = b.trajectory[anchor]
+        k = b.intrinsics
+        H, W = int(k.height), int(k.width)
+        F = len(frame_ids)
+        frames = np.zeros((F, 12), np.float64)
+        poses = []
+        for i, fid in enumerate(frame_ids):
+            wc = b.trajectory[fid]
+            frames[i, :9] = wc.rotation.matrix().reshape(-1)
+            frames[i, 9:] = wc.translation
+            rel = anchor_world.inverse().compose(wc)
+            poses.append(rl.Pose3(rel.rotation, rel.translation * scale))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        fr = torch.as_tensor(frames, device=dev)
+        depth = torch.empty((F, H, W), dtype=torch.float32, device=dev)
+        conf = torch.empty_like(depth)
+        key = (int(b.seed) * 0x9E3779B97F4A7C15 + call_index * 0xBF58476D1CE4E5B9 + 0x94D049BB133111EB) % (1 << 64)
+        _lib.check(_lib.lib().ec3r_synthetic_decode(self.solids.ctypes.data, len(self.solids), _lib.ptr(fr), F, H, W,
+                                                    self.K4.ctypes.data, scale, float(cfg.depth_noise_sigma), key,
+                                                    _lib.ptr(depth), _lib.ptr(conf), _lib.stream_ptr(self.stream)),
+                   "ec3r_synthetic_decode")
+        true_global = anchor_world.to_sim3().compose(rl.Sim3Transform(1.0 / scale, rl.Rotation3.identity(),
+                                                                      np.zeros(3)))
+        b.injected_gauges.append(rb.InjectedGauge(call_index, frame_ids, anchor, scale, true_global))
+        return rb.ReconstructionOutput(frame_ids, depth, conf, tuple(poses), k, call_index)

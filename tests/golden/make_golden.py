@@ -588,6 +588,38 @@ def gen_pnp():
     np.savez_compressed(os.path.join(OUT, "pnp.npz"), **out)
     print("pnp:", len(cases), "cases", [str(out[f"c{c}_status"]) for c in range(len(cases))])
 
+
+def gen_decode():
+    """SyntheticBackend.decode (backend.py:228-281) at 518 x 392 on the
+    reference's own world and a circle trajectory (SURVEY §8(d) cfg 1):
+    noise-free planes (depth_noise_sigma = 0) for bit-exact checks of the
+    device producer, plus the gauge and poses of a noisy backend."""
+    from submap_slam.backend import SyntheticBackend, SyntheticBackendConfig
+    world = generate_world(WorldConfig(room_size=(8.0, 8.0, 4.0), landmark_count=300), seed=0)
+    traj = generate_trajectory(TrajectorySpec(kind="circle", frame_count=16, radius=2.0, step_bound=1.0), world,
+                               seed=0)
+    out = {}
+    for tag, sigma in (("clean", 0.0), ("noisy", 0.01)):
+        cfg = SyntheticBackendConfig(depth_resolution=(518, 392), focal=400.0, depth_noise_sigma=sigma)
+        be = SyntheticBackend(world, traj, cfg, seed=100)
+        for call, ids in enumerate(((0, 1, 2, 3, 4), (4, 5, 6, 7, 8))):
+            r = be.decode([rbackend.KeyframeEmbedding(i, np.zeros((1, 1))) for i in ids])
+            pfx = f"{tag}{call}_"
+            out[pfx + "ids"] = np.array(ids)
+            out[pfx + "scale"] = np.float64(be.injected_gauges[-1].scale)
+            out[pfx + "pose_q"] = np.stack([p.rotation.q for p in r.poses])
+            out[pfx + "pose_t"] = np.stack([p.translation for p in r.poses])
+            if sigma == 0.0:
+                out[pfx + "depth"] = r.depths.astype(np.float32)
+                out[pfx + "conf"] = r.confidences.astype(np.float32)
+    out["traj_q"] = np.stack([p.rotation.q for p in traj])
+    out["traj_t"] = np.stack([p.translation for p in traj])
+    out["room_min"], out["room_max"] = np.asarray(world.room_min, float), np.asarray(world.room_max, float)
+    out["boxes"] = np.array([np.concatenate([np.asarray(a, float), np.asarray(b, float)])
+                             for a, b in world.config.interior_boxes]).reshape(-1, 6)
+    np.savez_compressed(os.path.join(OUT, "decode.npz"), **out)
+    print("decode:", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
+
 class _SM:
     """The sparse map surface detect_local_candidates uses (positions())."""
 
@@ -599,7 +631,8 @@ class _SM:
 
 
 if __name__ == "__main__":
-    gens = [gen_registration, gen_mapping, gen_match, gen_retrieval, gen_kernels, gen_local, gen_ransac, gen_pnp]
+    gens = [gen_registration, gen_mapping, gen_match, gen_retrieval, gen_kernels, gen_local, gen_ransac, gen_pnp,
+            gen_decode]
     want = set(sys.argv[1:])  # e.g. `make_golden.py pnp`: only those fixtures
     for g in gens:
         if not want or g.__name__[4:] in want:
