@@ -12,7 +12,7 @@ SUBSET=${SUBSET:-"match_many_small_pairs or match_tiny_pairs or match_golden_cas
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck; do
     timeout 1500 $CS --tool $tool --target-processes all --print-limit 50 --error-exitcode 17 \
-        python -m pytest tests/test_gpu_parity.py -m gpu -x -q -p no:cacheprovider -k "$SUBSET" \
+        python -m pytest tests/test_gpu_parity.py ${EXTRA_FILES:-} -m gpu -x -q -p no:cacheprovider -k "$SUBSET" \
         > "$OUT/sanitizer_$tool.log" 2>&1
     echo "$tool rc=$?"
     tail -3 "$OUT/sanitizer_$tool.log"
