@@ -1,4 +1,4 @@
-T=r02m; O=gpurun_out/$T; mkdir -p $O
-export EXTRA_FILES="tests/test_gpu_pnp.py tests/test_gpu_decode.py tests/test_gpu_fusion_engines.py"
-export SUBSET="match_many_small_pairs or match_tiny_pairs or match_golden_cases or voxel_fusion_vs_oracle or voxel_partials or registration_edges_vs_golden or register_chain_global_poses or homography_ransac_golden_batched or retrieval_golden or local_candidates_golden or kernels_nn_query_golden or pnp_golden or noise_free or binned_fusion_vs_oracle or binned_points"
-bash tools/sanitize.sh $T
+T=r02o; O=gpurun_out/$T; mkdir -p $O
+for ov in serial early late; do EC3R_BENCH_OVERLAP=$ov timeout 900 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline > $O/bench_$ov.json 2> $O/bench_$ov.err; echo b_rc=$?; tail -2 $O/bench_$ov.err
+python -c "
+import json;d=json.loads(open('$O/bench_$ov.json').read().strip().splitlines()[-1]);print('$ov', d['ms_per_step'],d['value'],d['stages_ms'],d['e2e']['ms_per_step'], d['roofline']['frac'], d['rooflines']['match']['frac'], d['rooflines']['register']['frac'])"; done

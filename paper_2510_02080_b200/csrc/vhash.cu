@@ -467,7 +467,11 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 if (!(lead & (1u << k))) continue;
                 if (ek[k] != bk[k] || gk[k] == -1) gk[k] = vb_find_or_insert(a.vb, bk[k]);
                 got[k] = gk[k];
-                if (tag[k] && gk[k] >= 0) bcache[slot[k]] = ((unsigned long long)tag[k] << 32) | (uint32_t)gk[k];
+                // the cache is lock-free: entries are single 64-bit words validated by
+                // their tag on read, so a racing reader sees the old or the new entry;
+                // the (rare) refill is an atomic exchange so the sanitizer sees it too
+                if (tag[k] && gk[k] >= 0)
+                    atomicExch(&bcache[slot[k]], ((unsigned long long)tag[k] << 32) | (uint32_t)gk[k]);
             }
         }
 #pragma unroll
