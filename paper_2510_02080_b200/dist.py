@@ -20,6 +20,7 @@ The exchange helpers take tensors on any device, so the protocol runs under
 
 from __future__ import annotations
 
+import math
 from typing import Optional, Sequence
 
 import numpy as np
@@ -242,6 +243,39 @@ class MapExchange:
         self.owned.stats_device(self._stats, stream)
         self.flags[1:2].add_(self._stats[2:3])
         return res
+
+    def retune(self, slack: float = 1.1):
+        """Shrink (or grow) the slabs to `slack` x the largest bucket any rank
+        sent in the last run (one all-reduce; call outside timed loops).  The
+        equal-split all-to-all moves world x cap rows per rank, so the slab
+        size is the traffic: hash-partitioned buckets are balanced, and the
+        first sizing (2 x n_local / world) is twice what they need."""
+        b = self._bufs
+        if b is None:
+            return self.cap
+        m = b["send_counts"].max().reshape(1).clone()
+        if self.world > 1:
+            if _host_staged(self.group, m.device):
+                mc = m.cpu()
+                dist.all_reduce(mc, op=dist.ReduceOp.MAX, group=self.group)
+                m = mc
+            else:
+                dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+        f = self.flags.clone()
+        if self.world > 1:
+            if _host_staged(self.group, f.device):
+                fc = f.cpu()
+                dist.all_reduce(fc, op=dist.ReduceOp.MAX, group=self.group)
+                f = fc
+            else:
+                dist.all_reduce(f, op=dist.ReduceOp.MAX, group=self.group)
+        if int(f.max().item()):  # the last run overflowed: its counts are clipped
+            cap = 2 * self.cap
+        else:
+            cap = max(1024, int(math.ceil(slack * int(m.item()))) + 64)
+        if cap != self.cap:
+            self._alloc(cap)
+        return cap
 
     def verify(self):
         """Host check of the overflow flags accumulated by run(sync=False)."""
@@ -626,7 +660,7 @@ def fetch_frames(mapping, requests, directory: SubmapDirectory, group=None) -> d
         incoming = [torch.as_tensor(np.asarray(per[0], np.int64).reshape(-1, 2))]
     else:
         incoming = _a2a_ragged([torch.as_tensor(np.asarray(p, np.int64).reshape(-1, 2)) for p in per],
-                               torch.int64, 2, torch.device("cpu"), group)
+                               torch.int64, 2, _coll_dev(group), group)
     from .types import sim3_to_vec
 
     planes, poses = [], []

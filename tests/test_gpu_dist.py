@@ -294,6 +294,13 @@ def _loop_worker(rank, world, port, q):
         a = ex.run(local, int(out[0].shape[0]), sync=False)
         ex.verify()
         n = int(a[4].item())
+        a = tuple(x.clone() for x in a)
+        cap0 = ex.cap
+        cap1 = ex.retune()  # slabs sized from the observed buckets: same partition
+        a2 = ex.run(local, int(out[0].shape[0]), sync=False)
+        ex.verify()
+        assert cap1 < cap0 and int(a2[4].item()) == n
+        assert all(torch.equal(x[:n], y[:n]) for x, y in zip(a[:4], a2[:4]))
         b = D.MapExchange(0.02).run(local, int(out[0].shape[0]))
         res = dict(edges=[(i, j, D.edge_rows([(i, j, t, inf)])[0], c, r) for i, j, t, inf, c, r in edges],
                    loop=loop_pose,
