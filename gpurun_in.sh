@@ -1,6 +1,8 @@
-T=r02q; O=gpurun_out/$T; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_dist.py -q -x -k loop > $O/dist.log 2>&1; echo t_rc=$?; tail -2 $O/dist.log
-NCCL_DEBUG=WARN timeout 600 python tools/nccl_one_gpu.py > $O/nccl.log 2>&1; echo rc=$?; tail -2 $O/nccl.log
-for n in 2 4 8; do timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2955$n bench.py --gpus $n --steps 3 --warmup 3 --no-extras --no-cpu-baseline > $O/n${n}_nccl.json 2> $O/n${n}_nccl.err; echo n${n}_rc=$?; tail -2 $O/n${n}_nccl.err
+T=r02r; O=gpurun_out/$T; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_parity.py tests/test_gpu_dist.py -q -x -k "voxel or fused or bench or loop or window" > $O/tests.log 2>&1; echo tests_rc=$?; tail -3 $O/tests.log
+timeout 900 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline > $O/bench.json 2> $O/bench.err; echo b_rc=$?
 python -c "
-import json;d=json.loads(open('$O/n${n}_nccl.json').read().strip().splitlines()[-1]);print($n, d['ms_per_step'], d['value'], d['config'].get('validation_only'), d['config']['voxels_per_gpu'], d['stages_ms'])"; done
+import json;d=json.loads(open('$O/bench.json').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d['stages_ms'])"
+EC3R_BENCH_OVERLAP=serial timeout 900 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline > $O/bench_serial.json 2> $O/bench_serial.err
+python -c "
+import json;d=json.loads(open('$O/bench_serial.json').read().strip().splitlines()[-1]);print('serial', d['ms_per_step'],d['value'],d['stages_ms'])"

@@ -60,6 +60,7 @@ struct ec3r_vhash {
     float4* ftab;                    // per-frame affine tables of the last insert_frames
     int64_t ftab_cap;                // float4 entries
     int64_t last_count;              // voxels of the last sorted extract (host-known), -1 if unknown
+    bool emit_key32;                 // the last read-back extent fit the emit's 32-bit block keys
     // binned super-block engine (vbin.cu, EC3R_FUSE_ENGINE=binned): frame and
     // point inserts go there; partial merges (multi-GPU owner maps) always use
     // the block hash.  A map holds one kind of content between clears.
@@ -921,24 +922,77 @@ __global__ void vc_block_prep_kernel(const unsigned int* __restrict__ counts,
     }
 }
 
-__device__ __forceinline__ int64_t lb_u64(const unsigned long long* a, int64_t n, unsigned long long v) {
+// 32-bit sort keys relative to the used blocks' minimum corner: x 11 | y 11 |
+// z 10 bits (the _pack key order).  bb[0..2] = min block coordinates,
+// bb[3..5] = max; bb[6] set when the extent does not fit (the caller then
+// re-runs with the 64-bit keys).
+constexpr int VC_XB = 11, VC_YB = 11, VC_ZB = 10;
+
+__global__ void vc_bbox_kernel(const unsigned long long* __restrict__ block_keys,
+                               const unsigned long long* __restrict__ counters, int64_t nb, int* __restrict__ bb) {
+    const int64_t used = vc_used(counters, nb);
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < used; b += (int64_t)gridDim.x * blockDim.x) {
+        long long c[3];
+        unpack_cells(block_keys[b], c[0], c[1], c[2]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { mn[a] = min(mn[a], (int)c[a]); mx[a] = max(mx[a], (int)c[a]); }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; ++a)
+            if (mn[a] <= mx[a]) { atomicMin(&bb[a], mn[a]); atomicMax(&bb[3 + a], mx[a]); }
+}
+
+__global__ void vc_key32_kernel(const unsigned long long* __restrict__ block_keys,
+                                const unsigned long long* __restrict__ counters, int64_t nb, int* __restrict__ bb,
+                                uint32_t* __restrict__ skey, uint32_t* __restrict__ ids) {
+    const int64_t used = vc_used(counters, nb);
+    const bool fits = used == 0 || ((unsigned)(bb[3] - bb[0]) < (1u << VC_XB) &&
+                                    (unsigned)(bb[4] - bb[1]) < (1u << VC_YB) &&
+                                    (unsigned)(bb[5] - bb[2]) < (1u << VC_ZB));
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !fits) bb[6] = 1;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k = 0xFFFFFFFFu;
+        if (b < used && fits) {
+            long long c[3];
+            unpack_cells(block_keys[b], c[0], c[1], c[2]);
+            k = ((uint32_t)(c[0] - bb[0]) << (VC_YB + VC_ZB)) | ((uint32_t)(c[1] - bb[1]) << VC_ZB) |
+                (uint32_t)(c[2] - bb[2]);
+        }
+        skey[b] = k;
+        ids[b] = (uint32_t)b;
+    }
+}
+
+template <typename K>
+__device__ __forceinline__ int64_t lb_key(const K* a, int64_t n, unsigned long long v) {
     int64_t lo = 0, hi = n;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if (a[mid] < v) lo = mid + 1; else hi = mid;
+        if ((unsigned long long)a[mid] < v) lo = mid + 1; else hi = mid;
     }
     return lo;
 }
 
-__global__ void vc_groups_kernel(const unsigned long long* __restrict__ skeys, const uint32_t* __restrict__ sids,
-                                 const unsigned long long* __restrict__ counters, int64_t nb,
+// x-group (same bx) and xy-group (same bx, by) of every used block from the
+// key-sorted blocks: x = key >> sx, xy = key >> sy
+template <typename K>
+__global__ void vc_groups_kernel(const K* __restrict__ skeys, const uint32_t* __restrict__ sids,
+                                 const unsigned long long* __restrict__ counters, int64_t nb, int sx, int sy,
                                  ColGroup* __restrict__ grp) {
     const int64_t n = vc_used(counters, nb);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = skeys[i];
-        const unsigned long long x = k >> 42, xy = k >> 21;
-        const int64_t s_x = lb_u64(skeys, n, x << 42), e_x = lb_u64(skeys, n, (x + 1) << 42);
-        const int64_t s_xy = lb_u64(skeys, n, xy << 21), e_xy = lb_u64(skeys, n, (xy + 1) << 21);
+        const unsigned long long k = (unsigned long long)skeys[i];
+        const unsigned long long x = k >> sx, xy = k >> sy;
+        const int64_t s_x = lb_key(skeys, n, x << sx), e_x = lb_key(skeys, n, (x + 1) << sx);
+        const int64_t s_xy = lb_key(skeys, n, xy << sy), e_xy = lb_key(skeys, n, (xy + 1) << sy);
         grp[sids[i]] = ColGroup{(int)s_x, (int)(e_x - s_x), (int)(s_xy - s_x), (int)(e_xy - s_xy), (int)(i - s_xy), 0};
     }
 }
@@ -1003,6 +1057,8 @@ __global__ void vc_gather_kernel(const float4* __restrict__ sums, const unsigned
 
 struct ColWs {
     uint8_t* colcnt;
+    int* bb;  // bounding box + overflow flag of the 32-bit keys
+    uint32_t *skey32, *skey32_s;
     unsigned long long *skey, *skey_s;
     uint32_t *ids, *ids_s;
     ColGroup* grp;
@@ -1012,13 +1068,19 @@ struct ColWs {
 };
 
 static size_t col_ws_layout(int64_t nb, char* base, ColWs* w) {
-    size_t cs = 0, cc = 0;
+    size_t cs = 0, cc = 0, c32 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, cs, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                     (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nb, 0, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, c32, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)nb, 0, 32);
+    cs = std::max(cs, c32);
     cub::DeviceScan::ExclusiveSum(nullptr, cc, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(nb * 16 + 1));
     Carver cv{base, 0};
     ColWs t;
     t.colcnt = cv.take<uint8_t>(nb * 16);
+    t.bb = cv.take<int>(8);
+    t.skey32 = cv.take<uint32_t>(nb);
+    t.skey32_s = cv.take<uint32_t>(nb);
     t.skey = cv.take<unsigned long long>(nb);
     t.skey_s = cv.take<unsigned long long>(nb);
     t.ids = cv.take<uint32_t>(nb);
@@ -1041,20 +1103,45 @@ static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsu
     ColWs w;
     if (col_ws_layout(nb, (char*)workspace, &w) > workspace_bytes) return EC3R_EWORKSPACE;
     h->last_count = -1;
+    // 32-bit sort keys (4 radix passes instead of 8) when the host knows the
+    // map's block extent fit them at the last read-back; a map that outgrew
+    // them is caught by the flag read below and re-emitted with 64-bit keys
+    const bool k32 = read_count && h->emit_key32;
     EC3R_CUDA_TRY(cudaMemsetAsync(w.scan_in, 0, sizeof(uint32_t) * (size_t)(nb * 16 + 1), st));
     const unsigned gw = (unsigned)std::min<int64_t>((nb * 32 + 255) / 256, (int64_t)kNumSMs * 16);
     vc_block_prep_kernel<<<gw, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, w.colcnt, w.skey, w.ids);
     EC3R_CHECK_LAUNCH("vc_block_prep_kernel");
-    size_t cb = w.cub_bytes;
-    if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.skey, w.skey_s, w.ids, w.ids_s, (int)nb, 0, 64, st) !=
-        cudaSuccess) {
-        set_last_error("cub::DeviceRadixSort::SortPairs(blocks)", cudaGetLastError());
-        return EC3R_ECUDA;
+    const int bb_init[8] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN, 0, 0};
+    if (read_count) {  // the box is always measured when the host reads back (it decides the next emit's keys)
+        EC3R_CUDA_TRY(cudaMemcpyAsync(w.bb, bb_init, sizeof(bb_init), cudaMemcpyHostToDevice, st));
+        const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, (int64_t)kNumSMs * 4);
+        vc_bbox_kernel<<<gb, 256, 0, st>>>(h->block_keys, h->counters, nb, w.bb);
+        EC3R_CHECK_LAUNCH("vc_bbox_kernel");
     }
-    count_launch();
     const unsigned gt = (unsigned)std::min<int64_t>((nb + 255) / 256, (int64_t)kNumSMs * 8);
-    vc_groups_kernel<<<gt, 256, 0, st>>>(w.skey_s, w.ids_s, h->counters, nb, w.grp);
-    EC3R_CHECK_LAUNCH("vc_groups_kernel");
+    size_t cb = w.cub_bytes;
+    if (k32) {
+        vc_key32_kernel<<<gt, 256, 0, st>>>(h->block_keys, h->counters, nb, w.bb, w.skey32, w.ids);
+        EC3R_CHECK_LAUNCH("vc_key32_kernel");
+        if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.skey32, w.skey32_s, w.ids, w.ids_s, (int)nb, 0, 32,
+                                            st) != cudaSuccess) {
+            set_last_error("cub::DeviceRadixSort::SortPairs(blocks, 32-bit)", cudaGetLastError());
+            return EC3R_ECUDA;
+        }
+        count_launch();
+        vc_groups_kernel<uint32_t><<<gt, 256, 0, st>>>(w.skey32_s, w.ids_s, h->counters, nb, VC_YB + VC_ZB, VC_ZB,
+                                                       w.grp);
+        EC3R_CHECK_LAUNCH("vc_groups_kernel");
+    } else {
+        if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.skey, w.skey_s, w.ids, w.ids_s, (int)nb, 0, 64, st) !=
+            cudaSuccess) {
+            set_last_error("cub::DeviceRadixSort::SortPairs(blocks)", cudaGetLastError());
+            return EC3R_ECUDA;
+        }
+        count_launch();
+        vc_groups_kernel<unsigned long long><<<gt, 256, 0, st>>>(w.skey_s, w.ids_s, h->counters, nb, 42, 21, w.grp);
+        EC3R_CHECK_LAUNCH("vc_groups_kernel");
+    }
     const unsigned gc = (unsigned)std::min<int64_t>((nb * 16 + 255) / 256, (int64_t)kNumSMs * 16);
     vc_colpos_kernel<<<gc, 256, 0, st>>>(w.grp, w.colcnt, h->counters, nb, w.scan_in, w.colsrc);
     EC3R_CHECK_LAUNCH("vc_colpos_kernel");
@@ -1070,8 +1157,16 @@ static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsu
     EC3R_CHECK_LAUNCH("vc_gather_kernel");
     if (!read_count) return EC3R_OK;  // *n_out (device) holds U
     int64_t U = 0;
+    int bb[8];
     EC3R_CUDA_TRY(cudaMemcpyAsync(&U, n_out, sizeof(U), cudaMemcpyDeviceToHost, st));
+    EC3R_CUDA_TRY(cudaMemcpyAsync(bb, w.bb, sizeof(bb), cudaMemcpyDeviceToHost, st));
     EC3R_CUDA_TRY(cudaStreamSynchronize(st));
+    const bool fits = bb[0] > bb[3] || ((unsigned)(bb[3] - bb[0]) < (1u << VC_XB) &&
+                                        (unsigned)(bb[4] - bb[1]) < (1u << VC_YB) &&
+                                        (unsigned)(bb[5] - bb[2]) < (1u << VC_ZB));
+    h->emit_key32 = fits;
+    if (k32 && !fits)  // the map outgrew the 32-bit keys since the last emit: redo with 64-bit keys
+        return column_emit(h, keys, centroid, wsum, count, n_out, workspace, workspace_bytes, read_count, st);
     h->last_count = U;
     return EC3R_OK;
 }
@@ -1157,6 +1252,7 @@ extern "C" int ec3r_vhash_create_sized(ec3r_vhash** out, int64_t max_voxels, int
     if (!out || max_voxels < 2 || max_blocks < 1 || !(cell_size > 0)) return EC3R_EARG;
     ec3r_vhash* h = new ec3r_vhash();
     h->last_count = -1;
+    h->emit_key32 = false;
     h->bf = nullptr;
     h->bf_active = h->legacy_active = false;
     {

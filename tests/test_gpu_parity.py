@@ -330,6 +330,27 @@ def test_voxel_points_api_and_extreme_coordinates():
     assert np.max(np.abs(c - o["centroid"])) < 1e-3  # float32 output at 2 km
 
 
+def test_voxel_sorted_emit_key_widths():
+    """The sorted emit's block sort uses 32-bit relative keys once a fill's
+    extent is known to fit them (x, y < 2048 blocks, z < 1024) and falls back
+    to the 64-bit _pack keys when a later fill of the same map outgrows them:
+    keys, counts and centroids equal the oracle through all three fills."""
+    from paper_2510_02080_b200 import mapping
+    rng = np.random.default_rng(11)
+    vm = mapping.VoxelMap(0.02, 1 << 20)
+    sim = np.array([1.0, 1.0, 0, 0, 0, 0.0, 0.0, 0.0])
+    for spread in (2.0, 3.0, 60.0):  # 64-bit (first), 32-bit, then > 2048 blocks of 8 cm in x: 64-bit again
+        p = rng.normal(size=(50_000, 3)) * np.array([spread, 1.0, 0.5])
+        conf = rng.uniform(0.05, 1.0, size=len(p))
+        vm.clear()
+        vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"), sim)
+        k, c, w, n = (x.cpu().numpy() for x in vm.extract())
+        o = ofuse.fuse_points(p, conf, 0.02)
+        np.testing.assert_array_equal(k, o["keys"])
+        np.testing.assert_array_equal(n, o["count"])
+        assert np.max(np.abs(c - o["centroid"])) < 1e-4
+
+
 def test_voxel_partials_owner_buckets_and_merge_roundtrip():
     """Multi-GPU device half: extract_partials buckets every voxel by
     owner = mix64(key) mod n (dist.owner_of), and merging all buckets into a
