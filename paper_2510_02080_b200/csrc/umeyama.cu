@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -315,96 +316,71 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     const int e = blockIdx.x / UM_CL;
     const int s0 = a.edge_seg[e], s1 = a.edge_seg[e + 1];
     __shared__ double scratch[(UM_NT / 32) * 24];
-    __shared__ double part1[8], part2[24], part3[4];
-    __shared__ double tot1[8], tot2[24], tot3[4];
-    __shared__ float wmax_warp[UM_NT / 32];
-    __shared__ float part_wmax;
+    __shared__ double part2[24], part3[4];
+    __shared__ double tot2[24], tot3[4];
     __shared__ Solution sol;
     for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[col_ix(u, Wq)] = (u - a.cx) / a.fx;
     for (int v = threadIdx.x; v < a.H; v += UM_NT) yc[v] = (v - a.cy) / a.fy;
     __syncthreads();
     const int W = a.W;
 
-    // ---- phase 1: validity, max of w = min(conf_a, conf_b), rough centroids
-    float wmax = -1.0f;
-    double a1[7] = {0, 0, 0, 0, 0, 0, 0};
-    int cur_seg = -1;
-    float Ra[3][3], ta[3], Rb[3][3], tb[3];
-    for_each_pixel4(a, s0, s1, rank, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb,
-                                         float4 wb) {
-        if (sg != cur_seg) {
-            cur_seg = sg;
+    // ---- shift: fp64 mean of a fixed 8 x 8 sample of the first segment's
+    // valid pixels (identical in every CTA of the cluster), so the raw
+    // moments are centred before the single streaming pass; the sample's
+    // max w seeds the running floor bound below.
+    double shp[3], shq[3];
+    float wsamp;
+    {
+        __shared__ double smp[64][7];
+        __shared__ float smw[64];
+        const int sa = a.seg_slots[2 * s0], sb = a.seg_slots[2 * s0 + 1];
+        const size_t HW = (size_t)a.H * a.W;
+        if (threadIdx.x < 64) {
+            const int i = threadIdx.x >> 3, j = threadIdx.x & 7;
+            const int v = ((2 * i + 1) * a.H) / 16, u = ((2 * j + 1) * W) / 16;
+            const size_t px = (size_t)v * W + u;
+            const float zA = a.depth[(size_t)sa * HW + px], zB = a.depth[(size_t)sb * HW + px];
+            const float cA = a.conf[(size_t)sa * HW + px], cB = a.conf[(size_t)sb * HW + px];
+            const bool ok = zA > 0.f && zB > 0.f;
+            double R[3][3], t[3];
+            const double x = xc[col_ix(u, Wq)], y = yc[v];
+            load_rot(a.slot_poses + 8 * sa, R, t);
+            for (int k = 0; k < 3; ++k) smp[threadIdx.x][k] = ok ? zA * (R[k][0] * x + R[k][1] * y + R[k][2]) + t[k] : 0.0;
+            load_rot(a.slot_poses + 8 * sb, R, t);
+            for (int k = 0; k < 3; ++k)
+                smp[threadIdx.x][3 + k] = ok ? zB * (R[k][0] * x + R[k][1] * y + R[k][2]) + t[k] : 0.0;
+            smp[threadIdx.x][6] = ok ? 1.0 : 0.0;
+            smw[threadIdx.x] = ok ? fminf(cA, cB) : -1.0f;
+        }
+        __syncthreads();
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        float wm = -1.0f;
+        for (int k = 0; k < 64; ++k) {  // every thread, same order: no broadcast round
+            for (int c = 0; c < 7; ++c) acc[c] += smp[k][c];
+            wm = fmaxf(wm, smw[k]);
+        }
+        if (acc[6] > 0) {
+            for (int k = 0; k < 3; ++k) { shp[k] = acc[k] / acc[6]; shq[k] = acc[3 + k] / acc[6]; }
+        } else {  // no valid sample pixel: the first segment's frame origins
             double R[3][3], t[3];
             load_rot(a.slot_poses + 8 * sa, R, t);
-            for (int i = 0; i < 3; ++i) { ta[i] = (float)t[i]; for (int j = 0; j < 3; ++j) Ra[i][j] = (float)R[i][j]; }
+            for (int k = 0; k < 3; ++k) shp[k] = t[k];
             load_rot(a.slot_poses + 8 * sb, R, t);
-            for (int i = 0; i < 3; ++i) { tb[i] = (float)t[i]; for (int j = 0; j < 3; ++j) Rb[i][j] = (float)R[i][j]; }
+            for (int k = 0; k < 3; ++k) shq[k] = t[k];
         }
-        const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
-        const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
-        float sp[3] = {0, 0, 0}, sq[3] = {0, 0, 0};
-        int nv = 0;
-        int u0, v0;
-        pix_uv(a, pix, u0, v0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (zA[k] > 0.f && zB[k] > 0.f) {
-                int u = u0 + k, v = v0;
-                if (u >= W) pix_uv(a, pix + k, u, v);  // the group crosses a row end
-                const float x = (float)xc[col_ix(u, Wq)], y = (float)yc[v];
-                wmax = fmaxf(wmax, fminf(cA[k], cB[k]));
-                ++nv;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    sp[i] += zA[k] * (Ra[i][0] * x + Ra[i][1] * y + Ra[i][2]) + ta[i];
-                    sq[i] += zB[k] * (Rb[i][0] * x + Rb[i][1] * y + Rb[i][2]) + tb[i];
-                }
-            }
-        }
-        a1[0] += nv;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) { a1[1 + i] += sp[i]; a1[4 + i] += sq[i]; }
-    });
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-    if ((threadIdx.x & 31) == 0) wmax_warp[threadIdx.x >> 5] = wmax;
-    cta_sum<7>(a1, scratch, part1);
-    if (threadIdx.x == 0) {
-        float m = -1.0f;
-        for (int w = 0; w < UM_NT / 32; ++w) m = fmaxf(m, wmax_warp[w]);
-        part_wmax = m;
+        wsamp = wm;
     }
-    cl.sync();
-    if (threadIdx.x < 7) {
-        double r = 0;
-        for (int c = 0; c < UM_CL; ++c) r += cl.map_shared_rank(part1, c)[threadIdx.x];
-        tot1[threadIdx.x] = r;
-    } else if (threadIdx.x == 7) {
-        float m = -1.0f;
-        for (int c = 0; c < UM_CL; ++c) m = fmaxf(m, *cl.map_shared_rank(&part_wmax, c));
-        tot1[7] = (double)m;
-    }
-    __syncthreads();
-    const double nvalid = tot1[0];
-    if (rank == 0 && threadIdx.x == 0) out_npairs[e] = (int64_t)nvalid;
-    if (nvalid < a.min_corr) {  // mapping.py:174
-        if (rank == 0 && threadIdx.x == 0) { out_status[e] = EC3R_ST_SKIP; out_count[e] = 0; }
-        cl.sync();
-        return;
-    }
-    // floor = frac * float(w.max())  (mapping.py:176), exact in float64
-    const double floorv = __dmul_rn(a.floor_frac, tot1[7]);
-    double shp[3], shq[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) { shp[i] = tot1[1 + i] / nvalid; shq[i] = tot1[4 + i] / nvalid; }
 
-    // ---- phase 2: keep = w >= floor; shifted float64 raw moments
-    // Per segment, the two frames' float64 affine maps live in shared tables
-    // (point = z * (col[u] + row[v]) + t), not in registers: 24 float64
-    // accumulators + two rotations would cap the kernel at one CTA per SM.
-    double a2[24];
-#pragma unroll
-    for (int k = 0; k < 24; ++k) a2[k] = 0;
+    // ---- single pass: validity count, max w, and the shifted float64 raw
+    // moments of every pixel that is certainly kept.  keep = w >= floor with
+    // floor = frac * max(w) (mapping.py:176-177) is only known after the
+    // pass, but confidences lie in [0, 1] (backend.py:51-58, :262), so
+    // max(w) <= 1 and every w >= tau = frac * 1 is kept; a w below
+    // frac * (running max) is certainly dropped.  The few pixels in between
+    // are listed per thread and settled once the floor is known.  Inputs
+    // outside the contract (max(w) > 1) or a full list re-run the two-pass
+    // form (uniform decision in the cluster), so the result never depends
+    // on the bound.
     double* colA = yc + a.H;          // [3][4 Wq] (col_ix layout)
     double* rowA = colA + 3 * Wp;     // [3][H]
     double* colB = rowA + 3 * a.H;    // [3][4 Wq]
@@ -429,54 +405,167 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             tAB[3 + threadIdx.x] = tb_[threadIdx.x] - shq[threadIdx.x];
         }
     };
-    for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
-                                                     float4 zb, float4 wb) {
-        const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
-        const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
-        uint32_t kbits = 0;
-        int u0, v0;
-        pix_uv(a, pix, u0, v0);
+    double a2[24];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool valid = zA[k] > 0.f && zB[k] > 0.f;
-            const float wf = fminf(cA[k], cB[k]);
-            const bool keep = valid && ((double)wf >= floorv);  // mapping.py:177
-            if (keep) {
-                kbits |= 1u << (8 * k);
-                int u = u0 + k, v = v0;
-                if (u >= W) pix_uv(a, pix + k, u, v);
-                const int cu = col_ix(u, Wq);
-                const double wi = (double)wf;
-                const double zaa = zA[k], zbb = zB[k];
-                double pp[3], qq[3];
+    for (int k = 0; k < 24; ++k) a2[k] = 0;
+    auto add_moments = [&](double wi, const double (&pp)[3], const double (&qq)[3]) {
+        a2[0] += wi;
+        a2[1] += 1.0;
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    pp[i] = zaa * (colA[i * Wp + cu] + rowA[i * a.H + v]) + tAB[i];
-                    qq[i] = zbb * (colB[i * Wp + cu] + rowB[i * a.H + v]) + tAB[3 + i];
+        for (int i = 0; i < 3; ++i) {
+            const double wp = wi * pp[i];
+            a2[2 + i] += wp;
+            a2[5 + i] += wi * qq[i];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) a2[8 + 3 * j + i] += wp * qq[j];  // sum w q_j p_i
+        }
+        const double wp0 = wi * pp[0], wp1 = wi * pp[1], wp2 = wi * pp[2];
+        a2[17] += wp0 * pp[0]; a2[18] += wp0 * pp[1]; a2[19] += wp0 * pp[2];
+        a2[20] += wp1 * pp[1]; a2[21] += wp1 * pp[2]; a2[22] += wp2 * pp[2];
+        a2[23] += wi * (qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2]);
+    };
+    // one moment-pass body: keep(valid, wf) decides per pixel; 'unc' pixels
+    // (single pass only) go to the thread's list
+    constexpr int kUnc = 4;
+    __shared__ int2 unc_list[UM_NT][kUnc];
+    int n_unc = 0;
+    bool unc_full = false;
+    // float thresholds: (double)w >= d  <=>  w >= float_ru(d) for float w
+    const float tau_f = __double2float_ru(__dmul_rn(a.floor_frac, 1.0));
+    float m_run = wsamp;
+    float lo_f = m_run > 0.f ? __double2float_ru(__dmul_rn(a.floor_frac, (double)m_run)) : 0.f;
+    int nvalid_t = 0;
+    auto pass = [&](auto single_c, float floor_f) {
+        constexpr bool single = decltype(single_c)::value;
+        for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
+                                                         float4 zb, float4 wb) {
+            const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
+            const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
+            uint32_t kbits = 0;
+            int u0, v0;
+            pix_uv(a, pix, u0, v0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool valid = zA[k] > 0.f && zB[k] > 0.f;
+                const float wf = fminf(cA[k], cB[k]);
+                bool keep;
+                if constexpr (single) {
+                    nvalid_t += valid;
+                    if (valid && wf > m_run) {
+                        m_run = wf;
+                        lo_f = __double2float_ru(__dmul_rn(a.floor_frac, (double)wf));
+                    }
+                    keep = valid && wf >= tau_f;
+                    if (valid && !keep && !(wf < lo_f)) {
+                        if (n_unc < kUnc) unc_list[threadIdx.x][n_unc++] = make_int2(sg, pix + k);
+                        else unc_full = true;
+                    }
+                } else {
+                    keep = valid && wf >= floor_f;  // mapping.py:177
                 }
-                a2[0] += wi;
-                a2[1] += 1.0;
+                if (keep) {
+                    kbits |= 1u << (8 * k);
+                    int u = u0 + k, v = v0;
+                    if (u >= W) pix_uv(a, pix + k, u, v);
+                    const int cu = col_ix(u, Wq);
+                    const double zaa = zA[k], zbb = zB[k];
+                    double pp[3], qq[3];
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const double wp = wi * pp[i];
-                    a2[2 + i] += wp;
-                    a2[5 + i] += wi * qq[i];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) a2[8 + 3 * j + i] += wp * qq[j];  // sum w q_j p_i
+                    for (int i = 0; i < 3; ++i) {
+                        pp[i] = zaa * (colA[i * Wp + cu] + rowA[i * a.H + v]) + tAB[i];
+                        qq[i] = zbb * (colB[i * Wp + cu] + rowB[i * a.H + v]) + tAB[3 + i];
+                    }
+                    add_moments((double)wf, pp, qq);
                 }
-                const double wp0 = wi * pp[0], wp1 = wi * pp[1], wp2 = wi * pp[2];
-                a2[17] += wp0 * pp[0]; a2[18] += wp0 * pp[1]; a2[19] += wp0 * pp[2];
-                a2[20] += wp1 * pp[1]; a2[21] += wp1 * pp[2]; a2[22] += wp2 * pp[2];
-                a2[23] += wi * (qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2]);
             }
+            if (keep_masks) {
+                const int HW = a.H * a.W;
+                uint8_t* km = keep_masks + (size_t)sg * HW + pix;
+                if (((HW & 3) == 0)) *reinterpret_cast<uint32_t*>(km) = kbits;
+                else for (int k = 0; k < 4 && pix + k < HW; ++k) km[k] = (kbits >> (8 * k)) & 1;
+            }
+        });
+    };
+    pass(std::true_type{}, 0.f);
+
+    // cluster totals of the pass: valid count, max w, list overflow
+    float wmax = m_run;
+    unsigned full = unc_full ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        nvalid_t += __shfl_xor_sync(0xffffffffu, nvalid_t, o);
+        full |= __shfl_xor_sync(0xffffffffu, full, o);
+    }
+    __shared__ float wmax_warp[UM_NT / 32];
+    __shared__ int nv_warp[UM_NT / 32];
+    __shared__ unsigned full_warp[UM_NT / 32];
+    __shared__ double part1[3];
+    __shared__ double tot1[3];
+    if ((threadIdx.x & 31) == 0) {
+        wmax_warp[threadIdx.x >> 5] = wmax;
+        nv_warp[threadIdx.x >> 5] = nvalid_t;
+        full_warp[threadIdx.x >> 5] = full;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = -1.0f;
+        long long nv = 0;
+        unsigned f = 0;
+        for (int w = 0; w < UM_NT / 32; ++w) { m = fmaxf(m, wmax_warp[w]); nv += nv_warp[w]; f |= full_warp[w]; }
+        part1[0] = (double)nv;
+        part1[1] = (double)m;
+        part1[2] = (double)f;
+    }
+    cl.sync();
+    if (threadIdx.x == 0) {
+        double nv = 0, m = -1.0, f = 0;
+        for (int c = 0; c < UM_CL; ++c) {
+            const double* pc = cl.map_shared_rank(part1, c);
+            nv += pc[0];
+            m = fmax(m, pc[1]);
+            f = fmax(f, pc[2]);
         }
-        if (keep_masks) {
-            const int HW = a.H * a.W;
-            uint8_t* km = keep_masks + (size_t)sg * HW + pix;
-            if (((HW & 3) == 0)) *reinterpret_cast<uint32_t*>(km) = kbits;
-            else for (int k = 0; k < 4 && pix + k < HW; ++k) km[k] = (kbits >> (8 * k)) & 1;
+        tot1[0] = nv; tot1[1] = m; tot1[2] = f;
+    }
+    __syncthreads();
+    const double nvalid = tot1[0];
+    if (rank == 0 && threadIdx.x == 0) out_npairs[e] = (int64_t)nvalid;
+    if (nvalid < a.min_corr) {  // mapping.py:174
+        if (rank == 0 && threadIdx.x == 0) { out_status[e] = EC3R_ST_SKIP; out_count[e] = 0; }
+        cl.sync();
+        return;
+    }
+    // floor = frac * float(w.max())  (mapping.py:176), exact in float64
+    const double floorv = __dmul_rn(a.floor_frac, tot1[1]);
+    if (tot1[2] != 0.0 || !(tot1[1] <= 1.0)) {
+        // outside the single-pass bound: the two-pass form (moments of every
+        // w >= floor from scratch; rewrites the keep mask)
+#pragma unroll
+        for (int k = 0; k < 24; ++k) a2[k] = 0;
+        pass(std::false_type{}, __double2float_ru(floorv));
+    } else {
+        // settle the thread's listed pixels (exact float64 chain, own order)
+        const size_t HW = (size_t)a.H * a.W;
+        for (int i = 0; i < n_unc; ++i) {
+            const int2 ent = unc_list[threadIdx.x][i];
+            const int sa = a.seg_slots[2 * ent.x], sb = a.seg_slots[2 * ent.x + 1];
+            const float cA = a.conf[(size_t)sa * HW + ent.y], cB = a.conf[(size_t)sb * HW + ent.y];
+            const float wf = fminf(cA, cB);
+            if (!((double)wf >= floorv)) continue;
+            const float zA = a.depth[(size_t)sa * HW + ent.y], zB = a.depth[(size_t)sb * HW + ent.y];
+            int u, v;
+            pix_uv(a, ent.y, u, v);
+            const double x = xc[col_ix(u, Wq)], y = yc[v];
+            double R[3][3], t[3], pp[3], qq[3];
+            load_rot(a.slot_poses + 8 * sa, R, t);
+            for (int k = 0; k < 3; ++k) pp[k] = (double)zA * (R[k][0] * x + R[k][2] + R[k][1] * y) + (t[k] - shp[k]);
+            load_rot(a.slot_poses + 8 * sb, R, t);
+            for (int k = 0; k < 3; ++k) qq[k] = (double)zB * (R[k][0] * x + R[k][2] + R[k][1] * y) + (t[k] - shq[k]);
+            add_moments((double)wf, pp, qq);
+            if (keep_masks) keep_masks[(size_t)ent.x * HW + ent.y] = 1;
         }
-    });
+    }
     cta_sum<24>(a2, scratch, part2);
     cluster_sum<24>(cl, part2, tot2);
     const double Wsum = tot2[0], nkeep = tot2[1];

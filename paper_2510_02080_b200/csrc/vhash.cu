@@ -284,6 +284,34 @@ __global__ void vh_frame_tables_kernel(FrameGeom a, float4* __restrict__ ftab) {
 // ~300 G when a warp's lanes hit consecutive voxels), and the sweep order
 // (frame-major ... all frames interleaved) and pool working set changed the
 // time by < 10%, so the pool's L2 residency is not the limiter.
+#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
+// experiment: log every run's reduction (vid, sums, count) in issue order, then
+// replay the log as pure reductions: the atomic floor of this address stream
+__device__ float4* g_log_sums;
+__device__ uint2* g_log_vid;
+__device__ unsigned long long g_log_n, g_log_cap;
+__device__ __forceinline__ void exp_log_run(uint32_t vid, float x, float y, float z, float w, uint32_t n) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(&g_log_n, (unsigned long long)g.size());
+    const unsigned long long i = g.shfl(base, 0) + g.thread_rank();
+    if (i < g_log_cap) {
+        g_log_sums[i] = make_float4(x, y, z, w);
+        g_log_vid[i] = make_uint2(vid, n);
+    }
+}
+__global__ void exp_replay_kernel(float4* __restrict__ sums, unsigned int* __restrict__ counts, int with_count) {
+    const unsigned long long n = min(g_log_n, g_log_cap);
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        // with_count & 2: replay the addresses only (constant payload, 8 B of log per run)
+        const uint2 v = __ldcs(g_log_vid + i);
+        const float4 s = (with_count & 2) ? make_float4(1e-3f, 1e-3f, 1e-3f, 0.5f) : __ldcs(g_log_sums + i);
+        red_add_v4(sums + v.x, s.x, s.y, s.z, s.w);
+        if (with_count & 1) red_add_u32(counts + v.x, v.y);
+    }
+}
+#endif
 constexpr int ST_H = 8, ST_W = 16;
 #ifndef EC3R_BC_BITS
 #define EC3R_BC_BITS 11
@@ -418,6 +446,46 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 }
             }
         }
+#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 1
+        // experiment: keys only
+#pragma unroll
+        for (int k = 0; k < 4; ++k) n_oor += (unsigned)(cx[k] ^ cy[k] ^ cz[k]) & (valid[k] ? 1u : 0u);
+        continue;
+#endif
+#if defined(EC3R_FI_EXP) && (EC3R_FI_EXP == 3 || EC3R_FI_EXP == 4)
+        // experiment: one read-only directory load per pixel instead of the cache / table
+        {
+            uint32_t vidx[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t hb = (uint32_t)table_slot(pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2), 0xFFFFFFFFull) % 100000u;
+                const uint32_t g = __ldg(a.vb.block_slot + hb);
+                vidx[k] = valid[k] ? (((hb ^ (g & 1u)) << 6) | (uint32_t)((cx[k] & 3) | ((cy[k] & 3) << 2) | ((cz[k] & 3) << 4))) : 0xFFFFFFFFu;
+            }
+#if EC3R_FI_EXP == 4
+#pragma unroll
+            for (int k = 0; k < 4; ++k) n_oor += vidx[k] & 1u;
+#else
+            float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f, qn = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float c = cs[k];
+                const float cont = (k > 0 && vidx[k] == vidx[k - 1]) ? 1.f : 0.f;
+                qx = fmaf(cont, qx, c * (ox[k] - (float)cx[k] * cellf));
+                qy = fmaf(cont, qy, c * (oy[k] - (float)cy[k] * cellf));
+                qz = fmaf(cont, qz, c * (oz[k] - (float)cz[k] * cellf));
+                qw = fmaf(cont, qw, c);
+                qn = fmaf(cont, qn, 1.f);
+                const bool last = vidx[k] != 0xFFFFFFFFu && (k == 3 || vidx[k + 1 < 4 ? k + 1 : 3] != vidx[k]);
+                if (last) {
+                    red_add_v4(a.vb.sums + vidx[k], qx, qy, qz, qw);
+                    red_add_u32(a.vb.counts + vidx[k], (uint32_t)qn);
+                }
+            }
+#endif
+        }
+        continue;
+#endif
         // phase B: block indices.  The CTA's shared-memory block cache maps
         // an exact 30-bit block key relative to the frame's camera block to
         // the pool block; the four lookups of a lane are independent LDS.64.
@@ -482,6 +550,11 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 if (miss[k]) got[k] = g;
             }
         }
+#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 2
+#pragma unroll
+        for (int k = 0; k < 4; ++k) n_oor += (unsigned)got[k] & 1u;
+        continue;
+#endif
         // phase C: reductions into the pool.  Consecutive pixels of the lane
         // in the same voxel form a run whose sums ride along (FFMA with a
         // 0/1 continuation flag); only a run's last pixel issues the two
@@ -504,8 +577,12 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             rn = fmaf(cont, rn, 1.f);
             const bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
             if (last) {
+#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
+                exp_log_run(vid[k], rx, ry, rz, rw, (uint32_t)rn);
+#else
                 red_add_v4(a.vb.sums + vid[k], rx, ry, rz, rw);
                 red_add_u32(a.vb.counts + vid[k], (uint32_t)rn);
+#endif
             }
         }
     }
@@ -1635,3 +1712,29 @@ extern "C" int ec3r_vhash_stats_device(ec3r_vhash* h, int64_t* out5, void* strea
     EC3R_CHECK_LAUNCH("vb_stats_dev_kernel");
     return EC3R_OK;
 }
+
+#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
+extern "C" __attribute__((visibility("default"))) int ec3r_exp_log_alloc(long long cap) {
+    float4* a; uint2* b;
+    if (cudaMalloc(&a, 16 * (size_t)cap) != cudaSuccess || cudaMalloc(&b, 8 * (size_t)cap) != cudaSuccess) return -1;
+    unsigned long long z = 0, c = (unsigned long long)cap;
+    cudaMemcpyToSymbol(ec3r::g_log_sums, &a, sizeof(a));
+    cudaMemcpyToSymbol(ec3r::g_log_vid, &b, sizeof(b));
+    cudaMemcpyToSymbol(ec3r::g_log_n, &z, sizeof(z));
+    cudaMemcpyToSymbol(ec3r::g_log_cap, &c, sizeof(c));
+    return 0;
+}
+extern "C" __attribute__((visibility("default"))) long long ec3r_exp_log_count() {
+    unsigned long long n = 0;
+    cudaMemcpyFromSymbol(&n, ec3r::g_log_n, sizeof(n));
+    return (long long)n;
+}
+extern "C" __attribute__((visibility("default"))) int ec3r_exp_log_reset() {
+    unsigned long long z = 0;
+    return cudaMemcpyToSymbol(ec3r::g_log_n, &z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+extern "C" __attribute__((visibility("default"))) int ec3r_exp_replay(ec3r_vhash* h, int grid, int with_count) {
+    ec3r::exp_replay_kernel<<<grid, 256>>>(h->sums, h->counts, with_count);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -795,6 +795,61 @@ def test_registration_full_resolution_edges_vs_oracle():
         assert abs(r.rms - e["rms"]) <= 1e-5 * max(1.0, e["rms"])
 
 
+@pytest.mark.parametrize("kind", ["listed", "over_one", "uniform"])
+def test_registration_single_pass_bound_paths(kind):
+    """The single-pass registration (keep = w >= 0.1 max w decided during the
+    pass from the [0, 1] confidence bound) against the oracle on inputs that
+    take each of its paths: 'listed' (max w ~ 0.7 and sparse pixels between
+    the final floor and 0.1: settled from the per-thread lists), 'over_one'
+    (confidences up to 2: the two-pass re-run) and 'uniform' (uniform
+    confidences: lists overflow, two-pass re-run).  Counts, statuses and keep
+    masks exact, Sim(3) within 1e-5 (mapping.py:162-188)."""
+    from paper_2510_02080_b200 import mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(21, cfg, seed=4, device="cuda")
+    conf = sb.conf.clone()
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    if kind == "listed":
+        conf *= 0.7
+        n = conf[0].numel()
+        for f in range(conf.shape[0]):
+            idx = torch.randint(0, n, (400,), generator=gen, device="cuda")
+            vals = torch.where(torch.arange(400, device="cuda") % 2 == 0, 0.08, 0.05).to(conf.dtype)
+            conf[f].view(-1)[idx] = torch.where(sb.depth[f].view(-1)[idx] > 0, vals, conf[f].view(-1)[idx])
+    elif kind == "over_one":
+        conf *= 2.0
+    else:
+        conf = torch.where(sb.depth > 0, torch.rand(conf.shape, generator=gen, device="cuda"), conf)
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms = [dm.add_submap(ids, sb.depth[o:o + len(ids)], conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    pairs = [(sms[j], sms[j - 1]) for j in range(1, len(sms))]
+    res, km = mapping.register_edges(dm.pool, pairs, with_keep_masks=True)
+    km = km.cpu().numpy()
+    dense = []
+    for ids, o in zip(sb.frame_ids, sb.slot_offsets):
+        F = len(ids)
+        dense.append(dict(depth=sb.depth[o:o + F].cpu().numpy(), conf=conf[o:o + F].cpu().numpy(),
+                          frame_ids=np.array(ids), pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:],
+                          K=sb.K4))
+    assert len(res) >= 3
+    for j, r in zip(range(1, len(sms)), res):
+        e = ref.registration_edge(dense[j], dense[j - 1])
+        assert e["status"] == ref.STATUS_OK and r.status == 0, (j, e["status"], r.status)
+        assert r.count == e["count"], (j, r.count, e["count"])
+        sh = [i for i, kf in enumerate(dense[j]["frame_ids"]) if kf in list(dense[j - 1]["frame_ids"])][0]
+        fb = list(dense[j - 1]["frame_ids"]).index(dense[j]["frame_ids"][sh])
+        both = (dense[j]["depth"][sh] > 0) & (dense[j - 1]["depth"][fb] > 0)
+        np.testing.assert_array_equal(km[j - 1][both].astype(bool), e["keep"])
+        if kind == "listed":
+            assert (~e["keep"]).any() and e["keep"][np.minimum(dense[j]["conf"][sh], dense[j - 1]["conf"][fb])[both]
+                                                   < 0.1].any()
+        tr = r.transform
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, e["s"], e["q"], e["t"])
+        assert abs(r.rms - e["rms"]) <= 1e-5 * max(1.0, e["rms"])
+
+
 # --------------------------------------------------------------------------
 # K9 (§8f rank 4): batched homography RANSAC
 
