@@ -223,6 +223,7 @@ struct PoolArgs {
     double floor_frac;
     int min_corr, with_scale;
     float inv_w;  // 1/W for the division-free row split (images < 2^21 pixels)
+    int use_tma;  // planes 16-byte aligned and H*W % 4 == 0: TMA-staged walk
 };
 
 // Row / column of pixel px without an integer division: floor((px + 1/2) / W)
@@ -295,6 +296,80 @@ __device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, i
     }
 }
 
+// The same walk with the four planes staged in shared memory by TMA bulk
+// copies: a ring of RE_NS stages of 4 x 4 KB (one visit of the CTA: 1,024
+// pixels per plane), RE_NS - 1 visits in flight, one mbarrier per stage.
+// Planes must be 16-byte aligned with H*W % 4 == 0 (checked by the caller).
+constexpr int RE_NS = 3;
+constexpr int RE_CHUNK = 4 * UM_NT;  // pixels per plane per visit
+struct Ring {
+    float* buf;          // [RE_NS][4][RE_CHUNK]
+    uint64_t* bar;       // [RE_NS]
+    uint32_t parity;     // bit s: next wait parity of stage s
+    int next;            // stage of the next visit
+};
+
+__device__ __forceinline__ uint32_t re_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <class S, class F>
+__device__ __forceinline__ void for_each_pixel4_seg_tma(const PoolArgs& a, int s0, int s1, int rank, Ring& rg,
+                                                        S&& seg_fn, F&& f) {
+    const int HW = a.H * a.W;
+    constexpr int kStride = 4 * UM_CL * UM_NT;
+    const int base0 = 4 * rank * UM_NT;
+    const int n_it = base0 < HW ? (HW - base0 + kStride - 1) / kStride : 0;
+    for (int sg = s0; sg < s1; ++sg) {
+        const int sa = a.seg_slots[2 * sg], sb = a.seg_slots[2 * sg + 1];
+        __syncthreads();
+        seg_fn(sa, sb);
+        __syncthreads();
+        const float* src[4] = {a.depth + (size_t)sa * HW, a.conf + (size_t)sa * HW, a.depth + (size_t)sb * HW,
+                               a.conf + (size_t)sb * HW};
+        auto issue = [&](int it, int st) {
+            const int pb = base0 + it * kStride;
+            const uint32_t bytes = 4u * (uint32_t)min(RE_CHUNK, HW - pb);
+            const uint32_t bar = re_smem_u32(rg.bar + st);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(4u * bytes)
+                         : "memory");
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        re_smem_u32(rg.buf + (st * 4 + pl) * RE_CHUNK)),
+                    "l"(src[pl] + pb), "r"(bytes), "r"(bar)
+                    : "memory");
+        };
+        if (threadIdx.x == 0)
+            for (int j = 0; j < min(RE_NS, n_it); ++j) issue(j, (rg.next + j) % RE_NS);
+        for (int it = 0; it < n_it; ++it) {
+            const int st = rg.next;
+            rg.next = (st + 1 == RE_NS) ? 0 : st + 1;
+            const uint32_t par = (rg.parity >> st) & 1u;
+            rg.parity ^= 1u << st;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "RE_WAIT_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra RE_WAIT_%=;\n"
+                "}\n" ::"r"(re_smem_u32(rg.bar + st)),
+                "r"(par)
+                : "memory");
+            const int pix = base0 + it * kStride + 4 * threadIdx.x;
+            if (pix < HW) {
+                const float* b = rg.buf + st * 4 * RE_CHUNK + 4 * threadIdx.x;
+                const float4 za = *reinterpret_cast<const float4*>(b);
+                const float4 wa = *reinterpret_cast<const float4*>(b + RE_CHUNK);
+                const float4 zb = *reinterpret_cast<const float4*>(b + 2 * RE_CHUNK);
+                const float4 wb = *reinterpret_cast<const float4*>(b + 3 * RE_CHUNK);
+                f(sg, sa, sb, pix, za, wa, zb, wb);
+            }
+            __syncthreads();  // stage st is free again
+            if (threadIdx.x == 0 && it + RE_NS < n_it) issue(it + RE_NS, st);
+        }
+    }
+}
+
 template <typename F>
 __device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s1, int rank, F&& f) {
     for_each_pixel4_seg(a, s0, s1, rank, [](int, int) {}, f);
@@ -321,6 +396,19 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     __shared__ Solution sol;
     for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[col_ix(u, Wq)] = (u - a.cx) / a.fx;
     for (int v = threadIdx.x; v < a.H; v += UM_NT) yc[v] = (v - a.cy) / a.fy;
+    // TMA ring after the tables (xc, yc, 2 x (col, row) = 7 (H + Wp) doubles)
+    __shared__ __align__(8) uint64_t ring_bar[RE_NS];
+    Ring rg;
+    rg.buf = reinterpret_cast<float*>(tabs + 7 * (a.H + Wp));
+    rg.bar = ring_bar;
+    rg.parity = 0;
+    rg.next = 0;
+    const bool use_tma = a.use_tma != 0;
+    if (threadIdx.x == 0 && use_tma) {
+        for (int st = 0; st < RE_NS; ++st)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(re_smem_u32(ring_bar + st)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const int W = a.W;
 
@@ -331,8 +419,9 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     double shp[3], shq[3];
     float wsamp;
     {
-        __shared__ double smp[64][7];
-        __shared__ float smw[64];
+        // scratch in the (not yet used) ring memory
+        double (*smp)[7] = reinterpret_cast<double (*)[7]>(tabs + 7 * (a.H + Wp));
+        float* smw = reinterpret_cast<float*>(tabs + 7 * (a.H + Wp) + 64 * 7);
         const int sa = a.seg_slots[2 * s0], sb = a.seg_slots[2 * s0 + 1];
         const size_t HW = (size_t)a.H * a.W;
         if (threadIdx.x < 64) {
@@ -353,14 +442,20 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             smw[threadIdx.x] = ok ? fminf(cA, cB) : -1.0f;
         }
         __syncthreads();
-        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        float wm = -1.0f;
-        for (int k = 0; k < 64; ++k) {  // every thread, same order: no broadcast round
-            for (int c = 0; c < 7; ++c) acc[c] += smp[k][c];
-            wm = fmaxf(wm, smw[k]);
+        __shared__ double shift_sh[7];
+        if (threadIdx.x < 7) {  // column sums in sample order
+            double acc = 0;
+            for (int k = 0; k < 64; ++k) acc += smp[k][threadIdx.x];
+            shift_sh[threadIdx.x] = acc;
+        } else if (threadIdx.x == 32) {
+            float wm = -1.0f;
+            for (int k = 0; k < 64; ++k) wm = fmaxf(wm, smw[k]);
+            smw[64] = wm;
         }
-        if (acc[6] > 0) {
-            for (int k = 0; k < 3; ++k) { shp[k] = acc[k] / acc[6]; shq[k] = acc[3 + k] / acc[6]; }
+        __syncthreads();
+        const double cnt = shift_sh[6];
+        if (cnt > 0) {
+            for (int k = 0; k < 3; ++k) { shp[k] = shift_sh[k] / cnt; shq[k] = shift_sh[3 + k] / cnt; }
         } else {  // no valid sample pixel: the first segment's frame origins
             double R[3][3], t[3];
             load_rot(a.slot_poses + 8 * sa, R, t);
@@ -368,7 +463,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             load_rot(a.slot_poses + 8 * sb, R, t);
             for (int k = 0; k < 3; ++k) shq[k] = t[k];
         }
-        wsamp = wm;
+        wsamp = smw[64];
     }
 
     // ---- single pass: validity count, max w, and the shifted float64 raw
@@ -437,8 +532,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     int nvalid_t = 0;
     auto pass = [&](auto single_c, float floor_f) {
         constexpr bool single = decltype(single_c)::value;
-        for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
-                                                         float4 zb, float4 wb) {
+        auto body = [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb, float4 wb) {
             const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
             const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
             uint32_t kbits = 0;
@@ -484,7 +578,9 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
                 if (((HW & 3) == 0)) *reinterpret_cast<uint32_t*>(km) = kbits;
                 else for (int k = 0; k < 4 && pix + k < HW; ++k) km[k] = (kbits >> (8 * k)) & 1;
             }
-        });
+        };
+        if (use_tma) for_each_pixel4_seg_tma(a, s0, s1, rank, rg, build, body);
+        else for_each_pixel4_seg(a, s0, s1, rank, build, body);
     };
     pass(std::true_type{}, 0.f);
 
@@ -567,15 +663,25 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         }
     }
     cta_sum<24>(a2, scratch, part2);
-    cluster_sum<24>(cl, part2, tot2);
+    // only rank 0 finishes the edge: it sums the published partials in rank
+    // order, and once it has read them the other CTAs leave (their SMs take
+    // the next edges while rank 0 runs the serial closed form)
+    cl.sync();
+    if (rank == 0 && threadIdx.x < 24) {
+        double r = 0;
+        for (int c = 0; c < UM_CL; ++c) r += cl.map_shared_rank(part2, c)[threadIdx.x];
+        tot2[threadIdx.x] = r;
+    }
+    cl.sync();
+    if (rank != 0) return;
+    __syncthreads();
     const double Wsum = tot2[0], nkeep = tot2[1];
     int early = 0;
     if (nkeep < a.min_corr) early = EC3R_ST_SKIP;       // mapping.py:178
     else if (nkeep < 3) early = EC3R_ST_TOO_FEW;         // registration.py:59
     else if (!(Wsum > 0)) early = EC3R_ST_ALL_ZERO;      // registration.py:68
     if (early) {
-        if (rank == 0 && threadIdx.x == 0) { out_status[e] = early; out_count[e] = (int64_t)nkeep; }
-        cl.sync();
+        if (threadIdx.x == 0) { out_status[e] = early; out_count[e] = (int64_t)nkeep; }
         return;
     }
     // the closed form: thread 32 decomposes the source moments while thread 0
@@ -626,8 +732,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         double v0[3], v1[3];
         for (int i = 0; i < 3; ++i) { v0[i] = sol.src_V[i][0]; v1[i] = sol.src_V[i][1]; }
         double a3[2] = {0, 0};
-        for_each_pixel4_seg(a, s0, s1, rank, build, [&](int sg, int sa, int sb, int pix, float4 za, float4 wa,
-                                                         float4 zb, float4 wb) {
+        auto eig_body = [&](int sg, int sa, int sb, int pix, float4 za, float4 wa, float4 zb, float4 wb) {
             const float zA[4] = {za.x, za.y, za.z, za.w}, cA[4] = {wa.x, wa.y, wa.z, wa.w};
             const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
             for (int k = 0; k < 4; ++k) {
@@ -645,14 +750,18 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
                     a3[1] += wf * y1 * y1;
                 }
             }
-        });
+        };
+        // rank 0 alone (the others have left): every rank's share in turn
+        for (int r = 0; r < UM_CL; ++r) {
+            if (use_tma) for_each_pixel4_seg_tma(a, s0, s1, r, rg, build, eig_body);
+            else for_each_pixel4_seg(a, s0, s1, r, build, eig_body);
+        }
         __syncthreads();
-        cta_sum<2>(a3, scratch, part3);
-        cluster_sum<2>(cl, part3, tot3 + 2);  // tot3[2..3]; tot3[0..1] no longer needed
+        cta_sum<2>(a3, scratch, tot3 + 2);  // tot3[2..3]; tot3[0..1] no longer needed
         const double sv0 = sqrt(fmax(tot3[2] / Wsum, 0.0)), sv1 = sqrt(fmax(tot3[3] / Wsum, 0.0));
         degenerate = src_degenerate(fmax(sv0, sv1), fmin(sv0, sv1));
     }
-    if (rank == 0 && threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
         int st = sol.status;
         if (degenerate) st = EC3R_ST_DEGENERATE;
         out_status[e] = st;
@@ -660,7 +769,6 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
         write_sim3(out_sim3 + 8 * e, sol);
         out_rms[e] = sqrt(sol.rms2_closed);
     }
-    cl.sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -903,7 +1011,13 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
     a.floor_frac = floor_frac; a.min_corr = min_corr; a.with_scale = with_scale;
     a.inv_w = (int64_t)H * W < (1 << 21) ? 1.0f / (float)W : 0.f;
     const size_t Wp = 4 * (size_t)((W + 3) / 4);
-    const size_t smem = sizeof(double) * 7 * (size_t)(H + Wp);  // xc, yc + two frames' col/row tables
+    a.use_tma = ((int64_t)H * W % 4 == 0) &&
+                ((reinterpret_cast<uintptr_t>(depth_pool) | reinterpret_cast<uintptr_t>(conf_pool)) & 15) == 0 &&
+                getenv("EC3R_RE_NOTMA") == nullptr;
+    // xc, yc + two frames' col/row tables, then the TMA ring (which also holds
+    // the 64-pixel shift sample: 64 x 7 doubles + 64 floats)
+    const size_t ring = std::max(sizeof(float) * RE_NS * 4 * RE_CHUNK, sizeof(double) * 64 * 8 + 4);
+    const size_t smem = sizeof(double) * 7 * (size_t)(H + Wp) + ring;
     if (smem > 48 * 1024) {
         EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
