@@ -224,6 +224,7 @@ struct PoolArgs {
     int min_corr, with_scale;
     float inv_w;  // 1/W for the division-free row split (images < 2^21 pixels)
     int use_tma;  // planes 16-byte aligned and H*W % 4 == 0: TMA-staged walk
+    int ncl;      // CTAs per edge (the cluster size of the launch)
 };
 
 // Row / column of pixel px without an integer division: floor((px + 1/2) / W)
@@ -283,7 +284,7 @@ __device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, i
         };
         // the next visit's four 16-byte loads are in flight while this one
         // is reduced
-        constexpr int kStride = 4 * UM_CL * UM_NT;
+        const int kStride = 4 * a.ncl * UM_NT;
         int pix = 4 * (rank * UM_NT + threadIdx.x);
         float4 za, wa, zb, wb;
         if (pix < HW) load(pix, za, wa, zb, wb);
@@ -300,7 +301,10 @@ __device__ __forceinline__ void for_each_pixel4_seg(const PoolArgs& a, int s0, i
 // copies: a ring of RE_NS stages of 4 x 4 KB (one visit of the CTA: 1,024
 // pixels per plane), RE_NS - 1 visits in flight, one mbarrier per stage.
 // Planes must be 16-byte aligned with H*W % 4 == 0 (checked by the caller).
-constexpr int RE_NS = 3;
+#ifndef EC3R_RE_NS
+#define EC3R_RE_NS 3
+#endif
+constexpr int RE_NS = EC3R_RE_NS;
 constexpr int RE_CHUNK = 4 * UM_NT;  // pixels per plane per visit
 struct Ring {
     float* buf;          // [RE_NS][4][RE_CHUNK]
@@ -315,7 +319,7 @@ template <class S, class F>
 __device__ __forceinline__ void for_each_pixel4_seg_tma(const PoolArgs& a, int s0, int s1, int rank, Ring& rg,
                                                         S&& seg_fn, F&& f) {
     const int HW = a.H * a.W;
-    constexpr int kStride = 4 * UM_CL * UM_NT;
+    const int kStride = 4 * a.ncl * UM_NT;
     const int base0 = 4 * rank * UM_NT;
     const int n_it = base0 < HW ? (HW - base0 + kStride - 1) / kStride : 0;
     for (int sg = s0; sg < s1; ++sg) {
@@ -378,7 +382,8 @@ __device__ __forceinline__ void for_each_pixel4(const PoolArgs& a, int s0, int s
 #ifndef EC3R_RE_MINB
 #define EC3R_RE_MINB 2  // resident CTAs per SM the register budget is sized for
 #endif
-__global__ void __cluster_dims__(UM_CL, 1, 1) __launch_bounds__(UM_NT, EC3R_RE_MINB)
+// Launched with a runtime cluster size a.ncl (<= 8, cudaLaunchKernelEx).
+__global__ void __launch_bounds__(UM_NT, EC3R_RE_MINB)
 register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restrict__ out_rms,
                       int64_t* __restrict__ out_count, int64_t* __restrict__ out_npairs,
                       int32_t* __restrict__ out_status, uint8_t* __restrict__ keep_masks) {
@@ -388,7 +393,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     double* yc = tabs + Wp;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
-    const int e = blockIdx.x / UM_CL;
+    const int e = blockIdx.x / a.ncl;
     const int s0 = a.edge_seg[e], s1 = a.edge_seg[e + 1];
     __shared__ double scratch[(UM_NT / 32) * 24];
     __shared__ double part2[24], part3[4];
@@ -616,7 +621,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     cl.sync();
     if (threadIdx.x == 0) {
         double nv = 0, m = -1.0, f = 0;
-        for (int c = 0; c < UM_CL; ++c) {
+        for (int c = 0; c < a.ncl; ++c) {
             const double* pc = cl.map_shared_rank(part1, c);
             nv += pc[0];
             m = fmax(m, pc[1]);
@@ -669,7 +674,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     cl.sync();
     if (rank == 0 && threadIdx.x < 24) {
         double r = 0;
-        for (int c = 0; c < UM_CL; ++c) r += cl.map_shared_rank(part2, c)[threadIdx.x];
+        for (int c = 0; c < a.ncl; ++c) r += cl.map_shared_rank(part2, c)[threadIdx.x];
         tot2[threadIdx.x] = r;
     }
     cl.sync();
@@ -752,7 +757,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             }
         };
         // rank 0 alone (the others have left): every rank's share in turn
-        for (int r = 0; r < UM_CL; ++r) {
+        for (int r = 0; r < a.ncl; ++r) {
             if (use_tma) for_each_pixel4_seg_tma(a, s0, s1, r, rg, build, eig_body);
             else for_each_pixel4_seg(a, s0, s1, r, build, eig_body);
         }
@@ -1022,9 +1027,58 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
         EC3R_CUDA_TRY(cudaFuncSetAttribute(register_edges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
     }
+    // Cluster size: one wave of clusters when the edges allow it.  With c
+    // CTAs per edge the launch takes ceil(n / clusters_c) waves of 1/c of an
+    // edge each plus a per-CTA fixed cost (tables, shift sample, closed form
+    // on rank 0: ~3% of an edge's streaming, measured); pick the c in
+    // {1, 2, 4, 8} minimising ceil(n / clusters_c) (1/c + 0.03), clusters_c
+    // = the co-resident clusters of size c (cudaOccupancyMaxActiveClusters;
+    // sizes 5-7 measured slower: they pack the GPCs worse).  EC3R_RE_CL
+    // forces c.
+    static int max_clusters[4] = {0, 0, 0, 0};
+    int ncl = 4;
+    double best = 1e30;
+    for (int i = 0; i < 4; ++i) {
+        const int c = 1 << i;
+        if (max_clusters[i] == 0) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)(c * 64));
+            q.blockDim = dim3(UM_NT);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = (unsigned)c;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, register_edges_kernel, &q) != cudaSuccess || nc < 1) {
+                cudaGetLastError();
+                nc = std::max(1, 2 * kNumSMs / c);
+            }
+            max_clusters[i] = nc;
+        }
+        const double cost = (double)((n_edges + max_clusters[i] - 1) / max_clusters[i]) * (1.0 / c + 0.03);
+        if (cost < best - 1e-12) { best = cost; ncl = c; }
+    }
+    if (const char* f = getenv("EC3R_RE_CL")) ncl = std::min(8, std::max(1, atoi(f)));
+    a.ncl = ncl;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n_edges * ncl));
+    cfg.blockDim = dim3(UM_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)ncl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     KernelTimer tk(TK_REGISTER, as_stream(stream));
-    register_edges_kernel<<<n_edges * UM_CL, UM_NT, smem, as_stream(stream)>>>(a, out_sim3, out_rms, out_count,
-                                                                               out_npairs, out_status, keep_masks);
+    EC3R_CUDA_TRY(cudaLaunchKernelEx(&cfg, register_edges_kernel, a, out_sim3, out_rms, out_count, out_npairs,
+                                     out_status, keep_masks));
     EC3R_CHECK_LAUNCH("register_edges_kernel");
     tk.stop();
     return EC3R_OK;
