@@ -450,6 +450,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-floor", action="store_true", help="skip the fusion reduction-floor replay")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: validation of the N>1 path with ranks sharing a GPU (not a measurement)")
     args = ap.parse_args()
@@ -583,6 +584,15 @@ def main():
                   "achieved": flops_match / (stages["match"] * 1e-3) / 1e12, "peak": peaks["bf16_tflops"],
                   "frac": flops_match / (stages["match"] * 1e-3) / 1e12 / peaks["bf16_tflops"]},
     }
+    if rank == 0 and world == 1 and not args.no_floor and step.vmap is not None and \
+            os.environ.get("EC3R_FUSE_ENGINE", "hash") != "binned":
+        # the fusion kernel against its own reduction stream
+        fl = reduction_floor(step)
+        kt = roof["fuse_insert"]["ms"]
+        fl["what"] = ("the insert's 2 reductions per run (red.global.add.v4.f32 + red.global.add.u32), replayed "
+                      "alone from a log of the same launch; frac = replay / kernel")
+        fl["frac"] = fl["replay_ms"] / kt if kt else None
+        roof["fuse_insert"]["reduction_floor"] = fl
     dominant = max(roof, key=lambda k: roof[k]["ms"])
     value = P * world / (ms * 1e-3)
 
@@ -716,6 +726,47 @@ def run_e2e(step, dm, desc, args, world):
             "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(out_bytes), "steps": steps,
             "pipelined": "inputs double-buffered: step i+1 H2D overlaps step i compute",
             "h2d_pinned_gbs": h2d_gbs}
+
+
+def reduction_floor(step, reps=10):
+    """The fusion insert's reduction floor, measured live: one insert logs
+    its runs' (pool voxel, count) pairs in issue order instead of reducing
+    (ec3r_vhash_diag_log), then the logged reductions alone are replayed
+    into the same map (ec3r_vhash_diag_replay; float4 sums + u32 counts, and
+    the sums alone).  Median of `reps` replays, the map cleared before each."""
+    import torch
+
+    from paper_2510_02080_b200 import _lib
+
+    L = _lib.lib()
+    vm, pool, slots = step.vmap, step.dm.pool, step.slots
+    cap = int(slots.numel()) * pool.H * pool.W
+    runs = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+    n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    vm.clear()
+    _lib.check(L.ec3r_vhash_diag_log(vm._h, _lib.ptr(runs), cap, _lib.ptr(n_dev)), "ec3r_vhash_diag_log")
+    vm.insert_frames(pool, slots)
+    n_runs = int(n_dev.item())
+    out = {"runs": n_runs, "reps": reps}
+    for wc, key in ((1, "replay_ms"), (0, "replay_sums_only_ms")):
+        ts = []
+        for _ in range(reps + 2):
+            vm.clear()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            _lib.check(L.ec3r_vhash_diag_replay(vm._h, _lib.ptr(runs), _lib.ptr(n_dev), cap, wc, None),
+                       "ec3r_vhash_diag_replay")
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[key] = float(np.median(ts[2:]))
+    # leave the map as the step left it
+    vm.clear()
+    vm.insert_frames(pool, slots)
+    torch.cuda.synchronize()
+    del runs
+    return out
 
 
 def _time_ms(fn, reps=5, warm=2):

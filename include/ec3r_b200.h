@@ -209,6 +209,17 @@ EC3R_API int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, co
                              int H, int W, const double* K4_h, const double* slot_poses,
                              const double* slot_globals, const int32_t* slots, int n,
                              void* stream);
+/* Reduction-floor diagnostic (no reference counterpart; bench.py extras).
+ * ec3r_vhash_diag_log arms the NEXT ec3r_vhash_insert_frames call on h to
+ * log its runs instead of reducing them: (pool voxel, count) uint32 pairs in
+ * issue order into runs[0..cap), *n_dev (device, zeroed by the caller)
+ * counting them; the map is left unchanged.  ec3r_vhash_diag_replay issues
+ * exactly the logged reductions into h's pool (a float4 add per run, plus
+ * the u32 count add when with_count != 0): the cost of the insert's own
+ * reduction stream without its loads, keys and lookups. */
+EC3R_API int ec3r_vhash_diag_log(ec3r_vhash* h, void* runs, int64_t cap, unsigned long long* n_dev);
+EC3R_API int ec3r_vhash_diag_replay(ec3r_vhash* h, const void* runs, const unsigned long long* n_dev, int64_t cap,
+                                    int with_count, void* stream);
 /* Fuse explicit points (N,3) float64 with conf (N) float64 under sim3_h. */
 EC3R_API int ec3r_vhash_insert_points(ec3r_vhash* h, const double* points, const double* conf, int64_t n,
                              const double* sim3_h, void* stream);

@@ -42,6 +42,8 @@ _PROTOS = {
     "ec3r_vhash_destroy": (_I, [_P]),
     "ec3r_vhash_capacity": (_I64, [_P]),
     "ec3r_vhash_clear": (_I, [_P, _P]),
+    "ec3r_vhash_diag_log": (_I, [_P, _P, _I64, _P]),
+    "ec3r_vhash_diag_replay": (_I, [_P, _P, _P, _I64, _I, _P]),
     "ec3r_vhash_insert_frames": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _I, _P]),
     "ec3r_vhash_insert_points": (_I, [_P, _P, _P, _I64, _P, _P]),
     "ec3r_vhash_stats_get": (_I, [_P, _P, _P]),

@@ -65,6 +65,10 @@ struct ec3r_vhash {
     // point inserts go there; partial merges (multi-GPU owner maps) always use
     // the block hash.  A map holds one kind of content between clears.
     ec3r::BinFuse* bf;
+    // reduction-floor diagnostic: the next insert_frames logs its runs here
+    uint2* diag_runs;
+    unsigned long long* diag_n;
+    int64_t diag_cap;
     bool binned;
     bool bf_active, legacy_active;
 };
@@ -234,6 +238,9 @@ constexpr int FI_ROWS = EC3R_FI_ROWS;
 
 struct FuseArgs : FrameGeom {
     VB vb;
+    uint2* log_runs;                // LOG instance only (see RunLog)
+    unsigned long long* log_n;
+    unsigned long long log_cap;
 };
 
 // Per listed frame j, the composite G o P_f folded into a float32 affine map
@@ -284,34 +291,36 @@ __global__ void vh_frame_tables_kernel(FrameGeom a, float4* __restrict__ ftab) {
 // ~300 G when a warp's lanes hit consecutive voxels), and the sweep order
 // (frame-major ... all frames interleaved) and pool working set changed the
 // time by < 10%, so the pool's L2 residency is not the limiter.
-#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
-// experiment: log every run's reduction (vid, sums, count) in issue order, then
-// replay the log as pure reductions: the atomic floor of this address stream
-__device__ float4* g_log_sums;
-__device__ uint2* g_log_vid;
-__device__ unsigned long long g_log_n, g_log_cap;
-__device__ __forceinline__ void exp_log_run(uint32_t vid, float x, float y, float z, float w, uint32_t n) {
+// Reduction-floor diagnostic (ec3r_vhash_diag_*): the insert's LOG
+// instance writes every run's reduction target and count (vid, n) in issue
+// order instead of reducing; exp_replay_kernel then issues exactly those
+// reductions (constant conf-weighted payload, or the logged count), so the
+// replay time is the cost of the kernel's own reduction stream without the
+// keys, loads and lookups around it.
+struct RunLog {
+    uint2* runs;                    // (vid, n)
+    unsigned long long* n;          // device counter
+    unsigned long long cap;
+};
+__device__ __forceinline__ void log_run(const RunLog& lg, uint32_t vid, uint32_t n) {
     cg::coalesced_group g = cg::coalesced_threads();
     unsigned long long base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(&g_log_n, (unsigned long long)g.size());
+    if (g.thread_rank() == 0) base = atomicAdd(lg.n, (unsigned long long)g.size());
     const unsigned long long i = g.shfl(base, 0) + g.thread_rank();
-    if (i < g_log_cap) {
-        g_log_sums[i] = make_float4(x, y, z, w);
-        g_log_vid[i] = make_uint2(vid, n);
-    }
+    if (i < lg.cap) lg.runs[i] = make_uint2(vid, n);
 }
-__global__ void exp_replay_kernel(float4* __restrict__ sums, unsigned int* __restrict__ counts, int with_count) {
-    const unsigned long long n = min(g_log_n, g_log_cap);
+__global__ void vh_replay_runs_kernel(const uint2* __restrict__ runs, const unsigned long long* __restrict__ n_ptr,
+                                      unsigned long long cap, float4* __restrict__ sums,
+                                      unsigned int* __restrict__ counts, int with_count) {
+    const unsigned long long n = min(*n_ptr, cap);
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        // with_count & 2: replay the addresses only (constant payload, 8 B of log per run)
-        const uint2 v = __ldcs(g_log_vid + i);
-        const float4 s = (with_count & 2) ? make_float4(1e-3f, 1e-3f, 1e-3f, 0.5f) : __ldcs(g_log_sums + i);
-        red_add_v4(sums + v.x, s.x, s.y, s.z, s.w);
-        if (with_count & 1) red_add_u32(counts + v.x, v.y);
+        const uint2 v = __ldcs(runs + i);
+        red_add_v4(sums + v.x, 1e-3f, 1e-3f, 1e-3f, 0.5f);
+        if (with_count) red_add_u32(counts + v.x, v.y);
     }
 }
-#endif
+
 constexpr int ST_H = 8, ST_W = 16;
 #ifndef EC3R_BC_BITS
 #define EC3R_BC_BITS 11
@@ -323,6 +332,7 @@ constexpr int BC_BITS = EC3R_BC_BITS;  // shared-memory block cache: 2048 entrie
 #endif
 constexpr int FI_G = EC3R_FI_G;
 
+template <bool LOG>
 __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
     extern __shared__ float4 sA[];  // A[W]
     __shared__ float4 sB[FI_ROWS];
@@ -577,12 +587,12 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             rn = fmaf(cont, rn, 1.f);
             const bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
             if (last) {
-#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
-                exp_log_run(vid[k], rx, ry, rz, rw, (uint32_t)rn);
-#else
-                red_add_v4(a.vb.sums + vid[k], rx, ry, rz, rw);
-                red_add_u32(a.vb.counts + vid[k], (uint32_t)rn);
-#endif
+                if constexpr (LOG) {
+                    log_run(RunLog{a.log_runs, a.log_n, a.log_cap}, vid[k], (uint32_t)rn);
+                } else {
+                    red_add_v4(a.vb.sums + vid[k], rx, ry, rz, rw);
+                    red_add_u32(a.vb.counts + vid[k], (uint32_t)rn);
+                }
             }
         }
     }
@@ -1465,11 +1475,22 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     h->legacy_active = true;
     const size_t smem = sizeof(float4) * (size_t)W;
     if (smem > 48 * 1024)
-        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, (n + FI_G - 1) / FI_G);
+    a.log_runs = nullptr; a.log_n = nullptr; a.log_cap = 0;
+    if (h->diag_runs) {  // diagnostic: log this insert's runs instead of reducing (one call)
+        a.log_runs = h->diag_runs; a.log_n = h->diag_n; a.log_cap = (unsigned long long)h->diag_cap;
+        h->diag_runs = nullptr; h->diag_n = nullptr; h->diag_cap = 0;
+        if (smem > 48 * 1024)
+            EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        vh_insert_frames_kernel<true><<<grid, FI_NT, smem, st>>>(a);
+        EC3R_CHECK_LAUNCH("vh_insert_frames_kernel<log>");
+        return EC3R_OK;
+    }
     KernelTimer tk(TK_FUSE_INSERT, st);
-    vh_insert_frames_kernel<<<grid, FI_NT, smem, st>>>(a);
+    vh_insert_frames_kernel<false><<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
     tk.stop();
     return EC3R_OK;
@@ -1713,28 +1734,28 @@ extern "C" int ec3r_vhash_stats_device(ec3r_vhash* h, int64_t* out5, void* strea
     return EC3R_OK;
 }
 
-#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 6
-extern "C" __attribute__((visibility("default"))) int ec3r_exp_log_alloc(long long cap) {
-    float4* a; uint2* b;
-    if (cudaMalloc(&a, 16 * (size_t)cap) != cudaSuccess || cudaMalloc(&b, 8 * (size_t)cap) != cudaSuccess) return -1;
-    unsigned long long z = 0, c = (unsigned long long)cap;
-    cudaMemcpyToSymbol(ec3r::g_log_sums, &a, sizeof(a));
-    cudaMemcpyToSymbol(ec3r::g_log_vid, &b, sizeof(b));
-    cudaMemcpyToSymbol(ec3r::g_log_n, &z, sizeof(z));
-    cudaMemcpyToSymbol(ec3r::g_log_cap, &c, sizeof(c));
-    return 0;
+
+// ---------------------------------------------------------------------------
+// Reduction-floor diagnostic (bench.py extras, tools/fuse_timing.py).
+// ec3r_vhash_diag_log arms the next ec3r_vhash_insert_frames call to write
+// its runs' (pool voxel, count) pairs, in issue order, to runs[0..cap) with
+// *n_dev counting them (the map itself is left unchanged); *n_dev must be
+// zero.  ec3r_vhash_diag_replay issues exactly those reductions into the
+// map's pool (with_count = 0: the float4 sums only) and nothing else.
+
+extern "C" int ec3r_vhash_diag_log(ec3r_vhash* h, void* runs, int64_t cap, unsigned long long* n_dev) {
+    if (!h || !runs || !n_dev || cap <= 0) return EC3R_EARG;
+    h->diag_runs = static_cast<uint2*>(runs);
+    h->diag_n = n_dev;
+    h->diag_cap = cap;
+    return EC3R_OK;
 }
-extern "C" __attribute__((visibility("default"))) long long ec3r_exp_log_count() {
-    unsigned long long n = 0;
-    cudaMemcpyFromSymbol(&n, ec3r::g_log_n, sizeof(n));
-    return (long long)n;
+
+extern "C" int ec3r_vhash_diag_replay(ec3r_vhash* h, const void* runs, const unsigned long long* n_dev, int64_t cap,
+                                      int with_count, void* stream) {
+    if (!h || !runs || !n_dev || cap <= 0) return EC3R_EARG;
+    ec3r::vh_replay_runs_kernel<<<ec3r::kNumSMs * 8, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint2*>(runs), n_dev, (unsigned long long)cap, h->sums, h->counts, with_count);
+    EC3R_CHECK_LAUNCH("vh_replay_runs_kernel");
+    return EC3R_OK;
 }
-extern "C" __attribute__((visibility("default"))) int ec3r_exp_log_reset() {
-    unsigned long long z = 0;
-    return cudaMemcpyToSymbol(ec3r::g_log_n, &z, sizeof(z)) == cudaSuccess ? 0 : -1;
-}
-extern "C" __attribute__((visibility("default"))) int ec3r_exp_replay(ec3r_vhash* h, int grid, int with_count) {
-    ec3r::exp_replay_kernel<<<grid, 256>>>(h->sums, h->counts, with_count);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-#endif

@@ -15,13 +15,13 @@ echo "tests_rc=$?"
 timeout 600 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.log" 2>&1
 echo "bench_rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k "regex:ec3r::|CUB_200802" -c 600 --csv \
-    --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-extras \
+    --log-file "$OUT/launches.csv" python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --no-floor \
     > "$OUT/ncu_bench.log" 2>&1
 echo "ncu_rc=$?"
 if [ "$MODE" = "full" ]; then
     timeout 900 ncu --set full --clock-control none --import-source on \
-        -k "regex:vh_insert_frames_kernel|register_edges_kernel|mt_tc_kernel" -c 3 \
-        -o "$OUT/prof" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras \
+        -k "regex:vh_insert_frames_kernel|register_edges_kernel|mt_tc_kernel" -c 6 \
+        -o "$OUT/prof" python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --no-floor \
         > "$OUT/ncu_full.log" 2>&1
     echo "full_rc=$?"
 fi

@@ -26,7 +26,9 @@ def main(rep):
     res = {}
     for r in rows[2:]:
         d = dict(zip(hdr, r))
-        name = next((h for h in HOT if d["Kernel Name"].startswith(h)), None)
+        kn = d["Kernel Name"]
+        kn = kn[5:] if kn.startswith("void ") else kn  # templated kernels: "void name<...>(...)"
+        name = next((h for h in HOT if kn.startswith(h)), None)
         if name is None or name in res:
             continue
         u = dict(zip(hdr, units))
