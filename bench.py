@@ -202,6 +202,12 @@ class Step:
         # registration clusters need); "serial" = one stream.  Measured
         # (profiles/r02o_*): serial 2.96, early 2.92, late 2.87 ms per step.
         self.overlap = os.environ.get("EC3R_BENCH_OVERLAP", "late")
+        # the sorted emit without the host read of U (EC3R_BENCH_EMIT_SYNC=1
+        # restores it): U is known from the sizing fill and checked on the
+        # device count after the timed region, so the host never waits
+        # mid-step and the next step's launches are queued before this one
+        # ends (measured: 2.78 -> 2.70 ms per step, profiles/r02aa_*)
+        self.emit_sync = os.environ.get("EC3R_BENCH_EMIT_SYNC", "0") == "1"
 
     def _event(self):
         e = self.torch.cuda.Event(enable_timing=True)
@@ -264,7 +270,12 @@ class Step:
             launch_match()
         nvtx.range_push("emit" if self.exchange is None else "exchange+emit")
         if self.exchange is None:
-            keys, cen, wsum, cnt_v = self.vmap.extract(sort=True, out=self.out)
+            if self.emit_sync:
+                keys, cen, wsum, cnt_v = self.vmap.extract(sort=True, out=self.out)
+            else:
+                # no host read of U mid-step (it is known from the sizing fill):
+                # the host keeps the queue full across the step boundary
+                keys, cen, wsum, cnt_v, self.n_dev = self.vmap.extract(sort=True, out=self.out, sync=False)
         else:
             # N > 1: global map partitioned by voxel key — owner-bucketed
             # partials, one NCCL all-to-all, owner-side merge + sorted emit
@@ -279,7 +290,7 @@ class Step:
         ev["t_emit"] = self._event()
         main.wait_event(ev["m1"])  # join the matcher
         ev["t_end"] = self._event()
-        if self.exchange is None or not self.async_exchange:
+        if (self.exchange is None and self.emit_sync) or (self.exchange is not None and not self.async_exchange):
             self.n_voxels = int(keys.numel())
         if record is not None:
             record.append(ev)
@@ -527,6 +538,10 @@ def main():
         step.exchange.verify()  # overflow flags of the host-sync-free exchange
         step.n_voxels = int(step.n_dev.item())
         step.async_exchange = False
+    elif step.exchange is None and not step.emit_sync:
+        step.n_voxels = int(step.n_dev.item())  # U of the last step (device count, read after the timed region)
+        if step.n_voxels > int(step.out[0].shape[0]):
+            raise RuntimeError("voxel emit exceeded the preallocated rows")
     ktimes = _lib.kernel_times()  # per hot kernel: CUDA events on its launching stream
     if world > 1:
         dist.barrier()

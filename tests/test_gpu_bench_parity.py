@@ -49,6 +49,8 @@ def bench_step():
     step.run()
     out = tuple(x.clone() for x in step.run())
     torch.cuda.synchronize()
+    if step.n_dev is not None:  # the step's host-sync-free emit: U only on the device
+        assert int(step.n_dev.item()) == int(out[0].shape[0])
     reg = step.plan.run(dm.pool)
     torch.cuda.synchronize()
     dense = []
