@@ -47,7 +47,18 @@ constexpr int TC_NA = 2;         // A blocks resident per unit
 constexpr int TC_BN = 128;       // columns per B tile (UMMA N)
 constexpr int TC_BK = 64;        // bf16 per 128-byte swizzle row
 constexpr int TC_STAGES = 4;     // B ring depth
+#ifndef EC3R_MT_EPI16
+#define EC3R_MT_EPI16 0  // 1: 16 epilogue warps on 16-column chunks (measured slower: 1.043 vs 0.937 ms,
+                         // 96 registers by the per-SMSP register file, spills); 0: 8 warps on 32-column chunks
+#endif
+#if EC3R_MT_EPI16
+constexpr int TC_EPI_WARPS = 16;  // 4 per TMEM lane quarter: one per 32-column quarter of the tile
+constexpr int TC_CW = 16;         // columns per chunk (one tcgen05.ld.32x32b.x16 per A block)
+#else
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: one per column half
+constexpr int TC_CW = 32;
+#endif
+constexpr int TC_HP = TC_EPI_WARPS / 4;  // column parts per tile (warps per lane quarter)
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
 constexpr int TC_THREADS = 64 + TC_EPI_THREADS;  // producer + MMA + epilogue warps
 constexpr int TC_BOX_BYTES = TC_BM * TC_BK * 2;  // 16 KB (A box and B box alike)
@@ -171,6 +182,25 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[16]) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld_async(uint32_t taddr, uint32_t (&r)[N]) {
+    if constexpr (N == 16) tmem_ld16_async(taddr, r);
+    else tmem_ld32_async(taddr, r);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
     asm volatile(""
@@ -291,36 +321,37 @@ struct RowTop2 {
     int cb;  // column base of the chunk holding b (b's code has the column within the chunk)
 };
 
-template <int J>
-__device__ __forceinline__ void make_keys(const uint32_t (&r0)[32], const uint32_t (&r1)[32], uint32_t creg0,
-                                          uint32_t creg1, float (&k0)[32], float (&k1)[32]) {
-    if constexpr (J < 32) {
+template <int J, int N>
+__device__ __forceinline__ void make_keys(const uint32_t (&r0)[N], const uint32_t (&r1)[N], uint32_t creg0,
+                                          uint32_t creg1, float (&k0)[N], float (&k1)[N]) {
+    if constexpr (J < N) {
         k0[J] = make_key<KEY_MASK | ((uint32_t)J << 6)>(r0[J], creg0);
         k1[J] = make_key<KEY_MASK | ((uint32_t)J << 6)>(r1[J], creg1);
-        make_keys<J + 1>(r0, r1, creg0, creg1, k0, k1);
+        make_keys<J + 1, N>(r0, r1, creg0, creg1, k0, k1);
     }
 }
 
-__device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[32], uint32_t (&r1)[32], int nv0, int nv1, int cbase,
+template <int N>
+__device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[N], uint32_t (&r1)[N], int nv0, int nv1, int cbase,
                                                uint32_t creg0, uint32_t creg1, RowTop2& R0, RowTop2& R1,
                                                uint32_t cb, int lane) {
     // interior chunks (every row and column valid) skip the predicates
-    if (!__all_sync(0xffffffffu, nv0 == 32 && nv1 == 32)) {
+    if (!__all_sync(0xffffffffu, nv0 == N && nv1 == N)) {
         const uint32_t neg = __float_as_uint(KEY_NEG);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < N; ++j) {
             if (j >= nv0) r0[j] = neg;
             if (j >= nv1) r1[j] = neg;
         }
     }
-    float k0[32], k1[32];
-    make_keys<0>(r0, r1, creg0, creg1, k0, k1);
+    float k0[N], k1[N];
+    make_keys<0, N>(r0, r1, creg0, creg1, k0, k1);
     // row side: top-2 over pairs (hi, lo) — 5 ops per 2 keys per row
     {
         float m0 = fmaxf(k0[0], k0[1]), s0 = fminf(k0[0], k0[1]);
         float m1 = fmaxf(k1[0], k1[1]), s1 = fminf(k1[0], k1[1]);
 #pragma unroll
-        for (int j = 2; j < 32; j += 2) {
+        for (int j = 2; j < N; j += 2) {
             const float h0 = fmaxf(k0[j], k0[j + 1]), l0 = fminf(k0[j], k0[j + 1]);
             const float t0 = fminf(m0, h0);
             m0 = fmaxf(m0, h0);
@@ -342,7 +373,7 @@ __device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[32], uint32_t (&r1
     // column side: fold the thread's two rows, then top-1 / top-2 over the
     // warp (keys are unique within a column: the code holds block and lane)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < N; ++j) {
         const float hi = fmaxf(k0[j], k1[j]), lo = fminf(k0[j], k1[j]);
         const float m = warp_max_f32(hi);
         const float m2 = warp_max_f32(hi == m ? lo : hi);
@@ -359,8 +390,8 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
     unsigned char* sA = smem;                                   // TC_NA * KB boxes
     unsigned char* sB = sA + (size_t)TC_NA * KB * TC_BOX_BYTES;  // TC_STAGES boxes
     float2* colbuf = (float2*)(sB + (size_t)TC_STAGES * TC_BOX_BYTES);  // [2 tiles][4 quarters][TC_BN]
-    float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);                     // [2 units][TC_NA * TC_BM] half-row summaries
-    uint64_t* bars = (uint64_t*)(rsc + 2 * TC_NA * TC_BM);
+    float4* rsc = (float4*)(colbuf + 2 * 4 * TC_BN);  // [2 units][TC_HP - 1][TC_NA * TC_BM] part-row summaries
+    uint64_t* bars = (uint64_t*)(rsc + 2 * (TC_HP - 1) * TC_NA * TC_BM);
     uint64_t* a_full = bars + 0;   // per k-block slice of the resident A (both blocks)
     uint64_t* a_empty = bars + 4;
     uint64_t* b_full = bars + 8;
@@ -471,7 +502,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
         // [h*64, h*64+64), as two 32-column chunks (the second chunk's TMEM
         // load is in flight while the first is reduced).
         const int q = warp & 3;
-        const int h = (warp - 2) >> 2;
+        const int h = (warp - 2) >> 2;  // column part of the tile: [h * 2 TC_CW, +2 TC_CW)
         const int et = threadIdx.x - 64;  // 0..255
         const uint32_t creg0 = KEY_MASK | (uint32_t)lane;         // A block 0
         const uint32_t creg1 = KEY_MASK | 32u | (uint32_t)lane;   // A block 1
@@ -501,20 +532,22 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 mbar_wait(t_full + acc, acc_phase);
                 tc_fence_after();
                 const int col0 = un.col0 + t * TC_BN;
-                const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + h * 64);
-                const uint32_t cbq = smem_u32(colbuf + (size_t)(tb * 4 + q) * TC_BN + h * 64);
-                uint32_t ra[32], rb[32], rc[32], rd[32];
-                tmem_ld32_async(ta, ra);
-                tmem_ld32_async(ta + TC_BN, rb);
+                const uint32_t ta =
+                    tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NA * TC_BN + h * 2 * TC_CW);
+                const uint32_t cbq = smem_u32(colbuf + (size_t)(tb * 4 + q) * TC_BN + h * 2 * TC_CW);
+                uint32_t ra[TC_CW], rb[TC_CW], rc[TC_CW], rd[TC_CW];
+                tmem_ld_async(ta, ra);
+                tmem_ld_async(ta + TC_BN, rb);
                 tmem_wait_ld();
                 reg_fence(ra);
                 reg_fence(rb);
-                tmem_ld32_async(ta + 32, rc);
-                tmem_ld32_async(ta + TC_BN + 32, rd);
+                tmem_ld_async(ta + TC_CW, rc);
+                tmem_ld_async(ta + TC_BN + TC_CW, rd);
                 {
-                    const int cbase = col0 + h * 64;
-                    const int ncol = min(32, M - cbase);
-                    chunk_epilogue(ra, rb, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq, lane);
+                    const int cbase = col0 + h * 2 * TC_CW;
+                    const int ncol = min(TC_CW, M - cbase);
+                    chunk_epilogue<TC_CW>(ra, rb, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq,
+                                          lane);
                 }
                 tmem_wait_ld();
                 reg_fence(rc);
@@ -524,10 +557,10 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 mbar_arrive(t_empty + acc);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 {
-                    const int cbase = col0 + h * 64 + 32;
-                    const int ncol = min(32, M - cbase);
-                    chunk_epilogue(rc, rd, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1, cbq + 256u,
-                                   lane);
+                    const int cbase = col0 + h * 2 * TC_CW + TC_CW;
+                    const int ncol = min(TC_CW, M - cbase);
+                    chunk_epilogue<TC_CW>(rc, rd, rv0 ? ncol : 0, rv1 ? ncol : 0, cbase, creg0, creg1, R0, R1,
+                                          cbq + 8u * TC_CW, lane);
                 }
 #if EC3R_MT_SPLITBAR
                 if (merger) named_sync(2 + tb, TC_EPI_THREADS);
@@ -565,21 +598,35 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
             // h = 1 warps can finish a 1-2 tile unit and write its summaries
             // while the h = 0 warps still read the previous unit's; the buffer
             // they reuse two units later is ordered by the named_sync(1) in between
-            const int ti = q * 32 + lane + (uiter & 1) * (TC_NA * TC_BM);
-            const int c0 = R0.cb + (int)((__float_as_uint(R0.b) >> 6) & 31u);
-            const int c1 = R1.cb + (int)((__float_as_uint(R1.b) >> 6) & 31u);
-            if (h == 1) {
-                rsc[ti] = make_float4(R0.b, R0.s, __int_as_float(c0), 0.f);
-                rsc[TC_BM + ti] = make_float4(R1.b, R1.s, __int_as_float(c1), 0.f);
+            // rsc[parity][part h - 1][A block][row]: parts 1.. hand their
+            // (best, second, column) to part 0, which folds them in column
+            // order (strictly greater wins: the first column on equal keys)
+            const int ti = q * 32 + lane + (uiter & 1) * ((TC_HP - 1) * TC_NA * TC_BM);
+            int c0 = R0.cb + (int)((__float_as_uint(R0.b) >> 6) & 31u);
+            int c1 = R1.cb + (int)((__float_as_uint(R1.b) >> 6) & 31u);
+            if (h >= 1) {
+                float4* rp = rsc + (h - 1) * TC_NA * TC_BM;
+                rp[ti] = make_float4(R0.b, R0.s, __int_as_float(c0), 0.f);
+                rp[TC_BM + ti] = make_float4(R1.b, R1.s, __int_as_float(c1), 0.f);
             }
             named_sync(1, TC_EPI_THREADS);
             if (h == 0) {
-                const float4 o0 = rsc[ti], o1 = rsc[TC_BM + ti];
+#pragma unroll
+                for (int hp = 0; hp < TC_HP - 1; ++hp) {
+                    const float4* rp = rsc + hp * TC_NA * TC_BM;
+                    const float4 o0 = rp[ti], o1 = rp[TC_BM + ti];
+                    R0.s = fmax3f(R0.s, o0.y, fminf(R0.b, o0.x));
+                    c0 = o0.x > R0.b ? __float_as_int(o0.z) : c0;
+                    R0.b = fmaxf(R0.b, o0.x);
+                    R1.s = fmax3f(R1.s, o1.y, fminf(R1.b, o1.x));
+                    c1 = o1.x > R1.b ? __float_as_int(o1.z) : c1;
+                    R1.b = fmaxf(R1.b, o1.x);
+                }
                 if (rv0) {
                     RowCand rc;
-                    rc.k1 = fmaxf(R0.b, o0.x);
-                    rc.k2 = fmax3f(R0.s, o0.y, fminf(R0.b, o0.x));
-                    rc.c1 = o0.x > R0.b ? __float_as_int(o0.z) : c0;
+                    rc.k1 = R0.b;
+                    rc.k2 = R0.s;
+                    rc.c1 = c0;
                     rc.pad = 0;
                     p.cand[row0 * p.n_split + un.split] = rc;
                     if (p.n_split == 1) {
@@ -590,9 +637,9 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                 }
                 if (rv1) {
                     RowCand rc;
-                    rc.k1 = fmaxf(R1.b, o1.x);
-                    rc.k2 = fmax3f(R1.s, o1.y, fminf(R1.b, o1.x));
-                    rc.c1 = o1.x > R1.b ? __float_as_int(o1.z) : c1;
+                    rc.k1 = R1.b;
+                    rc.k2 = R1.s;
+                    rc.c1 = c1;
                     rc.pad = 0;
                     p.cand[row1 * p.n_split + un.split] = rc;
                     if (p.n_split == 1) {
@@ -887,7 +934,8 @@ static bool make_map(CUtensorMap* m, const uint16_t* base, int64_t rows, int D) 
 
 static size_t tc_smem_bytes(int kblocks) {
     return 1024 + (size_t)TC_NA * kblocks * TC_BOX_BYTES + (size_t)TC_STAGES * TC_BOX_BYTES +
-           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * 2 * TC_NA * TC_BM + 8 * (8 + 2 * TC_STAGES + 4) + 16;
+           sizeof(float2) * 2 * 4 * TC_BN + sizeof(float4) * 2 * (TC_HP - 1) * TC_NA * TC_BM +
+           8 * (8 + 2 * TC_STAGES + 4) + 16;
 }
 
 // column slots: one per (unit, column) = sum over pairs of ceil(N/256) * M
