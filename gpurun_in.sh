@@ -1,5 +1,7 @@
-T=r02ae; O=gpurun_out/$T; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_parity.py -q -x -k "match or bench or verify" > $O/tests.log 2>&1; echo tests_rc=$?; tail -2 $O/tests.log
-timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-floor > $O/bench.json 2> $O/bench.err
+T=r02af; O=gpurun_out/$T; mkdir -p $O
+for v in default colfirst nosplit default; do
+if [ $v = default ]; then unset EC3R_B200_LIB; else export EC3R_B200_LIB=variants/libec3r_$v.so; fi
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-floor --no-extras > $O/bench_$v.json 2> $O/bench_$v.err
 python -c "
-import json;d=json.loads(open('$O/bench.json').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4), {k:round(v,3) for k,v in d['stages_ms'].items()}); print(d['rooflines']['match']); print(json.dumps(d['extras'].get('matcher_sweep'))[:1500])"
+import json;d=json.loads(open('$O/bench_$v.json').read().strip().splitlines()[-1]);print('$v', round(d['ms_per_step'],4), round(d['rooflines']['match']['ms'],4), round(d['rooflines']['match']['frac'],4))"
+done

@@ -275,6 +275,9 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+#ifndef EC3R_MT_COLFIRST
+#define EC3R_MT_COLFIRST 0  // chunk epilogue: column side before the row side
+#endif
 #ifndef EC3R_MT_SPLITBAR
 #define EC3R_MT_SPLITBAR 1  // per-tile colbuf handoff: only the merging warps wait
 #endif
@@ -346,6 +349,41 @@ __device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[N], uint32_t (&r1)
     }
     float k0[N], k1[N];
     make_keys<0, N>(r0, r1, creg0, creg1, k0, k1);
+#if EC3R_MT_COLFIRST
+    // column side: fold the thread's two rows, then top-1 / top-2 over the
+    // warp (keys are unique within a column: the code holds block and lane)
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const float hi = fmaxf(k0[j], k1[j]), lo = fminf(k0[j], k1[j]);
+        const float m = warp_max_f32(hi);
+        const float m2 = warp_max_f32(hi == m ? lo : hi);
+        if (lane == 0) sts_f2(cb + 8u * j, m, m2);
+    }
+    // row side: top-2 over pairs (hi, lo) — 5 ops per 2 keys per row
+    {
+        float m0 = fmaxf(k0[0], k0[1]), s0 = fminf(k0[0], k0[1]);
+        float m1 = fmaxf(k1[0], k1[1]), s1 = fminf(k1[0], k1[1]);
+#pragma unroll
+        for (int j = 2; j < N; j += 2) {
+            const float h0 = fmaxf(k0[j], k0[j + 1]), l0 = fminf(k0[j], k0[j + 1]);
+            const float t0 = fminf(m0, h0);
+            m0 = fmaxf(m0, h0);
+            s0 = fmax3f(s0, l0, t0);
+            const float h1 = fmaxf(k1[j], k1[j + 1]), l1 = fminf(k1[j], k1[j + 1]);
+            const float t1 = fminf(m1, h1);
+            m1 = fmaxf(m1, h1);
+            s1 = fmax3f(s1, l1, t1);
+        }
+        const float t0 = fminf(R0.b, m0);
+        R0.cb = m0 > R0.b ? cbase : R0.cb;
+        R0.b = fmaxf(R0.b, m0);
+        R0.s = fmax3f(R0.s, s0, t0);
+        const float t1 = fminf(R1.b, m1);
+        R1.cb = m1 > R1.b ? cbase : R1.cb;
+        R1.b = fmaxf(R1.b, m1);
+        R1.s = fmax3f(R1.s, s1, t1);
+    }
+#else
     // row side: top-2 over pairs (hi, lo) — 5 ops per 2 keys per row
     {
         float m0 = fmaxf(k0[0], k0[1]), s0 = fminf(k0[0], k0[1]);
@@ -379,6 +417,8 @@ __device__ __forceinline__ void chunk_epilogue(uint32_t (&r0)[N], uint32_t (&r1)
         const float m2 = warp_max_f32(hi == m ? lo : hi);
         if (lane == 0) sts_f2(cb + 8u * j, m, m2);
     }
+#endif
+
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
