@@ -332,10 +332,29 @@ constexpr int BC_BITS = EC3R_BC_BITS;  // shared-memory block cache: 2048 entrie
 #endif
 constexpr int FI_G = EC3R_FI_G;
 
-template <bool LOG>
+// Opt-in (EC3R_FI_TMA=1): on the bench workload the strip ring measured 1.4 %
+// slower than the register-prefetched 64-bit loads (1.198 vs 1.181 ms,
+// profiles/r02ag_*): the kernel runs at its reduction floor, and the strip
+// hand-offs add barrier waits without removing any reduction.
+static bool tma_requested() {
+    const char* e = getenv("EC3R_FI_TMA");
+    return e != nullptr && e[0] == '1';
+}
+
+// TMA form (TMA = true, one frame per CTA): the band's depth and confidence
+// stream through shared memory as 8-row strips (one sub-tile row), each a
+// contiguous 8 W-float span of both planes moved by two cp.async.bulk copies
+// into a 2-stage ring; a warp waits on a strip's mbarrier before its first
+// sub-tile there, and the last warp to leave a strip refills its stage with
+// the strip two ahead.  Requires H W % 4 == 0 and 16-byte aligned planes.
+__device__ __forceinline__ uint32_t vh_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <bool LOG, bool TMA>
 __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
-    extern __shared__ float4 sA[];  // A[W]
+    extern __shared__ float4 sA[];  // A[W], then (TMA) the strip ring [2 stages][2 planes][8 W]
     __shared__ float4 sB[FI_ROWS];
+    __shared__ __align__(8) uint64_t strip_full[2];
+    __shared__ int strip_left[2];
     __shared__ unsigned long long cta_cnt[4];
     __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
     const int W = a.W, H = a.H;
@@ -368,6 +387,69 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     __syncthreads();
     const float* dbase = a.depth + (size_t)slot * HW;
     const float* cbase = a.conf + (size_t)slot * HW;
+    const int n_strips = (rows + ST_H - 1) / ST_H;
+    float* ring = reinterpret_cast<float*>(sA + W);
+    auto issue_strip = [&](int s) {  // one thread: strip s of the band into stage s & 1
+        const int r0 = s * ST_H, nr = min(ST_H, rows - r0);
+        const uint32_t bytes = 4u * (uint32_t)(nr * W);
+        const uint32_t bar = vh_smem_u32(strip_full + (s & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * bytes) : "memory");
+        const size_t off = (size_t)(v_band + r0) * W;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         vh_smem_u32(ring + (size_t)((s & 1) * 2 + 0) * ST_H * W)),
+                     "l"(dbase + off), "r"(bytes), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         vh_smem_u32(ring + (size_t)((s & 1) * 2 + 1) * ST_H * W)),
+                     "l"(cbase + off), "r"(bytes), "r"(bar)
+                     : "memory");
+    };
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) {
+            for (int q = 0; q < 2; ++q) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(vh_smem_u32(strip_full + q)) : "memory");
+                strip_left[q] = 0;
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int q = 0; q < 2 && q < n_strips; ++q) issue_strip(q);
+        }
+        __syncthreads();
+    }
+    int cur_strip = -1;
+    // warp-wide: strips are entered in order, each after its copy landed;
+    // leaving one counts the warp out and the last warp refills the stage
+    auto leave_strip = [&](int s) {
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&strip_left[s & 1], 1) == FI_NT / 32 - 1) {
+                strip_left[s & 1] = 0;
+                if (s + 2 < n_strips) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue_strip(s + 2);
+                }
+            }
+        }
+    };
+    auto enter_strip = [&](int s) {
+        while (cur_strip < s) {
+            if (cur_strip >= 0) leave_strip(cur_strip);
+            ++cur_strip;
+            if (cur_strip < n_strips) {
+                const uint32_t bar = vh_smem_u32(strip_full + (cur_strip & 1));
+                const uint32_t par = (uint32_t)(cur_strip >> 1) & 1u;
+                asm volatile(
+                    "{\n"
+                    ".reg .pred p;\n"
+                    "VH_WAIT_%=:\n"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                    "@!p bra VH_WAIT_%=;\n"
+                    "}\n" ::"r"(bar),
+                    "r"(par)
+                    : "memory");
+            }
+        }
+    };
 
     // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
     auto advance = [&](int& sy, int& sx) {
@@ -401,14 +483,40 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     while (sx >= stx) { sx -= stx; ++sy; }
     int py = sy, px = sx;  // prefetch cursor
     float nz[4], nc[4];
-    if (py < n_sy) load4(py, px, nz, nc);
+    if constexpr (!TMA) {
+        if (py < n_sy) load4(py, px, nz, nc);
+    }
     for (; sy < n_sy; advance(sy, sx)) {
         const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
         float zs[4], cs[4];
+        if constexpr (TMA) {
+            enter_strip(sy);
+            const float* zr = ring + (size_t)((sy & 1) * 2) * ST_H * W + dv * W + u0;
+            const float* cr = zr + ST_H * W;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
-        advance(py, px);
-        if (py < n_sy) load4(py, px, nz, nc);
+            for (int k = 0; k < 4; ++k) { zs[k] = 0.f; cs[k] = 0.f; }
+            if (r < rows) {
+                if (pairs) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (u0 + 2 * h + 1 < W) {
+                            const float2 z2 = *reinterpret_cast<const float2*>(zr + 2 * h);
+                            const float2 c2 = *reinterpret_cast<const float2*>(cr + 2 * h);
+                            zs[2 * h] = z2.x; zs[2 * h + 1] = z2.y;
+                            cs[2 * h] = c2.x; cs[2 * h + 1] = c2.y;
+                        }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (u0 + k < W) { zs[k] = zr[k]; cs[k] = cr[k]; }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
+            advance(py, px);
+            if (py < n_sy) load4(py, px, nz, nc);
+        }
         const float4 Bv = sB[min(r, rows - 1)];
 
         // phase A: keys and contributions of the lane's 4 pixels, branch-free
@@ -596,6 +704,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             }
         }
     }
+    if constexpr (TMA) enter_strip(n_strips);  // count this warp out of the remaining strips
     }  // frames of this CTA
     // counters: warp reduce then one shared atomic per warp, one global per CTA
 #pragma unroll
@@ -1475,22 +1584,37 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     h->legacy_active = true;
     const size_t smem = sizeof(float4) * (size_t)W;
     if (smem > 48 * 1024)
-        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<false>,
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<false, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // TMA strip ring: 2 stages x 2 planes x 8 rows of W floats after A[W]
+    const size_t smem_tma = smem + sizeof(float) * 2 * 2 * ST_H * (size_t)W;
+    const bool tma = FI_G == 1 && ((int64_t)H * W) % 4 == 0 &&
+                     ((reinterpret_cast<uintptr_t>(depth_pool) | reinterpret_cast<uintptr_t>(conf_pool)) & 15) == 0 &&
+                     smem_tma <= 160 * 1024 && tma_requested();
+    if (tma) {
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<false, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma));
+        EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<true, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma));
+    }
     const dim3 grid((H + FI_ROWS - 1) / FI_ROWS, (n + FI_G - 1) / FI_G);
     a.log_runs = nullptr; a.log_n = nullptr; a.log_cap = 0;
     if (h->diag_runs) {  // diagnostic: log this insert's runs instead of reducing (one call)
         a.log_runs = h->diag_runs; a.log_n = h->diag_n; a.log_cap = (unsigned long long)h->diag_cap;
         h->diag_runs = nullptr; h->diag_n = nullptr; h->diag_cap = 0;
-        if (smem > 48 * 1024)
-            EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        vh_insert_frames_kernel<true><<<grid, FI_NT, smem, st>>>(a);
+        if (tma) vh_insert_frames_kernel<true, true><<<grid, FI_NT, smem_tma, st>>>(a);
+        else {
+            if (smem > 48 * 1024)
+                EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<true, false>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            vh_insert_frames_kernel<true, false><<<grid, FI_NT, smem, st>>>(a);
+        }
         EC3R_CHECK_LAUNCH("vh_insert_frames_kernel<log>");
         return EC3R_OK;
     }
     KernelTimer tk(TK_FUSE_INSERT, st);
-    vh_insert_frames_kernel<false><<<grid, FI_NT, smem, st>>>(a);
+    if (tma) vh_insert_frames_kernel<false, true><<<grid, FI_NT, smem_tma, st>>>(a);
+    else vh_insert_frames_kernel<false, false><<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
     tk.stop();
     return EC3R_OK;

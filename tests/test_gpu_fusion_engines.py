@@ -143,3 +143,36 @@ def test_binned_points_and_partials_roundtrip(binned, monkeypatch):
         np.testing.assert_array_equal(n1, n0)
         np.testing.assert_allclose(w1, w0, rtol=1e-6)
         assert np.max(np.abs(c1 - c0)) < 1e-3  # float32 centroids at 1.2 km
+
+
+def test_tma_strip_insert_vs_oracle(golden, monkeypatch):
+    """The opt-in TMA strip form of the block-hash insert (EC3R_FI_TMA=1:
+    8-row strips of depth and confidence through a 2-stage cp.async.bulk
+    ring) against the declared fusion rule, and equal keys / counts to the
+    default register-loaded form on a full-resolution bench-generator map."""
+    monkeypatch.setenv("EC3R_FI_TMA", "1")
+    g = golden("mapping")
+    dm, sms, sms_g = _registered(g)
+    for cell in (0.02, 0.05):
+        dm._vmap = None
+        out = dm.fused_cloud(voxel=cell)
+        o = ofuse.fuse_submaps(sms_g, _globs(sms), cell)
+        np.testing.assert_array_equal(out["keys"], o["keys"])
+        np.testing.assert_array_equal(out["count"], o["count"])
+        np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-5)
+        assert np.max(np.abs(out["centroid"] - o["centroid"])) < 1e-4
+    from paper_2510_02080_b200 import mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(31, cfg, seed=11, device="cuda")
+    dm2 = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms2 = [dm2.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+            for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    dm2.register_chain(sms2)
+    slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms2]).astype(np.int32), device="cuda")
+    _, a, _ = mapping.fuse_slots(dm2.pool, slots, 0.02)
+    monkeypatch.delenv("EC3R_FI_TMA")
+    _, b, _ = mapping.fuse_slots(dm2.pool, slots, 0.02)
+    assert a[0].numel() > 100_000
+    assert torch.equal(a[0], b[0]) and torch.equal(a[3], b[3])
+    assert torch.allclose(a[2], b[2], rtol=1e-5)
+    assert float((a[1] - b[1]).abs().max()) < 1e-5
