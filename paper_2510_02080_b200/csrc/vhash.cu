@@ -354,7 +354,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     extern __shared__ float4 sA[];  // A[W], then (TMA) the strip ring [2 stages][2 planes][8 W]
     __shared__ float4 sB[FI_ROWS];
     __shared__ __align__(8) uint64_t strip_full[2];
-    __shared__ int strip_left[2];
     __shared__ unsigned long long cta_cnt[4];
     __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
     const int W = a.W, H = a.H;
@@ -408,7 +407,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         if (threadIdx.x == 0) {
             for (int q = 0; q < 2; ++q) {
                 asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(vh_smem_u32(strip_full + q)) : "memory");
-                strip_left[q] = 0;
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             for (int q = 0; q < 2 && q < n_strips; ++q) issue_strip(q);
@@ -416,38 +414,38 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         __syncthreads();
     }
     int cur_strip = -1;
-    // warp-wide: strips are entered in order, each after its copy landed;
-    // leaving one counts the warp out and the last warp refills the stage
-    auto leave_strip = [&](int s) {
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();
-            if (atomicAdd(&strip_left[s & 1], 1) == FI_NT / 32 - 1) {
-                strip_left[s & 1] = 0;
-                if (s + 2 < n_strips) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    issue_strip(s + 2);
-                }
-            }
-        }
+    // warp-wide: strips are entered in order, each after its copy landed
+    // (full[stage] mbarrier).  Leaving strip s is a named barrier (id 1 +
+    // stage): warps 1..7 arrive, warp 0 syncs -- so it knows every warp is
+    // done with the stage -- and refills it with strip s + 2.
+    auto mbar_wait_vh = [&](uint64_t* bar, uint32_t par) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "VH_WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra VH_WAIT_%=;\n"
+            "}\n" ::"r"(vh_smem_u32(bar)),
+            "r"(par)
+            : "memory");
     };
     auto enter_strip = [&](int s) {
         while (cur_strip < s) {
-            if (cur_strip >= 0) leave_strip(cur_strip);
-            ++cur_strip;
-            if (cur_strip < n_strips) {
-                const uint32_t bar = vh_smem_u32(strip_full + (cur_strip & 1));
-                const uint32_t par = (uint32_t)(cur_strip >> 1) & 1u;
-                asm volatile(
-                    "{\n"
-                    ".reg .pred p;\n"
-                    "VH_WAIT_%=:\n"
-                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-                    "@!p bra VH_WAIT_%=;\n"
-                    "}\n" ::"r"(bar),
-                    "r"(par)
-                    : "memory");
+            if (cur_strip >= 0) {
+                const int id = 1 + (cur_strip & 1);
+                if (warp != 0) {
+                    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(FI_NT) : "memory");
+                } else {
+                    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(FI_NT) : "memory");
+                    if (lane == 0 && cur_strip + 2 < n_strips) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_strip(cur_strip + 2);
+                    }
+                    __syncwarp();
+                }
             }
+            ++cur_strip;
+            if (cur_strip < n_strips) mbar_wait_vh(strip_full + (cur_strip & 1), (uint32_t)(cur_strip >> 1) & 1u);
         }
     };
 
