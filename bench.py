@@ -699,7 +699,7 @@ def run_e2e(step, dm, desc, args, world):
     U0 = int(max(step.out[0].shape[0], step.n_voxels) * 1.25) + 1  # N > 1: the owned partition may be larger
     h_out = [torch.empty((U0,) + tuple(x.shape[1:]), dtype=x.dtype).pin_memory() for x in step.out]
     h_match = torch.empty(int(ao[-1]), dtype=torch.int32).pin_memory()
-    steps = max(2, min(args.steps, 5))
+    steps = max(2, min(args.steps, 20))  # enough steps to amortise the pipeline fill (first H2D)
     out_bytes = 0
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)

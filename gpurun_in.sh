@@ -1,9 +1,7 @@
-T=r02al; O=gpurun_out/$T; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_fusion_engines.py -q -x -k "tma" > $O/tests.log 2>&1; echo tests_rc=$?; tail -2 $O/tests.log
-/usr/local/cuda/bin/compute-sanitizer --tool racecheck --target-processes all --print-limit 20 --error-exitcode 17 python -m pytest tests/test_gpu_fusion_engines.py -m gpu -x -q -p no:cacheprovider -k tma_strip > $O/sanitizer_racecheck_tma.log 2>&1; echo rc=$?; tail -3 $O/sanitizer_racecheck_tma.log
-for v in tma notma; do
-if [ $v = tma ]; then export EC3R_FI_TMA=1; else unset EC3R_FI_TMA; fi
-timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/bench_$v.json 2> $O/bench_$v.err
+T=r02am; O=gpurun_out/$T; mkdir -p $O
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?; tail -2 $O/smoke.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo b_rc=$?
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; echo ref_rc=$?
 python -c "
-import json;d=json.loads(open('$O/bench_$v.json').read().strip().splitlines()[-1]);r=d['rooflines']['fuse_insert'];print('$v', round(d['ms_per_step'],4), round(r['ms'],4))"
-done
+import json;d=json.loads(open('$O/bench.json').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4), d['value'], {k:round(v,3) for k,v in d['stages_ms'].items()}); print(d['e2e']); print(d['roofline']); print(d['clocks'], d['gpu_launches'])
+r=json.loads(open('$O/bench_ref.json').read().strip().splitlines()[-1]); print({k:r[k] for k in ('impl','value','unit','ms_per_step')}, r.get('cpu_baseline',{}).get('sample','')[:200])"
