@@ -33,12 +33,16 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 METRIC = "fused map points/sec and descriptor matches/sec at 1/2/4/8 B200 vs CPU ref"
 
 
-def load_traffic():
+def load_traffic(config: int = 1):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of each hot
-    kernel, from the committed ncu --set full capture (profiles/)."""
-    p = os.path.join(ROOT, "profiles", "kernel_traffic.json")
-    if os.path.exists(p):
-        return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).get("kernels", {}).items()}
+    kernel, from the committed ncu --set full capture of the same config
+    (profiles/kernel_traffic_c<config>.json; kernel_traffic.json holds
+    configs[1]); {} when that config has no capture (traffic null)."""
+    names = [f"kernel_traffic_c{config}.json"] + (["kernel_traffic.json"] if config == 1 else [])
+    for n in names:
+        p = os.path.join(ROOT, "profiles", n)
+        if os.path.exists(p):
+            return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).get("kernels", {}).items()}
     return {}
 
 
@@ -351,11 +355,22 @@ def _ref_submaps(sb, cfg, n_submaps):
     return out, t_ip
 
 
-def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: float = 20.0, use_reference=True):
-    """Times the reference CPU path on a bounded sample of the configs[1]
-    workload and scales it to the GPU step's mix (60 submaps decoded and
-    fused, 59 registration edges, 1500 tracking matches of 1024 x 1024 x 256):
-    step time = 60 x t(submap) + 59 x t(edge) + 1500 x t(match).
+def step_mix(keyframes: int):
+    """(submaps, edges, tracked frames) of one GPU step over `keyframes`
+    keyframes per GPU: KeyframeBuffer flushes of 5 new keyframes (+ the shared
+    old one), one regular edge per submap after the first, 5 tracked frames
+    per keyframe (SURVEY §8(d) cfg 2)."""
+    n_sub = max(keyframes // 5, 1)
+    return n_sub, max(n_sub - 1, 1), 5 * keyframes
+
+
+def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: float = 20.0, use_reference=True,
+               mix=(60, 59, 1500), invalid: float = 0.0):
+    """Times the reference CPU path on a bounded sample of the workload and
+    scales it to the GPU step's mix (S submaps decoded and fused, E
+    registration edges, T tracking matches of 1024 x 1024 x 256; configs[1]:
+    60, 59, 1500; configs[3]: 300, 299, 7500):
+    step time = S x t(submap) + E x t(edge) + T x t(match).
 
     With the reference importable (baseline/_ref): its own inverse_project,
     Mapping._shared_correspondences + the gate of _registration_edges +
@@ -370,7 +385,7 @@ def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: fl
     from paper_2510_02080_b200 import synth
 
     cfg = synth.SceneConfig()
-    sb = synth.make_submaps(5 * n_submaps + 1, cfg, seed=seed, device="cpu")
+    sb = synth.make_submaps(5 * n_submaps + 1, cfg, seed=seed, device="cpu", invalid_fraction=invalid)
     A, B, ao, bo = synth.make_descriptor_pairs(n_match, 1024, 1024, 256, 0.05, seed=seed, device="cpu")
     a = A.view(torch.bfloat16).double().numpy()
     b = B.view(torch.bfloat16).double().numpy()
@@ -427,15 +442,17 @@ def cpu_sample(n_submaps: int = 3, n_match: int = 2, seed: int = 0, budget_s: fl
     t_match = time.perf_counter() - t1
     n_edges = max(n_submaps - 1, 1)
     t_sub, t_edge, t_m = t_fuse / n_submaps, t_edges / n_edges, t_match / done
-    step_s = 60 * t_sub + 59 * t_edge + 1500 * t_m
-    step_pts = pts / n_submaps * 60
+    S, E, T = mix
+    step_s = S * t_sub + E * t_edge + T * t_m
+    step_pts = pts / n_submaps * S
     return {"kind": kind, "points": pts, "points_per_s": step_pts / step_s, "step_s": step_s,
             "t_submap_s": t_sub, "t_edge_s": t_edge, "t_match_s": t_m,
             "pairs_per_s": 1024 * 1024 / t_m,
             "sample": f"{'unmodified reference (baseline/_ref)' if kind == 'reference' else 'oracle port'}: "
                       f"{n_submaps} submaps decoded + fused at 2 cm ({pts} points, 518x392), {n_edges} registration "
-                      f"edge(s), {done} match(es) of 1024x1024x256; scaled to the GPU step's mix "
-                      f"(60 submaps, 59 edges, 1500 matches): step = 60 t_submap + 59 t_edge + 1500 t_match"}
+                      f"edge(s), {done} match(es) of 1024x1024x256"
+                      f"{', %.0f%% invalid pixels' % (100 * invalid) if invalid else ''}; scaled to the GPU step's "
+                      f"mix ({S} submaps, {E} edges, {T} matches): step = {S} t_submap + {E} t_edge + {T} t_match"}
 
 
 def cpu_cores():
@@ -453,9 +470,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS),
-                    help="BASELINE configs[i] preset (1: the headline, 3: 1500-keyframe map, 4: 500 keyframes per "
-                         "GPU with ~50%% invalid pixels)")
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS),
+                    help="BASELINE configs[i] preset (3, the default: the 1500-keyframe map quoted at 1/2/4/8 GPUs, "
+                         "so the driver's scaling curve runs on it; 1: the 300-keyframe sequence; 4: 500 keyframes "
+                         "per GPU with ~50%% invalid pixels)")
     ap.add_argument("--keyframes", type=int, default=None, help="override the preset's keyframes per GPU")
     ap.add_argument("--desc", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -562,7 +580,7 @@ def main():
     P = int(n_points)
     U = step.n_voxels
     C = int(step.seg.shape[0]) * H * W  # overlap pixel pairs streamed by registration
-    traffic = load_traffic()
+    traffic = load_traffic(args.config if args.keyframes == CONFIGS[args.config]["keyframes"] else -1)
 
     def kms(name):  # average launch duration of a hot kernel over the timed region
         t, n = ktimes.get(name, (0.0, 0))
@@ -621,7 +639,7 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        c = cpu_sample()
+        c = cpu_sample(mix=step_mix(args.keyframes), invalid=args.invalid)
         cpu = {"value": c["points_per_s"], "unit": "fused map points/s", "cores": cpu_cores(), "kind": c["kind"],
                "sample": c["sample"], "step_s": c["step_s"], "matches_value": c["pairs_per_s"],
                "matches_unit": "candidate pairs/s", "same_config": True}
@@ -651,7 +669,8 @@ def main():
             "emitted_matches_per_s": n_matches * world / (ms * 1e-3),
             "stages_ms": stages,
             "roofline": dict(roof[dominant], stage=dominant, peak_source=f"{peak_src} MEASURED_PEAKS.json",
-                             traffic_source="profiles/kernel_traffic.json (ncu --set full, dram bytes per launch)"),
+                             traffic_source=f"profiles/kernel_traffic_c{args.config}.json (ncu --set full, dram bytes per "
+                                            "launch of this config)"),
             "rooflines": roof,
             "stage_rooflines": stage_roof,
             "cpu_baseline": cpu,
@@ -955,13 +974,15 @@ def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU implementation (the
     unmodified package from baseline/_ref; the oracle port only when it is
     absent) on the host cores, rank 0 only.  Each step is a bounded sample
-    of the configs[1] workload scaled to the GPU step's mix (cpu_sample)."""
+    of the selected config's workload scaled to its GPU step's mix
+    (cpu_sample, step_mix)."""
     if rank != 0:
         return
     vals, mvals, steps_s = [], [], []
     c = None
     for k in range(args.warmup + args.steps):
-        c = cpu_sample(n_submaps=2, n_match=1, seed=k, budget_s=15.0)
+        c = cpu_sample(n_submaps=2, n_match=1, seed=k, budget_s=15.0, mix=step_mix(args.keyframes),
+                       invalid=args.invalid)
         if k >= args.warmup:
             vals.append(c["points_per_s"])
             mvals.append(c["pairs_per_s"])
@@ -971,10 +992,11 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": float(np.median(steps_s)) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator, CPU)",
             "impl": "reference",
-            "config": {"workload": "configs[1]: TUM-style 300 keyframes / 60 submaps, 1024 descriptors per frame, "
-                                   "tracking match + align + fuse",
+            "config": {"workload": args.workload, "keyframes_per_gpu": args.keyframes,
+                       "invalid_pixel_fraction": args.invalid,
                        "sample": "each step a bounded sample (2 submaps, 1 edge, 1 match) scaled to the full "
-                                 "step's mix: 60 submaps decoded + fused, 59 edges, 1500 matches", "voxel_m": 0.02},
+                                 "step's mix: %d submaps decoded + fused, %d edges, %d matches" %
+                                 step_mix(args.keyframes), "voxel_m": 0.02},
             "matches_per_s": float(np.median(mvals)), "matches_unit": "candidate descriptor pairs/s",
             "cpu_baseline": {"value": v, "unit": "fused map points/s", "cores": cpu_cores(), "kind": c["kind"],
                              "sample": c["sample"]},

@@ -1,7 +1,5 @@
-T=r02am; O=gpurun_out/$T; mkdir -p $O
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?; tail -2 $O/smoke.log
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo b_rc=$?
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; echo ref_rc=$?
+bash tools/gpu_check.sh r02ao full
+O=gpurun_out/r02ao
 python -c "
-import json;d=json.loads(open('$O/bench.json').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4), d['value'], {k:round(v,3) for k,v in d['stages_ms'].items()}); print(d['e2e']); print(d['roofline']); print(d['clocks'], d['gpu_launches'])
-r=json.loads(open('$O/bench_ref.json').read().strip().splitlines()[-1]); print({k:r[k] for k in ('impl','value','unit','ms_per_step')}, r.get('cpu_baseline',{}).get('sample','')[:200])"
+import json;d=json.loads(open('$O/bench.log').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d['config']['workload'][:40], {k:round(v,3) for k,v in d['stages_ms'].items()}); print(d['e2e']['ms_per_step'], d['cpu_baseline']['value'], d['cpu_baseline']['sample'][-120:])" 2>&1 | tail -3
+tail -2 $O/gpu_tests.log; cat $O/kernel_traffic.json | head -40
