@@ -1,5 +1,7 @@
-bash tools/gpu_check.sh r02ao full
-O=gpurun_out/r02ao
+T=r02ap; O=gpurun_out/$T; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_chain.py tests/test_gpu_parity.py tests/test_gpu_bench_parity.py tests/test_gpu_dist.py -q -x -k "chain or regist or bench or window or loop" > $O/tests.log 2>&1; echo tests_rc=$?; tail -2 $O/tests.log
+for c in 3 1; do
+timeout 600 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/bench_c$c.json 2> $O/bench_c$c.err
 python -c "
-import json;d=json.loads(open('$O/bench.log').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d['config']['workload'][:40], {k:round(v,3) for k,v in d['stages_ms'].items()}); print(d['e2e']['ms_per_step'], d['cpu_baseline']['value'], d['cpu_baseline']['sample'][-120:])" 2>&1 | tail -3
-tail -2 $O/gpu_tests.log; cat $O/kernel_traffic.json | head -40
+import json;d=json.loads(open('$O/bench_c$c.json').read().strip().splitlines()[-1]);print('c$c', round(d['ms_per_step'],4), {k:round(v,3) for k,v in d['stages_ms'].items()}, round(d['rooflines']['register']['ms'],4))"
+done

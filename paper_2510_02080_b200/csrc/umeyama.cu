@@ -881,17 +881,33 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
         int* an1 = an0 + n_sub;
         int* rt0 = an1 + n_sub;
         int* rt1 = rt0 + n_sub;
-        // statuses and strongest edges first (sequential: a submap that is
-        // not committed is not a partner of later submaps)
-        if (threadIdx.x == 0)
-            for (int j = 0; j < n_sub; ++j) {
+        // statuses and strongest edges first.  A submap that is not
+        // committed is not a partner of later submaps, so status j depends on
+        // its partners' (all < j): rounds of parallel re-evaluation from
+        // "all committed" reach the sequential walk's result (after round r
+        // every submap r partner-levels deep is final) and stop when nothing
+        // changes -- two rounds when every edge is usable
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) sst_w[j] = EC3R_ST_OK;
+        __syncthreads();
+        for (;;) {
+            for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
                 int st;
-                const int best = chain_select(j, eo, est, ec, ep, sst_w, &st);
-                sst_w[j] = st;
-                an0[j] = best >= 0 ? ep[best] : -1;
-                rt0[j] = best >= 0 ? -1 : j;
-                rt1[j] = best;
+                rt1[j] = chain_select(j, eo, est, ec, ep, sst_w, &st);
+                an1[j] = st;
             }
+            __syncthreads();
+            int changed = 0;
+            for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
+                changed |= an1[j] != sst_w[j];
+                sst_w[j] = an1[j];
+            }
+            if (!__syncthreads_or(changed)) break;
+        }
+        for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
+            const int best = rt1[j];
+            an0[j] = best >= 0 ? ep[best] : -1;
+            rt0[j] = best >= 0 ? -1 : j;
+        }
         __syncthreads();
         for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) {
             const int best = rt1[j];
@@ -941,15 +957,12 @@ __global__ void __launch_bounds__(CHAIN_NT) chain_poses_kernel(
         for (int i = threadIdx.x; i < 8 * n_sub; i += CHAIN_NT) sub_globals[i] = g[i];
         for (int j = threadIdx.x; j < n_sub; j += CHAIN_NT) sub_status[j] = sst[j];
     }
-    const int s_end = sub_slot_off[n_sub];
-    for (int sidx = threadIdx.x; sidx < s_end; sidx += CHAIN_NT) {
-        // slot -> submap: slots of a submap are contiguous (sub_slot_off)
-        int lo = 0, hi = n_sub;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (sub_slot_off[mid] <= sidx) lo = mid; else hi = mid;
-        }
-        for (int k = 0; k < 8; ++k) slot_globals[8 * sidx + k] = g[8 * lo + k];
+    // slot broadcast: a warp per submap, lane (slot, k) of its contiguous
+    // slots (sub_slot_off) -- no per-slot search through global offsets
+    const int lane = threadIdx.x & 31;
+    for (int j = threadIdx.x >> 5; j < n_sub; j += CHAIN_NT / 32) {
+        const int s0 = sub_slot_off[j], s1 = sub_slot_off[j + 1];
+        for (int i = lane; i < 8 * (s1 - s0); i += 32) slot_globals[8 * (size_t)s0 + i] = g[8 * j + (i & 7)];
     }
 }
 
