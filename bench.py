@@ -607,7 +607,15 @@ def main():
     # chain, fusion, sorted emit) against HBM with SURVEY §8(d)'s bytes
     # (depth-input variant: 8 B/px + 16 B per overlap pair + 24 B per voxel),
     # and the whole matcher (tensor pass + certification) against bf16
-    af_ms = stages["reg"] + stages["chain"] + stages["insert"] + stages["emit"]
+    # the emit stage runs beside the matcher (it waits for SMs the matcher
+    # holds), so the align + fuse figure takes the emit timed alone, after the
+    # timed region, on the step's own map and buffers
+    emit_alone = None
+    if step.exchange is None:
+        torch.cuda.synchronize()
+        emit_alone = _time_ms(lambda: step.vmap.extract(sort=True, out=step.out, sync=False), reps=10, warm=2)
+        stages["emit_alone"] = emit_alone
+    af_ms = stages["reg"] + stages["chain"] + stages["insert"] + (emit_alone if emit_alone else stages["emit"])
     af_bytes = 8 * P + 16 * C + 24 * U
     stage_roof = {
         "align_fuse": {"bound": "hbm", "ms": af_ms, "alg_bytes": af_bytes, "unit": "GB/s",
