@@ -231,10 +231,12 @@ struct PoolArgs {
 // through a float reciprocal is exact while px < 2^21 (relative error 2^-22
 // against a fractional-part distance of at least 1/(2W)); larger images take
 // the integer division.
-__device__ __forceinline__ void pix_uv(const PoolArgs& a, int px, int& u, int& v) {
-    if (a.inv_w > 0.f) v = __float2int_rd(__fmul_rn((float)px + 0.5f, a.inv_w));
-    else v = px / a.W;
-    u = px - v * a.W;
+// (scalars, not the PoolArgs reference: a reference to the kernel parameter
+// makes ptxas copy the struct to local memory and reload it per pixel)
+__device__ __forceinline__ void pix_uv(float inv_w, int W, int px, int& u, int& v) {
+    if (inv_w > 0.f) v = __float2int_rd(__fmul_rn((float)px + 0.5f, inv_w));
+    else v = px / W;
+    u = px - v * W;
 }
 
 // Shared column tables are stored by (u mod 4, u / 4): the lanes of a warp
@@ -409,6 +411,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     rg.parity = 0;
     rg.next = 0;
     const bool use_tma = a.use_tma != 0;
+    const float inv_w = a.inv_w;
     if (threadIdx.x == 0 && use_tma) {
         for (int st = 0; st < RE_NS; ++st)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(re_smem_u32(ring_bar + st)) : "memory");
@@ -542,7 +545,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             const float zB[4] = {zb.x, zb.y, zb.z, zb.w}, cB[4] = {wb.x, wb.y, wb.z, wb.w};
             uint32_t kbits = 0;
             int u0, v0;
-            pix_uv(a, pix, u0, v0);
+            pix_uv(inv_w, W, pix, u0, v0);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const bool valid = zA[k] > 0.f && zB[k] > 0.f;
@@ -565,7 +568,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
                 if (keep) {
                     kbits |= 1u << (8 * k);
                     int u = u0 + k, v = v0;
-                    if (u >= W) pix_uv(a, pix + k, u, v);
+                    if (u >= W) pix_uv(inv_w, W, pix + k, u, v);
                     const int cu = col_ix(u, Wq);
                     const double zaa = zA[k], zbb = zB[k];
                     double pp[3], qq[3];
@@ -656,7 +659,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
             if (!((double)wf >= floorv)) continue;
             const float zA = a.depth[(size_t)sa * HW + ent.y], zB = a.depth[(size_t)sb * HW + ent.y];
             int u, v;
-            pix_uv(a, ent.y, u, v);
+            pix_uv(inv_w, W, ent.y, u, v);
             const double x = xc[col_ix(u, Wq)], y = yc[v];
             double R[3][3], t[3], pp[3], qq[3];
             load_rot(a.slot_poses + 8 * sa, R, t);
@@ -744,7 +747,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
                 const float wf = fminf(cA[k], cB[k]);
                 if (zA[k] > 0.f && zB[k] > 0.f && (double)wf >= floorv) {
                     int u, v;
-                    pix_uv(a, pix + k, u, v);
+                    pix_uv(inv_w, W, pix + k, u, v);
                     const double z = zA[k];
                     double d[3];
                     for (int i = 0; i < 3; ++i) d[i] = z * (colA[i * Wp + col_ix(u, Wq)] + rowA[i * a.H + v]) + tAB[i];
