@@ -309,6 +309,54 @@ def test_voxel_fusion_full_resolution_submaps():
     assert st["n_slow_path"] < 0.02 * st["n_points_in"]
 
 
+@pytest.mark.parametrize("hw", [(389, 517), (392, 517), (391, 518)])
+def test_odd_frame_shapes_registration_and_fusion_vs_oracle(hw):
+    """Frames cropped to shapes the vectorised paths do not cover: an odd
+    width (scalar loads in fusion), H*W % 4 != 0 (registration leaves the TMA
+    ring for the direct walk and its ragged 4-pixel groups cross row ends):
+    edge statuses, keep counts and masks exact and Sim(3) within 1e-5 of the
+    oracle (mapping.py:162-188); voxel keys / counts bit-exact, centroids
+    within 1e-4 m (oracle/fuse.py)."""
+    from paper_2510_02080_b200 import mapping, synth
+    H, W = hw
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(16, cfg, seed=13, device="cuda")
+    depth = sb.depth[:, :H, :W].contiguous()
+    conf = sb.conf[:, :H, :W].contiguous()
+    dm = mapping.DenseMapping(H, W, sb.K4)  # cropping right / bottom keeps (fx, fy, cx, cy)
+    sms = [dm.add_submap(ids, depth[o:o + len(ids)], conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    dense = []
+    for ids, o in zip(sb.frame_ids, sb.slot_offsets):
+        F = len(ids)
+        dense.append(dict(depth=depth[o:o + F].cpu().numpy(), conf=conf[o:o + F].cpu().numpy(),
+                          frame_ids=np.array(ids), pose_q=sb.poses8[o:o + F, 1:5], pose_t=sb.poses8[o:o + F, 5:],
+                          K=sb.K4))
+    pairs = [(sms[j], sms[j - 1]) for j in range(1, len(sms))]
+    res, km = mapping.register_edges(dm.pool, pairs, with_keep_masks=True)
+    km = km.cpu().numpy()
+    for j, r in zip(range(1, len(sms)), res):
+        e = ref.registration_edge(dense[j], dense[j - 1])
+        assert e["status"] == ref.STATUS_OK and r.status == 0, (j, e["status"], r.status)
+        assert r.count == e["count"]
+        sh = [i for i, kf in enumerate(dense[j]["frame_ids"]) if kf in list(dense[j - 1]["frame_ids"])][0]
+        fb = list(dense[j - 1]["frame_ids"]).index(dense[j]["frame_ids"][sh])
+        both = (dense[j]["depth"][sh] > 0) & (dense[j - 1]["depth"][fb] > 0)
+        np.testing.assert_array_equal(km[j - 1][both].astype(bool), e["keep"])
+        tr = r.transform
+        _assert_sim3(tr.scale, tr.rotation.q, tr.translation, e["s"], e["q"], e["t"])
+    dm.register_chain(sms)
+    out = dm.fused_cloud(voxel=0.02)
+    globs = [(sm.global_pose.scale, np.asarray(sm.global_pose.rotation.q), np.asarray(sm.global_pose.translation))
+             for sm in sms]
+    o = ofuse.fuse_submaps(dense, globs, 0.02)
+    np.testing.assert_array_equal(out["keys"], o["keys"])
+    np.testing.assert_array_equal(out["count"], o["count"])
+    assert np.max(np.abs(out["centroid"] - o["centroid"])) < 1e-4
+    np.testing.assert_allclose(out["wsum"], o["wsum"], rtol=1e-4)
+    assert out["stats"]["n_points_in"] == o["n_in"]
+
+
 def test_voxel_points_api_and_extreme_coordinates():
     """insert_points path, out-of-range keys flagged, keys exact far from the origin."""
     from paper_2510_02080_b200 import mapping
