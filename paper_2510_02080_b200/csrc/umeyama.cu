@@ -18,6 +18,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1051,12 +1052,12 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
     // = the co-resident clusters of size c (cudaOccupancyMaxActiveClusters;
     // sizes 5-7 measured slower: they pack the GPCs worse).  EC3R_RE_CL
     // forces c.
-    static int max_clusters[4] = {0, 0, 0, 0};
+    static std::atomic<int> max_clusters[4];  // per cluster size, computed once (benign duplicate queries)
     int ncl = 4;
     double best = 1e30;
     for (int i = 0; i < 4; ++i) {
         const int c = 1 << i;
-        if (max_clusters[i] == 0) {
+        if (max_clusters[i].load() == 0) {
             cudaLaunchConfig_t q = {};
             q.gridDim = dim3((unsigned)(c * 64));
             q.blockDim = dim3(UM_NT);
@@ -1073,9 +1074,10 @@ extern "C" int ec3r_register_edges(const float* depth_pool, const float* conf_po
                 cudaGetLastError();
                 nc = std::max(1, 2 * kNumSMs / c);
             }
-            max_clusters[i] = nc;
+            max_clusters[i].store(nc);
         }
-        const double cost = (double)((n_edges + max_clusters[i] - 1) / max_clusters[i]) * (1.0 / c + 0.03);
+        const int mc = max_clusters[i].load();
+        const double cost = (double)((n_edges + mc - 1) / mc) * (1.0 / c + 0.03);
         if (cost < best - 1e-12) { best = cost; ncl = c; }
     }
     if (const char* f = getenv("EC3R_RE_CL")) ncl = std::min(8, std::max(1, atoi(f)));
