@@ -1,8 +1,9 @@
-T=r02ax; O=gpurun_out/$T; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "match" > $O/tests.log 2>&1; echo tests_rc=$?; tail -1 $O/tests.log
-for v in default row1 default row1; do
+T=r02ay; O=gpurun_out/$T; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_chain.py -q -x -k "regist or chain or single_pass or odd_frame" > $O/tests.log 2>&1; echo tests_rc=$?; tail -1 $O/tests.log
+for v in default syncall default syncall; do
 if [ $v = default ]; then unset EC3R_B200_LIB; else export EC3R_B200_LIB=variants/libec3r_$v.so; fi
-timeout 600 python bench.py --config 1 --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/bench_$v.json 2> $O/bench_$v.err
+for c in 1 3; do
+timeout 600 python bench.py --config $c --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/bench_${v}_$c.json 2> $O/bench_${v}_$c.err
 python -c "
-import json;d=json.loads(open('$O/bench_$v.json').read().strip().splitlines()[-1]);print('$v', round(d['ms_per_step'],4), round(d['rooflines']['match']['ms'],4), round(d['rooflines']['match']['frac'],4))"
-done
+import json;d=json.loads(open('$O/bench_${v}_$c.json').read().strip().splitlines()[-1]);print('$v c$c', round(d['ms_per_step'],4), round(d['rooflines']['register']['ms'],4), round(d['rooflines']['register']['frac'],4))"
+done; done
