@@ -237,7 +237,7 @@ class Step:
             # tracking matcher on its own stream (inputs ready: it follows the
             # step's start on the current stream)
             ms = self.match_stream if self.overlap != "serial" else main
-            ms.wait_event(ev["t_insert"] if self.overlap == "late" else ev["t0"])
+            ms.wait_event(ev[{"late": "t_insert", "mid": "t_reg"}.get(self.overlap, "t0")])
             ev["m0"] = torch.cuda.Event(enable_timing=True)
             ev["m0"].record(ms)
             nvtx.range_push("match")
@@ -247,7 +247,7 @@ class Step:
             ev["m1"] = torch.cuda.Event(enable_timing=True)
             ev["m1"].record(ms)
 
-        if self.overlap != "late":
+        if self.overlap in ("early", "serial"):
             launch_match()
         ev["t_reg0"] = self._event()
         # registration of all edges (one launch) + device pose chain (one launch)
@@ -255,6 +255,8 @@ class Step:
         out = self.plan.run(self.dm.pool) if self.chain is None else self.chain.run()
         nvtx.range_pop()
         ev["t_reg"] = self._event()  # both launches: stage "reg" = registration + chain
+        if self.overlap == "mid":
+            launch_match()
         self.edge_status, self.sub_status = out[4], out[6]
         ev["t_chain"] = self._event()
         if self.vmap is None:

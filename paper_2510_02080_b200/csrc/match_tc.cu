@@ -1125,7 +1125,10 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     if (prm.n_units > 0) {
         const size_t smem = tc_smem_bytes(prm.kblocks);
         EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int grid = prm.n_units < kNumSMs ? prm.n_units : kNumSMs;
+        int grid = prm.n_units < kNumSMs ? prm.n_units : kNumSMs;
+        // EC3R_MT_GRID caps the persistent grid (SMs left free for concurrent
+        // mapping kernels on another stream)
+        if (const char* g = getenv("EC3R_MT_GRID")) grid = std::max(1, std::min(grid, atoi(g)));
         KernelTimer tk(TK_MATCH_TC, st);
         mt_tc_kernel<<<grid, TC_THREADS, smem, st>>>(tmA, tmB, prm);
         EC3R_CHECK_LAUNCH("mt_tc_kernel");
