@@ -562,46 +562,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 }
             }
         }
-#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 1
-        // experiment: keys only
-#pragma unroll
-        for (int k = 0; k < 4; ++k) n_oor += (unsigned)(cx[k] ^ cy[k] ^ cz[k]) & (valid[k] ? 1u : 0u);
-        continue;
-#endif
-#if defined(EC3R_FI_EXP) && (EC3R_FI_EXP == 3 || EC3R_FI_EXP == 4)
-        // experiment: one read-only directory load per pixel instead of the cache / table
-        {
-            uint32_t vidx[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t hb = (uint32_t)table_slot(pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2), 0xFFFFFFFFull) % 100000u;
-                const uint32_t g = __ldg(a.vb.block_slot + hb);
-                vidx[k] = valid[k] ? (((hb ^ (g & 1u)) << 6) | (uint32_t)((cx[k] & 3) | ((cy[k] & 3) << 2) | ((cz[k] & 3) << 4))) : 0xFFFFFFFFu;
-            }
-#if EC3R_FI_EXP == 4
-#pragma unroll
-            for (int k = 0; k < 4; ++k) n_oor += vidx[k] & 1u;
-#else
-            float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f, qn = 0.f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float c = cs[k];
-                const float cont = (k > 0 && vidx[k] == vidx[k - 1]) ? 1.f : 0.f;
-                qx = fmaf(cont, qx, c * (ox[k] - (float)cx[k] * cellf));
-                qy = fmaf(cont, qy, c * (oy[k] - (float)cy[k] * cellf));
-                qz = fmaf(cont, qz, c * (oz[k] - (float)cz[k] * cellf));
-                qw = fmaf(cont, qw, c);
-                qn = fmaf(cont, qn, 1.f);
-                const bool last = vidx[k] != 0xFFFFFFFFu && (k == 3 || vidx[k + 1 < 4 ? k + 1 : 3] != vidx[k]);
-                if (last) {
-                    red_add_v4(a.vb.sums + vidx[k], qx, qy, qz, qw);
-                    red_add_u32(a.vb.counts + vidx[k], (uint32_t)qn);
-                }
-            }
-#endif
-        }
-        continue;
-#endif
         // phase B: block indices.  The CTA's shared-memory block cache maps
         // an exact 30-bit block key relative to the frame's camera block to
         // the pool block; the four lookups of a lane are independent LDS.64.
@@ -666,11 +626,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 if (miss[k]) got[k] = g;
             }
         }
-#if defined(EC3R_FI_EXP) && EC3R_FI_EXP == 2
-#pragma unroll
-        for (int k = 0; k < 4; ++k) n_oor += (unsigned)got[k] & 1u;
-        continue;
-#endif
         // phase C: reductions into the pool.  Consecutive pixels of the lane
         // in the same voxel form a run whose sums ride along (FFMA with a
         // 0/1 continuation flag); only a run's last pixel issues the two
