@@ -40,31 +40,28 @@ def main():
     st = vmap.stats()
     st["voxels"] = vmap.count()
     extra = {}
+    # the reduction floor of this insert (ec3r_vhash_diag_log / _replay): its
+    # runs logged in issue order, then replayed as pure reductions
     L = _lib.lib()
-    if hasattr(L, "ec3r_exp_replay"):
-        # EC3R_FI_EXP=6 variant: the insert logged its runs; replay them as
-        # pure reductions (the atomic floor of this address stream)
-        import ctypes as C
-        L.ec3r_exp_log_count.restype = C.c_longlong
-        assert L.ec3r_exp_log_alloc(C.c_longlong(80 << 20)) == 0
-        vmap.clear()
-        vmap.insert_frames(dm.pool, slots)
-        torch.cuda.synchronize()
-        n_runs = L.ec3r_exp_log_count()
-        for wc in (1, 0, 3, 2):
-            rt = []
-            for _ in range(args.reps + 2):
-                vmap.clear()
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record()
-                assert L.ec3r_exp_replay(vmap._h, 148 * 8, wc) == 0
-                b.record()
-                torch.cuda.synchronize()
-                rt.append(a.elapsed_time(b))
-            extra[{1: "replay_ms", 0: "replay_sums_only_ms", 3: "replay_addr_only_ms",
-                   2: "replay_addr_only_sums_only_ms"}[wc]] = float(np.median(rt[2:]))
-        extra["runs"] = int(n_runs)
+    cap = int(slots.numel()) * dm.pool.H * dm.pool.W
+    runs = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+    n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    vmap.clear()
+    _lib.check(L.ec3r_vhash_diag_log(vmap._h, _lib.ptr(runs), cap, _lib.ptr(n_dev)), "ec3r_vhash_diag_log")
+    vmap.insert_frames(dm.pool, slots)
+    extra["runs"] = int(n_dev.item())
+    for wc, key in ((1, "replay_ms"), (0, "replay_sums_only_ms")):
+        rt = []
+        for _ in range(args.reps + 2):
+            vmap.clear()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            _lib.check(L.ec3r_vhash_diag_replay(vmap._h, _lib.ptr(runs), _lib.ptr(n_dev), cap, wc, None), "replay")
+            b.record()
+            torch.cuda.synchronize()
+            rt.append(a.elapsed_time(b))
+        extra[key] = float(np.median(rt[2:]))
     print(json.dumps({"lib": os.environ.get("EC3R_B200_LIB", "default"), "insert_ms": float(np.median(ts[2:])),
                       "min_ms": float(np.min(ts[2:])), "stats": {k: int(v) for k, v in st.items()}, **extra}))
 
