@@ -216,7 +216,8 @@ EC3R_API int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, co
  * counting them; the map is left unchanged.  ec3r_vhash_diag_replay issues
  * exactly the logged reductions into h's pool (a float4 add per run, plus
  * the u32 count add when with_count != 0): the cost of the insert's own
- * reduction stream without its loads, keys and lookups. */
+ * reduction stream without its loads, keys and lookups.  Block-hash engine
+ * only (EC3R_EARG on a map created for the binned engine). */
 EC3R_API int ec3r_vhash_diag_log(ec3r_vhash* h, void* runs, int64_t cap, unsigned long long* n_dev);
 EC3R_API int ec3r_vhash_diag_replay(ec3r_vhash* h, const void* runs, const unsigned long long* n_dev, int64_t cap,
                                     int with_count, void* stream);

@@ -1822,6 +1822,7 @@ extern "C" int ec3r_vhash_stats_device(ec3r_vhash* h, int64_t* out5, void* strea
 
 extern "C" int ec3r_vhash_diag_log(ec3r_vhash* h, void* runs, int64_t cap, unsigned long long* n_dev) {
     if (!h || !runs || !n_dev || cap <= 0) return EC3R_EARG;
+    if (h->bf) return EC3R_EARG;  // the block-hash engine's reductions only (the binned engine has none)
     h->diag_runs = static_cast<uint2*>(runs);
     h->diag_n = n_dev;
     h->diag_cap = cap;
