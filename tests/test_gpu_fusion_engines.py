@@ -176,3 +176,33 @@ def test_tma_strip_insert_vs_oracle(golden, monkeypatch):
     assert torch.equal(a[0], b[0]) and torch.equal(a[3], b[3])
     assert torch.allclose(a[2], b[2], rtol=1e-5)
     assert float((a[1] - b[1]).abs().max()) < 1e-5
+
+
+def test_reduction_floor_diag_log_and_replay():
+    """ec3r_vhash_diag_log / _replay (the bench's reduction-floor measure):
+    the logged runs cover every fused point exactly once (their counts sum to
+    n_points_in), the logging insert leaves the map unreduced, and replaying
+    the log with counts reproduces the normal insert's voxel keys and counts."""
+    from paper_2510_02080_b200 import _lib, mapping, synth
+    cfg = synth.SceneConfig()
+    sb = synth.make_submaps(11, cfg, seed=7, device="cuda")
+    dm = mapping.DenseMapping(cfg.height, cfg.width, sb.K4)
+    sms = [dm.add_submap(ids, sb.depth[o:o + len(ids)], sb.conf[o:o + len(ids)], list(sb.poses8[o:o + len(ids)]))
+           for ids, o in zip(sb.frame_ids, sb.slot_offsets)]
+    dm.register_chain(sms)
+    slots = torch.as_tensor(np.concatenate([sm.slots for sm in sms]).astype(np.int32), device="cuda")
+    vm, ref_out, st = mapping.fuse_slots(dm.pool, slots, 0.02)
+    L = _lib.lib()
+    cap = int(slots.numel()) * cfg.height * cfg.width
+    runs = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+    n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    vm.clear()
+    _lib.check(L.ec3r_vhash_diag_log(vm._h, _lib.ptr(runs), cap, _lib.ptr(n_dev)), "diag_log")
+    vm.insert_frames(dm.pool, slots)
+    n = int(n_dev.item())
+    assert 0 < n <= st["n_points_in"]
+    assert int(runs[:n, 1].sum().item()) == st["n_points_in"]
+    assert vm.count() == 0  # logged, not reduced
+    _lib.check(L.ec3r_vhash_diag_replay(vm._h, _lib.ptr(runs), _lib.ptr(n_dev), cap, 1, None), "diag_replay")
+    keys, _, _, cnt = vm.extract(sort=True)
+    assert torch.equal(keys, ref_out[0]) and torch.equal(cnt, ref_out[3])
