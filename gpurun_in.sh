@@ -1,8 +1,14 @@
-T=r02be; O=gpurun_out/$T; mkdir -p $O
-timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29521 bench.py --gpus 4 --steps 3 --warmup 3 --no-extras > $O/n4_c3.json 2> $O/n4_c3.err; echo n4_rc=$?
-tail -1 $O/n4_c3.json | python -c "
-import json,sys;d=json.loads(sys.stdin.read());print(d['n_gpus'], round(d['ms_per_step'],2), d['value'], d['config'].get('validation_only','')[:60], d['config']['workload'][:30])"
-timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29522 bench.py --gpus 8 --config 1 --steps 3 --warmup 3 --no-extras --no-e2e > $O/n8_c1.json 2> $O/n8_c1.err; echo n8_rc=$?
-tail -1 $O/n8_c1.json | python -c "
-import json,sys;d=json.loads(sys.stdin.read());print(d['n_gpus'], round(d['ms_per_step'],2), d['value'], d['config'].get('validation_only','')[:60])"
-tail -3 $O/n8_c1.err | cut -c1-200
+T=r02bh; O=gpurun_out/$T; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_bench_parity.py -q -x -k "match or bench_tracking" > $O/tests.log 2>&1; echo tests_rc=$?; tail -1 $O/tests.log
+for v in default oldfin; do
+if [ $v = default ]; then unset EC3R_B200_LIB; else export EC3R_B200_LIB=variants/libec3r_$v.so; fi
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:mx_finalize|mt_need_cols" -c 4 --csv --log-file $O/l_$v.csv python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --no-floor > /dev/null 2>&1
+python - <<PY
+import csv
+rows=[r for r in csv.reader(open('$O/l_$v.csv')) if len(r)>10]
+h=rows[0]; i=h.index('Kernel Name'); j=h.index('Metric Value')
+for r in rows[1:]: print('$v', r[i][:20], r[j])
+PY
+done
+for c in 3 1; do timeout 600 python bench.py --config $c --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/b$c.json 2>/dev/null; python -c "
+import json;d=json.loads(open('$O/b$c.json').read().strip().splitlines()[-1]);print('c$c', round(d['ms_per_step'],4), {k:round(v,3) for k,v in d['stages_ms'].items()})"; done

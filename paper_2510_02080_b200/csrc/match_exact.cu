@@ -173,8 +173,24 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
                                    int64_t total_a, double ratio2, int32_t* __restrict__ match_b,
                                    int32_t* __restrict__ n_match) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the CTA's first pair once (a proportional guess, exact for equal-sized
+    // pairs, else the binary search), then each row steps forward: a CTA's
+    // rows span few pairs
+    __shared__ int p_cta;
+    if (threadIdx.x == 0) {
+        const int64_t r0 = (int64_t)blockIdx.x * blockDim.x < total_a ? (int64_t)blockIdx.x * blockDim.x : total_a - 1;
+        const int64_t g = total_a > 0 ? r0 * n_pairs / total_a : 0;
+        int q = (int)(g < (int64_t)n_pairs - 1 ? g : (int64_t)n_pairs - 1);
+        int steps = 0;
+        while (q > 0 && a_off[q] > r0 && steps < 4) { --q; ++steps; }
+        while (q + 1 < n_pairs && a_off[q + 1] <= r0 && steps < 8) { ++q; ++steps; }
+        const bool ok = a_off[q] <= r0 && (q + 1 >= n_pairs || a_off[q + 1] > r0);
+        p_cta = ok ? q : find_pair(a_off, n_pairs, r0);
+    }
+    __syncthreads();
     if (r >= total_a) return;
-    const int p = find_pair(a_off, n_pairs, r);
+    int p = p_cta;
+    while (p + 1 < n_pairs && a_off[p + 1] <= r) ++p;
     const int64_t a0 = a_off[p], b0 = b_off[p], m = b_off[p + 1] - b0;
     int out = -1;
     const MatchRowState s = rs[r];

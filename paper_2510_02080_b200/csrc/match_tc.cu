@@ -722,8 +722,18 @@ __device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int n_pa
 // all threads of the CTA (it contains a barrier).
 __device__ __forceinline__ int pair_of_cta(const int64_t* __restrict__ off, int n_pairs, int64_t r, int64_t total) {
     __shared__ int p0;
-    if (threadIdx.x == 0) p0 = pair_of(off, n_pairs, (int64_t)blockIdx.x * blockDim.x < total
-                                                          ? (int64_t)blockIdx.x * blockDim.x : total - 1);
+    if (threadIdx.x == 0) {
+        const int64_t r0 = (int64_t)blockIdx.x * blockDim.x < total ? (int64_t)blockIdx.x * blockDim.x : total - 1;
+        // proportional guess (exact for equal-sized pairs, the batched
+        // tracking case), a few steps either way, else the binary search
+        const int64_t g = total > 0 ? r0 * n_pairs / total : 0;
+        int q = (int)(g < (int64_t)n_pairs - 1 ? g : (int64_t)n_pairs - 1);
+        int steps = 0;
+        while (q > 0 && off[q] > r0 && steps < 4) { --q; ++steps; }
+        while (q + 1 < n_pairs && off[q + 1] <= r0 && steps < 8) { ++q; ++steps; }
+        const bool ok = off[q] <= r0 && (q + 1 >= n_pairs || off[q + 1] > r0);
+        p0 = ok ? q : pair_of(off, n_pairs, r0);
+    }
     __syncthreads();
     int p = p0;
     if (r < total)
