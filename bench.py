@@ -481,7 +481,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--no-floor", action="store_true", help="skip the fusion reduction-floor replay")
+    ap.add_argument("--no-floor", action="store_true",
+                    help="skip the post-timing diagnostics (fusion reduction-floor replay, emit timed alone); "
+                         "ncu launch lists use it so they hold the steps only")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: validation of the N>1 path with ranks sharing a GPU (not a measurement)")
     args = ap.parse_args()
@@ -613,7 +615,7 @@ def main():
     # holds), so the align + fuse figure takes the emit timed alone, after the
     # timed region, on the step's own map and buffers
     emit_alone = None
-    if step.exchange is None:
+    if step.exchange is None and not args.no_floor:
         torch.cuda.synchronize()
         emit_alone = _time_ms(lambda: step.vmap.extract(sort=True, out=step.out, sync=False), reps=10, warm=2)
         stages["emit_alone"] = emit_alone
