@@ -562,8 +562,9 @@ def main():
         step.async_exchange = False
     elif step.exchange is None and not step.emit_sync:
         step.n_voxels = int(step.n_dev.item())  # U of the last step (device count, read after the timed region)
-        if step.n_voxels > int(step.out[0].shape[0]):
-            raise RuntimeError("voxel emit exceeded the preallocated rows")
+        if step.n_voxels > int(step.out[0].shape[0]) or step.vmap.stats()["n_overflow"] != 0:
+            raise RuntimeError("host-sync-free voxel emit overflowed (rows or 32-bit keys): "
+                               "rerun with EC3R_BENCH_EMIT_SYNC=1")
     ktimes = _lib.kernel_times()  # per hot kernel: CUDA events on its launching stream
     if world > 1:
         dist.barrier()

@@ -832,6 +832,7 @@ static unsigned grid_for(int64_t n) {
 
 __global__ void bbox_init_kernel(int* bbox) {
     if (threadIdx.x < 3) { bbox[threadIdx.x] = INT_MAX; bbox[3 + threadIdx.x] = INT_MIN; }
+    if (threadIdx.x == 6 || threadIdx.x == 7) bbox[threadIdx.x] = 0;  // column emit: the 32-bit key overflow flag
 }
 
 // Compaction, pass 1 (one warp per pool block): occupied voxels per block
@@ -1100,13 +1101,19 @@ __global__ void vc_bbox_kernel(const unsigned long long* __restrict__ block_keys
 }
 
 __global__ void vc_key32_kernel(const unsigned long long* __restrict__ block_keys,
-                                const unsigned long long* __restrict__ counters, int64_t nb, int* __restrict__ bb,
-                                uint32_t* __restrict__ skey, uint32_t* __restrict__ ids) {
+                                unsigned long long* __restrict__ counters, int64_t nb, int* __restrict__ bb,
+                                uint32_t* __restrict__ skey, uint32_t* __restrict__ ids, int report) {
     const int64_t used = vc_used(counters, nb);
     const bool fits = used == 0 || ((unsigned)(bb[3] - bb[0]) < (1u << VC_XB) &&
                                     (unsigned)(bb[4] - bb[1]) < (1u << VC_YB) &&
                                     (unsigned)(bb[5] - bb[2]) < (1u << VC_ZB));
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !fits) bb[6] = 1;
+    // a map that outgrew the 32-bit keys: the host-read emit re-runs with
+    // 64-bit keys; the host-sync-free emit reports it as emit overflow
+    // (counters[5], stats n_overflow), so its caller re-runs synced
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !fits) {
+        bb[6] = 1;
+        if (report) atomicAdd(&counters[5], 1ull);
+    }
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         uint32_t k = 0xFFFFFFFFu;
         if (b < used && fits) {
@@ -1255,14 +1262,14 @@ static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsu
     // 32-bit sort keys (4 radix passes instead of 8) when the host knows the
     // map's block extent fit them at the last read-back; a map that outgrew
     // them is caught by the flag read below and re-emitted with 64-bit keys
-    const bool k32 = read_count && h->emit_key32;
+    const bool k32 = h->emit_key32;  // fit established by an earlier host-read emit (checked on the device)
     EC3R_CUDA_TRY(cudaMemsetAsync(w.scan_in, 0, sizeof(uint32_t) * (size_t)(nb * 16 + 1), st));
     const unsigned gw = (unsigned)std::min<int64_t>((nb * 32 + 255) / 256, (int64_t)kNumSMs * 16);
     vc_block_prep_kernel<<<gw, 256, 0, st>>>(h->counts, h->block_keys, h->counters, nb, w.colcnt, w.skey, w.ids);
     EC3R_CHECK_LAUNCH("vc_block_prep_kernel");
-    const int bb_init[8] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN, 0, 0};
-    if (read_count) {  // the box is always measured when the host reads back (it decides the next emit's keys)
-        EC3R_CUDA_TRY(cudaMemcpyAsync(w.bb, bb_init, sizeof(bb_init), cudaMemcpyHostToDevice, st));
+    if (read_count || k32) {  // the box decides the next emit's key width (host read) / this emit's keys
+        bbox_init_kernel<<<1, 32, 0, st>>>(w.bb);
+        EC3R_CHECK_LAUNCH("bbox_init_kernel");
         const unsigned gb = (unsigned)std::min<int64_t>((nb + 255) / 256, (int64_t)kNumSMs * 4);
         vc_bbox_kernel<<<gb, 256, 0, st>>>(h->block_keys, h->counters, nb, w.bb);
         EC3R_CHECK_LAUNCH("vc_bbox_kernel");
@@ -1270,7 +1277,7 @@ static int column_emit(ec3r_vhash* h, int64_t* keys, float* centroid, float* wsu
     const unsigned gt = (unsigned)std::min<int64_t>((nb + 255) / 256, (int64_t)kNumSMs * 8);
     size_t cb = w.cub_bytes;
     if (k32) {
-        vc_key32_kernel<<<gt, 256, 0, st>>>(h->block_keys, h->counters, nb, w.bb, w.skey32, w.ids);
+        vc_key32_kernel<<<gt, 256, 0, st>>>(h->block_keys, h->counters, nb, w.bb, w.skey32, w.ids, read_count ? 0 : 1);
         EC3R_CHECK_LAUNCH("vc_key32_kernel");
         if (cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.skey32, w.skey32_s, w.ids, w.ids_s, (int)nb, 0, 32,
                                             st) != cudaSuccess) {

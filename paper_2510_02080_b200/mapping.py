@@ -272,7 +272,9 @@ class VoxelMap:
         tensors of length U (sorted by key when sort=True).  `out` may hold
         preallocated buffers of at least U rows.  sync=False (sorted only):
         no host read of U; returns the full `out` buffers plus the device
-        int64[1] count instead."""
+        int64[1] count instead -- check stats()["n_overflow"] == 0 afterwards
+        (it also counts a map that outgrew the 32-bit sort keys a previous
+        synced extract chose; re-run with sync=True then)."""
         L = _lib.lib()
         if out is None:
             if not sync:

@@ -399,6 +399,44 @@ def test_voxel_sorted_emit_key_widths():
         assert np.max(np.abs(c - o["centroid"])) < 1e-4
 
 
+def test_voxel_sync_free_emit_key_widths():
+    """The host-sync-free sorted emit (extract(sync=False), the bench step's)
+    uses the 32-bit block keys a previous synced extract established and checks
+    the fit on the device: equal output to the synced emit while the map fits,
+    and a reported overflow (stats n_overflow) -- not silently wrong keys --
+    once the map outgrows them; a synced extract then recovers."""
+    from paper_2510_02080_b200 import mapping
+    rng = np.random.default_rng(12)
+    vm = mapping.VoxelMap(0.02, 1 << 20)
+    sim = np.array([1.0, 1.0, 0, 0, 0, 0.0, 0.0, 0.0])
+
+    def fill(spread):
+        p = rng.normal(size=(50_000, 3)) * np.array([spread, 1.0, 0.5])
+        conf = rng.uniform(0.05, 1.0, size=len(p))
+        vm.clear()
+        vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"), sim)
+        return p, conf
+
+    p, conf = fill(2.0)
+    ref_out = tuple(x.clone() for x in vm.extract())  # synced: establishes the 32-bit fit
+    U = int(ref_out[0].shape[0])
+    out = tuple(torch.empty_like(x) for x in ref_out)
+    k, c, w, n, n_dev = vm.extract(out=out, sync=False)
+    assert int(n_dev.item()) == U and vm.stats()["n_overflow"] == 0
+    for a, b in zip((k, c, w, n), ref_out):
+        assert torch.equal(a, b)
+    p, conf = fill(60.0)  # > 2048 blocks of 8 cm in x: outgrows the 32-bit keys
+    big = tuple(torch.empty((U * 4,) + tuple(x.shape[1:]), dtype=x.dtype, device="cuda") for x in ref_out)
+    vm.extract(out=big, sync=False)
+    assert vm.stats()["n_overflow"] > 0
+    vm.clear()
+    vm.insert_points(torch.as_tensor(p, device="cuda"), torch.as_tensor(conf, device="cuda"), sim)
+    k, c, w, n = (x.cpu().numpy() for x in vm.extract())
+    o = ofuse.fuse_points(p, conf, 0.02)
+    np.testing.assert_array_equal(k, o["keys"])
+    np.testing.assert_array_equal(n, o["count"])
+
+
 def test_voxel_partials_owner_buckets_and_merge_roundtrip():
     """Multi-GPU device half: extract_partials buckets every voxel by
     owner = mix64(key) mod n (dist.owner_of), and merging all buckets into a
