@@ -237,7 +237,11 @@ EC3R_API int ec3r_vhash_extract(ec3r_vhash* h, int64_t* keys, float* centroid, f
                        size_t workspace_bytes, void* stream);
 /* sort: 0 = block order, 1 = key order (U read back to the host, see
  * ec3r_vhash_extract_count), 2 = key order without the host read (U only in
- * *n_out on the device). */
+ * *n_out on the device).  The block sort uses 32-bit relative keys once a
+ * sort = 1 extract found the map's block extent fits them; sort = 2 checks
+ * that fit on the device and, if the map has outgrown it, counts an emit
+ * overflow (ec3r_vhash_stats_get n_overflow) instead of re-running: check the
+ * stats after a sort = 2 extract and repeat it with sort = 1 on overflow. */
 /* Voxel count of the last sorted extract on this handle (already known on
  * the host), or -1: lets a caller size its outputs without a device read. */
 EC3R_API int64_t ec3r_vhash_extract_count(const ec3r_vhash* h);
