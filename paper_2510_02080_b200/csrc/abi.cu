@@ -53,7 +53,8 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
                  cudaStream_t st);
 int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
                        const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
-                       int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st);
+                       const MatchRowD* rsd, int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws,
+                       cudaStream_t st);
 size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs);
 
 }  // namespace ec3r
@@ -98,6 +99,7 @@ extern "C" size_t ec3r_match_workspace(const int64_t* a_off_h, const int64_t* b_
     if (!a_off_h || !b_off_h || n_pairs < 0) return 0;
     const int64_t total_a = a_off_h[n_pairs], total_b = b_off_h[n_pairs];
     return 3 * align256(sizeof(int64_t) * (size_t)(n_pairs + 1)) + align256(sizeof(MatchRowState) * (size_t)total_a) +
+           align256(sizeof(MatchRowD) * (size_t)total_a) +
            align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int32_t) * (size_t)total_a) +
            align256(sizeof(int32_t) * (size_t)total_b) + align256(sizeof(int64_t) * 8) +
            match_tc_workspace(a_off_h, b_off_h, n_pairs);
@@ -137,6 +139,7 @@ extern "C" int ec3r_match_batched_rows(const uint16_t* A, const uint16_t* B, con
     int64_t* b_off = cv.take<int64_t>(n_pairs + 1);
     int64_t* b_row = cv.take<int64_t>(n_pairs + 1);
     MatchRowState* rs = cv.take<MatchRowState>(total_a);
+    MatchRowD* rsd = cv.take<MatchRowD>(total_a);
     int32_t* col_best = cv.take<int32_t>(total_b);
     int32_t* flag_rows = cv.take<int32_t>(total_a);
     int32_t* flag_cols = cv.take<int32_t>(total_b);
@@ -160,23 +163,23 @@ extern "C" int ec3r_match_batched_rows(const uint16_t* A, const uint16_t* B, con
         if (rc) return rc;
         if (tc_used) {
             rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, flag_rows, counters + 0, 0,
-                                      nullptr, nullptr, 0, rs, col_best, st);
+                                      nullptr, nullptr, 0, rs, rsd, col_best, st);
             if (rc) return rc;
-            rc = match_tc_need_cols(a_off, b_off, a_off_h, b_off_h, n_pairs, ratio, eps_tc, rs, col_best, flag_cols,
-                                    counters, tc_ws, st);
+            rc = match_tc_need_cols(a_off, b_off, a_off_h, b_off_h, n_pairs, ratio, eps_tc, rs, rsd, col_best,
+                                    flag_cols, counters, tc_ws, st);
             if (rc) return rc;
             rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, nullptr, nullptr, 0,
-                                      flag_cols, counters + 1, 0, rs, col_best, st);
+                                      flag_cols, counters + 1, 0, rs, rsd, col_best, st);
         } else {
             rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, flag_rows, counters + 0, 0,
-                                      flag_cols, counters + 1, 0, rs, col_best, st);
+                                      flag_cols, counters + 1, 0, rs, rsd, col_best, st);
         }
     } else {
         rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, nullptr, nullptr, total_a, nullptr,
-                                  nullptr, total_b, rs, col_best, st);
+                                  nullptr, total_b, rs, rsd, col_best, st);
     }
     if (rc) return rc;
-    return match_finalize(rs, col_best, a_off, b_off, n_pairs, total_a, ratio, match_b, n_match, st);
+    return match_finalize(rs, rsd, col_best, a_off, b_off, n_pairs, total_a, ratio, match_b, n_match, st);
 }
 
 extern "C" int ec3r_match_stats(const void* workspace, int64_t total_a, int64_t total_b, int n_pairs,
@@ -187,6 +190,7 @@ extern "C" int ec3r_match_stats(const void* workspace, int64_t total_a, int64_t 
     cv.take<int64_t>(n_pairs + 1);
     cv.take<int64_t>(n_pairs + 1);
     cv.take<MatchRowState>(total_a);
+    cv.take<MatchRowD>(total_a);
     cv.take<int32_t>(total_b);
     cv.take<int32_t>(total_a);
     cv.take<int32_t>(total_b);

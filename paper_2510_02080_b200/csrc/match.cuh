@@ -6,13 +6,18 @@
 namespace ec3r {
 
 // Per A-row outcome of the row side of match_descriptors (tracking.py:155,166).
+// The hot part is 8 bytes (read by every certification pass); the float64
+// (d1, d2) of a row live in a separate MatchRowD array, written only by the
+// exact re-scan and read only when ratio_ok == -1.
 struct MatchRowState {
-    double d1;   // d2 value of the best column
-    double d2;   // second order statistic of the row's d2 values
-    int32_t best;  // best column within the pair (first index on ties), -1 if none
-    int32_t ratio_ok;  // -1: decide from (d1, d2); 0 / 1: ratio test already certified reject / pass
-    int32_t mutual;    // -1: decide from col_best; 0 / 1: mutual check certified (tracking.py:160-162)
-    int32_t pad;
+    int32_t best;     // best column within the pair (first index on ties), -1 if none
+    int8_t ratio_ok;  // -1: decide from (d1, d2); 0 / 1: ratio test already certified reject / pass
+    int8_t mutual;    // -1: decide from col_best; 0 / 1: mutual check certified (tracking.py:160-162)
+    int16_t pad;
+};
+struct MatchRowD {
+    double d1;  // d2 value of the best column
+    double d2;  // second order statistic of the row's d2 values
 };
 
 // 16-byte row chunks widened to float64 (rows are 16-byte aligned: D is
@@ -72,9 +77,10 @@ __device__ __forceinline__ double warp_dot16(const T* a, const T* b, int D, int 
 int match_exact_dispatch(const void* A, const void* B, int dtype, int D, const int64_t* a_off, const int64_t* b_off,
                          const int64_t* b_row, int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
                          const int32_t* cols, const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs,
+                         MatchRowD* rsd,
                          int32_t* col_best, cudaStream_t st);
 
-int match_finalize(const MatchRowState* rs, const int32_t* col_best, const int64_t* a_off, const int64_t* b_off,
+int match_finalize(const MatchRowState* rs, const MatchRowD* rsd, const int32_t* col_best, const int64_t* a_off, const int64_t* b_off,
                    int n_pairs, int64_t total_a, double ratio, int32_t* match_b, int32_t* n_match, cudaStream_t st);
 
 }  // namespace ec3r

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A,
                                                         const int64_t* __restrict__ b_row, int n_pairs,
                                                         const int32_t* __restrict__ rows,
                                                         const int64_t* __restrict__ n_rows_ptr, int64_t n_rows_all,
-                                                        MatchRowState* __restrict__ rs) {
+                                                        MatchRowState* __restrict__ rs, MatchRowD* __restrict__ rsd) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ double sd1[MX_WARPS], sd2[MX_WARPS];
     __shared__ int si1[MX_WARPS];
@@ -113,11 +113,13 @@ __global__ void __launch_bounds__(MX_NT) mx_rows_kernel(const T* __restrict__ A,
                 if (better(sd1[w], si1[w], m1, mi)) { m2 = fmin(m1, sd2[w]); m1 = sd1[w]; mi = si1[w]; }
                 else m2 = fmin(m2, sd1[w]);
             }
-            rs[r].best = (b1 > b0) ? mi : -1;
-            rs[r].d1 = m1;
-            rs[r].d2 = m2;
-            rs[r].ratio_ok = -1;
-            rs[r].mutual = -1;
+            MatchRowState h;
+            h.best = (b1 > b0) ? mi : -1;
+            h.ratio_ok = -1;
+            h.mutual = -1;
+            h.pad = 0;
+            rs[r] = h;
+            rsd[r] = MatchRowD{m1, m2};
         }
         __syncthreads();
     }
@@ -168,7 +170,8 @@ __global__ void __launch_bounds__(MX_NT) mx_cols_kernel(const T* __restrict__ A,
 }
 
 // Final decision per A row (tracking.py:159-169).
-__global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const int32_t* __restrict__ col_best,
+__global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const MatchRowD* __restrict__ rsd,
+                                   const int32_t* __restrict__ col_best,
                                    const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
                                    int64_t total_a, double ratio2, int32_t* __restrict__ match_b,
                                    int32_t* __restrict__ n_match) {
@@ -197,7 +200,10 @@ __global__ void mx_finalize_kernel(const MatchRowState* __restrict__ rs, const i
     if (m > 0 && s.best >= 0) {
         bool keep;
         if (s.ratio_ok >= 0) keep = s.ratio_ok != 0;  // certified from the tensor-core keys
-        else keep = !(m > 1 && s.d1 > ratio2 * s.d2);
+        else {
+            const MatchRowD d = rsd[r];
+            keep = !(m > 1 && d.d1 > ratio2 * d.d2);
+        }
         if (keep && (s.mutual == 1 || (s.mutual == -1 && col_best[b0 + s.best] == (int)(r - a0)))) out = s.best;
     }
     match_b[r] = out;
@@ -211,14 +217,14 @@ template <typename T>
 int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int64_t* b_off, const int64_t* b_row,
                  int n_pairs,
                  const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all, const int32_t* cols,
-                 const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs, int32_t* col_best,
+                 const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs, MatchRowD* rsd, int32_t* col_best,
                  cudaStream_t st) {
     if (D % Vec16<T>::N != 0) return EC3R_EARG;  // rows must be 16-byte chunked
     const size_t smem = 0;
     const unsigned grid = kNumSMs * 8;
     if (rows != nullptr || n_rows_all > 0) {
         mx_rows_kernel<T><<<grid, 256, smem, st>>>(A, B, D, a_off, b_off, b_row, n_pairs, rows, n_rows_ptr, n_rows_all,
-                                                    rs);
+                                                    rs, rsd);
         EC3R_CHECK_LAUNCH("mx_rows_kernel");
     }
     if (cols != nullptr || n_cols_all > 0) {
@@ -232,26 +238,27 @@ int launch_exact(const T* A, const T* B, int D, const int64_t* a_off, const int6
 int match_exact_dispatch(const void* A, const void* B, int dtype, int D, const int64_t* a_off, const int64_t* b_off,
                          const int64_t* b_row, int n_pairs, const int32_t* rows, const int64_t* n_rows_ptr, int64_t n_rows_all,
                          const int32_t* cols, const int64_t* n_cols_ptr, int64_t n_cols_all, MatchRowState* rs,
-                         int32_t* col_best, cudaStream_t st) {
+                         MatchRowD* rsd, int32_t* col_best, cudaStream_t st) {
     switch (dtype) {
         case 0:
             return launch_exact<uint16_t>((const uint16_t*)A, (const uint16_t*)B, D, a_off, b_off, b_row, n_pairs, rows,
-                                          n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
+                                          n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, rsd, col_best, st);
         case 1:
             return launch_exact<float>((const float*)A, (const float*)B, D, a_off, b_off, b_row, n_pairs, rows, n_rows_ptr,
-                                       n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
+                                       n_rows_all, cols, n_cols_ptr, n_cols_all, rs, rsd, col_best, st);
         case 2:
             return launch_exact<double>((const double*)A, (const double*)B, D, a_off, b_off, b_row, n_pairs, rows,
-                                        n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, col_best, st);
+                                        n_rows_ptr, n_rows_all, cols, n_cols_ptr, n_cols_all, rs, rsd, col_best, st);
     }
     return EC3R_EARG;
 }
 
-int match_finalize(const MatchRowState* rs, const int32_t* col_best, const int64_t* a_off, const int64_t* b_off,
+int match_finalize(const MatchRowState* rs, const MatchRowD* rsd, const int32_t* col_best, const int64_t* a_off,
+                   const int64_t* b_off,
                    int n_pairs, int64_t total_a, double ratio, int32_t* match_b, int32_t* n_match, cudaStream_t st) {
     EC3R_CUDA_TRY(cudaMemsetAsync(n_match, 0, sizeof(int32_t) * n_pairs, st));
     if (total_a == 0) return EC3R_OK;
-    mx_finalize_kernel<<<(unsigned)((total_a + 255) / 256), 256, 0, st>>>(rs, col_best, a_off, b_off, n_pairs,
+    mx_finalize_kernel<<<(unsigned)((total_a + 255) / 256), 256, 0, st>>>(rs, rsd, col_best, a_off, b_off, n_pairs,
                                                                          total_a, ratio * ratio, match_b, n_match);
     EC3R_CHECK_LAUNCH("mx_finalize_kernel");
     return EC3R_OK;

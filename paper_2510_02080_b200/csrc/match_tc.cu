@@ -297,7 +297,7 @@ constexpr double kRatioSlack = 1e-9;
 // Returns false when the row needs the float64 re-scan.
 __device__ __forceinline__ bool row_decision(const RowCand& c, int64_t M, double eps_tc, double ratio2,
                                              MatchRowState& s) {
-    s.d1 = INFINITY; s.d2 = INFINITY; s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
+    s.best = -1; s.ratio_ok = 0; s.mutual = 0; s.pad = 0;
     if (M == 0) return true;  // no columns: no match
     if (M == 1) {             // one column: argmax certain, ratio test skipped (tracking.py:165)
         s.best = 0;
@@ -790,7 +790,8 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
                              int64_t total_a, const RowCand* __restrict__ cand, int n_split,
                              const unsigned long long* __restrict__ col_slots,
                              const long long* __restrict__ pair_slot, double eps_tc, double ratio2,
-                             MatchRowState* __restrict__ rs, int32_t* __restrict__ col_best,
+                             MatchRowState* __restrict__ rs, const MatchRowD* __restrict__ rsd,
+                             int32_t* __restrict__ col_best,
                              int32_t* __restrict__ pending, int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int p = pair_of_cta(a_off, n_pairs, r, total_a);
@@ -799,7 +800,9 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
     const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
     const MatchRowState s = rs[r];
     if (M == 0 || s.best < 0) return;
-    const bool keep = s.ratio_ok == 1 || (s.ratio_ok == -1 && (M <= 1 || !(s.d1 > ratio2 * s.d2)));
+    // (d1, d2) exist only for rows the exact re-scan decided (ratio_ok == -1)
+    const MatchRowD sd = s.ratio_ok == -1 ? rsd[r] : MatchRowD{INFINITY, INFINITY};
+    const bool keep = s.ratio_ok == 1 || (s.ratio_ok == -1 && (M <= 1 || !(sd.d1 > ratio2 * sd.d2)));
     if (!keep) return;
     const int64_t c = b0 + s.best, lr = r - a0;
     // merge the column's per-unit top-2 keys (units = 256-row blocks)
@@ -839,7 +842,7 @@ __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* _
             const RowCand rcand = cand[r * n_split];
             double kv = 0.0, ke = -1.0;
             if (rcand.c1 == s.best) { kv = rcand.k1; ke = key_eps(kv, eps_tc); }
-            else if (s.ratio_ok == -1 && s.d1 > 0.0) { kv = 1.0 - 0.5 * s.d1; ke = 1e-12; }
+            else if (s.ratio_ok == -1 && sd.d1 > 0.0) { kv = 1.0 - 0.5 * sd.d1; ke = 1e-12; }
             if (ke >= 0.0 && cv - key_eps(cv, eps_tc) > kv + ke) mutual = 0;
         }
     }
@@ -1163,12 +1166,13 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
 // columns that need the float64 column re-scan.  col_best is reset to -1.
 int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
                        const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
-                       int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws, cudaStream_t st) {
+                       const MatchRowD* rsd, int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws,
+                       cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
     const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     EC3R_CUDA_TRY(cudaMemsetAsync(col_best, 0xFF, sizeof(int32_t) * (size_t)tb, st));
     mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split, w.slots, w.pair_slot,
-                                                               eps_tc, ratio * ratio, rs, col_best, flag_cols,
+                                                               eps_tc, ratio * ratio, rs, rsd, col_best, flag_cols,
                                                                counters);
     EC3R_CHECK_LAUNCH("mt_need_cols");
     return EC3R_OK;
