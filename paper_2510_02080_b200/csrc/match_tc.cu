@@ -892,31 +892,51 @@ __global__ void mt_flag_all_kernel(int32_t* __restrict__ list, int64_t n) {
 __global__ void __launch_bounds__(1024) mt_unit_scan(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off,
                                                     int n_pairs, int n_split, long long* __restrict__ unit_base,
                                                     long long* __restrict__ pair_slot) {
+    // each thread owns kPer consecutive pairs (serial prefix in registers),
+    // one block scan of the per-thread totals per 1024 * kPer pairs: one
+    // pass for batches up to 8,192 pairs (7,500 tracked frames: ~30 -> ~5 us)
+    constexpr int kPer = 8;
     using BScan = cub::BlockScan<long long, 1024>;
     __shared__ typename BScan::TempStorage scan_tmp;
     __shared__ long long base_u, base_s;
     if (threadIdx.x == 0) { base_u = 0; base_s = 0; }
     __syncthreads();
-    for (int p0 = 0; p0 < n_pairs; p0 += 1024) {
-        const int p = p0 + threadIdx.x;
-        long long nu = 0, ns = 0;
-        if (p < n_pairs) {
-            const int64_t M = b_off[p + 1] - b_off[p], N = a_off[p + 1] - a_off[p];
-            if (M > 0) {
-                const long long tiles = (M + TC_BN - 1) / TC_BN;
-                const long long rb = (N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM);
-                nu = rb * (tiles < n_split ? tiles : n_split);
-                ns = rb * M;
+    for (int p0 = 0; p0 < n_pairs; p0 += 1024 * kPer) {
+        const int q0 = p0 + threadIdx.x * kPer;
+        auto counts = [&](int p, long long& nu, long long& ns) {
+            nu = 0; ns = 0;
+            if (p < n_pairs) {
+                const int64_t M = b_off[p + 1] - b_off[p], N = a_off[p + 1] - a_off[p];
+                if (M > 0) {
+                    const long long tiles = (M + TC_BN - 1) / TC_BN;
+                    const long long rb = (N + TC_NA * TC_BM - 1) / (TC_NA * TC_BM);
+                    nu = rb * (tiles < n_split ? tiles : n_split);
+                    ns = rb * M;
+                }
             }
+        };
+        long long su = 0, ss = 0;
+        for (int k = 0; k < kPer; ++k) {  // totals, then the writes recompute (the offsets sit in L1)
+            long long nu, ns;
+            counts(q0 + k, nu, ns);
+            su += nu;
+            ss += ns;
         }
-        // exclusive block scans (warp shuffles; one barrier pair per scan)
         long long eu, es, tu, ts;
-        BScan(scan_tmp).ExclusiveSum(nu, eu, tu);
+        BScan(scan_tmp).ExclusiveSum(su, eu, tu);
         __syncthreads();
-        BScan(scan_tmp).ExclusiveSum(ns, es, ts);
-        if (p < n_pairs) {
-            unit_base[p] = base_u + eu;
-            pair_slot[p] = base_s + es;
+        BScan(scan_tmp).ExclusiveSum(ss, es, ts);
+        long long cu = base_u + eu, cs = base_s + es;
+        for (int k = 0; k < kPer; ++k) {
+            const int p = q0 + k;
+            long long nu, ns;
+            counts(p, nu, ns);
+            if (p < n_pairs) {
+                unit_base[p] = cu;
+                pair_slot[p] = cs;
+            }
+            cu += nu;
+            cs += ns;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -936,10 +956,16 @@ __global__ void mt_units_kernel(const int64_t* __restrict__ a_off, const int64_t
                                 const long long* __restrict__ pair_slot, int64_t n_units, TcUnit* __restrict__ units) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= n_units) return;
-    int lo = 0, hi = n_pairs;  // unit_base[lo] <= u < unit_base[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (unit_base[mid] <= u) lo = mid; else hi = mid;
+    // proportional guess (exact for equal-sized pairs), else binary search
+    const int64_t tot = unit_base[n_pairs];
+    int lo = (int)min((int64_t)n_pairs - 1, tot > 0 ? u * n_pairs / tot : (int64_t)0);
+    if (!(unit_base[lo] <= u && u < unit_base[lo + 1])) {
+        lo = 0;
+        int hi = n_pairs;  // unit_base[lo] <= u < unit_base[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (unit_base[mid] <= u) lo = mid; else hi = mid;
+        }
     }
     while (lo + 1 < n_pairs && unit_base[lo + 1] <= u) ++lo;  // skip pairs without units
     const int p = lo;
