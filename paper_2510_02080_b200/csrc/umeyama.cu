@@ -399,7 +399,7 @@ register_edges_kernel(PoolArgs a, double* __restrict__ out_sim3, double* __restr
     const int e = blockIdx.x / a.ncl;
     const int s0 = a.edge_seg[e], s1 = a.edge_seg[e + 1];
     __shared__ double scratch[(UM_NT / 32) * 24];
-    __shared__ double part2[24], part3[4];
+    __shared__ double part2[24];
     __shared__ double tot2[24], tot3[4];
     __shared__ Solution sol;
     for (int u = threadIdx.x; u < a.W; u += UM_NT) xc[col_ix(u, Wq)] = (u - a.cx) / a.fx;
