@@ -1,9 +1,15 @@
-T=r02fin4; O=gpurun_out/$T; mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo tests_rc=$?; tail -1 $O/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?; tail -1 $O/smoke.log
-timeout 900 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err; echo c3_rc=$?
-timeout 900 python bench.py --config 1 > $O/bench_c1.json 2> $O/bench_c1.err; echo c1_rc=$?
-for c in c3 c1; do python -c "
-import json;d=json.loads(open('$O/bench_$c.json').read().strip().splitlines()[-1]);print('$c', round(d['ms_per_step'],4), d['value'], {k:(round(v['ms'],4), round(v['frac'],4)) for k,v in d['rooflines'].items()}, round(d['roofline'].get('reduction_floor',{}).get('frac',0),3), round(d['e2e']['ms_per_step'],2), d['cpu_baseline']['value'], d['stage_rooflines']['align_fuse']['frac'])"; done
-for cl in 4 8; do EC3R_RE_CL=$cl timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/re_$cl.json 2>/dev/null; python -c "
-import json;d=json.loads(open('$O/re_$cl.json').read().strip().splitlines()[-1]);print('c3 cl$cl', round(d['rooflines']['register']['ms'],4))"; done
+T=r02fin5; O=gpurun_out/$T; mkdir -p $O
+for c in 3 1; do
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:vh_insert_frames_kernel|register_edges_kernel|mt_tc_kernel" -c 6 \
+  -o $O/prof_c$c python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/ncu_c$c.log 2>&1; echo full_rc=$?
+python tools/ncu_traffic.py $O/prof_c$c.ncu-rep > $O/kernel_traffic_c$c.json 2> $O/traffic_c$c.err
+tools/ncu_metrics.sh $O/prof_c$c.ncu-rep > $O/full_metrics_c$c.txt 2>&1
+ncu -i $O/prof_c$c.ncu-rep --page source --csv --print-source sass > $O/source.csv 2>/dev/null
+python tools/ncu_stalls.py $O/source.csv 25 > $O/stalls_c$c.txt 2>&1
+rm -f $O/source.csv
+done
+rm -f $O/*.ncu-rep
+python -c "
+import json
+for c in (3,1):
+  d=json.load(open('$O/kernel_traffic_c%d.json'%c))['kernels']; print(c, {k:(round(v['dram_bytes_per_launch']/1e9,3), round(v['ncu_ms_per_launch'],3)) for k,v in d.items()})"
