@@ -1,15 +1,5 @@
-T=r02fin5; O=gpurun_out/$T; mkdir -p $O
-for c in 3 1; do
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:vh_insert_frames_kernel|register_edges_kernel|mt_tc_kernel" -c 6 \
-  -o $O/prof_c$c python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/ncu_c$c.log 2>&1; echo full_rc=$?
-python tools/ncu_traffic.py $O/prof_c$c.ncu-rep > $O/kernel_traffic_c$c.json 2> $O/traffic_c$c.err
-tools/ncu_metrics.sh $O/prof_c$c.ncu-rep > $O/full_metrics_c$c.txt 2>&1
-ncu -i $O/prof_c$c.ncu-rep --page source --csv --print-source sass > $O/source.csv 2>/dev/null
-python tools/ncu_stalls.py $O/source.csv 25 > $O/stalls_c$c.txt 2>&1
-rm -f $O/source.csv
-done
-rm -f $O/*.ncu-rep
-python -c "
-import json
-for c in (3,1):
-  d=json.load(open('$O/kernel_traffic_c%d.json'%c))['kernels']; print(c, {k:(round(v['dram_bytes_per_launch']/1e9,3), round(v['ncu_ms_per_launch'],3)) for k,v in d.items()})"
+T=r02bm; O=gpurun_out/$T; mkdir -p $O
+for g in 148 144 140 136 128; do for c in 1 3; do
+EC3R_MT_GRID=$g timeout 600 python bench.py --config $c --steps 40 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/b_${g}_$c.json 2>/dev/null; python -c "
+import json;d=json.loads(open('$O/b_${g}_$c.json').read().strip().splitlines()[-1]);print('grid $g c$c', round(d['ms_per_step'],4), {k:round(v,3) for k,v in d['stages_ms'].items()})"
+done; done
