@@ -332,6 +332,13 @@ constexpr int BC_BITS = EC3R_BC_BITS;  // shared-memory block cache: 2048 entrie
 #endif
 constexpr int FI_G = EC3R_FI_G;
 
+#ifndef EC3R_FI_DEDUP
+#define EC3R_FI_DEDUP 0  // 1: merge a reduction slot's equal-voxel run ends across lanes before issuing
+                         // (halves the reduction floor, but the hand-off makes the insert slower:
+                         // 1.36 vs 1.19 ms on configs[1], profiles/r02g_fusion_conflicts.json)
+#endif
+constexpr bool FI_DEDUP = EC3R_FI_DEDUP != 0;
+
 // Opt-in (EC3R_FI_TMA=1): on the bench workload the strip ring measured 1.4 %
 // slower than the register-prefetched 64-bit loads (1.198 vs 1.181 ms,
 // profiles/r02ag_*): the kernel runs at its reduction floor, and the strip
@@ -356,6 +363,8 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     __shared__ __align__(8) uint64_t strip_full[2];
     __shared__ unsigned long long cta_cnt[4];
     __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
+    __shared__ float4 dd_sum[FI_DEDUP ? FI_NT : 1];      // per-slot run hand-off to the group's lowest lane
+    __shared__ float dd_n[FI_DEDUP ? FI_NT : 1];
     const int W = a.W, H = a.H;
     const int HW = H * W;
     const int v_band = blockIdx.x * FI_ROWS;
@@ -449,13 +458,15 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         }
     };
 
+    const int n_sy = (rows + ST_H - 1) / ST_H;
+    auto row_of = [&](int sy_) { return sy_ * ST_H + dv; };
     // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
     auto advance = [&](int& sy, int& sx) {
         sx += FI_NT / 32;
         while (sx >= stx) { sx -= stx; ++sy; }
     };
     auto load4 = [&](int sy, int sx, float (&z)[4], float (&c)[4]) {
-        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+        const int r = row_of(sy), u0 = sx * ST_W + du;
 #pragma unroll
         for (int k = 0; k < 4; ++k) { z[k] = 0.f; c[k] = 0.f; }
         if (r >= rows) return;
@@ -476,7 +487,6 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         }
     };
 
-    const int n_sy = (rows + ST_H - 1) / ST_H;
     int sy = 0, sx = warp;
     while (sx >= stx) { sx -= stx; ++sy; }
     int py = sy, px = sx;  // prefetch cursor
@@ -485,7 +495,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         if (py < n_sy) load4(py, px, nz, nc);
     }
     for (; sy < n_sy; advance(sy, sx)) {
-        const int r = sy * ST_H + dv, u0 = sx * ST_W + du;
+        const int r = row_of(sy), u0 = sx * ST_W + du;
         float zs[4], cs[4];
         if constexpr (TMA) {
             enter_strip(sy);
@@ -646,13 +656,49 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             rz = fmaf(cont, rz, c * (oz[k] - (float)cz[k] * cellf));
             rw = fmaf(cont, rw, c);
             rn = fmaf(cont, rn, 1.f);
-            const bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
+            bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
+            float sx = rx, sy = ry, sz = rz, sw = rw, sn = rn;
+            if constexpr (FI_DEDUP) {
+                // Lanes of one reduction instruction that target the same
+                // voxel serialise in the memory pipeline (the replayed log
+                // with each 32-run group's equal voxels merged takes 0.60 ms
+                // instead of 1.13 ms for 14 % fewer runs,
+                // tools/fuse_order_probe.py), so equal run ends of this slot
+                // (mostly vertical neighbours) are summed into their lowest
+                // lane first and issued once.  Opt-in: the live kernel is
+                // latency-bound at 16 warps per SM, and the shared-memory
+                // hand-off costs more than the reductions it removes.
+                const unsigned peers = __match_any_sync(0xffffffffu, last ? vid[k] : 0xFFFFFFFFu);
+                const bool grp = last && (peers & (peers - 1u)) != 0u;
+                if (__any_sync(0xffffffffu, grp)) {
+                    if (grp) {
+                        dd_sum[threadIdx.x] = make_float4(rx, ry, rz, rw);
+                        dd_n[threadIdx.x] = rn;
+                    }
+                    __syncwarp();
+                    if (grp) {
+                        if (lane == __ffs(peers) - 1) {
+                            unsigned o = peers & (peers - 1u);  // the other members
+                            while (o) {
+                                const int b = (threadIdx.x & ~31) + __ffs(o) - 1;
+                                o &= o - 1u;
+                                const float4 v = dd_sum[b];
+                                sx += v.x; sy += v.y; sz += v.z; sw += v.w;
+                                sn += dd_n[b];
+                            }
+                        } else {
+                            last = false;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
             if (last) {
                 if constexpr (LOG) {
-                    log_run(RunLog{a.log_runs, a.log_n, a.log_cap}, vid[k], (uint32_t)rn);
+                    log_run(RunLog{a.log_runs, a.log_n, a.log_cap}, vid[k], (uint32_t)sn);
                 } else {
-                    red_add_v4(a.vb.sums + vid[k], rx, ry, rz, rw);
-                    red_add_u32(a.vb.counts + vid[k], (uint32_t)rn);
+                    red_add_v4(a.vb.sums + vid[k], sx, sy, sz, sw);
+                    red_add_u32(a.vb.counts + vid[k], (uint32_t)sn);
                 }
             }
         }
