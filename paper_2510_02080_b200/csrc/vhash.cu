@@ -321,7 +321,12 @@ __global__ void vh_replay_runs_kernel(const uint2* __restrict__ runs, const unsi
     }
 }
 
-constexpr int ST_H = 8, ST_W = 16;
+#ifndef EC3R_FI_PX
+#define EC3R_FI_PX 4  // horizontally adjacent pixels per lane (4 or 2; sub-tile 8 x 4*FI_PX)
+#endif
+constexpr int FI_PX = EC3R_FI_PX;
+static_assert(FI_PX == 4 || FI_PX == 2, "FI_PX");
+constexpr int ST_H = 8, ST_W = 4 * FI_PX;
 #ifndef EC3R_BC_BITS
 #define EC3R_BC_BITS 11
 #endif
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     }
     const float inv = a.inv_cell_f, cellf = a.cell_f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int dv = lane >> 2, du = 4 * (lane & 3);
+    const int dv = lane >> 2, du = FI_PX * (lane & 3);
     const int stx = (W + ST_W - 1) / ST_W;
     const bool pairs = (W & 1) == 0;
     unsigned int n_in = 0, n_oor = 0, n_ovf = 0, n_slow = 0;
@@ -465,15 +470,15 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         sx += FI_NT / 32;
         while (sx >= stx) { sx -= stx; ++sy; }
     };
-    auto load4 = [&](int sy, int sx, float (&z)[4], float (&c)[4]) {
+    auto load4 = [&](int sy, int sx, float (&z)[FI_PX], float (&c)[FI_PX]) {
         const int r = row_of(sy), u0 = sx * ST_W + du;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { z[k] = 0.f; c[k] = 0.f; }
+        for (int k = 0; k < FI_PX; ++k) { z[k] = 0.f; c[k] = 0.f; }
         if (r >= rows) return;
         const size_t off = (size_t)(v_band + r) * W + u0;
         if (pairs) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < FI_PX / 2; ++h)
                 if (u0 + 2 * h + 1 < W) {
                     const float2 z2 = __ldcs(reinterpret_cast<const float2*>(dbase + off + 2 * h));
                     const float2 c2 = __ldcs(reinterpret_cast<const float2*>(cbase + off + 2 * h));
@@ -482,7 +487,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                 }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < FI_PX; ++k)
                 if (u0 + k < W) { z[k] = __ldcs(dbase + off + k); c[k] = __ldcs(cbase + off + k); }
         }
     };
@@ -490,23 +495,23 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     int sy = 0, sx = warp;
     while (sx >= stx) { sx -= stx; ++sy; }
     int py = sy, px = sx;  // prefetch cursor
-    float nz[4], nc[4];
+    float nz[FI_PX], nc[FI_PX];
     if constexpr (!TMA) {
         if (py < n_sy) load4(py, px, nz, nc);
     }
     for (; sy < n_sy; advance(sy, sx)) {
         const int r = row_of(sy), u0 = sx * ST_W + du;
-        float zs[4], cs[4];
+        float zs[FI_PX], cs[FI_PX];
         if constexpr (TMA) {
             enter_strip(sy);
             const float* zr = ring + (size_t)((sy & 1) * 2) * ST_H * W + dv * W + u0;
             const float* cr = zr + ST_H * W;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) { zs[k] = 0.f; cs[k] = 0.f; }
+            for (int k = 0; k < FI_PX; ++k) { zs[k] = 0.f; cs[k] = 0.f; }
             if (r < rows) {
                 if (pairs) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
+                    for (int h = 0; h < FI_PX / 2; ++h)
                         if (u0 + 2 * h + 1 < W) {
                             const float2 z2 = *reinterpret_cast<const float2*>(zr + 2 * h);
                             const float2 c2 = *reinterpret_cast<const float2*>(cr + 2 * h);
@@ -515,13 +520,13 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
                         }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
+                    for (int k = 0; k < FI_PX; ++k)
                         if (u0 + k < W) { zs[k] = zr[k]; cs[k] = cr[k]; }
                 }
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
+            for (int k = 0; k < FI_PX; ++k) { zs[k] = nz[k]; cs[k] = nc[k]; }
             advance(py, px);
             if (py < n_sy) load4(py, px, nz, nc);
         }
@@ -529,12 +534,12 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
 
         // phase A: keys and contributions of the lane's 4 pixels, branch-free
         // except the (rare) exact float64 re-run near a voxel face
-        bool valid[4];
-        int cx[4], cy[4], cz[4];
-        float ox[4], oy[4], oz[4];
+        bool valid[FI_PX];
+        int cx[FI_PX], cy[FI_PX], cz[FI_PX];
+        float ox[FI_PX], oy[FI_PX], oz[FI_PX];
         unsigned slow = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             const float z = zs[k], c = cs[k];
             const float4 Au = sA[min(u0 + k, W - 1)];  // columns past W are zero-filled (invalid)
             const float dx = Au.x + Bv.x, dy = Au.y + Bv.y, dz = Au.z + Bv.z;
@@ -558,7 +563,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         }
         if (slow) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < FI_PX; ++k) {
                 if (!(slow & (1u << k))) continue;
                 long long cc[3];
                 exact_cells(a.slot_poses + 8 * slot, a.slot_globals + 8 * slot, ray_coef(u0 + k, a.cx, a.fx),
@@ -578,10 +583,10 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         // A miss (first touch of a block by this CTA, a block > 40 m from
         // the camera, or a cache collision) resolves through the global
         // table and refills the cache.
-        int got[4], local[4];
-        uint32_t tag[4], slot[4];
+        int got[FI_PX], local[FI_PX];
+        uint32_t tag[FI_PX], slot[FI_PX];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             local[k] = (cx[k] & 3) | ((cy[k] & 3) << 2) | ((cz[k] & 3) << 4);
             const unsigned rx = (unsigned)((cx[k] >> 2) - ob.x + 512), ry = (unsigned)((cy[k] >> 2) - ob.y + 512),
                            rz = (unsigned)((cz[k] >> 2) - ob.z + 512);
@@ -593,12 +598,12 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         // misses: lanes sharing a block elect one leader per pixel slot; the
         // leaders' first probes of the 4 slots are in flight together and
         // only a first-probe miss walks the probe chain / inserts
-        bool miss[4];
-        int leader[4];
-        unsigned long long bk[4];
+        bool miss[FI_PX];
+        int leader[FI_PX];
+        unsigned long long bk[FI_PX];
         unsigned lead = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             miss[k] = valid[k] && got[k] == -3;
             leader[k] = -1;
             bk[k] = pack_block(cx[k] >> 2, cy[k] >> 2, cz[k] >> 2);
@@ -609,16 +614,16 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             }
         }
         if (lead) {
-            unsigned long long ek[4];
-            int gk[4];
+            unsigned long long ek[FI_PX];
+            int gk[FI_PX];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < FI_PX; ++k) {
                 ek[k] = kEmpty;
                 gk[k] = -1;
                 if (lead & (1u << k)) load_entry(a.vb.table + table_slot(bk[k], a.vb.tmask), ek[k], gk[k]);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < FI_PX; ++k) {
                 if (!(lead & (1u << k))) continue;
                 if (ek[k] != bk[k] || gk[k] == -1) gk[k] = vb_find_or_insert(a.vb, bk[k]);
                 got[k] = gk[k];
@@ -630,7 +635,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             if (leader[k] >= 0) {
                 const int g = __shfl_sync(0xffffffffu, got[k], leader[k]);
                 if (miss[k]) got[k] = g;
@@ -640,15 +645,15 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
         // in the same voxel form a run whose sums ride along (FFMA with a
         // 0/1 continuation flag); only a run's last pixel issues the two
         // reductions (predicated, no branches).
-        uint32_t vid[4];
+        uint32_t vid[FI_PX];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             if (valid[k] && got[k] < 0) ++n_ovf;
             vid[k] = (valid[k] && got[k] >= 0) ? (((uint32_t)got[k] << 6) | (uint32_t)local[k]) : 0xFFFFFFFFu;
         }
         float rx = 0.f, ry = 0.f, rz = 0.f, rw = 0.f, rn = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FI_PX; ++k) {
             const float c = cs[k];
             const float cont = (k > 0 && vid[k] == vid[k - 1]) ? 1.f : 0.f;
             rx = fmaf(cont, rx, c * (ox[k] - (float)cx[k] * cellf));
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             rz = fmaf(cont, rz, c * (oz[k] - (float)cz[k] * cellf));
             rw = fmaf(cont, rw, c);
             rn = fmaf(cont, rn, 1.f);
-            bool last = vid[k] != 0xFFFFFFFFu && (k == 3 || vid[k + 1 < 4 ? k + 1 : 3] != vid[k]);
+            bool last = vid[k] != 0xFFFFFFFFu && (k == FI_PX - 1 || vid[k + 1 < FI_PX ? k + 1 : FI_PX - 1] != vid[k]);
             float sx = rx, sy = ry, sz = rz, sw = rw, sn = rn;
             if constexpr (FI_DEDUP) {
                 // Lanes of one reduction instruction that target the same
