@@ -66,3 +66,36 @@ def fuse_submaps(submaps, globals_, cell_size):
 
     x, conf = fused_cloud(submaps, globals_)
     return fuse_points(x, conf, cell_size)
+
+
+def fuse_submaps_streamed(submaps, globals_, cell_size, chunk=16):
+    """fuse_submaps in bounded memory (TEST ORACLE ONLY): rules (i)-(v)
+    applied to groups of ``chunk`` submaps, whose per-key partial sums
+    (Σconf·x, Σconf, count) are merged by key.  Keys, counts and
+    n_out_of_range are identical to fuse_submaps; the float64 sums differ
+    only by summation order (far below the 1e-4 parity tolerances)."""
+    from .ref_numpy import world_points
+
+    parts = []
+    n_oor = n_in = 0
+    for g0 in range(0, len(submaps), chunk):
+        xs, cs = [], []
+        for sm, (s, q, t) in zip(submaps[g0:g0 + chunk], globals_[g0:g0 + chunk]):
+            x, c = world_points(sm, s, q, t)
+            xs.append(x)
+            cs.append(c)
+        f = fuse_points(np.concatenate(xs), np.concatenate(cs), cell_size)
+        n_oor += f["n_out_of_range"]
+        n_in += f["n_in"]
+        parts.append((f["keys"], f["centroid"] * f["wsum"][:, None], f["wsum"], f["count"]))
+    if not parts:
+        return fuse_points(np.zeros((0, 3)), np.zeros(0), cell_size)
+    keys = np.concatenate([p[0] for p in parts])
+    order = np.argsort(keys, kind="stable")
+    keys_s = keys[order]
+    uniq, start = np.unique(keys_s, return_index=True)
+    sx = np.add.reduceat(np.concatenate([p[1] for p in parts])[order], start, axis=0)
+    wsum = np.add.reduceat(np.concatenate([p[2] for p in parts])[order], start)
+    count = np.add.reduceat(np.concatenate([p[3] for p in parts])[order], start)
+    return dict(keys=uniq.astype(np.int64), centroid=sx / wsum[:, None], wsum=wsum,
+                count=count.astype(np.int64), n_out_of_range=n_oor, n_in=n_in)

@@ -1,0 +1,131 @@
+"""Parity of the headline bench step itself: configs[3] (bench.py's default,
+1,500 keyframes / 300 submaps / 364 M points / 7,500 tracked frames per GPU)
+run through the exact bench.Step and checked against the CPU oracle:
+
+  * all 298 registration edges (mapping.py:162-188, registration.py:38-102):
+    status, pair count and keep count bit-exact, Sim(3) within 1e-5 relative;
+  * all 299 chained global poses (mapping.py:190-211) within 1e-5 relative;
+  * the full ~5.9 M-voxel map at 2 cm (mapping.py:56-57,332-338 + the declared
+    voxel rule, oracle/fuse.py, streamed in bounded host memory): keys and
+    counts bit-exact, centroids within 1e-4 m, wsum within 1e-4 relative;
+  * every 100th of the 7,500 tracked frames' matches (tracking.py:143-170)
+    bit-exact.
+
+tests/test_gpu_bench_parity.py holds the same checks on configs[1].
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fuse as ofuse
+from oracle import ref_numpy as ref
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+SIM3_RTOL = 1e-5
+ST = {0: ref.STATUS_OK, 1: ref.STATUS_SKIP, 2: ref.STATUS_TOO_FEW, 3: ref.STATUS_ALL_ZERO, 4: ref.STATUS_DEGENERATE,
+      5: ref.STATUS_DEGENERATE}
+
+
+@pytest.fixture(scope="module")
+def c3():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import bench
+
+    dm, sms, desc, halo = bench.build_workload(0, 1, bench.CONFIGS[3]["keyframes"], 1024, "cuda")
+    step = bench.Step(dm, sms, desc, halo=halo)
+    step.run()  # sizes the voxel map (outside the timed region in bench.py)
+    step.run()
+    out = tuple(x.cpu().numpy() for x in step.run())
+    mb = step.mb.cpu().numpy()
+    if step.n_dev is not None:
+        assert int(step.n_dev.item()) == int(out[0].shape[0])
+    reg = tuple(x.cpu().numpy() for x in step.plan.run(dm.pool))
+    torch.cuda.synchronize()
+    dense = []
+    for sm in sms:
+        sl = torch.as_tensor(np.asarray(sm.slots, np.int64), device="cuda")
+        p8 = dm.pool.poses[sl].cpu().numpy()
+        dense.append(dict(depth=dm.pool.depth[sl].cpu().numpy(), conf=dm.pool.conf[sl].cpu().numpy(),
+                          frame_ids=np.array(sm.keyframe_ids), pose_q=p8[:, 1:5], pose_t=p8[:, 5:],
+                          K=np.asarray(dm.pool.K4)))
+    index = {sm.id: i for i, sm in enumerate(sms)}
+    pairs = [(index[a.id], index[b.id]) for a, b in step.plan.pairs]
+    oracle_edges = [ref.registration_edge(dense[i], dense[j]) for i, j in pairs]
+    A, B, a_off, b_off, b_row = desc
+    sample = []
+    for f in range(0, len(a_off) - 1, 100):
+        M = int(b_off[f + 1] - b_off[f])
+        sample.append((f, A.view(torch.bfloat16)[a_off[f]:a_off[f + 1]].double().cpu().numpy(),
+                       B.view(torch.bfloat16)[b_row[f]:b_row[f] + M].double().cpu().numpy(),
+                       mb[a_off[f]:a_off[f + 1]]))
+    del step, desc, A, B, dm
+    torch.cuda.empty_cache()
+    return dict(n_sub=len(sms), pairs=pairs, out=out, reg=reg, dense=dense, oracle_edges=oracle_edges,
+                sample=sample)
+
+
+def _sim3_close(v, s, q, t):
+    assert abs(v[0] - s) <= SIM3_RTOL * abs(s), (v[0], s)
+    np.testing.assert_allclose(ref.canonical_quat(v[1:5]), ref.canonical_quat(q), atol=SIM3_RTOL)
+    np.testing.assert_allclose(v[5:], t, atol=SIM3_RTOL * max(1.0, float(np.abs(t).max())))
+
+
+def test_c3_registration_edges_vs_oracle(c3):
+    sim3, rms, count, npairs, status = c3["reg"][:5]
+    assert c3["n_sub"] >= 299 and len(c3["pairs"]) >= 298
+    for e, o in enumerate(c3["oracle_edges"]):
+        assert ST[int(status[e])] == o["status"], (e, int(status[e]), o["status"])
+        assert int(npairs[e]) == o["n_pairs"], e
+        if int(status[e]) == 0:
+            assert int(count[e]) == o["count"], e
+            _sim3_close(sim3[e], o["s"], o["q"], o["t"])
+            assert abs(rms[e] - o["rms"]) <= 1e-5 * max(o["rms"], 1e-9)
+
+
+def test_c3_chained_poses_vs_oracle(c3):
+    """The oracle's edges chained on the host (left fold, strongest partner
+    = max count, first on ties) against the device chain."""
+    sub_g, sub_st = c3["reg"][5], c3["reg"][6]
+    best = {}
+    for (j, p), o in zip(c3["pairs"], c3["oracle_edges"]):
+        if o["status"] == ref.STATUS_OK and (j not in best or o["count"] > best[j][0]):
+            best[j] = (o["count"], p, (o["s"], o["q"], o["t"]))
+    glob = {0: (1.0, np.array([1.0, 0, 0, 0]), np.zeros(3))}
+    for j in range(1, c3["n_sub"]):
+        _, p, tr = best[j]
+        glob[j] = ref.sim3_compose(glob[p], tr)
+    assert (sub_st == 0).all()
+    for j in range(c3["n_sub"]):
+        s, q, t = glob[j]
+        _sim3_close(sub_g[j], s, q, t)
+
+
+def test_c3_fused_map_vs_oracle(c3):
+    """The full configs[3] map fused by the (streamed) oracle from the same
+    decoded planes under the device's chained poses."""
+    keys, cen, wsum, cnt = c3["out"]
+    sub_g = c3["reg"][5]
+    globs = [(float(v[0]), v[1:5], v[5:]) for v in sub_g]
+    o = ofuse.fuse_submaps_streamed(c3["dense"], globs, 0.02)
+    assert len(o["keys"]) > 5_000_000 and o["n_in"] > 300_000_000
+    np.testing.assert_array_equal(keys, o["keys"])
+    np.testing.assert_array_equal(cnt, o["count"])
+    assert np.max(np.abs(cen - o["centroid"])) < 1e-4
+    np.testing.assert_allclose(wsum, o["wsum"], rtol=1e-4)
+
+
+def test_c3_tracking_matches_sample_vs_oracle(c3):
+    assert len(c3["sample"]) >= 75
+    for f, fa, fb, seg in c3["sample"]:
+        exp = ref.match_descriptors_vec(fa, fb, 0.8)
+        ia = np.flatnonzero(seg >= 0)
+        np.testing.assert_array_equal(np.stack([ia, seg[ia]], axis=1), exp, err_msg=f"frame {f}")

@@ -89,6 +89,22 @@ def test_fused_cloud_bit_exact_and_keys(golden):
     assert np.all(f["centroid"] >= lo - 1e-9) and np.all(f["centroid"] <= lo + 0.02 + 1e-9)
 
 
+def test_streamed_fusion_equals_fuse_submaps(golden):
+    """fuse_submaps_streamed (the bounded-memory oracle the configs[3] GPU
+    parity test uses) against fuse_submaps on the golden submaps, one submap
+    per chunk so every shared voxel goes through the partial merge."""
+    g = golden("mapping")
+    sms, globs = mapping_submaps(g)
+    for cell in (0.02, 0.05):
+        a = ofuse.fuse_submaps(sms, globs, cell)
+        b = ofuse.fuse_submaps_streamed(sms, globs, cell, chunk=1)
+        np.testing.assert_array_equal(a["keys"], b["keys"])
+        np.testing.assert_array_equal(a["count"], b["count"])
+        assert a["n_in"] == b["n_in"] and a["n_out_of_range"] == b["n_out_of_range"]
+        np.testing.assert_allclose(b["centroid"], a["centroid"], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(b["wsum"], a["wsum"], rtol=1e-12)
+
+
 def test_match_cases(golden):
     g = golden("match")
     for i in range(int(g["n_cases"])):
