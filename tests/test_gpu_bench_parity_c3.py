@@ -1,14 +1,17 @@
 """Parity of the headline bench step itself: configs[3] (bench.py's default,
-1,500 keyframes / 300 submaps / 364 M points / 7,500 tracked frames per GPU)
-run through the exact bench.Step and checked against the CPU oracle:
+1,500 keyframes / 300 submaps / 364 M points / 7,500 tracked frames per GPU),
+and the configs[4] per-GPU shard (500 keyframes, ~50 % invalid pixels), run
+through the exact bench.Step and checked against the CPU oracle:
 
-  * all 298 registration edges (mapping.py:162-188, registration.py:38-102):
-    status, pair count and keep count bit-exact, Sim(3) within 1e-5 relative;
-  * all 299 chained global poses (mapping.py:190-211) within 1e-5 relative;
-  * the full ~5.9 M-voxel map at 2 cm (mapping.py:56-57,332-338 + the declared
+  * every registration edge, 298 on configs[3] (mapping.py:162-188,
+    registration.py:38-102): status, pair count and keep count bit-exact,
+    Sim(3) within 1e-5 relative;
+  * every chained global pose, 299 on configs[3] (mapping.py:190-211), within
+    1e-5 relative;
+  * the full fused map at 2 cm (~5.9 M voxels on configs[3]) (mapping.py:56-57,332-338 + the declared
     voxel rule, oracle/fuse.py, streamed in bounded host memory): keys and
     counts bit-exact, centroids within 1e-4 m, wsum within 1e-4 relative;
-  * every 100th of the 7,500 tracked frames' matches (tracking.py:143-170)
+  * every 100th tracked frame's matches (tracking.py:143-170)
     bit-exact.
 
 tests/test_gpu_bench_parity.py holds the same checks on configs[1].
@@ -34,13 +37,14 @@ ST = {0: ref.STATUS_OK, 1: ref.STATUS_SKIP, 2: ref.STATUS_TOO_FEW, 3: ref.STATUS
       5: ref.STATUS_DEGENERATE}
 
 
-@pytest.fixture(scope="module")
-def c3():
+@pytest.fixture(scope="module", params=[3, 4], ids=["configs3", "configs4"])
+def c3(request):
     if not torch.cuda.is_available():
         pytest.skip("needs CUDA")
     import bench
 
-    dm, sms, desc, halo = bench.build_workload(0, 1, bench.CONFIGS[3]["keyframes"], 1024, "cuda")
+    pc = bench.CONFIGS[request.param]
+    dm, sms, desc, halo = bench.build_workload(0, 1, pc["keyframes"], 1024, "cuda", invalid=pc["invalid"])
     step = bench.Step(dm, sms, desc, halo=halo)
     step.run()  # sizes the voxel map (outside the timed region in bench.py)
     step.run()
@@ -69,8 +73,8 @@ def c3():
                        mb[a_off[f]:a_off[f + 1]]))
     del step, desc, A, B, dm
     torch.cuda.empty_cache()
-    return dict(n_sub=len(sms), pairs=pairs, out=out, reg=reg, dense=dense, oracle_edges=oracle_edges,
-                sample=sample)
+    return dict(config=request.param, n_sub=len(sms), pairs=pairs, out=out, reg=reg, dense=dense,
+                oracle_edges=oracle_edges, sample=sample)
 
 
 def _sim3_close(v, s, q, t):
@@ -81,7 +85,7 @@ def _sim3_close(v, s, q, t):
 
 def test_c3_registration_edges_vs_oracle(c3):
     sim3, rms, count, npairs, status = c3["reg"][:5]
-    assert c3["n_sub"] >= 299 and len(c3["pairs"]) >= 298
+    assert c3["n_sub"] >= (299 if c3["config"] == 3 else 99) and len(c3["pairs"]) >= c3["n_sub"] - 1
     for e, o in enumerate(c3["oracle_edges"]):
         assert ST[int(status[e])] == o["status"], (e, int(status[e]), o["status"])
         assert int(npairs[e]) == o["n_pairs"], e
@@ -116,7 +120,11 @@ def test_c3_fused_map_vs_oracle(c3):
     sub_g = c3["reg"][5]
     globs = [(float(v[0]), v[1:5], v[5:]) for v in sub_g]
     o = ofuse.fuse_submaps_streamed(c3["dense"], globs, 0.02)
-    assert len(o["keys"]) > 5_000_000 and o["n_in"] > 300_000_000
+    if c3["config"] == 3:
+        assert len(o["keys"]) > 5_000_000 and o["n_in"] > 300_000_000
+    else:  # half the pixels invalid (depth 0 / conf 0)
+        px = sum(d["depth"].size for d in c3["dense"])
+        assert 0.45 < o["n_in"] / px < 0.55
     np.testing.assert_array_equal(keys, o["keys"])
     np.testing.assert_array_equal(cnt, o["count"])
     assert np.max(np.abs(cen - o["centroid"])) < 1e-4
@@ -124,7 +132,7 @@ def test_c3_fused_map_vs_oracle(c3):
 
 
 def test_c3_tracking_matches_sample_vs_oracle(c3):
-    assert len(c3["sample"]) >= 75
+    assert len(c3["sample"]) >= (75 if c3["config"] == 3 else 25)
     for f, fa, fb, seg in c3["sample"]:
         exp = ref.match_descriptors_vec(fa, fb, 0.8)
         ia = np.flatnonzero(seg >= 0)
