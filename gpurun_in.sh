@@ -1,5 +1,9 @@
-T=r02bm; O=gpurun_out/$T; mkdir -p $O
-for g in 148 144 140 136 128; do for c in 1 3; do
-EC3R_MT_GRID=$g timeout 600 python bench.py --config $c --steps 40 --warmup 5 --no-cpu-baseline --no-e2e --no-extras --no-floor > $O/b_${g}_$c.json 2>/dev/null; python -c "
-import json;d=json.loads(open('$O/b_${g}_$c.json').read().strip().splitlines()[-1]);print('grid $g c$c', round(d['ms_per_step'],4), {k:round(v,3) for k,v in d['stages_ms'].items()})"
-done; done
+#!/usr/bin/env bash
+# r02g12: final validation at HEAD: full GPU suite, smoke, driver-style bench (N=1), reference arm,
+# N=2 over NCCL on the shared GPU (validation only), ncu launch list
+O=gpurun_out/r02g12; mkdir -p $O
+BENCH_ARGS="--steps 20 --warmup 5" bash tools/gpu_check.sh r02g12
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.log 2>&1; echo ref_rc=$?
+timeout 600 python bench.py --config 1 --steps 20 --warmup 5 --no-extras > $O/bench_c1.log 2>&1; echo c1_rc=$?
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --config 1 --steps 5 --warmup 3 --no-extras --no-e2e --no-cpu-baseline > $O/bench_n2.log 2>&1; echo n2_rc=$?

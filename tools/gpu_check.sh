@@ -10,7 +10,7 @@ MODE=${2:-}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > "$OUT/smi.txt" 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > "$OUT/gpu_tests.log" 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q --timeout 600 > "$OUT/gpu_tests.log" 2>&1
 echo "tests_rc=$?"
 timeout 600 python bench.py ${BENCH_ARGS:-} > "$OUT/bench.log" 2>&1
 echo "bench_rc=$?"
