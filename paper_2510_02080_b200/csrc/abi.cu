@@ -49,10 +49,9 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
                  const int64_t* b_row_d, int64_t n_b_rows,
                  const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
                  double norm_bound, double ratio, MatchRowState* rs, int32_t* flag_rows, int32_t* flag_cols,
-                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, double* eps_out,
-                 cudaStream_t st);
+                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, cudaStream_t st);
 int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
-                       const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
+                       const int64_t* b_off_h, int n_pairs, double ratio, MatchRowState* rs,
                        const MatchRowD* rsd, int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws,
                        cudaStream_t st);
 size_t match_tc_workspace(const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs);
@@ -156,16 +155,14 @@ extern "C" int ec3r_match_batched_rows(const uint16_t* A, const uint16_t* B, con
         // tensor-core pass: certifies most rows and lists the rest; the
         // passing rows' mutual checks then list the columns they need
         int tc_used = 0;
-        double eps_tc = 0.0;
         rc = match_tc_run(A, B, a_off, b_off, b_row, n_b_rows, a_off_h, b_off_h, n_pairs, D, exact_dtype, norm_bound,
-                          ratio, rs,
-                          flag_rows, flag_cols, counters, tc_ws, tc_bytes, &tc_used, &eps_tc, st);
+                          ratio, rs, flag_rows, flag_cols, counters, tc_ws, tc_bytes, &tc_used, st);
         if (rc) return rc;
         if (tc_used) {
             rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, flag_rows, counters + 0, 0,
                                       nullptr, nullptr, 0, rs, rsd, col_best, st);
             if (rc) return rc;
-            rc = match_tc_need_cols(a_off, b_off, a_off_h, b_off_h, n_pairs, ratio, eps_tc, rs, rsd, col_best,
+            rc = match_tc_need_cols(a_off, b_off, a_off_h, b_off_h, n_pairs, ratio, rs, rsd, col_best,
                                     flag_cols, counters, tc_ws, st);
             if (rc) return rc;
             rc = match_exact_dispatch(A_x, B_x, exact_dtype, D, a_off, b_off, b_row, n_pairs, nullptr, nullptr, 0,

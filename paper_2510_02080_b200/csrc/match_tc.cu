@@ -30,6 +30,7 @@
 // argmax; a column only when a passing row needs its argmax and the keys do
 // not settle it.
 
+#include <atomic>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -103,7 +104,8 @@ struct TcParams {
     MatchRowState* rs;
     int32_t* pending;
     int64_t* counters;
-    double eps_tc, ratio2;
+    const double* eps_d;  // tensor-core error bound eps_tc (device: no host round trip for the norm bound)
+    double ratio2;
 };
 
 // ---------------------------------------------------------------------------
@@ -671,7 +673,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     p.cand[row0 * p.n_split + un.split] = rc;
                     if (p.n_split == 1) {
                         MatchRowState st;
-                        if (row_decision(rc, M, p.eps_tc, p.ratio2, st)) p.rs[row0] = st;
+                        if (row_decision(rc, M, __ldg(p.eps_d), p.ratio2, st)) p.rs[row0] = st;
                         else p.pending[atomicAdd((unsigned long long*)&p.counters[0], 1ull)] = (int32_t)row0;
                     }
                 }
@@ -684,7 +686,7 @@ mt_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CU
                     p.cand[row1 * p.n_split + un.split] = rc;
                     if (p.n_split == 1) {
                         MatchRowState st;
-                        if (row_decision(rc, M, p.eps_tc, p.ratio2, st)) p.rs[row1] = st;
+                        if (row_decision(rc, M, __ldg(p.eps_d), p.ratio2, st)) p.rs[row1] = st;
                         else p.pending[atomicAdd((unsigned long long*)&p.counters[0], 1ull)] = (int32_t)row1;
                     }
                 }
@@ -750,12 +752,14 @@ __device__ __forceinline__ int pair_of_cta(const int64_t* __restrict__ off, int 
 //     the runner-up cannot clamp to d2 = 0) and the bounds pass;
 // everything else is listed for the float64 row re-scan.
 __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
-                               int64_t total_a, RowCand* __restrict__ cand, int n_split, double eps_tc, double ratio2,
+                               int64_t total_a, RowCand* __restrict__ cand, int n_split,
+                               const double* __restrict__ eps_d, double ratio2,
                                MatchRowState* __restrict__ rs, int32_t* __restrict__ pending,
                                int64_t* __restrict__ counters, int only_empty) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int p = pair_of_cta(a_off, n_pairs, r, total_a);
     if (r >= total_a) return;
+    const double eps_tc = *eps_d;
     const int64_t M = b_off[p + 1] - b_off[p];
     if (only_empty && M != 0) return;  // decided in the tensor-core epilogue
     MatchRowState s;
@@ -789,13 +793,14 @@ __global__ void mt_decide_rows(const int64_t* __restrict__ a_off, const int64_t*
 __global__ void mt_need_cols(const int64_t* __restrict__ a_off, const int64_t* __restrict__ b_off, int n_pairs,
                              int64_t total_a, const RowCand* __restrict__ cand, int n_split,
                              const unsigned long long* __restrict__ col_slots,
-                             const long long* __restrict__ pair_slot, double eps_tc, double ratio2,
+                             const long long* __restrict__ pair_slot, const double* __restrict__ eps_d, double ratio2,
                              MatchRowState* __restrict__ rs, const MatchRowD* __restrict__ rsd,
                              int32_t* __restrict__ col_best,
                              int32_t* __restrict__ pending, int64_t* __restrict__ counters) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int p = pair_of_cta(a_off, n_pairs, r, total_a);
     if (r >= total_a) return;
+    const double eps_tc = *eps_d;
     const int64_t a0 = a_off[p], N = a_off[p + 1] - a0;
     const int64_t b0 = b_off[p], M = b_off[p + 1] - b0;
     const MatchRowState s = rs[r];
@@ -1082,6 +1087,24 @@ static TcWs carve_tc(void* tc_ws, const int64_t* a_off_h, const int64_t* b_off_h
     return w;
 }
 
+// eps_tc, the tensor-core error bound (K5): fp32 accumulation of
+// exact bf16 products, + bf16 rounding of the inputs when the exact rows are
+// wider; the key quantisation is added per value (key_eps).  The norm bound
+// is the caller's, or the device max row norms (mt_norm_kernel) rounded up.
+__global__ void mt_eps_kernel(const unsigned int* __restrict__ nb, double norm_bound, int exact_dtype,
+                              double* __restrict__ eps) {
+    if (threadIdx.x != 0) return;
+    if (!(norm_bound > 0)) {
+        const float fa = __uint_as_float(nb[0]), fb = __uint_as_float(nb[1]);
+        norm_bound = sqrt((double)fa * (1.0 + 1e-5)) * sqrt((double)fb * (1.0 + 1e-5)) + 1e-30;
+    }
+    double e = ldexp(norm_bound, -14);
+    if (exact_dtype != 0) e += ldexp(norm_bound, -7);
+    *eps = e;
+}
+// the device eps_tc lives in the workspace's norm words (nb[4..5])
+static double* tc_eps(const TcWs& w) { return reinterpret_cast<double*>(w.nb + 4); }
+
 // Tensor-core pass + stage-1 row decisions.  *tc_used = 0 when the shape or
 // alignment rules out the tensor cores: every row and column is then listed
 // for the float64 re-scan (counters[0] = rows, counters[1] = cols).
@@ -1089,8 +1112,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
                  const int64_t* b_row_d, int64_t n_b_rows,
                  const int64_t* a_off_h, const int64_t* b_off_h, int n_pairs, int D, int exact_dtype,
                  double norm_bound, double ratio, MatchRowState* rs, int32_t* flag_rows, int32_t* flag_cols,
-                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, double* eps_out,
-                 cudaStream_t st) {
+                 int64_t* counters, void* tc_ws, size_t tc_ws_bytes, int* tc_used, cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
     *tc_used = 0;
     const bool tc_ok = (D % TC_BK == 0) && D <= 256 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0 && ta > 0 &&
@@ -1126,7 +1148,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         EC3R_CHECK_LAUNCH("mt_units_kernel");
     }
     if (!(norm_bound > 0)) {
-        // max squared row norms of A and B (float32, rounded up below)
+        // max squared row norms of A and B (float32, rounded up in mt_eps_kernel)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.nb, 0, 8, st));
         const auto norm_grid = [](int64_t rows) {
             return (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows * 32 + 255) / 256, (int64_t)kNumSMs * 8));
@@ -1135,20 +1157,10 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
         mt_norm_kernel<<<norm_grid(n_b_rows), 256, 0, st>>>(B, n_b_rows, D, w.nb + 1);
         EC3R_CHECK_LAUNCH("mt_norm_kernel");
-        unsigned int h[2];
-        EC3R_CUDA_TRY(cudaMemcpyAsync(h, w.nb, 8, cudaMemcpyDeviceToHost, st));
-        EC3R_CUDA_TRY(cudaStreamSynchronize(st));
-        float fa, fb;
-        memcpy(&fa, &h[0], 4);
-        memcpy(&fb, &h[1], 4);
-        norm_bound = sqrt((double)fa * (1.0 + 1e-5)) * sqrt((double)fb * (1.0 + 1e-5)) + 1e-30;
     }
-    // tensor-core error bound (K5): fp32 accumulation of exact
-    // bf16 products, + bf16 rounding of the inputs when the exact rows are
-    // wider.  The key quantisation is added per value (key_eps).
-    double eps_tc = ldexp(norm_bound, -14);
-    if (exact_dtype != 0) eps_tc += ldexp(norm_bound, -7);
-    *eps_out = eps_tc;
+    // eps_tc on the device (no host round trip: back-to-back calls queue)
+    mt_eps_kernel<<<1, 32, 0, st>>>(w.nb, norm_bound, exact_dtype, tc_eps(w));
+    EC3R_CHECK_LAUNCH("mt_eps_kernel");
     CUtensorMap tmA, tmB;
     if (!make_map(&tmA, A, ta, D) || !make_map(&tmB, B, n_b_rows, D)) {
         set_last_error_msg("cuTensorMapEncodeTiled failed");
@@ -1158,12 +1170,16 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
     prm.a_off = a_off_d; prm.b_off = b_off_d; prm.b_row = b_row_d;
     prm.units = w.units; prm.n_units = (int)n_units; prm.kblocks = D / TC_BK;
     prm.cand = w.cand; prm.n_split = w.n_split; prm.col_slots = w.slots;
-    prm.rs = rs; prm.pending = flag_rows; prm.counters = counters; prm.eps_tc = eps_tc; prm.ratio2 = ratio * ratio;
+    prm.rs = rs; prm.pending = flag_rows; prm.counters = counters; prm.eps_d = tc_eps(w); prm.ratio2 = ratio * ratio;
     if (w.n_split > 1)  // ranges past a short pair's columns stay invalid (c1 = -1)
         EC3R_CUDA_TRY(cudaMemsetAsync(w.cand, 0xFF, sizeof(RowCand) * (size_t)ta * w.n_split, st));
     if (prm.n_units > 0) {
         const size_t smem = tc_smem_bytes(prm.kblocks);
-        EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        static std::atomic<size_t> smem_set{0};  // raise the opt-in limit once per size (benign duplicate sets)
+        if (smem > smem_set.load()) {
+            EC3R_CUDA_TRY(cudaFuncSetAttribute(mt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set.store(smem);
+        }
         int grid = prm.n_units < kNumSMs ? prm.n_units : kNumSMs;
         // EC3R_MT_GRID caps the persistent grid (SMs left free for concurrent
         // mapping kernels on another stream)
@@ -1180,7 +1196,7 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
         any_empty = b_off_h[pi + 1] == b_off_h[pi] && a_off_h[pi + 1] > a_off_h[pi];
     if (w.n_split > 1 || any_empty) {
         mt_decide_rows<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand,
-                                                                     w.n_split, eps_tc, ratio * ratio, rs, flag_rows,
+                                                                     w.n_split, tc_eps(w), ratio * ratio, rs, flag_rows,
                                                                      counters, w.n_split == 1 ? 1 : 0);
         EC3R_CHECK_LAUNCH("mt_decide_rows");
     }
@@ -1191,15 +1207,15 @@ int match_tc_run(const uint16_t* A, const uint16_t* B, const int64_t* a_off_d, c
 // Mutual checks of the passing rows (after the row re-scan); lists the
 // columns that need the float64 column re-scan.  col_best is reset to -1.
 int match_tc_need_cols(const int64_t* a_off_d, const int64_t* b_off_d, const int64_t* a_off_h,
-                       const int64_t* b_off_h, int n_pairs, double ratio, double eps_tc, MatchRowState* rs,
+                       const int64_t* b_off_h, int n_pairs, double ratio, MatchRowState* rs,
                        const MatchRowD* rsd, int32_t* col_best, int32_t* flag_cols, int64_t* counters, void* tc_ws,
                        cudaStream_t st) {
     const int64_t ta = a_off_h[n_pairs], tb = b_off_h[n_pairs];
     const TcWs w = carve_tc(tc_ws, a_off_h, b_off_h, n_pairs);
     EC3R_CUDA_TRY(cudaMemsetAsync(col_best, 0xFF, sizeof(int32_t) * (size_t)tb, st));
-    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split, w.slots, w.pair_slot,
-                                                               eps_tc, ratio * ratio, rs, rsd, col_best, flag_cols,
-                                                               counters);
+    mt_need_cols<<<(unsigned)((ta + 255) / 256), 256, 0, st>>>(a_off_d, b_off_d, n_pairs, ta, w.cand, w.n_split,
+                                                               w.slots, w.pair_slot, tc_eps(w), ratio * ratio, rs,
+                                                               rsd, col_best, flag_cols, counters);
     EC3R_CHECK_LAUNCH("mt_need_cols");
     return EC3R_OK;
 }
