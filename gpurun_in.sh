@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
-# r02g16: matcher without the per-call host sync: latency anatomy, matcher tests, bench
-O=gpurun_out/r02g16; mkdir -p $O
-timeout 600 python tools/match_latency.py > $O/lat.jsonl 2> $O/lat.err
-timeout 1500 python -m pytest tests -m gpu -x -q --timeout 900 -k "match or track or loop or verify or dropin or smoke" > $O/tests.log 2>&1; echo tests_rc=$?
-timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench.log 2>&1; echo bench_rc=$?
+# r02g17: final validation at HEAD: full GPU suite, smoke, driver-style bench (N=1), reference arm, ncu launch list
+O=gpurun_out/r02g17; mkdir -p $O
+BENCH_ARGS="--steps 20 --warmup 5" bash tools/gpu_check.sh r02g17
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.log 2>&1; echo ref_rc=$?
+timeout 600 python bench.py --config 1 --steps 20 --warmup 5 --no-extras > $O/bench_c1.log 2>&1; echo c1_rc=$?
