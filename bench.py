@@ -844,7 +844,7 @@ def run_extras(peaks):
     from paper_2510_02080_b200 import _lib, kernels, synth, tracking
 
     out = {"matcher_sweep": [], "nn_query": [], "raycast": None}
-    for n in (2048, 8192, 32768):
+    for n in (2048, 4096, 8192, 16384, 32768):  # SURVEY §8(d) cfg 3 sweep
         A, B, ao, bo = synth.make_descriptor_pairs(1, n, n, 256, 0.05, seed=n, device="cuda")
         run = lambda: tracking.match_batched_device(A, B, None, None, 0, ao, bo, 0.8)  # noqa: E731
         run()
