@@ -280,6 +280,11 @@ class VoxelMap:
             if not sync:
                 raise ValueError("extract(sync=False) needs preallocated out buffers")
             cap = self.count(stream)
+            if cap == 0:  # an empty map (nothing valid was inserted): empty outputs, no emit
+                return (torch.empty(0, dtype=torch.int64, device="cuda"),
+                        torch.empty((0, 3), dtype=torch.float32, device="cuda"),
+                        torch.empty(0, dtype=torch.float32, device="cuda"),
+                        torch.empty(0, dtype=torch.int32, device="cuda"))
             out = (torch.empty(cap, dtype=torch.int64, device="cuda"),
                    torch.empty((cap, 3), dtype=torch.float32, device="cuda"),
                    torch.empty(cap, dtype=torch.float32, device="cuda"),
