@@ -44,15 +44,28 @@ def _build(ids_sel=None, id0=None):
     return dm, sms, len(sb.frame_ids)
 
 
+def _init(rank, world, port, backend):
+    """gloo (CUDA payloads staged through the host) or NCCL itself: two NCCL
+    ranks on one GPU take distinct NCCL_HOSTIDs (NCCL then treats them as
+    separate hosts and uses its socket transport on loopback; validation of
+    the NCCL forms, not a measurement)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if backend == "nccl":
+        os.environ.update(NCCL_HOSTID=f"ec3r-test-rank{rank}", NCCL_SOCKET_IFNAME="lo", NCCL_IB_DISABLE="1")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
 def _poses(sms):
     from paper_2510_02080_b200.types import sim3_to_vec
     return np.stack([sim3_to_vec(sm.global_pose) for sm in sms])
 
 
-def _worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _worker(rank, world, port, q, backend="gloo"):
+    _init(rank, world, port, backend)
     try:
         from paper_2510_02080_b200 import dist as D
         torch.cuda.set_device(0)
@@ -69,14 +82,15 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_register_window_two_ranks_equals_single_process():
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_register_window_two_ranks_equals_single_process(backend):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -111,10 +125,8 @@ def test_register_window_two_ranks_equals_single_process():
     assert sum(cnt.values()) == int(ref_map["count"].sum())
 
 
-def _chain_worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _chain_worker(rank, world, port, q, backend="gloo"):
+    _init(rank, world, port, backend)
     try:
         from paper_2510_02080_b200 import dist as D
         from paper_2510_02080_b200 import mapping, synth
@@ -147,7 +159,8 @@ def _chain_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_window_chain_device_two_ranks_equals_single_chain():
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_window_chain_device_two_ranks_equals_single_chain(backend):
     """The bench's N > 1 registration step (dist.WindowChain: halo P2P,
     ChainPlan, all-gather of window poses, ec3r_apply_window_offset) on two
     ranks equals the single-process device chain over the whole sequence."""
@@ -157,7 +170,7 @@ def test_window_chain_device_two_ranks_equals_single_chain():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -187,10 +200,8 @@ def test_window_chain_device_two_ranks_equals_single_chain():
 K_RET = 1200
 
 
-def _ret_worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _ret_worker(rank, world, port, q, backend="gloo"):
+    _init(rank, world, port, backend)
     try:
         from paper_2510_02080_b200 import dist as D
         from paper_2510_02080_b200 import loops, synth
@@ -205,7 +216,8 @@ def _ret_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_retrieval_sharded_two_ranks_equals_single_and_oracle():
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_retrieval_sharded_two_ranks_equals_single_and_oracle(backend):
     """dist.retrieval_sharded with two ranks (gloo, one GPU): each rank scores
     its coarse rows on the device; the gathered lists equal the single-GPU
     lists, and the admitted pairs equal the oracle's update_similarity."""
@@ -214,7 +226,7 @@ def test_retrieval_sharded_two_ranks_equals_single_and_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ret_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ret_worker, args=(r, 2, port, q, backend)) for r in range(2)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=600) for _ in range(2))
@@ -257,10 +269,8 @@ def _loop_frames(sb, kf_a, kf_b):
     return out
 
 
-def _loop_worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _loop_worker(rank, world, port, q, backend="gloo"):
+    _init(rank, world, port, backend)
     try:
         from paper_2510_02080_b200 import dist as D
         from paper_2510_02080_b200 import mapping, synth
@@ -315,7 +325,8 @@ def _loop_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_loop_edges_across_shards_pgo_and_map_exchange():
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_loop_edges_across_shards_pgo_and_map_exchange(backend):
     """Two ranks (gloo, one GPU): a loop submap on rank 1 sharing keyframes
     with a submap of each rank is registered through dist.fetch_frames +
     one batched launch; its edges and pose equal single-process registration
@@ -329,7 +340,7 @@ def test_loop_edges_across_shards_pgo_and_map_exchange():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_loop_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_loop_worker, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=600) for _ in range(world))
