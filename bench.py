@@ -69,18 +69,27 @@ class ClockSampler:
         self._proc = None
 
     def start(self):
+        """Starts nvidia-smi and waits (<= 5 s) for its first row, so the
+        sampler is live when the timed region begins (mark() opens it)."""
         try:
             self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                           stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 5.0 and self._proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self._proc = None
+        self.t_mark = time.perf_counter()
+
+    def mark(self):
+        self.t_mark = time.perf_counter()
 
     def _read(self):
         for line in self._proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def stop(self):
         if self._proc is not None:
@@ -89,7 +98,13 @@ class ClockSampler:
                 self._proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self._proc.kill()
-        rows = [r for r in self.rows if len(r) >= 9]
+        valid = [(t, r) for t, r in self.rows if len(r) >= 9]
+        rows = [r for t, r in valid if t >= self.t_mark]
+        extra = {}
+        if not rows and valid:  # region shorter than the sampling interval: the sample just before it
+            t, r = max((x for x in valid if x[0] < self.t_mark), default=valid[0], key=lambda x: x[0])
+            rows = [r]
+            extra = {"samples_in_region": 0, "nearest_before_ms": (self.t_mark - t) * 1e3}
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -97,7 +112,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows) if not extra else 0, **extra}
 
 
 # ---------------------------------------------------------------------------
@@ -549,6 +564,7 @@ def main():
     _lib.timing_enable(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark()
     e0.record()
     for _ in range(args.steps):
         step.run(records)
