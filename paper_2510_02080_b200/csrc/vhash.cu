@@ -227,7 +227,11 @@ __global__ void vb_clear_used_kernel(BlockEntry* __restrict__ table, int64_t tca
 // ---------------------------------------------------------------------------
 // frame insertion
 
-constexpr int FI_NT = 256;
+#ifndef EC3R_FI_NT
+#define EC3R_FI_NT 256  // threads per insert CTA
+#endif
+constexpr int FI_NT = EC3R_FI_NT;
+constexpr int kSmallCtaWaves = 8;  // 128-thread insert CTAs from this many waves of them (see the launch)
 #ifndef EC3R_FI_ROWS
 #define EC3R_FI_ROWS 64  // image rows per CTA
 #endif
@@ -361,21 +365,21 @@ static bool tma_requested() {
 // the strip two ahead.  Requires H W % 4 == 0 and 16-byte aligned planes.
 __device__ __forceinline__ uint32_t vh_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <bool LOG, bool TMA>
-__global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(FuseArgs a) {
+template <bool LOG, bool TMA, int NT = FI_NT>
+__global__ void __launch_bounds__(NT, EC3R_FI_MINB * FI_NT / NT) vh_insert_frames_kernel(FuseArgs a) {
     extern __shared__ float4 sA[];  // A[W], then (TMA) the strip ring [2 stages][2 planes][8 W]
     __shared__ float4 sB[FI_ROWS];
     __shared__ __align__(8) uint64_t strip_full[2];
     __shared__ unsigned long long cta_cnt[4];
     __shared__ unsigned long long bcache[1 << BC_BITS];  // (tag << 32) | pool block, tag 0 = empty
-    __shared__ float4 dd_sum[FI_DEDUP ? FI_NT : 1];      // per-slot run hand-off to the group's lowest lane
-    __shared__ float dd_n[FI_DEDUP ? FI_NT : 1];
+    __shared__ float4 dd_sum[FI_DEDUP ? NT : 1];      // per-slot run hand-off to the group's lowest lane
+    __shared__ float dd_n[FI_DEDUP ? NT : 1];
     const int W = a.W, H = a.H;
     const int HW = H * W;
     const int v_band = blockIdx.x * FI_ROWS;
     const int rows = min(FI_ROWS, H - v_band);
     if (threadIdx.x < 4) cta_cnt[threadIdx.x] = 0;
-    for (int i = threadIdx.x; i < (1 << BC_BITS); i += FI_NT) bcache[i] = 0ull;
+    for (int i = threadIdx.x; i < (1 << BC_BITS); i += NT) bcache[i] = 0ull;
     // cache keys are block coordinates relative to the first frame's camera block
     int3 ob;
     {
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     const int slot = a.slots[j];
     const float4* tab = a.ftab + (size_t)j * (W + H + 1);
     __syncthreads();  // the previous frame's tables are no longer read
-    for (int u = threadIdx.x; u < W; u += FI_NT) sA[u] = __ldg(tab + u);
+    for (int u = threadIdx.x; u < W; u += NT) sA[u] = __ldg(tab + u);
     if (threadIdx.x < rows) sB[threadIdx.x] = __ldg(tab + W + v_band + threadIdx.x);
     const float4 Tm = __ldg(tab + W + H);
     __syncthreads();
@@ -448,9 +452,9 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
             if (cur_strip >= 0) {
                 const int id = 1 + (cur_strip & 1);
                 if (warp != 0) {
-                    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(FI_NT) : "memory");
+                    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(NT) : "memory");
                 } else {
-                    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(FI_NT) : "memory");
+                    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory");
                     if (lane == 0 && cur_strip + 2 < n_strips) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         issue_strip(cur_strip + 2);
@@ -467,7 +471,7 @@ __global__ void __launch_bounds__(FI_NT, EC3R_FI_MINB) vh_insert_frames_kernel(F
     auto row_of = [&](int sy_) { return sy_ * ST_H + dv; };
     // sub-tile st = sy * stx + sx, walked incrementally (no divisions)
     auto advance = [&](int& sy, int& sx) {
-        sx += FI_NT / 32;
+        sx += NT / 32;
         while (sx >= stx) { sx -= stx; ++sy; }
     };
     auto load4 = [&](int sy, int sx, float (&z)[FI_PX], float (&c)[FI_PX]) {
@@ -1623,9 +1627,23 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
         EC3R_CHECK_LAUNCH("vh_insert_frames_kernel<log>");
         return EC3R_OK;
     }
+    // CTA size: 128-thread CTAs (4 per SM, the same 16 warps and register
+    // budget) when the launch is long enough that their finer granularity
+    // pays; 256-thread CTAs when 128-thread ones would leave a heavy last
+    // wave (measured, profiles/r02g24_fusion_cta_size.json: configs[3], 21
+    // waves of 128: 5.31 vs 5.55 ms; configs[1], 4.3 waves: 1.255 vs 1.20 ms).
+    // EC3R_FI_NT128=0/1 forces either form.
+    const int64_t ctas = (int64_t)grid.x * grid.y;
+    bool small = ctas >= (int64_t)kSmallCtaWaves * 4 * kNumSMs;
+    if (const char* e = getenv("EC3R_FI_NT128")) small = e[0] == '1';
     KernelTimer tk(TK_FUSE_INSERT, st);
     if (tma) vh_insert_frames_kernel<false, true><<<grid, FI_NT, smem_tma, st>>>(a);
-    else vh_insert_frames_kernel<false, false><<<grid, FI_NT, smem, st>>>(a);
+    else if (small) {
+        if (smem > 48 * 1024)
+            EC3R_CUDA_TRY(cudaFuncSetAttribute(vh_insert_frames_kernel<false, false, 128>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        vh_insert_frames_kernel<false, false, 128><<<grid, 128, smem, st>>>(a);
+    } else vh_insert_frames_kernel<false, false><<<grid, FI_NT, smem, st>>>(a);
     EC3R_CHECK_LAUNCH("vh_insert_frames_kernel");
     tk.stop();
     return EC3R_OK;
