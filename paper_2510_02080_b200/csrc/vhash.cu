@@ -231,7 +231,7 @@ __global__ void vb_clear_used_kernel(BlockEntry* __restrict__ table, int64_t tca
 #define EC3R_FI_NT 256  // threads per insert CTA
 #endif
 constexpr int FI_NT = EC3R_FI_NT;
-constexpr int kSmallCtaWaves = 8;  // 128-thread insert CTAs from this many waves of them (see the launch)
+constexpr int kSmallCtaWaves = 6;  // 128-thread insert CTAs from this many waves of them (see the launch)
 #ifndef EC3R_FI_ROWS
 #define EC3R_FI_ROWS 64  // image rows per CTA
 #endif
@@ -1631,7 +1631,8 @@ extern "C" int ec3r_vhash_insert_frames(ec3r_vhash* h, const float* depth_pool, 
     // budget) when the launch is long enough that their finer granularity
     // pays; 256-thread CTAs when 128-thread ones would leave a heavy last
     // wave (measured, profiles/r02g24_fusion_cta_size.json: configs[3], 21
-    // waves of 128: 5.31 vs 5.55 ms; configs[1], 4.3 waves: 1.255 vs 1.20 ms).
+    // waves of 128: 5.31 vs 5.55 ms; configs[4] shard, 7.0 waves: 1.655 vs
+    // 1.70 ms; configs[1], 4.3 waves: 1.255 vs 1.20 ms).
     // EC3R_FI_NT128=0/1 forces either form.
     const int64_t ctas = (int64_t)grid.x * grid.y;
     bool small = ctas >= (int64_t)kSmallCtaWaves * 4 * kNumSMs;
