@@ -1,7 +1,6 @@
 #!/usr/bin/env bash
-# r02g28: auto CTA form at 6 waves: configs[4] / [1] / [3] bench, fusion tests
-O=gpurun_out/r02g28; mkdir -p $O
-for c in 4 1 3; do
-  timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-extras > $O/bench_c$c.log 2>&1; echo c${c}_rc=$?
-done
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -k "fus or voxel or edges or smoke" > $O/tests.log 2>&1; echo tests_rc=$?
+# r02g30: final check of the shipped binary: full GPU suite, smoke, driver-style bench
+O=gpurun_out/r02g30; mkdir -p $O
+timeout 1800 python -m pytest tests -m gpu -x -q --timeout 600 > $O/gpu_tests.log 2>&1; echo tests_rc=$?
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?
+timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench.log 2>&1; echo bench_rc=$?
